@@ -1,0 +1,207 @@
+"""ctypes wrapper over oracle/_ref/librfref.so — TEST INFRASTRUCTURE ONLY.
+
+librfref.so is the UNMODIFIED reference library (/root/reference/proj/src)
+compiled against oracle/shim/ plus oracle/ref_driver.cpp.  Only tests/,
+__graft_entry__.smoke() and bench.py's CPU-baseline / reference arm may use it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "librfref.so")
+
+_f = C.POINTER(C.c_float)
+_i = C.POINTER(C.c_int)
+_u8 = C.POINTER(C.c_uint8)
+_u16 = C.POINTER(C.c_uint16)
+_d = C.POINTER(C.c_double)
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(LIB_PATH)
+        L.rr_orbit_poses.argtypes = [_f, C.c_float, C.c_int, C.c_float, _f]
+        L.rr_render.argtypes = [C.c_int, _f, _i, _f, C.c_float, C.c_float, C.c_int, _u16, _f, _u8]
+        L.rr_scene_sdf.argtypes = [C.c_int, _f]
+        L.rr_scene_sdf.restype = C.c_float
+        L.rr_build_view.argtypes = [_u16, _i, _f, C.c_float, C.c_float, C.c_int, _f]
+        L.rr_hash_index.argtypes = [_i, C.c_uint32]
+        L.rr_hash_index.restype = C.c_uint32
+        L.rr_traverse_blocks.argtypes = [_f, _f, _i, C.c_int]
+        L.rr_block_in_frustum.argtypes = [_i, _f, _i, _f, _f]
+        L.rr_update_voxel_depth.argtypes = [_u8, _f, _f, _i, _f, C.c_float, C.c_int, _f, C.c_int]
+        L.rr_update_voxel_depth.restype = C.c_float
+        L.rr_create.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
+        L.rr_create.restype = C.c_void_p
+        L.rr_destroy.argtypes = [C.c_void_p]
+        L.rr_allocate.argtypes = [C.c_void_p, _f, _i, _f, _f, _f, _i, _d]
+        L.rr_integrate.argtypes = [C.c_void_p, _f, _u8, _i, _f, _i, _f, _f, _f, _f, _d]
+        L.rr_render_ranges.argtypes = [C.c_void_p, _f, _i, _f, _f, _f, _d]
+        L.rr_render_icp.argtypes = [C.c_void_p, _f, _i, _f, _f, _f, _f, _f, _d]
+        L.rr_set_ranges.argtypes = [C.c_void_p, _i, _f, _f]
+        L.rr_total_entries.argtypes = [C.c_void_p]
+        L.rr_total_entries.restype = C.c_uint32
+        L.rr_export_entries.argtypes = [C.c_void_p, _i]
+        L.rr_export_blocks.argtypes = [C.c_void_p, _i, C.c_int, _u8]
+        L.rr_export_visible.argtypes = [C.c_void_p, _i, _u8]
+        L.rr_free_counts.argtypes = [C.c_void_p, _i, _i]
+        _lib = L
+    return _lib
+
+
+def P(a, t):
+    if a is None:
+        return None
+    return a.ctypes.data_as(t)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _wh(intr):
+    return np.array([intr["width"], intr["height"]], dtype=np.int32)
+
+
+def _f4(intr):
+    return np.array([intr["fx"], intr["fy"], intr["cx"], intr["cy"]], dtype=np.float32)
+
+
+def params_vec(p) -> np.ndarray:
+    return np.array([p["voxelSize"], p["mu"], p["maxW"], p["viewFrustum_min"], p["viewFrustum_max"],
+                     1.0 if p.get("stopIntegratingAtMaxW", False) else 0.0], dtype=np.float32)
+
+
+def orbit_poses(target, distance, frames, max_angle=0.5) -> np.ndarray:
+    out = np.zeros((frames, 3, 4), np.float32)
+    t = _f32(target)
+    lib().rr_orbit_poses(P(t, _f), distance, frames, max_angle, P(out, _f))
+    return out
+
+
+def render(scene_kind, pose34, intr, aff=(1.0 / 5000.0, 0.0), rgb=False):
+    w, h = intr["width"], intr["height"]
+    raw = np.zeros((h, w), np.uint16)
+    dep = np.zeros((h, w), np.float32)
+    col = np.zeros((h, w, 3), np.uint8) if rgb else None
+    pose = _f32(pose34)
+    wh, f4 = _wh(intr), _f4(intr)
+    lib().rr_render(scene_kind, P(pose, _f), P(wh, _i), P(f4, _f), aff[0], aff[1], 1 if rgb else 0,
+                    P(raw, _u16), P(dep, _f), P(col, _u8))
+    return raw, dep, col
+
+
+def build_view(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=1):
+    w, h = intr["width"], intr["height"]
+    sizes = [(w >> l) * (h >> l) for l in range(levels)]
+    out = np.zeros(sum(sizes), np.float32)
+    raw = np.ascontiguousarray(raw, np.uint16)
+    wh, f4 = _wh(intr), _f4(intr)
+    lib().rr_build_view(P(raw, _u16), P(wh, _i), P(f4, _f), aff[0], aff[1], levels, P(out, _f))
+    res, o = [], 0
+    for l, s in enumerate(sizes):
+        res.append(out[o:o + s].reshape(h >> l, w >> l))
+        o += s
+    return res
+
+
+class RefEngine:
+    """VoxelBlockMap + FusionEngine + RenderState of the reference."""
+
+    def __init__(self, buckets, excess, capacity):
+        self.h = lib().rr_create(buckets, excess, capacity)
+        if not self.h:
+            raise ValueError("reference rejected the map config")
+        self.capacity = capacity
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().rr_destroy(self.h)
+            self.h = None
+
+    def allocate(self, depth, intr, pose34, params):
+        stats = np.zeros(4, np.int32)
+        ms = C.c_double(0)
+        d = _f32(depth)
+        pose = _f32(pose34)
+        pv = params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        lib().rr_allocate(self.h, P(d, _f), P(wh, _i), P(f4, _f), P(pose, _f), P(pv, _f), P(stats, _i), C.byref(ms))
+        return stats, ms.value
+
+    def integrate(self, depth, intr, pose34, params, rgb=None, intr_rgb=None, extr34=None):
+        ms = C.c_double(0)
+        d = _f32(depth)
+        pose = _f32(pose34)
+        pv = params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        whr = _wh(intr_rgb) if intr_rgb else None
+        f4r = _f4(intr_rgb) if intr_rgb else None
+        ex = _f32(extr34) if extr34 is not None else None
+        c = np.ascontiguousarray(rgb, np.uint8) if rgb is not None else None
+        lib().rr_integrate(self.h, P(d, _f), P(c, _u8), P(wh, _i), P(f4, _f), P(whr, _i), P(f4r, _f), P(ex, _f),
+                           P(pose, _f), P(pv, _f), C.byref(ms))
+        return ms.value
+
+    def render_ranges(self, pose34, intr, params):
+        rng = np.zeros((intr["height"], intr["width"], 2), np.float32)
+        ms = C.c_double(0)
+        pose = _f32(pose34)
+        pv = params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        lib().rr_render_ranges(self.h, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(rng, _f), C.byref(ms))
+        return rng, ms.value
+
+    def set_ranges(self, intr, rng):
+        wh, f4 = _wh(intr), _f4(intr)
+        r = _f32(rng)
+        lib().rr_set_ranges(self.h, P(wh, _i), P(f4, _f), P(r, _f))
+
+    def render_icp(self, pose34, intr, params):
+        h, w = intr["height"], intr["width"]
+        rc = np.zeros((h, w, 4), np.float32)
+        pts = np.zeros((h, w, 4), np.float32)
+        nrm = np.zeros((h, w, 4), np.float32)
+        ms = C.c_double(0)
+        pose = _f32(pose34)
+        pv = params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        lib().rr_render_icp(self.h, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(rc, _f), P(pts, _f),
+                            P(nrm, _f), C.byref(ms))
+        return rc, pts, nrm, ms.value
+
+    def entries(self):
+        n = lib().rr_total_entries(self.h)
+        out = np.zeros((n, 5), np.int32)
+        lib().rr_export_entries(self.h, P(out, _i))
+        return out
+
+    def blocks(self, ptrs):
+        ptrs = np.ascontiguousarray(ptrs, np.int32)
+        out = np.zeros((len(ptrs), 512, 8), np.uint8)
+        if len(ptrs):
+            lib().rr_export_blocks(self.h, P(ptrs, _i), len(ptrs), P(out, _u8))
+        return out
+
+    def visible(self):
+        n = lib().rr_total_entries(self.h)
+        lst = np.zeros(n, np.int32)
+        types = np.zeros(n, np.uint8)
+        k = lib().rr_export_visible(self.h, P(lst, _i), P(types, _u8))
+        return lst[:k].copy(), types
+
+    def free_counts(self):
+        nb, ne = C.c_int(0), C.c_int(0)
+        lib().rr_free_counts(self.h, C.byref(nb), C.byref(ne))
+        return nb.value, ne.value

@@ -1,0 +1,1079 @@
+/* oracle/rfo.c — CPU restatement oracle (TEST INFRASTRUCTURE ONLY; see rfo.h).
+ *
+ * Float association follows the reference's Eigen expressions
+ * (3-term reductions e0 + (e1 + e2); mat*vec row i = R_i0 x0 + (R_i1 x1 + R_i2 x2)).
+ * Compiled with -ffp-contract=off, so no FMA contraction.
+ */
+#include "rfo.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  float x, y, z;
+} v3;
+typedef struct {
+  int x, y, z;
+} i3;
+typedef struct {
+  float R[9]; /* row-major */
+  float t[3];
+} pose_t;
+typedef struct {
+  int w, h;
+  float fx, fy, cx, cy;
+} intr_t;
+typedef struct {
+  float voxelSize, mu;
+  int maxW;
+  float vfMin, vfMax;
+  int stopAtMaxW;
+} params_t;
+typedef struct {
+  int x, y, z, offset, ptr;
+} entry_t;
+typedef struct {
+  int16_t sdf;
+  uint8_t w;
+  uint8_t clr[3];
+  uint8_t wc;
+  uint8_t pad;
+} voxel_t;
+
+#define BS 8
+#define BS3 512
+#define SDF_ONE 32767
+
+struct rfo_map {
+  uint32_t buckets, excess, capacity;
+  entry_t* entries;
+  voxel_t* vba;
+  int* freeBlocks;
+  int nFreeBlocks;
+  int* freeExcess;
+  int nFreeExcess;
+  int* visible;
+  int nVisible;
+  uint8_t* visibility;
+  /* FusionEngine scratch (proj/include/rf/fusion.hpp:76-78) */
+  uint8_t* allocType;
+  i3* blockCoords;
+  uint8_t* marked;
+  /* RenderState.expectedRange (proj/include/rf/raycast.hpp:16) */
+  float* range;
+  int rangeW, rangeH;
+  /* shard filter */
+  int rank, world, tileShift;
+};
+
+/* ------------------------------------------------------------ core math */
+/* proj/include/rf/pose.hpp:29 apply = R*x + t; Eigen lazy-product order */
+static v3 pose_apply(const pose_t* p, v3 x) {
+  v3 o;
+  o.x = (p->R[0] * x.x + (p->R[1] * x.y + p->R[2] * x.z)) + p->t[0];
+  o.y = (p->R[3] * x.x + (p->R[4] * x.y + p->R[5] * x.z)) + p->t[1];
+  o.z = (p->R[6] * x.x + (p->R[7] * x.y + p->R[8] * x.z)) + p->t[2];
+  return o;
+}
+/* R * x without translation */
+static v3 rot_apply(const float* R, v3 x) {
+  v3 o;
+  o.x = R[0] * x.x + (R[1] * x.y + R[2] * x.z);
+  o.y = R[3] * x.x + (R[4] * x.y + R[5] * x.z);
+  o.z = R[6] * x.x + (R[7] * x.y + R[8] * x.z);
+  return o;
+}
+/* proj/include/rf/pose.hpp:33-36 inverse = (R^T, -(R^T t)) */
+static pose_t pose_inverse(const pose_t* p) {
+  pose_t q;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) q.R[r * 3 + c] = p->R[c * 3 + r];
+  v3 t = {p->t[0], p->t[1], p->t[2]};
+  v3 rt = rot_apply(q.R, t);
+  q.t[0] = -rt.x;
+  q.t[1] = -rt.y;
+  q.t[2] = -rt.z;
+  return q;
+}
+/* proj/include/rf/pose.hpp:31 compose = (R R', R t' + t) */
+static pose_t pose_compose(const pose_t* a, const pose_t* b) {
+  pose_t q;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      q.R[r * 3 + c] = a->R[r * 3 + 0] * b->R[0 * 3 + c] + (a->R[r * 3 + 1] * b->R[1 * 3 + c] + a->R[r * 3 + 2] * b->R[2 * 3 + c]);
+  v3 t = {b->t[0], b->t[1], b->t[2]};
+  v3 rt = rot_apply(a->R, t);
+  q.t[0] = rt.x + a->t[0];
+  q.t[1] = rt.y + a->t[1];
+  q.t[2] = rt.z + a->t[2];
+  return q;
+}
+static pose_t pose_from12(const float* p) {
+  pose_t q;
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) q.R[r * 3 + c] = p[r * 4 + c];
+    q.t[r] = p[r * 4 + 3];
+  }
+  return q;
+}
+static intr_t intr_from(const int* wh, const float* f4) {
+  intr_t i = {wh[0], wh[1], f4[0], f4[1], f4[2], f4[3]};
+  return i;
+}
+static params_t params_from(const float* p) {
+  params_t s = {p[0], p[1], (int)p[2], p[3], p[4], p[5] != 0.f};
+  return s;
+}
+/* proj/include/rf/camera.hpp:23-25 */
+static v3 backproject(const intr_t* in, float u, float v, float z) {
+  v3 o = {(u - in->cx) / in->fx * z, (v - in->cy) / in->fy * z, z};
+  return o;
+}
+static float dot3(v3 a, v3 b) { return a.x * b.x + (a.y * b.y + a.z * b.z); }
+static float sqnorm3(v3 a) { return a.x * a.x + (a.y * a.y + a.z * a.z); }
+static v3 cross3(v3 a, v3 b) {
+  v3 o = {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+  return o;
+}
+/* std::min / std::max semantics: min(a,b) = (b < a) ? b : a */
+static float smin(float a, float b) { return (b < a) ? b : a; }
+static float smax(float a, float b) { return (a < b) ? b : a; }
+
+/* proj/include/rf/voxel.hpp:16-21 */
+static float sdf_to_logical(int16_t s) { return (float)s / (float)SDF_ONE; }
+static int16_t sdf_from_logical(float f) {
+  float c = f < -1.f ? -1.f : (1.f < f ? 1.f : f); /* std::clamp */
+  return (int16_t)lroundf(c * (float)SDF_ONE);
+}
+
+/* ---------------------------------------------------------- hash map */
+/* proj/include/rf/voxel_block_map.hpp:47-52 */
+static uint32_t hash_index(i3 p, uint32_t mask) {
+  return (((uint32_t)p.x * 73856093u) ^ ((uint32_t)p.y * 19349669u) ^ ((uint32_t)p.z * 83492791u)) & mask;
+}
+uint32_t rfo_hash_index(const int* pos3, uint32_t mask) {
+  i3 p = {pos3[0], pos3[1], pos3[2]};
+  return hash_index(p, mask);
+}
+static int allocated(const entry_t* e) { return e->ptr >= -1; }
+static int same_pos(const entry_t* e, i3 p) { return e->x == p.x && e->y == p.y && e->z == p.z; }
+
+/* proj/src/voxel_block_map.cpp:26-34 */
+static int find_entry(const rfo_map* m, i3 p) {
+  int idx = (int)hash_index(p, m->buckets - 1);
+  for (;;) {
+    const entry_t* e = &m->entries[idx];
+    if (allocated(e) && same_pos(e, p)) return idx;
+    if (e->offset < 1) return -1;
+    idx = (int)m->buckets + e->offset - 1;
+  }
+}
+/* proj/src/voxel_block_map.cpp:36-61 (the BlockCache never changes results,
+ * proj/tests/unit/test_voxelmap.cpp:183-198, so it is omitted) */
+static const voxel_t* find_voxel(const rfo_map* m, i3 v) {
+  i3 b = {v.x >> 3, v.y >> 3, v.z >> 3};
+  int idx = find_entry(m, b);
+  int ptr = idx >= 0 ? m->entries[idx].ptr : -1;
+  if (ptr < 0) return NULL;
+  int lin = (v.x - b.x * BS) + (v.y - b.y * BS) * BS + (v.z - b.z * BS) * BS * BS;
+  return &m->vba[(size_t)ptr * BS3 + lin];
+}
+/* proj/src/voxel_block_map.cpp:74-105; returns entry idx or -1 */
+static int allocate_block(rfo_map* m, i3 p) {
+  int idx = (int)hash_index(p, m->buckets - 1);
+  if (allocated(&m->entries[idx])) {
+    for (;;) {
+      entry_t* e = &m->entries[idx];
+      if (same_pos(e, p) && allocated(e)) return idx;
+      if (e->offset < 1) break;
+      idx = (int)m->buckets + e->offset - 1;
+    }
+    if (m->nFreeExcess == 0 || m->nFreeBlocks == 0) return -1;
+    int excessIdx = m->freeExcess[--m->nFreeExcess];
+    int blockPtr = m->freeBlocks[--m->nFreeBlocks];
+    int newIdx = (int)m->buckets + excessIdx;
+    entry_t ne = {p.x, p.y, p.z, 0, blockPtr};
+    m->entries[newIdx] = ne;
+    m->entries[idx].offset = excessIdx + 1;
+    return newIdx;
+  }
+  if (m->nFreeBlocks == 0) return -1;
+  int blockPtr = m->freeBlocks[--m->nFreeBlocks];
+  int keep = m->entries[idx].offset;
+  entry_t ne = {p.x, p.y, p.z, keep, blockPtr};
+  m->entries[idx] = ne;
+  return idx;
+}
+
+rfo_map* rfo_create(uint32_t buckets, uint32_t excess, uint32_t capacity) {
+  if (buckets == 0 || (buckets & (buckets - 1)) != 0) return NULL; /* voxel_block_map.cpp:10-11 */
+  rfo_map* m = (rfo_map*)calloc(1, sizeof(rfo_map));
+  m->buckets = buckets;
+  m->excess = excess;
+  m->capacity = capacity;
+  size_t total = (size_t)buckets + excess;
+  m->entries = (entry_t*)malloc(sizeof(entry_t) * total);
+  m->vba = (voxel_t*)malloc(sizeof(voxel_t) * (size_t)capacity * BS3);
+  m->freeBlocks = (int*)malloc(sizeof(int) * (capacity ? capacity : 1));
+  m->freeExcess = (int*)malloc(sizeof(int) * (excess ? excess : 1));
+  m->visible = (int*)malloc(sizeof(int) * total);
+  m->visibility = (uint8_t*)malloc(total);
+  m->allocType = (uint8_t*)malloc(total);
+  m->blockCoords = (i3*)malloc(sizeof(i3) * total);
+  m->marked = (uint8_t*)malloc(total);
+  m->world = 1;
+  rfo_clear(m);
+  return m;
+}
+
+void rfo_destroy(rfo_map* m) {
+  if (!m) return;
+  free(m->entries);
+  free(m->vba);
+  free(m->freeBlocks);
+  free(m->freeExcess);
+  free(m->visible);
+  free(m->visibility);
+  free(m->allocType);
+  free(m->blockCoords);
+  free(m->marked);
+  free(m->range);
+  free(m);
+}
+
+/* proj/src/voxel_block_map.cpp:15-24 */
+void rfo_clear(rfo_map* m) {
+  size_t total = (size_t)m->buckets + m->excess;
+  entry_t e0 = {0, 0, 0, 0, -2};
+  for (size_t i = 0; i < total; ++i) m->entries[i] = e0;
+  voxel_t v0;
+  memset(&v0, 0, sizeof v0);
+  v0.sdf = SDF_ONE;
+  for (size_t i = 0; i < (size_t)m->capacity * BS3; ++i) m->vba[i] = v0;
+  for (uint32_t i = 0; i < m->capacity; ++i) m->freeBlocks[i] = (int)i;
+  m->nFreeBlocks = (int)m->capacity;
+  for (uint32_t i = 0; i < m->excess; ++i) m->freeExcess[i] = (int)i;
+  m->nFreeExcess = (int)m->excess;
+  m->nVisible = 0;
+  memset(m->visibility, 0, total);
+  memset(m->allocType, 0, total);
+  memset(m->marked, 0, total);
+}
+
+void rfo_set_shard(rfo_map* m, int rank, int world, int tileShift) {
+  m->rank = rank;
+  m->world = world;
+  m->tileShift = tileShift;
+}
+
+static int owner_of(i3 b, int world, int shift) {
+  i3 t = {b.x >> shift, b.y >> shift, b.z >> shift};
+  return (int)(hash_index(t, 0xFFFFFFFFu) % (uint32_t)world);
+}
+static int shard_keeps(const rfo_map* m, i3 b) {
+  if (m->world <= 1) return 1;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        i3 n = {b.x + dx, b.y + dy, b.z + dz};
+        if (owner_of(n, m->world, m->tileShift) == m->rank) return 1;
+      }
+  return 0;
+}
+
+/* ------------------------------------------------------------- fusion */
+/* proj/src/fusion.cpp:72-114 — Amanatides-Woo DDA in block units */
+typedef void (*visit_fn)(void* ctx, i3 cell);
+static void traverse_blocks(v3 a, v3 b, visit_fn visit, void* ctx) {
+  i3 cell = {(int)floorf(a.x), (int)floorf(a.y), (int)floorf(a.z)};
+  i3 endCell = {(int)floorf(b.x), (int)floorf(b.y), (int)floorf(b.z)};
+  visit(ctx, cell);
+  if (cell.x == endCell.x && cell.y == endCell.y && cell.z == endCell.z) return;
+  float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
+  float av[3] = {a.x, a.y, a.z};
+  int c[3] = {cell.x, cell.y, cell.z};
+  int e[3] = {endCell.x, endCell.y, endCell.z};
+  int step[3];
+  float tMax[3], tDelta[3];
+  for (int k = 0; k < 3; ++k) {
+    if (d[k] > 0.f) {
+      step[k] = 1;
+      tMax[k] = ((float)(c[k] + 1) - av[k]) / d[k];
+      tDelta[k] = 1.f / d[k];
+    } else if (d[k] < 0.f) {
+      step[k] = -1;
+      tMax[k] = ((float)c[k] - av[k]) / d[k];
+      tDelta[k] = -1.f / d[k];
+    } else {
+      step[k] = 0;
+      tMax[k] = FLT_MAX;
+      tDelta[k] = FLT_MAX;
+    }
+  }
+  int maxSteps = abs(e[0] - c[0]) + abs(e[1] - c[1]) + abs(e[2] - c[2]) + 8;
+  for (int i = 0; i < maxSteps; ++i) {
+    int axis = 0;
+    if (tMax[1] < tMax[0]) axis = 1;
+    if (tMax[2] < tMax[axis]) axis = 2;
+    if (tMax[axis] > 1.f) break;
+    c[axis] += step[axis];
+    tMax[axis] += tDelta[axis];
+    i3 cc = {c[0], c[1], c[2]};
+    visit(ctx, cc);
+    if (c[0] == e[0] && c[1] == e[1] && c[2] == e[2]) break;
+  }
+  if (!(c[0] == e[0] && c[1] == e[1] && c[2] == e[2])) visit(ctx, endCell);
+}
+
+typedef struct {
+  int* out;
+  int n, max;
+} collect_ctx;
+static void collect_visit(void* ctx, i3 c) {
+  collect_ctx* cc = (collect_ctx*)ctx;
+  if (cc->n < cc->max) {
+    cc->out[3 * cc->n] = c.x;
+    cc->out[3 * cc->n + 1] = c.y;
+    cc->out[3 * cc->n + 2] = c.z;
+  }
+  cc->n++;
+}
+int rfo_traverse_blocks(const float* a3, const float* b3, int* cellsOut, int maxCells) {
+  v3 a = {a3[0], a3[1], a3[2]}, b = {b3[0], b3[1], b3[2]};
+  collect_ctx cc = {cellsOut, 0, maxCells};
+  traverse_blocks(a, b, collect_visit, &cc);
+  return cc.n;
+}
+
+/* proj/src/fusion.cpp:116-130 */
+static int block_in_frustum(i3 p, const pose_t* pose, const intr_t* in, const params_t* s, float marginPx) {
+  const float bs = s->voxelSize * (float)BS;
+  for (int c = 0; c < 8; ++c) {
+    v3 corner = {((float)p.x + (float)(c & 1)) * bs, ((float)p.y + (float)((c >> 1) & 1)) * bs,
+                 ((float)p.z + (float)((c >> 2) & 1)) * bs};
+    v3 pc = pose_apply(pose, corner);
+    if (pc.z < s->vfMin || pc.z > s->vfMax) continue;
+    float px = in->fx * pc.x / pc.z + in->cx;
+    float py = in->fy * pc.y / pc.z + in->cy;
+    if (px >= -marginPx && py >= -marginPx && px <= (float)(in->w - 1) + marginPx &&
+        py <= (float)(in->h - 1) + marginPx)
+      return 1;
+  }
+  return 0;
+}
+int rfo_block_in_frustum(const int* pos3, const float* pose12, const int* wh, const float* f4, const float* params6) {
+  i3 p = {pos3[0], pos3[1], pos3[2]};
+  pose_t pose = pose_from12(pose12);
+  intr_t in = intr_from(wh, f4);
+  params_t s = params_from(params6);
+  return block_in_frustum(p, &pose, &in, &s, 0.f);
+}
+
+/* proj/src/fusion.cpp:9-36 */
+static float update_voxel_depth(voxel_t* vx, v3 pt, const pose_t* M, const intr_t* in, float mu, int maxW,
+                                const float* depth, int dw, int dh, int stopAtMaxW) {
+  v3 pc = pose_apply(M, pt);
+  if (pc.z <= 0.f) return -1.f;
+  float px = in->fx * pc.x / pc.z + in->cx;
+  float py = in->fy * pc.y / pc.z + in->cy;
+  if (px < 1 || px > (float)(dw - 2) || py < 1 || py > (float)(dh - 2)) return -1.f;
+  float dm = depth[(size_t)(int)(py + 0.5f) * dw + (int)(px + 0.5f)];
+  if (dm <= 0.f) return -1.f;
+  float eta = dm - pc.z;
+  if (eta < -mu) return eta;
+  float oldF = sdf_to_logical(vx->sdf);
+  int oldW = vx->w;
+  if (stopAtMaxW && oldW >= maxW) return eta;
+  float newF = smin(1.f, eta / mu);
+  int newW = 1;
+  float merged = ((float)oldW * oldF + (float)newW * newF) / (float)(oldW + newW);
+  newW = (oldW + newW) < maxW ? (oldW + newW) : maxW;
+  vx->sdf = sdf_from_logical(merged);
+  vx->w = (uint8_t)newW;
+  return eta;
+}
+float rfo_update_voxel_depth(uint8_t* voxel8, const float* pt3, const float* pose12, const int* wh, const float* f4,
+                             float mu, int maxW, const float* depth, int stopAtMaxW) {
+  voxel_t v;
+  memcpy(&v, voxel8, 8);
+  v3 pt = {pt3[0], pt3[1], pt3[2]};
+  pose_t pose = pose_from12(pose12);
+  intr_t in = intr_from(wh, f4);
+  float eta = update_voxel_depth(&v, pt, &pose, &in, mu, maxW, depth, wh[0], wh[1], stopAtMaxW);
+  memcpy(voxel8, &v, 8);
+  return eta;
+}
+
+/* proj/src/fusion.cpp:38-70 */
+static void update_voxel_colour(voxel_t* vx, v3 pt, const pose_t* M, const intr_t* in, int maxW, const uint8_t* rgb,
+                                int rw, int rh) {
+  v3 pc = pose_apply(M, pt);
+  if (pc.z <= 0.f) return;
+  float px = in->fx * pc.x / pc.z + in->cx;
+  float py = in->fy * pc.y / pc.z + in->cy;
+  if (px < 1 || px > (float)(rw - 2) || py < 1 || py > (float)(rh - 2)) return;
+  int x0 = (int)floorf(px), y0 = (int)floorf(py);
+  float fx = px - (float)x0, fy = py - (float)y0;
+  float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
+  const uint8_t* c00 = rgb + 3 * ((size_t)y0 * rw + x0);
+  const uint8_t* c10 = rgb + 3 * ((size_t)y0 * rw + x0 + 1);
+  const uint8_t* c01 = rgb + 3 * ((size_t)(y0 + 1) * rw + x0);
+  const uint8_t* c11 = rgb + 3 * ((size_t)(y0 + 1) * rw + x0 + 1);
+  int oldW = vx->wc;
+  for (int k = 0; k < 3; ++k) {
+    float sample = w00 * (float)c00[k] + w10 * (float)c10[k] + w01 * (float)c01[k] + w11 * (float)c11[k];
+    float merged = ((float)oldW * (float)vx->clr[k] + sample) / (float)(oldW + 1);
+    long r = lroundf(merged);
+    vx->clr[k] = (uint8_t)(r < 0 ? 0 : (r > 255 ? 255 : r));
+  }
+  vx->wc = (uint8_t)((oldW + 1) < maxW ? (oldW + 1) : maxW);
+}
+
+typedef struct {
+  rfo_map* m;
+} mark_ctx;
+/* proj/src/fusion.cpp:155-177 (markBlock) */
+static void mark_visit(void* ctx, i3 p) {
+  rfo_map* m = ((mark_ctx*)ctx)->m;
+  if (!shard_keeps(m, p)) return;
+  int idx = (int)hash_index(p, m->buckets - 1);
+  const entry_t* e = &m->entries[idx];
+  if (allocated(e)) {
+    for (;;) {
+      if (same_pos(e, p)) {
+        m->marked[idx] = e->ptr >= 0 ? 1 : 2;
+        return;
+      }
+      if (e->offset < 1) break;
+      idx = (int)m->buckets + e->offset - 1;
+      e = &m->entries[idx];
+    }
+    m->allocType[idx] = 2;
+    m->blockCoords[idx] = p;
+  } else {
+    m->allocType[idx] = 1;
+    m->blockCoords[idx] = p;
+  }
+}
+
+/* proj/src/fusion.cpp:144-235 */
+int rfo_allocate(rfo_map* m, const float* depth, const int* wh, const float* f4, const float* pose12,
+                 const float* params6, int* stats4) {
+  const size_t total = (size_t)m->buckets + m->excess;
+  memset(m->allocType, 0, total); /* ensureScratch :132-142 */
+  memset(m->marked, 0, total);
+  intr_t in = intr_from(wh, f4);
+  params_t s = params_from(params6);
+  pose_t pose = pose_from12(pose12);
+  pose_t camToWorld = pose_inverse(&pose);
+  const float invBlock = 1.f / (s.voxelSize * (float)BS);
+  int requested = 0, allocatedN = 0, failures = 0;
+
+  /* stage 1 :179-187 */
+  mark_ctx ctx = {m};
+  for (int y = 0; y < in.h; ++y)
+    for (int x = 0; x < in.w; ++x) {
+      float d = depth[(size_t)y * in.w + x];
+      if (d <= 0.f || d < s.vfMin || d > s.vfMax) continue;
+      v3 nearP = pose_apply(&camToWorld, backproject(&in, (float)x, (float)y, d - s.mu));
+      v3 farP = pose_apply(&camToWorld, backproject(&in, (float)x, (float)y, d + s.mu));
+      v3 a = {nearP.x * invBlock, nearP.y * invBlock, nearP.z * invBlock};
+      v3 b = {farP.x * invBlock, farP.y * invBlock, farP.z * invBlock};
+      traverse_blocks(a, b, mark_visit, &ctx);
+    }
+
+  /* stage 2 :190-201 */
+  for (size_t idx = 0; idx < total; ++idx) {
+    if (m->allocType[idx] == 0) continue;
+    ++requested;
+    int e = allocate_block(m, m->blockCoords[idx]);
+    if (e < 0) {
+      ++failures;
+      continue;
+    }
+    ++allocatedN;
+    m->marked[e] = 1;
+  }
+
+  /* stage 3 :205-233 — candidates = marked ∪ previous visible, frustum
+   * tested, sorted by idx.  Candidate indices are unique, so an ascending scan
+   * of the candidate flags yields the same sorted list. */
+  for (int i = 0; i < m->nVisible; ++i)
+    if (!m->marked[m->visible[i]]) m->marked[m->visible[i]] = 3; /* prev-visible candidate */
+  memset(m->visibility, 0, total);
+  int nv = 0;
+  for (size_t idx = 0; idx < total; ++idx) {
+    if (!m->marked[idx]) continue;
+    const entry_t* e = &m->entries[idx];
+    if (!allocated(e)) continue;
+    i3 p = {e->x, e->y, e->z};
+    if (block_in_frustum(p, &pose, &in, &s, 0.f)) {
+      m->visibility[idx] = e->ptr >= 0 ? 1 : 2;
+      m->visible[nv++] = (int)idx;
+    }
+  }
+  m->nVisible = nv;
+  stats4[0] = requested;
+  stats4[1] = allocatedN;
+  stats4[2] = failures;
+  stats4[3] = nv;
+  return 0;
+}
+
+/* proj/src/fusion.cpp:237-263 */
+int rfo_integrate(rfo_map* m, const float* depth, const uint8_t* rgb, const int* whD, const float* f4D,
+                  const int* whRgb, const float* f4Rgb, const float* extr12, const float* pose12,
+                  const float* params6) {
+  intr_t inD = intr_from(whD, f4D);
+  intr_t inRgb = whRgb ? intr_from(whRgb, f4Rgb) : inD;
+  params_t s = params_from(params6);
+  pose_t pose = pose_from12(pose12);
+  pose_t extr;
+  if (extr12) {
+    extr = pose_from12(extr12);
+  } else {
+    memset(&extr, 0, sizeof extr);
+    extr.R[0] = extr.R[4] = extr.R[8] = 1.f;
+  }
+  pose_t Mrgb = pose_compose(&extr, &pose);
+  for (int i = 0; i < m->nVisible; ++i) {
+    const entry_t* e = &m->entries[m->visible[i]];
+    if (e->ptr < 0) continue;
+    voxel_t* blk = &m->vba[(size_t)e->ptr * BS3];
+    int ox = e->x * BS, oy = e->y * BS, oz = e->z * BS;
+    for (int z = 0; z < BS; ++z)
+      for (int y = 0; y < BS; ++y)
+        for (int x = 0; x < BS; ++x) {
+          voxel_t* v = &blk[x + y * BS + z * BS * BS];
+          v3 pt = {(float)(ox + x) * s.voxelSize, (float)(oy + y) * s.voxelSize, (float)(oz + z) * s.voxelSize};
+          float eta = update_voxel_depth(v, pt, &pose, &inD, s.mu, s.maxW, depth, inD.w, inD.h, s.stopAtMaxW);
+          if (rgb && eta >= -s.mu) update_voxel_colour(v, pt, &Mrgb, &inRgb, s.maxW, rgb, inRgb.w, inRgb.h);
+        }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------ raycast */
+static void ensure_range(rfo_map* m, int w, int h) {
+  if (m->rangeW != w || m->rangeH != h) {
+    free(m->range);
+    m->range = (float*)malloc(sizeof(float) * 2 * (size_t)w * h);
+    m->rangeW = w;
+    m->rangeH = h;
+  }
+}
+
+/* proj/src/raycast.cpp:38-71 (projectBlock), :86-127 (render_expected_ranges).
+ * The 16x16 fragment split of each block's pixel rectangle only partitions
+ * the min/max merge (commutative), so merging the rectangle directly yields
+ * identical ranges. */
+int rfo_render_ranges(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
+                      float* rangeOut) {
+  intr_t in = intr_from(wh, f4);
+  params_t s = params_from(params6);
+  pose_t pose = pose_from12(pose12);
+  ensure_range(m, in.w, in.h);
+  for (size_t i = 0; i < (size_t)in.w * in.h; ++i) {
+    m->range[2 * i] = FLT_MAX;
+    m->range[2 * i + 1] = -1.f;
+  }
+  const float bs = s.voxelSize * (float)BS;
+  for (int vi = 0; vi < m->nVisible; ++vi) {
+    const entry_t* e = &m->entries[m->visible[vi]];
+    if (!allocated(e)) continue;
+    float x0 = FLT_MAX, y0 = FLT_MAX, x1 = -FLT_MAX, y1 = -FLT_MAX, zMin = FLT_MAX, zMax = 0.f;
+    int valid = 0;
+    for (int c = 0; c < 8; ++c) {
+      v3 corner = {((float)e->x + (float)(c & 1)) * bs, ((float)e->y + (float)((c >> 1) & 1)) * bs,
+                   ((float)e->z + (float)((c >> 2) & 1)) * bs};
+      v3 pc = pose_apply(&pose, corner);
+      if (pc.z < 1e-6f) continue;
+      float px = in.fx * pc.x / pc.z + in.cx;
+      float py = in.fy * pc.y / pc.z + in.cy;
+      x0 = smin(x0, px);
+      y0 = smin(y0, py);
+      x1 = smax(x1, px);
+      y1 = smax(y1, py);
+      zMin = smin(zMin, pc.z);
+      zMax = smax(zMax, pc.z);
+      ++valid;
+    }
+    if (valid == 0) continue;
+    int bx0 = (int)floorf(x0), by0 = (int)floorf(y0), bx1 = (int)ceilf(x1), by1 = (int)ceilf(y1);
+    bx0 = bx0 > 0 ? bx0 : 0;
+    by0 = by0 > 0 ? by0 : 0;
+    bx1 = bx1 < in.w - 1 ? bx1 : in.w - 1;
+    by1 = by1 < in.h - 1 ? by1 : in.h - 1;
+    if (bx0 > bx1 || by0 > by1) continue;
+    float zlo = smax(zMin, s.vfMin), zhi = smin(zMax, s.vfMax);
+    if (zlo > zhi) continue;
+    for (int y = by0; y <= by1; ++y)
+      for (int x = bx0; x <= bx1; ++x) {
+        float* r = &m->range[2 * ((size_t)y * in.w + x)];
+        r[0] = smin(r[0], zlo);
+        r[1] = smax(r[1], zhi);
+      }
+  }
+  if (rangeOut) memcpy(rangeOut, m->range, sizeof(float) * 2 * (size_t)in.w * in.h);
+  return 0;
+}
+
+int rfo_set_ranges(rfo_map* m, const int* wh, const float* rangeIn) {
+  ensure_range(m, wh[0], wh[1]);
+  memcpy(m->range, rangeIn, sizeof(float) * 2 * (size_t)wh[0] * wh[1]);
+  return 0;
+}
+
+/* MapField (proj/include/rf/raycast.hpp:32-45) */
+static int field_resident(const rfo_map* m, v3 p) {
+  i3 b = {((int)floorf(p.x)) >> 3, ((int)floorf(p.y)) >> 3, ((int)floorf(p.z)) >> 3};
+  int idx = find_entry(m, b);
+  return idx >= 0 && m->entries[idx].ptr >= 0; /* blockResident voxel_block_map.cpp:63-72 */
+}
+/* readSdfNearest voxel_block_map.cpp:178-185 */
+static float sdf_nearest(const rfo_map* m, v3 p, int* ok) {
+  i3 v = {(int)lroundf(p.x), (int)lroundf(p.y), (int)lroundf(p.z)};
+  const voxel_t* vx = find_voxel(m, v);
+  *ok = vx != NULL;
+  return vx ? sdf_to_logical(vx->sdf) : 1.f;
+}
+/* readSdfWeightTrilinear voxel_block_map.cpp:130-156 */
+static float sdf_trilinear(const rfo_map* m, v3 p, int* ok) {
+  int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
+  float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
+  float sdf = 0.f;
+  for (int k = 0; k < 8; ++k) {
+    i3 c = {bx + (k & 1), by + ((k >> 1) & 1), bz + ((k >> 2) & 1)};
+    const voxel_t* vx = find_voxel(m, c);
+    if (!vx) {
+      *ok = 0;
+      return 1.f;
+    }
+    float bw = ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+    sdf += bw * sdf_to_logical(vx->sdf);
+  }
+  *ok = 1;
+  return sdf;
+}
+
+static v3 at_t(v3 o, v3 d, float t) {
+  v3 r = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+  return r;
+}
+
+/* cast_ray_field proj/include/rf/raycast.hpp:54-112; returns 1 on hit */
+static int cast_ray(const rfo_map* m, v3 originM, v3 dirUnit, float tMinM, float tMaxM, float mu, float vs,
+                    v3* hit) {
+  const float coarseStep = (float)BS * vs;
+  const float fineStep = mu;
+  const float stepScale = mu;
+  v3 oV = {originM.x / vs, originM.y / vs, originM.z / vs};
+  v3 dV = {dirUnit.x / vs, dirUnit.y / vs, dirUnit.z / vs};
+  float t = tMinM;
+  enum { COARSE, FINE, SURFACE } state = field_resident(m, at_t(oV, dV, t)) ? FINE : COARSE;
+  while (t <= tMaxM) {
+    v3 p = at_t(oV, dV, t);
+    if (state == COARSE) {
+      if (field_resident(m, p)) {
+        state = FINE;
+        t = smax(tMinM, t - coarseStep);
+      } else {
+        t += coarseStep;
+      }
+      continue;
+    }
+    int ok = 0;
+    float sdf = sdf_nearest(m, p, &ok);
+    if (!ok) {
+      if (state == SURFACE) state = FINE;
+      t += fineStep;
+      continue;
+    }
+    if (sdf <= 0.1f) {
+      int okTri = 0;
+      float tri = sdf_trilinear(m, p, &okTri);
+      if (okTri) sdf = tri;
+    }
+    if (state == FINE) {
+      if (sdf < 0.f) return 0; /* WRONG_SIDE */
+      state = SURFACE;
+    }
+    if (sdf <= 0.f) {
+      float tHit = t + sdf * stepScale;
+      int okR = 0;
+      float f1 = sdf_trilinear(m, at_t(oV, dV, tHit), &okR);
+      if (okR) tHit += f1 * stepScale;
+      *hit = at_t(oV, dV, tHit);
+      return 1;
+    }
+    t += smax(sdf * stepScale, vs);
+  }
+  return 0;
+}
+
+/* field_normal proj/include/rf/raycast.hpp:137-153 */
+static int field_normal(const rfo_map* m, v3 h, v3* n) {
+  int ok[6];
+  v3 px = {h.x + 1.f, h.y + 0.f, h.z + 0.f}, mx = {h.x - 1.f, h.y - 0.f, h.z - 0.f};
+  v3 py = {h.x + 0.f, h.y + 1.f, h.z + 0.f}, my = {h.x - 0.f, h.y - 1.f, h.z - 0.f};
+  v3 pz = {h.x + 0.f, h.y + 0.f, h.z + 1.f}, mz = {h.x - 0.f, h.y - 0.f, h.z - 1.f};
+  v3 g;
+  g.x = sdf_trilinear(m, px, &ok[0]) - sdf_trilinear(m, mx, &ok[1]);
+  g.y = sdf_trilinear(m, py, &ok[2]) - sdf_trilinear(m, my, &ok[3]);
+  g.z = sdf_trilinear(m, pz, &ok[4]) - sdf_trilinear(m, mz, &ok[5]);
+  if (!(ok[0] && ok[1] && ok[2] && ok[3] && ok[4] && ok[5])) return 0;
+  float len = sqrtf(sqnorm3(g));
+  if (len < 1e-12f) return 0;
+  n->x = g.x / len;
+  n->y = g.y / len;
+  n->z = g.z / len;
+  return 1;
+}
+
+/* render_maps_field proj/include/rf/raycast.hpp:157-207, mode kIcpMaps */
+int rfo_render_icp(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
+                   float* raycastOut, float* pointsOut, float* normalsOut) {
+  intr_t in = intr_from(wh, f4);
+  params_t s = params_from(params6);
+  pose_t pose = pose_from12(pose12);
+  pose_t c2w = pose_inverse(&pose);
+  v3 origin = {c2w.t[0], c2w.t[1], c2w.t[2]};
+  if (m->rangeW != in.w || m->rangeH != in.h) return -1;
+  for (int y = 0; y < in.h; ++y)
+    for (int x = 0; x < in.w; ++x) {
+      size_t i = (size_t)y * in.w + x;
+      float* rc = raycastOut + 4 * i;
+      float* pt = pointsOut + 4 * i;
+      float* nm = normalsOut + 4 * i;
+      rc[0] = rc[1] = rc[2] = 0.f;
+      rc[3] = -1.f;
+      pt[0] = pt[1] = pt[2] = 0.f;
+      pt[3] = -1.f;
+      nm[0] = nm[1] = nm[2] = 0.f;
+      nm[3] = -1.f;
+      float r0 = m->range[2 * i], r1 = m->range[2 * i + 1];
+      if (!(r1 >= r0)) continue;
+      v3 dirCam = {((float)x - in.cx) / in.fx, ((float)y - in.cy) / in.fy, 1.f};
+      float norm = sqrtf(sqnorm3(dirCam));
+      v3 dw = rot_apply(c2w.R, dirCam);
+      v3 dirW = {dw.x / norm, dw.y / norm, dw.z / norm};
+      v3 hit;
+      if (!cast_ray(m, origin, dirW, r0 * norm, r1 * norm, s.mu, s.voxelSize, &hit)) continue;
+      rc[0] = hit.x;
+      rc[1] = hit.y;
+      rc[2] = hit.z;
+      rc[3] = 1.f;
+      pt[0] = hit.x * s.voxelSize;
+      pt[1] = hit.y * s.voxelSize;
+      pt[2] = hit.z * s.voxelSize;
+      pt[3] = 1.f;
+      v3 n;
+      if (field_normal(m, hit, &n)) {
+        nm[0] = n.x;
+        nm[1] = n.y;
+        nm[2] = n.z;
+        nm[3] = 1.f;
+      }
+    }
+  return 0;
+}
+
+/* --------------------------------------------------------------- view */
+/* proj/src/view.cpp:112-119 depth conversion, :69-88 downsample_depth */
+int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float affOffset, int levels,
+                   float* depthLevels) {
+  if (levels < 1) return -1;
+  int w = wh[0], h = wh[1];
+  float* out = depthLevels;
+  for (int i = 0; i < w * h; ++i) {
+    out[i] = -1.f;
+    if (raw[i] == 0) continue;
+    float mtr = (float)raw[i] * affScale + affOffset;
+    out[i] = mtr > 0.f ? mtr : -1.f;
+  }
+  const float* prev = out;
+  int pw = w, ph = h;
+  out += (size_t)w * h;
+  for (int l = 1; l < levels; ++l) {
+    int lw = pw / 2, lh = ph / 2;
+    for (int y = 0; y < lh; ++y)
+      for (int x = 0; x < lw; ++x) {
+        float sum = 0.f;
+        int n = 0;
+        for (int dy = 0; dy < 2; ++dy)
+          for (int dx = 0; dx < 2; ++dx) {
+            float d = prev[(size_t)(2 * y + dy) * pw + 2 * x + dx];
+            if (d > 0.f) {
+              sum += d;
+              ++n;
+            }
+          }
+        out[(size_t)y * lw + x] = n > 0 ? sum / (float)n : -1.f;
+      }
+    prev = out;
+    out += (size_t)lw * lh;
+    pw = lw;
+    ph = lh;
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- ICP */
+/* One evaluation of the point-to-plane normal equations:
+ * per valid pixel p of the level, p_w = T_cw p_cam; project p_w into the last
+ * render (nearest pixel); V, N = render point/normal; reject invalid maps and
+ * |p_w - V| > dist; r = (p_w - V).N; J = [p_w x N; N] (left-multiplied
+ * world-frame twist [omega; nu]).  Sums accumulate in double, row-major
+ * pixel order. */
+static void icp_accumulate(const float* depth, int lw, int lh, const intr_t* inl, const float* points,
+                           const float* normals, const intr_t* inr, const pose_t* renderPose, const pose_t* c2w,
+                           float dist, double* acc29) {
+  memset(acc29, 0, sizeof(double) * 29);
+  const float dist2 = dist * dist;
+  for (int y = 0; y < lh; ++y)
+    for (int x = 0; x < lw; ++x) {
+      float d = depth[(size_t)y * lw + x];
+      if (!(d > 0.f)) continue;
+      v3 pc = backproject(inl, (float)x, (float)y, d);
+      v3 pw = pose_apply(c2w, pc);
+      v3 q = pose_apply(renderPose, pw);
+      if (!(q.z > 0.f)) continue;
+      float u = inr->fx * q.x / q.z + inr->cx;
+      float v = inr->fy * q.y / q.z + inr->cy;
+      if (!(u >= 0.f && v >= 0.f && u <= (float)(inr->w - 1) && v <= (float)(inr->h - 1))) continue;
+      int iu = (int)(u + 0.5f), iv = (int)(v + 0.5f);
+      const float* V = points + 4 * ((size_t)iv * inr->w + iu);
+      const float* N = normals + 4 * ((size_t)iv * inr->w + iu);
+      if (!(V[3] > 0.f) || !(N[3] > 0.f)) continue;
+      v3 diff = {pw.x - V[0], pw.y - V[1], pw.z - V[2]};
+      if (sqnorm3(diff) > dist2) continue;
+      v3 n = {N[0], N[1], N[2]};
+      float r = dot3(diff, n);
+      v3 pxn = cross3(pw, n);
+      double J[6] = {pxn.x, pxn.y, pxn.z, n.x, n.y, n.z};
+      double rd = r;
+      int k = 0;
+      for (int a = 0; a < 6; ++a)
+        for (int b = a; b < 6; ++b) acc29[k++] += J[a] * J[b];
+      for (int a = 0; a < 6; ++a) acc29[21 + a] += J[a] * rd;
+      acc29[27] += rd * rd;
+      acc29[28] += 1.0;
+    }
+}
+
+int rfo_icp_reduce(const float* depth, int lw, int lh, const float* f4l, const float* points, const float* normals,
+                   const int* wh, const float* renderPose12, const float* renderF4, const float* camToWorld12,
+                   float dist, double* out29) {
+  int lwh[2] = {lw, lh};
+  intr_t inl = intr_from(lwh, f4l);
+  intr_t inr = intr_from(wh, renderF4);
+  pose_t rp = pose_from12(renderPose12);
+  pose_t c2w = pose_from12(camToWorld12);
+  icp_accumulate(depth, lw, lh, &inl, points, normals, &inr, &rp, &c2w, dist, out29);
+  return 0;
+}
+
+/* double-precision SE(3) helpers (proj/include/rf/pose.hpp:38-60, S = double) */
+typedef struct {
+  double R[9];
+  double t[3];
+} posed_t;
+static void matmul3d(const double* A, const double* B, double* C) {
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) C[r * 3 + c] = A[r * 3 + 0] * B[c] + (A[r * 3 + 1] * B[3 + c] + A[r * 3 + 2] * B[6 + c]);
+}
+static posed_t se3_exp(const double* tau) {
+  const double* w = tau;
+  const double* v = tau + 3;
+  double theta = sqrt(w[0] * w[0] + (w[1] * w[1] + w[2] * w[2]));
+  double W[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+  double WW[9];
+  matmul3d(W, W, WW);
+  double a, b, c;
+  if (theta < 1e-8) {
+    a = 1.0;
+    b = 0.5;
+    c = 1.0 / 6.0;
+  } else {
+    double s = sin(theta), co = cos(theta);
+    a = s / theta;
+    b = (1.0 - co) / (theta * theta);
+    c = (theta - s) / (theta * theta * theta);
+  }
+  posed_t p;
+  double V[9];
+  for (int i = 0; i < 9; ++i) {
+    double I = (i % 4 == 0) ? 1.0 : 0.0;
+    p.R[i] = I + a * W[i] + b * WW[i];
+    V[i] = I + b * W[i] + c * WW[i];
+  }
+  for (int r = 0; r < 3; ++r) p.t[r] = V[r * 3] * v[0] + (V[r * 3 + 1] * v[1] + V[r * 3 + 2] * v[2]);
+  return p;
+}
+static posed_t posed_compose(const posed_t* a, const posed_t* b) {
+  posed_t q;
+  matmul3d(a->R, b->R, q.R);
+  for (int r = 0; r < 3; ++r)
+    q.t[r] = (a->R[r * 3] * b->t[0] + (a->R[r * 3 + 1] * b->t[1] + a->R[r * 3 + 2] * b->t[2])) + a->t[r];
+  return q;
+}
+static posed_t posed_inverse(const posed_t* p) {
+  posed_t q;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) q.R[r * 3 + c] = p->R[c * 3 + r];
+  for (int r = 0; r < 3; ++r) q.t[r] = -(q.R[r * 3] * p->t[0] + (q.R[r * 3 + 1] * p->t[1] + q.R[r * 3 + 2] * p->t[2]));
+  return q;
+}
+static pose_t posed_to_f(const posed_t* p) {
+  pose_t q;
+  for (int i = 0; i < 9; ++i) q.R[i] = (float)p->R[i];
+  for (int i = 0; i < 3; ++i) q.t[i] = (float)p->t[i];
+  return q;
+}
+
+/* Solve H x = -g for symmetric positive-definite H (Cholesky, fixed order).
+ * Returns 0 on success, -1 if H is not positive definite / det < 1e-12. */
+int rfo_solve6(const double* acc29, double* x) {
+  double A[36];
+  int k = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) {
+      A[a * 6 + b] = acc29[k];
+      A[b * 6 + a] = acc29[k];
+      ++k;
+    }
+  double L[36] = {0};
+  double det = 1.0;
+  for (int j = 0; j < 6; ++j) {
+    double s = A[j * 6 + j];
+    for (int p = 0; p < j; ++p) s -= L[j * 6 + p] * L[j * 6 + p];
+    if (!(s > 0.0)) return -1;
+    det *= s;
+    double ljj = sqrt(s);
+    L[j * 6 + j] = ljj;
+    for (int i = j + 1; i < 6; ++i) {
+      double t = A[i * 6 + j];
+      for (int p = 0; p < j; ++p) t -= L[i * 6 + p] * L[j * 6 + p];
+      L[i * 6 + j] = t / ljj;
+    }
+  }
+  if (det < 1e-12) return -1; /* SPEC.md:352 degenerate Hessian */
+  double yv[6];
+  for (int i = 0; i < 6; ++i) {
+    double t = -acc29[21 + i];
+    for (int p = 0; p < i; ++p) t -= L[i * 6 + p] * yv[p];
+    yv[i] = t / L[i * 6 + i];
+  }
+  for (int i = 5; i >= 0; --i) {
+    double t = yv[i];
+    for (int p = i + 1; p < 6; ++p) t -= L[p * 6 + i] * x[p];
+    x[i] = t / L[i * 6 + i];
+  }
+  return 0;
+}
+
+/* Coarse-to-fine tracking loop: levels
+ * coarse -> fine, at most iters[l] iterations per level, stop a level when
+ * ||delta|| < 1e-4, give up on a level when fewer than minCount pixels
+ * associate or the Hessian is degenerate.  T_cw <- exp(delta) T_cw. */
+int rfo_icp_track(const float* depthLevels, const int* wh, const float* f4, const float* points,
+                  const float* normals, const float* renderPose12, const float* renderF4, const float* initPose12,
+                  const int* icp6, const float* dist3, float* poseOut12, double* statsOut8) {
+  const int levels = icp6[0];
+  const int minCount = icp6[4];
+  intr_t in0 = intr_from(wh, f4);
+  intr_t inr = intr_from(wh, renderF4);
+  pose_t rp = pose_from12(renderPose12);
+  pose_t init = pose_from12(initPose12);
+  pose_t c2wf = pose_inverse(&init);
+  posed_t c2w;
+  for (int i = 0; i < 9; ++i) c2w.R[i] = c2wf.R[i];
+  for (int i = 0; i < 3; ++i) c2w.t[i] = c2wf.t[i];
+  /* level offsets inside depthLevels */
+  size_t off[8];
+  size_t o = 0;
+  for (int l = 0; l < levels; ++l) {
+    off[l] = o;
+    o += (size_t)(in0.w >> l) * (in0.h >> l);
+  }
+  double acc[29];
+  int totalIt = 0, converged = 0;
+  memset(statsOut8, 0, sizeof(double) * 8);
+  statsOut8[7] = 1;
+  for (int l = levels - 1; l >= 0; --l) {
+    intr_t inl = in0;
+    float sc = ldexpf(1.f, -l);
+    inl.w = in0.w >> l;
+    inl.h = in0.h >> l;
+    inl.fx = in0.fx * sc;
+    inl.fy = in0.fy * sc;
+    inl.cx = in0.cx * sc;
+    inl.cy = in0.cy * sc;
+    int it;
+    for (it = 0; it < icp6[1 + l]; ++it) {
+      pose_t c2wF = posed_to_f(&c2w);
+      icp_accumulate(depthLevels + off[l], inl.w, inl.h, &inl, points, normals, &inr, &rp, &c2wF, dist3[l], acc);
+      statsOut8[1] = acc[28];
+      statsOut8[2] = acc[27];
+      if (acc[28] < (double)minCount) {
+        statsOut8[7] = 0;
+        break;
+      }
+      double delta[6];
+      if (rfo_solve6(acc, delta) != 0) {
+        statsOut8[7] = 0;
+        break;
+      }
+      posed_t inc = se3_exp(delta);
+      c2w = posed_compose(&inc, &c2w);
+      ++totalIt;
+      double nrm = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2] + delta[3] * delta[3] +
+                        delta[4] * delta[4] + delta[5] * delta[5]);
+      if (nrm < 1e-4) {
+        converged = 1;
+        ++it;
+        break;
+      }
+    }
+    statsOut8[4 + l] = it;
+  }
+  statsOut8[0] = totalIt;
+  statsOut8[3] = converged;
+  posed_t w2c = posed_inverse(&c2w);
+  pose_t outp = posed_to_f(&w2c);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) poseOut12[r * 4 + c] = outp.R[r * 3 + c];
+    poseOut12[r * 4 + 3] = outp.t[r];
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------- export */
+uint32_t rfo_total_entries(const rfo_map* m) { return m->buckets + m->excess; }
+int rfo_export_entries(const rfo_map* m, int* out5) {
+  size_t total = (size_t)m->buckets + m->excess;
+  for (size_t i = 0; i < total; ++i) {
+    out5[5 * i] = m->entries[i].x;
+    out5[5 * i + 1] = m->entries[i].y;
+    out5[5 * i + 2] = m->entries[i].z;
+    out5[5 * i + 3] = m->entries[i].offset;
+    out5[5 * i + 4] = m->entries[i].ptr;
+  }
+  return (int)total;
+}
+int rfo_export_blocks(const rfo_map* m, const int* ptrs, int n, uint8_t* out) {
+  for (int b = 0; b < n; ++b) memcpy(out + (size_t)b * BS3 * 8, &m->vba[(size_t)ptrs[b] * BS3], BS3 * 8);
+  return 0;
+}
+int rfo_export_visible(const rfo_map* m, int* listOut, uint8_t* typesOut) {
+  if (listOut) memcpy(listOut, m->visible, sizeof(int) * m->nVisible);
+  if (typesOut) memcpy(typesOut, m->visibility, (size_t)m->buckets + m->excess);
+  return m->nVisible;
+}
+int rfo_free_counts(const rfo_map* m, int* nb, int* ne) {
+  *nb = m->nFreeBlocks;
+  *ne = m->nFreeExcess;
+  return 0;
+}

@@ -1,0 +1,91 @@
+/* oracle/rfo.h — CPU restatement oracle of the dense-fusion hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline leg may load oracle/_build/librfo.so, and only as the checker.
+ *
+ * Plain C11, compiled with -ffp-contract=off.  Every function restates the
+ * reference (/root/reference/proj) at the file:line cited beside it, with the
+ * float association order of the reference's Eigen expressions
+ * (oracle/shim/Eigen/Core documents the order: 3-term sums are e0+(e1+e2)).
+ * It is pinned bit-for-bit against the reference itself compiled here
+ * (oracle/_ref/librfref.so) by tests/test_oracle_pin.py.
+ *
+ * Conventions shared with the product C-ABI (include/rfg.h):
+ *   pose12  row-major 3x4 [R|t], world -> camera (proj/include/rf/raycast.hpp:21)
+ *   wh[2]   image width, height;  f4[4] = fx, fy, cx, cy
+ *   params6 voxelSize, mu, maxW, viewFrustum_min, viewFrustum_max, stopIntegratingAtMaxW
+ *   voxel   8 bytes = VoxelSRgb {int16 sdf, u8 w_depth, u8 clr[3], u8 w_color, pad}
+ *   entry   5 int32 = HashEntry {x, y, z, offset, ptr}
+ */
+#ifndef RFO_H
+#define RFO_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rfo_map rfo_map;
+
+uint32_t rfo_hash_index(const int* pos3, uint32_t mask);
+int rfo_traverse_blocks(const float* a3, const float* b3, int* cellsOut, int maxCells);
+int rfo_block_in_frustum(const int* pos3, const float* pose12, const int* wh, const float* f4, const float* params6);
+float rfo_update_voxel_depth(uint8_t* voxel8, const float* pt3, const float* pose12, const int* wh, const float* f4,
+                             float mu, int maxW, const float* depth, int stopAtMaxW);
+
+rfo_map* rfo_create(uint32_t buckets, uint32_t excess, uint32_t capacity);
+void rfo_destroy(rfo_map* m);
+void rfo_clear(rfo_map* m);
+/* Spatial sharding filter (multi-GPU parity oracle):
+ * a block is kept on `rank` when any block of its 3x3x3 neighbourhood is
+ * owned by `rank`; owner = hash of the (block >> tileShift) super-tile mod world.
+ * world <= 1 disables the filter. */
+void rfo_set_shard(rfo_map* m, int rank, int world, int tileShift);
+
+int rfo_allocate(rfo_map* m, const float* depth, const int* wh, const float* f4, const float* pose12,
+                 const float* params6, int* stats4);
+int rfo_integrate(rfo_map* m, const float* depth, const uint8_t* rgb, const int* whD, const float* f4D,
+                  const int* whRgb, const float* f4Rgb, const float* extr12, const float* pose12,
+                  const float* params6);
+int rfo_render_ranges(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
+                      float* rangeOut);
+int rfo_set_ranges(rfo_map* m, const int* wh, const float* rangeIn);
+int rfo_render_icp(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
+                   float* raycastOut, float* pointsOut, float* normalsOut);
+
+/* build_view depth path (proj/src/view.cpp:112-119,134-142): level 0 then each
+ * pyramid level, concatenated into depthLevels. */
+int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float affOffset, int levels,
+                   float* depthLevels);
+
+/* ICP point-to-plane depth tracker (absent in the reference; restated from
+ * see DESIGN.md "ICP oracle").
+ *   depthLevels: pyramid as produced by rfo_build_view, level 0 is wh
+ *   points/normals: last render (float4 per pixel, w > 0 valid), renderPose12
+ *   and renderF4 describe that render (resolution wh).
+ *   icp6 = {levels, iters_l0, iters_l1, iters_l2, minCount, reserved}
+ *   dist3 = outlier distance gate per level (metres)
+ *   poseOut12 = tracked world->camera pose; statsOut8 = {iterations run,
+ *   final count, final sum r^2, converged flag, per-level iterations x3, ok} */
+int rfo_icp_track(const float* depthLevels, const int* wh, const float* f4, const float* points,
+                  const float* normals, const float* renderPose12, const float* renderF4, const float* initPose12,
+                  const int* icp6, const float* dist3, float* poseOut12, double* statsOut8);
+/* One ICP evaluation (29 sums) at a given level and float pose; used by the
+ * GPU reduction parity test. out29 = H upper (21, row-major), g (6), E, n. */
+int rfo_icp_reduce(const float* depth, int lw, int lh, const float* f4l, const float* points, const float* normals,
+                   const int* wh, const float* renderPose12, const float* renderF4, const float* camToWorld12,
+                   float dist, double* out29);
+
+/* Cholesky solve of H delta = -g from the 29 sums; -1 when degenerate. */
+int rfo_solve6(const double* acc29, double* x);
+
+uint32_t rfo_total_entries(const rfo_map* m);
+int rfo_export_entries(const rfo_map* m, int* out5);
+int rfo_export_blocks(const rfo_map* m, const int* ptrs, int n, uint8_t* out);
+int rfo_export_visible(const rfo_map* m, int* listOut, uint8_t* typesOut);
+int rfo_free_counts(const rfo_map* m, int* nb, int* ne);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

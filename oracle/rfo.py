@@ -1,0 +1,210 @@
+"""ctypes wrapper over oracle/_build/librfo.so (the C restatement oracle).
+
+TEST INFRASTRUCTURE ONLY — imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline leg, never by the product package.  The API mirrors
+oracle/ref.py so tests can swap the reference build and the restatement.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from .ref import P, _d, _f, _f4, _f32, _i, _u8, _u16, _wh, params_vec
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "librfo.so")
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE, "rfo"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.rfo_hash_index.argtypes = [_i, C.c_uint32]
+        L.rfo_hash_index.restype = C.c_uint32
+        L.rfo_traverse_blocks.argtypes = [_f, _f, _i, C.c_int]
+        L.rfo_block_in_frustum.argtypes = [_i, _f, _i, _f, _f]
+        L.rfo_update_voxel_depth.argtypes = [_u8, _f, _f, _i, _f, C.c_float, C.c_int, _f, C.c_int]
+        L.rfo_update_voxel_depth.restype = C.c_float
+        L.rfo_create.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
+        L.rfo_create.restype = vp
+        L.rfo_destroy.argtypes = [vp]
+        L.rfo_clear.argtypes = [vp]
+        L.rfo_set_shard.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+        L.rfo_allocate.argtypes = [vp, _f, _i, _f, _f, _f, _i]
+        L.rfo_integrate.argtypes = [vp, _f, _u8, _i, _f, _i, _f, _f, _f, _f]
+        L.rfo_render_ranges.argtypes = [vp, _f, _i, _f, _f, _f]
+        L.rfo_set_ranges.argtypes = [vp, _i, _f]
+        L.rfo_render_icp.argtypes = [vp, _f, _i, _f, _f, _f, _f, _f]
+        L.rfo_build_view.argtypes = [_u16, _i, C.c_float, C.c_float, C.c_int, _f]
+        L.rfo_icp_track.argtypes = [_f, _i, _f, _f, _f, _f, _f, _f, _i, _f, _f, _d]
+        L.rfo_icp_reduce.argtypes = [_f, C.c_int, C.c_int, _f, _f, _f, _i, _f, _f, _f, C.c_float, _d]
+        L.rfo_solve6.argtypes = [_d, _d]
+        L.rfo_total_entries.argtypes = [vp]
+        L.rfo_total_entries.restype = C.c_uint32
+        L.rfo_export_entries.argtypes = [vp, _i]
+        L.rfo_export_blocks.argtypes = [vp, _i, C.c_int, _u8]
+        L.rfo_export_visible.argtypes = [vp, _i, _u8]
+        L.rfo_free_counts.argtypes = [vp, _i, _i]
+        _lib = L
+    return _lib
+
+
+def hash_index(pos, mask):
+    p = np.ascontiguousarray(pos, np.int32)
+    return lib().rfo_hash_index(P(p, _i), mask)
+
+
+def traverse_blocks(a, b, max_cells=256):
+    out = np.zeros((max_cells, 3), np.int32)
+    a, b = _f32(a), _f32(b)
+    n = lib().rfo_traverse_blocks(P(a, _f), P(b, _f), P(out, _i), max_cells)
+    return out[:min(n, max_cells)].copy()
+
+
+def block_in_frustum(pos, pose34, intr, params):
+    p = np.ascontiguousarray(pos, np.int32)
+    pose = _f32(pose34)
+    pv = params_vec(params)
+    wh, f4 = _wh(intr), _f4(intr)
+    return bool(lib().rfo_block_in_frustum(P(p, _i), P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f)))
+
+
+def build_view(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=1):
+    w, h = intr["width"], intr["height"]
+    sizes = [(w >> l) * (h >> l) for l in range(levels)]
+    out = np.zeros(sum(sizes), np.float32)
+    raw = np.ascontiguousarray(raw, np.uint16)
+    wh = _wh(intr)
+    lib().rfo_build_view(P(raw, _u16), P(wh, _i), aff[0], aff[1], levels, P(out, _f))
+    res, o = [], 0
+    for l, s in enumerate(sizes):
+        res.append(out[o:o + s].reshape(h >> l, w >> l))
+        o += s
+    return res
+
+
+def icp_track(levels_depth, intr, points, normals, render_pose34, render_intr, init_pose34,
+              iters=(6, 10, 20), min_count=10, dist=(0.1, 0.1, 0.1)):
+    flat = np.ascontiguousarray(np.concatenate([d.reshape(-1) for d in levels_depth]), np.float32)
+    wh, f4 = _wh(intr), _f4(intr)
+    rf4 = _f4(render_intr)
+    icp6 = np.array([len(levels_depth), iters[0], iters[1], iters[2], min_count, 0], np.int32)
+    d3 = _f32(dist)
+    out = np.zeros((3, 4), np.float32)
+    stats = np.zeros(8, np.float64)
+    pts, nrm = _f32(points), _f32(normals)
+    rp, ip = _f32(render_pose34), _f32(init_pose34)
+    lib().rfo_icp_track(P(flat, _f), P(wh, _i), P(f4, _f), P(pts, _f), P(nrm, _f), P(rp, _f), P(rf4, _f),
+                        P(ip, _f), P(icp6, _i), P(d3, _f), P(out, _f), P(stats, _d))
+    return out, stats
+
+
+def icp_reduce(depth_l, f4l, points, normals, intr, render_pose34, render_intr, cam_to_world34, dist):
+    d = _f32(depth_l)
+    lh, lw = d.shape
+    f4l = _f32(f4l)
+    out = np.zeros(29, np.float64)
+    pts, nrm = _f32(points), _f32(normals)
+    rp, c2w = _f32(render_pose34), _f32(cam_to_world34)
+    wh, rf4 = _wh(intr), _f4(render_intr)
+    lib().rfo_icp_reduce(P(d, _f), lw, lh, P(f4l, _f), P(pts, _f), P(nrm, _f), P(wh, _i), P(rp, _f), P(rf4, _f),
+                         P(c2w, _f), dist, P(out, _d))
+    return out
+
+
+class OracleEngine:
+    """C restatement of VoxelBlockMap + FusionEngine + RenderState."""
+
+    def __init__(self, buckets, excess, capacity):
+        self.h = lib().rfo_create(buckets, excess, capacity)
+        if not self.h:
+            raise ValueError("bucketCount must be a power of two")
+        self.capacity = capacity
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().rfo_destroy(self.h)
+            self.h = None
+
+    def set_shard(self, rank, world, tile_shift=3):
+        lib().rfo_set_shard(self.h, rank, world, tile_shift)
+
+    def allocate(self, depth, intr, pose34, params):
+        stats = np.zeros(4, np.int32)
+        d, pose, pv = _f32(depth), _f32(pose34), params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        lib().rfo_allocate(self.h, P(d, _f), P(wh, _i), P(f4, _f), P(pose, _f), P(pv, _f), P(stats, _i))
+        return stats, 0.0
+
+    def integrate(self, depth, intr, pose34, params, rgb=None, intr_rgb=None, extr34=None):
+        d, pose, pv = _f32(depth), _f32(pose34), params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        whr = _wh(intr_rgb) if intr_rgb else None
+        f4r = _f4(intr_rgb) if intr_rgb else None
+        ex = _f32(extr34) if extr34 is not None else None
+        c = np.ascontiguousarray(rgb, np.uint8) if rgb is not None else None
+        lib().rfo_integrate(self.h, P(d, _f), P(c, _u8), P(wh, _i), P(f4, _f), P(whr, _i), P(f4r, _f), P(ex, _f),
+                            P(pose, _f), P(pv, _f))
+        return 0.0
+
+    def render_ranges(self, pose34, intr, params):
+        rng = np.zeros((intr["height"], intr["width"], 2), np.float32)
+        pose, pv = _f32(pose34), params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        lib().rfo_render_ranges(self.h, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(rng, _f))
+        return rng, 0.0
+
+    def set_ranges(self, intr, rng):
+        wh = _wh(intr)
+        r = _f32(rng)
+        lib().rfo_set_ranges(self.h, P(wh, _i), P(r, _f))
+
+    def render_icp(self, pose34, intr, params):
+        h, w = intr["height"], intr["width"]
+        rc = np.zeros((h, w, 4), np.float32)
+        pts = np.zeros((h, w, 4), np.float32)
+        nrm = np.zeros((h, w, 4), np.float32)
+        pose, pv = _f32(pose34), params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        rc_ = lib().rfo_render_icp(self.h, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(rc, _f), P(pts, _f),
+                                   P(nrm, _f))
+        if rc_ != 0:
+            raise RuntimeError("render_icp before render_ranges")
+        return rc, pts, nrm, 0.0
+
+    def entries(self):
+        n = lib().rfo_total_entries(self.h)
+        out = np.zeros((n, 5), np.int32)
+        lib().rfo_export_entries(self.h, P(out, _i))
+        return out
+
+    def blocks(self, ptrs):
+        ptrs = np.ascontiguousarray(ptrs, np.int32)
+        out = np.zeros((len(ptrs), 512, 8), np.uint8)
+        if len(ptrs):
+            lib().rfo_export_blocks(self.h, P(ptrs, _i), len(ptrs), P(out, _u8))
+        return out
+
+    def visible(self):
+        n = lib().rfo_total_entries(self.h)
+        lst = np.zeros(n, np.int32)
+        types = np.zeros(n, np.uint8)
+        k = lib().rfo_export_visible(self.h, P(lst, _i), P(types, _u8))
+        return lst[:k].copy(), types
+
+    def free_counts(self):
+        nb, ne = C.c_int(0), C.c_int(0)
+        lib().rfo_free_counts(self.h, C.byref(nb), C.byref(ne))
+        return nb.value, ne.value
