@@ -1,0 +1,204 @@
+/* rfg.h — C ABI of the B200-native dense-fusion hot path (librfg.so).
+ *
+ * Drop-in replacement for the reference's per-frame engine calls
+ * (/root/reference/proj).  The reference has no plugin/FFI layer: its
+ * boundary is the concrete C++ API listed beside each entry point.  A C++
+ * adapter with the reference's own names sits on top of this ABI in
+ * include/rfg.hpp; Python binds it with ctypes (paper_1708_00783_b200/_lib.py).
+ *
+ * Conventions
+ *  - Every call returns an int status (RFG_OK = 0, negative on error) and never
+ *    throws; rfg_last_error() returns the message of the last failure on the
+ *    calling thread.
+ *  - Poses are row-major 3x4 [R | t] float arrays, world -> camera
+ *    (proj/include/rf/raycast.hpp:21, proj/include/rf/synth.hpp:62).
+ *  - Pointers named *_dev are device pointers owned by the caller; the map
+ *    owns its hash table, voxel block array, free stacks, visible list and
+ *    scratch in device memory.
+ *  - Work is enqueued on the map's stream (rfg_map_set_stream); calls are
+ *    asynchronous unless they return host data (stats, exports), which
+ *    synchronise the stream.
+ *  - A CUDA error or an invalid argument fails loudly with a status code;
+ *    there is no CPU fallback.
+ */
+#ifndef RFG_H
+#define RFG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RFG_OK 0
+#define RFG_EINVAL (-1)   /* invalid argument (e.g. non-power-of-two bucketCount) */
+#define RFG_ECUDA (-2)    /* CUDA runtime error / no device */
+#define RFG_ENOMEM (-3)   /* device allocation failed */
+#define RFG_ERANGE (-4)   /* block coordinate outside the int16 entry layout, or DDA ordinal bound exceeded */
+#define RFG_ESTATE (-5)   /* call order violated (e.g. ICP maps before expected ranges) */
+
+typedef struct rfg_map rfg_map;
+
+/* VoxelBlockMapConfig, proj/include/rf/voxel_block_map.hpp:36-45.
+ * hasColour allocates the colour plane (ITMVoxel_s_rgb); 0 = depth-only
+ * (ITMVoxel_s: 4-byte {sdf, w_depth} voxels). */
+typedef struct {
+  uint32_t bucketCount;
+  uint32_t excessCount;
+  uint32_t blockCapacity;
+  int32_t hasColour;
+} rfg_map_config;
+
+/* Intrinsics, proj/include/rf/camera.hpp:13-47 */
+typedef struct {
+  int32_t width, height;
+  float fx, fy, cx, cy;
+} rfg_intrinsics;
+
+/* SceneParams, proj/include/rf/fusion.hpp:11-20 */
+typedef struct {
+  float voxelSize;
+  float mu;
+  int32_t maxW;
+  float viewFrustum_min;
+  float viewFrustum_max;
+  int32_t stopIntegratingAtMaxW;
+} rfg_scene_params;
+
+/* AllocationStats, proj/include/rf/fusion.hpp:22-27 */
+typedef struct {
+  int32_t requested, allocated, allocFailures, visibleCount;
+} rfg_alloc_stats;
+
+/* ------------------------------------------------------------------ map */
+/* VoxelBlockMap::VoxelBlockMap(const VoxelBlockMapConfig&)
+ * (proj/src/voxel_block_map.cpp:9-13): RFG_EINVAL when bucketCount is not a
+ * power of two (the reference throws std::invalid_argument). */
+int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out);
+int rfg_map_destroy(rfg_map* map);
+/* VoxelBlockMap::clear (proj/src/voxel_block_map.cpp:15-24) */
+int rfg_map_clear(rfg_map* map);
+/* cudaStream_t to enqueue on (NULL = legacy default stream). */
+int rfg_map_set_stream(rfg_map* map, void* cuda_stream);
+int rfg_map_sync(rfg_map* map);
+/* Multi-GPU spatial shard filter; world <= 1 disables. */
+int rfg_map_set_shard(rfg_map* map, int rank, int world, int tile_shift);
+const char* rfg_last_error(void);
+/* Number of kernels this library has launched in the process. */
+uint64_t rfg_kernel_launch_count(void);
+
+/* ---------------------------------------------------------- fusion engine */
+/* FusionEngine::allocate_from_depth (proj/src/fusion.cpp:144-235,
+ * proj/include/rf/fusion.hpp:63-68).  depth_dev: level-0 metres (View::depth_m),
+ * width*height floats, invalid <= 0.  stats may be NULL (fully asynchronous);
+ * otherwise the call synchronises and fills it. */
+int rfg_allocate_from_depth(rfg_map* map, const float* depth_dev, const rfg_intrinsics* intr, const float pose34[12],
+                            const rfg_scene_params* params, rfg_alloc_stats* stats);
+
+/* FusionEngine::integrate_frame (proj/src/fusion.cpp:237-263).  rgb_dev
+ * (packed RGB8, intr_rgb sized) may be NULL for depth-only fusion;
+ * extr34 = extrinsics_d_to_rgb (NULL = identity). */
+int rfg_integrate(rfg_map* map, const float* depth_dev, const uint8_t* rgb_dev, const rfg_intrinsics* intr_d,
+                  const rfg_intrinsics* intr_rgb, const float extr34[12], const float pose34[12],
+                  const rfg_scene_params* params);
+
+/* ------------------------------------------------------------- raycast */
+/* render_expected_ranges (proj/src/raycast.cpp:86-127): range_dev receives
+ * width*height float2 (min, max); unset pixels keep (FLT_MAX, -1). */
+int rfg_render_expected_ranges(rfg_map* map, const float pose34[12], const rfg_intrinsics* intr,
+                               const rfg_scene_params* params, float* range_dev);
+
+/* render_maps(..., RenderMode::kIcpMaps, ...) (proj/src/raycast.cpp:129-139,
+ * proj/include/rf/raycast.hpp:157-207).  Outputs are width*height float4
+ * images: raycastResult (voxel coords, w = 1 hit), points (world metres),
+ * normals (world unit normals); invalid = (0,0,0,-1). */
+int rfg_render_icp_maps(rfg_map* map, const float pose34[12], const rfg_intrinsics* intr,
+                        const rfg_scene_params* params, const float* range_dev, float* raycast_dev, float* points_dev,
+                        float* normals_dev);
+
+/* ---------------------------------------------------------------- view */
+/* build_view depth path (proj/src/view.cpp:100-143): raw u16 -> metres
+ * (m = raw*scale + offset, raw == 0 or m <= 0 -> -1) and `levels` pyramid
+ * levels by 2x2 valid-mean (downsample_depth, view.cpp:69-88), written
+ * back to back into depth_levels_dev. */
+int rfg_build_view_depth(const uint16_t* raw_dev, int width, int height, float aff_scale, float aff_offset, int levels,
+                         float* depth_levels_dev, void* cuda_stream);
+
+/* ----------------------------------------------------------------- ICP */
+/* Point-to-plane ICP tracker (ITMDepthTracker; absent in the reference, see
+ * DESIGN.md "ICP oracle" and SPEC.md:348-356).  depth_levels_dev as produced
+ * by rfg_build_view_depth; points/normals_dev and render_pose34 describe the
+ * previous ICP-map render at level-0 resolution.  iters[3] per level (level 0
+ * = finest), dist[3] outlier gates (m).  pose_out34 = tracked world->camera.
+ * stats8 = {iterations, count, sum r^2, converged, it_l0, it_l1, it_l2, ok}. */
+int rfg_icp_track(rfg_map* map, const float* depth_levels_dev, int levels, const rfg_intrinsics* intr,
+                  const float* points_dev, const float* normals_dev, const float render_pose34[12],
+                  const float init_pose34[12], const int iters[3], const float dist[3], int min_count,
+                  float pose_out34[12], double stats8[8]);
+/* One evaluation of the 29 normal-equation sums (H upper 21, g 6, sum r^2,
+ * count) at pyramid level `level` for camera->world pose cam_to_world34. */
+int rfg_icp_reduce(rfg_map* map, const float* depth_level_dev, int level, const rfg_intrinsics* intr,
+                   const float* points_dev, const float* normals_dev, const float render_pose34[12],
+                   const float cam_to_world34[12], float dist, double out29[29]);
+
+/* ------------------------------------------------------ frame pipeline */
+/* The per-frame driver (ITMMainEngine::ProcessFrame order):
+ * [track] -> allocate -> integrate -> expected ranges -> ICP-map raycast,
+ * device resident, capturable in a CUDA graph.  The pose of each frame
+ * lives on the device (tracked or supplied). */
+typedef struct rfg_pipeline rfg_pipeline;
+typedef struct {
+  rfg_intrinsics intr;     /* depth camera, level 0 */
+  rfg_scene_params params;
+  float aff_scale, aff_offset;  /* DepthAffine */
+  int32_t levels;          /* pyramid levels (1..3) */
+  int32_t track;           /* 1 = ICP tracking from the previous render */
+  int32_t iters[3];
+  float dist[3];
+  int32_t min_count;
+  int32_t use_graph;       /* capture the frame into a CUDA graph */
+} rfg_pipeline_config;
+
+int rfg_pipeline_create(rfg_map* map, const rfg_pipeline_config* cfg, rfg_pipeline** out);
+int rfg_pipeline_destroy(rfg_pipeline* p);
+/* Enqueue one frame from raw depth already on the device.  pose34 (host) is
+ * used when tracking is off or for the first frame; NULL keeps the device
+ * pose.  Asynchronous. */
+int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const float* pose34);
+/* Enqueue one frame from HOST raw depth (copied H2D inside the call). */
+int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* raw_host, const float* pose34);
+/* Read back the last frame's stats and pose (synchronises). */
+int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float pose_out34[12], double icp_stats8[8]);
+/* Device pointers of the pipeline's buffers (for parity checks). */
+int rfg_pipeline_buffers(rfg_pipeline* p, float** depth_levels, float** range, float** raycast, float** points,
+                         float** normals);
+/* Reset the device pose / tracking state (not the map). */
+int rfg_pipeline_reset(rfg_pipeline* p);
+
+/* --------------------------------------------------------------- export */
+uint32_t rfg_total_entries(const rfg_map* map);
+/* Host copies for parity: entries as 5 int32 {x, y, z, offset, ptr}
+ * (HashEntry, voxel_block_map.hpp:17-27) */
+int rfg_export_entries(rfg_map* map, int32_t* out5_host);
+/* VoxelSRgb bytes {sdf lo, sdf hi, w_depth, r, g, b, w_color, 0} of the given
+ * VBA blocks (512 voxels each) */
+int rfg_export_blocks(rfg_map* map, const int32_t* ptrs_host, int n, uint8_t* out_host);
+/* visibleList (sorted entry indices) and per-entry visibility bytes
+ * (nullable); returns the count in *count */
+int rfg_export_visible(rfg_map* map, int32_t* list_host, uint8_t* types_host, int32_t* count);
+int rfg_free_counts(rfg_map* map, int32_t* free_blocks, int32_t* free_excess);
+
+/* ------------------------------------------------------------ synthetic */
+/* Synthetic analytic scenes (the reference's synth module,
+ * proj/src/synth.cpp, re-implemented as a frame source for benchmarks):
+ * scene 0 = make_sphere_in_room_scene, 1 = multi-room (C4), 2 = checker wall. */
+int rfg_synth_orbit_poses(const float target3[3], float distance, int frames, float max_angle, float* out34);
+int rfg_synth_multiroom_poses(int frames, float* out34);
+int rfg_synth_render(int scene, const float pose34[12], const rfg_intrinsics* intr, float aff_scale, float aff_offset,
+                     int render_rgb, uint16_t* raw_out, float* depth_out, uint8_t* rgb_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RFG_H */

@@ -1,0 +1,419 @@
+// rfg_alloc.cu — voxel-block hash allocation and visible-list construction
+// (FusionEngine::allocate_from_depth, proj/src/fusion.cpp:144-235).
+//
+// Stage 1 (k_alloc_stage1): one thread per depth pixel walks the blocks
+//   stabbed by its d±mu segment (Amanatides-Woo DDA, fusion.cpp:72-114) and
+//   probes each block's bucket chain.  Found blocks are marked; missing ones
+//   request allocation at the bucket or chain tail.  The serial reference
+//   resolves intra-frame collisions "last writer wins" in (row-major pixel,
+//   DDA ordinal) order (fusion.cpp:168-176); here every request is keyed
+//   (pixel << 6 | ordinal) + 1 and an atomicMax per slot keeps the serial
+//   winner, aggregated per warp with __match_any_sync first.
+// Stage 2 (k_req_count / k_scan_tiles / k_req_assign): requests are served in
+//   ascending entry-index order, exactly as the serial scan (fusion.cpp:190-201):
+//   a request succeeds iff it is a bucket request or among the first
+//   nFreeExcess excess requests, and its rank among such candidates is below
+//   nFreeBlocks.  Ranks come from a tile scan, so the VBA block and excess
+//   slot each request pops are the ones the serial free stacks would pop —
+//   the resulting hash table is bit-identical, not only set-identical.
+// Stage 3 (k_vis_count / k_scan_tiles / k_vis_emit): candidates = this
+//   frame's marks ∪ the previous visible list (its visibility bytes), frustum
+//   tested (fusion.cpp:116-130), compacted in ascending index order (= the
+//   reference's std::sort, fusion.cpp:231).
+#include "rfg_common.cuh"
+
+namespace rfg {
+
+__device__ __forceinline__ Pose load_pose(const FrameArgs& fa) {
+  return pose_from12(fa.poseDev ? fa.poseDev : fa.pose);
+}
+
+// Amanatides-Woo traversal (fusion.cpp:72-114).  visit(cell, ordinal) is
+// called for each visited cell in order; returning false stops the walk.
+template <class F>
+__device__ __forceinline__ void traverse_blocks(f3 a, f3 b, F&& visit) {
+  int c[3] = {(int)floorf(a.x), (int)floorf(a.y), (int)floorf(a.z)};
+  const int e[3] = {(int)floorf(b.x), (int)floorf(b.y), (int)floorf(b.z)};
+  int ord = 0;
+  if (!visit(i3{c[0], c[1], c[2]}, ord++)) return;
+  if (c[0] == e[0] && c[1] == e[1] && c[2] == e[2]) return;
+  const float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
+  const float av[3] = {a.x, a.y, a.z};
+  int step[3];
+  float tMax[3], tDelta[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (d[k] > 0.f) {
+      step[k] = 1;
+      tMax[k] = ((float)(c[k] + 1) - av[k]) / d[k];
+      tDelta[k] = 1.f / d[k];
+    } else if (d[k] < 0.f) {
+      step[k] = -1;
+      tMax[k] = ((float)c[k] - av[k]) / d[k];
+      tDelta[k] = -1.f / d[k];
+    } else {
+      step[k] = 0;
+      tMax[k] = FLT_MAX;
+      tDelta[k] = FLT_MAX;
+    }
+  }
+  const int maxSteps = abs(e[0] - c[0]) + abs(e[1] - c[1]) + abs(e[2] - c[2]) + 8;
+  for (int i = 0; i < maxSteps; ++i) {
+    int axis = 0;
+    if (tMax[1] < tMax[0]) axis = 1;
+    if (tMax[2] < tMax[axis]) axis = 2;
+    if (tMax[axis] > 1.f) break;
+    c[axis] += step[axis];
+    tMax[axis] += tDelta[axis];
+    if (!visit(i3{c[0], c[1], c[2]}, ord++)) return;
+    if (c[0] == e[0] && c[1] == e[1] && c[2] == e[2]) break;
+  }
+  if (!(c[0] == e[0] && c[1] == e[1] && c[2] == e[2])) visit(i3{e[0], e[1], e[2]}, ord++);
+}
+
+// Segment of pixel (x, y) in block units (fusion.cpp:183-186).
+__device__ __forceinline__ bool pixel_segment(const float* depth, const FrameArgs& fa, const Pose& camToWorld,
+                                              int x, int y, f3* a, f3* b) {
+  const float d = depth[(size_t)y * fa.w + x];
+  if (d <= 0.f || d < fa.vfMin || d > fa.vfMax) return false;
+  const Intr in{fa.w, fa.h, fa.fx, fa.fy, fa.cx, fa.cy};
+  const float invBlock = 1.f / (fa.voxelSize * (float)kBlock);
+  const f3 nearP = pose_apply(camToWorld, backproject(in, (float)x, (float)y, d - fa.mu));
+  const f3 farP = pose_apply(camToWorld, backproject(in, (float)x, (float)y, d + fa.mu));
+  *a = f3{nearP.x * invBlock, nearP.y * invBlock, nearP.z * invBlock};
+  *b = f3{farP.x * invBlock, farP.y * invBlock, farP.z * invBlock};
+  return true;
+}
+
+// Shard filter: block kept on `rank` if any block of its 3x3x3
+// neighbourhood is owned by it (owner = hash of the super-tile mod world).
+__device__ __forceinline__ bool shard_keeps(const DevMap& m, i3 b) {
+  if (m.world <= 1) return true;
+  const int s = m.tileShift;
+  // distinct super-tiles touched by b-1..b+1 per axis
+  const int x0 = (b.x - 1) >> s, x1 = (b.x + 1) >> s;
+  const int y0 = (b.y - 1) >> s, y1 = (b.y + 1) >> s;
+  const int z0 = (b.z - 1) >> s, z1 = (b.z + 1) >> s;
+  for (int tz = z0; tz <= z1; ++tz)
+    for (int ty = y0; ty <= y1; ++ty)
+      for (int tx = x0; tx <= x1; ++tx)
+        if ((int)(hash_index(tx, ty, tz, 0xFFFFFFFFu) % (uint32_t)m.world) == m.rank) return true;
+  return false;
+}
+
+// ------------------------------------------------------------- stage 1
+__global__ void __launch_bounds__(256) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const bool inside = x < fa.w && y < fa.h;
+  const Pose camToWorld = pose_inverse(load_pose(fa));
+  f3 a, b;
+  const bool active = inside && pixel_segment(depth, fa, camToWorld, x, y, &a, &b);
+  if (!active) return;
+  const uint32_t pixKey = (uint32_t)(y * fa.w + x) << 6;
+  const uint32_t mask = m.buckets - 1;
+  traverse_blocks(a, b, [&](i3 cell, int ord) -> bool {
+    if (ord >= 64) {
+      atomicOr(&m.state->error, 1 << 1);  // ordinal bound (RFG_ERANGE)
+      return false;
+    }
+    if (!shard_keeps(m, cell)) return true;
+    if (!in_i16(cell)) {
+      atomicOr(&m.state->error, 1 << 0);  // coordinate outside the int16 entry layout
+      return true;
+    }
+    // markBlock (fusion.cpp:155-177)
+    int idx = (int)hash_index(cell.x, cell.y, cell.z, mask);
+    int4 e = ld_entry(m.entries, idx);
+    if (entry_allocated(e)) {
+      const int xy = pack_xy(cell);
+      for (;;) {
+        if (e.x == xy && e.y == cell.z) {
+          const uint8_t v = e.w >= 0 ? 1 : 2;
+          if (m.marked[idx] != v) m.marked[idx] = v;
+          return true;
+        }
+        if (e.z < 1) break;
+        idx = (int)m.buckets + e.z - 1;
+        e = ld_entry(m.entries, idx);
+      }
+    }
+    // request at bucket (type 1) or chain tail (type 2); serial last writer wins
+    const uint32_t key = (pixKey | (uint32_t)ord) + 1u;
+    if (m.reqKey[idx] < key) atomicMax(&m.reqKey[idx], key);
+    return true;
+  });
+}
+
+// Recompute the block a request key refers to (pixel, DDA ordinal).
+__device__ __forceinline__ i3 decode_request(uint32_t key, const float* depth, const FrameArgs& fa,
+                                             const Pose& camToWorld) {
+  const uint32_t k = key - 1u;
+  const int pixel = (int)(k >> 6), ord = (int)(k & 63u);
+  const int x = pixel % fa.w, y = pixel / fa.w;
+  f3 a, b;
+  i3 out{0, 0, 0};
+  if (!pixel_segment(depth, fa, camToWorld, x, y, &a, &b)) return out;
+  traverse_blocks(a, b, [&](i3 cell, int o) -> bool {
+    if (o == ord) {
+      out = cell;
+      return false;
+    }
+    return true;
+  });
+  return out;
+}
+
+// ------------------------------------------------------- block scan util
+template <int NT>
+__device__ __forceinline__ int2 block_exclusive_scan2(int2 v, int2* total) {
+  __shared__ int2 warpSums[NT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int2 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int a = __shfl_up_sync(0xffffffffu, inc.x, o);
+    int b = __shfl_up_sync(0xffffffffu, inc.y, o);
+    if (lane >= o) {
+      inc.x += a;
+      inc.y += b;
+    }
+  }
+  if (lane == 31) warpSums[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int2 s = lane < NT / 32 ? warpSums[lane] : make_int2(0, 0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, s.x, o);
+      int b = __shfl_up_sync(0xffffffffu, s.y, o);
+      if (lane >= o) {
+        s.x += a;
+        s.y += b;
+      }
+    }
+    if (lane < NT / 32) warpSums[lane] = s;  // inclusive warp prefix
+  }
+  __syncthreads();
+  int2 base = wid > 0 ? warpSums[wid - 1] : make_int2(0, 0);
+  *total = warpSums[NT / 32 - 1];
+  __syncthreads();
+  return make_int2(base.x + inc.x - v.x, base.y + inc.y - v.y);
+}
+
+// Exclusive scan of per-tile counts (single CTA).
+__global__ void __launch_bounds__(1024) k_scan_tiles(int2* counts, int2* prefix, int n, MapState* st, int mode) {
+  const int per = (n + 1023) / 1024;
+  const int lo = threadIdx.x * per;
+  int2 sum = make_int2(0, 0);
+  for (int i = lo; i < min(n, lo + per); ++i) {
+    sum.x += counts[i].x;
+    sum.y += counts[i].y;
+  }
+  int2 total;
+  int2 ex = block_exclusive_scan2<1024>(sum, &total);
+  for (int i = lo; i < min(n, lo + per); ++i) {
+    prefix[i] = ex;
+    ex.x += counts[i].x;
+    ex.y += counts[i].y;
+  }
+  if (threadIdx.x == 0) {
+    prefix[n] = total;
+    if (mode == 0) st->nRequests = total.x;
+    if (mode == 1) {
+      st->nVisible = total.x;
+      st->stats[3] = total.x;
+    }
+  }
+}
+
+// --------------------------------------------------------------- stage 2
+// Count requests (and excess-linked requests) per tile.
+__global__ void __launch_bounds__(kTileThreads) k_req_count(DevMap m) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    MapState* st = m.state;
+    st->snapFreeBlocks = st->nFreeBlocks;
+    st->snapFreeExcess = st->nFreeExcess;
+    st->succ = 0;
+    st->succType2 = 0;
+  }
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
+  int n = 0, n2 = 0;
+  if (base < m.total) {
+    const uint4* kp = reinterpret_cast<const uint4*>(m.reqKey + base);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 k4 = kp[q];
+      const uint32_t ks[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (ks[j]) {
+          ++n;
+          if (entry_allocated(ld_entry(m.entries, base + q * 4 + j))) ++n2;
+        }
+    }
+  }
+  int2 total;
+  block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
+  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = total;
+}
+
+// Serve requests in ascending index order with serial-equivalent ranks.
+__global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
+  uint32_t keys[16];
+  int n = 0, n2 = 0;
+  uint32_t isT2 = 0;
+  if (base < m.total) {
+    const uint4* kp = reinterpret_cast<const uint4*>(m.reqKey + base);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 k4 = kp[q];
+      keys[q * 4 + 0] = k4.x;
+      keys[q * 4 + 1] = k4.y;
+      keys[q * 4 + 2] = k4.z;
+      keys[q * 4 + 3] = k4.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (keys[j]) {
+        ++n;
+        if (entry_allocated(ld_entry(m.entries, base + j))) {
+          ++n2;
+          isT2 |= 1u << j;
+        }
+      }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) keys[j] = 0;
+  }
+  int2 total;
+  int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
+  if (n == 0) return;
+  const int2 tp = m.tilePrefix[blockIdx.x];
+  int before = tp.x + ex.x, before2 = tp.y + ex.y;
+  const int nB = m.state->snapFreeBlocks, nE = m.state->snapFreeExcess;
+  const Pose camToWorld = pose_inverse(load_pose(fa));
+  int succ = 0, succ2 = 0;
+  for (int j = 0; j < 16; ++j) {
+    if (!keys[j]) continue;
+    const int idx = (int)(base + j);
+    const bool t2 = (isT2 >> j) & 1u;
+    const int before1 = before - before2;
+    const int r2 = before2;
+    const bool cand = !t2 || r2 < nE;
+    const int rb = before1 + min(before2, nE);
+    m.reqKey[idx] = 0u;  // consume the request slot
+    ++before;
+    if (t2) ++before2;
+    if (!cand || rb >= nB) continue;
+    const i3 p = decode_request(keys[j], depth, fa, camToWorld);
+    const int blockPtr = m.freeBlocks[nB - 1 - rb];
+    if (!t2) {
+      // free bucket slot (voxel_block_map.cpp:96-104)
+      const int keep = m.entries[idx].z;
+      m.entries[idx] = make_entry(p.x, p.y, p.z, keep, blockPtr);
+      m.marked[idx] = 1;
+    } else {
+      // chain tail: link a fresh excess slot (voxel_block_map.cpp:84-93)
+      const int excessIdx = m.freeExcess[nE - 1 - r2];
+      const int newIdx = (int)m.buckets + excessIdx;
+      m.entries[newIdx] = make_entry(p.x, p.y, p.z, 0, blockPtr);
+      m.entries[idx].z = excessIdx + 1;
+      m.marked[newIdx] = 1;
+      ++succ2;
+    }
+    ++succ;
+  }
+  if (succ) atomicAdd(&m.state->succ, succ);
+  if (succ2) atomicAdd(&m.state->succType2, succ2);
+}
+
+// --------------------------------------------------------------- stage 3
+// proj/src/fusion.cpp:116-130
+__device__ __forceinline__ bool block_in_frustum(int bx, int by, int bz, const Pose& pose, const FrameArgs& fa) {
+  const float bs = fa.voxelSize * (float)kBlock;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const f3 corner{((float)bx + (float)(c & 1)) * bs, ((float)by + (float)((c >> 1) & 1)) * bs,
+                    ((float)bz + (float)((c >> 2) & 1)) * bs};
+    const f3 pc = pose_apply(pose, corner);
+    if (pc.z < fa.vfMin || pc.z > fa.vfMax) continue;
+    const float px = fa.fx * pc.x / pc.z + fa.cx;
+    const float py = fa.fy * pc.y / pc.z + fa.cy;
+    if (px >= -0.f && py >= -0.f && px <= (float)(fa.w - 1) + 0.f && py <= (float)(fa.h - 1) + 0.f) return true;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs fa) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // finalise stage 2 (all k_req_assign CTAs have completed)
+    MapState* st = m.state;
+    st->nFreeBlocks = st->snapFreeBlocks - st->succ;
+    st->nFreeExcess = st->snapFreeExcess - st->succType2;
+    st->stats[0] = st->nRequests;
+    st->stats[1] = st->succ;
+    st->stats[2] = st->nRequests - st->succ;
+  }
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
+  int n = 0;
+  if (base < m.total) {
+    uint4* mp = reinterpret_cast<uint4*>(m.marked + base);
+    uint4* vp = reinterpret_cast<uint4*>(m.visibility + base);
+    const uint4 mk = *mp;
+    const uint4 vk = *vp;
+    const uint32_t cand[4] = {mk.x | vk.x, mk.y | vk.y, mk.z | vk.z, mk.w | vk.w};
+    if (cand[0] | cand[1] | cand[2] | cand[3]) {
+      const Pose pose = load_pose(fa);
+      uint32_t out[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (!((cand[j >> 2] >> ((j & 3) * 8)) & 0xFFu)) continue;
+        const int4 e = ld_entry(m.entries, base + j);
+        if (!entry_allocated(e)) continue;
+        if (block_in_frustum(entry_x(e), entry_y(e), entry_z(e), pose, fa)) {
+          out[j >> 2] |= (e.w >= 0 ? 1u : 2u) << ((j & 3) * 8);
+          ++n;
+        }
+      }
+      *vp = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+    if (mk.x | mk.y | mk.z | mk.w) *mp = make_uint4(0, 0, 0, 0);
+  }
+  int2 total;
+  block_exclusive_scan2<kTileThreads>(make_int2(n, 0), &total);
+  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (base < m.total) v = *reinterpret_cast<const uint4*>(m.visibility + base);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  int n = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) n += ((w[j >> 2] >> ((j & 3) * 8)) & 0xFFu) ? 1 : 0;
+  int2 total;
+  int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, 0), &total);
+  if (n == 0) return;
+  int o = m.tilePrefix[blockIdx.x].x + ex.x;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if ((w[j >> 2] >> ((j & 3) * 8)) & 0xFFu) m.visibleList[o++] = (int)(base + j);
+}
+
+cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s) {
+  dim3 g1((fa.w + 31) / 32, (fa.h + 7) / 8);
+  k_alloc_stage1<<<g1, 256, 0, s>>>(m, depth, fa);
+  k_req_count<<<m.nTiles, kTileThreads, 0, s>>>(m);
+  k_scan_tiles<<<1, 1024, 0, s>>>(m.tileCounts, m.tilePrefix, m.nTiles, m.state, 0);
+  k_req_assign<<<m.nTiles, kTileThreads, 0, s>>>(m, depth, fa);
+  k_vis_count<<<m.nTiles, kTileThreads, 0, s>>>(m, fa);
+  k_scan_tiles<<<1, 1024, 0, s>>>(m.tileCounts, m.tilePrefix, m.nTiles, m.state, 1);
+  k_vis_emit<<<m.nTiles, kTileThreads, 0, s>>>(m);
+  count_launch(7);
+  return cudaGetLastError();
+}
+
+}  // namespace rfg

@@ -1,0 +1,609 @@
+// rfg_api.cu — C-ABI entry points of librfg.so (include/rfg.h): map
+// lifetime, the reference-mirroring per-stage calls, parity exports and the
+// device-resident frame pipeline with CUDA-graph replay.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rfg_common.cuh"
+
+namespace rfg {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_lastError;
+void set_error(const std::string& msg) { t_lastError = msg; }
+
+// rfg_icp.cu
+size_t icp_state_bytes();
+int icp_partial_slots();
+cudaError_t launch_icp_track(void* state, double* partials, const float* depthLevels, int levels, const Intr& in0,
+                             const float4* points, const float4* normals, const int* iters, const float* dist,
+                             int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
+                             cudaStream_t s);
+cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* depth, int lw, int lh, const float* f4l,
+                                   const Intr& in0, const float4* points, const float4* normals, const float* c2w,
+                                   const float* renderPose, float dist, cudaStream_t s);
+const double* icp_sums_ptr(void* state);
+const double* icp_stats_ptr(void* state);
+const float* icp_w2c_ptr(void* state);
+
+FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p, const float* pose34,
+                          const float* poseDev) {
+  FrameArgs fa;
+  fa.w = intr->width;
+  fa.h = intr->height;
+  fa.fx = intr->fx;
+  fa.fy = intr->fy;
+  fa.cx = intr->cx;
+  fa.cy = intr->cy;
+  fa.voxelSize = p->voxelSize;
+  fa.mu = p->mu;
+  fa.maxW = p->maxW;
+  fa.vfMin = p->viewFrustum_min;
+  fa.vfMax = p->viewFrustum_max;
+  fa.stopAtMaxW = p->stopIntegratingAtMaxW;
+  for (int i = 0; i < 12; ++i) fa.pose[i] = pose34 ? pose34[i] : ((i % 5 == 0) ? 1.f : 0.f);
+  fa.poseDev = poseDev;
+  return fa;
+}
+
+__global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_fill_u4(uint4* p, uint4 v, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_iota(int* p, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+__global__ void k_state_init(MapState* st, int nb, int ne) {
+  if (threadIdx.x) return;
+  memset(st, 0, sizeof(MapState));
+  st->nFreeBlocks = nb;
+  st->nFreeExcess = ne;
+}
+__global__ void k_set12(float* dst, Pose12 p) {
+  if (threadIdx.x < 12) dst[threadIdx.x] = p.v[threadIdx.x];
+}
+__global__ void k_copy12(float* dst, const float* src) {
+  if (threadIdx.x < 12) dst[threadIdx.x] = src[threadIdx.x];
+}
+// Gather VBA blocks (depth + colour planes) into VoxelSRgb byte layout.
+__global__ void k_export_blocks(const uint32_t* vbaD, const uint32_t* vbaC, const int* ptrs, int n, uint8_t* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * kBlock3; i += gridDim.x * blockDim.x) {
+    const int b = i / kBlock3, v = i % kBlock3;
+    const size_t src = (size_t)ptrs[b] * kBlock3 + v;
+    const uint32_t d = vbaD[src];
+    const uint32_t c = vbaC ? vbaC[src] : 0u;
+    uint8_t* o = out + (size_t)i * 8;
+    o[0] = d & 0xFF;
+    o[1] = (d >> 8) & 0xFF;
+    o[2] = (d >> 16) & 0xFF;
+    o[3] = c & 0xFF;
+    o[4] = (c >> 8) & 0xFF;
+    o[5] = (c >> 16) & 0xFF;
+    o[6] = (c >> 24) & 0xFF;
+    o[7] = 0;
+  }
+}
+__global__ void k_export_entries(const int4* e, int* out5, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int4 v = e[i];
+    out5[5 * i] = entry_x(v);
+    out5[5 * i + 1] = entry_y(v);
+    out5[5 * i + 2] = entry_z(v);
+    out5[5 * i + 3] = v.z;
+    out5[5 * i + 4] = v.w;
+  }
+}
+
+}  // namespace rfg
+
+using namespace rfg;
+
+namespace {
+
+bool valid_intr(const rfg_intrinsics* i) { return i && i->width > 0 && i->height > 0; }
+bool valid_params(const rfg_scene_params* p) { return p && p->voxelSize > 0.f && p->mu > 0.f; }
+
+#define RFG_REQUIRE(cond, msg)      \
+  do {                              \
+    if (!(cond)) {                  \
+      rfg::set_error(msg);          \
+      return RFG_EINVAL;            \
+    }                               \
+  } while (0)
+
+int check_device_error(rfg_map* m) {
+  RFG_CK(cudaMemcpyAsync(m->hostState, m->d.state, sizeof(MapState), cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaStreamSynchronize(m->stream));
+  if (m->hostState->error) {
+    const int e = m->hostState->error;
+    set_error(std::string("device flagged: ") + ((e & 1) ? "block coordinate outside int16 entry layout " : "") +
+              ((e & 2) ? "DDA ordinal bound (64) exceeded" : ""));
+    return RFG_ERANGE;
+  }
+  return RFG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rfg_last_error(void) { return t_lastError.c_str(); }
+uint64_t rfg_kernel_launch_count(void) { return g_launches.load(); }
+
+int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
+  RFG_REQUIRE(cfg && out, "null argument");
+  *out = nullptr;
+  // VoxelBlockMap ctor (voxel_block_map.cpp:10-11); bucketCount 0 is also rejected
+  RFG_REQUIRE(cfg->bucketCount != 0 && (cfg->bucketCount & (cfg->bucketCount - 1)) == 0,
+              "bucketCount must be a power of two");
+  RFG_REQUIRE(cfg->blockCapacity > 0, "blockCapacity must be positive");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device available (librfg has no CPU fallback)");
+    return RFG_ECUDA;
+  }
+  RFG_CK(cudaSetDevice(device));
+  rfg_map* m = new rfg_map();
+  memset(&m->d, 0, sizeof(DevMap));
+  m->cfg = *cfg;
+  m->device = device;
+  m->stream = nullptr;
+  DevMap& d = m->d;
+  d.buckets = cfg->bucketCount;
+  d.excess = cfg->excessCount;
+  d.capacity = cfg->blockCapacity;
+  d.total = d.buckets + d.excess;
+  d.nTiles = (int)((d.total + kTile - 1) / kTile);
+  const size_t padded = (size_t)d.nTiles * kTile;
+  d.world = 1;
+  auto alloc = [&](void** p, size_t bytes) -> bool {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  bool ok = alloc((void**)&d.entries, padded * sizeof(int4)) &&
+            alloc((void**)&d.vbaDepth, (size_t)d.capacity * kBlock3 * sizeof(uint32_t)) &&
+            (!cfg->hasColour || alloc((void**)&d.vbaColour, (size_t)d.capacity * kBlock3 * sizeof(uint32_t))) &&
+            alloc((void**)&d.freeBlocks, (size_t)d.capacity * sizeof(int)) &&
+            alloc((void**)&d.freeExcess, (size_t)(d.excess ? d.excess : 1) * sizeof(int)) &&
+            alloc((void**)&d.visibleList, padded * sizeof(int)) && alloc((void**)&d.visibility, padded) &&
+            alloc((void**)&d.reqKey, padded * sizeof(uint32_t)) && alloc((void**)&d.marked, padded) &&
+            alloc((void**)&d.state, sizeof(MapState)) && alloc((void**)&d.tileCounts, d.nTiles * sizeof(int2)) &&
+            alloc((void**)&d.tilePrefix, (d.nTiles + 1) * sizeof(int2)) &&
+            alloc((void**)&m->icpPartials, (size_t)icp_partial_slots() * 29 * sizeof(double)) &&
+            alloc((void**)&m->icpOut, icp_state_bytes()) && alloc((void**)&m->icpPose, 64 * sizeof(float));
+  if (ok && cudaMallocHost((void**)&m->hostState, sizeof(MapState)) != cudaSuccess) {
+    cudaGetLastError();
+    ok = false;
+  }
+  if (!ok) {
+    rfg_map_destroy(m);
+    set_error("device allocation failed");
+    return RFG_ENOMEM;
+  }
+  m->icpPartialSlots = icp_partial_slots();
+  const int rc = rfg_map_clear(m);
+  if (rc != RFG_OK) {
+    rfg_map_destroy(m);
+    return rc;
+  }
+  *out = m;
+  return RFG_OK;
+}
+
+int rfg_map_destroy(rfg_map* m) {
+  if (!m) return RFG_OK;
+  DevMap& d = m->d;
+  void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
+                  d.visibility, d.reqKey, d.marked,     d.state,          d.tileCounts, d.tilePrefix,
+                  m->icpPartials, m->icpOut, m->icpPose};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (m->hostState) cudaFreeHost(m->hostState);
+  delete m;
+  return RFG_OK;
+}
+
+// VoxelBlockMap::clear (voxel_block_map.cpp:15-24)
+int rfg_map_clear(rfg_map* m) {
+  RFG_REQUIRE(m, "null map");
+  DevMap& d = m->d;
+  cudaStream_t s = m->stream;
+  const size_t padded = (size_t)d.nTiles * kTile;
+  const int4 e0 = make_entry(0, 0, 0, 0, -2);
+  k_fill_u4<<<1024, 256, 0, s>>>(reinterpret_cast<uint4*>(d.entries), make_uint4(e0.x, e0.y, e0.z, e0.w), padded);
+  k_fill_u32<<<4096, 256, 0, s>>>(d.vbaDepth, kDefaultDepthVoxel, (size_t)d.capacity * kBlock3);
+  if (d.vbaColour) RFG_CK(cudaMemsetAsync(d.vbaColour, 0, (size_t)d.capacity * kBlock3 * 4, s));
+  k_iota<<<512, 256, 0, s>>>(d.freeBlocks, (int)d.capacity);
+  if (d.excess) k_iota<<<512, 256, 0, s>>>(d.freeExcess, (int)d.excess);
+  RFG_CK(cudaMemsetAsync(d.visibility, 0, padded, s));
+  RFG_CK(cudaMemsetAsync(d.marked, 0, padded, s));
+  RFG_CK(cudaMemsetAsync(d.reqKey, 0, padded * 4, s));
+  k_state_init<<<1, 32, 0, s>>>(d.state, (int)d.capacity, (int)d.excess);
+  count_launch(5);
+  RFG_CK(cudaGetLastError());
+  RFG_CK(cudaStreamSynchronize(s));
+  return RFG_OK;
+}
+
+int rfg_map_set_stream(rfg_map* m, void* stream) {
+  RFG_REQUIRE(m, "null map");
+  m->stream = static_cast<cudaStream_t>(stream);
+  return RFG_OK;
+}
+
+int rfg_map_sync(rfg_map* m) {
+  RFG_REQUIRE(m, "null map");
+  RFG_CK(cudaStreamSynchronize(m->stream));
+  return check_device_error(m);
+}
+
+int rfg_map_set_shard(rfg_map* m, int rank, int world, int tileShift) {
+  RFG_REQUIRE(m && world >= 1 && rank >= 0 && rank < world && tileShift >= 0 && tileShift < 16, "bad shard");
+  m->d.rank = rank;
+  m->d.world = world;
+  m->d.tileShift = tileShift;
+  return RFG_OK;
+}
+
+int rfg_allocate_from_depth(rfg_map* m, const float* depth, const rfg_intrinsics* intr, const float pose34[12],
+                            const rfg_scene_params* params, rfg_alloc_stats* stats) {
+  RFG_REQUIRE(m && depth && pose34, "null argument");
+  RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
+  RFG_REQUIRE((size_t)intr->width * intr->height < (1u << 25), "image too large for the 25-bit pixel key");
+  const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  RFG_CK(launch_allocate(m->d, depth, fa, m->stream));
+  if (stats) {
+    const int rc = check_device_error(m);  // synchronises, refreshes hostState
+    if (rc != RFG_OK) return rc;
+    memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
+  }
+  return RFG_OK;
+}
+
+int rfg_integrate(rfg_map* m, const float* depth, const uint8_t* rgb, const rfg_intrinsics* intrD,
+                  const rfg_intrinsics* intrRgb, const float extr34[12], const float pose34[12],
+                  const rfg_scene_params* params) {
+  RFG_REQUIRE(m && depth && pose34, "null argument");
+  RFG_REQUIRE(valid_intr(intrD) && valid_params(params), "invalid intrinsics / scene params");
+  RFG_REQUIRE(!rgb || (m->d.vbaColour && valid_intr(intrRgb)), "colour integration needs a colour map + rgb intrinsics");
+  const FrameArgs fa = make_frame_args(intrD, params, pose34, nullptr);
+  RFG_CK(launch_integrate(m->d, depth, rgb, fa, intrRgb, extr34, m->stream));
+  return RFG_OK;
+}
+
+int rfg_render_expected_ranges(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
+                               const rfg_scene_params* params, float* range) {
+  RFG_REQUIRE(m && pose34 && range, "null argument");
+  RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
+  const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  RFG_CK(launch_ranges(m->d, fa, reinterpret_cast<float2*>(range), m->stream));
+  return RFG_OK;
+}
+
+int rfg_render_icp_maps(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
+                        const rfg_scene_params* params, const float* range, float* raycast, float* points,
+                        float* normals) {
+  RFG_REQUIRE(m && pose34 && points && normals, "null argument");
+  if (!range) {
+    set_error("render_icp_maps needs the expected-range image (render_expected_ranges first)");
+    return RFG_ESTATE;
+  }
+  RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
+  const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  RFG_CK(launch_icp_maps(m->d, fa, reinterpret_cast<const float2*>(range), reinterpret_cast<float4*>(raycast),
+                         reinterpret_cast<float4*>(points), reinterpret_cast<float4*>(normals), m->stream));
+  return RFG_OK;
+}
+
+int rfg_build_view_depth(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
+                         void* stream) {
+  // build_view (view.cpp:102-106) rejects levels < 1
+  RFG_REQUIRE(raw && out && w > 0 && h > 0 && levels >= 1 && levels <= 4, "invalid build_view arguments");
+  RFG_CK(launch_build_view(raw, w, h, scale, offset, levels, out, static_cast<cudaStream_t>(stream)));
+  return RFG_OK;
+}
+
+int rfg_icp_track(rfg_map* m, const float* depthLevels, int levels, const rfg_intrinsics* intr, const float* points,
+                  const float* normals, const float renderPose34[12], const float initPose34[12], const int iters[3],
+                  const float dist[3], int minCount, float poseOut34[12], double stats8[8]) {
+  RFG_REQUIRE(m && depthLevels && points && normals && renderPose34 && initPose34 && iters && dist,
+              "null argument");
+  RFG_REQUIRE(valid_intr(intr) && levels >= 1 && levels <= 3, "invalid intrinsics / levels");
+  float host[24];
+  memcpy(host, initPose34, 48);
+  memcpy(host + 12, renderPose34, 48);
+  RFG_CK(cudaMemcpyAsync(m->icpPose, host, sizeof(host), cudaMemcpyHostToDevice, m->stream));
+  const Intr in0{intr->width, intr->height, intr->fx, intr->fy, intr->cx, intr->cy};
+  RFG_CK(launch_icp_track(m->icpOut, m->icpPartials, depthLevels, levels, in0, reinterpret_cast<const float4*>(points),
+                          reinterpret_cast<const float4*>(normals), iters, dist, minCount, m->icpPose,
+                          m->icpPose + 12, m->icpPose + 24, m->stream));
+  double st[8];
+  float pose[12];
+  RFG_CK(cudaMemcpyAsync(st, icp_stats_ptr(m->icpOut), sizeof(st), cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaMemcpyAsync(pose, m->icpPose + 24, sizeof(pose), cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaStreamSynchronize(m->stream));
+  if (poseOut34) memcpy(poseOut34, pose, sizeof(pose));
+  if (stats8) memcpy(stats8, st, sizeof(st));
+  return RFG_OK;
+}
+
+int rfg_icp_reduce(rfg_map* m, const float* depthLevel, int level, const rfg_intrinsics* intr, const float* points,
+                   const float* normals, const float renderPose34[12], const float camToWorld34[12], float dist,
+                   double out29[29]) {
+  RFG_REQUIRE(m && depthLevel && points && normals && renderPose34 && camToWorld34 && out29, "null argument");
+  RFG_REQUIRE(valid_intr(intr) && level >= 0 && level < 4, "invalid intrinsics / level");
+  float host[24];
+  memcpy(host, camToWorld34, 48);
+  memcpy(host + 12, renderPose34, 48);
+  RFG_CK(cudaMemcpyAsync(m->icpPose, host, sizeof(host), cudaMemcpyHostToDevice, m->stream));
+  const Intr in0{intr->width, intr->height, intr->fx, intr->fy, intr->cx, intr->cy};
+  const float sc = ldexpf(1.f, -level);
+  const float f4l[4] = {intr->fx * sc, intr->fy * sc, intr->cx * sc, intr->cy * sc};
+  RFG_CK(launch_icp_reduce_once(m->icpOut, m->icpPartials, depthLevel, intr->width >> level, intr->height >> level,
+                                f4l, in0, reinterpret_cast<const float4*>(points),
+                                reinterpret_cast<const float4*>(normals), m->icpPose, m->icpPose + 12, dist,
+                                m->stream));
+  RFG_CK(cudaMemcpyAsync(out29, icp_sums_ptr(m->icpOut), 29 * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaStreamSynchronize(m->stream));
+  return RFG_OK;
+}
+
+uint32_t rfg_total_entries(const rfg_map* m) { return m ? m->d.total : 0; }
+
+int rfg_export_entries(rfg_map* m, int32_t* out5) {
+  RFG_REQUIRE(m && out5, "null argument");
+  int* dbuf = nullptr;
+  RFG_CK(cudaMalloc(&dbuf, (size_t)m->d.total * 5 * sizeof(int)));
+  k_export_entries<<<1024, 256, 0, m->stream>>>(m->d.entries, dbuf, (int)m->d.total);
+  count_launch();
+  cudaMemcpyAsync(out5, dbuf, (size_t)m->d.total * 5 * sizeof(int), cudaMemcpyDeviceToHost, m->stream);
+  cudaError_t e = cudaStreamSynchronize(m->stream);
+  cudaFree(dbuf);
+  RFG_CK(e);
+  return check_device_error(m);
+}
+
+int rfg_export_blocks(rfg_map* m, const int32_t* ptrs, int n, uint8_t* out) {
+  RFG_REQUIRE(m && (n == 0 || (ptrs && out)) && n >= 0, "null argument");
+  if (n == 0) return RFG_OK;
+  for (int i = 0; i < n; ++i) RFG_REQUIRE(ptrs[i] >= 0 && (uint32_t)ptrs[i] < m->d.capacity, "block ptr out of range");
+  int* dptrs = nullptr;
+  uint8_t* dout = nullptr;
+  RFG_CK(cudaMalloc(&dptrs, n * sizeof(int)));
+  if (cudaMalloc(&dout, (size_t)n * kBlock3 * 8) != cudaSuccess) {
+    cudaFree(dptrs);
+    set_error("export buffer allocation failed");
+    return RFG_ENOMEM;
+  }
+  cudaMemcpyAsync(dptrs, ptrs, n * sizeof(int), cudaMemcpyHostToDevice, m->stream);
+  k_export_blocks<<<1024, 256, 0, m->stream>>>(m->d.vbaDepth, m->d.vbaColour, dptrs, n, dout);
+  count_launch();
+  cudaMemcpyAsync(out, dout, (size_t)n * kBlock3 * 8, cudaMemcpyDeviceToHost, m->stream);
+  cudaError_t e = cudaStreamSynchronize(m->stream);
+  cudaFree(dptrs);
+  cudaFree(dout);
+  RFG_CK(e);
+  return RFG_OK;
+}
+
+int rfg_export_visible(rfg_map* m, int32_t* list, uint8_t* types, int32_t* count) {
+  RFG_REQUIRE(m && count, "null argument");
+  const int rc = check_device_error(m);
+  if (rc != RFG_OK) return rc;
+  const int n = m->hostState->nVisible;
+  *count = n;
+  if (list && n) RFG_CK(cudaMemcpyAsync(list, m->d.visibleList, n * sizeof(int), cudaMemcpyDeviceToHost, m->stream));
+  if (types) RFG_CK(cudaMemcpyAsync(types, m->d.visibility, m->d.total, cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaStreamSynchronize(m->stream));
+  return RFG_OK;
+}
+
+int rfg_free_counts(rfg_map* m, int32_t* nb, int32_t* ne) {
+  RFG_REQUIRE(m && nb && ne, "null argument");
+  const int rc = check_device_error(m);
+  if (rc != RFG_OK) return rc;
+  *nb = m->hostState->nFreeBlocks;
+  *ne = m->hostState->nFreeExcess;
+  return RFG_OK;
+}
+
+// ------------------------------------------------------------- pipeline
+}  // extern "C"
+
+struct rfg_pipeline {
+  rfg_map* map;
+  rfg_pipeline_config cfg;
+  cudaStream_t stream;
+  uint16_t* rawDev;
+  float* depthLevels;
+  float2* range;
+  float4* raycast;
+  float4* points;
+  float4* normals;
+  float* poses;  // [0..11] current w2c, [12..23] render pose of the last raycast
+  double* hostIcp;
+  float* hostPose;
+  int frames;
+  cudaGraphExec_t exec[2];  // [0] no tracking, [1] tracking
+  uint64_t graphKernels[2];
+};
+
+namespace {
+
+cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
+  rfg_map* m = p->map;
+  const rfg_pipeline_config& c = p->cfg;
+  cudaStream_t s = p->stream;
+  cudaError_t e = launch_build_view(p->rawDev, c.intr.width, c.intr.height, c.aff_scale, c.aff_offset, c.levels,
+                                    p->depthLevels, s);
+  if (e != cudaSuccess) return e;
+  if (track) {
+    const Intr in0{c.intr.width, c.intr.height, c.intr.fx, c.intr.fy, c.intr.cx, c.intr.cy};
+    e = launch_icp_track(m->icpOut, m->icpPartials, p->depthLevels, c.levels, in0, p->points, p->normals, c.iters,
+                         c.dist, c.min_count, p->poses, p->poses + 12, p->poses, s);
+    if (e != cudaSuccess) return e;
+  }
+  const FrameArgs fa = make_frame_args(&c.intr, &c.params, nullptr, p->poses);
+  if ((e = launch_allocate(m->d, p->depthLevels, fa, s)) != cudaSuccess) return e;
+  if ((e = launch_integrate(m->d, p->depthLevels, nullptr, fa, nullptr, nullptr, s)) != cudaSuccess) return e;
+  if ((e = launch_ranges(m->d, fa, p->range, s)) != cudaSuccess) return e;
+  if ((e = launch_icp_maps(m->d, fa, p->range, p->raycast, p->points, p->normals, s)) != cudaSuccess) return e;
+  k_copy12<<<1, 32, 0, s>>>(p->poses + 12, p->poses);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int run_frame(rfg_pipeline* p, const float* pose34) {
+  const bool track = p->cfg.track && p->frames > 0;
+  if (pose34) {
+    Pose12 pv;
+    memcpy(pv.v, pose34, 48);
+    k_set12<<<1, 32, 0, p->stream>>>(p->poses, pv);
+    count_launch();
+  }
+  if (!p->cfg.use_graph) {
+    RFG_CK(enqueue_frame(p, track));
+  } else {
+    const int gi = track ? 1 : 0;
+    if (!p->exec[gi]) {
+      cudaGraph_t g;
+      const uint64_t before = g_launches.load();
+      RFG_CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+      cudaError_t e = enqueue_frame(p, track);
+      cudaError_t e2 = cudaStreamEndCapture(p->stream, &g);
+      RFG_CK(e);
+      RFG_CK(e2);
+      p->graphKernels[gi] = g_launches.load() - before;
+      g_launches.fetch_sub(p->graphKernels[gi]);  // capture does not launch
+      RFG_CK(cudaGraphInstantiate(&p->exec[gi], g, 0));
+      cudaGraphDestroy(g);
+    }
+    RFG_CK(cudaGraphLaunch(p->exec[gi], p->stream));
+    count_launch(p->graphKernels[gi]);
+  }
+  ++p->frames;
+  return RFG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline** out) {
+  RFG_REQUIRE(m && cfg && out, "null argument");
+  RFG_REQUIRE(valid_intr(&cfg->intr) && valid_params(&cfg->params), "invalid intrinsics / scene params");
+  RFG_REQUIRE(cfg->levels >= 1 && cfg->levels <= 3, "levels must be 1..3");
+  RFG_REQUIRE(!cfg->track || cfg->levels >= 1, "tracking needs a pyramid");
+  *out = nullptr;
+  rfg_pipeline* p = new rfg_pipeline();
+  memset(p, 0, sizeof(*p));
+  p->map = m;
+  p->cfg = *cfg;
+  const size_t n = (size_t)cfg->intr.width * cfg->intr.height;
+  size_t lv = 0;
+  for (int l = 0; l < cfg->levels; ++l) lv += (size_t)(cfg->intr.width >> l) * (cfg->intr.height >> l);
+  bool ok = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMalloc(&p->rawDev, n * 2 + 16) == cudaSuccess &&
+            cudaMalloc(&p->depthLevels, lv * 4 + 16) == cudaSuccess &&
+            cudaMalloc(&p->range, n * sizeof(float2)) == cudaSuccess &&
+            cudaMalloc(&p->raycast, n * sizeof(float4)) == cudaSuccess &&
+            cudaMalloc(&p->points, n * sizeof(float4)) == cudaSuccess &&
+            cudaMalloc(&p->normals, n * sizeof(float4)) == cudaSuccess &&
+            cudaMalloc(&p->poses, 32 * sizeof(float)) == cudaSuccess &&
+            cudaMallocHost(&p->hostIcp, 8 * sizeof(double)) == cudaSuccess &&
+            cudaMallocHost(&p->hostPose, 12 * sizeof(float)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    rfg_pipeline_destroy(p);
+    set_error("pipeline allocation failed");
+    return RFG_ENOMEM;
+  }
+  m->stream = p->stream;
+  const int rc = rfg_pipeline_reset(p);
+  if (rc != RFG_OK) {
+    rfg_pipeline_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return RFG_OK;
+}
+
+int rfg_pipeline_destroy(rfg_pipeline* p) {
+  if (!p) return RFG_OK;
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  for (int i = 0; i < 2; ++i)
+    if (p->exec[i]) cudaGraphExecDestroy(p->exec[i]);
+  void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->points, p->normals, p->poses};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (p->hostIcp) cudaFreeHost(p->hostIcp);
+  if (p->hostPose) cudaFreeHost(p->hostPose);
+  if (p->map && p->map->stream == p->stream) p->map->stream = nullptr;
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+  return RFG_OK;
+}
+
+int rfg_pipeline_reset(rfg_pipeline* p) {
+  RFG_REQUIRE(p, "null pipeline");
+  Pose12 id{};
+  id.v[0] = id.v[5] = id.v[10] = 1.f;
+  k_set12<<<1, 32, 0, p->stream>>>(p->poses, id);
+  k_set12<<<1, 32, 0, p->stream>>>(p->poses + 12, id);
+  count_launch(2);
+  RFG_CK(cudaGetLastError());
+  RFG_CK(cudaStreamSynchronize(p->stream));
+  p->frames = 0;
+  return RFG_OK;
+}
+
+int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw, const float* pose34) {
+  RFG_REQUIRE(p && raw, "null argument");
+  const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
+  if (raw != p->rawDev) RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
+  return run_frame(p, pose34);
+}
+
+int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const float* pose34) {
+  RFG_REQUIRE(p && rawHost, "null argument");
+  const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
+  RFG_CK(cudaMemcpyAsync(p->rawDev, rawHost, n * 2, cudaMemcpyHostToDevice, p->stream));
+  return run_frame(p, pose34);
+}
+
+int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34[12], double icpStats8[8]) {
+  RFG_REQUIRE(p, "null pipeline");
+  rfg_map* m = p->map;
+  RFG_CK(cudaMemcpyAsync(m->hostState, m->d.state, sizeof(MapState), cudaMemcpyDeviceToHost, p->stream));
+  if (poseOut34) RFG_CK(cudaMemcpyAsync(p->hostPose, p->poses, 48, cudaMemcpyDeviceToHost, p->stream));
+  if (icpStats8)
+    RFG_CK(cudaMemcpyAsync(p->hostIcp, icp_stats_ptr(m->icpOut), 64, cudaMemcpyDeviceToHost, p->stream));
+  RFG_CK(cudaStreamSynchronize(p->stream));
+  if (m->hostState->error) return check_device_error(m);
+  if (stats) memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
+  if (poseOut34) memcpy(poseOut34, p->hostPose, 48);
+  if (icpStats8) memcpy(icpStats8, p->hostIcp, 64);
+  return RFG_OK;
+}
+
+int rfg_pipeline_buffers(rfg_pipeline* p, float** depthLevels, float** range, float** raycast, float** points,
+                         float** normals) {
+  RFG_REQUIRE(p, "null pipeline");
+  if (depthLevels) *depthLevels = p->depthLevels;
+  if (range) *range = reinterpret_cast<float*>(p->range);
+  if (raycast) *raycast = reinterpret_cast<float*>(p->raycast);
+  if (points) *points = reinterpret_cast<float*>(p->points);
+  if (normals) *normals = reinterpret_cast<float*>(p->normals);
+  return RFG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// rfg_internal.h — device map layout, per-frame kernel arguments, error
+// plumbing.  Shared by the .cu translation units of librfg.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../include/rfg.h"
+
+namespace rfg {
+
+// Device-resident mutable scalars of a map.
+struct MapState {
+  int nFreeBlocks;   // free VBA stack size (freeBlockStack_.size())
+  int nFreeExcess;   // free excess stack size
+  int nVisible;      // visibleList_.size()
+  int error;         // sticky RFG_E* flag set by kernels
+  // per-frame allocation bookkeeping
+  int snapFreeBlocks, snapFreeExcess;  // stack sizes at the start of stage 2
+  int succ, succType2;                 // stage-2 successes (all / excess-linked)
+  int stats[4];                        // requested, allocated, allocFailures, visibleCount
+  int nRequests;                       // stage-2 request count
+  int pad[5];
+};
+
+// Plain-old-data view of a map passed by value to kernels.
+struct DevMap {
+  uint32_t buckets, excess, capacity, total;
+  int4* entries;           // total x 16 B
+  uint32_t* vbaDepth;      // capacity x 512 depth voxels (4 B)
+  uint32_t* vbaColour;     // capacity x 512 colour voxels (4 B) or nullptr
+  int* freeBlocks;         // capacity
+  int* freeExcess;         // excess
+  int* visibleList;        // total
+  uint8_t* visibility;     // total
+  uint32_t* reqKey;        // total: stage-1 last-writer key (0 = no request)
+  uint8_t* marked;         // total: stage-1/2 marks (0/1/2)
+  MapState* state;
+  int2* tileCounts;        // per 4096-entry tile
+  int2* tilePrefix;        // exclusive prefix (+ total at [nTiles])
+  int nTiles;
+  int rank, world, tileShift;  // shard filter
+};
+
+// Per-call frame arguments (camera, scene params, pose).
+struct FrameArgs {
+  int w, h;
+  float fx, fy, cx, cy;
+  float voxelSize, mu;
+  int maxW;
+  float vfMin, vfMax;
+  int stopAtMaxW;
+  float pose[12];          // world -> camera (used when poseDev == nullptr)
+  const float* poseDev;    // device-resident pose (tracking pipeline)
+};
+
+struct Pose12 {
+  float v[12];
+};
+
+constexpr int kTile = 4096;          // hash entries per scan tile
+constexpr int kTileThreads = 256;    // 16 entries per thread
+
+void set_error(const std::string& msg);
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p, const float* pose34,
+                          const float* poseDev);
+
+// kernel launchers (return cudaError_t of the launch)
+cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s);
+cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint8_t* rgb, const FrameArgs& fa,
+                             const rfg_intrinsics* intrRgb, const float* extr34, cudaStream_t s);
+cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s);
+cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* range, float4* raycast,
+                            float4* points, float4* normals, cudaStream_t s);
+cudaError_t launch_build_view(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
+                              cudaStream_t s);
+
+}  // namespace rfg
+
+struct rfg_map {
+  rfg::DevMap d;
+  rfg_map_config cfg;
+  int device;
+  cudaStream_t stream;
+  rfg::MapState* hostState;  // pinned mirror for readback
+  // ICP scratch
+  double* icpPartials;
+  int icpPartialSlots;
+  double* icpOut;            // device: 29 sums + solver state
+  float* icpPose;            // device: current cam->world (12) + world->cam (12) + render pose (12)
+};
+
+#define RFG_CK(call)                                                                      \
+  do {                                                                                    \
+    cudaError_t err_ = (call);                                                            \
+    if (err_ != cudaSuccess) {                                                            \
+      rfg::set_error(std::string(#call) + ": " + cudaGetErrorString(err_));               \
+      return RFG_ECUDA;                                                                   \
+    }                                                                                     \
+  } while (0)

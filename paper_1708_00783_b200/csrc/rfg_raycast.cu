@@ -1,0 +1,267 @@
+// rfg_raycast.cu — expected-range pass and ICP-map raycast
+// (render_expected_ranges proj/src/raycast.cpp:86-127;
+//  render_maps(kIcpMaps) proj/include/rf/raycast.hpp:157-207 with
+//  cast_ray_field :54-112 and field_normal :137-153).
+#include "rfg_common.cuh"
+
+namespace rfg {
+
+__device__ __forceinline__ Pose load_pose_r(const FrameArgs& fa) {
+  return pose_from12(fa.poseDev ? fa.poseDev : fa.pose);
+}
+
+// ------------------------------------------------------ expected ranges
+__global__ void k_range_clear(float2* range, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) range[i] = make_float2(FLT_MAX, -1.f);
+}
+
+// One warp per visible block: lanes 0-7 project the 8 corners (projectBlock,
+// raycast.cpp:38-71), the warp reduces the pixel rectangle and z span, then
+// min/max-merges the rectangle into the range image.  The reference splits
+// the rectangle into 16x16 fragments (:99-115) only to parallelise this merge;
+// min/max is exact and commutative, so the result is identical.  Positive
+// floats order like their int bit patterns, so the merges are integer
+// atomicMin/atomicMax on the bits (z values are > 0; unset max is -1).
+__global__ void __launch_bounds__(256) k_range_blocks(DevMap m, FrameArgs fa, float2* range) {
+  const int lane = threadIdx.x & 31;
+  const int warpsPerCta = blockDim.x >> 5;
+  const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
+  const int nw = gridDim.x * warpsPerCta;
+  const int nVis = *((volatile int*)&m.state->nVisible);
+  const Pose pose = load_pose_r(fa);
+  const float bs = fa.voxelSize * (float)kBlock;
+  for (int b = gw; b < nVis; b += nw) {
+    const int idx = m.visibleList[b];
+    const int4 e = ld_entry(m.entries, idx);
+    if (!entry_allocated(e)) continue;
+    float x0 = FLT_MAX, y0 = FLT_MAX, x1 = -FLT_MAX, y1 = -FLT_MAX, zMin = FLT_MAX, zMax = 0.f;
+    int valid = 0;
+    if (lane < 8) {
+      const int c = lane;
+      const f3 corner{((float)entry_x(e) + (float)(c & 1)) * bs, ((float)entry_y(e) + (float)((c >> 1) & 1)) * bs,
+                      ((float)entry_z(e) + (float)((c >> 2) & 1)) * bs};
+      const f3 pc = pose_apply(pose, corner);
+      if (!(pc.z < 1e-6f)) {
+        const float px = fa.fx * pc.x / pc.z + fa.cx;
+        const float py = fa.fy * pc.y / pc.z + fa.cy;
+        x0 = px;
+        y0 = py;
+        x1 = px;
+        y1 = py;
+        zMin = pc.z;
+        zMax = pc.z;
+        valid = 1;
+      }
+    }
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+      x0 = smin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+      y0 = smin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+      x1 = smax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+      y1 = smax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+      zMin = smin(zMin, __shfl_xor_sync(0xffffffffu, zMin, o));
+      zMax = smax(zMax, __shfl_xor_sync(0xffffffffu, zMax, o));
+      valid += __shfl_xor_sync(0xffffffffu, valid, o);
+    }
+    // lane 0's values now hold the reduction over lanes 0-7
+    x0 = __shfl_sync(0xffffffffu, x0, 0);
+    y0 = __shfl_sync(0xffffffffu, y0, 0);
+    x1 = __shfl_sync(0xffffffffu, x1, 0);
+    y1 = __shfl_sync(0xffffffffu, y1, 0);
+    zMin = __shfl_sync(0xffffffffu, zMin, 0);
+    zMax = __shfl_sync(0xffffffffu, zMax, 0);
+    valid = __shfl_sync(0xffffffffu, valid, 0);
+    if (valid == 0) continue;
+    const int bx0 = max(0, (int)floorf(x0)), by0 = max(0, (int)floorf(y0));
+    const int bx1 = min(fa.w - 1, (int)ceilf(x1)), by1 = min(fa.h - 1, (int)ceilf(y1));
+    if (bx0 > bx1 || by0 > by1) continue;
+    const float zlo = smax(zMin, fa.vfMin), zhi = smin(zMax, fa.vfMax);
+    if (zlo > zhi) continue;
+    const int lo = __float_as_int(zlo), hi = __float_as_int(zhi);
+    const int rw = bx1 - bx0 + 1;
+    const int npx = rw * (by1 - by0 + 1);
+    for (int p = lane; p < npx; p += 32) {
+      const int x = bx0 + p % rw, y = by0 + p / rw;
+      int* r = reinterpret_cast<int*>(range + (size_t)y * fa.w + x);
+      const int2 cur = __ldcg(reinterpret_cast<const int2*>(r));  // L2 value; stale reads only cost an extra atomic
+      if (lo < cur.x) atomicMin(r, lo);
+      if (hi > cur.y) atomicMax(r + 1, hi);
+    }
+  }
+}
+
+// ------------------------------------------------------------ raycast
+struct FieldReader {
+  const DevMap& m;
+  BlockCache cache;
+
+  // MapField::resident (raycast.hpp:38-42)
+  __device__ __forceinline__ bool resident(f3 p) {
+    const i3 b{((int)floorf(p.x)) >> 3, ((int)floorf(p.y)) >> 3, ((int)floorf(p.z)) >> 3};
+    return block_ptr(m, b, cache) >= 0;
+  }
+  __device__ __forceinline__ bool voxel(i3 v, uint32_t* out) {
+    const i3 b{v.x >> 3, v.y >> 3, v.z >> 3};
+    const int ptr = block_ptr(m, b, cache);
+    if (ptr < 0) return false;
+    const int lin = (v.x - b.x * kBlock) + (v.y - b.y * kBlock) * kBlock + (v.z - b.z * kBlock) * kBlock * kBlock;
+    *out = __ldg(m.vbaDepth + (size_t)ptr * kBlock3 + lin);
+    return true;
+  }
+  // readSdfNearest (voxel_block_map.cpp:178-185)
+  __device__ __forceinline__ float nearest(f3 p, bool& ok) {
+    uint32_t w;
+    ok = voxel(i3{(int)lroundf(p.x), (int)lroundf(p.y), (int)lroundf(p.z)}, &w);
+    return ok ? sdf_to_logical(vox_sdf(w)) : 1.f;
+  }
+  // readSdfWeightTrilinear (voxel_block_map.cpp:130-156)
+  __device__ __forceinline__ float trilinear(f3 p, bool& ok) {
+    const int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
+    const float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
+    float sdf = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t w;
+      if (!voxel(i3{bx + (k & 1), by + ((k >> 1) & 1), bz + ((k >> 2) & 1)}, &w)) {
+        ok = false;
+        return 1.f;
+      }
+      const float bw = ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+      sdf += bw * sdf_to_logical(vox_sdf(w));
+    }
+    ok = true;
+    return sdf;
+  }
+};
+
+__device__ __forceinline__ f3 at_t(f3 o, f3 d, float t) { return f3{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z}; }
+
+// cast_ray_field (raycast.hpp:54-112)
+__device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM, float tMaxM, float mu, float vs,
+                         f3* hit) {
+  const float coarseStep = (float)kBlock * vs;
+  const float fineStep = mu;
+  const float stepScale = mu;
+  const f3 oV{originM.x / vs, originM.y / vs, originM.z / vs};
+  const f3 dV{dirUnit.x / vs, dirUnit.y / vs, dirUnit.z / vs};
+  float t = tMinM;
+  enum { COARSE, FINE, SURFACE };
+  int state = field.resident(at_t(oV, dV, t)) ? FINE : COARSE;
+  while (t <= tMaxM) {
+    const f3 p = at_t(oV, dV, t);
+    if (state == COARSE) {
+      if (field.resident(p)) {
+        state = FINE;
+        t = smax(tMinM, t - coarseStep);
+      } else {
+        t += coarseStep;
+      }
+      continue;
+    }
+    bool ok = false;
+    float sdf = field.nearest(p, ok);
+    if (!ok) {
+      if (state == SURFACE) state = FINE;
+      t += fineStep;
+      continue;
+    }
+    if (sdf <= 0.1f) {
+      bool okTri = false;
+      const float tri = field.trilinear(p, okTri);
+      if (okTri) sdf = tri;
+    }
+    if (state == FINE) {
+      if (sdf < 0.f) return false;  // WRONG_SIDE
+      state = SURFACE;
+    }
+    if (sdf <= 0.f) {
+      float tHit = t + sdf * stepScale;
+      bool okR = false;
+      const float f1 = field.trilinear(at_t(oV, dV, tHit), okR);
+      if (okR) tHit += f1 * stepScale;
+      *hit = at_t(oV, dV, tHit);
+      return true;
+    }
+    t += smax(sdf * stepScale, vs);
+  }
+  return false;
+}
+
+// field_normal (raycast.hpp:137-153)
+__device__ __forceinline__ bool field_normal(FieldReader& field, f3 h, f3* n) {
+  bool ok[6];
+  f3 g;
+  g.x = field.trilinear(f3{h.x + 1.f, h.y + 0.f, h.z + 0.f}, ok[0]) -
+        field.trilinear(f3{h.x - 1.f, h.y - 0.f, h.z - 0.f}, ok[1]);
+  g.y = field.trilinear(f3{h.x + 0.f, h.y + 1.f, h.z + 0.f}, ok[2]) -
+        field.trilinear(f3{h.x - 0.f, h.y - 1.f, h.z - 0.f}, ok[3]);
+  g.z = field.trilinear(f3{h.x + 0.f, h.y + 0.f, h.z + 1.f}, ok[4]) -
+        field.trilinear(f3{h.x - 0.f, h.y - 0.f, h.z - 1.f}, ok[5]);
+  if (!(ok[0] && ok[1] && ok[2] && ok[3] && ok[4] && ok[5])) return false;
+  const float len = sqrtf(sqnorm3(g));
+  if (len < 1e-12f) return false;
+  *n = f3{g.x / len, g.y / len, g.z / len};
+  return true;
+}
+
+// One thread per pixel in 16x8 tiles (neighbouring rays share blocks).
+__global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, const float2* __restrict__ range,
+                                                     float4* raycast, float4* points, float4* normals) {
+  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (x >= fa.w || y >= fa.h) return;
+  const size_t i = (size_t)y * fa.w + x;
+  const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
+  float4 rc = invalid, pt = invalid, nm = invalid;
+  const float2 r = range[i];
+  if (r.y >= r.x) {
+    const Pose c2w = pose_inverse(load_pose_r(fa));
+    const f3 origin{c2w.t[0], c2w.t[1], c2w.t[2]};
+    const f3 dirCam{((float)x - fa.cx) / fa.fx, ((float)y - fa.cy) / fa.fy, 1.f};
+    const float norm = sqrtf(sqnorm3(dirCam));
+    const f3 dw = rot_apply(c2w.R, dirCam);
+    const f3 dirW{dw.x / norm, dw.y / norm, dw.z / norm};
+    FieldReader field{m};
+    field.cache.reset();
+    f3 hit;
+    if (cast_ray(field, origin, dirW, r.x * norm, r.y * norm, fa.mu, fa.voxelSize, &hit)) {
+      rc = make_float4(hit.x, hit.y, hit.z, 1.f);
+      pt = make_float4(hit.x * fa.voxelSize, hit.y * fa.voxelSize, hit.z * fa.voxelSize, 1.f);
+      f3 n;
+      if (field_normal(field, hit, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
+    }
+  }
+  if (raycast) raycast[i] = rc;
+  points[i] = pt;
+  normals[i] = nm;
+}
+
+int range_grid() {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = sms * 8;
+  }
+  return grid;
+}
+
+cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s) {
+  const int n = fa.w * fa.h;
+  k_range_clear<<<(n + 255) / 256, 256, 0, s>>>(range, n);
+  k_range_blocks<<<range_grid(), 256, 0, s>>>(m, fa, range);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* range, float4* raycast,
+                            float4* points, float4* normals, cudaStream_t s) {
+  dim3 g((fa.w + 15) / 16, (fa.h + 7) / 8);
+  k_raycast_icp<<<g, 128, 0, s>>>(m, fa, range, raycast, points, normals);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace rfg

@@ -1,0 +1,545 @@
+"""Host API mirroring the reference's engine interface (rf:: namespace of
+/root/reference/proj) on top of the librfg.so C ABI.
+
+Names, argument meaning and error behaviour follow the reference so parity
+tests read like its own tests:
+
+  VoxelBlockMapConfig / VoxelBlockMap      proj/include/rf/voxel_block_map.hpp:36-144
+  SceneParams / AllocationStats            proj/include/rf/fusion.hpp:11-27
+  FusionEngine.allocate_from_depth /
+               integrate_frame             proj/include/rf/fusion.hpp:52-79
+  RenderState / render_expected_ranges /
+  render_maps(RenderMode.kIcpMaps)         proj/include/rf/raycast.hpp:15-129
+  build_view (depth + pyramid)             proj/include/rf/view.hpp:38-39
+  track_depth (ICP)                        SPEC.md:348-356 (absent in the reference)
+
+Images live on the GPU as torch tensors (torch is the device-memory and
+stream plumbing); every computation runs in librfg's sm_100a kernels.
+Poses are (3, 4) float32 arrays [R | t], world -> camera.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+_f = C.POINTER(C.c_float)
+_d = C.POINTER(C.c_double)
+_i = C.POINTER(C.c_int32)
+_u8 = C.POINTER(C.c_uint8)
+_u16 = C.POINTER(C.c_uint16)
+
+
+def _fp(a: np.ndarray):
+    return a.ctypes.data_as(_f)
+
+
+def _pose(p) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(p, dtype=np.float32).reshape(3, 4))
+    return a
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device tensor expected (librfg has no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError("contiguous tensor expected")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream_handle():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+# ---------------------------------------------------------------- config
+@dataclass
+class Intrinsics:
+    """proj/include/rf/camera.hpp:13-47"""
+    width: int = 0
+    height: int = 0
+    fx: float = 0.0
+    fy: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+
+    def atLevel(self, level: int) -> "Intrinsics":
+        s = float(np.ldexp(np.float32(1.0), -level))
+        return Intrinsics(self.width >> level, self.height >> level, float(np.float32(self.fx) * np.float32(s)),
+                          float(np.float32(self.fy) * np.float32(s)), float(np.float32(self.cx) * np.float32(s)),
+                          float(np.float32(self.cy) * np.float32(s)))
+
+    def c(self) -> _lib.Intrinsics_:
+        return _lib.Intrinsics_(self.width, self.height, self.fx, self.fy, self.cx, self.cy)
+
+    def as_dict(self):
+        return dict(width=self.width, height=self.height, fx=self.fx, fy=self.fy, cx=self.cx, cy=self.cy)
+
+
+@dataclass
+class DepthAffine:
+    """proj/include/rf/camera.hpp:50-62 (m = raw*scale + offset)"""
+    scale: float = 1.0 / 1000.0
+    offset: float = 0.0
+
+
+@dataclass
+class RgbdCalib:
+    """proj/include/rf/camera.hpp:64-69"""
+    intrinsics_rgb: Intrinsics = field(default_factory=Intrinsics)
+    intrinsics_d: Intrinsics = field(default_factory=Intrinsics)
+    extrinsics_d_to_rgb: np.ndarray = field(default_factory=lambda: np.eye(3, 4, dtype=np.float32))
+    depth_affine: DepthAffine = field(default_factory=DepthAffine)
+
+
+@dataclass
+class SceneParams:
+    """proj/include/rf/fusion.hpp:11-20"""
+    voxelSize: float = 0.005
+    mu: float = 0.02
+    maxW: int = 100
+    viewFrustum_min: float = 0.2
+    viewFrustum_max: float = 6.0
+    stopIntegratingAtMaxW: bool = False
+
+    def blockSizeMetres(self) -> float:
+        return float(np.float32(self.voxelSize) * np.float32(8))
+
+    def c(self) -> _lib.SceneParams_:
+        return _lib.SceneParams_(self.voxelSize, self.mu, self.maxW, self.viewFrustum_min, self.viewFrustum_max,
+                                 1 if self.stopIntegratingAtMaxW else 0)
+
+    def as_dict(self):
+        return dict(voxelSize=self.voxelSize, mu=self.mu, maxW=self.maxW, viewFrustum_min=self.viewFrustum_min,
+                    viewFrustum_max=self.viewFrustum_max, stopIntegratingAtMaxW=self.stopIntegratingAtMaxW)
+
+
+@dataclass
+class VoxelBlockMapConfig:
+    """proj/include/rf/voxel_block_map.hpp:36-45"""
+    bucketCount: int = 1 << 20
+    excessCount: int = 1 << 17
+    blockCapacity: int = 1 << 18
+
+    @staticmethod
+    def small() -> "VoxelBlockMapConfig":
+        return VoxelBlockMapConfig(1 << 14, 1 << 11, 1 << 13)
+
+
+@dataclass
+class AllocationStats:
+    """proj/include/rf/fusion.hpp:22-27"""
+    requested: int = 0
+    allocated: int = 0
+    allocFailures: int = 0
+    visibleCount: int = 0
+
+    def as_array(self):
+        return np.array([self.requested, self.allocated, self.allocFailures, self.visibleCount], np.int32)
+
+
+class Visibility(enum.IntEnum):
+    """proj/include/rf/voxel_block_map.hpp:29-34"""
+    kInvisible = 0
+    kVisible = 1
+    kVisibleSwapped = 2
+    kBoundary = 3
+
+
+class RenderMode(enum.IntEnum):
+    """proj/include/rf/raycast.hpp:28"""
+    kIcpMaps = 0
+    kColour = 1
+    kGrey = 2
+
+
+# ------------------------------------------------------------------ map
+class VoxelBlockMap:
+    """Device-resident hashed TSDF (ordered buckets + excess list over a voxel
+    block array).  Raises ValueError for a non-power-of-two bucketCount, like
+    the reference constructor (proj/src/voxel_block_map.cpp:9-13)."""
+
+    def __init__(self, config: VoxelBlockMapConfig | None = None, device: int = 0, colour: bool = False):
+        self._h = None
+        cfg = config or VoxelBlockMapConfig.small()
+        self._config = cfg
+        self.device = device
+        self.colour = colour
+        c = _lib.MapConfig(cfg.bucketCount, cfg.excessCount, cfg.blockCapacity, 1 if colour else 0)
+        h = C.c_void_p()
+        rc = lib().rfg_map_create(C.byref(c), device, C.byref(h))
+        if rc == _lib.RFG_EINVAL:
+            raise ValueError(lib().rfg_last_error().decode())
+        check(rc)
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            lib().rfg_map_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def config(self) -> VoxelBlockMapConfig:
+        return self._config
+
+    def bucketCount(self) -> int:
+        return self._config.bucketCount
+
+    def totalEntries(self) -> int:
+        return self._config.bucketCount + self._config.excessCount
+
+    def hashMask(self) -> int:
+        return self._config.bucketCount - 1
+
+    def bind_stream(self):
+        check(lib().rfg_map_set_stream(self._h, _stream_handle()))
+
+    def clear(self):
+        self.bind_stream()
+        check(lib().rfg_map_clear(self._h))
+
+    def set_shard(self, rank: int, world: int, tile_shift: int = 3):
+        check(lib().rfg_map_set_shard(self._h, rank, world, tile_shift))
+
+    def sync(self):
+        check(lib().rfg_map_sync(self._h))
+
+    # -- parity exports (host copies) --
+    def entries(self) -> np.ndarray:
+        """(totalEntries, 5) int32 {x, y, z, offset, ptr}"""
+        out = np.zeros((self.totalEntries(), 5), np.int32)
+        check(lib().rfg_export_entries(self._h, out.ctypes.data_as(_i)))
+        return out
+
+    def blocks(self, ptrs) -> np.ndarray:
+        """(n, 512, 8) uint8 VoxelSRgb bytes of the given VBA blocks"""
+        ptrs = np.ascontiguousarray(ptrs, np.int32)
+        out = np.zeros((len(ptrs), 512, 8), np.uint8)
+        check(lib().rfg_export_blocks(self._h, ptrs.ctypes.data_as(_i), len(ptrs), out.ctypes.data_as(_u8)))
+        return out
+
+    def visible(self):
+        n = C.c_int32(0)
+        lst = np.zeros(self.totalEntries(), np.int32)
+        types = np.zeros(self.totalEntries(), np.uint8)
+        check(lib().rfg_export_visible(self._h, lst.ctypes.data_as(_i), types.ctypes.data_as(_u8), C.byref(n)))
+        return lst[:n.value].copy(), types
+
+    def visibleList(self) -> np.ndarray:
+        return self.visible()[0]
+
+    def visibilityTypes(self) -> np.ndarray:
+        return self.visible()[1]
+
+    def free_counts(self):
+        nb, ne = C.c_int32(0), C.c_int32(0)
+        check(lib().rfg_free_counts(self._h, C.byref(nb), C.byref(ne)))
+        return nb.value, ne.value
+
+    def freeBlockCount(self) -> int:
+        return self.free_counts()[0]
+
+    def freeExcessCount(self) -> int:
+        return self.free_counts()[1]
+
+    def allocatedBlockCount(self) -> int:
+        return self._config.blockCapacity - self.freeBlockCount()
+
+
+# ------------------------------------------------------------------ view
+@dataclass
+class ViewLevel:
+    depth: torch.Tensor
+    intr: Intrinsics
+
+
+@dataclass
+class View:
+    """proj/include/rf/view.hpp:24-34 (device images)."""
+    calib: RgbdCalib
+    depth_m: torch.Tensor
+    rgb: torch.Tensor | None = None
+    pyramid: list = field(default_factory=list)
+
+    def hasColour(self) -> bool:
+        return self.rgb is not None
+
+
+def build_view(raw_depth, rgb, calib: RgbdCalib, levels: int = 3) -> View:
+    """build_view depth path (proj/src/view.cpp:100-143) on the GPU.
+    raw_depth: (H, W) uint16 (numpy or CUDA tensor).  Raises ValueError on a
+    size mismatch or levels < 1, like the reference (view.cpp:102-106)."""
+    intr = calib.intrinsics_d
+    raw = torch.as_tensor(raw_depth)
+    if raw.dtype != torch.uint16 and raw.dtype != torch.int16:
+        raw = torch.as_tensor(np.ascontiguousarray(np.asarray(raw_depth, dtype=np.uint16)).view(np.int16))
+    if tuple(raw.shape) != (intr.height, intr.width):
+        raise ValueError("build_view: depth image size does not match calibration")
+    if levels < 1:
+        raise ValueError("build_view: levels must be >= 1")
+    if rgb is not None and tuple(rgb.shape[:2]) != (calib.intrinsics_rgb.height, calib.intrinsics_rgb.width):
+        raise ValueError("build_view: rgb image size does not match calibration")
+    raw = raw.cuda().contiguous()
+    sizes = [(intr.width >> l) * (intr.height >> l) for l in range(levels)]
+    buf = torch.empty(sum(sizes), dtype=torch.float32, device=raw.device)
+    check(lib().rfg_build_view_depth(_ptr(raw), intr.width, intr.height, calib.depth_affine.scale,
+                                     calib.depth_affine.offset, levels, _ptr(buf), _stream_handle()))
+    pyr, o = [], 0
+    for l, s in enumerate(sizes):
+        il = intr.atLevel(l)
+        pyr.append(ViewLevel(buf[o:o + s].view(il.height, il.width), il))
+        o += s
+    rgb_t = None
+    if rgb is not None:
+        rgb_t = torch.as_tensor(np.ascontiguousarray(rgb, dtype=np.uint8)).cuda() if not torch.is_tensor(rgb) \
+            else rgb.cuda().contiguous()
+    return View(calib=calib, depth_m=pyr[0].depth, rgb=rgb_t, pyramid=pyr)
+
+
+def view_from_depth(depth_m, intr: Intrinsics, rgb=None, calib: RgbdCalib | None = None) -> View:
+    """A View around an existing metres depth image (float32, device or host)."""
+    d = torch.as_tensor(np.ascontiguousarray(depth_m, np.float32)) if not torch.is_tensor(depth_m) else depth_m
+    d = d.cuda().contiguous()
+    cal = calib or RgbdCalib(intrinsics_rgb=intr, intrinsics_d=intr)
+    rgb_t = None
+    if rgb is not None:
+        rgb_t = torch.as_tensor(np.ascontiguousarray(rgb, np.uint8)).cuda() if not torch.is_tensor(rgb) \
+            else rgb.cuda().contiguous()
+    return View(calib=cal, depth_m=d, rgb=rgb_t, pyramid=[ViewLevel(d, intr)])
+
+
+# --------------------------------------------------------------- fusion
+class FusionEngine:
+    """proj/include/rf/fusion.hpp:52-79 — per-frame allocation + integration."""
+
+    def allocate_from_depth(self, map: VoxelBlockMap, view: View, pose, params: SceneParams,
+                            sync: bool = True) -> AllocationStats | None:
+        p = _pose(pose)
+        map.bind_stream()
+        st = _lib.AllocStats_()
+        intr = view.calib.intrinsics_d.c()
+        check(lib().rfg_allocate_from_depth(map.handle, _ptr(view.depth_m), C.byref(intr), _fp(p),
+                                            C.byref(params.c()), C.byref(st) if sync else None))
+        if not sync:
+            return None
+        return AllocationStats(st.requested, st.allocated, st.allocFailures, st.visibleCount)
+
+    def integrate_frame(self, map: VoxelBlockMap, view: View, pose, params: SceneParams):
+        p = _pose(pose)
+        map.bind_stream()
+        intr_d = view.calib.intrinsics_d.c()
+        intr_rgb = view.calib.intrinsics_rgb.c()
+        extr = _pose(view.calib.extrinsics_d_to_rgb)
+        use_colour = view.hasColour() and map.colour
+        check(lib().rfg_integrate(map.handle, _ptr(view.depth_m), _ptr(view.rgb) if use_colour else None,
+                                  C.byref(intr_d), C.byref(intr_rgb), _fp(extr), _fp(p), C.byref(params.c())))
+
+
+# -------------------------------------------------------------- raycast
+class RenderState:
+    """proj/include/rf/raycast.hpp:15-26 (device images)."""
+
+    def __init__(self):
+        self.expectedRange = None
+        self.raycastResult = None
+        self.points = None
+        self.normals = None
+        self.pose = np.eye(3, 4, dtype=np.float32)
+        self.intr = Intrinsics()
+        self.hasRaycast = False
+
+    def resize(self, intr: Intrinsics):
+        if self.points is not None and self.intr.width == intr.width and self.intr.height == intr.height:
+            return
+        h, w = intr.height, intr.width
+        self.expectedRange = torch.empty((h, w, 2), dtype=torch.float32, device="cuda")
+        self.expectedRange[..., 0] = float(np.finfo(np.float32).max)
+        self.expectedRange[..., 1] = -1.0
+        inv = torch.tensor([0.0, 0.0, 0.0, -1.0], device="cuda")
+        self.raycastResult = inv.repeat(h, w, 1).contiguous()
+        self.points = inv.repeat(h, w, 1).contiguous()
+        self.normals = inv.repeat(h, w, 1).contiguous()
+        self.intr = intr
+        self.hasRaycast = False
+
+
+def render_expected_ranges(map: VoxelBlockMap, pose, intr: Intrinsics, params: SceneParams, state: RenderState):
+    """proj/src/raycast.cpp:86-127"""
+    state.resize(intr)
+    p = _pose(pose)
+    map.bind_stream()
+    check(lib().rfg_render_expected_ranges(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()),
+                                           _ptr(state.expectedRange)))
+
+
+def render_maps(map: VoxelBlockMap, pose, intr: Intrinsics, params: SceneParams, mode: RenderMode,
+                state: RenderState):
+    """proj/src/raycast.cpp:129-139 — only RenderMode.kIcpMaps is on the hot
+    path; colour/grey shading is out of scope."""
+    if mode != RenderMode.kIcpMaps:
+        raise NotImplementedError("only RenderMode.kIcpMaps is implemented on the B200 path")
+    if state.expectedRange is None:
+        raise RuntimeError("render_maps needs render_expected_ranges first")
+    state.resize(intr)
+    p = _pose(pose)
+    map.bind_stream()
+    check(lib().rfg_render_icp_maps(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()),
+                                    _ptr(state.expectedRange), _ptr(state.raycastResult), _ptr(state.points),
+                                    _ptr(state.normals)))
+    state.pose = p.copy()
+    state.intr = intr
+    state.hasRaycast = True
+
+
+# ------------------------------------------------------------------ ICP
+@dataclass
+class TrackerIterationSummary:
+    iterations: int
+    count: int
+    residual_sum: float
+    converged: bool
+    per_level: tuple
+    ok: bool
+
+
+def track_depth(map: VoxelBlockMap, view: View, state: RenderState, init_pose, iters=(6, 10, 20),
+                dist=(0.1, 0.1, 0.1), min_count: int = 10):
+    """Point-to-plane ICP of the view's depth pyramid against
+    the last ICP-map render in `state`.  iters/dist are indexed by pyramid
+    level (0 = finest; SPEC.md:391 caps 20/10/6 coarse -> fine)."""
+    if not state.hasRaycast:
+        raise RuntimeError("track_depth needs an ICP-map render (render_maps) first")
+    levels = len(view.pyramid)
+    base = view.pyramid[0].depth
+    # the pyramid levels are views into one contiguous buffer (build_view)
+    p0 = base.data_ptr()
+    expect = p0
+    for lv in view.pyramid:
+        if lv.depth.data_ptr() != expect:
+            raise ValueError("track_depth needs a pyramid produced by build_view")
+        expect += lv.depth.numel() * 4
+    init = _pose(init_pose)
+    rp = _pose(state.pose)
+    it = (C.c_int32 * 3)(*[int(x) for x in iters])
+    ds = (C.c_float * 3)(*[float(x) for x in dist])
+    out = np.zeros((3, 4), np.float32)
+    st = np.zeros(8, np.float64)
+    map.bind_stream()
+    check(lib().rfg_icp_track(map.handle, C.c_void_p(p0), levels, C.byref(view.calib.intrinsics_d.c()),
+                              _ptr(state.points), _ptr(state.normals), _fp(rp), _fp(init), it, ds, min_count,
+                              _fp(out), st.ctypes.data_as(_d)))
+    summ = TrackerIterationSummary(int(st[0]), int(st[1]), float(st[2]), bool(st[3]),
+                                   (int(st[4]), int(st[5]), int(st[6])), bool(st[7]))
+    return out, summ
+
+
+def icp_reduce(map: VoxelBlockMap, depth_level: torch.Tensor, level: int, intr0: Intrinsics, state: RenderState,
+               cam_to_world, dist: float) -> np.ndarray:
+    """One evaluation of the 29 point-to-plane sums (H upper 21, g 6, sum r^2, n)."""
+    out = np.zeros(29, np.float64)
+    c2w = _pose(cam_to_world)
+    rp = _pose(state.pose)
+    map.bind_stream()
+    check(lib().rfg_icp_reduce(map.handle, _ptr(depth_level.contiguous()), level, C.byref(intr0.c()),
+                               _ptr(state.points), _ptr(state.normals), _fp(rp), _fp(c2w), dist,
+                               out.ctypes.data_as(_d)))
+    return out
+
+
+# ------------------------------------------------------------- pipeline
+class Pipeline:
+    """Device-resident per-frame driver (ITMMainEngine::ProcessFrame order,
+    SPEC.md:764): [ICP track] -> allocate -> integrate -> expected ranges ->
+    ICP-map raycast, optionally replayed as a CUDA graph."""
+
+    def __init__(self, map: VoxelBlockMap, intr: Intrinsics, params: SceneParams,
+                 affine: DepthAffine = DepthAffine(1.0 / 5000.0, 0.0), levels: int = 3, track: bool = True,
+                 iters=(6, 10, 20), dist=(0.1, 0.1, 0.1), min_count: int = 10, use_graph: bool = True):
+        self.map = map
+        self.intr = intr
+        cfg = _lib.PipelineConfig_()
+        cfg.intr = intr.c()
+        cfg.params = params.c()
+        cfg.aff_scale = affine.scale
+        cfg.aff_offset = affine.offset
+        cfg.levels = levels
+        cfg.track = 1 if track else 0
+        cfg.iters = (C.c_int32 * 3)(*iters)
+        cfg.dist = (C.c_float * 3)(*dist)
+        cfg.min_count = min_count
+        cfg.use_graph = 1 if use_graph else 0
+        self._h = C.c_void_p()
+        check(lib().rfg_pipeline_create(map.handle, C.byref(cfg), C.byref(self._h)))
+        self._levels = levels
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            lib().rfg_pipeline_destroy(self._h)
+            self._h = None
+
+    def process(self, raw, pose=None):
+        """raw: CUDA uint16/int16 tensor (device path) or numpy uint16 (host path)."""
+        p = _fp(_pose(pose)) if pose is not None else None
+        if torch.is_tensor(raw) and raw.is_cuda:
+            check(lib().rfg_pipeline_process_raw(self._h, _ptr(raw), p))
+        else:
+            a = np.ascontiguousarray(raw, np.uint16) if not torch.is_tensor(raw) else raw.numpy()
+            check(lib().rfg_pipeline_process_host(self._h, a.ctypes.data_as(C.c_void_p), p))
+
+    def result(self):
+        st = _lib.AllocStats_()
+        pose = np.zeros((3, 4), np.float32)
+        icp = np.zeros(8, np.float64)
+        check(lib().rfg_pipeline_result(self._h, C.byref(st), _fp(pose), icp.ctypes.data_as(_d)))
+        return AllocationStats(st.requested, st.allocated, st.allocFailures, st.visibleCount), pose, icp
+
+    def buffers(self):
+        ptrs = [C.c_void_p() for _ in range(5)]
+        check(lib().rfg_pipeline_buffers(self._h, *[C.byref(p) for p in ptrs]))
+        return [p.value for p in ptrs]
+
+    def reset(self):
+        check(lib().rfg_pipeline_reset(self._h))
+
+
+# ------------------------------------------------------------ synthetic
+def orbit_trajectory(target=(0.0, 0.15, 1.4), distance=1.4, frames=100, max_angle=0.5) -> np.ndarray:
+    """proj/src/synth.cpp:173-195 (world -> camera poses, (frames, 3, 4))."""
+    out = np.zeros((frames, 3, 4), np.float32)
+    t = np.ascontiguousarray(target, np.float32)
+    check(lib().rfg_synth_orbit_poses(_fp(t), distance, frames, max_angle, _fp(out)))
+    return out
+
+
+def multiroom_trajectory(frames=100) -> np.ndarray:
+    out = np.zeros((frames, 3, 4), np.float32)
+    check(lib().rfg_synth_multiroom_poses(frames, _fp(out)))
+    return out
+
+
+SCENE_SPHERE_IN_ROOM = 0
+SCENE_MULTI_ROOM = 1
+SCENE_CHECKER_WALL = 2
+
+
+def synth_render(scene: int, pose, intr: Intrinsics, affine=DepthAffine(1.0 / 5000.0, 0.0), rgb=False):
+    """synth_render_depth (proj/src/synth.cpp:136-171): (raw u16, depth m, rgb)."""
+    h, w = intr.height, intr.width
+    raw = np.zeros((h, w), np.uint16)
+    dep = np.zeros((h, w), np.float32)
+    col = np.zeros((h, w, 3), np.uint8) if rgb else None
+    p = _pose(pose)
+    check(lib().rfg_synth_render(scene, _fp(p), C.byref(intr.c()), affine.scale, affine.offset, 1 if rgb else 0,
+                                 raw.ctypes.data_as(_u16), _fp(dep),
+                                 col.ctypes.data_as(_u8) if col is not None else None))
+    return raw, dep, col
