@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 dense-fusion hot path (BASELINE.json metric:
+depth frames/s of alloc + integrate + raycast at 640x480, 5 mm voxels).
+
+Workload (BASELINE.json configs[1], "C2"): the synthetic sphere-in-room orbit
+sequence (100 frames, 640x480, known poses), 5 mm voxels, mu = 2 cm,
+0x40000-bucket hash (excess 0x20000, 0x40000 blocks), depth-only voxels, ICP
+depth tracker on a 3-level pyramid.  One step = one frame through the
+device-resident pipeline: build_view (raw u16 -> metres + pyramid) -> ICP
+track against the previous render -> allocate (stages 1-3) -> integrate ->
+expected ranges -> ICP-map raycast, replayed as a CUDA graph.  Frames are
+pre-staged in HBM; L2 is flushed (256 MiB write) before every timed frame and
+timing uses CUDA events on the pipeline's stream around each frame.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Under torchrun (N > 1) the voxel-hash space is sharded spatially over the
+ranks (each allocates/integrates its own blocks + a 1-block halo) and the
+raycast is composed by a per-pixel nearest-hit NCCL reduction; the tracker
+runs replicated on the composed maps.  `--impl reference` times the
+reference's own CPU implementation (oracle/_ref, compiled from
+/root/reference sources; the ICP stage, absent from the reference, is the C
+port oracle/rfo.c) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "depth frames/s (alloc+integrate+raycast) @640x480, 5mm voxels; HBM GB/s vs peak"
+UNIT = "frames/s"
+N_FRAMES = 100
+INTR = dict(width=640, height=480, fx=525.0, fy=525.0, cx=319.5, cy=239.5)
+PARAMS = dict(voxelSize=0.005, mu=0.02, maxW=100, viewFrustum_min=0.2, viewFrustum_max=6.0,
+              stopIntegratingAtMaxW=False)
+MAPCFG = (0x40000, 0x20000, 0x40000)
+AFF = (1.0 / 5000.0, 0.0)
+ICP_ITERS = (6, 10, 20)  # per level, finest first (20/10/6 coarse -> fine)
+ICP_DIST = (0.01, 0.02, 0.04)  # outlier gates per level, finest first
+WORKLOAD = ("C2: synthetic sphere-in-room orbit, 100 frames 640x480 (known poses), 5 mm voxels, mu 2 cm, "
+            "0x40000-bucket hash (+0x20000 excess, 0x40000 blocks), depth-only ITMVoxel_s, "
+            "ICP depth tracker 3-level pyramid; step = 1 frame: view+ICP+alloc+visible+integrate+ranges+raycast")
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device=0, period=0.05):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.period = period
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_reference_run(n_warm: int, n_timed: int, budget_s: float = 1e9):
+    """Reference CPU path on the same workload: oracle/_ref (the reference's own
+    sources, single-threaded) for view/alloc/integrate/ranges/raycast and the C
+    port for ICP.  Returns (frames/s, kind, frames timed, per-stage ms)."""
+    from oracle import ref, rfo
+
+    kind = "reference" if ref.available() else "port"
+    poses = ref.orbit_poses([0, 0.15, 1.4], 1.4, N_FRAMES, 0.5) if kind == "reference" else None
+    if poses is None:
+        from paper_1708_00783_b200 import fusion as F
+        poses = F.orbit_trajectory(frames=N_FRAMES)
+    E = (ref.RefEngine if kind == "reference" else rfo.OracleEngine)(*MAPCFG)
+    render = ref.render if kind == "reference" else None
+    stage = {"view": 0.0, "icp": 0.0, "allocate": 0.0, "integrate": 0.0, "ranges": 0.0, "raycast": 0.0}
+    pose = poses[0].copy()
+    last = None
+    t_total, timed = 0.0, 0
+    t_start = time.perf_counter()
+    for f in range(n_warm + n_timed):
+        if render is not None:
+            raw, _, _ = render(0, poses[f], INTR)
+        else:
+            from paper_1708_00783_b200 import fusion as F
+            raw, _, _ = F.synth_render(0, poses[f], F.Intrinsics(**INTR))
+        t0 = time.perf_counter()
+        lv = (ref.build_view if kind == "reference" else rfo.build_view)(raw, INTR, AFF, 3)
+        t1 = time.perf_counter()
+        if last is not None:
+            pose, _ = rfo.icp_track(lv, INTR, last[0], last[1], last[2], INTR, pose, ICP_ITERS, 10, ICP_DIST)
+        t2 = time.perf_counter()
+        E.allocate(lv[0], INTR, pose, PARAMS)
+        t3 = time.perf_counter()
+        E.integrate(lv[0], INTR, pose, PARAMS)
+        t4 = time.perf_counter()
+        E.render_ranges(pose, INTR, PARAMS)
+        t5 = time.perf_counter()
+        _, pts, nrm, _ = E.render_icp(pose, INTR, PARAMS)
+        t6 = time.perf_counter()
+        last = (pts, nrm, pose.copy())
+        if f >= n_warm:
+            timed += 1
+            t_total += t6 - t0
+            for k, a, b in (("view", t0, t1), ("icp", t1, t2), ("allocate", t2, t3), ("integrate", t3, t4),
+                            ("ranges", t4, t5), ("raycast", t5, t6)):
+                stage[k] += (b - a) * 1e3
+            if time.perf_counter() - t_start > budget_s:
+                break
+    per = {k: v / max(timed, 1) for k, v in stage.items()}
+    return timed / t_total, kind, timed, per
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    fps, kind, n, per = cpu_reference_run(args.warmup, args.steps, budget_s=args.ref_budget)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 / fps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "frames_timed": n, "steps_requested": args.steps,
+                   "sample": f"frames {args.warmup}..{args.warmup + n - 1} of the orbit sequence"},
+        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"{n} frames after {args.warmup} warm-up frames; single-threaded reference "
+                                   "(oracle/_ref = /root/reference/proj sources) + C-port ICP",
+                         "stage_ms": per},
+        "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ B200
+def make_frames():
+    from paper_1708_00783_b200 import fusion as F
+    intr = F.Intrinsics(**INTR)
+    poses = F.orbit_trajectory(frames=N_FRAMES)
+    raws = np.stack([F.synth_render(F.SCENE_SPHERE_IN_ROOM, poses[f], intr)[0] for f in range(N_FRAMES)])
+    return poses, raws
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_00783_b200 import fusion as F
+    from paper_1708_00783_b200._lib import launch_count
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    intr = F.Intrinsics(**INTR)
+    params = F.SceneParams(**PARAMS)
+    poses, raws = make_frames()
+    raw_dev = torch.from_numpy(raws.view(np.int16)).cuda()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    if world > 1:
+        from paper_1708_00783_b200.shard import ShardedPipeline
+        make_pipe = lambda m, graph, profile=False: ShardedPipeline(  # noqa: E731
+            m, intr, params, rank, world, levels=3, iters=ICP_ITERS, dist=ICP_DIST)
+    else:
+        make_pipe = lambda m, graph, profile=False: F.Pipeline(  # noqa: E731
+            m, intr, params, F.DepthAffine(*AFF), levels=3, track=True, iters=ICP_ITERS, dist=ICP_DIST,
+            use_graph=graph, profile=profile)
+
+    m = F.VoxelBlockMap(F.VoxelBlockMapConfig(*MAPCFG), device=local)
+    if world > 1:
+        m.set_shard(rank, world, 3)
+    pipe = make_pipe(m, True)
+    stream = torch.cuda.ExternalStream(pipe.stream)
+
+    def reset():
+        torch.cuda.synchronize()
+        m.clear()
+        pipe.reset()
+        torch.cuda.synchronize()
+
+    # ---- timed region: warmup W frames, then K frames (sequence restarts with
+    # a fresh map, untimed, every 100 frames) ----
+    total = args.warmup + args.steps
+    order = [i % N_FRAMES for i in range(total)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    launches0 = None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i, f in enumerate(order):
+        if f == 0:
+            reset()
+        if i == args.warmup:
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            sampler.start()
+            launches0 = launch_count()
+        flush.fill_(i & 0xFF)  # evict L2 (untimed; outside the event pair)
+        with torch.cuda.stream(stream):
+            stream.wait_stream(torch.cuda.current_stream())
+            if i >= args.warmup:
+                evs[i - args.warmup][0].record(stream)
+            pipe.process(raw_dev[f], poses[0] if f == 0 else None)
+            if i >= args.warmup:
+                evs[i - args.warmup][1].record(stream)
+        torch.cuda.current_stream().wait_stream(stream)
+    torch.cuda.synchronize()
+    launches = launch_count() - launches0
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_total = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    fps = args.steps / (ms_total / 1e3)  # one frame stream (strong scaling over ranks)
+    stats, pose_out, icp = pipe.result()
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if args.e2e_steps > 0:
+        raw_pinned = torch.from_numpy(raws.view(np.int16)).pin_memory()
+        reset()
+        e2e_total = 0.0
+        n_e2e = min(args.e2e_steps, N_FRAMES)
+        warm = min(args.warmup, n_e2e - 1)
+        for f in range(n_e2e):
+            flush.fill_(f & 0xFF)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pipe.process(raw_pinned[f].numpy().view(np.uint16), poses[0] if f == 0 else None)
+            st, _, _ = pipe.result()  # D2H of stats + pose + ICP summary
+            t1 = time.perf_counter()
+            if f >= warm:
+                e2e_total += t1 - t0
+        if world > 1:
+            t = torch.tensor([e2e_total], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_total = float(t.item())
+        e2e = {"value": (n_e2e - warm) / e2e_total, "unit": UNIT, "h2d_bytes_per_step": INTR["width"] * INTR["height"] * 2,
+               "d2h_bytes_per_step": 64 + 48 + 64, "frames": n_e2e - warm,
+               "path": "Pipeline.process(host raw u16) + Pipeline.result() per frame (rfg_pipeline_process_host/result)"}
+
+    # ---- per-stage device times (non-graph profile pass, same frames) ----
+    prof = None
+    roof = None
+    if world == 1 and args.profile_frames > 0:
+        ppipe = F.Pipeline(m, intr, params, F.DepthAffine(*AFF), levels=3, track=True, iters=ICP_ITERS,
+                           dist=ICP_DIST, use_graph=False, profile=True)
+        torch.cuda.synchronize()
+        m.clear()
+        ppipe.reset()
+        acc, nvis = {}, []
+        n_prof = 0
+        for f in range(min(N_FRAMES, args.warmup + args.profile_frames)):
+            flush.fill_(f & 0xFF)
+            torch.cuda.synchronize()
+            ppipe.process(raw_dev[f], poses[0] if f == 0 else None)
+            st_ms = ppipe.stage_times()
+            st, _, _ = ppipe.result()
+            if f >= args.warmup:
+                n_prof += 1
+                nvis.append(st.visibleCount)
+                for k, v in st_ms.items():
+                    acc[k] = acc.get(k, 0.0) + v
+        prof = {k: v / n_prof for k, v in acc.items()}
+        peak, peak_kind = load_peaks()
+        mean_vis = float(np.mean(nvis))
+        # integration: 2 x 2 KiB depth plane per visible block + the depth image
+        int_bytes = mean_vis * 2 * 512 * 4 + INTR["width"] * INTR["height"] * 4
+        achieved = int_bytes / (prof["integrate"] * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get("integrate_dram_bytes_per_launch")
+        except Exception:
+            pass
+        roof = {"kernel": "k_integrate (TSDF integration, rfg_integrate.cu)", "bound": "hbm", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_kind, "algorithmic_bytes_per_launch": int_bytes,
+                "mean_visible_blocks": mean_vis, "launch_ms": prof["integrate"]}
+        del ppipe
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    cpu = None
+    if args.cpu_frames > 0 and world == 1:
+        try:
+            v, kind, n, per = cpu_reference_run(2, args.cpu_frames)
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+                   "sample": f"frames 2..{1 + n} of the same orbit sequence (2 warm-up frames), single-threaded; "
+                             "ICP stage is the C port (the reference has no tracker)", "stage_ms": per}
+        except Exception as e:  # the checker must not take the bench down
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "unavailable", "sample": str(e)}
+
+    line = {
+        "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "l2": "flushed (256 MiB write) before every timed frame",
+                   "parallelism": f"spatial hash shards x{world}" if world > 1 else "single GPU",
+                   "graph": True, "last_frame_stats": stats.as_array().tolist(),
+                   "icp_last": {"iterations": int(icp[0]), "count": int(icp[1]), "per_level": icp[4:7].tolist()}},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roof, "stage_ms": prof,
+        "cpu_baseline": cpu, "step_ms_p50": float(np.median(step_ms)), "step_ms_max": float(np.max(step_ms)),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=95)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--profile-frames", type=int, default=30)
+    ap.add_argument("--cpu-frames", type=int, default=5)
+    ap.add_argument("--ref-budget", type=float, default=150.0, help="reference arm time budget (s)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -158,6 +158,7 @@ typedef struct {
   float dist[3];
   int32_t min_count;
   int32_t use_graph;       /* capture the frame into a CUDA graph */
+  int32_t profile;         /* record CUDA events between stages (non-graph mode only) */
 } rfg_pipeline_config;
 
 int rfg_pipeline_create(rfg_map* map, const rfg_pipeline_config* cfg, rfg_pipeline** out);
@@ -175,6 +176,11 @@ int rfg_pipeline_buffers(rfg_pipeline* p, float** depth_levels, float** range, f
                          float** normals);
 /* Reset the device pose / tracking state (not the map). */
 int rfg_pipeline_reset(rfg_pipeline* p);
+/* Per-stage device times (ms) of the last frame when cfg.profile = 1:
+ * {view, icp, allocate, integrate, ranges, raycast, total}.  Synchronises. */
+int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]);
+/* The pipeline's stream (cudaStream_t) for event timing by the caller. */
+void* rfg_pipeline_stream(rfg_pipeline* p);
 
 /* --------------------------------------------------------------- export */
 uint32_t rfg_total_entries(const rfg_map* map);

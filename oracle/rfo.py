@@ -96,7 +96,7 @@ def build_view(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=1):
 
 
 def icp_track(levels_depth, intr, points, normals, render_pose34, render_intr, init_pose34,
-              iters=(6, 10, 20), min_count=10, dist=(0.1, 0.1, 0.1)):
+              iters=(6, 10, 20), min_count=10, dist=(0.01, 0.02, 0.04)):
     flat = np.ascontiguousarray(np.concatenate([d.reshape(-1) for d in levels_depth]), np.float32)
     wh, f4 = _wh(intr), _f4(intr)
     rf4 = _f4(render_intr)

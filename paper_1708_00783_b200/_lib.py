@@ -45,7 +45,7 @@ class PipelineConfig_(C.Structure):
     _fields_ = [("intr", Intrinsics_), ("params", SceneParams_), ("aff_scale", C.c_float),
                 ("aff_offset", C.c_float), ("levels", C.c_int32), ("track", C.c_int32),
                 ("iters", C.c_int32 * 3), ("dist", C.c_float * 3), ("min_count", C.c_int32),
-                ("use_graph", C.c_int32)]
+                ("use_graph", C.c_int32), ("profile", C.c_int32)]
 
 
 # every symbol include/rfg.h declares, with its ctypes signature
@@ -83,6 +83,8 @@ SIGNATURES = {
     "rfg_pipeline_buffers": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                               C.POINTER(_vp)], C.c_int),
     "rfg_pipeline_reset": ([_vp], C.c_int),
+    "rfg_pipeline_stage_times": ([_vp, _f], C.c_int),
+    "rfg_pipeline_stream": ([_vp], _vp),
     "rfg_total_entries": ([_vp], C.c_uint32),
     "rfg_export_entries": ([_vp, _i], C.c_int),
     "rfg_export_blocks": ([_vp, _i, C.c_int, _u8], C.c_int),

@@ -435,6 +435,8 @@ struct rfg_pipeline {
   int frames;
   cudaGraphExec_t exec[2];  // [0] no tracking, [1] tracking
   uint64_t graphKernels[2];
+  cudaEvent_t ev[7];        // stage boundaries (profile mode)
+  bool tracked;             // last frame ran the tracker
 };
 
 namespace {
@@ -443,27 +445,39 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   rfg_map* m = p->map;
   const rfg_pipeline_config& c = p->cfg;
   cudaStream_t s = p->stream;
+  const bool prof = c.profile && !c.use_graph;
+  auto mark = [&](int k) {
+    if (prof) cudaEventRecord(p->ev[k], s);
+  };
+  mark(0);
   cudaError_t e = launch_build_view(p->rawDev, c.intr.width, c.intr.height, c.aff_scale, c.aff_offset, c.levels,
                                     p->depthLevels, s);
   if (e != cudaSuccess) return e;
+  mark(1);
   if (track) {
     const Intr in0{c.intr.width, c.intr.height, c.intr.fx, c.intr.fy, c.intr.cx, c.intr.cy};
     e = launch_icp_track(m->icpOut, m->icpPartials, p->depthLevels, c.levels, in0, p->points, p->normals, c.iters,
                          c.dist, c.min_count, p->poses, p->poses + 12, p->poses, s);
     if (e != cudaSuccess) return e;
   }
+  mark(2);
   const FrameArgs fa = make_frame_args(&c.intr, &c.params, nullptr, p->poses);
   if ((e = launch_allocate(m->d, p->depthLevels, fa, s)) != cudaSuccess) return e;
+  mark(3);
   if ((e = launch_integrate(m->d, p->depthLevels, nullptr, fa, nullptr, nullptr, s)) != cudaSuccess) return e;
+  mark(4);
   if ((e = launch_ranges(m->d, fa, p->range, s)) != cudaSuccess) return e;
+  mark(5);
   if ((e = launch_icp_maps(m->d, fa, p->range, p->raycast, p->points, p->normals, s)) != cudaSuccess) return e;
   k_copy12<<<1, 32, 0, s>>>(p->poses + 12, p->poses);
   count_launch();
+  mark(6);
   return cudaGetLastError();
 }
 
 int run_frame(rfg_pipeline* p, const float* pose34) {
   const bool track = p->cfg.track && p->frames > 0;
+  p->tracked = track;
   if (pose34) {
     Pose12 pv;
     memcpy(pv.v, pose34, 48);
@@ -527,6 +541,14 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
     set_error("pipeline allocation failed");
     return RFG_ENOMEM;
   }
+  for (int k = 0; k < 7; ++k)
+    if (cudaEventCreate(&p->ev[k]) != cudaSuccess) ok = false;
+  if (!ok) {
+    cudaGetLastError();
+    rfg_pipeline_destroy(p);
+    set_error("pipeline event creation failed");
+    return RFG_ECUDA;
+  }
   m->stream = p->stream;
   const int rc = rfg_pipeline_reset(p);
   if (rc != RFG_OK) {
@@ -545,6 +567,8 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->points, p->normals, p->poses};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  for (int k = 0; k < 7; ++k)
+    if (p->ev[k]) cudaEventDestroy(p->ev[k]);
   if (p->hostIcp) cudaFreeHost(p->hostIcp);
   if (p->hostPose) cudaFreeHost(p->hostPose);
   if (p->map && p->map->stream == p->stream) p->map->stream = nullptr;
@@ -594,6 +618,18 @@ int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34
   if (icpStats8) memcpy(icpStats8, p->hostIcp, 64);
   return RFG_OK;
 }
+
+int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]) {
+  RFG_REQUIRE(p && ms7, "null argument");
+  RFG_REQUIRE(p->cfg.profile && !p->cfg.use_graph, "stage times need profile = 1 and use_graph = 0");
+  RFG_CK(cudaEventSynchronize(p->ev[6]));
+  for (int k = 0; k < 6; ++k) RFG_CK(cudaEventElapsedTime(&ms7[k], p->ev[k], p->ev[k + 1]));
+  RFG_CK(cudaEventElapsedTime(&ms7[6], p->ev[0], p->ev[6]));
+  if (!p->tracked) ms7[1] = 0.f;
+  return RFG_OK;
+}
+
+void* rfg_pipeline_stream(rfg_pipeline* p) { return p ? (void*)p->stream : nullptr; }
 
 int rfg_pipeline_buffers(rfg_pipeline* p, float** depthLevels, float** range, float** raycast, float** points,
                          float** normals) {

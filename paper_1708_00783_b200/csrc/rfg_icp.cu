@@ -2,32 +2,43 @@
 //
 // The reference has no tracker; the algorithm is restated
 // from SPEC.md:348-356,390-395 and fixed by the CPU oracle
-// oracle/rfo.c:rfo_icp_track.  Per iteration:
-//   k_icp_reduce  — every valid pyramid pixel is backprojected, moved to the
-//                   world by the current estimate, projected into the last
-//                   ICP-map render (nearest pixel) and, if associated, adds
-//                   J J^T (21), J r (6), r^2 and 1 to double accumulators;
-//                   warp-shuffle tree + shared-memory reduction to one
-//                   partial per CTA (fixed grid => deterministic sums).
-//   k_icp_solve   — one warp sums the partials in fixed order, Cholesky-
-//                   solves H delta = -g, T_cw <- exp(delta) T_cw, and raises
-//                   the level's done flag on convergence/degeneracy so the
-//                   remaining enqueued iterations of that level exit at once.
-// All iterations are enqueued up front (no host round trip per iteration),
-// so the whole tracker can live inside the frame's CUDA graph.
+// oracle/rfo.c:rfo_icp_track.
+//
+// One cooperative kernel per pyramid level runs that level's whole
+// Gauss-Newton loop on the device:
+//   reduce  — every valid pyramid pixel is backprojected, moved to the world
+//             by the current estimate, projected into the last ICP-map render
+//             (nearest pixel) and, if associated and within the level's
+//             distance gate, adds J J^T (21), J r (6), r^2 and 1 to double
+//             accumulators; warp-shuffle tree + shared-memory reduction to one
+//             partial per CTA;
+//   grid.sync();
+//   solve   — CTA 0 sums the partials in a fixed order (deterministic),
+//             Cholesky-solves H delta = -g, T_cw <- exp(delta) T_cw, and raises
+//             the level's done flag on convergence (|delta| < 1e-4) or
+//             degeneracy;
+//   grid.sync();
+// so a frame's tracker is 1 + levels + 1 launches (no per-iteration launch,
+// no host round trip, nothing enqueued for iterations that are not needed) and
+// is capturable in the frame's CUDA graph.  The grid is one CTA per SM, fixed
+// for a device, so the reduction order — and the result — is run-to-run
+// deterministic.
+#include <cooperative_groups.h>
+
 #include "rfg_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rfg {
 
-constexpr int kIcpCtas = 296;  // 2 x 148 SMs; fixed => reduction order fixed
-constexpr int kIcpThreads = 256;
+constexpr int kIcpThreads = 512;
 
-// Device tracking state (lives in rfg_map::icpOut as doubles + floats).
+// Device tracking state (rfg_map::icpOut).
 struct IcpState {
   double c2w[12];       // current camera->world estimate (row-major 3x4)
   double sums[29];      // last evaluation
   double stats[8];      // {iterations, count, E, converged, it_l0, it_l1, it_l2, ok}
-  float c2wF[12];       // float cast of c2w used by the per-pixel kernel
+  float c2wF[12];       // float cast of c2w used by the per-pixel pass
   float w2cF[12];       // tracked world->camera (output pose)
   float renderPose[12]; // world->camera of the render being tracked against
   int done[4];          // per-level stop flags
@@ -37,13 +48,16 @@ struct IcpState {
 struct IcpLevelArgs {
   const float* depth;   // pyramid level
   int lw, lh;
-  float fx, fy, cx, cy; // level intrinsics
+  float fx, fy, cx, cy; // level intrinsics (Intrinsics::atLevel, camera.hpp:35-45)
   const float4* points;
   const float4* normals;
   int rw, rh;           // render size (level 0)
   float rfx, rfy, rcx, rcy;
-  float dist;
+  float dist;           // outlier gate |p_w - V| (m)
   int level;
+  int iters;
+  int minCount;
+  int evalOnly;         // 1: record the sums, never update the pose
 };
 
 // double-precision SE(3) (proj/include/rf/pose.hpp:45-60 with S = double)
@@ -56,11 +70,9 @@ __device__ void c2w_to_float(const double* c, float* f) {
   for (int i = 0; i < 12; ++i) f[i] = (float)c[i];
 }
 
-// Inverse of a float pose, promoted to double (oracle: pose_inverse in float,
-// then widened).
+// Inverse of a float pose, widened to double (the oracle does the same).
 __device__ void init_from_w2c(IcpState* st, const float* w2c) {
-  const Pose p = pose_from12(w2c);
-  const Pose q = pose_inverse(p);
+  const Pose q = pose_inverse(pose_from12(w2c));
   for (int r = 0; r < 3; ++r) {
     for (int c = 0; c < 3; ++c) st->c2w[r * 4 + c] = (double)q.R[r * 3 + c];
     st->c2w[r * 4 + 3] = (double)q.t[r];
@@ -77,68 +89,21 @@ __global__ void k_icp_init(IcpState* st, const float* w2c, const float* renderPo
   st->stats[7] = 1.0;
 }
 
+// Load an explicit float camera->world pose (single evaluations).
+__global__ void k_icp_set_c2w(IcpState* st, const float* c2w, const float* renderPose) {
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < 12; ++i) {
+    st->c2wF[i] = c2w[i];
+    st->c2w[i] = c2w[i];
+    st->renderPose[i] = renderPose[i];
+  }
+  for (int i = 0; i < 4; ++i) st->done[i] = 0;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   return v;
-}
-
-__global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(IcpState* st, IcpLevelArgs a, double* partials) {
-  __shared__ double sh[kIcpThreads / 32][29];
-  if (st->done[a.level]) return;
-  double acc[29];
-#pragma unroll
-  for (int k = 0; k < 29; ++k) acc[k] = 0.0;
-  const Pose c2w = pose_from12(st->c2wF);
-  const Pose rp = pose_from12(st->renderPose);
-  const Intr inl{a.lw, a.lh, a.fx, a.fy, a.cx, a.cy};
-  const float dist2 = a.dist * a.dist;
-  const int n = a.lw * a.lh;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    const float d = __ldg(a.depth + p);
-    if (!(d > 0.f)) continue;
-    const int x = p % a.lw, y = p / a.lw;
-    const f3 pc = backproject(inl, (float)x, (float)y, d);
-    const f3 pw = pose_apply(c2w, pc);
-    const f3 q = pose_apply(rp, pw);
-    if (!(q.z > 0.f)) continue;
-    const float u = a.rfx * q.x / q.z + a.rcx;
-    const float v = a.rfy * q.y / q.z + a.rcy;
-    if (!(u >= 0.f && v >= 0.f && u <= (float)(a.rw - 1) && v <= (float)(a.rh - 1))) continue;
-    const int iu = (int)(u + 0.5f), iv = (int)(v + 0.5f);
-    const float4 V = __ldg(a.points + (size_t)iv * a.rw + iu);
-    const float4 N = __ldg(a.normals + (size_t)iv * a.rw + iu);
-    if (!(V.w > 0.f) || !(N.w > 0.f)) continue;
-    const f3 diff{pw.x - V.x, pw.y - V.y, pw.z - V.z};
-    if (sqnorm3(diff) > dist2) continue;
-    const f3 nn{N.x, N.y, N.z};
-    const float r = dot3(diff, nn);
-    const f3 pxn = cross3(pw, nn);
-    const double J[6] = {pxn.x, pxn.y, pxn.z, nn.x, nn.y, nn.z};
-    const double rd = r;
-    int k = 0;
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int j = i; j < 6; ++j) acc[k++] += J[i] * J[j];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * rd;
-    acc[27] += rd * rd;
-    acc[28] += 1.0;
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < 29; ++k) {
-    const double s = warp_sum(acc[k]);
-    if (lane == 0) sh[wid][k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < 29) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kIcpThreads / 32; ++w) s += sh[w][threadIdx.x];
-    partials[blockIdx.x * 29 + threadIdx.x] = s;
-  }
 }
 
 // Cholesky solve (same operation order as oracle/rfo.c:rfo_solve6).
@@ -167,7 +132,7 @@ __device__ int solve6(const double* acc, double* x) {
       L[i * 6 + j] = t / ljj;
     }
   }
-  if (det < 1e-12) return -1;
+  if (det < 1e-12) return -1;  // SPEC.md:352
   double yv[6];
   for (int i = 0; i < 6; ++i) {
     double t = -acc[21 + i];
@@ -182,18 +147,9 @@ __device__ int solve6(const double* acc, double* x) {
   return 0;
 }
 
-__global__ void k_icp_solve(IcpState* st, const double* partials, int nPartials, int level, int minCount) {
-  if (st->done[level]) return;
-  // fixed-order sum of the per-CTA partials: lane k owns sum k
-  __shared__ double sums[29];
-  if (threadIdx.x < 29) {
-    double s = 0.0;
-    for (int c = 0; c < nPartials; ++c) s += partials[c * 29 + threadIdx.x];
-    sums[threadIdx.x] = s;
-    st->sums[threadIdx.x] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
+// Solve + update by one thread (oracle: rfo_icp_track loop body).
+__device__ void solve_and_update(IcpState* st, const double* sums, int level, int minCount) {
+  for (int k = 0; k < 29; ++k) st->sums[k] = sums[k];
   st->stats[1] = sums[28];
   st->stats[2] = sums[27];
   if (sums[28] < (double)minCount) {
@@ -207,7 +163,6 @@ __global__ void k_icp_solve(IcpState* st, const double* partials, int nPartials,
     st->done[level] = 1;
     return;
   }
-  // exp(delta) (pose.hpp:45-60)
   const double* w = delta;
   const double* v = delta + 3;
   const double theta = sqrt(w[0] * w[0] + (w[1] * w[1] + w[2] * w[2]));
@@ -232,13 +187,11 @@ __global__ void k_icp_solve(IcpState* st, const double* partials, int nPartials,
     V[i] = I + cb * W[i] + cc * WW[i];
   }
   for (int r = 0; r < 3; ++r) Et[r] = V[r * 3] * v[0] + (V[r * 3 + 1] * v[1] + V[r * 3 + 2] * v[2]);
-  // c2w <- exp(delta) * c2w
-  double CR[9], Ct[3];
+  double CR[9], Ct[3], NR[9];
   for (int r = 0; r < 3; ++r) {
     for (int c = 0; c < 3; ++c) CR[r * 3 + c] = st->c2w[r * 4 + c];
     Ct[r] = st->c2w[r * 4 + 3];
   }
-  double NR[9];
   matmul3d(ER, CR, NR);
   for (int r = 0; r < 3; ++r) {
     for (int c = 0; c < 3; ++c) st->c2w[r * 4 + c] = NR[r * 3 + c];
@@ -252,6 +205,94 @@ __global__ void k_icp_solve(IcpState* st, const double* partials, int nPartials,
   if (nrm < 1e-4) {
     st->stats[3] = 1.0;
     st->done[level] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a, double* partials) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[kIcpThreads / 32][29];
+  __shared__ double sums[29];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const Intr inl{a.lw, a.lh, a.fx, a.fy, a.cx, a.cy};
+  const float dist2 = a.dist * a.dist;
+  const int n = a.lw * a.lh;
+  for (int it = 0; it < a.iters; ++it) {
+    if (__ldcg(&st->done[a.level])) break;  // grid-uniform: written before the last grid.sync
+    float c2wF[12], rpF[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      c2wF[i] = __ldcg(&st->c2wF[i]);
+      rpF[i] = __ldcg(&st->renderPose[i]);
+    }
+    const Pose c2w = pose_from12(c2wF);
+    const Pose rp = pose_from12(rpF);
+    double acc[29];
+#pragma unroll
+    for (int k = 0; k < 29; ++k) acc[k] = 0.0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+      const float d = __ldg(a.depth + p);
+      if (!(d > 0.f)) continue;
+      const int x = p % a.lw, y = p / a.lw;
+      const f3 pc = backproject(inl, (float)x, (float)y, d);
+      const f3 pw = pose_apply(c2w, pc);
+      const f3 q = pose_apply(rp, pw);
+      if (!(q.z > 0.f)) continue;
+      const float u = a.rfx * q.x / q.z + a.rcx;
+      const float v = a.rfy * q.y / q.z + a.rcy;
+      if (!(u >= 0.f && v >= 0.f && u <= (float)(a.rw - 1) && v <= (float)(a.rh - 1))) continue;
+      const int iu = (int)(u + 0.5f), iv = (int)(v + 0.5f);
+      const float4 V = __ldg(a.points + (size_t)iv * a.rw + iu);
+      const float4 N = __ldg(a.normals + (size_t)iv * a.rw + iu);
+      if (!(V.w > 0.f) || !(N.w > 0.f)) continue;
+      const f3 diff{pw.x - V.x, pw.y - V.y, pw.z - V.z};
+      if (sqnorm3(diff) > dist2) continue;
+      const f3 nn{N.x, N.y, N.z};
+      const float r = dot3(diff, nn);
+      const f3 pxn = cross3(pw, nn);
+      const double J[6] = {pxn.x, pxn.y, pxn.z, nn.x, nn.y, nn.z};
+      const double rd = r;
+      int k = 0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = i; j < 6; ++j) acc[k++] += J[i] * J[j];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * rd;
+      acc[27] += rd * rd;
+      acc[28] += 1.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 29; ++k) {
+      const double s = warp_sum(acc[k]);
+      if (lane == 0) sh[wid][k] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 29) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kIcpThreads / 32; ++w) s += sh[w][threadIdx.x];
+      partials[blockIdx.x * 29 + threadIdx.x] = s;
+    }
+    grid.sync();
+    if (blockIdx.x == 0) {
+      // fixed-order final sum: warp w owns sums w, w+16; lanes stride the CTAs
+      for (int k = wid; k < 29; k += kIcpThreads / 32) {
+        double s = 0.0;
+        for (int c = lane; c < (int)gridDim.x; c += 32) s += __ldcg(partials + c * 29 + k);
+        s = warp_sum(s);
+        if (lane == 0) sums[k] = s;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (a.evalOnly) {
+          for (int k = 0; k < 29; ++k) st->sums[k] = sums[k];
+          st->done[a.level] = 1;
+        } else {
+          solve_and_update(st, sums, a.level, a.minCount);
+        }
+      }
+    }
+    grid.sync();
   }
 }
 
@@ -271,22 +312,59 @@ __global__ void k_icp_final(IcpState* st, float* w2cOut) {
     for (int i = 0; i < 12; ++i) w2cOut[i] = st->w2cF[i];
 }
 
-// Load an explicit float c2w pose (for single evaluations).
-__global__ void k_icp_set_c2w(IcpState* st, const float* c2w, const float* renderPose) {
-  if (threadIdx.x != 0) return;
-  for (int i = 0; i < 12; ++i) {
-    st->c2wF[i] = c2w[i];
-    st->c2w[i] = c2w[i];
-    st->renderPose[i] = renderPose[i];
+static int icp_grid() {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 148, perSm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, k_icp_level, kIcpThreads, 0);
+    grid = sms * (perSm >= 1 ? 1 : 0);  // one CTA per SM; co-residency required by grid.sync
   }
-  for (int i = 0; i < 4; ++i) st->done[i] = 0;
+  return grid;
 }
 
 size_t icp_state_bytes() { return sizeof(IcpState); }
-int icp_partial_slots() { return kIcpCtas; }
+int icp_partial_slots() { return 1024; }
+
+static cudaError_t launch_level(IcpState* st, const IcpLevelArgs& a, double* partials, cudaStream_t s) {
+  const int grid = icp_grid();
+  if (grid <= 0) return cudaErrorCooperativeLaunchTooLarge;
+  IcpState* stp = st;
+  IcpLevelArgs ap = a;
+  double* pp = partials;
+  void* args[] = {&stp, &ap, &pp};
+  count_launch();
+  return cudaLaunchCooperativeKernel((const void*)k_icp_level, dim3(grid), dim3(kIcpThreads), args, 0, s);
+}
+
+static IcpLevelArgs level_args(const float* depthLevels, int level, const Intr& in0, const float4* points,
+                               const float4* normals) {
+  IcpLevelArgs a{};
+  size_t off = 0;
+  for (int l = 0; l < level; ++l) off += (size_t)(in0.w >> l) * (in0.h >> l);
+  const float sc = ldexpf(1.f, -level);
+  a.depth = depthLevels + off;
+  a.lw = in0.w >> level;
+  a.lh = in0.h >> level;
+  a.fx = in0.fx * sc;
+  a.fy = in0.fy * sc;
+  a.cx = in0.cx * sc;
+  a.cy = in0.cy * sc;
+  a.points = points;
+  a.normals = normals;
+  a.rw = in0.w;
+  a.rh = in0.h;
+  a.rfx = in0.fx;
+  a.rfy = in0.fy;
+  a.rcx = in0.cx;
+  a.rcy = in0.cy;
+  a.level = level;
+  return a;
+}
 
 // Enqueue a complete coarse-to-fine track: init from (w2c, renderPose) device
-// pointers, every iteration of every level, final pose to w2cOut (device).
+// pointers, one cooperative launch per level, final pose to w2cOut (device).
 cudaError_t launch_icp_track(void* state, double* partials, const float* depthLevels, int levels, const Intr& in0,
                              const float4* points, const float4* normals, const int* iters, const float* dist,
                              int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
@@ -294,37 +372,15 @@ cudaError_t launch_icp_track(void* state, double* partials, const float* depthLe
   IcpState* st = static_cast<IcpState*>(state);
   k_icp_init<<<1, 32, 0, s>>>(st, w2cInit, renderPose);
   count_launch();
-  size_t off[4] = {0, 0, 0, 0};
-  size_t o = 0;
-  for (int l = 0; l < levels; ++l) {
-    off[l] = o;
-    o += (size_t)(in0.w >> l) * (in0.h >> l);
-  }
   for (int l = levels - 1; l >= 0; --l) {
-    IcpLevelArgs a;
-    const float sc = ldexpf(1.f, -l);
-    a.depth = depthLevels + off[l];
-    a.lw = in0.w >> l;
-    a.lh = in0.h >> l;
-    a.fx = in0.fx * sc;
-    a.fy = in0.fy * sc;
-    a.cx = in0.cx * sc;
-    a.cy = in0.cy * sc;
-    a.points = points;
-    a.normals = normals;
-    a.rw = in0.w;
-    a.rh = in0.h;
-    a.rfx = in0.fx;
-    a.rfy = in0.fy;
-    a.rcx = in0.cx;
-    a.rcy = in0.cy;
+    IcpLevelArgs a = level_args(depthLevels, l, in0, points, normals);
     a.dist = dist[l];
-    a.level = l;
-    for (int it = 0; it < iters[l]; ++it) {
-      k_icp_reduce<<<kIcpCtas, kIcpThreads, 0, s>>>(st, a, partials);
-      k_icp_solve<<<1, 32, 0, s>>>(st, partials, kIcpCtas, l, minCount);
-      count_launch(2);
-    }
+    a.iters = iters[l];
+    a.minCount = minCount;
+    a.evalOnly = 0;
+    if (a.iters <= 0) continue;
+    const cudaError_t e = launch_level(st, a, partials, s);
+    if (e != cudaSuccess) return e;
   }
   k_icp_final<<<1, 32, 0, s>>>(st, w2cOut);
   count_launch();
@@ -336,7 +392,8 @@ cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* d
                                    const float* renderPose, float dist, cudaStream_t s) {
   IcpState* st = static_cast<IcpState*>(state);
   k_icp_set_c2w<<<1, 32, 0, s>>>(st, c2w, renderPose);
-  IcpLevelArgs a;
+  count_launch();
+  IcpLevelArgs a = level_args(depth, 0, in0, points, normals);
   a.depth = depth;
   a.lw = lw;
   a.lh = lh;
@@ -344,22 +401,12 @@ cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* d
   a.fy = f4l[1];
   a.cx = f4l[2];
   a.cy = f4l[3];
-  a.points = points;
-  a.normals = normals;
-  a.rw = in0.w;
-  a.rh = in0.h;
-  a.rfx = in0.fx;
-  a.rfy = in0.fy;
-  a.rcx = in0.cx;
-  a.rcy = in0.cy;
   a.dist = dist;
   a.level = 3;
-  k_icp_reduce<<<kIcpCtas, kIcpThreads, 0, s>>>(st, a, partials);
-  // reuse the solver's fixed-order partial sum, with an impossible minCount
-  // so it records the sums without updating the pose
-  k_icp_solve<<<1, 32, 0, s>>>(st, partials, kIcpCtas, 3, 0x7fffffff);
-  count_launch(3);
-  return cudaGetLastError();
+  a.iters = 1;
+  a.minCount = 0;
+  a.evalOnly = 1;
+  return launch_level(st, a, partials, s);
 }
 
 const double* icp_sums_ptr(void* state) { return static_cast<IcpState*>(state)->sums; }

@@ -413,7 +413,7 @@ class TrackerIterationSummary:
 
 
 def track_depth(map: VoxelBlockMap, view: View, state: RenderState, init_pose, iters=(6, 10, 20),
-                dist=(0.1, 0.1, 0.1), min_count: int = 10):
+                dist=(0.01, 0.02, 0.04), min_count: int = 10):
     """Point-to-plane ICP of the view's depth pyramid against
     the last ICP-map render in `state`.  iters/dist are indexed by pyramid
     level (0 = finest; SPEC.md:391 caps 20/10/6 coarse -> fine)."""
@@ -464,7 +464,8 @@ class Pipeline:
 
     def __init__(self, map: VoxelBlockMap, intr: Intrinsics, params: SceneParams,
                  affine: DepthAffine = DepthAffine(1.0 / 5000.0, 0.0), levels: int = 3, track: bool = True,
-                 iters=(6, 10, 20), dist=(0.1, 0.1, 0.1), min_count: int = 10, use_graph: bool = True):
+                 iters=(6, 10, 20), dist=(0.01, 0.02, 0.04), min_count: int = 10, use_graph: bool = True,
+                 profile: bool = False):
         self.map = map
         self.intr = intr
         cfg = _lib.PipelineConfig_()
@@ -478,6 +479,7 @@ class Pipeline:
         cfg.dist = (C.c_float * 3)(*dist)
         cfg.min_count = min_count
         cfg.use_graph = 1 if use_graph else 0
+        cfg.profile = 1 if profile else 0
         self._h = C.c_void_p()
         check(lib().rfg_pipeline_create(map.handle, C.byref(cfg), C.byref(self._h)))
         self._levels = levels
@@ -510,6 +512,15 @@ class Pipeline:
 
     def reset(self):
         check(lib().rfg_pipeline_reset(self._h))
+
+    def stage_times(self) -> dict:
+        ms = np.zeros(7, np.float32)
+        check(lib().rfg_pipeline_stage_times(self._h, _fp(ms)))
+        return dict(zip(("view", "icp", "allocate", "integrate", "ranges", "raycast", "total"), ms.tolist()))
+
+    @property
+    def stream(self) -> int:
+        return int(lib().rfg_pipeline_stream(self._h) or 0)
 
 
 # ------------------------------------------------------------ synthetic
