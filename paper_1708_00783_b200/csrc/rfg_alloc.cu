@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
     if (cand[0] | cand[1] | cand[2] | cand[3]) {
       const Pose pose = load_pose(fa);
       uint32_t out[4] = {0, 0, 0, 0};
-#pragma unroll
+#pragma unroll 4
       for (int j = 0; j < 16; ++j) {
         if (!((cand[j >> 2] >> ((j & 3) * 8)) & 0xFFu)) continue;
         const int4 e = ld_entry(m.entries, base + j);

@@ -5,24 +5,23 @@
 // oracle/rfo.c:rfo_icp_track.
 //
 // One cooperative kernel per pyramid level runs that level's whole
-// Gauss-Newton loop on the device:
+// Gauss-Newton loop on the device.  Per iteration:
 //   reduce  — every valid pyramid pixel is backprojected, moved to the world
 //             by the current estimate, projected into the last ICP-map render
 //             (nearest pixel) and, if associated and within the level's
 //             distance gate, adds J J^T (21), J r (6), r^2 and 1 to double
 //             accumulators; warp-shuffle tree + shared-memory reduction to one
-//             partial per CTA;
+//             partial per CTA (partials double-buffered by iteration parity);
 //   grid.sync();
-//   solve   — CTA 0 sums the partials in a fixed order (deterministic),
-//             Cholesky-solves H delta = -g, T_cw <- exp(delta) T_cw, and raises
-//             the level's done flag on convergence (|delta| < 1e-4) or
-//             degeneracy;
-//   grid.sync();
-// so a frame's tracker is 1 + levels + 1 launches (no per-iteration launch,
-// no host round trip, nothing enqueued for iterations that are not needed) and
-// is capturable in the frame's CUDA graph.  The grid is one CTA per SM, fixed
-// for a device, so the reduction order — and the result — is run-to-run
-// deterministic.
+//   solve   — EVERY CTA sums all partials in the same fixed order and runs
+//             the same Cholesky solve and SE(3) update, so all CTAs hold the
+//             identical new estimate without a second grid barrier; CTA 0
+//             publishes it (pose, stats, done flag) to global memory.
+// A frame's tracker is therefore 1 + levels + 1 launches with one grid
+// barrier per iteration, nothing is enqueued for iterations that are not
+// needed, and the whole tracker is capturable in the frame's CUDA graph.  The
+// grid size is fixed per level, so the reduction order — and the result — is
+// run-to-run deterministic.
 #include <cooperative_groups.h>
 
 #include "rfg_common.cuh"
@@ -32,13 +31,14 @@ namespace cg = cooperative_groups;
 namespace rfg {
 
 constexpr int kIcpThreads = 512;
+constexpr int kIcpMaxCtas = 512;
 
 // Device tracking state (rfg_map::icpOut).
 struct IcpState {
   double c2w[12];       // current camera->world estimate (row-major 3x4)
   double sums[29];      // last evaluation
   double stats[8];      // {iterations, count, E, converged, it_l0, it_l1, it_l2, ok}
-  float c2wF[12];       // float cast of c2w used by the per-pixel pass
+  float c2wF[12];       // float cast of c2w
   float w2cF[12];       // tracked world->camera (output pose)
   float renderPose[12]; // world->camera of the render being tracked against
   int done[4];          // per-level stop flags
@@ -60,6 +60,16 @@ struct IcpLevelArgs {
   int evalOnly;         // 1: record the sums, never update the pose
 };
 
+// Per-CTA copy of the Gauss-Newton state (identical in every CTA).
+struct GnShared {
+  double c2w[12];
+  double sums[29];
+  double stats[8];
+  float c2wF[12];
+  float rp[12];
+  int done;
+};
+
 // double-precision SE(3) (proj/include/rf/pose.hpp:45-60 with S = double)
 __device__ void matmul3d(const double* A, const double* B, double* C) {
   for (int r = 0; r < 3; ++r)
@@ -70,19 +80,15 @@ __device__ void c2w_to_float(const double* c, float* f) {
   for (int i = 0; i < 12; ++i) f[i] = (float)c[i];
 }
 
-// Inverse of a float pose, widened to double (the oracle does the same).
-__device__ void init_from_w2c(IcpState* st, const float* w2c) {
+__global__ void k_icp_init(IcpState* st, const float* w2c, const float* renderPose) {
+  if (threadIdx.x != 0) return;
+  // inverse of the float pose, widened to double (the oracle does the same)
   const Pose q = pose_inverse(pose_from12(w2c));
   for (int r = 0; r < 3; ++r) {
     for (int c = 0; c < 3; ++c) st->c2w[r * 4 + c] = (double)q.R[r * 3 + c];
     st->c2w[r * 4 + 3] = (double)q.t[r];
   }
   c2w_to_float(st->c2w, st->c2wF);
-}
-
-__global__ void k_icp_init(IcpState* st, const float* w2c, const float* renderPose) {
-  if (threadIdx.x != 0) return;
-  init_from_w2c(st, w2c);
   for (int i = 0; i < 12; ++i) st->renderPose[i] = renderPose[i];
   for (int i = 0; i < 4; ++i) st->done[i] = 0;
   for (int i = 0; i < 8; ++i) st->stats[i] = 0.0;
@@ -147,20 +153,20 @@ __device__ int solve6(const double* acc, double* x) {
   return 0;
 }
 
-// Solve + update by one thread (oracle: rfo_icp_track loop body).
-__device__ void solve_and_update(IcpState* st, const double* sums, int level, int minCount) {
-  for (int k = 0; k < 29; ++k) st->sums[k] = sums[k];
-  st->stats[1] = sums[28];
-  st->stats[2] = sums[27];
-  if (sums[28] < (double)minCount) {
-    st->stats[7] = 0.0;
-    st->done[level] = 1;
+// One Gauss-Newton step on the CTA-local state (oracle: rfo_icp_track loop
+// body): count gate, Cholesky solve, T_cw <- exp(delta) T_cw, convergence.
+__device__ void gn_step(GnShared& g, int level, int minCount) {
+  g.stats[1] = g.sums[28];
+  g.stats[2] = g.sums[27];
+  if (g.sums[28] < (double)minCount) {
+    g.stats[7] = 0.0;
+    g.done = 1;
     return;
   }
   double delta[6];
-  if (solve6(sums, delta) != 0) {
-    st->stats[7] = 0.0;
-    st->done[level] = 1;
+  if (solve6(g.sums, delta) != 0) {
+    g.stats[7] = 0.0;
+    g.done = 1;
     return;
   }
   const double* w = delta;
@@ -189,43 +195,47 @@ __device__ void solve_and_update(IcpState* st, const double* sums, int level, in
   for (int r = 0; r < 3; ++r) Et[r] = V[r * 3] * v[0] + (V[r * 3 + 1] * v[1] + V[r * 3 + 2] * v[2]);
   double CR[9], Ct[3], NR[9];
   for (int r = 0; r < 3; ++r) {
-    for (int c = 0; c < 3; ++c) CR[r * 3 + c] = st->c2w[r * 4 + c];
-    Ct[r] = st->c2w[r * 4 + 3];
+    for (int c = 0; c < 3; ++c) CR[r * 3 + c] = g.c2w[r * 4 + c];
+    Ct[r] = g.c2w[r * 4 + 3];
   }
   matmul3d(ER, CR, NR);
   for (int r = 0; r < 3; ++r) {
-    for (int c = 0; c < 3; ++c) st->c2w[r * 4 + c] = NR[r * 3 + c];
-    st->c2w[r * 4 + 3] = (ER[r * 3] * Ct[0] + (ER[r * 3 + 1] * Ct[1] + ER[r * 3 + 2] * Ct[2])) + Et[r];
+    for (int c = 0; c < 3; ++c) g.c2w[r * 4 + c] = NR[r * 3 + c];
+    g.c2w[r * 4 + 3] = (ER[r * 3] * Ct[0] + (ER[r * 3 + 1] * Ct[1] + ER[r * 3 + 2] * Ct[2])) + Et[r];
   }
-  c2w_to_float(st->c2w, st->c2wF);
-  st->stats[0] += 1.0;
-  st->stats[4 + level] += 1.0;
+  c2w_to_float(g.c2w, g.c2wF);
+  g.stats[0] += 1.0;
+  g.stats[4 + level] += 1.0;
   const double nrm = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2] + delta[3] * delta[3] +
                           delta[4] * delta[4] + delta[5] * delta[5]);
   if (nrm < 1e-4) {
-    st->stats[3] = 1.0;
-    st->done[level] = 1;
+    g.stats[3] = 1.0;
+    g.done = 1;
   }
 }
 
 __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a, double* partials) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[kIcpThreads / 32][29];
-  __shared__ double sums[29];
+  __shared__ GnShared g;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 12; ++i) {
+      g.c2w[i] = __ldcg(&st->c2w[i]);
+      g.c2wF[i] = __ldcg(&st->c2wF[i]);
+      g.rp[i] = __ldcg(&st->renderPose[i]);
+    }
+    for (int i = 0; i < 8; ++i) g.stats[i] = __ldcg(&st->stats[i]);
+    g.done = __ldcg(&st->done[a.level]);
+  }
+  __syncthreads();
   const Intr inl{a.lw, a.lh, a.fx, a.fy, a.cx, a.cy};
   const float dist2 = a.dist * a.dist;
   const int n = a.lw * a.lh;
-  for (int it = 0; it < a.iters; ++it) {
-    if (__ldcg(&st->done[a.level])) break;  // grid-uniform: written before the last grid.sync
-    float c2wF[12], rpF[12];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) {
-      c2wF[i] = __ldcg(&st->c2wF[i]);
-      rpF[i] = __ldcg(&st->renderPose[i]);
-    }
-    const Pose c2w = pose_from12(c2wF);
-    const Pose rp = pose_from12(rpF);
+  const Pose rp = pose_from12(g.rp);
+  for (int it = 0; it < a.iters && !g.done; ++it) {
+    double* part = partials + (size_t)(it & 1) * kIcpMaxCtas * 29;
+    const Pose c2w = pose_from12(g.c2wF);
     double acc[29];
 #pragma unroll
     for (int k = 0; k < 29; ++k) acc[k] = 0.0;
@@ -271,28 +281,34 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < kIcpThreads / 32; ++w) s += sh[w][threadIdx.x];
-      partials[blockIdx.x * 29 + threadIdx.x] = s;
+      part[blockIdx.x * 29 + threadIdx.x] = s;
     }
     grid.sync();
-    if (blockIdx.x == 0) {
-      // fixed-order final sum: warp w owns sums w, w+16; lanes stride the CTAs
-      for (int k = wid; k < 29; k += kIcpThreads / 32) {
-        double s = 0.0;
-        for (int c = lane; c < (int)gridDim.x; c += 32) s += __ldcg(partials + c * 29 + k);
-        s = warp_sum(s);
-        if (lane == 0) sums[k] = s;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        if (a.evalOnly) {
-          for (int k = 0; k < 29; ++k) st->sums[k] = sums[k];
-          st->done[a.level] = 1;
-        } else {
-          solve_and_update(st, sums, a.level, a.minCount);
-        }
-      }
+    // every CTA: fixed-order final sum (warp w owns sums w, w+16; lanes
+    // stride the CTAs; shuffle tree) and the identical solve
+    for (int k = wid; k < 29; k += kIcpThreads / 32) {
+      double s = 0.0;
+      for (int c = lane; c < (int)gridDim.x; c += 32) s += __ldcg(part + c * 29 + k);
+      s = warp_sum(s);
+      if (lane == 0) g.sums[k] = s;
     }
-    grid.sync();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (a.evalOnly)
+        g.done = 1;
+      else
+        gn_step(g, a.level, a.minCount);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int i = 0; i < 12; ++i) {
+      st->c2w[i] = g.c2w[i];
+      st->c2wF[i] = g.c2wF[i];
+    }
+    for (int k = 0; k < 29; ++k) st->sums[k] = g.sums[k];
+    for (int i = 0; i < 8; ++i) st->stats[i] = g.stats[i];
+    st->done[a.level] = g.done;
   }
 }
 
@@ -312,23 +328,27 @@ __global__ void k_icp_final(IcpState* st, float* w2cOut) {
     for (int i = 0; i < 12; ++i) w2cOut[i] = st->w2cF[i];
 }
 
-static int icp_grid() {
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 148, perSm = 0;
+// CTAs for a level of n pixels: about one pixel per thread, at most one CTA
+// per SM (co-residency for grid.sync).  Fixed per (device, level size).
+static int icp_grid(int n) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0, perSm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, k_icp_level, kIcpThreads, 0);
-    grid = sms * (perSm >= 1 ? 1 : 0);  // one CTA per SM; co-residency required by grid.sync
+    if (perSm < 1) sms = -1;
   }
-  return grid;
+  if (sms <= 0) return 0;
+  const int want = (n + kIcpThreads - 1) / kIcpThreads;
+  return want < 1 ? 1 : (want < sms ? want : sms);
 }
 
 size_t icp_state_bytes() { return sizeof(IcpState); }
-int icp_partial_slots() { return 1024; }
+int icp_partial_slots() { return 2 * kIcpMaxCtas; }
 
 static cudaError_t launch_level(IcpState* st, const IcpLevelArgs& a, double* partials, cudaStream_t s) {
-  const int grid = icp_grid();
+  const int grid = icp_grid(a.lw * a.lh);
   if (grid <= 0) return cudaErrorCooperativeLaunchTooLarge;
   IcpState* stp = st;
   IcpLevelArgs ap = a;

@@ -92,43 +92,87 @@ __global__ void __launch_bounds__(256) k_range_blocks(DevMap m, FrameArgs fa, fl
 }
 
 // ------------------------------------------------------------ raycast
+// TSDF field reader (MapField, raycast.hpp:32-45) with the reference's
+// last-block cache.  Voxel offsets inside a block use bit operations
+// (v & 7 == v - (v >> 3) * 8 for negative v too).
 struct FieldReader {
-  const DevMap& m;
+  const int4* entries;
+  const uint32_t* vba;
+  uint32_t buckets;
   BlockCache cache;
+
+  __device__ __forceinline__ int ptr_of(int bx, int by, int bz) {
+    if (cache.bx == bx && cache.by == by && cache.bz == bz) return cache.ptr;
+    int ptr = -1;
+    if (bx >= -32768 && bx <= 32767 && by >= -32768 && by <= 32767 && bz >= -32768 && bz <= 32767) {
+      int idx = (int)hash_index(bx, by, bz, buckets - 1);
+      const int xy = (int)((uint32_t)(uint16_t)bx | ((uint32_t)(uint16_t)by << 16));
+      for (;;) {
+        const int4 e = __ldg(entries + idx);
+        if (e.w >= -1 && e.x == xy && e.y == bz) {
+          ptr = e.w;
+          break;
+        }
+        if (e.z < 1) break;
+        idx = (int)buckets + e.z - 1;
+      }
+    }
+    cache.bx = bx;
+    cache.by = by;
+    cache.bz = bz;
+    cache.ptr = ptr >= 0 ? ptr : -1;
+    return cache.ptr;
+  }
 
   // MapField::resident (raycast.hpp:38-42)
   __device__ __forceinline__ bool resident(f3 p) {
-    const i3 b{((int)floorf(p.x)) >> 3, ((int)floorf(p.y)) >> 3, ((int)floorf(p.z)) >> 3};
-    return block_ptr(m, b, cache) >= 0;
-  }
-  __device__ __forceinline__ bool voxel(i3 v, uint32_t* out) {
-    const i3 b{v.x >> 3, v.y >> 3, v.z >> 3};
-    const int ptr = block_ptr(m, b, cache);
-    if (ptr < 0) return false;
-    const int lin = (v.x - b.x * kBlock) + (v.y - b.y * kBlock) * kBlock + (v.z - b.z * kBlock) * kBlock * kBlock;
-    *out = __ldg(m.vbaDepth + (size_t)ptr * kBlock3 + lin);
-    return true;
+    return ptr_of(((int)floorf(p.x)) >> 3, ((int)floorf(p.y)) >> 3, ((int)floorf(p.z)) >> 3) >= 0;
   }
   // readSdfNearest (voxel_block_map.cpp:178-185)
   __device__ __forceinline__ float nearest(f3 p, bool& ok) {
-    uint32_t w;
-    ok = voxel(i3{(int)lroundf(p.x), (int)lroundf(p.y), (int)lroundf(p.z)}, &w);
-    return ok ? sdf_to_logical(vox_sdf(w)) : 1.f;
+    const int vx = (int)lroundf(p.x), vy = (int)lroundf(p.y), vz = (int)lroundf(p.z);
+    const int ptr = ptr_of(vx >> 3, vy >> 3, vz >> 3);
+    ok = ptr >= 0;
+    if (!ok) return 1.f;
+    const uint32_t w = __ldg(vba + (size_t)ptr * kBlock3 + ((vx & 7) | ((vy & 7) << 3) | ((vz & 7) << 6)));
+    return sdf_to_logical(vox_sdf(w));
   }
-  // readSdfWeightTrilinear (voxel_block_map.cpp:130-156)
-  __device__ __forceinline__ float trilinear(f3 p, bool& ok) {
+  // readSdfWeightTrilinear (voxel_block_map.cpp:130-156).  Any missing
+  // corner invalidates the read, so the corner order only matters for the
+  // weighted sum, which is accumulated in the reference's k order.  When the
+  // 2x2x2 cell lies inside one block (the common case) a single lookup feeds
+  // eight independent loads.
+  __device__ __noinline__ float trilinear(f3 p, bool& ok) {
     const int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
     const float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
-    float sdf = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      uint32_t w;
-      if (!voxel(i3{bx + (k & 1), by + ((k >> 1) & 1), bz + ((k >> 2) & 1)}, &w)) {
+    const int lx = bx & 7, ly = by & 7, lz = bz & 7;
+    uint32_t w[8];
+    if (lx < 7 && ly < 7 && lz < 7) {
+      const int ptr = ptr_of(bx >> 3, by >> 3, bz >> 3);
+      if (ptr < 0) {
         ok = false;
         return 1.f;
       }
+      const uint32_t* base = vba + (size_t)ptr * kBlock3 + (lx | (ly << 3) | (lz << 6));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = __ldg(base + ((k & 1) | ((k & 2) << 2) | ((k & 4) << 4)));
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int cx = bx + (k & 1), cy = by + ((k >> 1) & 1), cz = bz + ((k >> 2) & 1);
+        const int ptr = ptr_of(cx >> 3, cy >> 3, cz >> 3);
+        if (ptr < 0) {
+          ok = false;
+          return 1.f;
+        }
+        w[k] = __ldg(vba + (size_t)ptr * kBlock3 + ((cx & 7) | ((cy & 7) << 3) | ((cz & 7) << 6)));
+      }
+    }
+    float sdf = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
       const float bw = ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
-      sdf += bw * sdf_to_logical(vox_sdf(w));
+      sdf += bw * sdf_to_logical(vox_sdf(w[k]));
     }
     ok = true;
     return sdf;
@@ -222,7 +266,7 @@ __global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, con
     const float norm = sqrtf(sqnorm3(dirCam));
     const f3 dw = rot_apply(c2w.R, dirCam);
     const f3 dirW{dw.x / norm, dw.y / norm, dw.z / norm};
-    FieldReader field{m};
+    FieldReader field{m.entries, m.vbaDepth, m.buckets};
     field.cache.reset();
     f3 hit;
     if (cast_ray(field, origin, dirW, r.x * norm, r.y * norm, fa.mu, fa.voxelSize, &hit)) {
