@@ -1,0 +1,213 @@
+// rfg.hpp — header-only C++ adapter over the librfg.so C ABI (rfg.h) that
+// re-exposes the reference's engine interface under its own names, so a
+// maintainer can swap the CPU engine for the B200 one call by call:
+//
+//   rf::VoxelBlockMapConfig / VoxelBlockMap   proj/include/rf/voxel_block_map.hpp:36-144
+//   rf::SceneParams / AllocationStats         proj/include/rf/fusion.hpp:11-27
+//   rf::FusionEngine::allocate_from_depth /
+//                     integrate_frame         proj/include/rf/fusion.hpp:52-79
+//   rf::render_expected_ranges / render_maps  proj/include/rf/raycast.hpp:122-129
+//
+// Images are device pointers (the reference's View/RenderState hold host
+// Images; here the GPU owns them).  Errors follow the reference: an invalid
+// bucketCount throws std::invalid_argument (voxel_block_map.cpp:10-11); every
+// other failure throws rfg::Error carrying the C status code.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rfg.h"
+
+namespace rfg {
+
+using Pose34 = std::array<float, 12>;  // row-major [R | t], world -> camera
+
+inline Pose34 identity_pose() { return {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0}; }
+
+class Error : public std::runtime_error {
+ public:
+  Error(int code, const std::string& msg) : std::runtime_error(msg), code_(code) {}
+  int code() const { return code_; }
+
+ private:
+  int code_;
+};
+
+inline void check(int rc) {
+  if (rc == RFG_OK) return;
+  if (rc == RFG_EINVAL) throw std::invalid_argument(rfg_last_error());
+  throw Error(rc, std::string("librfg: ") + rfg_last_error());
+}
+
+struct VoxelBlockMapConfig {
+  std::uint32_t bucketCount = 1u << 20;
+  std::uint32_t excessCount = 1u << 17;
+  std::uint32_t blockCapacity = 1u << 18;
+  static VoxelBlockMapConfig small() { return {1u << 14, 1u << 11, 1u << 13}; }
+};
+
+struct Intrinsics {
+  int width = 0, height = 0;
+  float fx = 0, fy = 0, cx = 0, cy = 0;
+  rfg_intrinsics c() const { return {width, height, fx, fy, cx, cy}; }
+};
+
+struct SceneParams {
+  float voxelSize = 0.005f;
+  float mu = 0.02f;
+  int maxW = 100;
+  float viewFrustum_min = 0.2f;
+  float viewFrustum_max = 6.f;
+  bool stopIntegratingAtMaxW = false;
+  float blockSizeMetres() const { return voxelSize * 8; }
+  rfg_scene_params c() const {
+    return {voxelSize, mu, maxW, viewFrustum_min, viewFrustum_max, stopIntegratingAtMaxW ? 1 : 0};
+  }
+};
+
+struct AllocationStats {
+  int requested = 0, allocated = 0, allocFailures = 0, visibleCount = 0;
+};
+
+struct HashEntry {
+  int x, y, z, offset, ptr;
+  bool allocated() const { return ptr >= -1; }
+  bool inMemory() const { return ptr >= 0; }
+};
+
+class VoxelBlockMap {
+ public:
+  explicit VoxelBlockMap(const VoxelBlockMapConfig& cfg = VoxelBlockMapConfig::small(), bool colour = false,
+                         int device = 0)
+      : config_(cfg) {
+    rfg_map_config c{cfg.bucketCount, cfg.excessCount, cfg.blockCapacity, colour ? 1 : 0};
+    check(rfg_map_create(&c, device, &map_));
+  }
+  ~VoxelBlockMap() { rfg_map_destroy(map_); }
+  VoxelBlockMap(const VoxelBlockMap&) = delete;
+  VoxelBlockMap& operator=(const VoxelBlockMap&) = delete;
+
+  rfg_map* handle() const { return map_; }
+  const VoxelBlockMapConfig& config() const { return config_; }
+  std::uint32_t bucketCount() const { return config_.bucketCount; }
+  std::uint32_t totalEntries() const { return config_.bucketCount + config_.excessCount; }
+  std::uint32_t hashMask() const { return config_.bucketCount - 1; }
+  void clear() { check(rfg_map_clear(map_)); }
+  void setStream(void* cudaStream) { check(rfg_map_set_stream(map_, cudaStream)); }
+
+  std::vector<HashEntry> entries() const {
+    std::vector<HashEntry> out(totalEntries());
+    check(rfg_export_entries(map_, reinterpret_cast<int32_t*>(out.data())));
+    return out;
+  }
+  std::vector<int> visibleList() const {
+    std::int32_t n = 0;
+    check(rfg_export_visible(map_, nullptr, nullptr, &n));
+    std::vector<int> out(n);
+    check(rfg_export_visible(map_, out.data(), nullptr, &n));
+    return out;
+  }
+  int freeBlockCount() const {
+    std::int32_t nb = 0, ne = 0;
+    check(rfg_free_counts(map_, &nb, &ne));
+    return nb;
+  }
+  int allocatedBlockCount() const { return static_cast<int>(config_.blockCapacity) - freeBlockCount(); }
+
+ private:
+  VoxelBlockMapConfig config_;
+  rfg_map* map_ = nullptr;
+};
+
+class FusionEngine {
+ public:
+  AllocationStats allocate_from_depth(VoxelBlockMap& map, const float* depthDev, const Intrinsics& intr,
+                                      const Pose34& pose, const SceneParams& params) {
+    const rfg_intrinsics i = intr.c();
+    const rfg_scene_params p = params.c();
+    rfg_alloc_stats s{};
+    check(rfg_allocate_from_depth(map.handle(), depthDev, &i, pose.data(), &p, &s));
+    return {s.requested, s.allocated, s.allocFailures, s.visibleCount};
+  }
+  void integrate_frame(VoxelBlockMap& map, const float* depthDev, const Intrinsics& intr, const Pose34& pose,
+                       const SceneParams& params, const std::uint8_t* rgbDev = nullptr,
+                       const Intrinsics* intrRgb = nullptr, const Pose34* extrinsics = nullptr) {
+    const rfg_intrinsics i = intr.c();
+    const rfg_intrinsics ir = intrRgb ? intrRgb->c() : i;
+    const rfg_scene_params p = params.c();
+    check(rfg_integrate(map.handle(), depthDev, rgbDev, &i, &ir, extrinsics ? extrinsics->data() : nullptr,
+                        pose.data(), &p));
+  }
+};
+
+enum class RenderMode { kIcpMaps, kColour, kGrey };
+
+inline void render_expected_ranges(const VoxelBlockMap& map, const Pose34& pose, const Intrinsics& intr,
+                                   const SceneParams& params, float* rangeDev) {
+  const rfg_intrinsics i = intr.c();
+  const rfg_scene_params p = params.c();
+  check(rfg_render_expected_ranges(map.handle(), pose.data(), &i, &p, rangeDev));
+}
+
+inline void render_maps(const VoxelBlockMap& map, const Pose34& pose, const Intrinsics& intr,
+                        const SceneParams& params, RenderMode mode, const float* rangeDev, float* raycastDev,
+                        float* pointsDev, float* normalsDev) {
+  if (mode != RenderMode::kIcpMaps) throw Error(RFG_EINVAL, "only RenderMode::kIcpMaps runs on the B200 path");
+  const rfg_intrinsics i = intr.c();
+  const rfg_scene_params p = params.c();
+  check(rfg_render_icp_maps(map.handle(), pose.data(), &i, &p, rangeDev, raycastDev, pointsDev, normalsDev));
+}
+
+// ITMMainEngine::ProcessFrame-style driver (absent in the reference).
+class Pipeline {
+ public:
+  Pipeline(VoxelBlockMap& map, const Intrinsics& intr, const SceneParams& params, float affScale, float affOffset,
+           int levels = 3, bool track = true) {
+    rfg_pipeline_config c{};
+    c.intr = intr.c();
+    c.params = params.c();
+    c.aff_scale = affScale;
+    c.aff_offset = affOffset;
+    c.levels = levels;
+    c.track = track ? 1 : 0;
+    c.iters[0] = 6;
+    c.iters[1] = 10;
+    c.iters[2] = 20;
+    c.dist[0] = 0.01f;
+    c.dist[1] = 0.02f;
+    c.dist[2] = 0.04f;
+    c.min_count = 10;
+    c.use_graph = 1;
+    check(rfg_pipeline_create(map.handle(), &c, &p_));
+  }
+  ~Pipeline() { rfg_pipeline_destroy(p_); }
+  Pipeline(const Pipeline&) = delete;
+  Pipeline& operator=(const Pipeline&) = delete;
+
+  void processHost(const std::uint16_t* rawHost, const Pose34* pose = nullptr) {
+    check(rfg_pipeline_process_host(p_, rawHost, pose ? pose->data() : nullptr));
+  }
+  AllocationStats result(Pose34* poseOut = nullptr) {
+    rfg_alloc_stats s{};
+    Pose34 tmp;
+    check(rfg_pipeline_result(p_, &s, poseOut ? poseOut->data() : tmp.data(), nullptr));
+    return {s.requested, s.allocated, s.allocFailures, s.visibleCount};
+  }
+
+ private:
+  rfg_pipeline* p_ = nullptr;
+};
+
+// Synthetic frame source (proj/src/synth.cpp).
+inline std::vector<Pose34> orbit_trajectory(std::array<float, 3> target, float distance, int frames,
+                                            float maxAngle = 0.5f) {
+  std::vector<Pose34> out(frames);
+  check(rfg_synth_orbit_poses(target.data(), distance, frames, maxAngle, out.empty() ? nullptr : out[0].data()));
+  return out;
+}
+
+}  // namespace rfg

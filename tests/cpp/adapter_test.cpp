@@ -1,0 +1,51 @@
+// C++ use of the drop-in adapter (include/rfg.hpp), written like the
+// reference's own doctest cases.  Without a GPU it checks the error contract
+// and exits 0; with one it fuses a short synthetic sequence through the
+// public pipeline and checks the reference's frame-0 statistics.
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "rfg.hpp"
+
+static int failures = 0;
+#define CHECK(x)                                                   \
+  do {                                                             \
+    if (!(x)) {                                                    \
+      std::fprintf(stderr, "%s:%d: FAILED %s\n", __FILE__, __LINE__, #x); \
+      ++failures;                                                  \
+    }                                                              \
+  } while (0)
+
+int main() {
+  // voxel_block_map.cpp:10-11 — non-power-of-two bucket count throws
+  bool threw = false;
+  try {
+    rfg::VoxelBlockMap bad({1000, 16, 16});
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  try {
+    rfg::VoxelBlockMap map({0x40000, 0x20000, 0x40000});
+    const rfg::Intrinsics intr{640, 480, 525.f, 525.f, 319.5f, 239.5f};
+    const rfg::SceneParams params;
+    const auto poses = rfg::orbit_trajectory({0.f, 0.15f, 1.4f}, 1.4f, 100);
+    rfg::Pipeline pipe(map, intr, params, 1.f / 5000.f, 0.f, 3, /*track=*/false);
+    std::vector<std::uint16_t> raw(640 * 480);
+    std::vector<float> depth(640 * 480);
+    const rfg_intrinsics ci = intr.c();
+    rfg_synth_render(0, poses[0].data(), &ci, 1.f / 5000.f, 0.f, 0, raw.data(), depth.data(), nullptr);
+    pipe.processHost(raw.data(), &poses[0]);
+    const rfg::AllocationStats st = pipe.result();
+    // the reference's frame-0 statistics on C1 (tests/golden/c1_frames.json)
+    CHECK(st.requested == 8349 && st.allocated == 8349 && st.allocFailures == 0 && st.visibleCount == 8349);
+    CHECK(map.allocatedBlockCount() == 8349);
+    std::printf("adapter_test: GPU sequence ok\n");
+  } catch (const rfg::Error& e) {
+    CHECK(e.code() == RFG_ECUDA);  // no device: fail loudly, no CPU fallback
+    std::printf("adapter_test: no GPU (%s)\n", e.what());
+  }
+  return failures ? 1 : 0;
+}
