@@ -182,6 +182,18 @@ int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]);
 /* The pipeline's stream (cudaStream_t) for event timing by the caller. */
 void* rfg_pipeline_stream(rfg_pipeline* p);
 
+/* --------------------------------------------- multi-GPU composition */
+/* Per-pixel nearest-hit composition of spatially sharded renders
+ * (SURVEY.md §8(e)).  keys_dev[i] = (float bits of the hit's camera z) << 32
+ * | rank for a hit pixel, INT64_MAX for a miss; after an all-reduce MIN of
+ * the keys, rfg_compose_select zeroes every pixel this rank did not win (rank
+ * 0 keeps the invalid marker on pixels nobody hit), so an all-reduce SUM of
+ * the three maps yields the composed render exactly. */
+int rfg_compose_keys(const float* points_dev, const float pose34[12], int rank, int n, int64_t* keys_dev,
+                     void* cuda_stream);
+int rfg_compose_select(const int64_t* keymin_dev, int rank, int n, float* raycast_dev, float* points_dev,
+                       float* normals_dev, void* cuda_stream);
+
 /* --------------------------------------------------------------- export */
 uint32_t rfg_total_entries(const rfg_map* map);
 /* Host copies for parity: entries as 5 int32 {x, y, z, offset, ptr}

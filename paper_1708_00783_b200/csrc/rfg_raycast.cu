@@ -146,7 +146,7 @@ struct FieldReader {
     const int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
     const float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
-    uint32_t w[8];
+    float sdf = 0.f;
     if (lx < 7 && ly < 7 && lz < 7) {
       const int ptr = ptr_of(bx >> 3, by >> 3, bz >> 3);
       if (ptr < 0) {
@@ -154,9 +154,18 @@ struct FieldReader {
         return 1.f;
       }
       const uint32_t* base = vba + (size_t)ptr * kBlock3 + (lx | (ly << 3) | (lz << 6));
+      uint32_t w[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) w[k] = __ldg(base + ((k & 1) | ((k & 2) << 2) | ((k & 4) << 4)));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float bw =
+            ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+        sdf += bw * sdf_to_logical(vox_sdf(w[k]));
+      }
     } else {
+      // the cell straddles blocks: per-corner lookups; accumulating as we go
+      // is equivalent because a missing corner discards the sum
 #pragma unroll 1
       for (int k = 0; k < 8; ++k) {
         const int cx = bx + (k & 1), cy = by + ((k >> 1) & 1), cz = bz + ((k >> 2) & 1);
@@ -165,14 +174,11 @@ struct FieldReader {
           ok = false;
           return 1.f;
         }
-        w[k] = __ldg(vba + (size_t)ptr * kBlock3 + ((cx & 7) | ((cy & 7) << 3) | ((cz & 7) << 6)));
+        const uint32_t w = __ldg(vba + (size_t)ptr * kBlock3 + ((cx & 7) | ((cy & 7) << 3) | ((cz & 7) << 6)));
+        const float bw =
+            ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+        sdf += bw * sdf_to_logical(vox_sdf(w));
       }
-    }
-    float sdf = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float bw = ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
-      sdf += bw * sdf_to_logical(vox_sdf(w[k]));
     }
     ok = true;
     return sdf;
@@ -309,3 +315,65 @@ cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* 
 }
 
 }  // namespace rfg
+
+// ------------------------------------------------ multi-GPU composition
+namespace rfg {
+
+__global__ void k_compose_keys(const float4* __restrict__ points, Pose12 pose, int rank, int n,
+                               long long* __restrict__ keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 p = points[i];
+  long long k = 0x7fffffffffffffffLL;
+  if (p.w > 0.f) {
+    const Pose P = pose_from12(pose.v);
+    const float z = pose_apply(P, f3{p.x, p.y, p.z}).z;  // camera depth of the hit (> 0)
+    k = ((long long)(uint32_t)__float_as_int(fmaxf(z, 0.f)) << 32) | (long long)(uint32_t)rank;
+  }
+  keys[i] = k;
+}
+
+__global__ void k_compose_select(const long long* __restrict__ keymin, int rank, int n, float4* raycast,
+                                 float4* points, float4* normals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long k = keymin[i];
+  const bool nobody = k == 0x7fffffffffffffffLL;
+  const bool mine = !nobody && (int)(k & 0xffffffffLL) == rank;
+  if (mine) return;
+  const float4 inval = make_float4(0.f, 0.f, 0.f, (nobody && rank == 0) ? -1.f : 0.f);
+  if (raycast) raycast[i] = inval;
+  points[i] = inval;
+  normals[i] = inval;
+}
+
+}  // namespace rfg
+
+extern "C" int rfg_compose_keys(const float* points, const float pose34[12], int rank, int n, int64_t* keys,
+                                void* stream) {
+  if (!points || !pose34 || !keys || n < 0 || rank < 0) {
+    rfg::set_error("rfg_compose_keys: invalid argument");
+    return RFG_EINVAL;
+  }
+  rfg::Pose12 p;
+  for (int i = 0; i < 12; ++i) p.v[i] = pose34[i];
+  rfg::k_compose_keys<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(points), p, rank, n, reinterpret_cast<long long*>(keys));
+  rfg::count_launch();
+  RFG_CK(cudaGetLastError());
+  return RFG_OK;
+}
+
+extern "C" int rfg_compose_select(const int64_t* keymin, int rank, int n, float* raycast, float* points,
+                                  float* normals, void* stream) {
+  if (!keymin || !points || !normals || n < 0 || rank < 0) {
+    rfg::set_error("rfg_compose_select: invalid argument");
+    return RFG_EINVAL;
+  }
+  rfg::k_compose_select<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const long long*>(keymin), rank, n, reinterpret_cast<float4*>(raycast),
+      reinterpret_cast<float4*>(points), reinterpret_cast<float4*>(normals));
+  rfg::count_launch();
+  RFG_CK(cudaGetLastError());
+  return RFG_OK;
+}

@@ -1,0 +1,115 @@
+"""Multi-GPU spatial sharding of the voxel-hash space.
+
+One process per GPU (torch.distributed, NCCL over NVLink).  Each rank keeps a
+full-size hash table but allocates and integrates only the blocks it owns
+plus a 1-block halo (owner = hash of the block's 8^3-block super-tile mod
+world; the filter runs inside k_alloc_stage1, rfg_map_set_shard).  Every rank
+renders its shard; the ICP maps are then composed by a per-pixel nearest-hit
+reduction — the only data-path exchange:
+
+  keys = (float bits of hit camera-z) << 32 | rank   (rfg_compose_keys)
+  all_reduce(keys, MIN)                              (NCCL, 2.46 MB @ 640x480)
+  zero every pixel this rank did not win             (rfg_compose_select)
+  all_reduce(raycast | points | normals, SUM)        (NCCL, 14.7 MB; exact —
+                                                      one nonzero term per pixel)
+
+The ICP tracker then runs replicated on the composed maps, so tracking needs
+no per-iteration collective and every rank ends the frame with the same pose.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import fusion as F
+from ._lib import check, lib
+
+
+class Composer:
+    """Nearest-hit composition of per-rank ICP maps (device kernels + NCCL)."""
+
+    def __init__(self, rank: int, world: int, keys_fn=None, select_fn=None):
+        self.rank, self.world = rank, world
+        self.keys_fn = keys_fn or self._keys_gpu
+        self.select_fn = select_fn or self._select_gpu
+
+    def _keys_gpu(self, points: torch.Tensor, pose: np.ndarray) -> torch.Tensor:
+        n = points.numel() // 4
+        keys = torch.empty(n, dtype=torch.int64, device=points.device)
+        p = np.ascontiguousarray(pose, np.float32)
+        check(lib().rfg_compose_keys(C.c_void_p(points.data_ptr()), p.ctypes.data_as(C.POINTER(C.c_float)),
+                                     self.rank, n, C.c_void_p(keys.data_ptr()),
+                                     C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return keys
+
+    def _select_gpu(self, keymin: torch.Tensor, raycast, points, normals):
+        n = keymin.numel()
+        check(lib().rfg_compose_select(C.c_void_p(keymin.data_ptr()), self.rank, n, C.c_void_p(raycast.data_ptr()),
+                                       C.c_void_p(points.data_ptr()), C.c_void_p(normals.data_ptr()),
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+    def compose(self, pose: np.ndarray, raycast: torch.Tensor, points: torch.Tensor, normals: torch.Tensor):
+        """In place: after the call every rank holds the composed maps."""
+        keys = self.keys_fn(points, pose)
+        dist.all_reduce(keys, op=dist.ReduceOp.MIN)
+        self.select_fn(keys, raycast, points, normals)
+        maps = torch.stack([raycast, points, normals])  # one collective for the three maps
+        dist.all_reduce(maps, op=dist.ReduceOp.SUM)
+        raycast.copy_(maps[0])
+        points.copy_(maps[1])
+        normals.copy_(maps[2])
+        return keys
+
+
+class ShardedPipeline:
+    """Per-frame driver for one rank of a spatially sharded map:
+    build_view -> [replicated ICP on the composed maps] -> allocate ->
+    integrate -> expected ranges -> raycast -> nearest-hit composition."""
+
+    def __init__(self, map: F.VoxelBlockMap, intr: F.Intrinsics, params: F.SceneParams, rank: int, world: int,
+                 levels: int = 3, iters=(6, 10, 20), dist=(0.01, 0.02, 0.04),
+                 affine: F.DepthAffine = F.DepthAffine(1.0 / 5000.0, 0.0), min_count: int = 10):
+        self.map, self.intr, self.params = map, intr, params
+        self.rank, self.world = rank, world
+        self.levels, self.iters, self.dist, self.min_count = levels, iters, dist, min_count
+        self.calib = F.RgbdCalib(intrinsics_rgb=intr, intrinsics_d=intr, depth_affine=affine)
+        self.engine = F.FusionEngine()
+        self.state = F.RenderState()
+        self.composer = Composer(rank, world)
+        self._stream = torch.cuda.Stream()
+        self.reset()
+
+    @property
+    def stream(self) -> int:
+        return self._stream.cuda_stream
+
+    def reset(self):
+        self.pose = np.eye(3, 4, dtype=np.float32)
+        self.frames = 0
+        self.last_stats = F.AllocationStats()
+        self.last_icp = np.zeros(8)
+        self.state = F.RenderState()
+
+    def process(self, raw, pose=None):
+        with torch.cuda.stream(self._stream):
+            if pose is not None:
+                self.pose = np.asarray(pose, np.float32).reshape(3, 4).copy()
+            view = F.build_view(raw if torch.is_tensor(raw) else np.asarray(raw), None, self.calib, self.levels)
+            if self.frames > 0 and self.state.hasRaycast:
+                self.pose, summ = F.track_depth(self.map, view, self.state, self.pose, self.iters, self.dist,
+                                                self.min_count)
+                self.last_icp = np.array([summ.iterations, summ.count, summ.residual_sum, summ.converged,
+                                          *summ.per_level, summ.ok], np.float64)
+            self.last_stats = self.engine.allocate_from_depth(self.map, view, self.pose, self.params)
+            self.engine.integrate_frame(self.map, view, self.pose, self.params)
+            F.render_expected_ranges(self.map, self.pose, self.intr, self.params, self.state)
+            F.render_maps(self.map, self.pose, self.intr, self.params, F.RenderMode.kIcpMaps, self.state)
+            self.composer.compose(self.pose, self.state.raycastResult, self.state.points, self.state.normals)
+        self.frames += 1
+
+    def result(self):
+        torch.cuda.synchronize()
+        return self.last_stats, self.pose.copy(), self.last_icp
