@@ -101,8 +101,8 @@ struct FieldReader {
   uint32_t buckets;
   BlockCache cache;
 
-  __device__ __forceinline__ int ptr_of(int bx, int by, int bz) {
-    if (cache.bx == bx && cache.by == by && cache.bz == bz) return cache.ptr;
+  // findEntry + ptr (voxel_block_map.cpp:26-34,63-72), uncached
+  __device__ __forceinline__ int lookup(int bx, int by, int bz) const {
     int ptr = -1;
     if (bx >= -32768 && bx <= 32767 && by >= -32768 && by <= 32767 && bz >= -32768 && bz <= 32767) {
       int idx = (int)hash_index(bx, by, bz, buckets - 1);
@@ -117,10 +117,15 @@ struct FieldReader {
         idx = (int)buckets + e.z - 1;
       }
     }
+    return ptr >= 0 ? ptr : -1;
+  }
+
+  __device__ __forceinline__ int ptr_of(int bx, int by, int bz) {
+    if (cache.bx == bx && cache.by == by && cache.bz == bz) return cache.ptr;
     cache.bx = bx;
     cache.by = by;
     cache.bz = bz;
-    cache.ptr = ptr >= 0 ? ptr : -1;
+    cache.ptr = lookup(bx, by, bz);
     return cache.ptr;
   }
 
@@ -139,46 +144,48 @@ struct FieldReader {
   }
   // readSdfWeightTrilinear (voxel_block_map.cpp:130-156).  Any missing
   // corner invalidates the read, so the corner order only matters for the
-  // weighted sum, which is accumulated in the reference's k order.  When the
-  // 2x2x2 cell lies inside one block (the common case) a single lookup feeds
-  // eight independent loads.
-  __device__ __noinline__ float trilinear(f3 p, bool& ok) {
+  // weighted sum, which is accumulated in the reference's k order.  Each
+  // distinct block of the 2x2x2 cell is resolved once (1 lookup when the cell
+  // is inside a block, 2 when it straddles one face, ...), through the
+  // last-block cache for the base block, then the 8 voxel loads are issued
+  // independently.
+  __device__ __forceinline__ float trilinear(f3 p, bool& ok) {
     const int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
     const float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
+    const bool cx = lx == 7, cy = ly == 7, cz = lz == 7;  // cell crosses into the next block along x/y/z
+    const int bx0 = bx >> 3, by0 = by >> 3, bz0 = bz >> 3;
+    const int q0 = ptr_of(bx0, by0, bz0);
+    int qx = q0, qy = q0, qz = q0;
+    if (cx) qx = lookup(bx0 + 1, by0, bz0);
+    if (cy) qy = lookup(bx0, by0 + 1, bz0);
+    if (cz) qz = lookup(bx0, by0, bz0 + 1);
+    int qxy = cx ? qx : qy, qxz = cx ? qx : qz, qyz = cy ? qy : qz;
+    if (cx && cy) qxy = lookup(bx0 + 1, by0 + 1, bz0);
+    if (cx && cz) qxz = lookup(bx0 + 1, by0, bz0 + 1);
+    if (cy && cz) qyz = lookup(bx0, by0 + 1, bz0 + 1);
+    int qxyz = !cz ? qxy : (!cy ? qxz : (!cx ? qyz : lookup(bx0 + 1, by0 + 1, bz0 + 1)));
+    if ((q0 | qx | qy | qz | qxy | qxz | qyz | qxyz) < 0) {
+      ok = false;
+      return 1.f;
+    }
+    const int ox0 = lx, ox1 = (lx + 1) & 7, oy0 = ly << 3, oy1 = ((ly + 1) & 7) << 3, oz0 = lz << 6,
+              oz1 = ((lz + 1) & 7) << 6;
+    uint32_t w[8];
+    w[0] = __ldg(vba + (size_t)q0 * kBlock3 + (ox0 | oy0 | oz0));
+    w[1] = __ldg(vba + (size_t)qx * kBlock3 + (ox1 | oy0 | oz0));
+    w[2] = __ldg(vba + (size_t)qy * kBlock3 + (ox0 | oy1 | oz0));
+    w[3] = __ldg(vba + (size_t)qxy * kBlock3 + (ox1 | oy1 | oz0));
+    w[4] = __ldg(vba + (size_t)qz * kBlock3 + (ox0 | oy0 | oz1));
+    w[5] = __ldg(vba + (size_t)qxz * kBlock3 + (ox1 | oy0 | oz1));
+    w[6] = __ldg(vba + (size_t)qyz * kBlock3 + (ox0 | oy1 | oz1));
+    w[7] = __ldg(vba + (size_t)qxyz * kBlock3 + (ox1 | oy1 | oz1));
     float sdf = 0.f;
-    if (lx < 7 && ly < 7 && lz < 7) {
-      const int ptr = ptr_of(bx >> 3, by >> 3, bz >> 3);
-      if (ptr < 0) {
-        ok = false;
-        return 1.f;
-      }
-      const uint32_t* base = vba + (size_t)ptr * kBlock3 + (lx | (ly << 3) | (lz << 6));
-      uint32_t w[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) w[k] = __ldg(base + ((k & 1) | ((k & 2) << 2) | ((k & 4) << 4)));
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float bw =
-            ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
-        sdf += bw * sdf_to_logical(vox_sdf(w[k]));
-      }
-    } else {
-      // the cell straddles blocks: per-corner lookups; accumulating as we go
-      // is equivalent because a missing corner discards the sum
-#pragma unroll 1
-      for (int k = 0; k < 8; ++k) {
-        const int cx = bx + (k & 1), cy = by + ((k >> 1) & 1), cz = bz + ((k >> 2) & 1);
-        const int ptr = ptr_of(cx >> 3, cy >> 3, cz >> 3);
-        if (ptr < 0) {
-          ok = false;
-          return 1.f;
-        }
-        const uint32_t w = __ldg(vba + (size_t)ptr * kBlock3 + ((cx & 7) | ((cy & 7) << 3) | ((cz & 7) << 6)));
-        const float bw =
-            ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
-        sdf += bw * sdf_to_logical(vox_sdf(w));
-      }
+    for (int k = 0; k < 8; ++k) {
+      const float bw =
+          ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+      sdf += bw * sdf_to_logical(vox_sdf(w[k]));
     }
     ok = true;
     return sdf;
@@ -240,15 +247,32 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
 
 // field_normal (raycast.hpp:137-153)
 __device__ __forceinline__ bool field_normal(FieldReader& field, f3 h, f3* n) {
-  bool ok[6];
-  f3 g;
-  g.x = field.trilinear(f3{h.x + 1.f, h.y + 0.f, h.z + 0.f}, ok[0]) -
-        field.trilinear(f3{h.x - 1.f, h.y - 0.f, h.z - 0.f}, ok[1]);
-  g.y = field.trilinear(f3{h.x + 0.f, h.y + 1.f, h.z + 0.f}, ok[2]) -
-        field.trilinear(f3{h.x - 0.f, h.y - 1.f, h.z - 0.f}, ok[3]);
-  g.z = field.trilinear(f3{h.x + 0.f, h.y + 0.f, h.z + 1.f}, ok[4]) -
-        field.trilinear(f3{h.x - 0.f, h.y - 0.f, h.z - 1.f}, ok[5]);
-  if (!(ok[0] && ok[1] && ok[2] && ok[3] && ok[4] && ok[5])) return false;
+  // six reads at hit +/- one voxel per axis, as (h + (1,0,0)), (h - (1,0,0)),
+  // ... (the +0.f / -0.f components are kept: they are the reference's ops).
+  // One rolled loop keeps a single inlined copy of the trilinear read; any
+  // invalid read makes the normal invalid, so the loop may stop early.
+  f3 g{0.f, 0.f, 0.f};
+  float plus = 0.f;
+#pragma unroll 1
+  for (int d = 0; d < 6; ++d) {
+    const int ax = d >> 1;
+    const float ex = ax == 0 ? 1.f : 0.f, ey = ax == 1 ? 1.f : 0.f, ez = ax == 2 ? 1.f : 0.f;
+    const f3 q = (d & 1) ? f3{h.x - ex, h.y - ey, h.z - ez} : f3{h.x + ex, h.y + ey, h.z + ez};
+    bool ok = false;
+    const float v = field.trilinear(q, ok);
+    if (!ok) return false;
+    if (!(d & 1)) {
+      plus = v;
+    } else {
+      const float gd = plus - v;
+      if (ax == 0)
+        g.x = gd;
+      else if (ax == 1)
+        g.y = gd;
+      else
+        g.z = gd;
+    }
+  }
   const float len = sqrtf(sqnorm3(g));
   if (len < 1e-12f) return false;
   *n = f3{g.x / len, g.y / len, g.z / len};
