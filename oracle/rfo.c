@@ -944,7 +944,10 @@ int rfo_solve6(const double* acc29, double* x) {
       A[b * 6 + a] = acc29[k];
       ++k;
     }
+  /* Cholesky with the reciprocal of each pivot taken once (6 divisions instead
+   * of 33 — the GPU solver, rfg_icp.cu:solve6, runs the identical sequence) */
   double L[36] = {0};
+  double inv[6];
   double det = 1.0;
   for (int j = 0; j < 6; ++j) {
     double s = A[j * 6 + j];
@@ -953,10 +956,11 @@ int rfo_solve6(const double* acc29, double* x) {
     det *= s;
     double ljj = sqrt(s);
     L[j * 6 + j] = ljj;
+    inv[j] = 1.0 / ljj;
     for (int i = j + 1; i < 6; ++i) {
       double t = A[i * 6 + j];
       for (int p = 0; p < j; ++p) t -= L[i * 6 + p] * L[j * 6 + p];
-      L[i * 6 + j] = t / ljj;
+      L[i * 6 + j] = t * inv[j];
     }
   }
   if (det < 1e-12) return -1; /* SPEC.md:352 degenerate Hessian */
@@ -964,12 +968,12 @@ int rfo_solve6(const double* acc29, double* x) {
   for (int i = 0; i < 6; ++i) {
     double t = -acc29[21 + i];
     for (int p = 0; p < i; ++p) t -= L[i * 6 + p] * yv[p];
-    yv[i] = t / L[i * 6 + i];
+    yv[i] = t * inv[i];
   }
   for (int i = 5; i >= 0; --i) {
     double t = yv[i];
     for (int p = i + 1; p < 6; ++p) t -= L[p * 6 + i] * x[p];
-    x[i] = t / L[i * 6 + i];
+    x[i] = t * inv[i];
   }
   return 0;
 }

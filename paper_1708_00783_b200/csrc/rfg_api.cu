@@ -99,6 +99,30 @@ __global__ void k_export_entries(const int4* e, int* out5, int n) {
   }
 }
 
+constexpr int kBinCap = 2048;  // blocks per 32x32 screen tile before the overflow path
+
+int ensure_range_scratch(rfg_map* m, int width, int height) {
+  DevMap& d = m->d;
+  const int tx = (width + kRangeTilePx - 1) / kRangeTilePx, ty = (height + kRangeTilePx - 1) / kRangeTilePx;
+  if (d.bins && d.binTilesX == tx && d.binTilesY >= ty) return RFG_OK;
+  RFG_CK(cudaStreamSynchronize(m->stream));
+  if (d.bins) cudaFree(d.bins);
+  if (d.binCount) cudaFree(d.binCount);
+  d.bins = nullptr;
+  d.binCount = nullptr;
+  if (cudaMalloc(&d.bins, (size_t)tx * ty * kBinCap * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&d.binCount, (size_t)tx * ty * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("range scratch allocation failed");
+    return RFG_ENOMEM;
+  }
+  RFG_CK(cudaMemset(d.binCount, 0, (size_t)tx * ty * sizeof(int)));
+  d.binTilesX = tx;
+  d.binTilesY = ty;
+  d.binCap = kBinCap;
+  return RFG_OK;
+}
+
 }  // namespace rfg
 
 using namespace rfg;
@@ -178,6 +202,7 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
             alloc((void**)&d.reqKey, padded * sizeof(uint32_t)) && alloc((void**)&d.marked, padded) &&
             alloc((void**)&d.state, sizeof(MapState)) && alloc((void**)&d.tileCounts, d.nTiles * sizeof(int2)) &&
             alloc((void**)&d.tilePrefix, (d.nTiles + 1) * sizeof(int2)) &&
+            alloc((void**)&d.rangeBounds, padded * sizeof(int4)) &&
             alloc((void**)&m->icpPartials, (size_t)icp_partial_slots() * 29 * sizeof(double)) &&
             alloc((void**)&m->icpOut, icp_state_bytes()) && alloc((void**)&m->icpPose, 64 * sizeof(float));
   if (ok && cudaMallocHost((void**)&m->hostState, sizeof(MapState)) != cudaSuccess) {
@@ -204,7 +229,7 @@ int rfg_map_destroy(rfg_map* m) {
   DevMap& d = m->d;
   void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
                   d.visibility, d.reqKey, d.marked,     d.state,          d.tileCounts, d.tilePrefix,
-                  m->icpPartials, m->icpOut, m->icpPose};
+                  m->icpPartials, m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->hostState) cudaFreeHost(m->hostState);
@@ -285,6 +310,8 @@ int rfg_render_expected_ranges(rfg_map* m, const float pose34[12], const rfg_int
   RFG_REQUIRE(m && pose34 && range, "null argument");
   RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
   const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  const int rc = ensure_range_scratch(m, intr->width, intr->height);
+  if (rc != RFG_OK) return rc;
   RFG_CK(launch_ranges(m->d, fa, reinterpret_cast<float2*>(range), m->stream));
   return RFG_OK;
 }
@@ -550,6 +577,10 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
     return RFG_ECUDA;
   }
   m->stream = p->stream;
+  if (ensure_range_scratch(m, cfg->intr.width, cfg->intr.height) != RFG_OK) {
+    rfg_pipeline_destroy(p);
+    return RFG_ENOMEM;
+  }
   const int rc = rfg_pipeline_reset(p);
   if (rc != RFG_OK) {
     rfg_pipeline_destroy(p);

@@ -123,32 +123,43 @@ __device__ int solve6(const double* acc, double* x) {
       ++k;
     }
   double L[36];
+#pragma unroll
   for (int i = 0; i < 36; ++i) L[i] = 0.0;
+  double inv[6];
   double det = 1.0;
+#pragma unroll
   for (int j = 0; j < 6; ++j) {
     double s = A[j * 6 + j];
+#pragma unroll
     for (int p = 0; p < j; ++p) s -= L[j * 6 + p] * L[j * 6 + p];
     if (!(s > 0.0)) return -1;
     det *= s;
     const double ljj = sqrt(s);
     L[j * 6 + j] = ljj;
+    inv[j] = 1.0 / ljj;
+#pragma unroll
     for (int i = j + 1; i < 6; ++i) {
       double t = A[i * 6 + j];
+#pragma unroll
       for (int p = 0; p < j; ++p) t -= L[i * 6 + p] * L[j * 6 + p];
-      L[i * 6 + j] = t / ljj;
+      L[i * 6 + j] = t * inv[j];
     }
   }
   if (det < 1e-12) return -1;
   double yv[6];
+#pragma unroll
   for (int i = 0; i < 6; ++i) {
     double t = -acc[21 + i];
+#pragma unroll
     for (int p = 0; p < i; ++p) t -= L[i * 6 + p] * yv[p];
-    yv[i] = t / L[i * 6 + i];
+    yv[i] = t * inv[i];
   }
+#pragma unroll
   for (int i = 5; i >= 0; --i) {
     double t = yv[i];
+#pragma unroll
     for (int p = i + 1; p < 6; ++p) t -= L[p * 6 + i] * x[p];
-    x[i] = t / L[i * 6 + i];
+    x[i] = t * inv[i];
   }
   return 0;
 }
@@ -181,7 +192,8 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
     cb = 0.5;
     cc = 1.0 / 6.0;
   } else {
-    const double s = sin(theta), co = cos(theta);
+    double s, co;
+    sincos(theta, &s, &co);
     ca = s / theta;
     cb = (1.0 - co) / (theta * theta);
     cc = (theta - s) / (theta * theta * theta);
@@ -287,8 +299,16 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
     // every CTA: fixed-order final sum (warp w owns sums w, w+16; lanes
     // stride the CTAs; shuffle tree) and the identical solve
     for (int k = wid; k < 29; k += kIcpThreads / 32) {
+      // issue all of this lane's loads before the dependent adds
+      double v[kIcpMaxCtas / 32];
+#pragma unroll
+      for (int j = 0; j < kIcpMaxCtas / 32; ++j) {
+        const int c = lane + 32 * j;
+        v[j] = c < (int)gridDim.x ? __ldcg(part + c * 29 + k) : 0.0;
+      }
       double s = 0.0;
-      for (int c = lane; c < (int)gridDim.x; c += 32) s += __ldcg(part + c * 29 + k);
+#pragma unroll
+      for (int j = 0; j < kIcpMaxCtas / 32; ++j) s += v[j];
       s = warp_sum(s);
       if (lane == 0) g.sums[k] = s;
     }

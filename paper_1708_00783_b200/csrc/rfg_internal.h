@@ -43,6 +43,11 @@ struct DevMap {
   int2* tilePrefix;        // exclusive prefix (+ total at [nTiles])
   int nTiles;
   int rank, world, tileShift;  // shard filter
+  // expected-range scratch (screen-tile bins), sized for the image in use
+  int4* rangeBounds;       // per visible block: packed pixel rectangle + z span
+  int* binCount;           // per 32x32 screen tile
+  int* bins;               // binTilesX * binTilesY * binCap block indices
+  int binTilesX, binTilesY, binCap;
 };
 
 // Per-call frame arguments (camera, scene params, pose).
@@ -61,6 +66,7 @@ struct Pose12 {
   float v[12];
 };
 
+constexpr int kRangeTilePx = 16;     // expected-range screen tile edge (pixels)
 constexpr int kTile = 4096;          // hash entries per scan tile
 constexpr int kTileThreads = 256;    // 16 entries per thread
 
@@ -76,6 +82,9 @@ cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs
 cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint8_t* rgb, const FrameArgs& fa,
                              const rfg_intrinsics* intrRgb, const float* extr34, cudaStream_t s);
 cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s);
+// (Re)allocate the expected-range bins for a width x height image (host call,
+// not capturable; done at pipeline creation or on first use of a size).
+int ensure_range_scratch(struct ::rfg_map* m, int width, int height);
 cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* range, float4* raycast,
                             float4* points, float4* normals, cudaStream_t s);
 cudaError_t launch_build_view(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,

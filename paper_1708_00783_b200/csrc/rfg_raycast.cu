@@ -11,19 +11,27 @@ __device__ __forceinline__ Pose load_pose_r(const FrameArgs& fa) {
 }
 
 // ------------------------------------------------------ expected ranges
-__global__ void k_range_clear(float2* range, int n) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) range[i] = make_float2(FLT_MAX, -1.f);
+// The reference covers each visible block's projected pixel rectangle with
+// 16x16 fragments (count -> prefix sum -> emit, raycast.cpp:94-115) and
+// min/max-merges every fragment into the range image (:118-126).  Min/max is
+// exact and commutative, so any partition of the same rectangles gives the
+// identical image.  Here the partition is by SCREEN tile instead of by block:
+//   k_range_bin  — warp per visible block: lanes 0-7 project the corners
+//                  (projectBlock, raycast.cpp:38-71), the warp reduces the
+//                  rectangle and clipped z span, writes the block's bounds,
+//                  and appends the block to every 32x32-pixel screen tile its
+//                  rectangle touches (fixed-capacity bins);
+//   k_range_tile — one CTA per screen tile, one thread per pixel: min/max over
+//                  the tile's bin in registers, one store per pixel, no
+//                  per-pixel atomics.  A tile whose bin overflowed scans the
+//                  bounds of every visible block instead (same result).
+constexpr int kRangeTile = kRangeTilePx;
+
+__device__ __forceinline__ int4 pack_bounds(int x0, int y0, int x1, int y1, float lo, float hi) {
+  return make_int4(x0 | (y0 << 16), x1 | (y1 << 16), __float_as_int(lo), __float_as_int(hi));
 }
 
-// One warp per visible block: lanes 0-7 project the 8 corners (projectBlock,
-// raycast.cpp:38-71), the warp reduces the pixel rectangle and z span, then
-// min/max-merges the rectangle into the range image.  The reference splits
-// the rectangle into 16x16 fragments (:99-115) only to parallelise this merge;
-// min/max is exact and commutative, so the result is identical.  Positive
-// floats order like their int bit patterns, so the merges are integer
-// atomicMin/atomicMax on the bits (z values are > 0; unset max is -1).
-__global__ void __launch_bounds__(256) k_range_blocks(DevMap m, FrameArgs fa, float2* range) {
+__global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa) {
   const int lane = threadIdx.x & 31;
   const int warpsPerCta = blockDim.x >> 5;
   const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
@@ -34,10 +42,9 @@ __global__ void __launch_bounds__(256) k_range_blocks(DevMap m, FrameArgs fa, fl
   for (int b = gw; b < nVis; b += nw) {
     const int idx = m.visibleList[b];
     const int4 e = ld_entry(m.entries, idx);
-    if (!entry_allocated(e)) continue;
     float x0 = FLT_MAX, y0 = FLT_MAX, x1 = -FLT_MAX, y1 = -FLT_MAX, zMin = FLT_MAX, zMax = 0.f;
     int valid = 0;
-    if (lane < 8) {
+    if (lane < 8 && entry_allocated(e)) {
       const int c = lane;
       const f3 corner{((float)entry_x(e) + (float)(c & 1)) * bs, ((float)entry_y(e) + (float)((c >> 1) & 1)) * bs,
                       ((float)entry_z(e) + (float)((c >> 2) & 1)) * bs};
@@ -64,7 +71,7 @@ __global__ void __launch_bounds__(256) k_range_blocks(DevMap m, FrameArgs fa, fl
       zMax = smax(zMax, __shfl_xor_sync(0xffffffffu, zMax, o));
       valid += __shfl_xor_sync(0xffffffffu, valid, o);
     }
-    // lane 0's values now hold the reduction over lanes 0-7
+    // lane 0 holds the reduction over lanes 0-7
     x0 = __shfl_sync(0xffffffffu, x0, 0);
     y0 = __shfl_sync(0xffffffffu, y0, 0);
     x1 = __shfl_sync(0xffffffffu, x1, 0);
@@ -72,23 +79,59 @@ __global__ void __launch_bounds__(256) k_range_blocks(DevMap m, FrameArgs fa, fl
     zMin = __shfl_sync(0xffffffffu, zMin, 0);
     zMax = __shfl_sync(0xffffffffu, zMax, 0);
     valid = __shfl_sync(0xffffffffu, valid, 0);
-    if (valid == 0) continue;
-    const int bx0 = max(0, (int)floorf(x0)), by0 = max(0, (int)floorf(y0));
-    const int bx1 = min(fa.w - 1, (int)ceilf(x1)), by1 = min(fa.h - 1, (int)ceilf(y1));
-    if (bx0 > bx1 || by0 > by1) continue;
-    const float zlo = smax(zMin, fa.vfMin), zhi = smin(zMax, fa.vfMax);
-    if (zlo > zhi) continue;
-    const int lo = __float_as_int(zlo), hi = __float_as_int(zhi);
-    const int rw = bx1 - bx0 + 1;
-    const int npx = rw * (by1 - by0 + 1);
-    for (int p = lane; p < npx; p += 32) {
-      const int x = bx0 + p % rw, y = by0 + p / rw;
-      int* r = reinterpret_cast<int*>(range + (size_t)y * fa.w + x);
-      const int2 cur = __ldcg(reinterpret_cast<const int2*>(r));  // L2 value; stale reads only cost an extra atomic
-      if (lo < cur.x) atomicMin(r, lo);
-      if (hi > cur.y) atomicMax(r + 1, hi);
+    int bx0 = 1, by0 = 1, bx1 = 0, by1 = 0;  // empty rectangle unless valid
+    float zlo = 0.f, zhi = -1.f;
+    if (valid) {
+      bx0 = max(0, (int)floorf(x0));
+      by0 = max(0, (int)floorf(y0));
+      bx1 = min(fa.w - 1, (int)ceilf(x1));
+      by1 = min(fa.h - 1, (int)ceilf(y1));
+      zlo = smax(zMin, fa.vfMin);
+      zhi = smin(zMax, fa.vfMax);
+      if (bx0 > bx1 || by0 > by1 || zlo > zhi) {
+        bx0 = by0 = 1;
+        bx1 = by1 = 0;
+      }
+    }
+    if (lane == 0) m.rangeBounds[b] = pack_bounds(bx0, by0, bx1, by1, zlo, zhi);
+    if (bx0 > bx1) continue;
+    const int tx0 = bx0 / kRangeTile, tx1 = bx1 / kRangeTile, ty0 = by0 / kRangeTile, ty1 = by1 / kRangeTile;
+    const int ntx = tx1 - tx0 + 1, nt = ntx * (ty1 - ty0 + 1);
+    for (int k = lane; k < nt; k += 32) {
+      const int t = (ty0 + k / ntx) * m.binTilesX + tx0 + k % ntx;
+      const int slot = atomicAdd(&m.binCount[t], 1);
+      if (slot < m.binCap) m.bins[(size_t)t * m.binCap + slot] = b;
     }
   }
+}
+
+__global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m, FrameArgs fa, float2* range) {
+  __shared__ int4 sb[kRangeTile * kRangeTile];
+  const int t = blockIdx.y * m.binTilesX + blockIdx.x;
+  const int x = blockIdx.x * kRangeTile + (threadIdx.x & (kRangeTile - 1));
+  const int y = blockIdx.y * kRangeTile + threadIdx.x / kRangeTile;
+  const int count = m.binCount[t];
+  const bool overflow = count > m.binCap;
+  const int n = overflow ? *((volatile int*)&m.state->nVisible) : count;
+  int lo = __float_as_int(FLT_MAX), hi = __float_as_int(-1.f);  // unset: (FLT_MAX, -1)
+  for (int base = 0; base < n; base += kRangeTile * kRangeTile) {
+    const int i = base + threadIdx.x;
+    __syncthreads();
+    if (i < n) sb[threadIdx.x] = m.rangeBounds[overflow ? i : m.bins[(size_t)t * m.binCap + i]];
+    __syncthreads();
+    const int cnt = min(n - base, kRangeTile * kRangeTile);
+    for (int j = 0; j < cnt; ++j) {
+      const int4 bb = sb[j];
+      const int bx0 = bb.x & 0xFFFF, by0 = bb.x >> 16, bx1 = bb.y & 0xFFFF, by1 = bb.y >> 16;
+      if (x >= bx0 && x <= bx1 && y >= by0 && y <= by1) {
+        lo = min(lo, bb.z);  // positive floats order like their bit patterns
+        hi = max(hi, bb.w);  // -1.f (negative int) loses against any z > 0
+      }
+    }
+  }
+  if (x < fa.w && y < fa.h) range[(size_t)y * fa.w + x] = make_float2(__int_as_float(lo), __int_as_float(hi));
+  __syncthreads();
+  if (threadIdx.x == 0) m.binCount[t] = 0;  // ready for the next frame
 }
 
 // ------------------------------------------------------------ raycast
@@ -323,9 +366,10 @@ int range_grid() {
 }
 
 cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s) {
-  const int n = fa.w * fa.h;
-  k_range_clear<<<(n + 255) / 256, 256, 0, s>>>(range, n);
-  k_range_blocks<<<range_grid(), 256, 0, s>>>(m, fa, range);
+  const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
+  if (tx != m.binTilesX || ty > m.binTilesY) return cudaErrorInvalidValue;  // scratch sized by ensure_range_scratch
+  k_range_bin<<<range_grid(), 256, 0, s>>>(m, fa);
+  k_range_tile<<<dim3(tx, ty), kRangeTile * kRangeTile, 0, s>>>(m, fa, range);
   count_launch(2);
   return cudaGetLastError();
 }
