@@ -228,6 +228,10 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int2* counts, int2* prefix,
 }
 
 // --------------------------------------------------------------- stage 2
+// Tiles of kTile = 1024 hash entries, 4 consecutive entries per thread (one
+// 16-byte load of keys, one 4-byte load of flag bytes), so a tile's threads
+// cover it in ascending entry order and a CTA scan gives the serial ranks.
+
 // Count requests (and excess-linked requests) per tile.
 __global__ void __launch_bounds__(kTileThreads) k_req_count(DevMap m) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -237,22 +241,16 @@ __global__ void __launch_bounds__(kTileThreads) k_req_count(DevMap m) {
     st->succ = 0;
     st->succType2 = 0;
   }
-  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
   int n = 0, n2 = 0;
-  if (base < m.total) {
-    const uint4* kp = reinterpret_cast<const uint4*>(m.reqKey + base);
+  const uint4 k4 = *reinterpret_cast<const uint4*>(m.reqKey + base);  // padded: always in bounds
+  const uint32_t ks[4] = {k4.x, k4.y, k4.z, k4.w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 k4 = kp[q];
-      const uint32_t ks[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (ks[j]) {
-          ++n;
-          if (entry_allocated(ld_entry(m.entries, base + q * 4 + j))) ++n2;
-        }
+  for (int j = 0; j < 4; ++j)
+    if (ks[j]) {
+      ++n;
+      if (entry_allocated(ld_entry(m.entries, base + j))) ++n2;
     }
-  }
   int2 total;
   block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
   if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = total;
@@ -260,43 +258,32 @@ __global__ void __launch_bounds__(kTileThreads) k_req_count(DevMap m) {
 
 // Serve requests in ascending index order with serial-equivalent ranks.
 __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
-  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
-  uint32_t keys[16];
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
+  const uint4 k4 = *reinterpret_cast<const uint4*>(m.reqKey + base);
+  const uint32_t keys[4] = {k4.x, k4.y, k4.z, k4.w};
   int n = 0, n2 = 0;
   uint32_t isT2 = 0;
-  if (base < m.total) {
-    const uint4* kp = reinterpret_cast<const uint4*>(m.reqKey + base);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 k4 = kp[q];
-      keys[q * 4 + 0] = k4.x;
-      keys[q * 4 + 1] = k4.y;
-      keys[q * 4 + 2] = k4.z;
-      keys[q * 4 + 3] = k4.w;
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (keys[j]) {
-        ++n;
-        if (entry_allocated(ld_entry(m.entries, base + j))) {
-          ++n2;
-          isT2 |= 1u << j;
-        }
+  for (int j = 0; j < 4; ++j)
+    if (keys[j]) {
+      ++n;
+      if (entry_allocated(ld_entry(m.entries, base + j))) {
+        ++n2;
+        isT2 |= 1u << j;
       }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) keys[j] = 0;
-  }
+    }
   int2 total;
-  int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
+  const int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
   if (n == 0) return;
   const int2 tp = m.tilePrefix[blockIdx.x];
   int before = tp.x + ex.x, before2 = tp.y + ex.y;
   const int nB = m.state->snapFreeBlocks, nE = m.state->snapFreeExcess;
   const Pose camToWorld = pose_inverse(load_pose(fa));
   int succ = 0, succ2 = 0;
-  for (int j = 0; j < 16; ++j) {
-    if (!keys[j]) continue;
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t key = j == 0 ? keys[0] : (j == 1 ? keys[1] : (j == 2 ? keys[2] : keys[3]));
+    if (!key) continue;
     const int idx = (int)(base + j);
     const bool t2 = (isT2 >> j) & 1u;
     const int before1 = before - before2;
@@ -307,7 +294,7 @@ __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const flo
     ++before;
     if (t2) ++before2;
     if (!cand || rb >= nB) continue;
-    const i3 p = decode_request(keys[j], depth, fa, camToWorld);
+    const i3 p = decode_request(key, depth, fa, camToWorld);
     const int blockPtr = m.freeBlocks[nB - 1 - rb];
     if (!t2) {
       // free bucket slot (voxel_block_map.cpp:96-104)
@@ -333,7 +320,7 @@ __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const flo
 // proj/src/fusion.cpp:116-130
 __device__ __forceinline__ bool block_in_frustum(int bx, int by, int bz, const Pose& pose, const FrameArgs& fa) {
   const float bs = fa.voxelSize * (float)kBlock;
-#pragma unroll
+#pragma unroll 1
   for (int c = 0; c < 8; ++c) {
     const f3 corner{((float)bx + (float)(c & 1)) * bs, ((float)by + (float)((c >> 1) & 1)) * bs,
                     ((float)bz + (float)((c >> 2) & 1)) * bs};
@@ -346,7 +333,12 @@ __device__ __forceinline__ bool block_in_frustum(int bx, int by, int bz, const P
   return false;
 }
 
+// Candidates (this frame's marks | previous visibility bytes) of the tile are
+// queued in shared memory and frustum-tested one per thread, so the tests are
+// spread over the CTA whatever the hash distribution.
 __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs fa) {
+  __shared__ int queue[kTile];
+  __shared__ int nq, nvis;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // finalise stage 2 (all k_req_assign CTAs have completed)
     MapState* st = m.state;
@@ -356,51 +348,53 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
     st->stats[1] = st->succ;
     st->stats[2] = st->nRequests - st->succ;
   }
-  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
-  int n = 0;
-  if (base < m.total) {
-    uint4* mp = reinterpret_cast<uint4*>(m.marked + base);
-    uint4* vp = reinterpret_cast<uint4*>(m.visibility + base);
-    const uint4 mk = *mp;
-    const uint4 vk = *vp;
-    const uint32_t cand[4] = {mk.x | vk.x, mk.y | vk.y, mk.z | vk.z, mk.w | vk.w};
-    if (cand[0] | cand[1] | cand[2] | cand[3]) {
-      const Pose pose = load_pose(fa);
-      uint32_t out[4] = {0, 0, 0, 0};
-#pragma unroll 4
-      for (int j = 0; j < 16; ++j) {
-        if (!((cand[j >> 2] >> ((j & 3) * 8)) & 0xFFu)) continue;
-        const int4 e = ld_entry(m.entries, base + j);
-        if (!entry_allocated(e)) continue;
-        if (block_in_frustum(entry_x(e), entry_y(e), entry_z(e), pose, fa)) {
-          out[j >> 2] |= (e.w >= 0 ? 1u : 2u) << ((j & 3) * 8);
-          ++n;
-        }
-      }
-      *vp = make_uint4(out[0], out[1], out[2], out[3]);
-    }
-    if (mk.x | mk.y | mk.z | mk.w) *mp = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    nq = 0;
+    nvis = 0;
   }
-  int2 total;
-  block_exclusive_scan2<kTileThreads>(make_int2(n, 0), &total);
-  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = total;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
+  uint32_t* mp = reinterpret_cast<uint32_t*>(m.marked + base);
+  uint32_t* vp = reinterpret_cast<uint32_t*>(m.visibility + base);
+  const uint32_t mk = *mp, vk = *vp;
+  const uint32_t cand = mk | vk;
+  if (cand) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((cand >> (8 * j)) & 0xFFu) queue[atomicAdd(&nq, 1)] = (int)(base + j);
+    *vp = 0u;  // rewritten below for the candidates that stay visible
+  }
+  if (mk) *mp = 0u;
+  __syncthreads();
+  const Pose pose = load_pose(fa);
+  int n = 0;
+  for (int i = threadIdx.x; i < nq; i += kTileThreads) {
+    const int idx = queue[i];
+    const int4 e = ld_entry(m.entries, idx);
+    if (!entry_allocated(e)) continue;
+    if (block_in_frustum(entry_x(e), entry_y(e), entry_z(e), pose, fa)) {
+      m.visibility[idx] = e.w >= 0 ? 1 : 2;
+      ++n;
+    }
+  }
+  if (n) atomicAdd(&nvis, n);
+  __syncthreads();
+  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = make_int2(nvis, 0);
 }
 
 __global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
-  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 16;
-  uint4 v = make_uint4(0, 0, 0, 0);
-  if (base < m.total) v = *reinterpret_cast<const uint4*>(m.visibility + base);
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
+  const uint32_t w = *reinterpret_cast<const uint32_t*>(m.visibility + base);
   int n = 0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) n += ((w[j >> 2] >> ((j & 3) * 8)) & 0xFFu) ? 1 : 0;
+  for (int j = 0; j < 4; ++j) n += ((w >> (8 * j)) & 0xFFu) ? 1 : 0;
   int2 total;
-  int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, 0), &total);
+  const int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, 0), &total);
   if (n == 0) return;
   int o = m.tilePrefix[blockIdx.x].x + ex.x;
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if ((w[j >> 2] >> ((j & 3) * 8)) & 0xFFu) m.visibleList[o++] = (int)(base + j);
+  for (int j = 0; j < 4; ++j)
+    if ((w >> (8 * j)) & 0xFFu) m.visibleList[o++] = (int)(base + j);
 }
 
 cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s) {

@@ -39,7 +39,7 @@ struct DevMap {
   uint32_t* reqKey;        // total: stage-1 last-writer key (0 = no request)
   uint8_t* marked;         // total: stage-1/2 marks (0/1/2)
   MapState* state;
-  int2* tileCounts;        // per 4096-entry tile
+  int2* tileCounts;        // per kTile-entry tile
   int2* tilePrefix;        // exclusive prefix (+ total at [nTiles])
   int nTiles;
   int rank, world, tileShift;  // shard filter
@@ -67,8 +67,8 @@ struct Pose12 {
 };
 
 constexpr int kRangeTilePx = 16;     // expected-range screen tile edge (pixels)
-constexpr int kTile = 4096;          // hash entries per scan tile
-constexpr int kTileThreads = 256;    // 16 entries per thread
+constexpr int kTile = 1024;          // hash entries per scan tile
+constexpr int kTileThreads = 256;    // 4 consecutive entries per thread
 
 void set_error(const std::string& msg);
 extern std::atomic<uint64_t> g_launches;
