@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, con
   if (x >= fa.w || y >= fa.h) return;
   const size_t i = (size_t)y * fa.w + x;
   const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
-  float4 rc = invalid, pt = invalid, nm = invalid;
+  float4 rc = invalid, pt = invalid;
   const float2 r = range[i];
   if (r.y >= r.x) {
     const Pose c2w = pose_inverse(load_pose_r(fa));
@@ -345,12 +345,29 @@ __global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, con
     if (cast_ray(field, origin, dirW, r.x * norm, r.y * norm, fa.mu, fa.voxelSize, &hit)) {
       rc = make_float4(hit.x, hit.y, hit.z, 1.f);
       pt = make_float4(hit.x * fa.voxelSize, hit.y * fa.voxelSize, hit.z * fa.voxelSize, 1.f);
-      f3 n;
-      if (field_normal(field, hit, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
     }
   }
-  if (raycast) raycast[i] = rc;
+  raycast[i] = rc;
   points[i] = pt;
+}
+
+// field_normal (raycast.hpp:137-153) at every hit, in its own kernel: the
+// six trilinear reads are uniform work across the warp instead of running
+// behind the divergent march.
+__global__ void __launch_bounds__(128) k_raycast_normals(DevMap m, FrameArgs fa, const float4* __restrict__ raycast,
+                                                         float4* normals) {
+  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (x >= fa.w || y >= fa.h) return;
+  const size_t i = (size_t)y * fa.w + x;
+  const float4 r = raycast[i];
+  float4 nm = make_float4(0.f, 0.f, 0.f, -1.f);
+  if (r.w > 0.f) {
+    FieldReader field{m.entries, m.vbaDepth, m.buckets};
+    field.cache.reset();
+    f3 n;
+    if (field_normal(field, f3{r.x, r.y, r.z}, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
+  }
   normals[i] = nm;
 }
 
@@ -376,9 +393,11 @@ cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, c
 
 cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* range, float4* raycast,
                             float4* points, float4* normals, cudaStream_t s) {
+  if (!raycast) return cudaErrorInvalidValue;  // the normals pass reads the hits
   dim3 g((fa.w + 15) / 16, (fa.h + 7) / 8);
   k_raycast_icp<<<g, 128, 0, s>>>(m, fa, range, raycast, points, normals);
-  count_launch();
+  k_raycast_normals<<<g, 128, 0, s>>>(m, fa, raycast, normals);
+  count_launch(2);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,19 @@
+"""Exhaustive exactness checks of arithmetic shortcuts in the kernels."""
+import os
+import subprocess
+import tempfile
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_sdf_to_logical_fast_path_is_ieee_exact_for_all_int16():
+    src = os.path.join(ROOT, "tests", "cuda", "div32767.cu")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "div32767")
+        subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                        "-fmad=false", "-std=c++17", src, "-o", exe], check=True)
+        p = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+        assert p.returncode == 0 and "mismatches 0" in p.stdout, p.stdout + p.stderr
