@@ -117,6 +117,23 @@ int rfg_render_icp_maps(rfg_map* map, const float pose34[12], const rfg_intrinsi
                         const rfg_scene_params* params, const float* range_dev, float* raycast_dev, float* points_dev,
                         float* normals_dev);
 
+/* Approximate raycast (useApproximateRaycast).
+ * forward_project (proj/src/raycast.cpp:141-188): the previous raycastResult
+ * in raycast_dev is re-projected into new_pose34 (nearest point per pixel,
+ * ties keep the first in row-major source order); points are set for the
+ * forwarded pixels and normals left invalid, exactly as the reference.
+ * has_raycast = 0 (no previous raycast) marks every pixel missing.  The
+ * row-major linear indices (y * width + x) of the missing pixels go to
+ * missing_dev (capacity width*height) and their count to *n_missing_dev. */
+int rfg_forward_project(rfg_map* map, int has_raycast, float* raycast_dev, float* points_dev, float* normals_dev,
+                        const float new_pose34[12], const rfg_intrinsics* intr, float voxel_size, int32_t* missing_dev,
+                        int32_t* n_missing_dev);
+/* render_maps(kIcpMaps, missingOnly) (proj/include/rf/raycast.hpp:200-202):
+ * raycast only the listed pixels (device list and device count). */
+int rfg_render_icp_maps_list(rfg_map* map, const float pose34[12], const rfg_intrinsics* intr,
+                             const rfg_scene_params* params, const float* range_dev, const int32_t* missing_dev,
+                             const int32_t* n_missing_dev, float* raycast_dev, float* points_dev, float* normals_dev);
+
 /* ---------------------------------------------------------------- view */
 /* build_view depth path (proj/src/view.cpp:100-143): raw u16 -> metres
  * (m = raw*scale + offset, raw == 0 or m <= 0 -> -1) and `levels` pyramid

@@ -50,6 +50,8 @@ def lib():
         L.rr_render_ranges.argtypes = [C.c_void_p, _f, _i, _f, _f, _f, _d]
         L.rr_render_icp.argtypes = [C.c_void_p, _f, _i, _f, _f, _f, _f, _f, _d]
         L.rr_set_ranges.argtypes = [C.c_void_p, _i, _f, _f]
+        L.rr_forward_project.argtypes = [C.c_void_p, _f, _i, _f, C.c_float, _i]
+        L.rr_render_icp_missing.argtypes = [C.c_void_p, _f, _i, _f, _f, _i, C.c_int, _f, _f, _f]
         L.rr_total_entries.argtypes = [C.c_void_p]
         L.rr_total_entries.restype = C.c_uint32
         L.rr_export_entries.argtypes = [C.c_void_p, _i]
@@ -180,6 +182,26 @@ class RefEngine:
         lib().rr_render_icp(self.h, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(rc, _f), P(pts, _f),
                             P(nrm, _f), C.byref(ms))
         return rc, pts, nrm, ms.value
+
+    def forward_project(self, pose34, intr, voxel_size):
+        """forward_project (raycast.cpp:141-188): (N, 2) int32 missing (x, y)."""
+        out = np.zeros((intr["width"] * intr["height"], 2), np.int32)
+        pose = _f32(pose34)
+        wh, f4 = _wh(intr), _f4(intr)
+        n = lib().rr_forward_project(self.h, P(pose, _f), P(wh, _i), P(f4, _f), voxel_size, P(out, _i))
+        return out[:n].copy()
+
+    def render_icp_missing(self, pose34, intr, params, missing):
+        h, w = intr["height"], intr["width"]
+        rc = np.zeros((h, w, 4), np.float32)
+        pts = np.zeros((h, w, 4), np.float32)
+        nrm = np.zeros((h, w, 4), np.float32)
+        pose, pv = _f32(pose34), params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        ms = np.ascontiguousarray(missing, np.int32)
+        lib().rr_render_icp_missing(self.h, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(ms, _i), len(ms),
+                                    P(rc, _f), P(pts, _f), P(nrm, _f))
+        return rc, pts, nrm
 
     def entries(self):
         n = lib().rr_total_entries(self.h)

@@ -302,6 +302,38 @@ int rr_render_icp(void* h, const float* pose12, const int* wh, const float* f4, 
   return 0;
 }
 
+// forward_project (proj/src/raycast.cpp:141-188) on the engine's RenderState:
+// returns the number of missing pixels and writes them as (x, y) pairs.
+int rr_forward_project(void* h, const float* pose12, const int* wh, const float* f4, float voxelSize,
+                       int* missingXY) {
+  auto* e = static_cast<Engine*>(h);
+  const auto missing = forward_project(e->render, poseFrom12(pose12), intrFrom(wh, f4), voxelSize);
+  for (std::size_t i = 0; i < missing.size(); ++i) {
+    missingXY[2 * i] = missing[i].x();
+    missingXY[2 * i + 1] = missing[i].y();
+  }
+  return static_cast<int>(missing.size());
+}
+
+// render_maps(kIcpMaps, missingOnly) (raycast.hpp:200-202); outputs the full
+// state images afterwards.
+int rr_render_icp_missing(void* h, const float* pose12, const int* wh, const float* f4, const float* params,
+                          const int* missingXY, int n, float* raycastOut, float* pointsOut, float* normalsOut) {
+  auto* e = static_cast<Engine*>(h);
+  std::vector<Eigen::Vector2i> missing(n);
+  for (int i = 0; i < n; ++i) missing[i] = Eigen::Vector2i(missingXY[2 * i], missingXY[2 * i + 1]);
+  render_maps(e->map, poseFrom12(pose12), intrFrom(wh, f4), paramsFrom(params), RenderMode::kIcpMaps, e->render,
+              &missing);
+  const std::size_t np = e->render.points.size();
+  for (std::size_t i = 0; i < np; ++i)
+    for (int k = 0; k < 4; ++k) {
+      raycastOut[4 * i + k] = e->render.raycastResult.data()[i][k];
+      pointsOut[4 * i + k] = e->render.points.data()[i][k];
+      normalsOut[4 * i + k] = e->render.normals.data()[i][k];
+    }
+  return 0;
+}
+
 // Set the expected-range image directly (used to drive render_icp from a
 // range image produced elsewhere).
 int rr_set_ranges(void* h, const int* wh, const float* f4, const float* rangeIn) {

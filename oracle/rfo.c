@@ -780,6 +780,116 @@ int rfo_render_icp(rfo_map* m, const float* pose12, const int* wh, const float* 
   return 0;
 }
 
+/* render_maps(kIcpMaps, missingOnly) (raycast.hpp:200-202): doPixel for the
+ * listed (x, y) pixels only; the other pixels of the in/out images keep their
+ * values. */
+int rfo_render_icp_list(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
+                        const int* missingXY, int n, float* raycastOut, float* pointsOut, float* normalsOut) {
+  intr_t in = intr_from(wh, f4);
+  params_t s = params_from(params6);
+  pose_t pose = pose_from12(pose12);
+  pose_t c2w = pose_inverse(&pose);
+  v3 origin = {c2w.t[0], c2w.t[1], c2w.t[2]};
+  if (m->rangeW != in.w || m->rangeH != in.h) return -1;
+  for (int k = 0; k < n; ++k) {
+    const int x = missingXY[2 * k], y = missingXY[2 * k + 1];
+    size_t i = (size_t)y * in.w + x;
+    float* rc = raycastOut + 4 * i;
+    float* pt = pointsOut + 4 * i;
+    float* nm = normalsOut + 4 * i;
+    rc[0] = rc[1] = rc[2] = 0.f;
+    rc[3] = -1.f;
+    pt[0] = pt[1] = pt[2] = 0.f;
+    pt[3] = -1.f;
+    nm[0] = nm[1] = nm[2] = 0.f;
+    nm[3] = -1.f;
+    float r0 = m->range[2 * i], r1 = m->range[2 * i + 1];
+    if (!(r1 >= r0)) continue;
+    v3 dirCam = {((float)x - in.cx) / in.fx, ((float)y - in.cy) / in.fy, 1.f};
+    float norm = sqrtf(sqnorm3(dirCam));
+    v3 dw = rot_apply(c2w.R, dirCam);
+    v3 dirW = {dw.x / norm, dw.y / norm, dw.z / norm};
+    v3 hit;
+    if (!cast_ray(m, origin, dirW, r0 * norm, r1 * norm, s.mu, s.voxelSize, &hit)) continue;
+    rc[0] = hit.x;
+    rc[1] = hit.y;
+    rc[2] = hit.z;
+    rc[3] = 1.f;
+    pt[0] = hit.x * s.voxelSize;
+    pt[1] = hit.y * s.voxelSize;
+    pt[2] = hit.z * s.voxelSize;
+    pt[3] = 1.f;
+    v3 nrm;
+    if (field_normal(m, hit, &nrm)) {
+      nm[0] = nrm.x;
+      nm[1] = nrm.y;
+      nm[2] = nrm.z;
+      nm[3] = 1.f;
+    }
+  }
+  return 0;
+}
+
+/* forward_project (proj/src/raycast.cpp:141-188).  hasRaycast = 0: every
+ * pixel is missing.  Otherwise the previous raycastResult (in/out) is
+ * re-projected into newPose keeping the nearest point per pixel (strictly
+ * nearer replaces, so ties keep the first in row-major source order);
+ * points are set for the forwarded pixels, normals stay invalid.  Returns the
+ * number of missing pixels, written row-major as (x, y) pairs. */
+int rfo_forward_project(int hasRaycast, float* raycast, float* points, float* normals, const float* newPose12,
+                        const int* wh, const float* f4, float voxelSize, int* missingXY) {
+  intr_t in = intr_from(wh, f4);
+  const size_t n = (size_t)in.w * in.h;
+  int nm = 0;
+  if (!hasRaycast) {
+    for (int y = 0; y < in.h; ++y)
+      for (int x = 0; x < in.w; ++x) {
+        missingXY[2 * nm] = x;
+        missingXY[2 * nm + 1] = y;
+        ++nm;
+      }
+    return nm;
+  }
+  pose_t pose = pose_from12(newPose12);
+  float* prev = (float*)malloc(sizeof(float) * 4 * n);
+  float* depthBuf = (float*)malloc(sizeof(float) * n);
+  memcpy(prev, raycast, sizeof(float) * 4 * n);
+  for (size_t i = 0; i < n; ++i) {
+    depthBuf[i] = FLT_MAX;
+    for (int k = 0; k < 3; ++k) raycast[4 * i + k] = points[4 * i + k] = normals[4 * i + k] = 0.f;
+    raycast[4 * i + 3] = points[4 * i + 3] = normals[4 * i + 3] = -1.f;
+  }
+  for (size_t i = 0; i < n; ++i) {
+    const float* r = prev + 4 * i;
+    if (r[3] <= 0.f) continue;
+    v3 world = {r[0] * voxelSize, r[1] * voxelSize, r[2] * voxelSize};
+    v3 pc = pose_apply(&pose, world);
+    if (pc.z <= 0.f) continue;
+    float px = in.fx * pc.x / pc.z + in.cx;
+    float py = in.fy * pc.y / pc.z + in.cy;
+    int ix = (int)lroundf(px), iy = (int)lroundf(py);
+    if (ix < 0 || iy < 0 || ix >= in.w || iy >= in.h) continue;
+    size_t t = (size_t)iy * in.w + ix;
+    if (pc.z >= depthBuf[t]) continue;
+    depthBuf[t] = pc.z;
+    memcpy(raycast + 4 * t, r, sizeof(float) * 4);
+    points[4 * t] = world.x;
+    points[4 * t + 1] = world.y;
+    points[4 * t + 2] = world.z;
+    points[4 * t + 3] = 1.f;
+  }
+  for (int y = 0; y < in.h; ++y)
+    for (int x = 0; x < in.w; ++x)
+      if (raycast[4 * ((size_t)y * in.w + x) + 3] <= 0.f) {
+        missingXY[2 * nm] = x;
+        missingXY[2 * nm + 1] = y;
+        ++nm;
+      }
+  free(prev);
+  free(depthBuf);
+  return nm;
+}
+
 /* --------------------------------------------------------------- view */
 /* proj/src/view.cpp:112-119 depth conversion, :69-88 downsample_depth */
 int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float affOffset, int levels,

@@ -53,6 +53,14 @@ int rfo_set_ranges(rfo_map* m, const int* wh, const float* rangeIn);
 int rfo_render_icp(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
                    float* raycastOut, float* pointsOut, float* normalsOut);
 
+/* Approximate raycast (useApproximateRaycast): forward_project
+ * (proj/src/raycast.cpp:141-188) and render_maps(kIcpMaps, missingOnly)
+ * (proj/include/rf/raycast.hpp:200-202).  Images are caller-owned in/out. */
+int rfo_forward_project(int hasRaycast, float* raycast, float* points, float* normals, const float* newPose12,
+                        const int* wh, const float* f4, float voxelSize, int* missingXY);
+int rfo_render_icp_list(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
+                        const int* missingXY, int n, float* raycastOut, float* pointsOut, float* normalsOut);
+
 /* build_view depth path (proj/src/view.cpp:112-119,134-142): level 0 then each
  * pyramid level, concatenated into depthLevels. */
 int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float affOffset, int levels,

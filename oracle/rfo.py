@@ -51,6 +51,8 @@ def lib():
         L.rfo_icp_track.argtypes = [_f, _i, _f, _f, _f, _f, _f, _f, _i, _f, _f, _d]
         L.rfo_icp_reduce.argtypes = [_f, C.c_int, C.c_int, _f, _f, _f, _i, _f, _f, _f, C.c_float, _d]
         L.rfo_solve6.argtypes = [_d, _d]
+        L.rfo_forward_project.argtypes = [C.c_int, _f, _f, _f, _f, _i, _f, C.c_float, _i]
+        L.rfo_render_icp_list.argtypes = [vp, _f, _i, _f, _f, _i, C.c_int, _f, _f, _f]
         L.rfo_total_entries.argtypes = [vp]
         L.rfo_total_entries.restype = C.c_uint32
         L.rfo_export_entries.argtypes = [vp, _i]
@@ -124,6 +126,19 @@ def icp_reduce(depth_l, f4l, points, normals, intr, render_pose34, render_intr, 
     return out
 
 
+def forward_project(has_raycast, raycast, points, normals, pose34, intr, voxel_size):
+    """forward_project (raycast.cpp:141-188) on caller-owned (H, W, 4) images,
+    updated in place; returns the (N, 2) int32 missing (x, y) list."""
+    out = np.zeros((intr["width"] * intr["height"], 2), np.int32)
+    pose = _f32(pose34)
+    wh, f4 = _wh(intr), _f4(intr)
+    for a in (raycast, points, normals):
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    n = lib().rfo_forward_project(1 if has_raycast else 0, P(raycast, _f), P(points, _f), P(normals, _f),
+                                  P(pose, _f), P(wh, _i), P(f4, _f), voxel_size, P(out, _i))
+    return out[:n].copy()
+
+
 class OracleEngine:
     """C restatement of VoxelBlockMap + FusionEngine + RenderState."""
 
@@ -183,6 +198,16 @@ class OracleEngine:
         if rc_ != 0:
             raise RuntimeError("render_icp before render_ranges")
         return rc, pts, nrm, 0.0
+
+    def render_icp_list(self, pose34, intr, params, missing, raycast, points, normals):
+        """render_maps(kIcpMaps, missingOnly) on caller-owned images (in place)."""
+        pose, pv = _f32(pose34), params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        ms = np.ascontiguousarray(missing, np.int32)
+        rc_ = lib().rfo_render_icp_list(self.h, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(ms, _i), len(ms),
+                                        P(raycast, _f), P(points, _f), P(normals, _f))
+        if rc_ != 0:
+            raise RuntimeError("render_icp_list before render_ranges")
 
     def entries(self):
         n = lib().rfo_total_entries(self.h)

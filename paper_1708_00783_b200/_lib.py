@@ -71,6 +71,9 @@ SIGNATURES = {
     "rfg_render_expected_ranges": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), _vp], C.c_int),
     "rfg_render_icp_maps": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), _vp, _vp, _vp, _vp],
                             C.c_int),
+    "rfg_forward_project": ([_vp, C.c_int, _vp, _vp, _vp, _f, C.POINTER(Intrinsics_), C.c_float, _vp, _vp], C.c_int),
+    "rfg_render_icp_maps_list": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), _vp, _vp, _vp, _vp,
+                                  _vp, _vp], C.c_int),
     "rfg_build_view_depth": ([_vp, C.c_int, C.c_int, C.c_float, C.c_float, C.c_int, _vp, _vp], C.c_int),
     "rfg_icp_track": ([_vp, _vp, C.c_int, C.POINTER(Intrinsics_), _vp, _vp, _f, _f, _i, _f, C.c_int, _f, _d],
                       C.c_int),

@@ -229,7 +229,8 @@ int rfg_map_destroy(rfg_map* m) {
   DevMap& d = m->d;
   void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
                   d.visibility, d.reqKey, d.marked,     d.state,          d.tileCounts, d.tilePrefix,
-                  m->icpPartials, m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount};
+                  m->icpPartials, m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount,
+                  m->fwdPrev, m->fwdKeys, m->fwdTileCounts, m->fwdTilePrefix};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->hostState) cudaFreeHost(m->hostState);
@@ -328,6 +329,53 @@ int rfg_render_icp_maps(rfg_map* m, const float pose34[12], const rfg_intrinsics
   const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
   RFG_CK(launch_icp_maps(m->d, fa, reinterpret_cast<const float2*>(range), reinterpret_cast<float4*>(raycast),
                          reinterpret_cast<float4*>(points), reinterpret_cast<float4*>(normals), m->stream));
+  return RFG_OK;
+}
+
+int rfg_forward_project(rfg_map* m, int hasRaycast, float* raycast, float* points, float* normals,
+                        const float newPose34[12], const rfg_intrinsics* intr, float voxelSize, int32_t* missing,
+                        int32_t* nMissing) {
+  RFG_REQUIRE(m && raycast && points && normals && newPose34 && missing && nMissing, "null argument");
+  RFG_REQUIRE(valid_intr(intr) && voxelSize > 0.f, "invalid intrinsics / voxel size");
+  const int n = intr->width * intr->height;
+  if (m->fwdN < n) {
+    RFG_CK(cudaStreamSynchronize(m->stream));
+    cudaFree(m->fwdPrev);
+    cudaFree(m->fwdKeys);
+    cudaFree(m->fwdTileCounts);
+    cudaFree(m->fwdTilePrefix);
+    const int tiles = (n + kTile - 1) / kTile;
+    if (cudaMalloc(&m->fwdPrev, (size_t)n * sizeof(float4)) != cudaSuccess ||
+        cudaMalloc(&m->fwdKeys, (size_t)n * 8) != cudaSuccess ||
+        cudaMalloc(&m->fwdTileCounts, tiles * sizeof(int2)) != cudaSuccess ||
+        cudaMalloc(&m->fwdTilePrefix, tiles * sizeof(int2)) != cudaSuccess) {
+      cudaGetLastError();
+      m->fwdN = 0;
+      set_error("forward-projection scratch allocation failed");
+      return RFG_ENOMEM;
+    }
+    m->fwdN = n;
+  }
+  RFG_CK(launch_forward_project(hasRaycast, reinterpret_cast<float4*>(raycast), reinterpret_cast<float4*>(points),
+                                reinterpret_cast<float4*>(normals), newPose34, intr->width, intr->height, intr->fx,
+                                intr->fy, intr->cx, intr->cy, voxelSize, m->fwdPrev, m->fwdKeys, m->fwdTileCounts,
+                                m->fwdTilePrefix, missing, nMissing, m->stream));
+  return RFG_OK;
+}
+
+int rfg_render_icp_maps_list(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
+                             const rfg_scene_params* params, const float* range, const int32_t* missing,
+                             const int32_t* nMissing, float* raycast, float* points, float* normals) {
+  RFG_REQUIRE(m && pose34 && missing && nMissing && raycast && points && normals, "null argument");
+  if (!range) {
+    set_error("render_icp_maps_list needs the expected-range image (render_expected_ranges first)");
+    return RFG_ESTATE;
+  }
+  RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
+  const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  RFG_CK(launch_icp_maps_list(m->d, fa, reinterpret_cast<const float2*>(range), missing, nMissing,
+                              intr->width * intr->height, reinterpret_cast<float4*>(raycast),
+                              reinterpret_cast<float4*>(points), reinterpret_cast<float4*>(normals), m->stream));
   return RFG_OK;
 }
 

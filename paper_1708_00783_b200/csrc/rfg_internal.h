@@ -87,6 +87,13 @@ cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, c
 int ensure_range_scratch(struct ::rfg_map* m, int width, int height);
 cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* range, float4* raycast,
                             float4* points, float4* normals, cudaStream_t s);
+cudaError_t launch_icp_maps_list(const DevMap& m, const FrameArgs& fa, const float2* range, const int* list,
+                                 const int* count, int maxCount, float4* raycast, float4* points, float4* normals,
+                                 cudaStream_t s);
+cudaError_t launch_forward_project(int hasRaycast, float4* raycast, float4* points, float4* normals,
+                                   const float* pose34, int w, int h, float fx, float fy, float cx, float cy,
+                                   float vs, float4* prev, unsigned long long* keys, int2* tileCounts,
+                                   int2* tilePrefix, int* list, int* count, cudaStream_t s);
 cudaError_t launch_build_view(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
                               cudaStream_t s);
 
@@ -103,6 +110,12 @@ struct rfg_map {
   int icpPartialSlots;
   double* icpOut;            // device: 29 sums + solver state
   float* icpPose;            // device: current cam->world (12) + world->cam (12) + render pose (12)
+  // forward-projection scratch (approximate raycast), sized for fwdN pixels
+  float4* fwdPrev;
+  unsigned long long* fwdKeys;
+  int2* fwdTileCounts;
+  int2* fwdTilePrefix;
+  int fwdN;
 };
 
 #define RFG_CK(call)                                                                      \

@@ -322,12 +322,10 @@ __device__ __forceinline__ bool field_normal(FieldReader& field, f3 h, f3* n) {
   return true;
 }
 
-// One thread per pixel in 16x8 tiles (neighbouring rays share blocks).
-__global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, const float2* __restrict__ range,
-                                                     float4* raycast, float4* points, float4* normals) {
-  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
-  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
-  if (x >= fa.w || y >= fa.h) return;
+// render_maps_field doPixel (raycast.hpp:167-189) without the normal: the
+// raycastResult and points of pixel (x, y).
+__device__ __forceinline__ void raycast_pixel(const DevMap& m, const FrameArgs& fa, const float2* __restrict__ range,
+                                              int x, int y, float4* raycast, float4* points) {
   const size_t i = (size_t)y * fa.w + x;
   const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
   float4 rc = invalid, pt = invalid;
@@ -351,15 +349,9 @@ __global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, con
   points[i] = pt;
 }
 
-// field_normal (raycast.hpp:137-153) at every hit, in its own kernel: the
-// six trilinear reads are uniform work across the warp instead of running
-// behind the divergent march.
-__global__ void __launch_bounds__(128) k_raycast_normals(DevMap m, FrameArgs fa, const float4* __restrict__ raycast,
-                                                         float4* normals) {
-  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
-  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
-  if (x >= fa.w || y >= fa.h) return;
-  const size_t i = (size_t)y * fa.w + x;
+// field_normal (raycast.hpp:137-153) at the hit stored in raycast[i].
+__device__ __forceinline__ void normal_pixel(const DevMap& m, const float4* __restrict__ raycast, float4* normals,
+                                             size_t i) {
   const float4 r = raycast[i];
   float4 nm = make_float4(0.f, 0.f, 0.f, -1.f);
   if (r.w > 0.f) {
@@ -369,6 +361,149 @@ __global__ void __launch_bounds__(128) k_raycast_normals(DevMap m, FrameArgs fa,
     if (field_normal(field, f3{r.x, r.y, r.z}, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
   }
   normals[i] = nm;
+}
+
+// One thread per pixel in 16x8 tiles (neighbouring rays share blocks).
+__global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, const float2* __restrict__ range,
+                                                     float4* raycast, float4* points) {
+  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (x >= fa.w || y >= fa.h) return;
+  raycast_pixel(m, fa, range, x, y, raycast, points);
+}
+
+// Normals at every hit, in their own kernel: the six trilinear reads are
+// uniform work across the warp instead of running behind the divergent march.
+__global__ void __launch_bounds__(128) k_raycast_normals(DevMap m, FrameArgs fa, const float4* __restrict__ raycast,
+                                                         float4* normals) {
+  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (x >= fa.w || y >= fa.h) return;
+  normal_pixel(m, raycast, normals, (size_t)y * fa.w + x);
+}
+
+// render_maps(..., missingOnly) (raycast.hpp:200-202): the listed pixels only.
+__global__ void __launch_bounds__(128) k_raycast_list(DevMap m, FrameArgs fa, const float2* __restrict__ range,
+                                                      const int* __restrict__ list, const int* __restrict__ count,
+                                                      float4* raycast, float4* points) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= *count) return;
+  const int i = list[k];
+  raycast_pixel(m, fa, range, i % fa.w, i / fa.w, raycast, points);
+}
+
+__global__ void __launch_bounds__(128) k_normals_list(DevMap m, const int* __restrict__ list,
+                                                      const int* __restrict__ count, const float4* __restrict__ raycast,
+                                                      float4* normals) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= *count) return;
+  normal_pixel(m, raycast, normals, (size_t)list[k]);
+}
+
+// ------------------------------------------------------ forward projection
+// forward_project (raycast.cpp:141-188).  The serial reference visits the
+// previous hits in row-major order and keeps a target pixel's first point
+// unless a later one is strictly nearer; one 64-bit atomicMin per source
+// point on (float bits of camera z << 32 | source index) keeps exactly that
+// point (positive floats order like their bits; ties resolve to the smaller,
+// i.e. earlier, source index).
+__global__ void k_fwd_init(const float4* __restrict__ raycast, float4* prev, unsigned long long* keys, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  prev[i] = raycast[i];
+  keys[i] = ~0ull;
+}
+
+__global__ void k_fwd_scatter(const float4* __restrict__ prev, unsigned long long* keys, Pose12 pose, int w, int h,
+                              float fx, float fy, float cx, float cy, float vs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= w * h) return;
+  const float4 r = prev[i];
+  if (r.w <= 0.f) return;
+  const f3 world{r.x * vs, r.y * vs, r.z * vs};
+  const f3 pc = pose_apply(pose_from12(pose.v), world);
+  if (pc.z <= 0.f) return;
+  const float px = fx * pc.x / pc.z + cx;
+  const float py = fy * pc.y / pc.z + cy;
+  const int ix = (int)lroundf(px), iy = (int)lroundf(py);
+  if (ix < 0 || iy < 0 || ix >= w || iy >= h) return;
+  const unsigned long long key = ((unsigned long long)__float_as_uint(pc.z) << 32) | (unsigned)i;
+  atomicMin(keys + (size_t)iy * w + ix, key);
+}
+
+// Writes the forwarded (or invalid) maps and counts missing pixels per
+// 1024-pixel tile for the row-major compaction.
+__global__ void __launch_bounds__(kTileThreads) k_fwd_gather(const float4* __restrict__ prev,
+                                                              const unsigned long long* __restrict__ keys,
+                                                              float4* raycast, float4* points, float4* normals, int n,
+                                                              float vs, int2* tileCounts) {
+  const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
+  int miss = 0;
+  for (int j = 0; j < 4; ++j) {
+    const int t = blockIdx.x * kTile + j * kTileThreads + threadIdx.x;
+    if (t >= n) continue;
+    const unsigned long long key = keys[t];
+    float4 rc = invalid, pt = invalid;
+    if (key != ~0ull) {
+      rc = prev[(unsigned)(key & 0xffffffffull)];
+      pt = make_float4(rc.x * vs, rc.y * vs, rc.z * vs, 1.f);
+    }
+    raycast[t] = rc;
+    points[t] = pt;
+    normals[t] = invalid;  // the reference leaves forwarded normals invalid
+    miss += rc.w <= 0.f ? 1 : 0;
+  }
+  __shared__ int total;
+  if (threadIdx.x == 0) total = 0;
+  __syncthreads();
+  if (miss) atomicAdd(&total, miss);
+  __syncthreads();
+  if (threadIdx.x == 0) tileCounts[blockIdx.x] = make_int2(total, 0);
+}
+
+__global__ void k_pix_scan(const int2* counts, int2* prefix, int nTiles, int* total) {
+  if (threadIdx.x != 0) return;
+  int s = 0;
+  for (int i = 0; i < nTiles; ++i) {
+    prefix[i] = make_int2(s, 0);
+    s += counts[i].x;
+  }
+  *total = s;
+}
+
+// Row-major compaction of the missing pixels (tile-local order by a CTA scan).
+__global__ void __launch_bounds__(kTileThreads) k_fwd_emit(const float4* __restrict__ raycast, int n,
+                                                            const int2* __restrict__ prefix, int* list) {
+  __shared__ int warpSum[kTileThreads / 32];
+  const int base = blockIdx.x * kTile + threadIdx.x * 4;
+  int flags = 0, cnt = 0;
+  for (int j = 0; j < 4; ++j) {
+    const int t = base + j;
+    if (t < n && raycast[t].w <= 0.f) {
+      flags |= 1 << j;
+      ++cnt;
+    }
+  }
+  // block exclusive scan of cnt
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int inc = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) warpSum[wid] = inc;
+  __syncthreads();
+  int wbase = 0;
+  for (int k = 0; k < wid; ++k) wbase += warpSum[k];
+  int o = prefix[blockIdx.x].x + wbase + inc - cnt;
+  for (int j = 0; j < 4; ++j)
+    if (flags & (1 << j)) list[o++] = base + j;
+}
+
+__global__ void k_iota_count(int* list, int n, int* count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) list[i] = i;
+  if (i == 0) *count = n;
 }
 
 int range_grid() {
@@ -395,9 +530,42 @@ cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* 
                             float4* points, float4* normals, cudaStream_t s) {
   if (!raycast) return cudaErrorInvalidValue;  // the normals pass reads the hits
   dim3 g((fa.w + 15) / 16, (fa.h + 7) / 8);
-  k_raycast_icp<<<g, 128, 0, s>>>(m, fa, range, raycast, points, normals);
+  k_raycast_icp<<<g, 128, 0, s>>>(m, fa, range, raycast, points);
   k_raycast_normals<<<g, 128, 0, s>>>(m, fa, raycast, normals);
   count_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_icp_maps_list(const DevMap& m, const FrameArgs& fa, const float2* range, const int* list,
+                                 const int* count, int maxCount, float4* raycast, float4* points, float4* normals,
+                                 cudaStream_t s) {
+  const int g = (maxCount + 127) / 128;
+  if (g == 0) return cudaSuccess;
+  k_raycast_list<<<g, 128, 0, s>>>(m, fa, range, list, count, raycast, points);
+  k_normals_list<<<g, 128, 0, s>>>(m, list, count, raycast, normals);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_forward_project(int hasRaycast, float4* raycast, float4* points, float4* normals,
+                                   const float* pose34, int w, int h, float fx, float fy, float cx, float cy,
+                                   float vs, float4* prev, unsigned long long* keys, int2* tileCounts,
+                                   int2* tilePrefix, int* list, int* count, cudaStream_t s) {
+  const int n = w * h;
+  if (!hasRaycast) {
+    k_iota_count<<<(n + 255) / 256, 256, 0, s>>>(list, n, count);
+    count_launch();
+    return cudaGetLastError();
+  }
+  Pose12 p;
+  for (int i = 0; i < 12; ++i) p.v[i] = pose34[i];
+  const int nTiles = (n + kTile - 1) / kTile;
+  k_fwd_init<<<(n + 255) / 256, 256, 0, s>>>(raycast, prev, keys, n);
+  k_fwd_scatter<<<(n + 255) / 256, 256, 0, s>>>(prev, keys, p, w, h, fx, fy, cx, cy, vs);
+  k_fwd_gather<<<nTiles, kTileThreads, 0, s>>>(prev, keys, raycast, points, normals, n, vs, tileCounts);
+  k_pix_scan<<<1, 32, 0, s>>>(tileCounts, tilePrefix, nTiles, count);
+  k_fwd_emit<<<nTiles, kTileThreads, 0, s>>>(raycast, n, tilePrefix, list);
+  count_launch(5);
   return cudaGetLastError();
 }
 

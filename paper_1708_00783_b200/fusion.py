@@ -382,10 +382,28 @@ def render_expected_ranges(map: VoxelBlockMap, pose, intr: Intrinsics, params: S
                                            _ptr(state.expectedRange)))
 
 
+class MissingPixels:
+    """Device list of row-major linear pixel indices (forward_project output)."""
+
+    def __init__(self, capacity: int, width: int):
+        self.index = torch.empty(max(capacity, 1), dtype=torch.int32, device="cuda")
+        self.count = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.width = width
+
+    def __len__(self):
+        return int(self.count.item())
+
+    def xy(self) -> np.ndarray:
+        """(N, 2) int32 (x, y), the reference's std::vector<Vector2i> order."""
+        idx = self.index[:len(self)].cpu().numpy()
+        return np.stack([idx % self.width, idx // self.width], axis=1).astype(np.int32)
+
+
 def render_maps(map: VoxelBlockMap, pose, intr: Intrinsics, params: SceneParams, mode: RenderMode,
-                state: RenderState):
+                state: RenderState, missingOnly: MissingPixels | None = None):
     """proj/src/raycast.cpp:129-139 — only RenderMode.kIcpMaps is on the hot
-    path; colour/grey shading is out of scope."""
+    path; colour/grey shading is out of scope.  missingOnly
+    restricts the work to the listed pixels (raycast.hpp:200-202)."""
     if mode != RenderMode.kIcpMaps:
         raise NotImplementedError("only RenderMode.kIcpMaps is implemented on the B200 path")
     if state.expectedRange is None:
@@ -393,12 +411,36 @@ def render_maps(map: VoxelBlockMap, pose, intr: Intrinsics, params: SceneParams,
     state.resize(intr)
     p = _pose(pose)
     map.bind_stream()
-    check(lib().rfg_render_icp_maps(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()),
-                                    _ptr(state.expectedRange), _ptr(state.raycastResult), _ptr(state.points),
-                                    _ptr(state.normals)))
+    if missingOnly is None:
+        check(lib().rfg_render_icp_maps(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()),
+                                        _ptr(state.expectedRange), _ptr(state.raycastResult), _ptr(state.points),
+                                        _ptr(state.normals)))
+    else:
+        check(lib().rfg_render_icp_maps_list(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()),
+                                             _ptr(state.expectedRange), _ptr(missingOnly.index),
+                                             _ptr(missingOnly.count), _ptr(state.raycastResult),
+                                             _ptr(state.points), _ptr(state.normals)))
     state.pose = p.copy()
     state.intr = intr
     state.hasRaycast = True
+
+
+def forward_project(state: RenderState, newPose, intr: Intrinsics, voxelSize: float,
+                    map: VoxelBlockMap) -> MissingPixels:
+    """forward_project (proj/src/raycast.cpp:141-188) on the device images of
+    `state`; returns the pixels that must be raycast afresh."""
+    missing = MissingPixels(intr.width * intr.height, intr.width)
+    has = state.hasRaycast
+    state.resize(intr)
+    p = _pose(newPose)
+    map.bind_stream()
+    check(lib().rfg_forward_project(map.handle, 1 if has else 0, _ptr(state.raycastResult), _ptr(state.points),
+                                    _ptr(state.normals), _fp(p), C.byref(intr.c()), voxelSize,
+                                    _ptr(missing.index), _ptr(missing.count)))
+    if has:
+        state.pose = p.copy()
+        state.intr = intr
+    return missing
 
 
 # ------------------------------------------------------------------ ICP
