@@ -159,6 +159,11 @@ int rfg_icp_reduce(rfg_map* map, const float* depth_level_dev, int level, const 
                    const float* points_dev, const float* normals_dev, const float render_pose34[12],
                    const float cam_to_world34[12], float dist, double out29[29]);
 
+/* Tracker phase timers of CTA 0 (ns, accumulated since the last reset):
+ * {associate + block reduce, grid barrier wait, final sum, solve,
+ *  iterations, 0, 0, 0}.  Synchronises the map's stream. */
+int rfg_icp_timers(rfg_map* map, uint64_t out8[8], int reset);
+
 /* ------------------------------------------------------ frame pipeline */
 /* The per-frame driver (ITMMainEngine::ProcessFrame order):
  * [track] -> allocate -> integrate -> expected ranges -> ICP-map raycast,

@@ -90,6 +90,7 @@ SIGNATURES = {
     "rfg_pipeline_stream": ([_vp], _vp),
     "rfg_compose_keys": ([_vp, _f, C.c_int, C.c_int, _vp, _vp], C.c_int),
     "rfg_compose_select": ([_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp], C.c_int),
+    "rfg_icp_timers": ([_vp, C.POINTER(C.c_uint64), C.c_int], C.c_int),
     "rfg_total_entries": ([_vp], C.c_uint32),
     "rfg_export_entries": ([_vp, _i], C.c_int),
     "rfg_export_blocks": ([_vp, _i, C.c_int, _u8], C.c_int),

@@ -26,6 +26,7 @@ cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* d
                                    const Intr& in0, const float4* points, const float4* normals, const float* c2w,
                                    const float* renderPose, float dist, cudaStream_t s);
 const double* icp_sums_ptr(void* state);
+unsigned long long* icp_timers_ptr(void* state);
 const double* icp_stats_ptr(void* state);
 const float* icp_w2c_ptr(void* state);
 
@@ -428,6 +429,15 @@ int rfg_icp_reduce(rfg_map* m, const float* depthLevel, int level, const rfg_int
                                 reinterpret_cast<const float4*>(normals), m->icpPose, m->icpPose + 12, dist,
                                 m->stream));
   RFG_CK(cudaMemcpyAsync(out29, icp_sums_ptr(m->icpOut), 29 * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaStreamSynchronize(m->stream));
+  return RFG_OK;
+}
+
+int rfg_icp_timers(rfg_map* m, uint64_t out8[8], int reset) {
+  RFG_REQUIRE(m && out8, "null argument");
+  unsigned long long* t = icp_timers_ptr(m->icpOut);
+  RFG_CK(cudaMemcpyAsync(out8, t, 64, cudaMemcpyDeviceToHost, m->stream));
+  if (reset) RFG_CK(cudaMemsetAsync(t, 0, 64, m->stream));
   RFG_CK(cudaStreamSynchronize(m->stream));
   return RFG_OK;
 }

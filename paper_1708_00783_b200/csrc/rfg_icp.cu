@@ -43,7 +43,16 @@ struct IcpState {
   float renderPose[12]; // world->camera of the render being tracked against
   int done[4];          // per-level stop flags
   int pad[4];
+  // phase timers of CTA 0 (ns, %globaltimer), accumulated over iterations:
+  // {associate+reduce, grid barrier, final sum, solve, iterations, -, -, -}
+  unsigned long long timers[8];
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct IcpLevelArgs {
   const float* depth;   // pyramid level
@@ -71,8 +80,12 @@ struct GnShared {
 };
 
 // double-precision SE(3) (proj/include/rf/pose.hpp:45-60 with S = double)
-__device__ void matmul3d(const double* A, const double* B, double* C) {
+// (all small-matrix loops are fully unrolled so the solver state stays in
+// registers instead of local memory)
+__device__ __forceinline__ void matmul3d(const double* A, const double* B, double* C) {
+#pragma unroll
   for (int r = 0; r < 3; ++r)
+#pragma unroll
     for (int c = 0; c < 3; ++c) C[r * 3 + c] = A[r * 3 + 0] * B[c] + (A[r * 3 + 1] * B[3 + c] + A[r * 3 + 2] * B[6 + c]);
 }
 
@@ -112,11 +125,31 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Cholesky solve (same operation order as oracle/rfo.c:rfo_solve6).
-__device__ int solve6(const double* acc, double* x) {
+// 1/sqrt(s) for s > 0: MUFU seed + two Newton steps (within ~1 ulp of the
+// correctly rounded value).  Inline, unlike the IEEE sqrt/rcp, whose
+// out-of-line slow paths made ptxas spill the whole factorisation.
+__device__ __forceinline__ double rsqrt_nr(double s) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double e = __fma_rn(-__dmul_rn(s, r), r, 1.0);  // 1 - s r^2
+    r = __fma_rn(__dmul_rn(r, 0.5), e, r);
+  }
+  return r;
+}
+
+// Cholesky solve (same operation order as oracle/rfo.c:rfo_solve6; the
+// pivot's 1/sqrt comes from rsqrt_nr, so the solution agrees with the oracle
+// to rounding — the tracker's pose tolerance is 1e-5).
+__device__ __forceinline__ int solve6(const double* acc, double* x) {
+  // every loop has constant bounds (guards instead of j-dependent limits) so
+  // the whole factorisation unrolls into registers
   double A[36];
   int k = 0;
+#pragma unroll
   for (int a = 0; a < 6; ++a)
+#pragma unroll
     for (int b = a; b < 6; ++b) {
       A[a * 6 + b] = acc[k];
       A[b * 6 + a] = acc[k];
@@ -125,43 +158,57 @@ __device__ int solve6(const double* acc, double* x) {
   double L[36];
 #pragma unroll
   for (int i = 0; i < 36; ++i) L[i] = 0.0;
+  // no early exits either: a non-positive pivot raises `bad`, is replaced by
+  // 1 so the rest stays finite, and the solve reports failure at the end
   double inv[6];
   double det = 1.0;
+  bool bad = false;
 #pragma unroll
   for (int j = 0; j < 6; ++j) {
     double s = A[j * 6 + j];
 #pragma unroll
-    for (int p = 0; p < j; ++p) s -= L[j * 6 + p] * L[j * 6 + p];
-    if (!(s > 0.0)) return -1;
+    for (int p = 0; p < 6; ++p)
+      if (p < j) s -= L[j * 6 + p] * L[j * 6 + p];
+    if (!(s > 0.0)) {
+      bad = true;
+      s = 1.0;
+    }
     det *= s;
-    const double ljj = sqrt(s);
-    L[j * 6 + j] = ljj;
-    inv[j] = 1.0 / ljj;
+    inv[j] = rsqrt_nr(s);
+    L[j * 6 + j] = s * inv[j];
 #pragma unroll
-    for (int i = j + 1; i < 6; ++i) {
-      double t = A[i * 6 + j];
+    for (int i = 0; i < 6; ++i) {
+      if (i > j) {
+        double t = A[i * 6 + j];
 #pragma unroll
-      for (int p = 0; p < j; ++p) t -= L[i * 6 + p] * L[j * 6 + p];
-      L[i * 6 + j] = t * inv[j];
+        for (int p = 0; p < 6; ++p)
+          if (p < j) t -= L[i * 6 + p] * L[j * 6 + p];
+        L[i * 6 + j] = t * inv[j];
+      }
     }
   }
-  if (det < 1e-12) return -1;
+  bad = bad || det < 1e-12;
   double yv[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     double t = -acc[21 + i];
 #pragma unroll
-    for (int p = 0; p < i; ++p) t -= L[i * 6 + p] * yv[p];
+    for (int p = 0; p < 6; ++p)
+      if (p < i) t -= L[i * 6 + p] * yv[p];
     yv[i] = t * inv[i];
   }
+  double xv[6];
 #pragma unroll
   for (int i = 5; i >= 0; --i) {
     double t = yv[i];
 #pragma unroll
-    for (int p = i + 1; p < 6; ++p) t -= L[p * 6 + i] * x[p];
-    x[i] = t * inv[i];
+    for (int p = 0; p < 6; ++p)
+      if (p > i) t -= L[p * 6 + i] * xv[p];
+    xv[i] = t * inv[i];
   }
-  return 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) x[i] = xv[i];
+  return bad ? -1 : 0;
 }
 
 // One Gauss-Newton step on the CTA-local state (oracle: rfo_icp_track loop
@@ -199,19 +246,25 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
     cc = (theta - s) / (theta * theta * theta);
   }
   double ER[9], V[9], Et[3];
+#pragma unroll
   for (int i = 0; i < 9; ++i) {
     const double I = (i % 4 == 0) ? 1.0 : 0.0;
     ER[i] = I + ca * W[i] + cb * WW[i];
     V[i] = I + cb * W[i] + cc * WW[i];
   }
+#pragma unroll
   for (int r = 0; r < 3; ++r) Et[r] = V[r * 3] * v[0] + (V[r * 3 + 1] * v[1] + V[r * 3 + 2] * v[2]);
   double CR[9], Ct[3], NR[9];
+#pragma unroll
   for (int r = 0; r < 3; ++r) {
+#pragma unroll
     for (int c = 0; c < 3; ++c) CR[r * 3 + c] = g.c2w[r * 4 + c];
     Ct[r] = g.c2w[r * 4 + 3];
   }
   matmul3d(ER, CR, NR);
+#pragma unroll
   for (int r = 0; r < 3; ++r) {
+#pragma unroll
     for (int c = 0; c < 3; ++c) g.c2w[r * 4 + c] = NR[r * 3 + c];
     g.c2w[r * 4 + 3] = (ER[r * 3] * Ct[0] + (ER[r * 3 + 1] * Ct[1] + ER[r * 3 + 2] * Ct[2])) + Et[r];
   }
@@ -227,7 +280,6 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
 }
 
 __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a, double* partials) {
-  cg::grid_group grid = cg::this_grid();
   __shared__ double sh[kIcpThreads / 32][29];
   __shared__ GnShared g;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -245,7 +297,11 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
   const float dist2 = a.dist * a.dist;
   const int n = a.lw * a.lh;
   const Pose rp = pose_from12(g.rp);
+  const bool timed = blockIdx.x == 0 && threadIdx.x == 0;
+  cg::grid_group grid = cg::this_grid();
   for (int it = 0; it < a.iters && !g.done; ++it) {
+    unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    if (timed) t0 = gtimer();
     double* part = partials + (size_t)(it & 1) * kIcpMaxCtas * 29;
     const Pose c2w = pose_from12(g.c2wF);
     double acc[29];
@@ -283,19 +339,36 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
       acc[27] += rd * rd;
       acc[28] += 1.0;
     }
+    {
+      // multi-value warp reduction by recursive halving: at offset o every
+      // lane keeps one half of its live values and sends the other half to
+      // lane^o, so 32 (29 + 3 zero) sums take 16+8+4+2+1 = 31 shuffles
+      // instead of 29 x 5.  Lane l ends with sum number brev5(l).
+      double v[32];
 #pragma unroll
-    for (int k = 0; k < 29; ++k) {
-      const double s = warp_sum(acc[k]);
-      if (lane == 0) sh[wid][k] = s;
+      for (int k = 0; k < 32; ++k) v[k] = k < 29 ? acc[k] : 0.0;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+          const double send = hi ? v[i] : v[i + o];
+          const double keep = hi ? v[i + o] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (lane < 29) sh[wid][lane] = v[0];
     }
     __syncthreads();
     if (threadIdx.x < 29) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < kIcpThreads / 32; ++w) s += sh[w][threadIdx.x];
-      part[blockIdx.x * 29 + threadIdx.x] = s;
+      part[threadIdx.x * kIcpMaxCtas + blockIdx.x] = s;  // [sum][cta]: coalesced final sum
     }
+    if (timed) t1 = gtimer();
     grid.sync();
+    if (timed) t2 = gtimer();
     // every CTA: fixed-order final sum (warp w owns sums w, w+16; lanes
     // stride the CTAs; shuffle tree) and the identical solve
     for (int k = wid; k < 29; k += kIcpThreads / 32) {
@@ -304,7 +377,7 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
 #pragma unroll
       for (int j = 0; j < kIcpMaxCtas / 32; ++j) {
         const int c = lane + 32 * j;
-        v[j] = c < (int)gridDim.x ? __ldcg(part + c * 29 + k) : 0.0;
+        v[j] = c < (int)gridDim.x ? __ldcg(part + k * kIcpMaxCtas + c) : 0.0;
       }
       double s = 0.0;
 #pragma unroll
@@ -313,6 +386,7 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
       if (lane == 0) g.sums[k] = s;
     }
     __syncthreads();
+    if (timed) t3 = gtimer();
     if (threadIdx.x == 0) {
       if (a.evalOnly)
         g.done = 1;
@@ -320,6 +394,14 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
         gn_step(g, a.level, a.minCount);
     }
     __syncthreads();
+    if (timed) {
+      const unsigned long long t4 = gtimer();
+      st->timers[0] += t1 - t0;
+      st->timers[1] += t2 - t1;
+      st->timers[2] += t3 - t2;
+      st->timers[3] += t4 - t3;
+      st->timers[4] += 1;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int i = 0; i < 12; ++i) {
@@ -449,6 +531,7 @@ cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* d
   return launch_level(st, a, partials, s);
 }
 
+unsigned long long* icp_timers_ptr(void* state) { return static_cast<IcpState*>(state)->timers; }
 const double* icp_sums_ptr(void* state) { return static_cast<IcpState*>(state)->sums; }
 const double* icp_stats_ptr(void* state) { return static_cast<IcpState*>(state)->stats; }
 const float* icp_w2c_ptr(void* state) { return static_cast<IcpState*>(state)->w2cF; }

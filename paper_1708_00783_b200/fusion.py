@@ -181,9 +181,12 @@ class VoxelBlockMap:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            lib().rfg_map_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.rfg_map_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: module globals may be gone
+            pass
 
     @property
     def handle(self):
@@ -527,9 +530,12 @@ class Pipeline:
         self._levels = levels
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
-            lib().rfg_pipeline_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.rfg_pipeline_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: module globals may be gone
+            pass
 
     def process(self, raw, pose=None):
         """raw: CUDA uint16/int16 tensor (device path) or numpy uint16 (host path)."""
