@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "librfg.so")
+# RFG_LIB_PATH selects another build of the same library (A/B kernel variants
+# in tools/); there is still no fallback if it is missing
+LIB_PATH = os.environ.get("RFG_LIB_PATH") or os.path.join(PKG_DIR, "librfg.so")
 
 RFG_OK = 0
 RFG_EINVAL = -1

@@ -178,7 +178,7 @@ struct FieldReader {
   }
   // readSdfNearest (voxel_block_map.cpp:178-185)
   __device__ __forceinline__ float nearest(f3 p, bool& ok) {
-    const int vx = (int)lroundf(p.x), vy = (int)lroundf(p.y), vz = (int)lroundf(p.z);
+    const int vx = lround_haz(p.x), vy = lround_haz(p.y), vz = lround_haz(p.z);
     const int ptr = ptr_of(vx >> 3, vy >> 3, vz >> 3);
     ok = ptr >= 0;
     if (!ok) return 1.f;

@@ -17,3 +17,16 @@ def test_sdf_to_logical_fast_path_is_ieee_exact_for_all_int16():
                         "-fmad=false", "-std=c++17", src, "-o", exe], check=True)
         p = subprocess.run([exe], capture_output=True, text=True, timeout=60)
         assert p.returncode == 0 and "mismatches 0" in p.stdout, p.stdout + p.stderr
+
+
+def test_hoisted_division_and_lround_are_ieee_exact():
+    """div_fast/div_rcp (projection, eta/mu, weight merge) and lround_haz
+    (quantisation, nearest reads) against __fdiv_rn / lroundf."""
+    src = os.path.join(ROOT, "tests", "cuda", "divfast.cu")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "divfast")
+        subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                        "-fmad=false", "-std=c++17", src, "-o", exe], check=True)
+        p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stdout + p.stderr
+        assert "exhaustive mismatches 0  random mismatches 0  lround mismatches 0" in p.stdout, p.stdout
