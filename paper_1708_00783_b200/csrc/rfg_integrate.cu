@@ -70,7 +70,7 @@ __device__ __forceinline__ void update_colour(uint32_t& word, f3 pt, const Pose&
 #endif
 constexpr int kQG = RFG_INT_QG;  // rows (of 4 voxels) per project/gather/update group
 template <bool kColour>
-__global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate(DevMap m, const float* __restrict__ depth, FrameArgs fa,
+__global__ void __launch_bounds__(256, 2) k_integrate(DevMap m, const float* __restrict__ depth, FrameArgs fa,
                                                    ColourArgs ca) {
   const int lane = threadIdx.x & 31;
   const int warpsPerCta = blockDim.x >> 5;
@@ -187,6 +187,148 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate(DevMap m, const
   }
 }
 
+// ------------------------------------------------- depth-only, branch-free
+// The depth-only kernel (the C1/C2 hot path) computes every voxel's
+// projection and update unconditionally and selects the result, so a warp
+// issues one instruction stream instead of the union of the per-voxel
+// branches.  All divisions take the hoisted fast path; its exactness window
+// (tests/cuda/divfast.cu: dividends |a| in [2^-100, 2^40] and 0, divisors in
+// [2^-40, 2^40]) covers every quotient of a voxel whose camera z lies in
+// [2^-40, 2^40] with |fx X|, |fy Y|, |eta| <= 2^40 and mu in [2^-20, 2^20]:
+//   x/z, y/z : dividends below 2^-100 give |quotient| < 2^-60, which leaves
+//              u = cx (|cx| >= 2^-30) or u < 1 (invalid) either way;
+//   eta/mu   : eta = d - z is 0 or >= 2^-64 in magnitude when z >= 2^-40;
+//   merge    : (w F + newF) is 0 or >= 2^-84 (newF >= 2^-84, w F a multiple
+//              of 1/32767 for w >= 1), and den = w + 1 is in [1, 256].
+// Voxels outside the window (never at sane scales) are flagged and redone
+// with IEEE division behind one warp-uniform branch per group.
+__device__ __forceinline__ void project_exact(const Pose& pose, const FrameArgs& fa, float wLim, float hLim, float px,
+                                              float py, float pz, int* pixOut) {
+  const f3 pc = pose_apply(pose, f3{px, py, pz});
+  int p = -1;
+  if (pc.z > 0.f) {
+    const float u = div_ieee(fa.fx * pc.x, pc.z) + fa.cx;
+    const float v = div_ieee(fa.fy * pc.y, pc.z) + fa.cy;
+    if (!(u < 1 || u > wLim || v < 1 || v > hLim)) p = (int)(v + 0.5f) * fa.w + (int)(u + 0.5f);
+  }
+  *pixOut = p;
+}
+
+__device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float mu, int maxW) {
+  const int oldW = vox_w(wd);
+  const float oldF = sdf_to_logical(vox_sdf(wd));
+  const float newF = smin(1.f, div_ieee(eta, mu));
+  const float merged = div_ieee((float)oldW * oldF + newF, (float)(oldW + 1));
+  return vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
+}
+
+__global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m, const float* __restrict__ depth,
+                                                                       FrameArgs fa) {
+  const int lane = threadIdx.x & 31;
+  const int warpsPerCta = blockDim.x >> 5;
+  const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
+  const int nw = gridDim.x * warpsPerCta;
+  const int nVis = *((volatile int*)&m.state->nVisible);
+  const Pose pose = load_pose_i(fa);
+  const float wLim = (float)(fa.w - 2), hLim = (float)(fa.h - 2);
+  const float mu = fa.mu, vs = fa.voxelSize;
+  const bool muOk = mu >= 0x1p-20f && mu <= 0x1p20f;
+  const float rMu = div_rcp(mu);
+  const bool capW = fa.stopAtMaxW != 0;
+  const int maxW = fa.maxW;
+  for (int b = gw; b < nVis; b += nw) {
+    const int idx = m.visibleList[b];
+    const int4 e = ld_entry(m.entries, idx);
+    if (e.w < 0) continue;
+    const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
+    uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
+#pragma unroll
+    for (int g = 0; g < 4; g += kQG) {
+      uint32_t wd[4 * kQG];
+#pragma unroll
+      for (int q = g; q < g + kQG; ++q) {
+        const uint4 r = blk[q * 32 + lane];
+        wd[(q - g) * 4 + 0] = r.x;
+        wd[(q - g) * 4 + 1] = r.y;
+        wd[(q - g) * 4 + 2] = r.z;
+        wd[(q - g) * 4 + 3] = r.w;
+      }
+      // ---- project
+      float zc[4 * kQG];
+      int pix[4 * kQG];
+      unsigned slow = 0u;
+#pragma unroll
+      for (int q = g; q < g + kQG; ++q) {
+        const int lin = (q * 32 + lane) * 4;
+        const float pz = (float)(oz + (lin >> 6)) * vs;
+        const float py = (float)(oy + ((lin >> 3) & 7)) * vs;
+        const float r0 = pose.R[1] * py + pose.R[2] * pz;
+        const float r1 = pose.R[4] * py + pose.R[5] * pz;
+        const float r2 = pose.R[7] * py + pose.R[8] * pz;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = (q - g) * 4 + i;
+          const float px = (float)(ox + (lin & 7) + i) * vs;
+          const float cxw = (pose.R[0] * px + r0) + pose.t[0];
+          const float cyw = (pose.R[3] * px + r1) + pose.t[1];
+          const float czw = (pose.R[6] * px + r2) + pose.t[2];
+          const float ax = fa.fx * cxw, ay = fa.fy * cyw;
+          const float rz = div_rcp(czw);
+          const float u = div_fast(ax, czw, rz) + fa.cx;
+          const float v = div_fast(ay, czw, rz) + fa.cy;
+          const bool in = czw > 0.f && !(u < 1 || u > wLim || v < 1 || v > hLim);
+          pix[k] = in ? (int)(v + 0.5f) * fa.w + (int)(u + 0.5f) : -1;
+          zc[k] = czw;
+          const bool fast = czw >= 0x1p-40f && czw <= 0x1p40f && fabsf(ax) <= 0x1p40f && fabsf(ay) <= 0x1p40f;
+          slow |= (czw > 0.f && !fast) ? (1u << k) : 0u;
+        }
+      }
+      if (__any_sync(0xffffffffu, slow != 0u)) {
+#pragma unroll
+        for (int k = 0; k < 4 * kQG; ++k) {
+          if (slow & (1u << k)) {
+            const int lin = ((g + (k >> 2)) * 32 + lane) * 4;
+            project_exact(pose, fa, wLim, hLim, (float)(ox + (lin & 7) + (k & 3)) * vs,
+                          (float)(oy + ((lin >> 3) & 7)) * vs, (float)(oz + (lin >> 6)) * vs, &pix[k]);
+          }
+        }
+      }
+      // ---- gather
+      float dm[4 * kQG];
+#pragma unroll
+      for (int k = 0; k < 4 * kQG; ++k) dm[k] = pix[k] >= 0 ? __ldg(depth + pix[k]) : -1.f;
+      // ---- update (update_voxel_depth, fusion.cpp:9-36)
+#pragma unroll
+      for (int k = 0; k < 4 * kQG; ++k) {
+        const uint32_t w0 = wd[k];
+        const int oldW = vox_w(w0);
+        const float eta = dm[k] - zc[k];
+        const bool upd = pix[k] >= 0 && !(dm[k] <= 0.f) && !(eta < -mu) && !(capW && oldW >= maxW);
+        const float oldF = sdf_to_logical(vox_sdf(w0));
+        const float newF = smin(1.f, div_fast(eta, mu, rMu));
+        const float num = (float)oldW * oldF + newF;
+        const float den = (float)(oldW + 1);
+        const float merged = div_fast(num, den, div_rcp(den));
+        const uint32_t w1 = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
+        // out-of-window voxels keep w0 here and are redone exactly below
+        const bool slowK = upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << k)));
+        wd[k] = (upd && !slowK) ? w1 : w0;
+        slow = slowK ? (slow | (1u << k)) : (slow & ~(1u << k));
+      }
+      if (__any_sync(0xffffffffu, slow != 0u)) {
+#pragma unroll
+        for (int k = 0; k < 4 * kQG; ++k)
+          if (slow & (1u << k)) wd[k] = update_exact(wd[k], dm[k] - zc[k], mu, maxW);
+      }
+#pragma unroll
+      for (int q = g; q < g + kQG; ++q) {
+        const int k = (q - g) * 4;
+        blk[q * 32 + lane] = make_uint4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
+      }
+    }
+  }
+}
+
 int integrate_grid() {
   static int grid = 0;
   if (!grid) {
@@ -212,7 +354,7 @@ cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint8_t*
     for (int i = 0; i < 12; ++i) ca.extr[i] = extr34 ? extr34[i] : ((i % 5 == 0) ? 1.f : 0.f);
     k_integrate<true><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
   } else {
-    k_integrate<false><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
+    k_integrate_depth<<<integrate_grid(), 256, 0, s>>>(m, depth, fa);
   }
   count_launch();
   return cudaGetLastError();

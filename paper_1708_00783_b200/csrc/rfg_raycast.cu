@@ -134,6 +134,15 @@ __global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m,
   if (threadIdx.x == 0) m.binCount[t] = 0;  // ready for the next frame
 }
 
+#ifdef RFG_RC_STATS
+// debug build only: march statistics {rays, steps, coarse, invalid-fine,
+// nearest-valid, trilinear, lookups, -, hist[log2 steps] x 16, max steps}
+__device__ unsigned long long g_rc_stats[32];
+#define RC_STAT(i, v) atomicAdd(&g_rc_stats[i], (unsigned long long)(v))
+#else
+#define RC_STAT(i, v)
+#endif
+
 // ------------------------------------------------------------ raycast
 // TSDF field reader (MapField, raycast.hpp:32-45) with the reference's
 // last-block cache.  Voxel offsets inside a block use bit operations
@@ -146,6 +155,7 @@ struct FieldReader {
 
   // findEntry + ptr (voxel_block_map.cpp:26-34,63-72), uncached
   __device__ __forceinline__ int lookup(int bx, int by, int bz) const {
+    RC_STAT(6, 1);
     int ptr = -1;
     if (bx >= -32768 && bx <= 32767 && by >= -32768 && by <= 32767 && bz >= -32768 && bz <= 32767) {
       int idx = (int)hash_index(bx, by, bz, buckets - 1);
@@ -193,6 +203,7 @@ struct FieldReader {
   // last-block cache for the base block, then the 8 voxel loads are issued
   // independently.
   __device__ __forceinline__ float trilinear(f3 p, bool& ok) {
+    RC_STAT(5, 1);
     const int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
     const float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
@@ -248,8 +259,23 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
   float t = tMinM;
   enum { COARSE, FINE, SURFACE };
   int state = field.resident(at_t(oV, dV, t)) ? FINE : COARSE;
+#ifdef RFG_RC_STATS
+  int nSteps = 0, nCoarse = 0, nInv = 0, nNear = 0;
+  struct Fin {
+    int& a; int& b; int& c; int& d;
+    __device__ ~Fin() {
+      RC_STAT(0, 1); RC_STAT(1, a); RC_STAT(2, b); RC_STAT(3, c); RC_STAT(4, d);
+      RC_STAT(8 + min(15, 32 - __clz(a)), 1);
+      atomicMax(&g_rc_stats[31], (unsigned long long)a);
+    }
+  } fin{nSteps, nCoarse, nInv, nNear};
+#endif
   while (t <= tMaxM) {
     const f3 p = at_t(oV, dV, t);
+#ifdef RFG_RC_STATS
+    ++nSteps;
+    if (state == COARSE) ++nCoarse;
+#endif
     if (state == COARSE) {
       if (field.resident(p)) {
         state = FINE;
@@ -262,10 +288,16 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
     bool ok = false;
     float sdf = field.nearest(p, ok);
     if (!ok) {
+#ifdef RFG_RC_STATS
+      ++nInv;
+#endif
       if (state == SURFACE) state = FINE;
       t += fineStep;
       continue;
     }
+#ifdef RFG_RC_STATS
+    ++nNear;
+#endif
     if (sdf <= 0.1f) {
       bool okTri = false;
       const float tri = field.trilinear(p, okTri);
@@ -363,8 +395,14 @@ __device__ __forceinline__ void normal_pixel(const DevMap& m, const float4* __re
   normals[i] = nm;
 }
 
+#ifndef RFG_RC_MINB
+#define RFG_RC_MINB 1
+#endif
+#ifndef RFG_NRM_MINB
+#define RFG_NRM_MINB 1
+#endif
 // One thread per pixel in 16x8 tiles (neighbouring rays share blocks).
-__global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, const float2* __restrict__ range,
+__global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_icp(DevMap m, FrameArgs fa, const float2* __restrict__ range,
                                                      float4* raycast, float4* points) {
   const int x = blockIdx.x * 16 + (threadIdx.x & 15);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
@@ -374,7 +412,7 @@ __global__ void __launch_bounds__(128) k_raycast_icp(DevMap m, FrameArgs fa, con
 
 // Normals at every hit, in their own kernel: the six trilinear reads are
 // uniform work across the warp instead of running behind the divergent march.
-__global__ void __launch_bounds__(128) k_raycast_normals(DevMap m, FrameArgs fa, const float4* __restrict__ raycast,
+__global__ void __launch_bounds__(128, RFG_NRM_MINB) k_raycast_normals(DevMap m, FrameArgs fa, const float4* __restrict__ raycast,
                                                          float4* normals) {
   const int x = blockIdx.x * 16 + (threadIdx.x & 15);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
@@ -632,3 +670,15 @@ extern "C" int rfg_compose_select(const int64_t* keymin, int rank, int n, float*
   RFG_CK(cudaGetLastError());
   return RFG_OK;
 }
+
+#ifdef RFG_RC_STATS
+extern "C" int rfg_debug_rc_stats(unsigned long long* out32, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out32, rfg::g_rc_stats, sizeof(rfg::g_rc_stats));
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(rfg::g_rc_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

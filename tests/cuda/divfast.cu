@@ -1,9 +1,11 @@
 // Exactness of the arithmetic shortcuts in rfg_common.cuh against the IEEE
 // operations they replace (bit-for-bit):
-//   1. div_fast(a, b, div_rcp(b)) == a / b for every dividend a in div_ok's
-//      window, exhaustively, for the divisors the kernels use with a fixed
-//      divisor (mu values and every integer weight divisor 1..256);
-//   2. the same for 2^33 random (a, b) pairs with both inside the window;
+//   1. div_fast(a, b, div_rcp(b)) == a / b for every dividend a with |a| in
+//      [2^-100, 2^40] and a = +0, exhaustively, for the divisors the kernels
+//      use with a fixed divisor (mu values and every integer weight divisor
+//      1..256) — the window integration relies on (rfg_integrate.cu);
+//   2. the same for 2^33 random (a, b) pairs, |a| in [2^-100, 2^40] and
+//      |b| in [2^-40, 2^40] (the projection's x/z, y/z);
 //   3. lround_haz(v) == lroundf(v) for every float with |v| < 2^31 and NaN.
 #include <cstdio>
 #include <cstdint>
@@ -14,9 +16,9 @@ using rfg::div_ok;
 using rfg::div_rcp;
 using rfg::lround_haz;
 
-// all bit patterns of |a| in [2^-40, 2^40], both signs
+// all bit patterns of |a| in [2^-100, 2^40], both signs, and +0
 __global__ void k_exhaustive(const float* divisors, int nDiv, unsigned long long* bad) {
-  const uint32_t lo = __float_as_uint(0x1p-40f);
+  const uint32_t lo = __float_as_uint(0x1p-100f);
   const uint32_t hi = __float_as_uint(0x1p40f);
   const uint64_t n = (uint64_t)(hi - lo + 1) * 2;
   unsigned long long local = 0;
@@ -26,9 +28,11 @@ __global__ void k_exhaustive(const float* divisors, int nDiv, unsigned long long
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
       const uint32_t bits = lo + (uint32_t)(i >> 1) | ((uint32_t)(i & 1) << 31);
       const float a = __uint_as_float(bits);
-      if (!div_ok(a)) continue;
       if (__float_as_uint(div_fast(a, b, rb)) != __float_as_uint(__fdiv_rn(a, b))) ++local;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0 &&
+        __float_as_uint(div_fast(0.f, b, rb)) != __float_as_uint(__fdiv_rn(0.f, b)))
+      ++local;
   }
   if (local) atomicAdd(bad, local);
 }
@@ -42,18 +46,17 @@ __device__ __forceinline__ uint32_t mix(uint64_t x) {
   return (uint32_t)x;
 }
 
-__device__ __forceinline__ float in_window(uint32_t r) {
-  // exponent uniform over the window, random mantissa and sign
-  const uint32_t e = 127 - 40 + (r % 80);
+__device__ __forceinline__ float in_window(uint32_t r, int lo, int span) {
+  // exponent uniform over [2^lo, 2^(lo+span)), random mantissa and sign
+  const uint32_t e = 127 + lo + (r % span);
   return __uint_as_float((r & 0x80000000u) | (e << 23) | (mix(r) & 0x7FFFFFu));
 }
 
 __global__ void k_random(uint64_t n, unsigned long long* bad) {
   unsigned long long local = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const float a = in_window(mix(2 * i + 1));
-    const float b = in_window(mix(2 * i + 2));
-    if (!div_ok(a) || !div_ok(b)) continue;
+    const float a = in_window(mix(2 * i + 1), -100, 140);
+    const float b = in_window(mix(2 * i + 2), -40, 80);
     if (__float_as_uint(div_fast(a, b, div_rcp(b))) != __float_as_uint(__fdiv_rn(a, b))) ++local;
   }
   if (local) atomicAdd(bad, local);

@@ -1,0 +1,32 @@
+#!/usr/bin/env python
+"""Ray-march statistics of the C2 frames (needs a RFG_RC_STATS build:
+RFG_LIB_PATH=.variants/stats/librfg.so)."""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1708_00783_b200 import _lib  # noqa: E402
+from paper_1708_00783_b200 import fusion as F  # noqa: E402
+
+intr = F.Intrinsics(640, 480, 525.0, 525.0, 319.5, 239.5)
+poses = F.orbit_trajectory(frames=100)
+m = F.VoxelBlockMap(F.VoxelBlockMapConfig(0x40000, 0x20000, 0x40000))
+p = F.Pipeline(m, intr, F.SceneParams(), use_graph=False, profile=True)
+L = _lib.lib()
+buf = (C.c_ulonglong * 32)()
+for f in range(40):
+    raw = torch.from_numpy(F.synth_render(0, poses[f], intr)[0].view(np.int16)).cuda()
+    if f == 30:
+        L.rfg_debug_rc_stats(buf, 1)
+    p.process(raw, poses[0] if f == 0 else None)
+torch.cuda.synchronize()
+L.rfg_debug_rc_stats(buf, 0)
+s = list(buf)
+nf = 10
+print(f"per frame: rays {s[0]/nf:.0f} steps {s[1]/nf:.0f} coarse {s[2]/nf:.0f} invalid-fine {s[3]/nf:.0f} "
+      f"nearest {s[4]/nf:.0f} trilinear {s[5]/nf:.0f} lookups {s[6]/nf:.0f}  max steps {s[31]}")
+print("steps/ray histogram (log2 buckets):", {f"<{2**b}": s[8 + b] // nf for b in range(16) if s[8 + b]})
