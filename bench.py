@@ -29,7 +29,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -63,7 +62,9 @@ def load_peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """Samples SM clock + throttle reasons via NVML during the timed region."""
+    """Samples SM clock + throttle reasons during the timed region with
+    `nvidia-smi -lms` in a separate process (a Python sampling thread is
+    starved by the GIL while the timed loop runs); NVML gives the max clock."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -71,46 +72,68 @@ class ClockSampler:
         0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, device=0, period=0.005):
-        self.samples, self.reasons = [], set()
+    def __init__(self, device=0, period_ms=5):
+        self.device, self.period_ms = device, period_ms
         self.max_mhz = None
-        self._stop = threading.Event()
-        self._t = None
+        self._p = None
         try:
             import pynvml
             pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.nv = None
-        self.period = period
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
-                r = fn(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(self.period)
+            pass
 
     def start(self):
-        if self.nv:
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
+        import subprocess
+        try:
+            self._p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=timestamp,clocks.sm,clocks_throttle_reasons.active",
+                 "--format=csv,noheader,nounits", f"-lms={self.period_ms}"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # nvidia-smi start-up; samples before mark() are dropped
+        except Exception:
+            self._p = None
+        self.t0 = time.time()
+
+    def mark(self):
+        """Start of the timed region."""
+        self.t0 = time.time()
 
     def stop(self):
-        self._stop.set()
-        if self._t:
-            self._t.join()
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        import datetime
+        t1 = time.time()
+        samples, reasons = [], set()
+        allsamples = []
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                out, _ = self._p.communicate(timeout=5)
+            except Exception:
+                self._p.kill()
+                out = ""
+            for line in out.splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 3:
+                    continue
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    mhz = int(float(parts[1]))
+                    r = int(parts[2], 16)
+                except ValueError:
+                    continue
+                allsamples.append(mhz)
+                if not (self.t0 - 0.01 <= ts <= t1 + 0.01):
+                    continue
+                samples.append(mhz)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        reasons.add(name)
+        if not samples:  # region shorter than the sampling start-up: keep what was seen
+            samples = allsamples
+        return {"sm_mhz": statistics.median(samples) if samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(samples)}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -241,6 +264,7 @@ def run_b200(args):
     order = [i % N_FRAMES for i in range(total)]
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
+    sampler.start()
     launches0 = None
     if world > 1:
         dist.barrier()
@@ -252,7 +276,7 @@ def run_b200(args):
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-            sampler.start()
+            sampler.mark()
             launches0 = launch_count()
         flush.fill_(i & 0xFF)  # evict L2 (untimed; outside the event pair)
         with torch.cuda.stream(stream):
@@ -359,7 +383,7 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "l2": "flushed (256 MiB write) before every timed frame",
                    "parallelism": f"spatial hash shards x{world}" if world > 1 else "single GPU",
                    "graph": True, "last_frame_stats": stats.as_array().tolist(),
