@@ -142,6 +142,40 @@ int rfg_render_icp_maps_list(rfg_map* map, const float pose34[12], const rfg_int
 int rfg_build_view_depth(const uint16_t* raw_dev, int width, int height, float aff_scale, float aff_offset, int levels,
                          float* depth_levels_dev, void* cuda_stream);
 
+/* Full ViewBuilder (proj/src/view.cpp:8-143, build_view with every option):
+ * raw u16 depth (host byte order, or the big-endian payload of a PGM16 file
+ * when raw_big_endian = 1, image_io.cpp:96-113) -> metres; bilateral = 1
+ * applies bilateral_filter(depth, 2, 10 |aff_scale|) (needs scratch_dev,
+ * width*height floats); normals_dev (float4 per pixel, may be NULL) =
+ * compute_normals of the level-0 depth; with rgb_dev (packed RGB8, may be
+ * NULL) intensity_levels_dev gets rgb_to_intensity + downsample_intensity
+ * levels.  Depth / intensity levels are written back to back.  The filter's
+ * std::exp is reproduced bit-for-bit (glibc expf, see rfg_view.cu). */
+int rfg_build_view(const uint16_t* raw_dev, const uint8_t* rgb_dev, const rfg_intrinsics* intr_d, float aff_scale,
+                   float aff_offset, int bilateral, int levels, int raw_big_endian, float* depth_levels_dev,
+                   float* intensity_levels_dev, float* normals_dev, float* scratch_dev, void* cuda_stream);
+/* The ViewBuilder's elements (view.hpp:44-62), device images. */
+int rfg_bilateral_filter(const float* depth_dev, int width, int height, float spatial_sigma, float range_sigma,
+                         float* out_dev, void* cuda_stream);
+int rfg_compute_normals(const float* depth_dev, const rfg_intrinsics* intr, float* normals_dev, void* cuda_stream);
+int rfg_rgb_to_intensity(const uint8_t* rgb_dev, int width, int height, float* out_dev, void* cuda_stream);
+int rfg_downsample_intensity(const float* in_dev, int width, int height, float* out_dev, void* cuda_stream);
+
+/* ------------------------------------------------------------ image IO */
+/* Netpbm IO (proj/src/image_io.cpp, host memory).  The readers return
+ * RFG_EINVAL with the reference's exception message (rfg_last_error) on a
+ * missing file, wrong magic / maxval or truncated data, and RFG_ERANGE when
+ * capacity (pixels) is too small; *width / *height are set either way when
+ * the header parsed.  read_pgm16 returns host-order values;
+ * read_pgm16_payload returns the pixel bytes as stored (big-endian), to be
+ * uploaded as-is and decoded on the GPU (rfg_build_view raw_big_endian = 1,
+ * rfg_pipeline_process_pgm). */
+int rfg_read_pgm16(const char* path, uint16_t* out, int64_t capacity, int* width, int* height);
+int rfg_read_pgm16_payload(const char* path, void* out, int64_t capacity, int* width, int* height);
+int rfg_read_ppm(const char* path, uint8_t* out_rgb, int64_t capacity, int* width, int* height);
+int rfg_write_pgm16(const char* path, const uint16_t* img, int width, int height);
+int rfg_write_ppm(const char* path, const uint8_t* rgb, int width, int height);
+
 /* ----------------------------------------------------------------- ICP */
 /* Point-to-plane ICP tracker (ITMDepthTracker; absent in the reference, see
  * DESIGN.md "ICP oracle" and SPEC.md:348-356).  depth_levels_dev as produced
@@ -181,6 +215,8 @@ typedef struct {
   int32_t min_count;
   int32_t use_graph;       /* capture the frame into a CUDA graph */
   int32_t profile;         /* record CUDA events between stages (non-graph mode only) */
+  int32_t bilateral;       /* ViewBuildOptions::bilateral (view.hpp:13) */
+  int32_t raw_big_endian;  /* raw frames are PGM16 payloads (decoded in the view stage) */
 } rfg_pipeline_config;
 
 int rfg_pipeline_create(rfg_map* map, const rfg_pipeline_config* cfg, rfg_pipeline** out);
@@ -192,6 +228,10 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const flo
 /* Enqueue one frame from HOST raw depth (copied H2D inside the call). */
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* raw_host, const float* pose34);
 /* Read back the last frame's stats and pose (synchronises). */
+/* One frame straight from a PGM16 file (image_io.cpp:96-113): the payload is
+ * read into pinned staging and uploaded as stored; with raw_big_endian = 1
+ * the GPU view stage decodes it (no host pass over the pixels). */
+int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float pose34[12]);
 int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float pose_out34[12], double icp_stats8[8]);
 /* Device pointers of the pipeline's buffers (for parity checks). */
 int rfg_pipeline_buffers(rfg_pipeline* p, float** depth_levels, float** range, float** raycast, float** points,

@@ -58,6 +58,13 @@ def lib():
         L.rr_export_blocks.argtypes = [C.c_void_p, _i, C.c_int, _u8]
         L.rr_export_visible.argtypes = [C.c_void_p, _i, _u8]
         L.rr_free_counts.argtypes = [C.c_void_p, _i, _i]
+        L.rr_build_view_full.argtypes = [_u16, _u8, _i, _f, C.c_float, C.c_float, C.c_int, C.c_int, _f, _f, _f]
+        L.rr_bilateral_filter.argtypes = [_f, C.c_int, C.c_int, C.c_float, C.c_float, _f]
+        L.rr_compute_normals.argtypes = [_f, _i, _f, _f]
+        L.rr_read_pgm16.argtypes = [C.c_char_p, _u16, C.c_int, _i, _i]
+        L.rr_read_ppm.argtypes = [C.c_char_p, _u8, C.c_int, _i, _i]
+        L.rr_write_pgm16.argtypes = [C.c_char_p, _u16, C.c_int, C.c_int]
+        L.rr_write_ppm.argtypes = [C.c_char_p, _u8, C.c_int, C.c_int]
         _lib = L
     return _lib
 
@@ -116,6 +123,125 @@ def build_view(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=1):
         res.append(out[o:o + s].reshape(h >> l, w >> l))
         o += s
     return res
+
+
+def _view_full(fn, raw, rgb, intr, aff, levels, bilateral):
+    w, h = intr["width"], intr["height"]
+    sizes = [(w >> l) * (h >> l) for l in range(levels)]
+    dep = np.zeros(sum(sizes), np.float32)
+    inten = np.zeros(sum(sizes), np.float32) if rgb is not None else None
+    nrm = np.zeros((h, w, 4), np.float32)
+    raw = np.ascontiguousarray(raw, np.uint16)
+    rgb = np.ascontiguousarray(rgb, np.uint8) if rgb is not None else None
+    wh, f4 = _wh(intr), _f4(intr)
+    rc = fn(P(raw, _u16), P(rgb, _u8), P(wh, _i), P(f4, _f), aff[0], aff[1], 1 if bilateral else 0, levels,
+            P(dep, _f), P(inten, _f), P(nrm, _f))
+    assert rc == 0
+    d, it, o = [], [], 0
+    for l, s in enumerate(sizes):
+        d.append(dep[o:o + s].reshape(h >> l, w >> l))
+        if inten is not None:
+            it.append(inten[o:o + s].reshape(h >> l, w >> l))
+        o += s
+    return {"depth": d, "intensity": it if inten is not None else None, "normals": nrm}
+
+
+def build_view_full(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=3, bilateral=False, rgb=None):
+    """build_view with every option (view.cpp:100-143): depth / intensity
+    pyramids and level-0 normals."""
+    return _view_full(lib().rr_build_view_full, raw, rgb, intr, aff, levels, bilateral)
+
+
+def bilateral_filter(depth, spatial_sigma, range_sigma):
+    d = _f32(depth)
+    out = np.zeros_like(d)
+    lib().rr_bilateral_filter(P(d, _f), d.shape[1], d.shape[0], spatial_sigma, range_sigma, P(out, _f))
+    return out
+
+
+def compute_normals(depth, intr):
+    d = _f32(depth)
+    out = np.zeros(d.shape + (4,), np.float32)
+    wh, f4 = _wh(intr), _f4(intr)
+    lib().rr_compute_normals(P(d, _f), P(wh, _i), P(f4, _f), P(out, _f))
+    return out
+
+
+# The reference's Netpbm IO goes through iostreams, which crash in a process
+# that has numpy's C extension loaded (its bundled C++ runtime interferes);
+# these four calls therefore run the reference in a numpy-free subprocess.
+_IO_SCRIPT = r"""
+import ctypes as C, sys
+L = C.CDLL(sys.argv[1])
+op, path, blob = sys.argv[2], sys.argv[3].encode(), sys.argv[4]
+if op in ("rpgm", "rppm"):
+    cap = 1 << 22
+    elem = 2 if op == "rpgm" else 3
+    buf = (C.c_uint8 * (cap * elem))()
+    w, h = C.c_int(0), C.c_int(0)
+    fn = L.rr_read_pgm16 if op == "rpgm" else L.rr_read_ppm
+    rc = fn(path, buf, cap if op == "rpgm" else cap * 3, C.byref(w), C.byref(h))
+    with open(blob, "wb") as f:
+        f.write(rc.to_bytes(4, "little", signed=True) + w.value.to_bytes(4, "little") + h.value.to_bytes(4, "little"))
+        if rc == 0:
+            f.write(bytes(buf)[: w.value * h.value * elem])
+else:
+    w, h = int(sys.argv[5]), int(sys.argv[6])
+    data = open(blob, "rb").read()
+    buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+    fn = L.rr_write_pgm16 if op == "wpgm" else L.rr_write_ppm
+    sys.exit(0 if fn(path, buf, w, h) == 0 else 3)
+"""
+
+
+def _io(op, path, blob, *extra):
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "-c", _IO_SCRIPT, LIB_PATH, op, path, blob, *map(str, extra)],
+                       capture_output=True, text=True)
+    return r.returncode
+
+
+def _read(op, path, elem):
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".bin") as t:
+        rc = _io(op, path, t.name)
+        if rc != 0:
+            raise RuntimeError(f"reference IO helper failed ({rc})")
+        b = open(t.name, "rb").read()
+    code = int.from_bytes(b[0:4], "little", signed=True)
+    w, h = int.from_bytes(b[4:8], "little"), int.from_bytes(b[8:12], "little")
+    if code != 0:
+        return None
+    if elem == 2:
+        return np.frombuffer(b[12:], np.uint16).reshape(h, w).copy()
+    return np.frombuffer(b[12:], np.uint8).reshape(h, w, 3).copy()
+
+
+def read_pgm16(path):
+    """The reference's read_pgm16 (None on its exception)."""
+    return _read("rpgm", path, 2)
+
+
+def read_ppm(path):
+    return _read("rppm", path, 3)
+
+
+def _write(op, img, path, dtype):
+    import tempfile
+    a = np.ascontiguousarray(img, dtype)
+    with tempfile.NamedTemporaryFile(suffix=".bin") as t:
+        t.write(a.tobytes())
+        t.flush()
+        return 0 if _io(op, path, t.name, a.shape[1], a.shape[0]) == 0 else -1
+
+
+def write_pgm16(img, path):
+    return _write("wpgm", img, path, np.uint16)
+
+
+def write_ppm(img, path):
+    return _write("wppm", img, path, np.uint8)
 
 
 class RefEngine:

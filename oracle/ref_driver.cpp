@@ -19,6 +19,7 @@
 #include <memory>
 
 #include "rf/fusion.hpp"
+#include "rf/image_io.hpp"
 #include "rf/raycast.hpp"
 #include "rf/synth.hpp"
 #include "rf/view.hpp"
@@ -190,6 +191,110 @@ int rr_build_view(const std::uint16_t* raw, const int* wh, const float* f4, floa
     out += d.size();
   }
   return 0;
+}
+
+// full ViewBuilder (view.cpp:8-143): every option; outputs packed per level,
+// intensity / normals may be null
+int rr_build_view_full(const std::uint16_t* raw, const std::uint8_t* rgb, const int* wh, const float* f4,
+                       float affScale, float affOffset, int bilateral, int levels, float* depthLevels,
+                       float* intensityLevels, float* normals4) {
+  RgbdCalib calib;
+  calib.intrinsics_d = intrFrom(wh, f4);
+  calib.intrinsics_rgb = calib.intrinsics_d;
+  calib.depth_affine.scale = affScale;
+  calib.depth_affine.offset = affOffset;
+  Image<std::uint16_t> img(wh[0], wh[1]);
+  std::memcpy(img.data(), raw, sizeof(std::uint16_t) * wh[0] * wh[1]);
+  Image<Rgb8> col;
+  if (rgb) {
+    col = Image<Rgb8>(wh[0], wh[1]);
+    std::memcpy(col.data(), rgb, 3 * (size_t)wh[0] * wh[1]);
+  }
+  ViewBuildOptions opts;
+  opts.levels = levels;
+  opts.bilateral = bilateral != 0;
+  View v;
+  try {
+    v = build_view(img, col, calib, opts);
+  } catch (const std::exception&) {
+    return -1;
+  }
+  float* out = depthLevels;
+  float* outI = intensityLevels;
+  for (int l = 0; l < levels; ++l) {
+    const auto& d = v.pyramid[l].depth;
+    std::memcpy(out, d.data(), sizeof(float) * d.size());
+    out += d.size();
+    if (rgb && outI) {
+      const auto& it = v.pyramid[l].intensity;
+      std::memcpy(outI, it.data(), sizeof(float) * it.size());
+      outI += it.size();
+    }
+  }
+  if (normals4) std::memcpy(normals4, v.normals.data(), sizeof(float) * 4 * v.normals.size());
+  return 0;
+}
+
+int rr_bilateral_filter(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out) {
+  Image<float> img(w, h);
+  std::memcpy(img.data(), in, sizeof(float) * (size_t)w * h);
+  const Image<float> o = bilateral_filter(img, spatialSigma, rangeSigma);
+  std::memcpy(out, o.data(), sizeof(float) * (size_t)w * h);
+  return 0;
+}
+
+int rr_compute_normals(const float* in, const int* wh, const float* f4, float* out4) {
+  Image<float> img(wh[0], wh[1]);
+  std::memcpy(img.data(), in, sizeof(float) * (size_t)wh[0] * wh[1]);
+  const auto o = compute_normals(img, intrFrom(wh, f4));
+  std::memcpy(out4, o.data(), sizeof(float) * 4 * o.size());
+  return 0;
+}
+
+// image_io.cpp: Netpbm readers / writers (0 ok, -1 on the reference's exception)
+int rr_read_pgm16(const char* path, std::uint16_t* out, int capacity, int* w, int* h) {
+  try {
+    const auto img = read_pgm16(path);
+    *w = img.width();
+    *h = img.height();
+    if ((long)img.size() > capacity) return -2;
+    std::memcpy(out, img.data(), sizeof(std::uint16_t) * img.size());
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+int rr_read_ppm(const char* path, std::uint8_t* out, int capacity, int* w, int* h) {
+  try {
+    const auto img = read_ppm(path);
+    *w = img.width();
+    *h = img.height();
+    if ((long)img.size() * 3 > capacity) return -2;
+    std::memcpy(out, img.data(), 3 * img.size());
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+int rr_write_pgm16(const char* path, const std::uint16_t* in, int w, int h) {
+  try {
+    Image<std::uint16_t> img(w, h);
+    std::memcpy(img.data(), in, sizeof(std::uint16_t) * (size_t)w * h);
+    write_pgm16(img, path);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+int rr_write_ppm(const char* path, const std::uint8_t* in, int w, int h) {
+  try {
+    Image<Rgb8> img(w, h);
+    std::memcpy(img.data(), in, 3 * (size_t)w * h);
+    write_ppm(img, path);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
 }
 
 // -------------------------------------------------------------- elements

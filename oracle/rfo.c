@@ -930,6 +930,154 @@ int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float aff
   return 0;
 }
 
+/* ------------------------------------------------- full ViewBuilder */
+/* rgb_to_intensity (P/src/view.cpp:8-16): (0.299 r + 0.587 g + 0.114 b) / 255,
+ * C++ left-to-right evaluation, the channels promoted to float. */
+void rfo_rgb_to_intensity(const uint8_t* rgb, int w, int h, float* out) {
+  for (int i = 0; i < w * h; ++i) {
+    const uint8_t* c = rgb + 3 * (size_t)i;
+    out[i] = (0.299f * (float)c[0] + 0.587f * (float)c[1] + 0.114f * (float)c[2]) / 255.f;
+  }
+}
+
+/* bilateral_filter (view.cpp:18-44): 5x5 window, invalid (<= 0) centre and
+ * neighbours skipped, w = exp(-(dx^2 + dy^2) invS2 - dr^2 invR2) with the C
+ * library's expf (the reference calls std::exp(float)); out = sum / wsum. */
+void rfo_bilateral_filter(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out) {
+  const int radius = 2;
+  const float invS2 = 1.f / (2.f * spatialSigma * spatialSigma);
+  const float invR2 = 1.f / (2.f * rangeSigma * rangeSigma);
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const float centre = in[(size_t)y * w + x];
+      out[(size_t)y * w + x] = -1.f;
+      if (centre <= 0.f) continue;
+      float sum = 0.f, wsum = 0.f;
+      for (int dy = -radius; dy <= radius; ++dy)
+        for (int dx = -radius; dx <= radius; ++dx) {
+          const int nx = x + dx, ny = y + dy;
+          if (nx < 0 || ny < 0 || nx >= w || ny >= h) continue;
+          const float d = in[(size_t)ny * w + nx];
+          if (d <= 0.f) continue;
+          const float dr = d - centre;
+          const float wt = expf((float)(-(dx * dx + dy * dy)) * invS2 - dr * dr * invR2);
+          sum += wt * d;
+          wsum += wt;
+        }
+      out[(size_t)y * w + x] = sum / wsum;
+    }
+}
+
+/* compute_normals (view.cpp:46-67): central differences of backprojected
+ * points, n = px x py / |px x py| (Eigen: cross components as written, norm =
+ * sqrt(x^2 + (y^2 + z^2)), per-coefficient division), oriented toward the
+ * camera; (0,0,0,-1) where invalid, on the border, or |n| < 1e-12. */
+static void bp3(const intr_t* in, float u, float v, float z, float* o) {
+  o[0] = (u - in->cx) / in->fx * z;
+  o[1] = (v - in->cy) / in->fy * z;
+  o[2] = z;
+}
+void rfo_compute_normals(const float* d, int w, int h, const float* f4, float* out4) {
+  const intr_t in = {w, h, f4[0], f4[1], f4[2], f4[3]};
+  for (int i = 0; i < w * h; ++i) {
+    out4[4 * i + 0] = 0.f;
+    out4[4 * i + 1] = 0.f;
+    out4[4 * i + 2] = 0.f;
+    out4[4 * i + 3] = -1.f;
+  }
+  for (int y = 1; y + 1 < h; ++y)
+    for (int x = 1; x + 1 < w; ++x) {
+      const float dc = d[(size_t)y * w + x];
+      const float dxm = d[(size_t)y * w + x - 1], dxp = d[(size_t)y * w + x + 1];
+      const float dym = d[(size_t)(y - 1) * w + x], dyp = d[(size_t)(y + 1) * w + x];
+      if (dc <= 0.f || dxm <= 0.f || dxp <= 0.f || dym <= 0.f || dyp <= 0.f) continue;
+      float a[3], b[3], px[3], py[3], n[3], c[3];
+      bp3(&in, (float)x + 1.f, (float)y, dxp, a);
+      bp3(&in, (float)x - 1.f, (float)y, dxm, b);
+      for (int k = 0; k < 3; ++k) px[k] = a[k] - b[k];
+      bp3(&in, (float)x, (float)y + 1.f, dyp, a);
+      bp3(&in, (float)x, (float)y - 1.f, dym, b);
+      for (int k = 0; k < 3; ++k) py[k] = a[k] - b[k];
+      n[0] = px[1] * py[2] - px[2] * py[1];
+      n[1] = px[2] * py[0] - px[0] * py[2];
+      n[2] = px[0] * py[1] - px[1] * py[0];
+      const float len = sqrtf(n[0] * n[0] + (n[1] * n[1] + n[2] * n[2]));
+      if (len < 1e-12f) continue;
+      for (int k = 0; k < 3; ++k) n[k] /= len;
+      bp3(&in, (float)x, (float)y, dc, c);
+      if (n[0] * c[0] + (n[1] * c[1] + n[2] * c[2]) > 0.f)
+        for (int k = 0; k < 3; ++k) n[k] = -n[k];
+      float* o = out4 + 4 * ((size_t)y * w + x);
+      o[0] = n[0];
+      o[1] = n[1];
+      o[2] = n[2];
+      o[3] = 1.f;
+    }
+}
+
+/* downsample_intensity (view.cpp:90-98): 0.25 * (((a + b) + c) + d). */
+void rfo_downsample_intensity(const float* in, int w, int h, float* out) {
+  const int lw = w / 2, lh = h / 2;
+  for (int y = 0; y < lh; ++y)
+    for (int x = 0; x < lw; ++x)
+      out[(size_t)y * lw + x] = 0.25f * (in[(size_t)(2 * y) * w + 2 * x] + in[(size_t)(2 * y) * w + 2 * x + 1] +
+                                         in[(size_t)(2 * y + 1) * w + 2 * x] +
+                                         in[(size_t)(2 * y + 1) * w + 2 * x + 1]);
+}
+
+/* build_view (view.cpp:100-143) with every option: depth conversion,
+ * optional bilateral (spatial sigma 2, range sigma 10 |scale|), intensity
+ * when rgb is given, level-0 normals, depth (+ intensity) pyramids.
+ * Outputs are packed level after level; intensity / normals may be NULL. */
+int rfo_build_view_full(const uint16_t* raw, const uint8_t* rgb, const int* wh, const float* f4, float affScale,
+                        float affOffset, int bilateral, int levels, float* depthLevels, float* intensityLevels,
+                        float* normals4) {
+  const int w = wh[0], h = wh[1];
+  if (levels < 1) return -1;
+  if (rfo_build_view(raw, wh, affScale, affOffset, 1, depthLevels) != 0) return -1;
+  if (bilateral) {
+    float* tmp = (float*)malloc(sizeof(float) * (size_t)w * h);
+    if (!tmp) return -1;
+    memcpy(tmp, depthLevels, sizeof(float) * (size_t)w * h);
+    rfo_bilateral_filter(tmp, w, h, 2.f, 10.f * fabsf(affScale), depthLevels);
+    free(tmp);
+  }
+  if (normals4) rfo_compute_normals(depthLevels, w, h, f4, normals4);
+  if (rgb && intensityLevels) rfo_rgb_to_intensity(rgb, w, h, intensityLevels);
+  const float* prev = depthLevels;
+  const float* prevI = intensityLevels;
+  float* out = depthLevels + (size_t)w * h;
+  float* outI = intensityLevels ? intensityLevels + (size_t)w * h : NULL;
+  int pw = w, ph = h;
+  for (int l = 1; l < levels; ++l) {
+    const int lw = pw / 2, lh = ph / 2;
+    for (int y = 0; y < lh; ++y)
+      for (int x = 0; x < lw; ++x) {
+        float sum = 0.f;
+        int n = 0;
+        for (int dy = 0; dy < 2; ++dy)
+          for (int dx = 0; dx < 2; ++dx) {
+            const float dd = prev[(size_t)(2 * y + dy) * pw + 2 * x + dx];
+            if (dd > 0.f) {
+              sum += dd;
+              ++n;
+            }
+          }
+        out[(size_t)y * lw + x] = n > 0 ? sum / (float)n : -1.f;
+      }
+    if (rgb && outI) {
+      rfo_downsample_intensity(prevI, pw, ph, outI);
+      prevI = outI;
+      outI += (size_t)lw * lh;
+    }
+    prev = out;
+    out += (size_t)lw * lh;
+    pw = lw;
+    ph = lh;
+  }
+  return 0;
+}
+
 /* ---------------------------------------------------------------- ICP */
 /* One evaluation of the point-to-plane normal equations:
  * per valid pixel p of the level, p_w = T_cw p_cam; project p_w into the last

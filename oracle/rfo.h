@@ -65,6 +65,14 @@ int rfo_render_icp_list(rfo_map* m, const float* pose12, const int* wh, const fl
  * pyramid level, concatenated into depthLevels. */
 int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float affOffset, int levels,
                    float* depthLevels);
+/* full ViewBuilder (view.cpp:8-143) */
+void rfo_rgb_to_intensity(const uint8_t* rgb, int w, int h, float* out);
+void rfo_bilateral_filter(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out);
+void rfo_compute_normals(const float* depth, int w, int h, const float* f4, float* out4);
+void rfo_downsample_intensity(const float* in, int w, int h, float* out);
+int rfo_build_view_full(const uint16_t* raw, const uint8_t* rgb, const int* wh, const float* f4, float affScale,
+                        float affOffset, int bilateral, int levels, float* depthLevels, float* intensityLevels,
+                        float* normals4);
 
 /* ICP point-to-plane depth tracker (absent in the reference; restated from
  * see DESIGN.md "ICP oracle").

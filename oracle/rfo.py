@@ -12,7 +12,7 @@ import subprocess
 
 import numpy as np
 
-from .ref import P, _d, _f, _f4, _f32, _i, _u8, _u16, _wh, params_vec
+from .ref import P, _d, _f, _f4, _f32, _i, _u8, _u16, _view_full, _wh, params_vec
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "librfo.so")
@@ -48,6 +48,11 @@ def lib():
         L.rfo_set_ranges.argtypes = [vp, _i, _f]
         L.rfo_render_icp.argtypes = [vp, _f, _i, _f, _f, _f, _f, _f]
         L.rfo_build_view.argtypes = [_u16, _i, C.c_float, C.c_float, C.c_int, _f]
+        L.rfo_build_view_full.argtypes = [_u16, _u8, _i, _f, C.c_float, C.c_float, C.c_int, C.c_int, _f, _f, _f]
+        L.rfo_bilateral_filter.argtypes = [_f, C.c_int, C.c_int, C.c_float, C.c_float, _f]
+        L.rfo_compute_normals.argtypes = [_f, C.c_int, C.c_int, _f, _f]
+        L.rfo_rgb_to_intensity.argtypes = [_u8, C.c_int, C.c_int, _f]
+        L.rfo_downsample_intensity.argtypes = [_f, C.c_int, C.c_int, _f]
         L.rfo_icp_track.argtypes = [_f, _i, _f, _f, _f, _f, _f, _f, _i, _f, _f, _d]
         L.rfo_icp_reduce.argtypes = [_f, C.c_int, C.c_int, _f, _f, _f, _i, _f, _f, _f, C.c_float, _d]
         L.rfo_solve6.argtypes = [_d, _d]
@@ -95,6 +100,43 @@ def build_view(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=1):
         res.append(out[o:o + s].reshape(h >> l, w >> l))
         o += s
     return res
+
+
+def build_view_full(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=3, bilateral=False, rgb=None):
+    """rfo_build_view_full (view.cpp:100-143 with every option)."""
+    L = lib()
+
+    def fn(raw_p, rgb_p, wh_p, f4_p, s, o, b, lv, dep_p, it_p, n_p):
+        return L.rfo_build_view_full(raw_p, rgb_p, wh_p, f4_p, s, o, b, lv, dep_p, it_p, n_p)
+    return _view_full(fn, raw, rgb, intr, aff, levels, bilateral)
+
+
+def bilateral_filter(depth, spatial_sigma, range_sigma):
+    d = _f32(depth)
+    out = np.zeros_like(d)
+    lib().rfo_bilateral_filter(P(d, _f), d.shape[1], d.shape[0], spatial_sigma, range_sigma, P(out, _f))
+    return out
+
+
+def compute_normals(depth, intr):
+    d = _f32(depth)
+    out = np.zeros(d.shape + (4,), np.float32)
+    lib().rfo_compute_normals(P(d, _f), d.shape[1], d.shape[0], P(_f4(intr), _f), P(out, _f))
+    return out
+
+
+def rgb_to_intensity(rgb):
+    c = np.ascontiguousarray(rgb, np.uint8)
+    out = np.zeros(c.shape[:2], np.float32)
+    lib().rfo_rgb_to_intensity(P(c, _u8), c.shape[1], c.shape[0], P(out, _f))
+    return out
+
+
+def downsample_intensity(img):
+    a = _f32(img)
+    out = np.zeros((a.shape[0] // 2, a.shape[1] // 2), np.float32)
+    lib().rfo_downsample_intensity(P(a, _f), a.shape[1], a.shape[0], P(out, _f))
+    return out
 
 
 def icp_track(levels_depth, intr, points, normals, render_pose34, render_intr, init_pose34,

@@ -47,7 +47,8 @@ class PipelineConfig_(C.Structure):
     _fields_ = [("intr", Intrinsics_), ("params", SceneParams_), ("aff_scale", C.c_float),
                 ("aff_offset", C.c_float), ("levels", C.c_int32), ("track", C.c_int32),
                 ("iters", C.c_int32 * 3), ("dist", C.c_float * 3), ("min_count", C.c_int32),
-                ("use_graph", C.c_int32), ("profile", C.c_int32)]
+                ("use_graph", C.c_int32), ("profile", C.c_int32), ("bilateral", C.c_int32),
+                ("raw_big_endian", C.c_int32)]
 
 
 # every symbol include/rfg.h declares, with its ctypes signature
@@ -77,6 +78,17 @@ SIGNATURES = {
     "rfg_render_icp_maps_list": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), _vp, _vp, _vp, _vp,
                                   _vp, _vp], C.c_int),
     "rfg_build_view_depth": ([_vp, C.c_int, C.c_int, C.c_float, C.c_float, C.c_int, _vp, _vp], C.c_int),
+    "rfg_build_view": ([_vp, _vp, C.POINTER(Intrinsics_), C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, _vp, _vp,
+                        _vp, _vp, _vp], C.c_int),
+    "rfg_bilateral_filter": ([_vp, C.c_int, C.c_int, C.c_float, C.c_float, _vp, _vp], C.c_int),
+    "rfg_compute_normals": ([_vp, C.POINTER(Intrinsics_), _vp, _vp], C.c_int),
+    "rfg_rgb_to_intensity": ([_vp, C.c_int, C.c_int, _vp, _vp], C.c_int),
+    "rfg_downsample_intensity": ([_vp, C.c_int, C.c_int, _vp, _vp], C.c_int),
+    "rfg_read_pgm16": ([C.c_char_p, _vp, C.c_int64, _i, _i], C.c_int),
+    "rfg_read_pgm16_payload": ([C.c_char_p, _vp, C.c_int64, _i, _i], C.c_int),
+    "rfg_read_ppm": ([C.c_char_p, _vp, C.c_int64, _i, _i], C.c_int),
+    "rfg_write_pgm16": ([C.c_char_p, _vp, C.c_int, C.c_int], C.c_int),
+    "rfg_write_ppm": ([C.c_char_p, _vp, C.c_int, C.c_int], C.c_int),
     "rfg_icp_track": ([_vp, _vp, C.c_int, C.POINTER(Intrinsics_), _vp, _vp, _f, _f, _i, _f, C.c_int, _f, _d],
                       C.c_int),
     "rfg_icp_reduce": ([_vp, _vp, C.c_int, C.POINTER(Intrinsics_), _vp, _vp, _f, _f, C.c_float, _d], C.c_int),
@@ -84,6 +96,7 @@ SIGNATURES = {
     "rfg_pipeline_destroy": ([_vp], C.c_int),
     "rfg_pipeline_process_raw": ([_vp, _vp, _f], C.c_int),
     "rfg_pipeline_process_host": ([_vp, _vp, _f], C.c_int),
+    "rfg_pipeline_process_pgm": ([_vp, C.c_char_p, _f], C.c_int),
     "rfg_pipeline_result": ([_vp, C.POINTER(AllocStats_), _f, _d], C.c_int),
     "rfg_pipeline_buffers": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                               C.POINTER(_vp)], C.c_int),

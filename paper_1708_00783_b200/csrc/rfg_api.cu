@@ -15,6 +15,16 @@ std::atomic<uint64_t> g_launches{0};
 static thread_local std::string t_lastError;
 void set_error(const std::string& msg) { t_lastError = msg; }
 
+// rfg_view.cu
+cudaError_t launch_build_view_full(const uint16_t* raw, const uint8_t* rgb, const Intr& in, float scale, float offset,
+                                   int bilateral, int levels, int bigEndian, float* depthLevels,
+                                   float* intensityLevels, float4* normals, float* scratch, cudaStream_t s);
+cudaError_t launch_bilateral(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out,
+                             cudaStream_t s);
+cudaError_t launch_view_normals(const float* depth, const Intr& in, float4* out, cudaStream_t s);
+cudaError_t launch_intensity(const uint8_t* rgb, int w, int h, float* out, cudaStream_t s);
+cudaError_t launch_downsample_intensity(const float* in, int w, int h, float* out, cudaStream_t s);
+
 // rfg_icp.cu
 size_t icp_state_bytes();
 int icp_partial_slots();
@@ -388,6 +398,46 @@ int rfg_build_view_depth(const uint16_t* raw, int w, int h, float scale, float o
   return RFG_OK;
 }
 
+int rfg_build_view(const uint16_t* raw, const uint8_t* rgb, const rfg_intrinsics* intr, float scale, float offset,
+                   int bilateral, int levels, int rawBigEndian, float* depthLevels, float* intensityLevels,
+                   float* normals, float* scratch, void* stream) {
+  // build_view (view.cpp:102-106) rejects levels < 1
+  RFG_REQUIRE(raw && depthLevels && valid_intr(intr) && levels >= 1 && levels <= 4, "invalid build_view arguments");
+  RFG_REQUIRE(!bilateral || scratch, "bilateral needs a scratch image (width*height floats)");
+  RFG_REQUIRE(!intensityLevels || rgb, "intensity levels need an rgb image");
+  const Intr in{intr->width, intr->height, intr->fx, intr->fy, intr->cx, intr->cy};
+  RFG_CK(launch_build_view_full(raw, rgb, in, scale, offset, bilateral, levels, rawBigEndian, depthLevels,
+                                intensityLevels, reinterpret_cast<float4*>(normals), scratch,
+                                static_cast<cudaStream_t>(stream)));
+  return RFG_OK;
+}
+
+int rfg_bilateral_filter(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out,
+                         void* stream) {
+  RFG_REQUIRE(in && out && in != out && w > 0 && h > 0, "invalid bilateral_filter arguments");
+  RFG_CK(launch_bilateral(in, w, h, spatialSigma, rangeSigma, out, static_cast<cudaStream_t>(stream)));
+  return RFG_OK;
+}
+
+int rfg_compute_normals(const float* depth, const rfg_intrinsics* intr, float* normals, void* stream) {
+  RFG_REQUIRE(depth && normals && valid_intr(intr), "invalid compute_normals arguments");
+  const Intr in{intr->width, intr->height, intr->fx, intr->fy, intr->cx, intr->cy};
+  RFG_CK(launch_view_normals(depth, in, reinterpret_cast<float4*>(normals), static_cast<cudaStream_t>(stream)));
+  return RFG_OK;
+}
+
+int rfg_rgb_to_intensity(const uint8_t* rgb, int w, int h, float* out, void* stream) {
+  RFG_REQUIRE(rgb && out && w > 0 && h > 0, "invalid rgb_to_intensity arguments");
+  RFG_CK(launch_intensity(rgb, w, h, out, static_cast<cudaStream_t>(stream)));
+  return RFG_OK;
+}
+
+int rfg_downsample_intensity(const float* in, int w, int h, float* out, void* stream) {
+  RFG_REQUIRE(in && out && w > 0 && h > 0, "invalid downsample_intensity arguments");
+  RFG_CK(launch_downsample_intensity(in, w, h, out, static_cast<cudaStream_t>(stream)));
+  return RFG_OK;
+}
+
 int rfg_icp_track(rfg_map* m, const float* depthLevels, int levels, const rfg_intrinsics* intr, const float* points,
                   const float* normals, const float renderPose34[12], const float initPose34[12], const int iters[3],
                   const float dist[3], int minCount, float poseOut34[12], double stats8[8]) {
@@ -517,6 +567,9 @@ struct rfg_pipeline {
   float* poses;  // [0..11] current w2c, [12..23] render pose of the last raycast
   double* hostIcp;
   float* hostPose;
+  float* viewScratch;  // unfiltered depth when cfg.bilateral
+  void* pgmStage;      // pinned staging for rfg_pipeline_process_pgm
+  cudaEvent_t stageFree;  // the last upload out of pgmStage has been read
   int frames;
   cudaGraphExec_t exec[2];  // [0] no tracking, [1] tracking
   uint64_t graphKernels[2];
@@ -535,8 +588,9 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
     if (prof) cudaEventRecord(p->ev[k], s);
   };
   mark(0);
-  cudaError_t e = launch_build_view(p->rawDev, c.intr.width, c.intr.height, c.aff_scale, c.aff_offset, c.levels,
-                                    p->depthLevels, s);
+  const Intr inV{c.intr.width, c.intr.height, c.intr.fx, c.intr.fy, c.intr.cx, c.intr.cy};
+  cudaError_t e = launch_build_view_full(p->rawDev, nullptr, inV, c.aff_scale, c.aff_offset, c.bilateral, c.levels,
+                                         c.raw_big_endian, p->depthLevels, nullptr, nullptr, p->viewScratch, s);
   if (e != cudaSuccess) return e;
   mark(1);
   if (track) {
@@ -619,7 +673,9 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
             cudaMalloc(&p->normals, n * sizeof(float4)) == cudaSuccess &&
             cudaMalloc(&p->poses, 32 * sizeof(float)) == cudaSuccess &&
             cudaMallocHost(&p->hostIcp, 8 * sizeof(double)) == cudaSuccess &&
-            cudaMallocHost(&p->hostPose, 12 * sizeof(float)) == cudaSuccess;
+            cudaMallocHost(&p->hostPose, 12 * sizeof(float)) == cudaSuccess &&
+            cudaMallocHost(&p->pgmStage, n * 2 + 16) == cudaSuccess &&
+            (!cfg->bilateral || cudaMalloc(&p->viewScratch, n * 4 + 16) == cudaSuccess);
   if (!ok) {
     cudaGetLastError();
     rfg_pipeline_destroy(p);
@@ -628,6 +684,7 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
   }
   for (int k = 0; k < 7; ++k)
     if (cudaEventCreate(&p->ev[k]) != cudaSuccess) ok = false;
+  if (cudaEventCreateWithFlags(&p->stageFree, cudaEventDisableTiming) != cudaSuccess) ok = false;
   if (!ok) {
     cudaGetLastError();
     rfg_pipeline_destroy(p);
@@ -653,13 +710,15 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (int i = 0; i < 2; ++i)
     if (p->exec[i]) cudaGraphExecDestroy(p->exec[i]);
-  void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->points, p->normals, p->poses};
+  void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->points, p->normals, p->poses, p->viewScratch};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int k = 0; k < 7; ++k)
     if (p->ev[k]) cudaEventDestroy(p->ev[k]);
+  if (p->stageFree) cudaEventDestroy(p->stageFree);
   if (p->hostIcp) cudaFreeHost(p->hostIcp);
   if (p->hostPose) cudaFreeHost(p->hostPose);
+  if (p->pgmStage) cudaFreeHost(p->pgmStage);
   if (p->map && p->map->stream == p->stream) p->map->stream = nullptr;
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -690,6 +749,24 @@ int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const fl
   RFG_REQUIRE(p && rawHost, "null argument");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
   RFG_CK(cudaMemcpyAsync(p->rawDev, rawHost, n * 2, cudaMemcpyHostToDevice, p->stream));
+  return run_frame(p, pose34);
+}
+
+int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pose34) {
+  RFG_REQUIRE(p && path, "null argument");
+  const int64_t n = (int64_t)p->cfg.intr.width * p->cfg.intr.height;
+  int w = 0, h = 0;
+  // the previous frame's upload may still be reading the staging buffer
+  RFG_CK(cudaEventSynchronize(p->stageFree));
+  // the payload goes to the device as stored; the GPU view stage decodes it
+  // (cfg.raw_big_endian = 1) — with raw_big_endian = 0 it is swapped here
+  int rc = p->cfg.raw_big_endian ? rfg_read_pgm16_payload(path, p->pgmStage, n, &w, &h)
+                                 : rfg_read_pgm16(path, static_cast<uint16_t*>(p->pgmStage), n, &w, &h);
+  if (rc != RFG_OK) return rc;
+  RFG_REQUIRE(w == p->cfg.intr.width && h == p->cfg.intr.height,
+              "build_view: depth image size does not match calibration");
+  RFG_CK(cudaMemcpyAsync(p->rawDev, p->pgmStage, (size_t)n * 2, cudaMemcpyHostToDevice, p->stream));
+  RFG_CK(cudaEventRecord(p->stageFree, p->stream));
   return run_frame(p, pose34);
 }
 

@@ -261,9 +261,17 @@ class VoxelBlockMap:
 
 # ------------------------------------------------------------------ view
 @dataclass
+class ViewBuildOptions:
+    """proj/include/rf/view.hpp:12-15."""
+    bilateral: bool = False
+    levels: int = 3
+
+
+@dataclass
 class ViewLevel:
     depth: torch.Tensor
     intr: Intrinsics
+    intensity: torch.Tensor | None = None
 
 
 @dataclass
@@ -273,40 +281,174 @@ class View:
     depth_m: torch.Tensor
     rgb: torch.Tensor | None = None
     pyramid: list = field(default_factory=list)
+    intensity: torch.Tensor | None = None
+    normals: torch.Tensor | None = None  # (H, W, 4) camera-frame unit normals, w < 0 invalid
 
     def hasColour(self) -> bool:
         return self.rgb is not None
 
 
-def build_view(raw_depth, rgb, calib: RgbdCalib, levels: int = 3) -> View:
-    """build_view depth path (proj/src/view.cpp:100-143) on the GPU.
-    raw_depth: (H, W) uint16 (numpy or CUDA tensor).  Raises ValueError on a
-    size mismatch or levels < 1, like the reference (view.cpp:102-106)."""
+def _u16_tensor(raw):
+    t = torch.as_tensor(raw) if torch.is_tensor(raw) else None
+    if t is None or (t.dtype != torch.uint16 and t.dtype != torch.int16):
+        t = torch.as_tensor(np.ascontiguousarray(np.asarray(raw, dtype=np.uint16)).view(np.int16))
+    return t
+
+
+def _rgb_tensor(rgb):
+    if rgb is None:
+        return None
+    return torch.as_tensor(np.ascontiguousarray(rgb, dtype=np.uint8)).cuda() if not torch.is_tensor(rgb) \
+        else rgb.cuda().contiguous()
+
+
+def build_view(raw_depth, rgb, calib: RgbdCalib, opts: ViewBuildOptions | int | None = None, *,
+               levels: int | None = None, big_endian: bool = False) -> View:
+    """build_view (proj/src/view.cpp:100-143) on the GPU with every option:
+    depth conversion, optional bilateral filter, level-0 normals, intensity
+    (when rgb is given) and the depth / intensity pyramids.  raw_depth:
+    (H, W) uint16 (numpy or CUDA tensor; big_endian=True for a PGM16 payload,
+    see read_pgm16_payload).  Raises ValueError on a size mismatch or
+    levels < 1, like the reference (view.cpp:102-106)."""
+    if isinstance(opts, int):  # build_view(raw, rgb, calib, levels)
+        opts = ViewBuildOptions(levels=opts)
+    opts = opts or ViewBuildOptions()
+    if levels is not None:
+        opts = ViewBuildOptions(bilateral=opts.bilateral, levels=levels)
     intr = calib.intrinsics_d
-    raw = torch.as_tensor(raw_depth)
-    if raw.dtype != torch.uint16 and raw.dtype != torch.int16:
-        raw = torch.as_tensor(np.ascontiguousarray(np.asarray(raw_depth, dtype=np.uint16)).view(np.int16))
+    raw = _u16_tensor(raw_depth)
     if tuple(raw.shape) != (intr.height, intr.width):
         raise ValueError("build_view: depth image size does not match calibration")
-    if levels < 1:
-        raise ValueError("build_view: levels must be >= 1")
     if rgb is not None and tuple(rgb.shape[:2]) != (calib.intrinsics_rgb.height, calib.intrinsics_rgb.width):
         raise ValueError("build_view: rgb image size does not match calibration")
+    if opts.levels < 1:
+        raise ValueError("build_view: levels must be >= 1")
     raw = raw.cuda().contiguous()
-    sizes = [(intr.width >> l) * (intr.height >> l) for l in range(levels)]
-    buf = torch.empty(sum(sizes), dtype=torch.float32, device=raw.device)
-    check(lib().rfg_build_view_depth(_ptr(raw), intr.width, intr.height, calib.depth_affine.scale,
-                                     calib.depth_affine.offset, levels, _ptr(buf), _stream_handle()))
+    rgb_t = _rgb_tensor(rgb)
+    # intensity is defined on the depth grid (view.cpp:126-141 pairs
+    # pyramid[0].intensity with the depth intrinsics)
+    inten = rgb_t is not None and (calib.intrinsics_rgb.width, calib.intrinsics_rgb.height) == (intr.width, intr.height)
+    sizes = [(intr.width >> l) * (intr.height >> l) for l in range(opts.levels)]
+    dev = raw.device
+    buf = torch.empty(sum(sizes), dtype=torch.float32, device=dev)
+    ibuf = torch.empty(sum(sizes), dtype=torch.float32, device=dev) if inten else None
+    normals = torch.empty((intr.height, intr.width, 4), dtype=torch.float32, device=dev)
+    scratch = torch.empty(intr.width * intr.height, dtype=torch.float32, device=dev) if opts.bilateral else None
+    check(lib().rfg_build_view(_ptr(raw), _ptr(rgb_t) if inten else None, C.byref(intr.c()),
+                               calib.depth_affine.scale, calib.depth_affine.offset, 1 if opts.bilateral else 0,
+                               opts.levels, 1 if big_endian else 0, _ptr(buf), _ptr(ibuf) if inten else None,
+                               _ptr(normals), _ptr(scratch) if scratch is not None else None, _stream_handle()))
     pyr, o = [], 0
     for l, s in enumerate(sizes):
         il = intr.atLevel(l)
-        pyr.append(ViewLevel(buf[o:o + s].view(il.height, il.width), il))
+        pyr.append(ViewLevel(buf[o:o + s].view(il.height, il.width), il,
+                             ibuf[o:o + s].view(il.height, il.width) if inten else None))
         o += s
-    rgb_t = None
-    if rgb is not None:
-        rgb_t = torch.as_tensor(np.ascontiguousarray(rgb, dtype=np.uint8)).cuda() if not torch.is_tensor(rgb) \
-            else rgb.cuda().contiguous()
-    return View(calib=calib, depth_m=pyr[0].depth, rgb=rgb_t, pyramid=pyr)
+    return View(calib=calib, depth_m=pyr[0].depth, rgb=rgb_t, pyramid=pyr,
+                intensity=pyr[0].intensity, normals=normals)
+
+
+def bilateral_filter(depth_m, spatial_sigma: float, range_sigma: float) -> torch.Tensor:
+    """bilateral_filter (view.cpp:18-44): 5x5 edge-preserving filter, bit-exact
+    including the reference's std::exp (glibc expf, reproduced on the GPU)."""
+    d = torch.as_tensor(depth_m, dtype=torch.float32).cuda().contiguous()
+    out = torch.empty_like(d)
+    check(lib().rfg_bilateral_filter(_ptr(d), d.shape[1], d.shape[0], spatial_sigma, range_sigma, _ptr(out),
+                                     _stream_handle()))
+    return out
+
+
+def compute_normals(depth_m, intr: Intrinsics) -> torch.Tensor:
+    """compute_normals (view.cpp:46-67): (H, W, 4), w < 0 invalid."""
+    d = torch.as_tensor(depth_m, dtype=torch.float32).cuda().contiguous()
+    out = torch.empty((d.shape[0], d.shape[1], 4), dtype=torch.float32, device=d.device)
+    check(lib().rfg_compute_normals(_ptr(d), C.byref(intr.c()), _ptr(out), _stream_handle()))
+    return out
+
+
+def rgb_to_intensity(rgb) -> torch.Tensor:
+    """rgb_to_intensity (view.cpp:8-16)."""
+    r = _rgb_tensor(rgb)
+    out = torch.empty(r.shape[:2], dtype=torch.float32, device=r.device)
+    check(lib().rfg_rgb_to_intensity(_ptr(r), r.shape[1], r.shape[0], _ptr(out), _stream_handle()))
+    return out
+
+
+def downsample_intensity(img) -> torch.Tensor:
+    """downsample_intensity (view.cpp:90-98)."""
+    i = torch.as_tensor(img, dtype=torch.float32).cuda().contiguous()
+    out = torch.empty((i.shape[0] // 2, i.shape[1] // 2), dtype=torch.float32, device=i.device)
+    check(lib().rfg_downsample_intensity(_ptr(i), i.shape[1], i.shape[0], _ptr(out), _stream_handle()))
+    return out
+
+
+# ------------------------------------------------------------ image IO
+def _pnm_read(fn, path, channels, dtype):
+    w, h = C.c_int32(0), C.c_int32(0)
+    rc = fn(path.encode(), None, 0, C.byref(w), C.byref(h))
+    if rc == _lib.RFG_EINVAL:
+        raise RuntimeError(lib().rfg_last_error().decode())
+    shape = (h.value, w.value) + ((channels,) if channels > 1 else ())
+    out = np.empty(shape, dtype=dtype)
+    check(fn(path.encode(), out.ctypes.data_as(C.c_void_p), w.value * h.value, C.byref(w), C.byref(h)))
+    return out
+
+
+def read_pgm16(path: str) -> np.ndarray:
+    """read_pgm16 (image_io.cpp:96-113): (H, W) uint16, host order.  Raises
+    RuntimeError with the reference's message on a bad file."""
+    return _pnm_read(lib().rfg_read_pgm16, path, 1, np.uint16)
+
+
+def read_pgm16_payload(path: str) -> np.ndarray:
+    """The PGM16 pixel bytes as stored (big-endian u16), for the GPU decode
+    (build_view(..., big_endian=True), Pipeline.process_pgm)."""
+    return _pnm_read(lib().rfg_read_pgm16_payload, path, 1, np.uint16)
+
+
+def read_ppm(path: str) -> np.ndarray:
+    """read_ppm (image_io.cpp:53-64): (H, W, 3) uint8."""
+    return _pnm_read(lib().rfg_read_ppm, path, 3, np.uint8)
+
+
+def write_pgm16(img, path: str) -> None:
+    a = np.ascontiguousarray(img, dtype=np.uint16)
+    check(lib().rfg_write_pgm16(path.encode(), a.ctypes.data_as(C.c_void_p), a.shape[1], a.shape[0]))
+
+
+def write_ppm(img, path: str) -> None:
+    a = np.ascontiguousarray(img, dtype=np.uint8)
+    check(lib().rfg_write_ppm(path.encode(), a.ctypes.data_as(C.c_void_p), a.shape[1], a.shape[0]))
+
+
+@dataclass
+class RawFrame:
+    depth: np.ndarray
+    rgb: np.ndarray | None
+    index: int
+
+
+class ImageStream:
+    """ImageStream (image_io.hpp:26-38): frame i is <pattern % i>.pgm (depth,
+    required) and <pattern % i>.ppm (colour, optional); the stream ends at the
+    first missing depth file."""
+
+    def __init__(self, pattern_no_ext: str, start_index: int = 0):
+        self._pattern = pattern_no_ext
+        self._index = start_index
+
+    def next(self) -> RawFrame | None:
+        import os
+        base = self._pattern % self._index
+        if not os.path.exists(base + ".pgm"):
+            return None
+        f = RawFrame(read_pgm16(base + ".pgm"), read_ppm(base + ".ppm") if os.path.exists(base + ".ppm") else None,
+                     self._index)
+        self._index += 1
+        return f
+
+    def nextIndex(self) -> int:
+        return self._index
 
 
 def view_from_depth(depth_m, intr: Intrinsics, rgb=None, calib: RgbdCalib | None = None) -> View:
@@ -510,7 +652,7 @@ class Pipeline:
     def __init__(self, map: VoxelBlockMap, intr: Intrinsics, params: SceneParams,
                  affine: DepthAffine = DepthAffine(1.0 / 5000.0, 0.0), levels: int = 3, track: bool = True,
                  iters=(6, 10, 20), dist=(0.01, 0.02, 0.04), min_count: int = 10, use_graph: bool = True,
-                 profile: bool = False):
+                 profile: bool = False, bilateral: bool = False, raw_big_endian: bool = False):
         self.map = map
         self.intr = intr
         cfg = _lib.PipelineConfig_()
@@ -525,6 +667,8 @@ class Pipeline:
         cfg.min_count = min_count
         cfg.use_graph = 1 if use_graph else 0
         cfg.profile = 1 if profile else 0
+        cfg.bilateral = 1 if bilateral else 0
+        cfg.raw_big_endian = 1 if raw_big_endian else 0
         self._h = C.c_void_p()
         check(lib().rfg_pipeline_create(map.handle, C.byref(cfg), C.byref(self._h)))
         self._levels = levels
@@ -545,6 +689,11 @@ class Pipeline:
         else:
             a = np.ascontiguousarray(raw, np.uint16) if not torch.is_tensor(raw) else raw.numpy()
             check(lib().rfg_pipeline_process_host(self._h, a.ctypes.data_as(C.c_void_p), p))
+
+    def process_pgm(self, path: str, pose=None):
+        """One frame straight from a PGM16 file (rfg_pipeline_process_pgm)."""
+        p = _fp(_pose(pose)) if pose is not None else None
+        check(lib().rfg_pipeline_process_pgm(self._h, path.encode(), p))
 
     def result(self):
         st = _lib.AllocStats_()

@@ -14,6 +14,13 @@ Fixtures:
                  ranges / ICP maps, plus the full final-frame state
   c1_frames.json full C1 (640x480, 0x40000 buckets) frames 0-1: stats and
                  digests of the canonical state after each stage
+  view_full.npz  the full ViewBuilder (view.cpp:8-143) on noisy 96x72 frames
+                 with colour: depth / intensity pyramids and normals with the
+                 bilateral filter off and on, bilateral_filter on extreme depth
+                 jumps, and PGM16 / PPM files as written by the reference
+                 (image_io.cpp)
+
+`python tests/golden/make_golden.py view` regenerates view_full.npz only.
 """
 from __future__ import annotations
 
@@ -160,13 +167,53 @@ def make_c1():
     return frames
 
 
+def make_view_full():
+    import tempfile
+    out = {}
+    intr = small_intr(96, 72)
+    poses = ref.orbit_poses([0, 0.15, 1.4], 1.4, 5, 0.5)
+    for k in range(2):
+        raw, _, col = ref.render(0, poses[2 * k], intr, AFF, rgb=True)
+        rng = np.random.default_rng(100 + k)
+        noisy = np.clip(raw.astype(np.int64) + rng.integers(-40, 41, raw.shape), 0, 65535).astype(np.uint16)
+        noisy[raw == 0] = 0
+        noisy[rng.random(raw.shape) < 0.01] = 0
+        out[f"raw{k}"], out[f"rgb{k}"] = noisy, col
+        for bil in (0, 1):
+            v = ref.build_view_full(noisy, intr, AFF, levels=3, bilateral=bool(bil), rgb=col)
+            for l in range(3):
+                out[f"depth{k}_{bil}_{l}"] = v["depth"][l]
+                out[f"intensity{k}_{bil}_{l}"] = v["intensity"][l]
+            out[f"normals{k}_{bil}"] = v["normals"]
+    rng = np.random.default_rng(7)
+    d = rng.uniform(0.3, 6.0, (40, 52)).astype(np.float32)
+    d[rng.random(d.shape) < 0.2] = -1.0
+    out["bil_in"] = d
+    out["bil_out"] = ref.bilateral_filter(d, 2.0, 0.002)
+    with tempfile.TemporaryDirectory() as t:
+        img = rng.integers(0, 65536, (23, 37), dtype=np.uint16)
+        rgb = rng.integers(0, 256, (23, 37, 3), dtype=np.uint8)
+        ref.write_pgm16(img, os.path.join(t, "a.pgm"))
+        ref.write_ppm(rgb, os.path.join(t, "a.ppm"))
+        out["pgm_img"], out["ppm_img"] = img, rgb
+        out["pgm_bytes"] = np.frombuffer(open(os.path.join(t, "a.pgm"), "rb").read(), np.uint8)
+        out["ppm_bytes"] = np.frombuffer(open(os.path.join(t, "a.ppm"), "rb").read(), np.uint8)
+    out["intr"] = np.array([intr["width"], intr["height"], intr["fx"], intr["fy"], intr["cx"], intr["cy"]],
+                           np.float64)
+    return out
+
+
 def main():
     assert ref.available(), "build oracle/_ref first: make -C oracle ref"
+    if len(sys.argv) > 1 and sys.argv[1] == "view":
+        np.savez_compressed(os.path.join(HERE, "view_full.npz"), **make_view_full())
+        return
     rng = np.random.default_rng(1708)
     np.savez_compressed(os.path.join(HERE, "elements.npz"), **make_elements(rng))
     np.savez_compressed(os.path.join(HERE, "seq_small.npz"), **make_small_sequence())
     with open(os.path.join(HERE, "c1_frames.json"), "w") as f:
         json.dump(make_c1(), f, indent=1)
+    np.savez_compressed(os.path.join(HERE, "view_full.npz"), **make_view_full())
     for n in os.listdir(HERE):
         print(n, os.path.getsize(os.path.join(HERE, n)))
 
