@@ -134,6 +134,19 @@ int rfg_render_icp_maps_list(rfg_map* map, const float pose34[12], const rfg_int
                              const rfg_scene_params* params, const float* range_dev, const int32_t* missing_dev,
                              const int32_t* n_missing_dev, float* raycast_dev, float* points_dev, float* normals_dev);
 
+/* render_maps with any RenderMode (raycast.hpp:28,157-207): mode 0 kIcpMaps
+ * (= rfg_render_icp_maps), 1 kColour (colour_dev: RGB8 per pixel, the
+ * trilinear colour at the hit — zero for depth-only maps, like an
+ * un-coloured VoxelSRgb map), 2 kGrey (|n . ray| shading).  The _list form
+ * is render_maps(..., missingOnly). */
+int rfg_render_maps(rfg_map* map, const float pose34[12], const rfg_intrinsics* intr, const rfg_scene_params* params,
+                    int mode, const float* range_dev, float* raycast_dev, float* points_dev, float* normals_dev,
+                    uint8_t* colour_dev);
+int rfg_render_maps_list(rfg_map* map, const float pose34[12], const rfg_intrinsics* intr,
+                         const rfg_scene_params* params, int mode, const float* range_dev, const int32_t* missing_dev,
+                         const int32_t* n_missing_dev, float* raycast_dev, float* points_dev, float* normals_dev,
+                         uint8_t* colour_dev);
+
 /* ---------------------------------------------------------------- view */
 /* build_view depth path (proj/src/view.cpp:100-143): raw u16 -> metres
  * (m = raw*scale + offset, raw == 0 or m <= 0 -> -1) and `levels` pyramid

@@ -58,6 +58,7 @@ def lib():
         L.rr_export_blocks.argtypes = [C.c_void_p, _i, C.c_int, _u8]
         L.rr_export_visible.argtypes = [C.c_void_p, _i, _u8]
         L.rr_free_counts.argtypes = [C.c_void_p, _i, _i]
+        L.rr_render_maps.argtypes = [C.c_void_p, C.c_int, _f, _i, _f, _f, _f, _f, _f, _u8]
         L.rr_build_view_full.argtypes = [_u16, _u8, _i, _f, C.c_float, C.c_float, C.c_int, C.c_int, _f, _f, _f]
         L.rr_bilateral_filter.argtypes = [_f, C.c_int, C.c_int, C.c_float, C.c_float, _f]
         L.rr_compute_normals.argtypes = [_f, _i, _f, _f]
@@ -295,6 +296,20 @@ class RefEngine:
         wh, f4 = _wh(intr), _f4(intr)
         r = _f32(rng)
         lib().rr_set_ranges(self.h, P(wh, _i), P(f4, _f), P(r, _f))
+
+    def render_maps(self, mode, pose34, intr, params):
+        """render_maps with RenderMode 0 kIcpMaps / 1 kColour / 2 kGrey:
+        (raycast, points, normals, colour RGB8)."""
+        h, w = intr["height"], intr["width"]
+        rc = np.zeros((h, w, 4), np.float32)
+        pts = np.zeros((h, w, 4), np.float32)
+        nrm = np.zeros((h, w, 4), np.float32)
+        col = np.zeros((h, w, 3), np.uint8)
+        pose, pv = _f32(pose34), params_vec(params)
+        wh, f4 = _wh(intr), _f4(intr)
+        lib().rr_render_maps(self.h, mode, P(pose, _f), P(wh, _i), P(f4, _f), P(pv, _f), P(rc, _f), P(pts, _f),
+                             P(nrm, _f), P(col, _u8))
+        return rc, pts, nrm, col
 
     def render_icp(self, pose34, intr, params):
         h, w = intr["height"], intr["width"]

@@ -407,6 +407,26 @@ int rr_render_icp(void* h, const float* pose12, const int* wh, const float* f4, 
   return 0;
 }
 
+// render_maps with any RenderMode (raycast.cpp:129-139): 0 kIcpMaps,
+// 1 kColour, 2 kGrey; the three float4 maps plus the RGB8 colour image.
+int rr_render_maps(void* h, int mode, const float* pose12, const int* wh, const float* f4, const float* params,
+                   float* raycastOut, float* pointsOut, float* normalsOut, std::uint8_t* colourOut) {
+  auto* e = static_cast<Engine*>(h);
+  const RenderMode rm = mode == 1 ? RenderMode::kColour : (mode == 2 ? RenderMode::kGrey : RenderMode::kIcpMaps);
+  render_maps(e->map, poseFrom12(pose12), intrFrom(wh, f4), paramsFrom(params), rm, e->render);
+  const std::size_t n = e->render.points.size();
+  for (std::size_t i = 0; i < n; ++i) {
+    for (int k = 0; k < 4; ++k) {
+      if (raycastOut) raycastOut[4 * i + k] = e->render.raycastResult.data()[i][k];
+      if (pointsOut) pointsOut[4 * i + k] = e->render.points.data()[i][k];
+      if (normalsOut) normalsOut[4 * i + k] = e->render.normals.data()[i][k];
+    }
+    if (colourOut)
+      for (int k = 0; k < 3; ++k) colourOut[3 * i + k] = e->render.colour.data()[i][k];
+  }
+  return 0;
+}
+
 // forward_project (proj/src/raycast.cpp:141-188) on the engine's RenderState:
 // returns the number of missing pixels and writes them as (x, y) pairs.
 int rr_forward_project(void* h, const float* pose12, const int* wh, const float* f4, float voxelSize,

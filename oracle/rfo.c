@@ -930,6 +930,66 @@ int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float aff
   return 0;
 }
 
+/* ------------------------------------------------- colour / grey modes */
+/* readColourTrilinear (voxel_block_map.cpp:158-175): missing corners are
+ * skipped, clr += bw * (r, g, b) per component. */
+static v3 colour_trilinear(const rfo_map* m, v3 p) {
+  int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
+  float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
+  v3 c = {0.f, 0.f, 0.f};
+  for (int k = 0; k < 8; ++k) {
+    i3 q = {bx + (k & 1), by + ((k >> 1) & 1), bz + ((k >> 2) & 1)};
+    const voxel_t* vx = find_voxel(m, q);
+    if (!vx) continue;
+    float bw = ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+    c.x += bw * (float)vx->clr[0];
+    c.y += bw * (float)vx->clr[1];
+    c.z += bw * (float)vx->clr[2];
+  }
+  return c;
+}
+static uint8_t clamp_u8(float v) { return (uint8_t)(v < 0.f ? 0.f : (255.f < v ? 255.f : v)); }
+
+/* render_maps_field's colour (raycast.hpp:169,191-197, raycast.cpp:132-137)
+ * from the ICP maps of the same render: mode 1 = kColour (trilinear colour at
+ * the hit, clamped and truncated), 2 = kGrey (|n . dirWorld| clamped to
+ * [0, 1] * 255, only where the normal is valid); (0,0,0) elsewhere.  list /
+ * nList restrict it to the listed pixels (missingOnly), like the maps. */
+int rfo_render_colour(const rfo_map* m, int mode, const float* pose12, const int* wh, const float* f4,
+                      const float* raycast, const float* normals, const int* list, int nList, uint8_t* rgbOut) {
+  intr_t in = intr_from(wh, f4);
+  pose_t pose = pose_from12(pose12);
+  pose_t c2w = pose_inverse(&pose);
+  const int n = list ? nList : in.w * in.h;
+  for (int k = 0; k < n; ++k) {
+    const int i = list ? list[k] : k;
+    const int x = i % in.w, y = i / in.w;
+    uint8_t* o = rgbOut + 3 * (size_t)i;
+    o[0] = o[1] = o[2] = 0;
+    const float* rc = raycast + 4 * (size_t)i;
+    if (!(rc[3] > 0.f)) continue;
+    if (mode == 1) {
+      v3 h = {rc[0], rc[1], rc[2]};
+      v3 c = colour_trilinear(m, h);
+      o[0] = clamp_u8(c.x);
+      o[1] = clamp_u8(c.y);
+      o[2] = clamp_u8(c.z);
+    } else if (mode == 2) {
+      const float* nm = normals + 4 * (size_t)i;
+      if (!(nm[3] > 0.f)) continue;
+      v3 dirCam = {((float)x - in.cx) / in.fx, ((float)y - in.cy) / in.fy, 1.f};
+      float norm = sqrtf(sqnorm3(dirCam));
+      v3 dw = rot_apply(c2w.R, dirCam);
+      v3 dirW = {dw.x / norm, dw.y / norm, dw.z / norm};
+      float shade = fabsf(nm[0] * dirW.x + (nm[1] * dirW.y + nm[2] * dirW.z));
+      shade = shade < 0.f ? 0.f : (1.f < shade ? 1.f : shade);
+      const uint8_t g = (uint8_t)(shade * 255.f);
+      o[0] = o[1] = o[2] = g;
+    }
+  }
+  return 0;
+}
+
 /* ------------------------------------------------- full ViewBuilder */
 /* rgb_to_intensity (P/src/view.cpp:8-16): (0.299 r + 0.587 g + 0.114 b) / 255,
  * C++ left-to-right evaluation, the channels promoted to float. */

@@ -65,6 +65,8 @@ int rfo_render_icp_list(rfo_map* m, const float* pose12, const int* wh, const fl
  * pyramid level, concatenated into depthLevels. */
 int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float affOffset, int levels,
                    float* depthLevels);
+int rfo_render_colour(const rfo_map* m, int mode, const float* pose12, const int* wh, const float* f4,
+                      const float* raycast, const float* normals, const int* list, int nList, uint8_t* rgbOut);
 /* full ViewBuilder (view.cpp:8-143) */
 void rfo_rgb_to_intensity(const uint8_t* rgb, int w, int h, float* out);
 void rfo_bilateral_filter(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out);

@@ -48,6 +48,7 @@ def lib():
         L.rfo_set_ranges.argtypes = [vp, _i, _f]
         L.rfo_render_icp.argtypes = [vp, _f, _i, _f, _f, _f, _f, _f]
         L.rfo_build_view.argtypes = [_u16, _i, C.c_float, C.c_float, C.c_int, _f]
+        L.rfo_render_colour.argtypes = [vp, C.c_int, _f, _i, _f, _f, _f, _i, C.c_int, _u8]
         L.rfo_build_view_full.argtypes = [_u16, _u8, _i, _f, C.c_float, C.c_float, C.c_int, C.c_int, _f, _f, _f]
         L.rfo_bilateral_filter.argtypes = [_f, C.c_int, C.c_int, C.c_float, C.c_float, _f]
         L.rfo_compute_normals.argtypes = [_f, C.c_int, C.c_int, _f, _f]
@@ -240,6 +241,18 @@ class OracleEngine:
         if rc_ != 0:
             raise RuntimeError("render_icp before render_ranges")
         return rc, pts, nrm, 0.0
+
+    def render_colour(self, mode, pose34, intr, raycast, normals, missing=None, out=None):
+        """The colour image of render_maps(kColour = 1 / kGrey = 2) from the
+        maps of the same render (raycast.hpp:169,191-197); with `missing`
+        (pixel indices) only those pixels are (re)written, in `out`."""
+        h, w = intr["height"], intr["width"]
+        col = out if out is not None else np.zeros((h, w, 3), np.uint8)
+        ls = np.ascontiguousarray(missing, np.int32) if missing is not None else None
+        lib().rfo_render_colour(self.h, mode, P(_f32(pose34), _f), P(_wh(intr), _i), P(_f4(intr), _f),
+                                P(_f32(raycast), _f), P(_f32(normals), _f), P(ls, _i), 0 if ls is None else len(ls),
+                                P(col, _u8))
+        return col
 
     def render_icp_list(self, pose34, intr, params, missing, raycast, points, normals):
         """render_maps(kIcpMaps, missingOnly) on caller-owned images (in place)."""

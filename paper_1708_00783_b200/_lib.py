@@ -77,6 +77,10 @@ SIGNATURES = {
     "rfg_forward_project": ([_vp, C.c_int, _vp, _vp, _vp, _f, C.POINTER(Intrinsics_), C.c_float, _vp, _vp], C.c_int),
     "rfg_render_icp_maps_list": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), _vp, _vp, _vp, _vp,
                                   _vp, _vp], C.c_int),
+    "rfg_render_maps": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), C.c_int, _vp, _vp, _vp, _vp,
+                         _vp], C.c_int),
+    "rfg_render_maps_list": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), C.c_int, _vp, _vp, _vp, _vp,
+                              _vp, _vp, _vp], C.c_int),
     "rfg_build_view_depth": ([_vp, C.c_int, C.c_int, C.c_float, C.c_float, C.c_int, _vp, _vp], C.c_int),
     "rfg_build_view": ([_vp, _vp, C.POINTER(Intrinsics_), C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, _vp, _vp,
                         _vp, _vp, _vp], C.c_int),

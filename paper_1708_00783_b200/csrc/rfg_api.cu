@@ -390,6 +390,33 @@ int rfg_render_icp_maps_list(rfg_map* m, const float pose34[12], const rfg_intri
   return RFG_OK;
 }
 
+int rfg_render_maps(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr, const rfg_scene_params* params,
+                    int mode, const float* range, float* raycast, float* points, float* normals, uint8_t* colour) {
+  RFG_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (kIcpMaps), 1 (kColour) or 2 (kGrey)");
+  RFG_REQUIRE(mode == 0 || colour, "colour / grey modes need a colour image");
+  RFG_REQUIRE(raycast, "render_maps needs the raycast image (the colour pass reads the hits)");
+  const int rc = rfg_render_icp_maps(m, pose34, intr, params, range, raycast, points, normals);
+  if (rc != RFG_OK || mode == 0) return rc;
+  const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  RFG_CK(launch_render_colour(m->d, fa, mode, reinterpret_cast<const float4*>(raycast),
+                              reinterpret_cast<const float4*>(normals), nullptr, nullptr, 0, colour, m->stream));
+  return RFG_OK;
+}
+
+int rfg_render_maps_list(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
+                         const rfg_scene_params* params, int mode, const float* range, const int32_t* missing,
+                         const int32_t* nMissing, float* raycast, float* points, float* normals, uint8_t* colour) {
+  RFG_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (kIcpMaps), 1 (kColour) or 2 (kGrey)");
+  RFG_REQUIRE(mode == 0 || colour, "colour / grey modes need a colour image");
+  const int rc = rfg_render_icp_maps_list(m, pose34, intr, params, range, missing, nMissing, raycast, points, normals);
+  if (rc != RFG_OK || mode == 0) return rc;
+  const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  RFG_CK(launch_render_colour(m->d, fa, mode, reinterpret_cast<const float4*>(raycast),
+                              reinterpret_cast<const float4*>(normals), missing, nMissing,
+                              intr->width * intr->height, colour, m->stream));
+  return RFG_OK;
+}
+
 int rfg_build_view_depth(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
                          void* stream) {
   // build_view (view.cpp:102-106) rejects levels < 1

@@ -96,6 +96,9 @@ cudaError_t launch_forward_project(int hasRaycast, float4* raycast, float4* poin
                                    int2* tilePrefix, int* list, int* count, cudaStream_t s);
 cudaError_t launch_build_view(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
                               cudaStream_t s);
+cudaError_t launch_render_colour(const DevMap& m, const FrameArgs& fa, int mode, const float4* raycast,
+                                 const float4* normals, const int* list, const int* count, int maxCount,
+                                 uint8_t* rgb, cudaStream_t s);
 
 }  // namespace rfg
 

@@ -438,6 +438,80 @@ __global__ void __launch_bounds__(128) k_normals_list(DevMap m, const int* __res
   normal_pixel(m, raycast, normals, (size_t)list[k]);
 }
 
+// ------------------------------------------------ colour / grey render modes
+// render_maps_field's colour (raycast.hpp:169,191-197; colourAt =
+// readColourTrilinear clamped and truncated, raycast.cpp:132-137), computed
+// from the maps of the same render after the march and the normals:
+// mode 1 kColour = trilinear colour at the hit over the corners that exist,
+// mode 2 kGrey = |n . dirWorld| clamped to [0, 1] * 255 where the normal is
+// valid; (0, 0, 0) elsewhere.  3 B out + 32 B in (+ 8 colour gathers) per px.
+__device__ __forceinline__ uint8_t clamp_u8(float v) { return (uint8_t)(v < 0.f ? 0.f : (255.f < v ? 255.f : v)); }
+
+__global__ void __launch_bounds__(128) k_render_colour(DevMap m, FrameArgs fa, int mode,
+                                                       const float4* __restrict__ raycast,
+                                                       const float4* __restrict__ normals,
+                                                       const int* __restrict__ list, const int* __restrict__ count,
+                                                       uint8_t* __restrict__ rgb) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (list) {
+    if (i >= *count) return;
+    i = list[i];
+  } else if (i >= fa.w * fa.h) {
+    return;
+  }
+  uint8_t c0 = 0, c1 = 0, c2 = 0;
+  const float4 r = raycast[i];
+  if (r.w > 0.f) {
+    if (mode == 1 && m.vbaColour) {
+      FieldReader field{m.entries, m.vbaDepth, m.buckets};
+      field.cache.reset();
+      const int bx = (int)floorf(r.x), by = (int)floorf(r.y), bz = (int)floorf(r.z);
+      const float fx = r.x - (float)bx, fy = r.y - (float)by, fz = r.z - (float)bz;
+      float cr = 0.f, cg = 0.f, cb = 0.f;
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int vx = bx + (k & 1), vy = by + ((k >> 1) & 1), vz = bz + ((k >> 2) & 1);
+        const int ptr = field.ptr_of(vx >> 3, vy >> 3, vz >> 3);
+        if (ptr < 0) continue;
+        const uint32_t w = __ldg(m.vbaColour + (size_t)ptr * kBlock3 + ((vx & 7) | ((vy & 7) << 3) | ((vz & 7) << 6)));
+        const float bw = ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+        cr += bw * (float)(w & 0xFFu);
+        cg += bw * (float)((w >> 8) & 0xFFu);
+        cb += bw * (float)((w >> 16) & 0xFFu);
+      }
+      c0 = clamp_u8(cr);
+      c1 = clamp_u8(cg);
+      c2 = clamp_u8(cb);
+    } else if (mode == 2) {
+      const float4 n = normals[i];
+      if (n.w > 0.f) {
+        const int x = i % fa.w, y = i / fa.w;
+        const Pose c2w = pose_inverse(load_pose_r(fa));
+        const f3 dirCam{((float)x - fa.cx) / fa.fx, ((float)y - fa.cy) / fa.fy, 1.f};
+        const float norm = sqrtf(sqnorm3(dirCam));
+        const f3 dw = rot_apply(c2w.R, dirCam);
+        const f3 dirW{dw.x / norm, dw.y / norm, dw.z / norm};
+        float shade = fabsf(dot3(f3{n.x, n.y, n.z}, dirW));
+        shade = shade < 0.f ? 0.f : (1.f < shade ? 1.f : shade);
+        c0 = c1 = c2 = (uint8_t)(shade * 255.f);
+      }
+    }
+  }
+  rgb[3 * (size_t)i] = c0;
+  rgb[3 * (size_t)i + 1] = c1;
+  rgb[3 * (size_t)i + 2] = c2;
+}
+
+cudaError_t launch_render_colour(const DevMap& m, const FrameArgs& fa, int mode, const float4* raycast,
+                                 const float4* normals, const int* list, const int* count, int maxCount,
+                                 uint8_t* rgb, cudaStream_t s) {
+  const int n = list ? maxCount : fa.w * fa.h;
+  if (n <= 0) return cudaSuccess;
+  k_render_colour<<<(n + 127) / 128, 128, 0, s>>>(m, fa, mode, raycast, normals, list, count, rgb);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------ forward projection
 // forward_project (raycast.cpp:141-188).  The serial reference visits the
 // previous hits in row-major order and keeps a target pixel's first point

@@ -499,6 +499,7 @@ class RenderState:
         self.raycastResult = None
         self.points = None
         self.normals = None
+        self.colour = None  # (H, W, 3) uint8 (colour / grey modes)
         self.pose = np.eye(3, 4, dtype=np.float32)
         self.intr = Intrinsics()
         self.hasRaycast = False
@@ -514,6 +515,7 @@ class RenderState:
         self.raycastResult = inv.repeat(h, w, 1).contiguous()
         self.points = inv.repeat(h, w, 1).contiguous()
         self.normals = inv.repeat(h, w, 1).contiguous()
+        self.colour = torch.zeros((h, w, 3), dtype=torch.uint8, device="cuda")
         self.intr = intr
         self.hasRaycast = False
 
@@ -546,25 +548,24 @@ class MissingPixels:
 
 def render_maps(map: VoxelBlockMap, pose, intr: Intrinsics, params: SceneParams, mode: RenderMode,
                 state: RenderState, missingOnly: MissingPixels | None = None):
-    """proj/src/raycast.cpp:129-139 — only RenderMode.kIcpMaps is on the hot
-    path; colour/grey shading is out of scope.  missingOnly
-    restricts the work to the listed pixels (raycast.hpp:200-202)."""
-    if mode != RenderMode.kIcpMaps:
-        raise NotImplementedError("only RenderMode.kIcpMaps is implemented on the B200 path")
+    """proj/src/raycast.cpp:129-139 with every RenderMode (kIcpMaps, kColour,
+    kGrey -> state.colour).  missingOnly restricts the work to the listed
+    pixels (raycast.hpp:200-202)."""
     if state.expectedRange is None:
         raise RuntimeError("render_maps needs render_expected_ranges first")
     state.resize(intr)
     p = _pose(pose)
     map.bind_stream()
+    col = _ptr(state.colour) if mode != RenderMode.kIcpMaps else None
     if missingOnly is None:
-        check(lib().rfg_render_icp_maps(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()),
-                                        _ptr(state.expectedRange), _ptr(state.raycastResult), _ptr(state.points),
-                                        _ptr(state.normals)))
+        check(lib().rfg_render_maps(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()), int(mode),
+                                    _ptr(state.expectedRange), _ptr(state.raycastResult), _ptr(state.points),
+                                    _ptr(state.normals), col))
     else:
-        check(lib().rfg_render_icp_maps_list(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()),
-                                             _ptr(state.expectedRange), _ptr(missingOnly.index),
-                                             _ptr(missingOnly.count), _ptr(state.raycastResult),
-                                             _ptr(state.points), _ptr(state.normals)))
+        check(lib().rfg_render_maps_list(map.handle, _fp(p), C.byref(intr.c()), C.byref(params.c()), int(mode),
+                                         _ptr(state.expectedRange), _ptr(missingOnly.index),
+                                         _ptr(missingOnly.count), _ptr(state.raycastResult),
+                                         _ptr(state.points), _ptr(state.normals), col))
     state.pose = p.copy()
     state.intr = intr
     state.hasRaycast = True

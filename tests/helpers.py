@@ -86,6 +86,13 @@ class GpuEngine:
         return (self.state.raycastResult.cpu().numpy(), self.state.points.cpu().numpy(),
                 self.state.normals.cpu().numpy(), 0.0)
 
+    def render_maps(self, mode, pose34, intr, params):
+        """render_maps(mode): (raycast, points, normals, colour RGB8)."""
+        F = self.F
+        F.render_maps(self.map, pose34, self._intr(intr), self._params(params), F.RenderMode(mode), self.state)
+        return (self.state.raycastResult.cpu().numpy(), self.state.points.cpu().numpy(),
+                self.state.normals.cpu().numpy(), self.state.colour.cpu().numpy())
+
     def entries(self):
         return self.map.entries()
 
