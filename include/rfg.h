@@ -147,6 +147,20 @@ int rfg_render_maps_list(rfg_map* map, const float pose34[12], const rfg_intrins
                          const int32_t* n_missing_dev, float* raycast_dev, float* points_dev, float* normals_dev,
                          uint8_t* colour_dev);
 
+/* ---------------------------------------------------------------- mesh */
+/* extract_mesh (proj/src/meshing.cpp:144-217): marching cubes over the
+ * in-memory blocks of the map.  Vertices (metres) and triangles come out in
+ * exactly the reference's order (entry index, cell order, table order; a
+ * vertex numbered where its cell edge first appears).  The result stays in
+ * map-owned device memory until the next extraction; rfg_mesh_copy copies it
+ * to host or device buffers (3 floats per vertex, 3 uint32 per triangle).
+ * Synchronous (the sizes are read back). */
+int rfg_extract_mesh(rfg_map* map, float voxel_size, int64_t* n_vertices, int64_t* n_triangles);
+int rfg_mesh_copy(rfg_map* map, float* vertices3, uint32_t* triangles3);
+/* The 256-case triangulation table (meshing.cpp:27-118 marchingCubesTable):
+ * counts[m] triangles of cell-edge triples, tris[(m*16 + k)*3 + j], -1 pad. */
+int rfg_mc_table(int32_t counts256[256], int32_t tris[256 * 16 * 3]);
+
 /* ---------------------------------------------------------------- view */
 /* build_view depth path (proj/src/view.cpp:100-143): raw u16 -> metres
  * (m = raw*scale + offset, raw == 0 or m <= 0 -> -1) and `levels` pyramid

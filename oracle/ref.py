@@ -58,6 +58,10 @@ def lib():
         L.rr_export_blocks.argtypes = [C.c_void_p, _i, C.c_int, _u8]
         L.rr_export_visible.argtypes = [C.c_void_p, _i, _u8]
         L.rr_free_counts.argtypes = [C.c_void_p, _i, _i]
+        L.rr_extract_mesh.argtypes = [C.c_void_p, C.c_float, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
+        L.rr_mesh_copy.argtypes = [C.c_void_p, _f, C.POINTER(C.c_uint32)]
+        L.rr_mc_table.argtypes = [_i, _i]
+        L.rr_set_block.argtypes = [C.c_void_p, _i, C.POINTER(C.c_int16), _u8]
         L.rr_render_maps.argtypes = [C.c_void_p, C.c_int, _f, _i, _f, _f, _f, _f, _f, _u8]
         L.rr_build_view_full.argtypes = [_u16, _u8, _i, _f, C.c_float, C.c_float, C.c_int, C.c_int, _f, _f, _f]
         L.rr_bilateral_filter.argtypes = [_f, C.c_int, C.c_int, C.c_float, C.c_float, _f]
@@ -245,6 +249,15 @@ def write_ppm(img, path):
     return _write("wppm", img, path, np.uint8)
 
 
+def mc_table():
+    """detail::marchingCubesTable(): list of lists of edge triples."""
+    cnt = np.zeros(256, np.int32)
+    tri = np.zeros(256 * 16 * 3, np.int32)
+    lib().rr_mc_table(P(cnt, _i), P(tri, _i))
+    tri = tri.reshape(256, 16, 3)
+    return [[tuple(int(x) for x in tri[m, k]) for k in range(cnt[m])] for m in range(256)]
+
+
 class RefEngine:
     """VoxelBlockMap + FusionEngine + RenderState of the reference."""
 
@@ -296,6 +309,21 @@ class RefEngine:
         wh, f4 = _wh(intr), _f4(intr)
         r = _f32(rng)
         lib().rr_set_ranges(self.h, P(wh, _i), P(f4, _f), P(r, _f))
+
+    def extract_mesh(self, voxel_size):
+        """extract_mesh (meshing.cpp:144-217): (vertices (N,3) f32, triangles (M,3) u32)."""
+        nv, nt = C.c_longlong(0), C.c_longlong(0)
+        lib().rr_extract_mesh(self.h, voxel_size, C.byref(nv), C.byref(nt))
+        v = np.zeros((nv.value, 3), np.float32)
+        t = np.zeros((nt.value, 3), np.uint32)
+        lib().rr_mesh_copy(self.h, P(v, _f), P(t, C.POINTER(C.c_uint32)))
+        return v, t
+
+    def set_block(self, pos3, sdf512, w512):
+        p = np.ascontiguousarray(pos3, np.int32)
+        sd = np.ascontiguousarray(sdf512, np.int16)
+        w = np.ascontiguousarray(w512, np.uint8)
+        return lib().rr_set_block(self.h, P(p, _i), P(sd, C.POINTER(C.c_int16)), P(w, _u8))
 
     def render_maps(self, mode, pose34, intr, params):
         """render_maps with RenderMode 0 kIcpMaps / 1 kColour / 2 kGrey:

@@ -20,6 +20,7 @@
 
 #include "rf/fusion.hpp"
 #include "rf/image_io.hpp"
+#include "rf/meshing.hpp"
 #include "rf/raycast.hpp"
 #include "rf/synth.hpp"
 #include "rf/view.hpp"
@@ -116,6 +117,7 @@ struct Engine {
   VoxelBlockMap map;
   FusionEngine fusion;
   RenderState render;
+  Mesh mesh;
 };
 
 View makeView(const float* depth, const std::uint8_t* rgb, const Intrinsics& intrD, const Intrinsics& intrRgb,
@@ -423,6 +425,46 @@ int rr_render_maps(void* h, int mode, const float* pose12, const int* wh, const 
     }
     if (colourOut)
       for (int k = 0; k < 3; ++k) colourOut[3 * i + k] = e->render.colour.data()[i][k];
+  }
+  return 0;
+}
+
+// extract_mesh (meshing.cpp:144-217): keeps the mesh in the engine; counts out
+int rr_extract_mesh(void* h, float voxelSize, long long* nV, long long* nT) {
+  auto* e = static_cast<Engine*>(h);
+  e->mesh = extract_mesh(e->map, voxelSize);
+  *nV = (long long)e->mesh.vertices.size();
+  *nT = (long long)e->mesh.triangles.size();
+  return 0;
+}
+int rr_mesh_copy(void* h, float* v3, std::uint32_t* t3) {
+  auto* e = static_cast<Engine*>(h);
+  for (std::size_t i = 0; i < e->mesh.vertices.size(); ++i)
+    for (int k = 0; k < 3; ++k) v3[3 * i + k] = e->mesh.vertices[i][k];
+  for (std::size_t i = 0; i < e->mesh.triangles.size(); ++i)
+    for (int k = 0; k < 3; ++k) t3[3 * i + k] = e->mesh.triangles[i][k];
+  return 0;
+}
+// detail::marchingCubesTable (meshing.cpp:27-118): counts + edge triples
+int rr_mc_table(int* counts256, int* tris) {
+  const auto& t = detail::marchingCubesTable();
+  for (int m = 0; m < 256; ++m) {
+    counts256[m] = (int)t[m].size();
+    for (int k = 0; k < 16; ++k)
+      for (int j = 0; j < 3; ++j) tris[(m * 16 + k) * 3 + j] = k < (int)t[m].size() ? t[m][k][j] : -1;
+  }
+  return 0;
+}
+// direct voxel writes (test support: analytic TSDFs as the reference's
+// meshing tests build them, test_voxelmap.cpp:231-280)
+int rr_set_block(void* h, const int* pos3, const std::int16_t* sdf512, const std::uint8_t* w512) {
+  auto* e = static_cast<Engine*>(h);
+  const auto idx = e->map.allocateBlock(Eigen::Vector3i(pos3[0], pos3[1], pos3[2]));
+  if (!idx) return -1;
+  Voxel* b = e->map.blockData(e->map.entry(*idx).ptr);
+  for (int i = 0; i < kBlockSize3; ++i) {
+    b[i].sdf = sdf512[i];
+    b[i].w_depth = w512[i];
   }
   return 0;
 }

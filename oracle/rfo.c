@@ -990,6 +990,248 @@ int rfo_render_colour(const rfo_map* m, int mode, const float* pose12, const int
   return 0;
 }
 
+/* ------------------------------------------------------ marching cubes */
+/* The triangulation table by the reference's rule (meshing.cpp:27-118):
+ * pair the crossed edges on each face (ambiguous faces: the two edges at
+ * each inside corner), walk the cycles, orient each by its Newell normal
+ * against the inside->outside direction, fan it. */
+static const int MC_C[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0}, {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+static const int MC_E[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
+                                {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
+static const int MC_F[6][4] = {{0, 1, 2, 3}, {4, 5, 6, 7}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
+static int mc_cnt[256];
+static int mc_tri[256][16][3];
+static int mc_ready = 0;
+
+static int mc_edge(int a, int b) {
+  for (int e = 0; e < 12; ++e)
+    if ((MC_E[e][0] == a && MC_E[e][1] == b) || (MC_E[e][0] == b && MC_E[e][1] == a)) return e;
+  return -1;
+}
+static void mc_link(int nb[12][2], int a, int b) {
+  if (nb[a][0] < 0) nb[a][0] = b; else nb[a][1] = b;
+  if (nb[b][0] < 0) nb[b][0] = a; else nb[b][1] = a;
+}
+static void mc_build_table(void) {
+  if (mc_ready) return;
+  for (int mask = 0; mask < 256; ++mask) {
+    int nb[12][2];
+    for (int e = 0; e < 12; ++e) nb[e][0] = nb[e][1] = -1;
+    for (int f = 0; f < 6; ++f) {
+      int ce[4], n = 0;
+      for (int i = 0; i < 4; ++i) {
+        int e = mc_edge(MC_F[f][i], MC_F[f][(i + 1) % 4]);
+        if (((mask >> MC_E[e][0]) & 1) != ((mask >> MC_E[e][1]) & 1)) ce[n++] = e;
+      }
+      if (n == 2) {
+        mc_link(nb, ce[0], ce[1]);
+      } else if (n == 4) {
+        for (int i = 0; i < 4; ++i) {
+          int c = MC_F[f][i];
+          if ((mask >> c) & 1) mc_link(nb, mc_edge(MC_F[f][(i + 3) % 4], c), mc_edge(c, MC_F[f][(i + 1) % 4]));
+        }
+      }
+    }
+    mc_cnt[mask] = 0;
+    int used[12] = {0};
+    for (int st = 0; st < 12; ++st) {
+      int crossed = ((mask >> MC_E[st][0]) & 1) != ((mask >> MC_E[st][1]) & 1);
+      if (!crossed || used[st]) continue;
+      int cyc[12], len = 0, cur = st, prev = -1;
+      for (;;) {
+        cyc[len++] = cur;
+        used[cur] = 1;
+        int nxt = nb[cur][0] != prev ? nb[cur][0] : nb[cur][1];
+        prev = cur;
+        cur = nxt;
+        if (cur == st) break;
+      }
+      if (len < 3) continue;
+      float nw[3] = {0, 0, 0}, rf[3] = {0, 0, 0};
+      for (int i = 0; i < len; ++i) {
+        float a[3], b[3];
+        int ea = cyc[i], eb = cyc[(i + 1) % len];
+        for (int k = 0; k < 3; ++k) {
+          a[k] = 0.5f * (float)(MC_C[MC_E[ea][0]][k] + MC_C[MC_E[ea][1]][k]);
+          b[k] = 0.5f * (float)(MC_C[MC_E[eb][0]][k] + MC_C[MC_E[eb][1]][k]);
+        }
+        nw[0] += a[1] * b[2] - a[2] * b[1];
+        nw[1] += a[2] * b[0] - a[0] * b[2];
+        nw[2] += a[0] * b[1] - a[1] * b[0];
+        int c0 = MC_E[ea][0], c1 = MC_E[ea][1];
+        int in = ((mask >> c0) & 1) ? c0 : c1, out = ((mask >> c0) & 1) ? c1 : c0;
+        for (int k = 0; k < 3; ++k) rf[k] += (float)(MC_C[out][k] - MC_C[in][k]);
+      }
+      if (rf[0] * rf[0] + rf[1] * rf[1] + rf[2] * rf[2] > 1e-12f && nw[0] * rf[0] + nw[1] * rf[1] + nw[2] * rf[2] < 0.f)
+        for (int i = 0; i < len / 2; ++i) {
+          int t = cyc[i];
+          cyc[i] = cyc[len - 1 - i];
+          cyc[len - 1 - i] = t;
+        }
+      for (int i = 1; i + 1 < len; ++i) {
+        int k = mc_cnt[mask]++;
+        mc_tri[mask][k][0] = cyc[0];
+        mc_tri[mask][k][1] = cyc[i];
+        mc_tri[mask][k][2] = cyc[i + 1];
+      }
+    }
+  }
+  mc_ready = 1;
+}
+
+int rfo_mc_table(int* counts256, int* tris) {
+  mc_build_table();
+  for (int m = 0; m < 256; ++m) {
+    counts256[m] = mc_cnt[m];
+    for (int k = 0; k < 16; ++k)
+      for (int j = 0; j < 3; ++j) tris[(m * 16 + k) * 3 + j] = k < mc_cnt[m] ? mc_tri[m][k][j] : -1;
+  }
+  return 0;
+}
+
+/* meshing.cpp:146-153 */
+static uint64_t mc_key(int x, int y, int z, int axis) {
+  const int64_t kBias = 1 << 19;
+  uint64_t ux = (uint64_t)(x + kBias) & 0xFFFFF, uy = (uint64_t)(y + kBias) & 0xFFFFF;
+  uint64_t uz = (uint64_t)(z + kBias) & 0xFFFFF;
+  return (((ux << 20) | uy) << 20 | uz) << 2 | (uint64_t)axis;
+}
+
+typedef struct {
+  uint64_t* keys; /* ~0 = empty */
+  uint32_t* vals;
+  size_t cap, n;
+} mc_map;
+static uint32_t mc_map_get_or_add(mc_map* h, uint64_t k, uint32_t v, int* added) {
+  if (2 * (h->n + 1) > h->cap) { /* grow */
+    size_t nc = h->cap ? 2 * h->cap : 1 << 16;
+    uint64_t* nk = (uint64_t*)malloc(nc * 8);
+    uint32_t* nv = (uint32_t*)malloc(nc * 4);
+    memset(nk, 0xFF, nc * 8);
+    for (size_t i = 0; i < h->cap; ++i)
+      if (h->keys[i] != ~(uint64_t)0) {
+        size_t j = (size_t)((h->keys[i] * 0x9E3779B97F4A7C15ull) >> 20) & (nc - 1);
+        while (nk[j] != ~(uint64_t)0) j = (j + 1) & (nc - 1);
+        nk[j] = h->keys[i];
+        nv[j] = h->vals[i];
+      }
+    free(h->keys);
+    free(h->vals);
+    h->keys = nk;
+    h->vals = nv;
+    h->cap = nc;
+  }
+  size_t j = (size_t)((k * 0x9E3779B97F4A7C15ull) >> 20) & (h->cap - 1);
+  while (h->keys[j] != ~(uint64_t)0) {
+    if (h->keys[j] == k) {
+      *added = 0;
+      return h->vals[j];
+    }
+    j = (j + 1) & (h->cap - 1);
+  }
+  h->keys[j] = k;
+  h->vals[j] = v;
+  h->n++;
+  *added = 1;
+  return v;
+}
+
+/* extract_mesh (meshing.cpp:156-217): entries in index order, cells lz/ly/lx,
+ * a cell is skipped unless all 8 corners are allocated with w_depth > 0;
+ * a vertex is created the first time its lattice edge is met.  Outputs are
+ * malloc'ed (free with rfo_free). */
+int rfo_extract_mesh(const rfo_map* m, float voxelSize, float** vOut, uint32_t** tOut, long long* nV,
+                     long long* nT) {
+  mc_build_table();
+  size_t vcap = 1 << 16, tcap = 1 << 16, nv = 0, nt = 0;
+  float* V = (float*)malloc(vcap * 12);
+  uint32_t* T = (uint32_t*)malloc(tcap * 12);
+  mc_map h = {NULL, NULL, 0, 0};
+  const uint32_t total = m->buckets + m->excess;
+  for (uint32_t idx = 0; idx < total; ++idx) {
+    const entry_t* e = &m->entries[idx];
+    if (e->ptr < 0) continue;
+    for (int lz = 0; lz < BS; ++lz)
+      for (int ly = 0; ly < BS; ++ly)
+        for (int lx = 0; lx < BS; ++lx) {
+          const int cx = e->x * BS + lx, cy = e->y * BS + ly, cz = e->z * BS + lz;
+          float sdf[8];
+          int observed = 1;
+          for (int c = 0; c < 8 && observed; ++c) {
+            i3 v = {cx + MC_C[c][0], cy + MC_C[c][1], cz + MC_C[c][2]};
+            const voxel_t* vx = find_voxel(m, v);
+            observed = vx != NULL && vx->w > 0;
+            sdf[c] = vx ? sdf_to_logical(vx->sdf) : 1.f;
+          }
+          if (!observed) continue;
+          int mask = 0;
+          for (int c = 0; c < 8; ++c)
+            if (sdf[c] < 0.f) mask |= 1 << c;
+          for (int k = 0; k < mc_cnt[mask]; ++k) {
+            uint32_t id[3];
+            for (int q = 0; q < 3; ++q) {
+              const int ed = mc_tri[mask][k][q];
+              int a = MC_E[ed][0], b = MC_E[ed][1];
+              int va[3] = {cx + MC_C[a][0], cy + MC_C[a][1], cz + MC_C[a][2]};
+              int vb[3] = {cx + MC_C[b][0], cy + MC_C[b][1], cz + MC_C[b][2]};
+              float fa = sdf[a], fb = sdf[b];
+              int axis = va[0] != vb[0] ? 0 : (va[1] != vb[1] ? 1 : 2);
+              if (va[axis] > vb[axis]) {
+                for (int t = 0; t < 3; ++t) {
+                  int x = va[t];
+                  va[t] = vb[t];
+                  vb[t] = x;
+                }
+                float ft = fa;
+                fa = fb;
+                fb = ft;
+              }
+              int added = 0;
+              id[q] = mc_map_get_or_add(&h, mc_key(va[0], va[1], va[2], axis), (uint32_t)nv, &added);
+              if (added) {
+                const float denom = fa - fb;
+                const float t = fabsf(denom) < 1e-12f ? 0.5f : fa / denom;
+                float p[3] = {(float)va[0], (float)va[1], (float)va[2]};
+                p[axis] += t;
+                if (nv == vcap) V = (float*)realloc(V, (vcap *= 2) * 12);
+                V[3 * nv + 0] = p[0] * voxelSize;
+                V[3 * nv + 1] = p[1] * voxelSize;
+                V[3 * nv + 2] = p[2] * voxelSize;
+                ++nv;
+              }
+            }
+            if (nt == tcap) T = (uint32_t*)realloc(T, (tcap *= 2) * 12);
+            T[3 * nt + 0] = id[0];
+            T[3 * nt + 1] = id[1];
+            T[3 * nt + 2] = id[2];
+            ++nt;
+          }
+        }
+  }
+  free(h.keys);
+  free(h.vals);
+  *vOut = V;
+  *tOut = T;
+  *nV = (long long)nv;
+  *nT = (long long)nt;
+  return 0;
+}
+void rfo_free(void* p) { free(p); }
+
+/* direct voxel writes (analytic TSDF test maps, as the reference's meshing
+ * tests build them) */
+int rfo_set_block(rfo_map* m, const int* pos3, const int16_t* sdf512, const uint8_t* w512) {
+  i3 p = {pos3[0], pos3[1], pos3[2]};
+  int idx = allocate_block(m, p);
+  if (idx < 0) return -1;
+  voxel_t* b = &m->vba[(size_t)m->entries[idx].ptr * BS3];
+  for (int i = 0; i < BS3; ++i) {
+    b[i].sdf = sdf512[i];
+    b[i].w = w512[i];
+  }
+  return 0;
+}
+
 /* ------------------------------------------------- full ViewBuilder */
 /* rgb_to_intensity (P/src/view.cpp:8-16): (0.299 r + 0.587 g + 0.114 b) / 255,
  * C++ left-to-right evaluation, the channels promoted to float. */

@@ -67,6 +67,11 @@ int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float aff
                    float* depthLevels);
 int rfo_render_colour(const rfo_map* m, int mode, const float* pose12, const int* wh, const float* f4,
                       const float* raycast, const float* normals, const int* list, int nList, uint8_t* rgbOut);
+/* marching cubes (meshing.cpp) */
+int rfo_mc_table(int* counts256, int* tris);
+int rfo_extract_mesh(const rfo_map* m, float voxelSize, float** vOut, uint32_t** tOut, long long* nV, long long* nT);
+void rfo_free(void* p);
+int rfo_set_block(rfo_map* m, const int* pos3, const int16_t* sdf512, const uint8_t* w512);
 /* full ViewBuilder (view.cpp:8-143) */
 void rfo_rgb_to_intensity(const uint8_t* rgb, int w, int h, float* out);
 void rfo_bilateral_filter(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out);

@@ -48,6 +48,12 @@ def lib():
         L.rfo_set_ranges.argtypes = [vp, _i, _f]
         L.rfo_render_icp.argtypes = [vp, _f, _i, _f, _f, _f, _f, _f]
         L.rfo_build_view.argtypes = [_u16, _i, C.c_float, C.c_float, C.c_int, _f]
+        L.rfo_mc_table.argtypes = [_i, _i]
+        L.rfo_extract_mesh.argtypes = [vp, C.c_float, C.POINTER(C.POINTER(C.c_float)),
+                                       C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_longlong),
+                                       C.POINTER(C.c_longlong)]
+        L.rfo_free.argtypes = [vp]
+        L.rfo_set_block.argtypes = [vp, _i, C.POINTER(C.c_int16), _u8]
         L.rfo_render_colour.argtypes = [vp, C.c_int, _f, _i, _f, _f, _f, _i, C.c_int, _u8]
         L.rfo_build_view_full.argtypes = [_u16, _u8, _i, _f, C.c_float, C.c_float, C.c_int, C.c_int, _f, _f, _f]
         L.rfo_bilateral_filter.argtypes = [_f, C.c_int, C.c_int, C.c_float, C.c_float, _f]
@@ -101,6 +107,14 @@ def build_view(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=1):
         res.append(out[o:o + s].reshape(h >> l, w >> l))
         o += s
     return res
+
+
+def mc_table():
+    cnt = np.zeros(256, np.int32)
+    tri = np.zeros(256 * 16 * 3, np.int32)
+    lib().rfo_mc_table(P(cnt, _i), P(tri, _i))
+    tri = tri.reshape(256, 16, 3)
+    return [[tuple(int(x) for x in tri[m, k]) for k in range(cnt[m])] for m in range(256)]
 
 
 def build_view_full(raw, intr, aff=(1.0 / 5000.0, 0.0), levels=3, bilateral=False, rgb=None):
@@ -241,6 +255,23 @@ class OracleEngine:
         if rc_ != 0:
             raise RuntimeError("render_icp before render_ranges")
         return rc, pts, nrm, 0.0
+
+    def extract_mesh(self, voxel_size):
+        """rfo_extract_mesh (meshing.cpp:144-217): (vertices (N,3) f32, triangles (M,3) u32)."""
+        vp_, tp_ = C.POINTER(C.c_float)(), C.POINTER(C.c_uint32)()
+        nv, nt = C.c_longlong(0), C.c_longlong(0)
+        lib().rfo_extract_mesh(self.h, voxel_size, C.byref(vp_), C.byref(tp_), C.byref(nv), C.byref(nt))
+        v = np.ctypeslib.as_array(vp_, shape=(max(nv.value, 1) * 3,))[: nv.value * 3].reshape(-1, 3).copy()
+        t = np.ctypeslib.as_array(tp_, shape=(max(nt.value, 1) * 3,))[: nt.value * 3].reshape(-1, 3).copy()
+        lib().rfo_free(C.cast(vp_, C.c_void_p))
+        lib().rfo_free(C.cast(tp_, C.c_void_p))
+        return v, t
+
+    def set_block(self, pos3, sdf512, w512):
+        p = np.ascontiguousarray(pos3, np.int32)
+        sd = np.ascontiguousarray(sdf512, np.int16)
+        w = np.ascontiguousarray(w512, np.uint8)
+        return lib().rfo_set_block(self.h, P(p, _i), P(sd, C.POINTER(C.c_int16)), P(w, _u8))
 
     def render_colour(self, mode, pose34, intr, raycast, normals, missing=None, out=None):
         """The colour image of render_maps(kColour = 1 / kGrey = 2) from the

@@ -81,6 +81,9 @@ SIGNATURES = {
                          _vp], C.c_int),
     "rfg_render_maps_list": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), C.c_int, _vp, _vp, _vp, _vp,
                               _vp, _vp, _vp], C.c_int),
+    "rfg_extract_mesh": ([_vp, C.c_float, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
+    "rfg_mesh_copy": ([_vp, _vp, _vp], C.c_int),
+    "rfg_mc_table": ([_i, _i], C.c_int),
     "rfg_build_view_depth": ([_vp, C.c_int, C.c_int, C.c_float, C.c_float, C.c_int, _vp, _vp], C.c_int),
     "rfg_build_view": ([_vp, _vp, C.POINTER(Intrinsics_), C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, _vp, _vp,
                         _vp, _vp, _vp], C.c_int),

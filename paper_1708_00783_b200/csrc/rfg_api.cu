@@ -245,6 +245,7 @@ int rfg_map_destroy(rfg_map* m) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->hostState) cudaFreeHost(m->hostState);
+  mesh_free(m->mesh);
   delete m;
   return RFG_OK;
 }
@@ -415,6 +416,30 @@ int rfg_render_maps_list(rfg_map* m, const float pose34[12], const rfg_intrinsic
                               reinterpret_cast<const float4*>(normals), missing, nMissing,
                               intr->width * intr->height, colour, m->stream));
   return RFG_OK;
+}
+
+int rfg_extract_mesh(rfg_map* m, float voxelSize, int64_t* nVertices, int64_t* nTriangles) {
+  RFG_REQUIRE(m && nVertices && nTriangles && voxelSize > 0.f, "invalid extract_mesh arguments");
+  long long nv = 0, nt = 0;
+  RFG_CK(mesh_extract(m->d, voxelSize, &m->mesh, &nv, &nt, m->stream));
+  *nVertices = nv;
+  *nTriangles = nt;
+  return RFG_OK;
+}
+
+int rfg_mesh_copy(rfg_map* m, float* vertices3, uint32_t* triangles3) {
+  RFG_REQUIRE(m, "null map");
+  if (!m->mesh) {
+    set_error("mesh_copy before extract_mesh");
+    return RFG_ESTATE;
+  }
+  RFG_CK(mesh_copy(m->mesh, vertices3, triangles3, m->stream));
+  return RFG_OK;
+}
+
+int rfg_mc_table(int32_t counts256[256], int32_t tris[256 * 16 * 3]) {
+  RFG_REQUIRE(counts256 && tris, "null argument");
+  return mc_table_export(counts256, tris);
 }
 
 int rfg_build_view_depth(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,

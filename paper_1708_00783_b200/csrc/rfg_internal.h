@@ -96,6 +96,10 @@ cudaError_t launch_forward_project(int hasRaycast, float4* raycast, float4* poin
                                    int2* tilePrefix, int* list, int* count, cudaStream_t s);
 cudaError_t launch_build_view(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
                               cudaStream_t s);
+cudaError_t mesh_extract(const DevMap& m, float vs, void** mesh, long long* nVerts, long long* nTris, cudaStream_t s);
+cudaError_t mesh_copy(void* mesh, float* verts, unsigned int* tris, cudaStream_t s);
+void mesh_free(void* mesh);
+int mc_table_export(int* counts256, int* tris256x16x3);
 cudaError_t launch_render_colour(const DevMap& m, const FrameArgs& fa, int mode, const float4* raycast,
                                  const float4* normals, const int* list, const int* count, int maxCount,
                                  uint8_t* rgb, cudaStream_t s);
@@ -119,6 +123,7 @@ struct rfg_map {
   int2* fwdTileCounts;
   int2* fwdTilePrefix;
   int fwdN;
+  void* mesh;  // rfg_mesh.cu MeshBuffers (extract_mesh scratch + result)
 };
 
 #define RFG_CK(call)                                                                      \

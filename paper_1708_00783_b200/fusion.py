@@ -382,6 +382,39 @@ def downsample_intensity(img) -> torch.Tensor:
     return out
 
 
+# ----------------------------------------------------------------- mesh
+@dataclass
+class Mesh:
+    """proj/include/rf/meshing.hpp:12-15: vertices in metres, triangles as
+    vertex-index triples (normals toward positive sdf)."""
+    vertices: np.ndarray   # (N, 3) float32
+    triangles: np.ndarray  # (M, 3) uint32
+
+
+def extract_mesh(map: "VoxelBlockMap", voxelSize: float) -> Mesh:
+    """extract_mesh (proj/src/meshing.cpp:144-217) on the GPU: marching cubes
+    over the in-memory blocks, vertices and triangles in the reference's
+    order."""
+    nv, nt = C.c_int64(0), C.c_int64(0)
+    map.bind_stream()
+    check(lib().rfg_extract_mesh(map.handle, voxelSize, C.byref(nv), C.byref(nt)))
+    v = np.empty((nv.value, 3), np.float32)
+    t = np.empty((nt.value, 3), np.uint32)
+    check(lib().rfg_mesh_copy(map.handle, v.ctypes.data_as(C.c_void_p) if nv.value else None,
+                              t.ctypes.data_as(C.c_void_p) if nt.value else None))
+    return Mesh(v, t)
+
+
+def marching_cubes_table():
+    """The 256-case triangulation (meshing.cpp:27-118): list of lists of
+    edge triples."""
+    cnt = np.zeros(256, np.int32)
+    tri = np.zeros(256 * 16 * 3, np.int32)
+    check(lib().rfg_mc_table(cnt.ctypes.data_as(C.POINTER(C.c_int32)), tri.ctypes.data_as(C.POINTER(C.c_int32))))
+    tri = tri.reshape(256, 16, 3)
+    return [[tuple(int(x) for x in tri[m, k]) for k in range(cnt[m])] for m in range(256)]
+
+
 # ------------------------------------------------------------ image IO
 def _pnm_read(fn, path, channels, dtype):
     w, h = C.c_int32(0), C.c_int32(0)
