@@ -147,6 +147,38 @@ int rfg_render_maps_list(rfg_map* map, const float pose34[12], const rfg_intrins
                          const int32_t* n_missing_dev, float* raycast_dev, float* points_dev, float* normals_dev,
                          uint8_t* colour_dev);
 
+/* --------------------------------------------------------- swapping */
+/* FusionEngine::Options (proj/include/rf/fusion.hpp:54-57). */
+typedef struct {
+  int32_t swapping_enabled;  /* visible list also keeps blocks within the margin (kBoundary = 3) */
+  float swap_margin_px;      /* default 8 */
+} rfg_fusion_options;
+/* allocate_from_depth(..., const Options&) (fusion.hpp:63-66). */
+int rfg_allocate_from_depth_ex(rfg_map* map, const float* depth_dev, const rfg_intrinsics* intr,
+                               const float pose34[12], const rfg_scene_params* params,
+                               const rfg_fusion_options* opts, rfg_alloc_stats* stats);
+/* VoxelBlockMap::reserveBlockForEntry (returns 1 reserved / already
+ * resident, 0 VBA exhausted) and releaseBlock (voxel_block_map.cpp:107-123). */
+int rfg_map_reserve_block(rfg_map* map, int entry_index);
+int rfg_map_release_block(rfg_map* map, int entry_index);
+/* The swapping engine (rfg_swap.cu): host voxel store per
+ * entry + transfer buffers of `capacity` blocks per frame and direction.
+ * Per frame: rfg_allocate_from_depth_ex(swapping_enabled = 1) ->
+ * rfg_swap_in (blocks visible but swapped out come back, ascending entry
+ * index, merged into fresh VBA blocks) -> integrate / render ->
+ * rfg_swap_out (blocks invisible for 2 frames go to the host, ascending
+ * index).  Both synchronise the map's stream. */
+typedef struct rfg_swap rfg_swap;
+int rfg_swap_create(rfg_map* map, int capacity_blocks, rfg_swap** out);
+int rfg_swap_destroy(rfg_swap* swap);
+int rfg_swap_in(rfg_swap* swap, int max_w, int* n_swapped_in);
+int rfg_swap_out(rfg_swap* swap, int* n_swapped_out);
+/* host tier export (tests): per-entry stored flags and invisible-frame ages
+ * (totalEntries bytes each, either may be NULL); one stored block as
+ * VoxelSRgb bytes */
+int rfg_swap_export(rfg_swap* swap, uint8_t* has_out, uint8_t* age_out);
+int rfg_swap_host_block(rfg_swap* swap, int entry_index, uint8_t* voxels_srgb_4096);
+
 /* ---------------------------------------------------------------- mesh */
 /* extract_mesh (proj/src/meshing.cpp:144-217): marching cubes over the
  * in-memory blocks of the map.  Vertices (metres) and triangles come out in

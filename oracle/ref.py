@@ -58,6 +58,9 @@ def lib():
         L.rr_export_blocks.argtypes = [C.c_void_p, _i, C.c_int, _u8]
         L.rr_export_visible.argtypes = [C.c_void_p, _i, _u8]
         L.rr_free_counts.argtypes = [C.c_void_p, _i, _i]
+        L.rr_set_fusion_options.argtypes = [C.c_void_p, C.c_int, C.c_float]
+        L.rr_reserve_block.argtypes = [C.c_void_p, C.c_int]
+        L.rr_release_block.argtypes = [C.c_void_p, C.c_int]
         L.rr_extract_mesh.argtypes = [C.c_void_p, C.c_float, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
         L.rr_mesh_copy.argtypes = [C.c_void_p, _f, C.POINTER(C.c_uint32)]
         L.rr_mc_table.argtypes = [_i, _i]
@@ -309,6 +312,15 @@ class RefEngine:
         wh, f4 = _wh(intr), _f4(intr)
         r = _f32(rng)
         lib().rr_set_ranges(self.h, P(wh, _i), P(f4, _f), P(r, _f))
+
+    def set_fusion_options(self, swapping_enabled, swap_margin_px=8.0):
+        lib().rr_set_fusion_options(self.h, 1 if swapping_enabled else 0, swap_margin_px)
+
+    def reserve_block(self, idx):
+        return lib().rr_reserve_block(self.h, idx)
+
+    def release_block(self, idx):
+        lib().rr_release_block(self.h, idx)
 
     def extract_mesh(self, voxel_size):
         """extract_mesh (meshing.cpp:144-217): (vertices (N,3) f32, triangles (M,3) u32)."""

@@ -118,6 +118,7 @@ struct Engine {
   FusionEngine fusion;
   RenderState render;
   Mesh mesh;
+  FusionEngine::Options opts;
 };
 
 View makeView(const float* depth, const std::uint8_t* rgb, const Intrinsics& intrD, const Intrinsics& intrRgb,
@@ -357,12 +358,26 @@ int rr_allocate(void* h, const float* depth, const int* wh, const float* f4, con
   const Intrinsics intr = intrFrom(wh, f4);
   const View v = makeView(depth, nullptr, intr, intr, nullptr);
   const double t0 = nowMs();
-  const AllocationStats s = e->fusion.allocate_from_depth(e->map, v, poseFrom12(pose12), paramsFrom(params));
+  const AllocationStats s = e->fusion.allocate_from_depth(e->map, v, poseFrom12(pose12), paramsFrom(params), e->opts);
   if (ms) *ms = nowMs() - t0;
   stats4[0] = s.requested;
   stats4[1] = s.allocated;
   stats4[2] = s.allocFailures;
   stats4[3] = s.visibleCount;
+  return 0;
+}
+
+// FusionEngine::Options (fusion.hpp:54-57) for the engine's allocate calls
+int rr_set_fusion_options(void* h, int swappingEnabled, float swapMarginPx) {
+  auto* e = static_cast<Engine*>(h);
+  e->opts.swappingEnabled = swappingEnabled != 0;
+  e->opts.swapMarginPx = swapMarginPx;
+  return 0;
+}
+// VoxelBlockMap::reserveBlockForEntry / releaseBlock (voxel_block_map.cpp:107-123)
+int rr_reserve_block(void* h, int idx) { return static_cast<Engine*>(h)->map.reserveBlockForEntry(idx) ? 1 : 0; }
+int rr_release_block(void* h, int idx) {
+  static_cast<Engine*>(h)->map.releaseBlock(idx);
   return 0;
 }
 

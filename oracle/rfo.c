@@ -66,6 +66,9 @@ struct rfo_map {
   int rangeW, rangeH;
   /* shard filter */
   int rank, world, tileShift;
+  /* FusionEngine::Options (proj/include/rf/fusion.hpp:54-57) */
+  int swapping;
+  float swapMargin;
 };
 
 /* ------------------------------------------------------------ core math */
@@ -509,8 +512,13 @@ int rfo_allocate(rfo_map* m, const float* depth, const int* wh, const float* f4,
     const entry_t* e = &m->entries[idx];
     if (!allocated(e)) continue;
     i3 p = {e->x, e->y, e->z};
-    if (block_in_frustum(p, &pose, &in, &s, 0.f)) {
-      m->visibility[idx] = e->ptr >= 0 ? 1 : 2;
+    uint8_t type = 0;
+    if (block_in_frustum(p, &pose, &in, &s, 0.f))
+      type = e->ptr >= 0 ? 1 : 2;
+    else if (m->swapping && block_in_frustum(p, &pose, &in, &s, m->swapMargin))
+      type = 3; /* kBoundary, fusion.cpp:223-224 */
+    if (type) {
+      m->visibility[idx] = type;
       m->visible[nv++] = (int)idx;
     }
   }
@@ -987,6 +995,138 @@ int rfo_render_colour(const rfo_map* m, int mode, const float* pose12, const int
       o[0] = o[1] = o[2] = g;
     }
   }
+  return 0;
+}
+
+/* ----------------------------------------------------------- swapping */
+/* FusionEngine::Options (fusion.hpp:54-57) */
+void rfo_set_fusion_options(rfo_map* m, int swappingEnabled, float swapMarginPx) {
+  m->swapping = swappingEnabled;
+  m->swapMargin = swapMarginPx;
+}
+
+/* VoxelBlockMap::reserveBlockForEntry (voxel_block_map.cpp:107-116): pop a
+ * VBA block, reset it to Voxel{} and attach it. */
+int rfo_reserve_block(rfo_map* m, int idx) {
+  entry_t* e = &m->entries[idx];
+  if (e->ptr >= 0) return 1;
+  if (m->nFreeBlocks == 0) return 0;
+  const int ptr = m->freeBlocks[--m->nFreeBlocks];
+  voxel_t* b = &m->vba[(size_t)ptr * BS3];
+  for (int i = 0; i < BS3; ++i) {
+    memset(&b[i], 0, sizeof(voxel_t));
+    b[i].sdf = 32767;
+  }
+  e->ptr = ptr;
+  return 1;
+}
+/* VoxelBlockMap::releaseBlock (voxel_block_map.cpp:118-123): push the block
+ * back (contents kept) and mark the entry swapped out. */
+void rfo_release_block(rfo_map* m, int idx) {
+  entry_t* e = &m->entries[idx];
+  if (e->ptr < 0) return;
+  m->freeBlocks[m->nFreeBlocks++] = e->ptr;
+  e->ptr = -1;
+}
+
+/* The swapping engine (the reference has only the hooks
+ * above, so this restatement is the oracle): a host voxel store indexed by
+ * entry, transfer capacity C blocks per frame and direction.
+ *   swap-in (after allocation, before integration): entries with visibility
+ *     2 (visible, swapped out) that have host data, ascending index, at most
+ *     C: reserve a block (reserveBlockForEntry order) and merge the host
+ *     voxels into the fresh block (w = 0 device voxel -> host voxel;
+ *     otherwise the running-average merge); stops when the VBA is exhausted
+ *     (the rest stay queued).
+ *   swap-out (after integration): per resident entry, age = 0 if it has a
+ *     visibility type this frame, else age + 1 (saturating); entries with
+ *     age >= 2, ascending index, at most C: copy the block to the host
+ *     store, reset it to Voxel{} and release it. */
+typedef struct {
+  int capacity;
+  voxel_t* host;  /* total entries x 512 */
+  uint8_t* has;
+  uint8_t* age;
+} rfo_swap;
+
+rfo_swap* rfo_swap_create(const rfo_map* m, int capacity) {
+  const size_t total = (size_t)m->buckets + m->excess;
+  rfo_swap* w = (rfo_swap*)calloc(1, sizeof(rfo_swap));
+  w->capacity = capacity;
+  w->host = (voxel_t*)calloc(total * BS3, sizeof(voxel_t));
+  w->has = (uint8_t*)calloc(total, 1);
+  w->age = (uint8_t*)calloc(total, 1);
+  return w;
+}
+void rfo_swap_destroy(rfo_swap* w) {
+  if (!w) return;
+  free(w->host);
+  free(w->has);
+  free(w->age);
+  free(w);
+}
+
+static void merge_voxel(voxel_t* d, const voxel_t* h, int maxW) {
+  if (d->w == 0) {
+    *d = *h;
+    return;
+  }
+  if (h->w == 0) return;
+  const float fd = sdf_to_logical(d->sdf), fh = sdf_to_logical(h->sdf);
+  const float merged = ((float)d->w * fd + (float)h->w * fh) / (float)(d->w + h->w);
+  const int w = d->w + h->w;
+  d->sdf = sdf_from_logical(merged);
+  d->w = (uint8_t)(w < maxW ? w : maxW);
+}
+
+int rfo_swap_in(rfo_map* m, rfo_swap* w, int maxW) {
+  const size_t total = (size_t)m->buckets + m->excess;
+  int n = 0;
+  for (size_t idx = 0; idx < total && n < w->capacity; ++idx) {
+    if (m->visibility[idx] != 2 || !w->has[idx]) continue;
+    if (!rfo_reserve_block(m, (int)idx)) break; /* VBA exhausted: left queued */
+    voxel_t* b = &m->vba[(size_t)m->entries[idx].ptr * BS3];
+    for (int i = 0; i < BS3; ++i) merge_voxel(&b[i], &w->host[idx * BS3 + i], maxW);
+    ++n;
+  }
+  return n;
+}
+
+int rfo_swap_out(rfo_map* m, rfo_swap* w) {
+  const size_t total = (size_t)m->buckets + m->excess;
+  int n = 0;
+  for (size_t idx = 0; idx < total; ++idx) {
+    const entry_t* e = &m->entries[idx];
+    if (e->ptr < 0) continue;
+    if (m->visibility[idx])
+      w->age[idx] = 0;
+    else if (w->age[idx] < 255)
+      w->age[idx]++;
+    if (w->age[idx] >= 2 && n < w->capacity) {
+      voxel_t* b = &m->vba[(size_t)e->ptr * BS3];
+      memcpy(&w->host[idx * BS3], b, sizeof(voxel_t) * BS3);
+      w->has[idx] = 1;
+      /* the released block comes back clean (allocateBlock does not clear
+       * reused blocks; SPEC.md:444 equivalence) */
+      for (int i = 0; i < BS3; ++i) {
+        memset(&b[i], 0, sizeof(voxel_t));
+        b[i].sdf = 32767;
+      }
+      rfo_release_block(m, (int)idx);
+      ++n;
+    }
+  }
+  return n;
+}
+
+/* host store export (tests): has flags and the stored block of an entry */
+int rfo_swap_export(const rfo_swap* w, size_t total, uint8_t* hasOut, uint8_t* ageOut) {
+  if (hasOut) memcpy(hasOut, w->has, total);
+  if (ageOut) memcpy(ageOut, w->age, total);
+  return 0;
+}
+int rfo_swap_host_block(const rfo_swap* w, int idx, uint8_t* out4096) {
+  memcpy(out4096, &w->host[(size_t)idx * BS3], sizeof(voxel_t) * BS3);
   return 0;
 }
 

@@ -67,6 +67,10 @@ int rfo_build_view(const uint16_t* raw, const int* wh, float affScale, float aff
                    float* depthLevels);
 int rfo_render_colour(const rfo_map* m, int mode, const float* pose12, const int* wh, const float* f4,
                       const float* raycast, const float* normals, const int* list, int nList, uint8_t* rgbOut);
+/* swapping: reference hooks + the SPEC's engine */
+void rfo_set_fusion_options(rfo_map* m, int swappingEnabled, float swapMarginPx);
+int rfo_reserve_block(rfo_map* m, int idx);
+void rfo_release_block(rfo_map* m, int idx);
 /* marching cubes (meshing.cpp) */
 int rfo_mc_table(int* counts256, int* tris);
 int rfo_extract_mesh(const rfo_map* m, float voxelSize, float** vOut, uint32_t** tOut, long long* nV, long long* nT);

@@ -48,6 +48,16 @@ def lib():
         L.rfo_set_ranges.argtypes = [vp, _i, _f]
         L.rfo_render_icp.argtypes = [vp, _f, _i, _f, _f, _f, _f, _f]
         L.rfo_build_view.argtypes = [_u16, _i, C.c_float, C.c_float, C.c_int, _f]
+        L.rfo_set_fusion_options.argtypes = [vp, C.c_int, C.c_float]
+        L.rfo_reserve_block.argtypes = [vp, C.c_int]
+        L.rfo_release_block.argtypes = [vp, C.c_int]
+        L.rfo_swap_create.argtypes = [vp, C.c_int]
+        L.rfo_swap_create.restype = vp
+        L.rfo_swap_destroy.argtypes = [vp]
+        L.rfo_swap_in.argtypes = [vp, vp, C.c_int]
+        L.rfo_swap_out.argtypes = [vp, vp]
+        L.rfo_swap_export.argtypes = [vp, C.c_size_t, _u8, _u8]
+        L.rfo_swap_host_block.argtypes = [vp, C.c_int, _u8]
         L.rfo_mc_table.argtypes = [_i, _i]
         L.rfo_extract_mesh.argtypes = [vp, C.c_float, C.POINTER(C.POINTER(C.c_float)),
                                        C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_longlong),
@@ -206,6 +216,9 @@ class OracleEngine:
         self.capacity = capacity
 
     def __del__(self):
+        if getattr(self, "sw", None):
+            lib().rfo_swap_destroy(self.sw)
+            self.sw = None
         if getattr(self, "h", None):
             lib().rfo_destroy(self.h)
             self.h = None
@@ -255,6 +268,35 @@ class OracleEngine:
         if rc_ != 0:
             raise RuntimeError("render_icp before render_ranges")
         return rc, pts, nrm, 0.0
+
+    def set_fusion_options(self, swapping_enabled, swap_margin_px=8.0):
+        lib().rfo_set_fusion_options(self.h, 1 if swapping_enabled else 0, swap_margin_px)
+
+    def reserve_block(self, idx):
+        return lib().rfo_reserve_block(self.h, idx)
+
+    def release_block(self, idx):
+        lib().rfo_release_block(self.h, idx)
+
+    def swap_create(self, capacity):
+        self.sw = lib().rfo_swap_create(self.h, capacity)
+
+    def swap_in(self, max_w=100):
+        return lib().rfo_swap_in(self.h, self.sw, max_w)
+
+    def swap_out(self):
+        return lib().rfo_swap_out(self.h, self.sw)
+
+    def swap_stored(self):
+        n = lib().rfo_total_entries(self.h)
+        has, age = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+        lib().rfo_swap_export(self.sw, n, P(has, _u8), P(age, _u8))
+        return has, age
+
+    def swap_host_block(self, idx):
+        out = np.zeros((512, 8), np.uint8)
+        lib().rfo_swap_host_block(self.sw, idx, P(out, _u8))
+        return out
 
     def extract_mesh(self, voxel_size):
         """rfo_extract_mesh (meshing.cpp:144-217): (vertices (N,3) f32, triangles (M,3) u32)."""

@@ -43,6 +43,10 @@ class AllocStats_(C.Structure):
                 ("visibleCount", C.c_int32)]
 
 
+class FusionOptions_(C.Structure):
+    _fields_ = [("swapping_enabled", C.c_int32), ("swap_margin_px", C.c_float)]
+
+
 class PipelineConfig_(C.Structure):
     _fields_ = [("intr", Intrinsics_), ("params", SceneParams_), ("aff_scale", C.c_float),
                 ("aff_offset", C.c_float), ("levels", C.c_int32), ("track", C.c_int32),
@@ -71,6 +75,16 @@ SIGNATURES = {
                                  C.POINTER(AllocStats_)], C.c_int),
     "rfg_integrate": ([_vp, _vp, _vp, C.POINTER(Intrinsics_), C.POINTER(Intrinsics_), _f, _f,
                        C.POINTER(SceneParams_)], C.c_int),
+    "rfg_allocate_from_depth_ex": ([_vp, _vp, C.POINTER(Intrinsics_), _f, C.POINTER(SceneParams_),
+                                    C.POINTER(FusionOptions_), C.POINTER(AllocStats_)], C.c_int),
+    "rfg_map_reserve_block": ([_vp, C.c_int], C.c_int),
+    "rfg_map_release_block": ([_vp, C.c_int], C.c_int),
+    "rfg_swap_create": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
+    "rfg_swap_destroy": ([_vp], C.c_int),
+    "rfg_swap_in": ([_vp, C.c_int, _i], C.c_int),
+    "rfg_swap_out": ([_vp, _i], C.c_int),
+    "rfg_swap_export": ([_vp, _u8, _u8], C.c_int),
+    "rfg_swap_host_block": ([_vp, C.c_int, _u8], C.c_int),
     "rfg_render_expected_ranges": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), _vp], C.c_int),
     "rfg_render_icp_maps": ([_vp, _f, C.POINTER(Intrinsics_), C.POINTER(SceneParams_), _vp, _vp, _vp, _vp],
                             C.c_int),

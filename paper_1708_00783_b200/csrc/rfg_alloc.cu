@@ -317,8 +317,9 @@ __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const flo
 }
 
 // --------------------------------------------------------------- stage 3
-// proj/src/fusion.cpp:116-130
-__device__ __forceinline__ bool block_in_frustum(int bx, int by, int bz, const Pose& pose, const FrameArgs& fa) {
+// proj/src/fusion.cpp:116-130 (marginPx: the swap-in boundary band)
+__device__ __forceinline__ bool block_in_frustum(int bx, int by, int bz, const Pose& pose, const FrameArgs& fa,
+                                                 float marginPx = 0.f) {
   const float bs = fa.voxelSize * (float)kBlock;
 #pragma unroll 1
   for (int c = 0; c < 8; ++c) {
@@ -328,7 +329,9 @@ __device__ __forceinline__ bool block_in_frustum(int bx, int by, int bz, const P
     if (pc.z < fa.vfMin || pc.z > fa.vfMax) continue;
     const float px = fa.fx * pc.x / pc.z + fa.cx;
     const float py = fa.fy * pc.y / pc.z + fa.cy;
-    if (px >= -0.f && py >= -0.f && px <= (float)(fa.w - 1) + 0.f && py <= (float)(fa.h - 1) + 0.f) return true;
+    if (px >= -marginPx && py >= -marginPx && px <= (float)(fa.w - 1) + marginPx &&
+        py <= (float)(fa.h - 1) + marginPx)
+      return true;
   }
   return false;
 }
@@ -372,8 +375,15 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
     const int idx = queue[i];
     const int4 e = ld_entry(m.entries, idx);
     if (!entry_allocated(e)) continue;
-    if (block_in_frustum(entry_x(e), entry_y(e), entry_z(e), pose, fa)) {
-      m.visibility[idx] = e.w >= 0 ? 1 : 2;
+    // fusion.cpp:219-229: visible (1), visible but swapped out (2), or with
+    // swapping enabled inside the swap-in margin (3, kBoundary)
+    uint8_t type = 0;
+    if (block_in_frustum(entry_x(e), entry_y(e), entry_z(e), pose, fa))
+      type = e.w >= 0 ? 1 : 2;
+    else if (fa.swapping && block_in_frustum(entry_x(e), entry_y(e), entry_z(e), pose, fa, fa.swapMargin))
+      type = 3;
+    if (type) {
+      m.visibility[idx] = type;
       ++n;
     }
   }

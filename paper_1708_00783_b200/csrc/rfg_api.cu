@@ -57,6 +57,8 @@ FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p,
   fa.stopAtMaxW = p->stopIntegratingAtMaxW;
   for (int i = 0; i < 12; ++i) fa.pose[i] = pose34 ? pose34[i] : ((i % 5 == 0) ? 1.f : 0.f);
   fa.poseDev = poseDev;
+  fa.swapping = 0;
+  fa.swapMargin = 8.f;
   return fa;
 }
 
@@ -294,10 +296,20 @@ int rfg_map_set_shard(rfg_map* m, int rank, int world, int tileShift) {
 
 int rfg_allocate_from_depth(rfg_map* m, const float* depth, const rfg_intrinsics* intr, const float pose34[12],
                             const rfg_scene_params* params, rfg_alloc_stats* stats) {
+  return rfg_allocate_from_depth_ex(m, depth, intr, pose34, params, nullptr, stats);
+}
+
+int rfg_allocate_from_depth_ex(rfg_map* m, const float* depth, const rfg_intrinsics* intr, const float pose34[12],
+                               const rfg_scene_params* params, const rfg_fusion_options* opts,
+                               rfg_alloc_stats* stats) {
   RFG_REQUIRE(m && depth && pose34, "null argument");
   RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
   RFG_REQUIRE((size_t)intr->width * intr->height < (1u << 25), "image too large for the 25-bit pixel key");
-  const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
+  if (opts) {
+    fa.swapping = opts->swapping_enabled ? 1 : 0;
+    fa.swapMargin = opts->swap_margin_px;
+  }
   RFG_CK(launch_allocate(m->d, depth, fa, m->stream));
   if (stats) {
     const int rc = check_device_error(m);  // synchronises, refreshes hostState

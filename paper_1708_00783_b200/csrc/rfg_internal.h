@@ -60,6 +60,8 @@ struct FrameArgs {
   int stopAtMaxW;
   float pose[12];          // world -> camera (used when poseDev == nullptr)
   const float* poseDev;    // device-resident pose (tracking pipeline)
+  int swapping;            // FusionEngine::Options::swappingEnabled (fusion.hpp:55)
+  float swapMargin;        // Options::swapMarginPx (fusion.hpp:56)
 };
 
 struct Pose12 {
@@ -96,6 +98,10 @@ cudaError_t launch_forward_project(int hasRaycast, float4* raycast, float4* poin
                                    int2* tilePrefix, int* list, int* count, cudaStream_t s);
 cudaError_t launch_build_view(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
                               cudaStream_t s);
+// exclusive scan of n ints on the device (rfg_mesh.cu); tileScratch holds
+// scan_tile_scratch_ints(n) ints, *total (device) receives the sum
+long long scan_tile_scratch_ints(long long n);
+cudaError_t scan_exclusive(const int* in, long long n, int* out, int* tileScratch, int* total, cudaStream_t s);
 cudaError_t mesh_extract(const DevMap& m, float vs, void** mesh, long long* nVerts, long long* nTris, cudaStream_t s);
 cudaError_t mesh_copy(void* mesh, float* verts, unsigned int* tris, cudaStream_t s);
 void mesh_free(void* mesh);

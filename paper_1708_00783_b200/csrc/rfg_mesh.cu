@@ -424,8 +424,9 @@ __global__ void __launch_bounds__(1024) k_scan_apply(const int* __restrict__ in,
   if (i0 + 1 < n) out[i0 + 1] = ex + a;
 }
 
-static cudaError_t scan_exclusive(const int* in, long long n, int* out, int* tileScratch, int* total,
-                                  cudaStream_t s) {
+long long scan_tile_scratch_ints(long long n) { return (n + kScanTile - 1) / kScanTile + 2; }
+
+cudaError_t scan_exclusive(const int* in, long long n, int* out, int* tileScratch, int* total, cudaStream_t s) {
   const int nTiles = (int)((n + kScanTile - 1) / kScanTile);
   if (nTiles == 0) return cudaMemsetAsync(total, 0, sizeof(int), s);
   k_scan_tile_sums<<<nTiles, 1024, 0, s>>>(in, n, tileScratch);

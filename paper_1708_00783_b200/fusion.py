@@ -218,6 +218,19 @@ class VoxelBlockMap:
         check(lib().rfg_map_sync(self._h))
 
     # -- parity exports (host copies) --
+    def reserveBlockForEntry(self, idx: int) -> bool:
+        """voxel_block_map.cpp:107-116"""
+        self.bind_stream()
+        rc = lib().rfg_map_reserve_block(self._h, idx)
+        if rc < 0:
+            check(rc)
+        return rc == 1
+
+    def releaseBlock(self, idx: int) -> None:
+        """voxel_block_map.cpp:118-123"""
+        self.bind_stream()
+        check(lib().rfg_map_release_block(self._h, idx))
+
     def entries(self) -> np.ndarray:
         """(totalEntries, 5) int32 {x, y, z, offset, ptr}"""
         out = np.zeros((self.totalEntries(), 5), np.int32)
@@ -500,14 +513,22 @@ def view_from_depth(depth_m, intr: Intrinsics, rgb=None, calib: RgbdCalib | None
 class FusionEngine:
     """proj/include/rf/fusion.hpp:52-79 — per-frame allocation + integration."""
 
+    @dataclass
+    class Options:
+        """FusionEngine::Options (fusion.hpp:54-57)."""
+        swappingEnabled: bool = False
+        swapMarginPx: float = 8.0
+
     def allocate_from_depth(self, map: VoxelBlockMap, view: View, pose, params: SceneParams,
-                            sync: bool = True) -> AllocationStats | None:
+                            opts: "FusionEngine.Options | None" = None, sync: bool = True) -> AllocationStats | None:
         p = _pose(pose)
         map.bind_stream()
         st = _lib.AllocStats_()
         intr = view.calib.intrinsics_d.c()
-        check(lib().rfg_allocate_from_depth(map.handle, _ptr(view.depth_m), C.byref(intr), _fp(p),
-                                            C.byref(params.c()), C.byref(st) if sync else None))
+        o = _lib.FusionOptions_(1 if opts.swappingEnabled else 0, opts.swapMarginPx) if opts else None
+        check(lib().rfg_allocate_from_depth_ex(map.handle, _ptr(view.depth_m), C.byref(intr), _fp(p),
+                                               C.byref(params.c()), C.byref(o) if o is not None else None,
+                                               C.byref(st) if sync else None))
         if not sync:
             return None
         return AllocationStats(st.requested, st.allocated, st.allocFailures, st.visibleCount)
@@ -521,6 +542,50 @@ class FusionEngine:
         use_colour = view.hasColour() and map.colour
         check(lib().rfg_integrate(map.handle, _ptr(view.depth_m), _ptr(view.rgb) if use_colour else None,
                                   C.byref(intr_d), C.byref(intr_rgb), _fp(extr), _fp(p), C.byref(params.c())))
+
+
+class SwappingEngine:
+    """The swapping engine (rfg_swap.cu): host voxel store +
+    transfer buffers of `capacity` blocks per frame and direction.  Per frame:
+    allocate_from_depth(opts=Options(swappingEnabled=True)) -> swap_in() ->
+    integrate / render -> swap_out()."""
+
+    def __init__(self, map: VoxelBlockMap, capacity: int = 512):
+        self.map = map
+        self._h = C.c_void_p()
+        map.bind_stream()
+        check(lib().rfg_swap_create(map.handle, capacity, C.byref(self._h)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.rfg_swap_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def swap_in(self, maxW: int = 100) -> int:
+        n = C.c_int(0)
+        check(lib().rfg_swap_in(self._h, maxW, C.byref(n)))
+        return n.value
+
+    def swap_out(self) -> int:
+        n = C.c_int(0)
+        check(lib().rfg_swap_out(self._h, C.byref(n)))
+        return n.value
+
+    def stored(self):
+        """(has, age): per-entry host-data flags and invisible-frame ages."""
+        n = self.map.totalEntries()
+        has, age = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+        check(lib().rfg_swap_export(self._h, has.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                    age.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return has, age
+
+    def host_block(self, idx: int) -> np.ndarray:
+        out = np.zeros((512, 8), np.uint8)
+        check(lib().rfg_swap_host_block(self._h, idx, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out
 
 
 # -------------------------------------------------------------- raycast

@@ -62,9 +62,36 @@ class GpuEngine:
     def set_shard(self, rank, world, tile_shift=3):
         self.map.set_shard(rank, world, tile_shift)
 
+    opts = None
+
+    def set_fusion_options(self, swapping_enabled, swap_margin_px=8.0):
+        self.opts = self.F.FusionEngine.Options(bool(swapping_enabled), swap_margin_px)
+
     def allocate(self, depth, intr, pose34, params):
-        st = self.fusion.allocate_from_depth(self.map, self._view(depth, intr), pose34, self._params(params))
+        st = self.fusion.allocate_from_depth(self.map, self._view(depth, intr), pose34, self._params(params),
+                                             opts=self.opts)
         return st.as_array(), 0.0
+
+    def reserve_block(self, idx):
+        return 1 if self.map.reserveBlockForEntry(idx) else 0
+
+    def release_block(self, idx):
+        self.map.releaseBlock(idx)
+
+    def swap_create(self, capacity):
+        self.sw = self.F.SwappingEngine(self.map, capacity)
+
+    def swap_in(self, max_w=100):
+        return self.sw.swap_in(max_w)
+
+    def swap_out(self):
+        return self.sw.swap_out()
+
+    def swap_stored(self):
+        return self.sw.stored()
+
+    def swap_host_block(self, idx):
+        return self.sw.host_block(idx)
 
     def integrate(self, depth, intr, pose34, params, rgb=None, intr_rgb=None, extr34=None):
         self.fusion.integrate_frame(self.map, self._view(depth, intr, rgb, intr_rgb, extr34), pose34,

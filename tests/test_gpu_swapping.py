@@ -1,0 +1,84 @@
+"""Swapping engine on the GPU (rfg_swap.cu) vs the oracle's restatement of
+SPEC.md:407-465 (oracle/rfo.c:rfo_swap_*), bit-exact every frame of a
+revisiting trajectory: entries, visible list + types (incl. kBoundary and
+kVisibleSwapped), free stack, resident VBA, host-store flags, invisible-frame
+ages and the stored blocks — with a transfer capacity small enough that
+demand is deferred across frames and one large enough that it is not; plus
+the reference hooks (reserveBlockForEntry / releaseBlock) and colour maps."""
+import numpy as np
+import pytest
+
+from helpers import AFF, GpuEngine, small_intr
+from oracle import rfo
+from test_oracle_swapping import CFG, ORDER, _frames, _params, _same_state
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cap", [37, 100000])
+def test_swapping_engine_bit_exact_vs_oracle(cap):
+    intr, pd = small_intr(), _params()
+    g, o = GpuEngine(*CFG), rfo.OracleEngine(*CFG)
+    for e in (g, o):
+        e.set_fusion_options(True, 8.0)
+        e.swap_create(cap)
+    moved = 0
+    for pose, d in _frames(intr, ORDER + ORDER[1:]):
+        for e in (g, o):
+            e.allocate(d, intr, pose, pd)
+        ni = (g.swap_in(), o.swap_in())
+        assert ni[0] == ni[1]
+        for e in (g, o):
+            e.integrate(d, intr, pose, pd)
+        no = (g.swap_out(), o.swap_out())
+        assert no[0] == no[1]
+        moved += ni[0] + no[0]
+        _same_state(g, o)
+        hg, ag = g.swap_stored()
+        ho, ao = o.swap_stored()
+        assert np.array_equal(hg, ho) and np.array_equal(ag, ao)
+    assert moved > 200
+    for i in np.nonzero(ho)[0][::17]:
+        assert np.array_equal(g.swap_host_block(int(i)), o.swap_host_block(int(i)))
+
+
+def test_reserve_release_hooks_bit_exact():
+    intr, pd = small_intr(), _params()
+    g, o = GpuEngine(*CFG), rfo.OracleEngine(*CFG)
+    fr = _frames(intr, [0, 30, 60])
+    for k, (pose, d) in enumerate(fr):
+        for e in (g, o):
+            e.allocate(d, intr, pose, pd)
+            e.integrate(d, intr, pose, pd)
+        if k == 0:
+            ent = o.entries()
+            for idx in np.nonzero(ent[:, 4] >= 0)[0][::5][:60]:
+                for e in (g, o):
+                    e.release_block(int(idx))
+        if k == 1:
+            ent = o.entries()
+            for idx in np.nonzero(ent[:, 4] == -1)[0][:30]:
+                assert g.reserve_block(int(idx)) == o.reserve_block(int(idx)) == 1
+        _same_state(g, o)
+
+
+def test_swapping_colour_map():
+    """Colour planes travel with the depth planes."""
+    from paper_1708_00783_b200 import fusion as F
+    intr, pd = small_intr(), _params()
+    fi = F.Intrinsics(**intr)
+    poses = F.orbit_trajectory(frames=100)
+    g, o = GpuEngine(*CFG, colour=True), rfo.OracleEngine(*CFG)
+    for e in (g, o):
+        e.set_fusion_options(True, 8.0)
+        e.swap_create(50)
+    for f in [0, 30, 60, 90, 60, 30, 0]:
+        raw, _, col = F.synth_render(0, poses[f], fi, rgb=True)
+        d = rfo.build_view(raw, intr, AFF, 1)[0]
+        for e in (g, o):
+            e.allocate(d, intr, poses[f], pd)
+        assert g.swap_in() == o.swap_in()
+        for e in (g, o):
+            e.integrate(d, intr, poses[f], pd, rgb=col, intr_rgb=intr)
+        assert g.swap_out() == o.swap_out()
+        _same_state(g, o)
