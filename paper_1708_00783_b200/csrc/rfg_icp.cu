@@ -279,6 +279,81 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
   }
 }
 
+// One evaluation's per-CTA partial: every valid level pixel p (grid stride)
+// is associated and accumulated in double (J J^T, J r, r^2, count), reduced
+// per warp by recursive halving and over the CTA's warps; on return thread k
+// < 29 of the CTA holds sum k of its pixels (returned), the others 0.
+__device__ __forceinline__ double icp_cta_partial(const IcpLevelArgs& a, const GnShared& g, const Pose& rp,
+                                                  const Intr& inl, float dist2, int n, int p0, int pstride,
+                                                  double (*sh)[29]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double out = 0.0;
+  const Pose c2w = pose_from12(g.c2wF);
+  double acc[29];
+#pragma unroll
+  for (int k = 0; k < 29; ++k) acc[k] = 0.0;
+  for (int p = p0; p < n; p += pstride) {
+    const float d = __ldg(a.depth + p);
+    if (!(d > 0.f)) continue;
+    const int x = p % a.lw, y = p / a.lw;
+    const f3 pc = backproject(inl, (float)x, (float)y, d);
+    const f3 pw = pose_apply(c2w, pc);
+    const f3 q = pose_apply(rp, pw);
+    if (!(q.z > 0.f)) continue;
+    const float u = a.rfx * q.x / q.z + a.rcx;
+    const float v = a.rfy * q.y / q.z + a.rcy;
+    if (!(u >= 0.f && v >= 0.f && u <= (float)(a.rw - 1) && v <= (float)(a.rh - 1))) continue;
+    const int iu = (int)(u + 0.5f), iv = (int)(v + 0.5f);
+    const float4 V = __ldg(a.points + (size_t)iv * a.rw + iu);
+    const float4 N = __ldg(a.normals + (size_t)iv * a.rw + iu);
+    if (!(V.w > 0.f) || !(N.w > 0.f)) continue;
+    const f3 diff{pw.x - V.x, pw.y - V.y, pw.z - V.z};
+    if (sqnorm3(diff) > dist2) continue;
+    const f3 nn{N.x, N.y, N.z};
+    const float r = dot3(diff, nn);
+    const f3 pxn = cross3(pw, nn);
+    const double J[6] = {pxn.x, pxn.y, pxn.z, nn.x, nn.y, nn.z};
+    const double rd = r;
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = i; j < 6; ++j) acc[k++] += J[i] * J[j];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * rd;
+    acc[27] += rd * rd;
+    acc[28] += 1.0;
+  }
+  {
+    // multi-value warp reduction by recursive halving: at offset o every
+    // lane keeps one half of its live values and sends the other half to
+    // lane^o, so 32 (29 + 3 zero) sums take 16+8+4+2+1 = 31 shuffles
+    // instead of 29 x 5.  Lane l ends with sum number l.
+    double v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = k < 29 ? acc[k] : 0.0;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool hi = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < o; ++i) {
+        const double send = hi ? v[i] : v[i + o];
+        const double keep = hi ? v[i + o] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    if (lane < 29) sh[wid][lane] = v[0];
+  }
+  __syncthreads();
+  if (threadIdx.x < 29) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kIcpThreads / 32; ++w) s += sh[w][threadIdx.x];
+    out = s;
+  }
+  return out;
+}
+
 __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a, double* partials) {
   __shared__ double sh[kIcpThreads / 32][29];
   __shared__ GnShared g;
@@ -303,69 +378,9 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
     unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (timed) t0 = gtimer();
     double* part = partials + (size_t)(it & 1) * kIcpMaxCtas * 29;
-    const Pose c2w = pose_from12(g.c2wF);
-    double acc[29];
-#pragma unroll
-    for (int k = 0; k < 29; ++k) acc[k] = 0.0;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-      const float d = __ldg(a.depth + p);
-      if (!(d > 0.f)) continue;
-      const int x = p % a.lw, y = p / a.lw;
-      const f3 pc = backproject(inl, (float)x, (float)y, d);
-      const f3 pw = pose_apply(c2w, pc);
-      const f3 q = pose_apply(rp, pw);
-      if (!(q.z > 0.f)) continue;
-      const float u = a.rfx * q.x / q.z + a.rcx;
-      const float v = a.rfy * q.y / q.z + a.rcy;
-      if (!(u >= 0.f && v >= 0.f && u <= (float)(a.rw - 1) && v <= (float)(a.rh - 1))) continue;
-      const int iu = (int)(u + 0.5f), iv = (int)(v + 0.5f);
-      const float4 V = __ldg(a.points + (size_t)iv * a.rw + iu);
-      const float4 N = __ldg(a.normals + (size_t)iv * a.rw + iu);
-      if (!(V.w > 0.f) || !(N.w > 0.f)) continue;
-      const f3 diff{pw.x - V.x, pw.y - V.y, pw.z - V.z};
-      if (sqnorm3(diff) > dist2) continue;
-      const f3 nn{N.x, N.y, N.z};
-      const float r = dot3(diff, nn);
-      const f3 pxn = cross3(pw, nn);
-      const double J[6] = {pxn.x, pxn.y, pxn.z, nn.x, nn.y, nn.z};
-      const double rd = r;
-      int k = 0;
-#pragma unroll
-      for (int i = 0; i < 6; ++i)
-#pragma unroll
-        for (int j = i; j < 6; ++j) acc[k++] += J[i] * J[j];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * rd;
-      acc[27] += rd * rd;
-      acc[28] += 1.0;
-    }
-    {
-      // multi-value warp reduction by recursive halving: at offset o every
-      // lane keeps one half of its live values and sends the other half to
-      // lane^o, so 32 (29 + 3 zero) sums take 16+8+4+2+1 = 31 shuffles
-      // instead of 29 x 5.  Lane l ends with sum number brev5(l).
-      double v[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = k < 29 ? acc[k] : 0.0;
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const bool hi = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-          const double send = hi ? v[i] : v[i + o];
-          const double keep = hi ? v[i + o] : v[i];
-          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      if (lane < 29) sh[wid][lane] = v[0];
-    }
-    __syncthreads();
-    if (threadIdx.x < 29) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kIcpThreads / 32; ++w) s += sh[w][threadIdx.x];
-      part[threadIdx.x * kIcpMaxCtas + blockIdx.x] = s;  // [sum][cta]: coalesced final sum
-    }
+    const double ps = icp_cta_partial(a, g, rp, inl, dist2, n, blockIdx.x * blockDim.x + threadIdx.x,
+                                      gridDim.x * blockDim.x, sh);
+    if (threadIdx.x < 29) part[threadIdx.x * kIcpMaxCtas + blockIdx.x] = ps;  // [sum][cta]: coalesced final sum
     if (timed) t1 = gtimer();
     grid.sync();
     if (timed) t2 = gtimer();
