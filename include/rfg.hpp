@@ -7,6 +7,12 @@
 //   rf::FusionEngine::allocate_from_depth /
 //                     integrate_frame         proj/include/rf/fusion.hpp:52-79
 //   rf::render_expected_ranges / render_maps  proj/include/rf/raycast.hpp:122-129
+//   rf::build_view + view elements            proj/include/rf/view.hpp:12-62
+//   rf::extract_mesh / Mesh                   proj/include/rf/meshing.hpp:12-23
+//   rf::read_pgm16 / read_ppm / write_*       proj/include/rf/image_io.hpp:10-17
+//   FusionEngine::Options, reserve/release    proj/include/rf/fusion.hpp:54-57,
+//                                             voxel_block_map.hpp:104-109
+//   SwappingEngine (the reference has only the hooks)
 //
 // Images are device pointers (the reference's View/RenderState hold host
 // Images; here the GPU owns them).  Errors follow the reference: an invalid
@@ -117,20 +123,34 @@ class VoxelBlockMap {
     return nb;
   }
   int allocatedBlockCount() const { return static_cast<int>(config_.blockCapacity) - freeBlockCount(); }
+  // voxel_block_map.cpp:107-123
+  bool reserveBlockForEntry(int entryIdx) {
+    const int rc = rfg_map_reserve_block(map_, entryIdx);
+    if (rc < 0) check(rc);
+    return rc == 1;
+  }
+  void releaseBlock(int entryIdx) { check(rfg_map_release_block(map_, entryIdx)); }
 
  private:
   VoxelBlockMapConfig config_;
   rfg_map* map_ = nullptr;
 };
 
+struct FusionOptions {  // FusionEngine::Options, fusion.hpp:54-57
+  bool swappingEnabled = false;
+  float swapMarginPx = 8.f;
+};
+
 class FusionEngine {
  public:
+  using Options = FusionOptions;
   AllocationStats allocate_from_depth(VoxelBlockMap& map, const float* depthDev, const Intrinsics& intr,
-                                      const Pose34& pose, const SceneParams& params) {
+                                      const Pose34& pose, const SceneParams& params, const Options& opts = Options()) {
     const rfg_intrinsics i = intr.c();
     const rfg_scene_params p = params.c();
+    const rfg_fusion_options o{opts.swappingEnabled ? 1 : 0, opts.swapMarginPx};
     rfg_alloc_stats s{};
-    check(rfg_allocate_from_depth(map.handle(), depthDev, &i, pose.data(), &p, &s));
+    check(rfg_allocate_from_depth_ex(map.handle(), depthDev, &i, pose.data(), &p, &o, &s));
     return {s.requested, s.allocated, s.allocFailures, s.visibleCount};
   }
   void integrate_frame(VoxelBlockMap& map, const float* depthDev, const Intrinsics& intr, const Pose34& pose,
@@ -153,14 +173,120 @@ inline void render_expected_ranges(const VoxelBlockMap& map, const Pose34& pose,
   check(rfg_render_expected_ranges(map.handle(), pose.data(), &i, &p, rangeDev));
 }
 
+// raycast.cpp:129-139; colourDev (RGB8 per pixel) is written in kColour /
+// kGrey mode and may be null in kIcpMaps mode.
 inline void render_maps(const VoxelBlockMap& map, const Pose34& pose, const Intrinsics& intr,
                         const SceneParams& params, RenderMode mode, const float* rangeDev, float* raycastDev,
-                        float* pointsDev, float* normalsDev) {
-  if (mode != RenderMode::kIcpMaps) throw Error(RFG_EINVAL, "only RenderMode::kIcpMaps runs on the B200 path");
+                        float* pointsDev, float* normalsDev, std::uint8_t* colourDev = nullptr) {
   const rfg_intrinsics i = intr.c();
   const rfg_scene_params p = params.c();
-  check(rfg_render_icp_maps(map.handle(), pose.data(), &i, &p, rangeDev, raycastDev, pointsDev, normalsDev));
+  check(rfg_render_maps(map.handle(), pose.data(), &i, &p, static_cast<int>(mode), rangeDev, raycastDev, pointsDev,
+                        normalsDev, colourDev));
 }
+
+// ------------------------------------------------------------ view
+struct ViewBuildOptions {  // view.hpp:12-15
+  bool bilateral = false;
+  int levels = 3;
+};
+
+// build_view (view.cpp:100-143) on device images: depthLevelsDev receives the
+// depth pyramid back to back; intensityLevelsDev (needs rgbDev) and
+// normalsDev (float4 per pixel) may be null; scratchDev (width*height floats)
+// is needed with bilateral.  rawBigEndian: raw is a PGM16 payload.
+inline void build_view(const std::uint16_t* rawDev, const std::uint8_t* rgbDev, const Intrinsics& intrD,
+                       float affScale, float affOffset, const ViewBuildOptions& opts, float* depthLevelsDev,
+                       float* intensityLevelsDev = nullptr, float* normalsDev = nullptr, float* scratchDev = nullptr,
+                       void* cudaStream = nullptr, bool rawBigEndian = false) {
+  const rfg_intrinsics i = intrD.c();
+  const int rc = rfg_build_view(rawDev, rgbDev, &i, affScale, affOffset, opts.bilateral ? 1 : 0, opts.levels,
+                                rawBigEndian ? 1 : 0, depthLevelsDev, intensityLevelsDev, normalsDev, scratchDev,
+                                cudaStream);
+  if (rc == RFG_EINVAL) throw std::invalid_argument(rfg_last_error());  // view.cpp:102-106
+  check(rc);
+}
+inline void bilateral_filter(const float* inDev, int w, int h, float spatialSigma, float rangeSigma, float* outDev,
+                             void* cudaStream = nullptr) {
+  check(rfg_bilateral_filter(inDev, w, h, spatialSigma, rangeSigma, outDev, cudaStream));
+}
+inline void compute_normals(const float* depthDev, const Intrinsics& intr, float* normalsDev,
+                            void* cudaStream = nullptr) {
+  const rfg_intrinsics i = intr.c();
+  check(rfg_compute_normals(depthDev, &i, normalsDev, cudaStream));
+}
+
+// ------------------------------------------------------------ mesh
+struct Mesh {  // meshing.hpp:12-15 (metres; normals toward positive sdf)
+  std::vector<std::array<float, 3>> vertices;
+  std::vector<std::array<std::uint32_t, 3>> triangles;
+};
+inline Mesh extract_mesh(const VoxelBlockMap& map, float voxelSize) {
+  std::int64_t nv = 0, nt = 0;
+  check(rfg_extract_mesh(map.handle(), voxelSize, &nv, &nt));
+  Mesh m;
+  m.vertices.resize(static_cast<std::size_t>(nv));
+  m.triangles.resize(static_cast<std::size_t>(nt));
+  check(rfg_mesh_copy(map.handle(), nv ? m.vertices[0].data() : nullptr, nt ? m.triangles[0].data() : nullptr));
+  return m;
+}
+
+// ------------------------------------------------------------ image IO
+template <class T>
+struct HostImage {
+  int width = 0, height = 0;
+  std::vector<T> data;  // row-major; 3 bytes per pixel for RGB8
+};
+inline HostImage<std::uint16_t> read_pgm16(const std::string& path) {
+  HostImage<std::uint16_t> img;
+  int rc = rfg_read_pgm16(path.c_str(), nullptr, 0, &img.width, &img.height);
+  if (rc == RFG_EINVAL) throw std::runtime_error(rfg_last_error());  // image_io.cpp messages
+  img.data.resize(static_cast<std::size_t>(img.width) * img.height);
+  check(rfg_read_pgm16(path.c_str(), img.data.data(), static_cast<int64_t>(img.data.size()), &img.width,
+                       &img.height));
+  return img;
+}
+inline HostImage<std::uint8_t> read_ppm(const std::string& path) {
+  HostImage<std::uint8_t> img;
+  int rc = rfg_read_ppm(path.c_str(), nullptr, 0, &img.width, &img.height);
+  if (rc == RFG_EINVAL) throw std::runtime_error(rfg_last_error());
+  img.data.resize(static_cast<std::size_t>(img.width) * img.height * 3);
+  check(rfg_read_ppm(path.c_str(), img.data.data(), static_cast<int64_t>(img.width) * img.height, &img.width,
+                     &img.height));
+  return img;
+}
+inline void write_pgm16(const HostImage<std::uint16_t>& img, const std::string& path) {
+  check(rfg_write_pgm16(path.c_str(), img.data.data(), img.width, img.height));
+}
+inline void write_ppm(const HostImage<std::uint8_t>& img, const std::string& path) {
+  check(rfg_write_ppm(path.c_str(), img.data.data(), img.width, img.height));
+}
+
+// ------------------------------------------------------------ swapping
+// SPEC.md:407-465 over the reference's hooks; per frame:
+// allocate_from_depth(..., Options{true}) -> swapIn() -> integrate_frame ->
+// render -> swapOut().
+class SwappingEngine {
+ public:
+  SwappingEngine(VoxelBlockMap& map, int capacityBlocks = 512) {
+    check(rfg_swap_create(map.handle(), capacityBlocks, &s_));
+  }
+  ~SwappingEngine() { rfg_swap_destroy(s_); }
+  SwappingEngine(const SwappingEngine&) = delete;
+  SwappingEngine& operator=(const SwappingEngine&) = delete;
+  int swapIn(int maxW = 100) {
+    int n = 0;
+    check(rfg_swap_in(s_, maxW, &n));
+    return n;
+  }
+  int swapOut() {
+    int n = 0;
+    check(rfg_swap_out(s_, &n));
+    return n;
+  }
+
+ private:
+  rfg_swap* s_ = nullptr;
+};
 
 // ITMMainEngine::ProcessFrame-style driver (absent in the reference).
 class Pipeline {
@@ -190,6 +316,10 @@ class Pipeline {
 
   void processHost(const std::uint16_t* rawHost, const Pose34* pose = nullptr) {
     check(rfg_pipeline_process_host(p_, rawHost, pose ? pose->data() : nullptr));
+  }
+  // one frame from a PGM16 file (image_io.cpp:96-113)
+  void processPgm(const std::string& path, const Pose34* pose = nullptr) {
+    check(rfg_pipeline_process_pgm(p_, path.c_str(), pose ? pose->data() : nullptr));
   }
   AllocationStats result(Pose34* poseOut = nullptr) {
     rfg_alloc_stats s{};

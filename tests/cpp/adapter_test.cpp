@@ -4,6 +4,7 @@
 // public pipeline and checks the reference's frame-0 statistics.
 #include <cstdio>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "rfg.hpp"
@@ -27,6 +28,24 @@ int main() {
   }
   CHECK(threw);
 
+  // image_io.cpp round trip + the reference's error messages (host only)
+  {
+    rfg::HostImage<std::uint16_t> img;
+    img.width = 37;
+    img.height = 23;
+    for (int i = 0; i < 37 * 23; ++i) img.data.push_back(static_cast<std::uint16_t>(i * 977));
+    rfg::write_pgm16(img, "/tmp/rfg_adapter_test.pgm");
+    const auto back = rfg::read_pgm16("/tmp/rfg_adapter_test.pgm");
+    CHECK(back.width == 37 && back.height == 23 && back.data == img.data);
+    bool missing = false;
+    try {
+      (void)rfg::read_pgm16("/tmp/rfg_adapter_test_missing.pgm");
+    } catch (const std::runtime_error& e) {
+      missing = std::string(e.what()).find("cannot open") != std::string::npos;
+    }
+    CHECK(missing);
+  }
+
   try {
     rfg::VoxelBlockMap map({0x40000, 0x20000, 0x40000});
     const rfg::Intrinsics intr{640, 480, 525.f, 525.f, 319.5f, 239.5f};
@@ -42,6 +61,18 @@ int main() {
     // the reference's frame-0 statistics on C1 (tests/golden/c1_frames.json)
     CHECK(st.requested == 8349 && st.allocated == 8349 && st.allocFailures == 0 && st.visibleCount == 8349);
     CHECK(map.allocatedBlockCount() == 8349);
+    // marching cubes on the fused map (meshing.cpp:144-217)
+    const rfg::Mesh mesh = rfg::extract_mesh(map, params.voxelSize);
+    CHECK(mesh.triangles.size() > 10000 && mesh.vertices.size() > 5000);
+    for (const auto& t : mesh.triangles) CHECK(t[0] < mesh.vertices.size() && t[2] < mesh.vertices.size());
+    // releaseBlock / reserveBlockForEntry (voxel_block_map.cpp:107-123)
+    const auto ents = map.entries();
+    int idx = -1;
+    for (int i = 0; i < static_cast<int>(ents.size()) && idx < 0; ++i)
+      if (ents[i].inMemory()) idx = i;
+    map.releaseBlock(idx);
+    CHECK(map.entries()[idx].ptr == -1 && map.allocatedBlockCount() == 8348);
+    CHECK(map.reserveBlockForEntry(idx) && map.entries()[idx].inMemory());
     std::printf("adapter_test: GPU sequence ok\n");
   } catch (const rfg::Error& e) {
     CHECK(e.code() == RFG_ECUDA);  // no device: fail loudly, no CPU fallback
