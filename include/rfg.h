@@ -285,6 +285,11 @@ int rfg_pipeline_destroy(rfg_pipeline* p);
  * pose.  Asynchronous. */
 int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const float* pose34);
 /* Enqueue one frame from HOST raw depth (copied H2D inside the call). */
+/* As rfg_pipeline_process_raw for a frame produced on another CUDA stream:
+ * the pipeline reads it after the producer stream's pending work, and the
+ * producer stream's later work waits until the frame has been copied. */
+int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw_dev, const float pose34[12],
+                                    void* producer_cuda_stream);
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* raw_host, const float* pose34);
 /* Read back the last frame's stats and pose (synchronises). */
 /* One frame straight from a PGM16 file (image_io.cpp:96-113): the payload is

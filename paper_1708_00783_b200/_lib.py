@@ -117,6 +117,7 @@ SIGNATURES = {
     "rfg_pipeline_destroy": ([_vp], C.c_int),
     "rfg_pipeline_process_raw": ([_vp, _vp, _f], C.c_int),
     "rfg_pipeline_process_host": ([_vp, _vp, _f], C.c_int),
+    "rfg_pipeline_process_raw_stream": ([_vp, _vp, _f, _vp], C.c_int),
     "rfg_pipeline_process_pgm": ([_vp, C.c_char_p, _f], C.c_int),
     "rfg_pipeline_result": ([_vp, C.POINTER(AllocStats_), _f, _d], C.c_int),
     "rfg_pipeline_buffers": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),

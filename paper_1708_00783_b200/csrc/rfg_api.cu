@@ -634,6 +634,8 @@ struct rfg_pipeline {
   float* viewScratch;  // unfiltered depth when cfg.bilateral
   void* pgmStage;      // pinned staging for rfg_pipeline_process_pgm
   cudaEvent_t stageFree;  // the last upload out of pgmStage has been read
+  cudaEvent_t rawReady;   // producer stream -> pipeline stream (process_raw_stream)
+  cudaEvent_t rawRead;    // pipeline stream has copied the caller's frame
   int frames;
   cudaGraphExec_t exec[2];  // [0] no tracking, [1] tracking
   uint64_t graphKernels[2];
@@ -749,6 +751,8 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
   for (int k = 0; k < 7; ++k)
     if (cudaEventCreate(&p->ev[k]) != cudaSuccess) ok = false;
   if (cudaEventCreateWithFlags(&p->stageFree, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  if (cudaEventCreateWithFlags(&p->rawReady, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  if (cudaEventCreateWithFlags(&p->rawRead, cudaEventDisableTiming) != cudaSuccess) ok = false;
   if (!ok) {
     cudaGetLastError();
     rfg_pipeline_destroy(p);
@@ -780,6 +784,8 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   for (int k = 0; k < 7; ++k)
     if (p->ev[k]) cudaEventDestroy(p->ev[k]);
   if (p->stageFree) cudaEventDestroy(p->stageFree);
+  if (p->rawReady) cudaEventDestroy(p->rawReady);
+  if (p->rawRead) cudaEventDestroy(p->rawRead);
   if (p->hostIcp) cudaFreeHost(p->hostIcp);
   if (p->hostPose) cudaFreeHost(p->hostPose);
   if (p->pgmStage) cudaFreeHost(p->pgmStage);
@@ -806,6 +812,20 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw, const float* 
   RFG_REQUIRE(p && raw, "null argument");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
   if (raw != p->rawDev) RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
+  return run_frame(p, pose34);
+}
+
+int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const float* pose34, void* producer) {
+  RFG_REQUIRE(p && raw, "null argument");
+  cudaStream_t ps = static_cast<cudaStream_t>(producer);
+  const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
+  // the frame is read after the producer's pending work (its upload) ...
+  RFG_CK(cudaEventRecord(p->rawReady, ps));
+  RFG_CK(cudaStreamWaitEvent(p->stream, p->rawReady, 0));
+  if (raw != p->rawDev) RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
+  // ... and the producer's later work (e.g. reusing the buffer) waits for the copy
+  RFG_CK(cudaEventRecord(p->rawRead, p->stream));
+  RFG_CK(cudaStreamWaitEvent(ps, p->rawRead, 0));
   return run_frame(p, pose34);
 }
 

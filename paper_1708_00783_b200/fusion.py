@@ -781,10 +781,13 @@ class Pipeline:
             pass
 
     def process(self, raw, pose=None):
-        """raw: CUDA uint16/int16 tensor (device path) or numpy uint16 (host path)."""
+        """raw: CUDA uint16/int16 tensor (device path) or numpy uint16 (host path).
+        A device frame is ordered after the work queued on torch's current
+        stream (e.g. the upload that produced it) and kept alive until the
+        pipeline's stream has read it."""
         p = _fp(_pose(pose)) if pose is not None else None
         if torch.is_tensor(raw) and raw.is_cuda:
-            check(lib().rfg_pipeline_process_raw(self._h, _ptr(raw), p))
+            check(lib().rfg_pipeline_process_raw_stream(self._h, _ptr(raw), p, _stream_handle()))
         else:
             a = np.ascontiguousarray(raw, np.uint16) if not torch.is_tensor(raw) else raw.numpy()
             check(lib().rfg_pipeline_process_host(self._h, a.ctypes.data_as(C.c_void_p), p))
