@@ -134,13 +134,23 @@ def main():
         rm[mode.name] = {"us": round(dev_time(lambda: F.render_maps(m, pose, INTR, params, mode, st)), 2)}
     out["rows"]["f4_render_modes_640x480"] = rm
     F.render_maps(m, pose, INTR, params, F.RenderMode.kIcpMaps, st)
-    ap = {"full_raycast_us": rm["kIcpMaps"]["us"]}
+    ap = {}
+
+    # frame 40 rendered from scratch vs approximately (ranges at the new pose
+    # first in both, as the reference orders it)
+    def full():
+        F.render_expected_ranges(m, poses[40], INTR, params, st)
+        F.render_maps(m, poses[40], INTR, params, F.RenderMode.kIcpMaps, st)
+    ap["full_ranges+raycast_us"] = round(dev_time(full), 2)
+    F.render_maps(m, pose, INTR, params, F.RenderMode.kIcpMaps, st)  # frame-39 maps
 
     def approx():
+        F.render_expected_ranges(m, poses[40], INTR, params, st)
         miss = F.forward_project(st, poses[40], INTR, params.voxelSize, m)
         F.render_maps(m, poses[40], INTR, params, F.RenderMode.kIcpMaps, st, missingOnly=miss)
         return miss
-    ap["forward_project+missing_raycast_us"] = round(dev_time(approx), 2)
+    ap["ranges+forward_project+missing_raycast_us"] = round(dev_time(approx), 2)
+    F.render_maps(m, pose, INTR, params, F.RenderMode.kIcpMaps, st)
     ap["missing_pixels"] = len(approx())
     out["rows"]["f1_approximate_raycast_640x480"] = ap
 
