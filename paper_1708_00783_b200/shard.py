@@ -94,6 +94,12 @@ class ShardedPipeline:
         self.state = F.RenderState()
 
     def process(self, raw, pose=None):
+        # a device frame is read on this pipeline's stream: order it after its
+        # producer and keep it alive until read (torch pool streams are never
+        # destroyed, so record_stream is safe here)
+        self._stream.wait_stream(torch.cuda.current_stream())
+        if torch.is_tensor(raw) and raw.is_cuda:
+            raw.record_stream(self._stream)
         with torch.cuda.stream(self._stream):
             if pose is not None:
                 self.pose = np.asarray(pose, np.float32).reshape(3, 4).copy()
