@@ -263,8 +263,9 @@ def run_b200(args):
     total = args.warmup + args.steps
     order = [i % N_FRAMES for i in range(total)]
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler = ClockSampler(local, period_ms=max(args.clock_ms, 1))
+    if args.clock_ms > 0:
+        sampler.start()
     launches0 = None
     if world > 1:
         dist.barrier()
@@ -279,8 +280,9 @@ def run_b200(args):
             sampler.mark()
             launches0 = launch_count()
         flush.fill_(i & 0xFF)  # evict L2 (untimed; outside the event pair)
+        # the frame starts after the flush has finished (ordered on the device)
+        stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(stream):
-            stream.wait_stream(torch.cuda.current_stream())
             if i >= args.warmup:
                 evs[i - args.warmup][0].record(stream)
             pipe.process(raw_dev[f], poses[0] if f == 0 else None)
@@ -325,12 +327,13 @@ def run_b200(args):
                "d2h_bytes_per_step": 64 + 48 + 64, "frames": n_e2e - warm,
                "path": "Pipeline.process(host raw u16) + Pipeline.result() per frame (rfg_pipeline_process_host/result)"}
 
-    # ---- per-stage device times (non-graph profile pass, same frames) ----
+    # ---- per-stage device times: the same frames replayed through the same
+    # frame graph with event-record nodes between the stages ----
     prof = None
     roof = None
     if world == 1 and args.profile_frames > 0:
         ppipe = F.Pipeline(m, intr, params, F.DepthAffine(*AFF), levels=3, track=True, iters=ICP_ITERS,
-                           dist=ICP_DIST, use_graph=False, profile=True)
+                           dist=ICP_DIST, use_graph=True, profile=True)
         torch.cuda.synchronize()
         m.clear()
         ppipe.reset()
@@ -404,8 +407,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=100)
-    ap.add_argument("--profile-frames", type=int, default=30)
+    ap.add_argument("--profile-frames", type=int, default=95)
     ap.add_argument("--cpu-frames", type=int, default=5)
+    ap.add_argument("--clock-ms", type=int, default=5, help="nvidia-smi clock sampling period (0 = off)")
     ap.add_argument("--ref-budget", type=float, default=150.0, help="reference arm time budget (s)")
     args = ap.parse_args()
     if args.warmup < 3:

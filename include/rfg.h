@@ -273,7 +273,7 @@ typedef struct {
   float dist[3];
   int32_t min_count;
   int32_t use_graph;       /* capture the frame into a CUDA graph */
-  int32_t profile;         /* record CUDA events between stages (non-graph mode only) */
+  int32_t profile;         /* record CUDA events between stages (graph mode: event-record nodes) */
   int32_t bilateral;       /* ViewBuildOptions::bilateral (view.hpp:13) */
   int32_t raw_big_endian;  /* raw frames are PGM16 payloads (decoded in the view stage) */
 } rfg_pipeline_config;

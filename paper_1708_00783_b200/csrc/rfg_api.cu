@@ -649,9 +649,12 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   rfg_map* m = p->map;
   const rfg_pipeline_config& c = p->cfg;
   cudaStream_t s = p->stream;
-  const bool prof = c.profile && !c.use_graph;
+  // profile mode: events between the stages; under capture they become
+  // event-record nodes of the frame graph, so the stage times are those of
+  // the graph replay itself
+  const bool prof = c.profile != 0;
   auto mark = [&](int k) {
-    if (prof) cudaEventRecord(p->ev[k], s);
+    if (prof) cudaEventRecordWithFlags(p->ev[k], s, c.use_graph ? cudaEventRecordExternal : cudaEventRecordDefault);
   };
   mark(0);
   const Intr inV{c.intr.width, c.intr.height, c.intr.fx, c.intr.fy, c.intr.cx, c.intr.cy};
@@ -871,7 +874,7 @@ int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34
 
 int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]) {
   RFG_REQUIRE(p && ms7, "null argument");
-  RFG_REQUIRE(p->cfg.profile && !p->cfg.use_graph, "stage times need profile = 1 and use_graph = 0");
+  RFG_REQUIRE(p->cfg.profile, "stage times need profile = 1");
   RFG_CK(cudaEventSynchronize(p->ev[6]));
   for (int k = 0; k < 6; ++k) RFG_CK(cudaEventElapsedTime(&ms7[k], p->ev[k], p->ev[k + 1]));
   RFG_CK(cudaEventElapsedTime(&ms7[6], p->ev[0], p->ev[6]));
