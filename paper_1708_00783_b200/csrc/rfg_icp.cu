@@ -17,9 +17,10 @@
 //             the same Cholesky solve and SE(3) update, so all CTAs hold the
 //             identical new estimate without a second grid barrier; CTA 0
 //             publishes it (pose, stats, done flag) to global memory.
-// A frame's tracker is therefore 1 + levels + 1 launches with one grid
-// barrier per iteration, nothing is enqueued for iterations that are not
-// needed, and the whole tracker is capturable in the frame's CUDA graph.  The
+// A frame's whole tracker is ONE cooperative launch (k_icp_track: seed,
+// levels coarse to fine, output pose) with one grid barrier per iteration;
+// nothing is enqueued for iterations that are not needed, and the launch is
+// capturable in the frame's CUDA graph.  The
 // grid size is fixed per level, so the reduction order — and the result — is
 // run-to-run deterministic.
 #include <cooperative_groups.h>
@@ -44,7 +45,8 @@ struct IcpState {
   int done[4];          // per-level stop flags
   int pad[4];
   // phase timers of CTA 0 (ns, %globaltimer), accumulated over iterations:
-  // {associate+reduce, grid barrier, final sum, solve, iterations, -, -, -}
+  // {associate+reduce, grid barrier, final sum, solve, iterations,
+  //  level-0 total, level-1 total, level-2 total}
   unsigned long long timers[8];
 };
 
@@ -91,21 +93,6 @@ __device__ __forceinline__ void matmul3d(const double* A, const double* B, doubl
 
 __device__ void c2w_to_float(const double* c, float* f) {
   for (int i = 0; i < 12; ++i) f[i] = (float)c[i];
-}
-
-__global__ void k_icp_init(IcpState* st, const float* w2c, const float* renderPose) {
-  if (threadIdx.x != 0) return;
-  // inverse of the float pose, widened to double (the oracle does the same)
-  const Pose q = pose_inverse(pose_from12(w2c));
-  for (int r = 0; r < 3; ++r) {
-    for (int c = 0; c < 3; ++c) st->c2w[r * 4 + c] = (double)q.R[r * 3 + c];
-    st->c2w[r * 4 + 3] = (double)q.t[r];
-  }
-  c2w_to_float(st->c2w, st->c2wF);
-  for (int i = 0; i < 12; ++i) st->renderPose[i] = renderPose[i];
-  for (int i = 0; i < 4; ++i) st->done[i] = 0;
-  for (int i = 0; i < 8; ++i) st->stats[i] = 0.0;
-  st->stats[7] = 1.0;
 }
 
 // Load an explicit float camera->world pose (single evaluations).
@@ -229,16 +216,22 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
   }
   const double* w = delta;
   const double* v = delta + 3;
-  const double theta = sqrt(w[0] * w[0] + (w[1] * w[1] + w[2] * w[2]));
+  const double th2 = w[0] * w[0] + (w[1] * w[1] + w[2] * w[2]);
   const double W[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
   double WW[9];
   matmul3d(W, W, WW);
   double ca, cb, cc;
-  if (theta < 1e-8) {
-    ca = 1.0;
-    cb = 0.5;
-    cc = 1.0 / 6.0;
+  if (th2 < 0.0625 * 0.0625) {
+    // sin(t)/t, (1 - cos t)/t^2, (t - sin t)/t^3 by their Taylor series
+    // (nested to t^10; the truncation error is below 1e-19 for t < 1/16):
+    // no sincos, no divisions on the solver's serial path, and no
+    // cancellation in 1 - cos t and t - sin t at small angles
+    const double t2 = th2;
+    ca = 1.0 - t2 * (1.0 / 6.0) * (1.0 - t2 * (1.0 / 20.0) * (1.0 - t2 * (1.0 / 42.0) * (1.0 - t2 * (1.0 / 72.0) * (1.0 - t2 * (1.0 / 110.0)))));
+    cb = 0.5 * (1.0 - t2 * (1.0 / 12.0) * (1.0 - t2 * (1.0 / 30.0) * (1.0 - t2 * (1.0 / 56.0) * (1.0 - t2 * (1.0 / 90.0) * (1.0 - t2 * (1.0 / 132.0))))));
+    cc = (1.0 / 6.0) * (1.0 - t2 * (1.0 / 20.0) * (1.0 - t2 * (1.0 / 42.0) * (1.0 - t2 * (1.0 / 72.0) * (1.0 - t2 * (1.0 / 110.0) * (1.0 - t2 * (1.0 / 156.0))))));
   } else {
+    const double theta = sqrt(th2);
     double s, co;
     sincos(theta, &s, &co);
     ca = s / theta;
@@ -283,46 +276,114 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
 // is associated and accumulated in double (J J^T, J r, r^2, count), reduced
 // per warp by recursive halving and over the CTA's warps; on return thread k
 // < 29 of the CTA holds sum k of its pixels (returned), the others 0.
+// Pixels per thread whose camera-space point is kept in shared memory for
+// the whole level (computed at the level's first iteration; the depth and the
+// backprojection do not depend on the pose).  Level 0 at 640x480 on 148 CTAs
+// is 4.05 pixels per thread; pixels beyond the cached slots take the
+// uncached path.  Projection + gathers are issued kIcpGroup pixels at a
+// time so their loads are in flight together; pixels are accumulated in
+// the same order as a plain loop, so the sums do not depend on kIcpGroup.
+constexpr int kIcpPxCache = 4;
+constexpr int kIcpGroup = 2;
+
+// J J^T, J r, r^2, count of one associated pixel (the oracle's per-pixel
+// body, rfo_icp_track).
+__device__ __forceinline__ void icp_accumulate(double* acc, f3 pw, float4 V, float4 N, float dist2) {
+  if (!(V.w > 0.f) || !(N.w > 0.f)) return;
+  const f3 diff{pw.x - V.x, pw.y - V.y, pw.z - V.z};
+  if (sqnorm3(diff) > dist2) return;
+  const f3 nn{N.x, N.y, N.z};
+  const float r = dot3(diff, nn);
+  const f3 pxn = cross3(pw, nn);
+  const double J[6] = {pxn.x, pxn.y, pxn.z, nn.x, nn.y, nn.z};
+  const double rd = r;
+  int k = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = i; j < 6; ++j) acc[k++] += J[i] * J[j];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * rd;
+  acc[27] += rd * rd;
+  acc[28] += 1.0;
+}
+
+// nearest-pixel association in the last render: pixel index or -1
+__device__ __forceinline__ int icp_associate(const IcpLevelArgs& a, const Pose& rp, f3 pw) {
+  const f3 q = pose_apply(rp, pw);
+  if (!(q.z > 0.f)) return -1;
+  const float u = a.rfx * q.x / q.z + a.rcx;
+  const float v = a.rfy * q.y / q.z + a.rcy;
+  if (!(u >= 0.f && v >= 0.f && u <= (float)(a.rw - 1) && v <= (float)(a.rh - 1))) return -1;
+  const int iu = (int)(u + 0.5f), iv = (int)(v + 0.5f);
+  return iv * a.rw + iu;
+}
+
+// One evaluation's per-CTA partial: every valid level pixel p (grid stride)
+// is associated and accumulated in double (J J^T, J r, r^2, count), reduced
+// per warp by recursive halving and over the CTA's warps; on return thread k
+// < 29 of the CTA holds sum k of its pixels (returned), the others 0.
 __device__ __forceinline__ double icp_cta_partial(const IcpLevelArgs& a, const GnShared& g, const Pose& rp,
                                                   const Intr& inl, float dist2, int n, int p0, int pstride,
-                                                  double (*sh)[29]) {
+                                                  double (*sh)[29], float4* pcs, bool fill) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double out = 0.0;
   const Pose c2w = pose_from12(g.c2wF);
   double acc[29];
 #pragma unroll
   for (int k = 0; k < 29; ++k) acc[k] = 0.0;
-  for (int p = p0; p < n; p += pstride) {
+  if (fill) {
+#pragma unroll
+    for (int k = 0; k < kIcpPxCache; ++k) {
+      const int p = p0 + k * pstride;
+      float4 c = make_float4(0.f, 0.f, 0.f, -1.f);
+      if (p < n) {
+        const float d = __ldg(a.depth + p);
+        if (d > 0.f) {
+          const int x = p % a.lw, y = p / a.lw;
+          const f3 pc = backproject(inl, (float)x, (float)y, d);
+          c = make_float4(pc.x, pc.y, pc.z, 1.f);
+        }
+      }
+      pcs[k * kIcpThreads + threadIdx.x] = c;  // each thread reads back only its own slots
+    }
+  }
+#pragma unroll
+  for (int kb = 0; kb < kIcpPxCache; kb += kIcpGroup) {
+    f3 pw[kIcpGroup];
+    int pix[kIcpGroup];
+#pragma unroll
+    for (int j = 0; j < kIcpGroup; ++j) {
+      const float4 c = pcs[(kb + j) * kIcpThreads + threadIdx.x];
+      pix[j] = -1;
+      pw[j] = f3{0.f, 0.f, 0.f};
+      if (c.w > 0.f) {
+        pw[j] = pose_apply(c2w, f3{c.x, c.y, c.z});
+        pix[j] = icp_associate(a, rp, pw[j]);
+      }
+    }
+    float4 V[kIcpGroup], N[kIcpGroup];
+#pragma unroll
+    for (int j = 0; j < kIcpGroup; ++j) {
+      if (pix[j] >= 0) {
+        V[j] = __ldg(a.points + pix[j]);
+        N[j] = __ldg(a.normals + pix[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kIcpGroup; ++j)
+      if (pix[j] >= 0) icp_accumulate(acc, pw[j], V[j], N[j], dist2);
+  }
+  // pixels beyond the cached slots
+  for (int p = p0 + kIcpPxCache * pstride; p < n; p += pstride) {
     const float d = __ldg(a.depth + p);
     if (!(d > 0.f)) continue;
     const int x = p % a.lw, y = p / a.lw;
     const f3 pc = backproject(inl, (float)x, (float)y, d);
     const f3 pw = pose_apply(c2w, pc);
-    const f3 q = pose_apply(rp, pw);
-    if (!(q.z > 0.f)) continue;
-    const float u = a.rfx * q.x / q.z + a.rcx;
-    const float v = a.rfy * q.y / q.z + a.rcy;
-    if (!(u >= 0.f && v >= 0.f && u <= (float)(a.rw - 1) && v <= (float)(a.rh - 1))) continue;
-    const int iu = (int)(u + 0.5f), iv = (int)(v + 0.5f);
-    const float4 V = __ldg(a.points + (size_t)iv * a.rw + iu);
-    const float4 N = __ldg(a.normals + (size_t)iv * a.rw + iu);
-    if (!(V.w > 0.f) || !(N.w > 0.f)) continue;
-    const f3 diff{pw.x - V.x, pw.y - V.y, pw.z - V.z};
-    if (sqnorm3(diff) > dist2) continue;
-    const f3 nn{N.x, N.y, N.z};
-    const float r = dot3(diff, nn);
-    const f3 pxn = cross3(pw, nn);
-    const double J[6] = {pxn.x, pxn.y, pxn.z, nn.x, nn.y, nn.z};
-    const double rd = r;
-    int k = 0;
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int j = i; j < 6; ++j) acc[k++] += J[i] * J[j];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * rd;
-    acc[27] += rd * rd;
-    acc[28] += 1.0;
+    const int pix = icp_associate(a, rp, pw);
+    if (pix < 0) continue;
+    icp_accumulate(acc, pw, __ldg(a.points + pix), __ldg(a.normals + pix), dist2);
   }
   {
     // multi-value warp reduction by recursive halving: at offset o every
@@ -354,51 +415,48 @@ __device__ __forceinline__ double icp_cta_partial(const IcpLevelArgs& a, const G
   return out;
 }
 
-__global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a, double* partials) {
-  __shared__ double sh[kIcpThreads / 32][29];
-  __shared__ GnShared g;
+// One level's Gauss-Newton loop on the CTA-local state g.  CTAs with
+// blockIdx.x < nCta own the level's pixels (grid stride nCta x kIcpThreads);
+// the others only join the barriers, sum the same partials and run the same
+// solve.  `gi` counts iterations across levels so the partial buffers
+// alternate without a second barrier.
+__device__ __forceinline__ void icp_run_level(const IcpLevelArgs& a, double* partials, int nCta, GnShared& g,
+                                              double (*sh)[29], float4* pcs, int& gi, unsigned long long* tacc) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 12; ++i) {
-      g.c2w[i] = __ldcg(&st->c2w[i]);
-      g.c2wF[i] = __ldcg(&st->c2wF[i]);
-      g.rp[i] = __ldcg(&st->renderPose[i]);
-    }
-    for (int i = 0; i < 8; ++i) g.stats[i] = __ldcg(&st->stats[i]);
-    g.done = __ldcg(&st->done[a.level]);
-  }
-  __syncthreads();
   const Intr inl{a.lw, a.lh, a.fx, a.fy, a.cx, a.cy};
   const float dist2 = a.dist * a.dist;
   const int n = a.lw * a.lh;
   const Pose rp = pose_from12(g.rp);
   const bool timed = blockIdx.x == 0 && threadIdx.x == 0;
+  const bool owner = (int)blockIdx.x < nCta;
   cg::grid_group grid = cg::this_grid();
-  for (int it = 0; it < a.iters && !g.done; ++it) {
+  for (int it = 0; it < a.iters && !g.done; ++it, ++gi) {
     unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (timed) t0 = gtimer();
-    double* part = partials + (size_t)(it & 1) * kIcpMaxCtas * 29;
-    const double ps = icp_cta_partial(a, g, rp, inl, dist2, n, blockIdx.x * blockDim.x + threadIdx.x,
-                                      gridDim.x * blockDim.x, sh);
-    if (threadIdx.x < 29) part[threadIdx.x * kIcpMaxCtas + blockIdx.x] = ps;  // [sum][cta]: coalesced final sum
+    double* part = partials + (size_t)(gi & 1) * kIcpMaxCtas * 29;
+    if (owner) {
+      const double ps = icp_cta_partial(a, g, rp, inl, dist2, n, blockIdx.x * blockDim.x + threadIdx.x,
+                                        nCta * blockDim.x, sh, pcs, it == 0);
+      if (threadIdx.x < 29) part[threadIdx.x * kIcpMaxCtas + blockIdx.x] = ps;  // [sum][cta]: coalesced final sum
+    }
     if (timed) t1 = gtimer();
     grid.sync();
     if (timed) t2 = gtimer();
-    // every CTA: fixed-order final sum (warp w owns sums w, w+16; lanes
-    // stride the CTAs; shuffle tree) and the identical solve
+    // every CTA: fixed-order final sum over the owners (warp w owns sums w,
+    // w+16; lanes stride the CTAs; shuffle tree) and the identical solve
     for (int k = wid; k < 29; k += kIcpThreads / 32) {
       // issue all of this lane's loads before the dependent adds
       double v[kIcpMaxCtas / 32];
 #pragma unroll
       for (int j = 0; j < kIcpMaxCtas / 32; ++j) {
         const int c = lane + 32 * j;
-        v[j] = c < (int)gridDim.x ? __ldcg(part + k * kIcpMaxCtas + c) : 0.0;
+        v[j] = c < nCta ? __ldcg(part + k * kIcpMaxCtas + c) : 0.0;
       }
-      double s = 0.0;
+      double sum = 0.0;
 #pragma unroll
-      for (int j = 0; j < kIcpMaxCtas / 32; ++j) s += v[j];
-      s = warp_sum(s);
-      if (lane == 0) g.sums[k] = s;
+      for (int j = 0; j < kIcpMaxCtas / 32; ++j) sum += v[j];
+      sum = warp_sum(sum);
+      if (lane == 0) g.sums[k] = sum;
     }
     __syncthreads();
     if (timed) t3 = gtimer();
@@ -409,40 +467,116 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLeve
         gn_step(g, a.level, a.minCount);
     }
     __syncthreads();
-    if (timed) {
+    if (timed) {  // in registers; flushed once at the end of the kernel
       const unsigned long long t4 = gtimer();
-      st->timers[0] += t1 - t0;
-      st->timers[1] += t2 - t1;
-      st->timers[2] += t3 - t2;
-      st->timers[3] += t4 - t3;
-      st->timers[4] += 1;
+      tacc[0] += t1 - t0;
+      tacc[1] += t2 - t1;
+      tacc[2] += t3 - t2;
+      tacc[3] += t4 - t3;
+      tacc[4] += 1;
+      if (a.level < 3) tacc[5 + a.level] += t4 - t0;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+}
+
+__device__ __forceinline__ void icp_publish(IcpState* st, const GnShared& g, const unsigned long long* tacc) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st->timers[i] += tacc[i];
+  for (int i = 0; i < 12; ++i) {
+    st->c2w[i] = g.c2w[i];
+    st->c2wF[i] = g.c2wF[i];
+  }
+  for (int k = 0; k < 29; ++k) st->sums[k] = g.sums[k];
+  for (int i = 0; i < 8; ++i) st->stats[i] = g.stats[i];
+}
+
+// Single evaluation / single level on the state in `st` (rfg_icp_reduce).
+__global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a, double* partials) {
+  __shared__ double sh[kIcpThreads / 32][29];
+  __shared__ GnShared g;
+  __shared__ float4 pcs[kIcpPxCache * kIcpThreads];
+  if (threadIdx.x == 0) {
     for (int i = 0; i < 12; ++i) {
-      st->c2w[i] = g.c2w[i];
-      st->c2wF[i] = g.c2wF[i];
+      g.c2w[i] = __ldcg(&st->c2w[i]);
+      g.c2wF[i] = __ldcg(&st->c2wF[i]);
+      g.rp[i] = __ldcg(&st->renderPose[i]);
     }
-    for (int k = 0; k < 29; ++k) st->sums[k] = g.sums[k];
-    for (int i = 0; i < 8; ++i) st->stats[i] = g.stats[i];
+    for (int i = 0; i < 8; ++i) g.stats[i] = __ldcg(&st->stats[i]);
+    g.done = __ldcg(&st->done[a.level]);
+  }
+  __syncthreads();
+  int gi = 0;
+  unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  icp_run_level(a, partials, gridDim.x, g, sh, pcs, gi, tacc);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    icp_publish(st, g, tacc);
     st->done[a.level] = g.done;
   }
 }
 
-// world->camera output pose = inverse(c2w) cast to float.
-__global__ void k_icp_final(IcpState* st, float* w2cOut) {
-  if (threadIdx.x != 0) return;
-  double R[9], t[3];
-  for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) R[r * 3 + c] = st->c2w[c * 4 + r];
-  for (int r = 0; r < 3; ++r)
-    t[r] = -(R[r * 3] * st->c2w[3] + (R[r * 3 + 1] * st->c2w[7] + R[r * 3 + 2] * st->c2w[11]));
-  for (int r = 0; r < 3; ++r) {
-    for (int c = 0; c < 3; ++c) st->w2cF[r * 4 + c] = (float)R[r * 3 + c];
-    st->w2cF[r * 4 + 3] = (float)t[r];
+// The whole coarse-to-fine track of a frame in ONE cooperative launch
+// (k_icp_init + a launch per level + k_icp_final before): every CTA seeds
+// its state from the device-resident pose, runs the levels coarse to fine
+// with the same per-level pixel partition as a per-level launch (so the sums
+// and the pose are identical), and CTA 0 publishes the result.
+struct IcpTrackArgs {
+  IcpLevelArgs lv[3];
+  int nCta[3];
+  int levels;
+  const float* w2cInit;
+  const float* renderPose;
+  float* w2cOut;
+};
+
+__global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrackArgs ta, double* partials) {
+  __shared__ double sh[kIcpThreads / 32][29];
+  __shared__ GnShared g;
+  __shared__ float4 pcs[kIcpPxCache * kIcpThreads];
+#ifdef RFG_ICP_PHASES
+  const unsigned long long tEntry = gtimer();
+#endif
+  if (threadIdx.x == 0) {
+    // k_icp_init: inverse of the float pose, widened to double (as the oracle)
+    const Pose q = pose_inverse(pose_from12(ta.w2cInit));
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) g.c2w[r * 4 + c] = (double)q.R[r * 3 + c];
+      g.c2w[r * 4 + 3] = (double)q.t[r];
+    }
+    c2w_to_float(g.c2w, g.c2wF);
+    for (int i = 0; i < 12; ++i) g.rp[i] = ta.renderPose[i];
+    for (int i = 0; i < 8; ++i) g.stats[i] = 0.0;
+    g.stats[7] = 1.0;
+    for (int k = 0; k < 29; ++k) g.sums[k] = 0.0;
   }
-  if (w2cOut)
-    for (int i = 0; i < 12; ++i) w2cOut[i] = st->w2cF[i];
+  __syncthreads();
+  int gi = 0;
+  unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int l = ta.levels - 1; l >= 0; --l) {
+    if (ta.lv[l].iters <= 0) continue;
+    if (threadIdx.x == 0) g.done = 0;
+    __syncthreads();
+    icp_run_level(ta.lv[l], partials, ta.nCta[l], g, sh, pcs, gi, tacc);
+  }
+#ifdef RFG_ICP_PHASES
+  // kernel entry -> exit of CTA 0 (replaces the per-level slots)
+  tacc[5] = gtimer() - tEntry;
+  tacc[6] = tacc[7] = 0;
+#endif
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    icp_publish(st, g, tacc);
+    for (int i = 0; i < 12; ++i) st->renderPose[i] = g.rp[i];
+    // k_icp_final: world->camera output = inverse(c2w) cast to float
+    double R[9], t[3];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) R[r * 3 + c] = g.c2w[c * 4 + r];
+    for (int r = 0; r < 3; ++r) t[r] = -(R[r * 3] * g.c2w[3] + (R[r * 3 + 1] * g.c2w[7] + R[r * 3 + 2] * g.c2w[11]));
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) st->w2cF[r * 4 + c] = (float)R[r * 3 + c];
+      st->w2cF[r * 4 + 3] = (float)t[r];
+    }
+    if (ta.w2cOut)
+      for (int i = 0; i < 12; ++i) ta.w2cOut[i] = st->w2cF[i];
+  }
 }
 
 // CTAs for a level of n pixels: about one pixel per thread, at most one CTA
@@ -454,7 +588,9 @@ static int icp_grid(int n) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, k_icp_level, kIcpThreads, 0);
-    if (perSm < 1) sms = -1;
+    int perSmTrack = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSmTrack, k_icp_track, kIcpThreads, 0);
+    if (perSm < 1 || perSmTrack < 1) sms = -1;
   }
   if (sms <= 0) return 0;
   const int want = (n + kIcpThreads - 1) / kIcpThreads;
@@ -507,21 +643,27 @@ cudaError_t launch_icp_track(void* state, double* partials, const float* depthLe
                              int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
                              cudaStream_t s) {
   IcpState* st = static_cast<IcpState*>(state);
-  k_icp_init<<<1, 32, 0, s>>>(st, w2cInit, renderPose);
-  count_launch();
-  for (int l = levels - 1; l >= 0; --l) {
-    IcpLevelArgs a = level_args(depthLevels, l, in0, points, normals);
-    a.dist = dist[l];
-    a.iters = iters[l];
-    a.minCount = minCount;
-    a.evalOnly = 0;
-    if (a.iters <= 0) continue;
-    const cudaError_t e = launch_level(st, a, partials, s);
-    if (e != cudaSuccess) return e;
+  IcpTrackArgs ta{};
+  ta.levels = levels;
+  ta.w2cInit = w2cInit;
+  ta.renderPose = renderPose;
+  ta.w2cOut = w2cOut;
+  int grid = 1;
+  for (int l = 0; l < levels; ++l) {
+    ta.lv[l] = level_args(depthLevels, l, in0, points, normals);
+    ta.lv[l].dist = dist[l];
+    ta.lv[l].iters = iters[l];
+    ta.lv[l].minCount = minCount;
+    ta.lv[l].evalOnly = 0;
+    ta.nCta[l] = icp_grid(ta.lv[l].lw * ta.lv[l].lh);
+    if (ta.nCta[l] <= 0) return cudaErrorCooperativeLaunchTooLarge;
+    if (iters[l] > 0 && ta.nCta[l] > grid) grid = ta.nCta[l];
   }
-  k_icp_final<<<1, 32, 0, s>>>(st, w2cOut);
+  IcpState* stp = st;
+  double* pp = partials;
+  void* args[] = {&stp, &ta, &pp};
   count_launch();
-  return cudaGetLastError();
+  return cudaLaunchCooperativeKernel((const void*)k_icp_track, dim3(grid), dim3(kIcpThreads), args, 0, s);
 }
 
 cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* depth, int lw, int lh, const float* f4l,

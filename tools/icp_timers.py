@@ -31,3 +31,5 @@ names = ["associate+block reduce", "grid barrier", "final sum", "solve"]
 print(f"iterations {it} over 90 frames ({it / 90:.1f}/frame)")
 for k, nm in enumerate(names):
     print(f"  {nm:24s} {t[k] / it / 1e3:7.2f} us/iteration   {t[k] / 90 / 1e3:7.1f} us/frame")
+for lv in range(3):
+    print(f"  level {lv} iterations total   {t[5 + lv] / 90 / 1e3:7.1f} us/frame")
