@@ -8,7 +8,8 @@
 //   resolves intra-frame collisions "last writer wins" in (row-major pixel,
 //   DDA ordinal) order (fusion.cpp:168-176); here every request is keyed
 //   (pixel << 6 | ordinal) + 1 and an atomicMax per slot keeps the serial
-//   winner, aggregated per warp with __match_any_sync first.
+//   winner; visits are first merged per distinct block inside the CTA, so
+//   each chain is probed once per block and CTA.
 // Stage 2 (k_req_count / k_scan_tiles / k_req_assign): requests are served in
 //   ascending entry-index order, exactly as the serial scan (fusion.cpp:190-201):
 //   a request succeeds iff it is a bucket request or among the first
@@ -24,51 +25,62 @@
 
 namespace rfg {
 
-__device__ __forceinline__ Pose load_pose(const FrameArgs& fa) {
-  return pose_from12(fa.poseDev ? fa.poseDev : fa.pose);
+// Amanatides-Woo traversal (fusion.cpp:72-114).  visit(cell, ordinal) is
+// called for each visited cell in order; returning false stops the walk.
+// Per-axis DDA setup (fusion.cpp:87-100).
+__device__ __forceinline__ void dda_axis(float d, int c, float a, int& step, float& tMax, float& tDelta) {
+  if (d > 0.f) {
+    step = 1;
+    tMax = ((float)(c + 1) - a) / d;
+    tDelta = 1.f / d;
+  } else if (d < 0.f) {
+    step = -1;
+    tMax = ((float)c - a) / d;
+    tDelta = -1.f / d;
+  } else {
+    step = 0;
+    tMax = FLT_MAX;
+    tDelta = FLT_MAX;
+  }
 }
 
 // Amanatides-Woo traversal (fusion.cpp:72-114).  visit(cell, ordinal) is
 // called for each visited cell in order; returning false stops the walk.
+// Scalar per-axis state (no indexed arrays, so nothing lives in local memory).
 template <class F>
 __device__ __forceinline__ void traverse_blocks(f3 a, f3 b, F&& visit) {
-  int c[3] = {(int)floorf(a.x), (int)floorf(a.y), (int)floorf(a.z)};
-  const int e[3] = {(int)floorf(b.x), (int)floorf(b.y), (int)floorf(b.z)};
+  int cx = (int)floorf(a.x), cy = (int)floorf(a.y), cz = (int)floorf(a.z);
+  const int ex = (int)floorf(b.x), ey = (int)floorf(b.y), ez = (int)floorf(b.z);
   int ord = 0;
-  if (!visit(i3{c[0], c[1], c[2]}, ord++)) return;
-  if (c[0] == e[0] && c[1] == e[1] && c[2] == e[2]) return;
-  const float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
-  const float av[3] = {a.x, a.y, a.z};
-  int step[3];
-  float tMax[3], tDelta[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (d[k] > 0.f) {
-      step[k] = 1;
-      tMax[k] = ((float)(c[k] + 1) - av[k]) / d[k];
-      tDelta[k] = 1.f / d[k];
-    } else if (d[k] < 0.f) {
-      step[k] = -1;
-      tMax[k] = ((float)c[k] - av[k]) / d[k];
-      tDelta[k] = -1.f / d[k];
-    } else {
-      step[k] = 0;
-      tMax[k] = FLT_MAX;
-      tDelta[k] = FLT_MAX;
-    }
-  }
-  const int maxSteps = abs(e[0] - c[0]) + abs(e[1] - c[1]) + abs(e[2] - c[2]) + 8;
+  if (!visit(i3{cx, cy, cz}, ord++)) return;
+  if (cx == ex && cy == ey && cz == ez) return;
+  int sx, sy, sz;
+  float tmx, tmy, tmz, tdx, tdy, tdz;
+  dda_axis(b.x - a.x, cx, a.x, sx, tmx, tdx);
+  dda_axis(b.y - a.y, cy, a.y, sy, tmy, tdy);
+  dda_axis(b.z - a.z, cz, a.z, sz, tmz, tdz);
+  const int maxSteps = abs(ex - cx) + abs(ey - cy) + abs(ez - cz) + 8;
   for (int i = 0; i < maxSteps; ++i) {
-    int axis = 0;
-    if (tMax[1] < tMax[0]) axis = 1;
-    if (tMax[2] < tMax[axis]) axis = 2;
-    if (tMax[axis] > 1.f) break;
-    c[axis] += step[axis];
-    tMax[axis] += tDelta[axis];
-    if (!visit(i3{c[0], c[1], c[2]}, ord++)) return;
-    if (c[0] == e[0] && c[1] == e[1] && c[2] == e[2]) break;
+    // axis of the smallest tMax, ties to the lower axis (strict <, fusion.cpp:103-105)
+    const bool yFirst = tmy < tmx;
+    const float tm = yFirst ? tmy : tmx;
+    if (tmz < tm) {
+      if (tmz > 1.f) break;
+      cz += sz;
+      tmz += tdz;
+    } else if (yFirst) {
+      if (tmy > 1.f) break;
+      cy += sy;
+      tmy += tdy;
+    } else {
+      if (tmx > 1.f) break;
+      cx += sx;
+      tmx += tdx;
+    }
+    if (!visit(i3{cx, cy, cz}, ord++)) return;
+    if (cx == ex && cy == ey && cz == ez) break;
   }
-  if (!(c[0] == e[0] && c[1] == e[1] && c[2] == e[2])) visit(i3{e[0], e[1], e[2]}, ord++);
+  if (!(cx == ex && cy == ey && cz == ez)) visit(i3{ex, ey, ez}, ord++);
 }
 
 // Segment of pixel (x, y) in block units (fusion.cpp:183-186).
@@ -102,47 +114,88 @@ __device__ __forceinline__ bool shard_keeps(const DevMap& m, i3 b) {
 }
 
 // ------------------------------------------------------------- stage 1
+// markBlock (fusion.cpp:155-177) for one block and the largest request key
+// any of its visits carries: mark it if the chain holds it, otherwise
+// request it at the bucket / chain tail (serial last writer = max key).
+__device__ __forceinline__ void mark_or_request(const DevMap& m, i3 cell, uint32_t key) {
+  int idx = (int)hash_index(cell.x, cell.y, cell.z, m.buckets - 1);
+  int4 e = ld_entry(m.entries, idx);
+  if (entry_allocated(e)) {
+    const int xy = pack_xy(cell);
+    for (;;) {
+      if (e.x == xy && e.y == cell.z) {
+        const uint8_t v = e.w >= 0 ? 1 : 2;
+        if (m.marked[idx] != v) m.marked[idx] = v;
+        return;
+      }
+      if (e.z < 1) break;
+      idx = (int)m.buckets + e.z - 1;
+      e = ld_entry(m.entries, idx);
+    }
+  }
+  if (m.reqKey[idx] < key) atomicMax(&m.reqKey[idx], key);
+}
+
+// The pixels of a CTA (a 32x8 tile) stab a handful of distinct blocks many
+// times over (a 4 cm block covers ~15x15 pixels at 1.4 m).  Marks are
+// idempotent and a request slot keeps only the maximum key, so the visits
+// are first merged per distinct block in a shared-memory table (block ->
+// max key over the CTA's visits), and the hash chain is probed once per
+// distinct block instead of once per visit.  A visit that finds the table
+// full takes the direct path; the outcome is the same either way.
+constexpr int kCellSlots = 512;  // power of two; ~20-60 distinct blocks per CTA at C1
+
 __global__ void __launch_bounds__(256) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
+  __shared__ unsigned long long sCell[kCellSlots];  // (x | y << 16 | z << 32 | 1 << 48), 0 = empty
+  __shared__ uint32_t sKey[kCellSlots];
+  for (int i = threadIdx.x; i < kCellSlots; i += blockDim.x) {
+    sCell[i] = 0ull;
+    sKey[i] = 0u;
+  }
+  __syncthreads();
   const int x = blockIdx.x * 32 + (threadIdx.x & 31);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
   const bool inside = x < fa.w && y < fa.h;
-  const Pose camToWorld = pose_inverse(load_pose(fa));
+  const Pose camToWorld = pose_inverse(frame_pose(fa));
   f3 a, b;
   const bool active = inside && pixel_segment(depth, fa, camToWorld, x, y, &a, &b);
-  if (!active) return;
-  const uint32_t pixKey = (uint32_t)(y * fa.w + x) << 6;
-  const uint32_t mask = m.buckets - 1;
-  traverse_blocks(a, b, [&](i3 cell, int ord) -> bool {
-    if (ord >= 64) {
-      atomicOr(&m.state->error, 1 << 1);  // ordinal bound (RFG_ERANGE)
-      return false;
-    }
-    if (!shard_keeps(m, cell)) return true;
-    if (!in_i16(cell)) {
-      atomicOr(&m.state->error, 1 << 0);  // coordinate outside the int16 entry layout
-      return true;
-    }
-    // markBlock (fusion.cpp:155-177)
-    int idx = (int)hash_index(cell.x, cell.y, cell.z, mask);
-    int4 e = ld_entry(m.entries, idx);
-    if (entry_allocated(e)) {
-      const int xy = pack_xy(cell);
-      for (;;) {
-        if (e.x == xy && e.y == cell.z) {
-          const uint8_t v = e.w >= 0 ? 1 : 2;
-          if (m.marked[idx] != v) m.marked[idx] = v;
+  if (active) {
+    const uint32_t pixKey = (uint32_t)(y * fa.w + x) << 6;
+    traverse_blocks(a, b, [&](i3 cell, int ord) -> bool {
+      if (ord >= 64) {
+        atomicOr(&m.state->error, 1 << 1);  // ordinal bound (RFG_ERANGE)
+        return false;
+      }
+      if (!shard_keeps(m, cell)) return true;
+      if (!in_i16(cell)) {
+        atomicOr(&m.state->error, 1 << 0);  // coordinate outside the int16 entry layout
+        return true;
+      }
+      const uint32_t key = (pixKey | (uint32_t)ord) + 1u;
+      const unsigned long long packed = (unsigned long long)(uint16_t)cell.x |
+                                        ((unsigned long long)(uint16_t)cell.y << 16) |
+                                        ((unsigned long long)(uint16_t)cell.z << 32) | (1ull << 48);
+      int h = (int)(hash_index(cell.x, cell.y, cell.z, kCellSlots - 1));
+#pragma unroll 1
+      for (int probe = 0; probe < 32; ++probe) {
+        const unsigned long long old = atomicCAS(&sCell[h], 0ull, packed);
+        if (old == 0ull || old == packed) {
+          atomicMax(&sKey[h], key);
           return true;
         }
-        if (e.z < 1) break;
-        idx = (int)m.buckets + e.z - 1;
-        e = ld_entry(m.entries, idx);
+        h = (h + 1) & (kCellSlots - 1);
       }
-    }
-    // request at bucket (type 1) or chain tail (type 2); serial last writer wins
-    const uint32_t key = (pixKey | (uint32_t)ord) + 1u;
-    if (m.reqKey[idx] < key) atomicMax(&m.reqKey[idx], key);
-    return true;
-  });
+      mark_or_request(m, cell, key);  // table full: direct path
+      return true;
+    });
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCellSlots; i += blockDim.x) {
+    const unsigned long long c = sCell[i];
+    if (!c) continue;
+    const i3 cell{(int)(int16_t)(c & 0xFFFFu), (int)(int16_t)((c >> 16) & 0xFFFFu), (int)(int16_t)((c >> 32) & 0xFFFFu)};
+    mark_or_request(m, cell, sKey[i]);
+  }
 }
 
 // Recompute the block a request key refers to (pixel, DDA ordinal).
@@ -278,7 +331,7 @@ __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const flo
   const int2 tp = m.tilePrefix[blockIdx.x];
   int before = tp.x + ex.x, before2 = tp.y + ex.y;
   const int nB = m.state->snapFreeBlocks, nE = m.state->snapFreeExcess;
-  const Pose camToWorld = pose_inverse(load_pose(fa));
+  const Pose camToWorld = pose_inverse(frame_pose(fa));
   int succ = 0, succ2 = 0;
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
@@ -369,7 +422,7 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
   }
   if (mk) *mp = 0u;
   __syncthreads();
-  const Pose pose = load_pose(fa);
+  const Pose pose = frame_pose(fa);
   int n = 0;
   for (int i = threadIdx.x; i < nq; i += kTileThreads) {
     const int idx = queue[i];

@@ -19,10 +19,6 @@ struct ColourArgs {
   float extr[12];      // extrinsics_d_to_rgb
 };
 
-__device__ __forceinline__ Pose load_pose_i(const FrameArgs& fa) {
-  return pose_from12(fa.poseDev ? fa.poseDev : fa.pose);
-}
-
 // update_voxel_colour (fusion.cpp:38-70)
 __device__ __forceinline__ void update_colour(uint32_t& word, f3 pt, const Pose& M, const ColourArgs& ca, int maxW) {
   const f3 pc = pose_apply(M, pt);
@@ -77,7 +73,7 @@ __global__ void __launch_bounds__(256, 2) k_integrate(DevMap m, const float* __r
   const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
   const int nw = gridDim.x * warpsPerCta;
   const int nVis = *((volatile int*)&m.state->nVisible);
-  const Pose pose = load_pose_i(fa);
+  const Pose pose = frame_pose(fa);
   Pose Mrgb;
   if (kColour) Mrgb = pose_compose(pose_from12(ca.extr), pose);
   const float wLim = (float)(fa.w - 2), hLim = (float)(fa.h - 2);
@@ -229,7 +225,7 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
   const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
   const int nw = gridDim.x * warpsPerCta;
   const int nVis = *((volatile int*)&m.state->nVisible);
-  const Pose pose = load_pose_i(fa);
+  const Pose pose = frame_pose(fa);
   const float wLim = (float)(fa.w - 2), hLim = (float)(fa.h - 2);
   const float mu = fa.mu, vs = fa.voxelSize;
   const bool muOk = mu >= 0x1p-20f && mu <= 0x1p20f;

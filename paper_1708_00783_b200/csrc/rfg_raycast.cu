@@ -6,10 +6,6 @@
 
 namespace rfg {
 
-__device__ __forceinline__ Pose load_pose_r(const FrameArgs& fa) {
-  return pose_from12(fa.poseDev ? fa.poseDev : fa.pose);
-}
-
 // ------------------------------------------------------ expected ranges
 // The reference covers each visible block's projected pixel rectangle with
 // 16x16 fragments (count -> prefix sum -> emit, raycast.cpp:94-115) and
@@ -37,7 +33,7 @@ __global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa) {
   const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
   const int nw = gridDim.x * warpsPerCta;
   const int nVis = *((volatile int*)&m.state->nVisible);
-  const Pose pose = load_pose_r(fa);
+  const Pose pose = frame_pose(fa);
   const float bs = fa.voxelSize * (float)kBlock;
   for (int b = gw; b < nVis; b += nw) {
     const int idx = m.visibleList[b];
@@ -363,7 +359,7 @@ __device__ __forceinline__ void raycast_pixel(const DevMap& m, const FrameArgs& 
   float4 rc = invalid, pt = invalid;
   const float2 r = range[i];
   if (r.y >= r.x) {
-    const Pose c2w = pose_inverse(load_pose_r(fa));
+    const Pose c2w = pose_inverse(frame_pose(fa));
     const f3 origin{c2w.t[0], c2w.t[1], c2w.t[2]};
     const f3 dirCam{((float)x - fa.cx) / fa.fx, ((float)y - fa.cy) / fa.fy, 1.f};
     const float norm = sqrtf(sqnorm3(dirCam));
@@ -486,7 +482,7 @@ __global__ void __launch_bounds__(128) k_render_colour(DevMap m, FrameArgs fa, i
       const float4 n = normals[i];
       if (n.w > 0.f) {
         const int x = i % fa.w, y = i / fa.w;
-        const Pose c2w = pose_inverse(load_pose_r(fa));
+        const Pose c2w = pose_inverse(frame_pose(fa));
         const f3 dirCam{((float)x - fa.cx) / fa.fx, ((float)y - fa.cy) / fa.fy, 1.f};
         const float norm = sqrtf(sqnorm3(dirCam));
         const f3 dw = rot_apply(c2w.R, dirCam);
