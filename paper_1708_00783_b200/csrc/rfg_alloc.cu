@@ -143,9 +143,13 @@ __device__ __forceinline__ void mark_or_request(const DevMap& m, i3 cell, uint32
 // max key over the CTA's visits), and the hash chain is probed once per
 // distinct block instead of once per visit.  A visit that finds the table
 // full takes the direct path; the outcome is the same either way.
-constexpr int kCellSlots = 512;  // power of two; ~20-60 distinct blocks per CTA at C1
+constexpr int kCellSlots = 1024;  // power of two; ~30-90 distinct blocks per CTA at C1
+// A CTA covers a 32 x kStage1Rows pixel tile (8 rows per pass): 640x480 is
+// 600 CTAs, one wave at 5 CTAs per SM (740 slots), instead of 1.35 waves
+// of 32x8 tiles.
+constexpr int kStage1Rows = 16;
 
-__global__ void __launch_bounds__(256) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
+__global__ void __launch_bounds__(256, 5) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
   __shared__ unsigned long long sCell[kCellSlots];  // (x | y << 16 | z << 32 | 1 << 48), 0 = empty
   __shared__ uint32_t sKey[kCellSlots];
   for (int i = threadIdx.x; i < kCellSlots; i += blockDim.x) {
@@ -153,41 +157,50 @@ __global__ void __launch_bounds__(256) k_alloc_stage1(DevMap m, const float* __r
     sKey[i] = 0u;
   }
   __syncthreads();
-  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
-  const bool inside = x < fa.w && y < fa.h;
   const Pose camToWorld = pose_inverse(frame_pose(fa));
-  f3 a, b;
-  const bool active = inside && pixel_segment(depth, fa, camToWorld, x, y, &a, &b);
-  if (active) {
-    const uint32_t pixKey = (uint32_t)(y * fa.w + x) << 6;
-    traverse_blocks(a, b, [&](i3 cell, int ord) -> bool {
-      if (ord >= 64) {
-        atomicOr(&m.state->error, 1 << 1);  // ordinal bound (RFG_ERANGE)
-        return false;
-      }
-      if (!shard_keeps(m, cell)) return true;
-      if (!in_i16(cell)) {
-        atomicOr(&m.state->error, 1 << 0);  // coordinate outside the int16 entry layout
-        return true;
-      }
-      const uint32_t key = (pixKey | (uint32_t)ord) + 1u;
-      const unsigned long long packed = (unsigned long long)(uint16_t)cell.x |
-                                        ((unsigned long long)(uint16_t)cell.y << 16) |
-                                        ((unsigned long long)(uint16_t)cell.z << 32) | (1ull << 48);
-      int h = (int)(hash_index(cell.x, cell.y, cell.z, kCellSlots - 1));
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
 #pragma unroll 1
-      for (int probe = 0; probe < 32; ++probe) {
-        const unsigned long long old = atomicCAS(&sCell[h], 0ull, packed);
-        if (old == 0ull || old == packed) {
-          atomicMax(&sKey[h], key);
+  for (int row = 0; row < kStage1Rows; row += 8) {
+    const int y = blockIdx.y * kStage1Rows + row + (threadIdx.x >> 5);
+    const bool inside = x < fa.w && y < fa.h;
+    f3 a, b;
+    const bool active = inside && pixel_segment(depth, fa, camToWorld, x, y, &a, &b);
+    if (active) {
+      const uint32_t pixKey = (uint32_t)(y * fa.w + x) << 6;
+      traverse_blocks(a, b, [&](i3 cell, int ord) -> bool {
+        if (ord >= 64) {
+          atomicOr(&m.state->error, 1 << 1);  // ordinal bound (RFG_ERANGE)
+          return false;
+        }
+        if (!shard_keeps(m, cell)) return true;
+        if (!in_i16(cell)) {
+          atomicOr(&m.state->error, 1 << 0);  // coordinate outside the int16 entry layout
           return true;
         }
-        h = (h + 1) & (kCellSlots - 1);
-      }
-      mark_or_request(m, cell, key);  // table full: direct path
-      return true;
-    });
+        const uint32_t key = (pixKey | (uint32_t)ord) + 1u;
+        const unsigned long long packed = (unsigned long long)(uint16_t)cell.x |
+                                          ((unsigned long long)(uint16_t)cell.y << 16) |
+                                          ((unsigned long long)(uint16_t)cell.z << 32) | (1ull << 48);
+        int h = (int)(hash_index(cell.x, cell.y, cell.z, kCellSlots - 1));
+  #pragma unroll 1
+        for (int probe = 0; probe < 32; ++probe) {
+          const unsigned long long old = atomicCAS(&sCell[h], 0ull, packed);
+          if (old == 0ull) {
+            // first visit of this block in the CTA: start pulling its bucket
+            // entry into L2 now, so the probe after the DDA phase hits it
+            const int4* bucket = m.entries + hash_index(cell.x, cell.y, cell.z, m.buckets - 1);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(bucket));
+          }
+          if (old == 0ull || old == packed) {
+            atomicMax(&sKey[h], key);
+            return true;
+          }
+          h = (h + 1) & (kCellSlots - 1);
+        }
+        mark_or_request(m, cell, key);  // table full: direct path
+        return true;
+      });
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kCellSlots; i += blockDim.x) {
@@ -461,7 +474,7 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
 }
 
 cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s) {
-  dim3 g1((fa.w + 31) / 32, (fa.h + 7) / 8);
+  dim3 g1((fa.w + 31) / 32, (fa.h + kStage1Rows - 1) / kStage1Rows);
   k_alloc_stage1<<<g1, 256, 0, s>>>(m, depth, fa);
   k_req_count<<<m.nTiles, kTileThreads, 0, s>>>(m);
   k_scan_tiles<<<1, 1024, 0, s>>>(m.tileCounts, m.tilePrefix, m.nTiles, m.state, 0);

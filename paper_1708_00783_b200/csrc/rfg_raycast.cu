@@ -130,10 +130,12 @@ __global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m,
   if (threadIdx.x == 0) m.binCount[t] = 0;  // ready for the next frame
 }
 
+#if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
+__device__ unsigned long long g_rc_stats[32];
+#endif
 #ifdef RFG_RC_STATS
 // debug build only: march statistics {rays, steps, coarse, invalid-fine,
 // nearest-valid, trilinear, lookups, -, hist[log2 steps] x 16, max steps}
-__device__ unsigned long long g_rc_stats[32];
 #define RC_STAT(i, v) atomicAdd(&g_rc_stats[i], (unsigned long long)(v))
 #else
 #define RC_STAT(i, v)
@@ -244,7 +246,12 @@ struct FieldReader {
 
 __device__ __forceinline__ f3 at_t(f3 o, f3 d, float t) { return f3{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z}; }
 
-// cast_ray_field (raycast.hpp:54-112)
+// cast_ray_field (raycast.hpp:54-112).  Each fine/surface step first does
+// its reads (the nearest voxel, then the trilinear value where the nearest
+// one is valid and <= 0.1) and only then branches on the outcome, so the
+// lanes of a warp that took different branches in the previous step still
+// issue the reads together (18.7 instead of 15.6 active lanes per warp and
+// 9 % fewer instructions than branching on the invalid read first).
 __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM, float tMaxM, float mu, float vs,
                          f3* hit) {
   const float coarseStep = (float)kBlock * vs;
@@ -267,13 +274,14 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
   } fin{nSteps, nCoarse, nInv, nNear};
 #endif
   while (t <= tMaxM) {
-    const f3 p = at_t(oV, dV, t);
 #ifdef RFG_RC_STATS
     ++nSteps;
-    if (state == COARSE) ++nCoarse;
 #endif
     if (state == COARSE) {
-      if (field.resident(p)) {
+#ifdef RFG_RC_STATS
+      ++nCoarse;
+#endif
+      if (field.resident(at_t(oV, dV, t))) {
         state = FINE;
         t = smax(tMinM, t - coarseStep);
       } else {
@@ -281,8 +289,15 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
       }
       continue;
     }
+    // reads
     bool ok = false;
-    float sdf = field.nearest(p, ok);
+    float sdf = field.nearest(at_t(oV, dV, t), ok);
+    if (ok && sdf <= 0.1f) {
+      bool okTri = false;
+      const float tri = field.trilinear(at_t(oV, dV, t), okTri);
+      if (okTri) sdf = tri;
+    }
+    // the reference's state machine on them
     if (!ok) {
 #ifdef RFG_RC_STATS
       ++nInv;
@@ -294,11 +309,6 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
 #ifdef RFG_RC_STATS
     ++nNear;
 #endif
-    if (sdf <= 0.1f) {
-      bool okTri = false;
-      const float tri = field.trilinear(p, okTri);
-      if (okTri) sdf = tri;
-    }
     if (state == FINE) {
       if (sdf < 0.f) return false;  // WRONG_SIDE
       state = SURFACE;
@@ -402,8 +412,29 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_icp(DevMap m, Fram
                                                      float4* raycast, float4* points) {
   const int x = blockIdx.x * 16 + (threadIdx.x & 15);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
-  if (x >= fa.w || y >= fa.h) return;
-  raycast_pixel(m, fa, range, x, y, raycast, points);
+#if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (threadIdx.x == 0) atomicMin(&g_rc_stats[24], t0);
+#endif
+  if (x < fa.w && y < fa.h) raycast_pixel(m, fa, range, x, y, raycast, points);
+#if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  unsigned long long dur = t1 - t0, end = t1, sum = t1 - t0;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    dur = max(dur, __shfl_xor_sync(0xffffffffu, dur, o));
+    end = max(end, __shfl_xor_sync(0xffffffffu, end, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&g_rc_stats[7], dur);  // longest thread (ray) duration, ns
+    atomicMax(&g_rc_stats[25], end);
+    atomicAdd(&g_rc_stats[26], sum);
+    atomicAdd(&g_rc_stats[27], 32ull);
+  }
+#endif
 }
 
 // Normals at every hit, in their own kernel: the six trilinear reads are
@@ -741,12 +772,13 @@ extern "C" int rfg_compose_select(const int64_t* keymin, int rank, int n, float*
   return RFG_OK;
 }
 
-#ifdef RFG_RC_STATS
+#if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
 extern "C" int rfg_debug_rc_stats(unsigned long long* out32, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out32, rfg::g_rc_stats, sizeof(rfg::g_rc_stats));
   if (reset) {
     unsigned long long z[32] = {};
+    z[24] = ~0ull;  // min start time
     cudaMemcpyToSymbol(rfg::g_rc_stats, z, sizeof(z));
   }
   return 0;

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Ray-march statistics of the C2 frames (needs a RFG_RC_STATS build:
+"""Ray-march statistics of the C2 frames (needs a RFG_RC_STATS or RFG_RC_TIMING build:
 RFG_LIB_PATH=.variants/stats/librfg.so)."""
 import ctypes as C
 import os
@@ -18,15 +18,23 @@ m = F.VoxelBlockMap(F.VoxelBlockMapConfig(0x40000, 0x20000, 0x40000))
 p = F.Pipeline(m, intr, F.SceneParams(), use_graph=False, profile=True)
 L = _lib.lib()
 buf = (C.c_ulonglong * 32)()
+acc = np.zeros(32, np.float64)
+timing = []
 for f in range(40):
     raw = torch.from_numpy(F.synth_render(0, poses[f], intr)[0].view(np.int16)).cuda()
-    if f == 30:
-        L.rfg_debug_rc_stats(buf, 1)
+    torch.cuda.synchronize()
+    L.rfg_debug_rc_stats(buf, 1)
     p.process(raw, poses[0] if f == 0 else None)
-torch.cuda.synchronize()
-L.rfg_debug_rc_stats(buf, 0)
-s = list(buf)
+    torch.cuda.synchronize()
+    L.rfg_debug_rc_stats(buf, 0)
+    if f >= 30:
+        acc += np.array(list(buf), np.float64)
+        timing.append((buf[7] / 1e3, (buf[25] - buf[24]) / 1e3, buf[26] / max(buf[27], 1) / 1e3))
+s = acc
 nf = 10
+tm = np.array(timing)
+print(f"k_raycast_icp per frame: span {tm[:, 1].mean():.1f} us, longest ray {tm[:, 0].mean():.1f} us "
+      f"(max {tm[:, 0].max():.1f}), mean ray {tm[:, 2].mean():.2f} us")
 print(f"per frame: rays {s[0]/nf:.0f} steps {s[1]/nf:.0f} coarse {s[2]/nf:.0f} invalid-fine {s[3]/nf:.0f} "
-      f"nearest {s[4]/nf:.0f} trilinear {s[5]/nf:.0f} lookups {s[6]/nf:.0f}  max steps {s[31]}")
-print("steps/ray histogram (log2 buckets):", {f"<{2**b}": s[8 + b] // nf for b in range(16) if s[8 + b]})
+      f"nearest {s[4]/nf:.0f} trilinear {s[5]/nf:.0f} lookups {s[6]/nf:.0f}  max steps (last frame) {buf[31]}")
+print("steps/ray histogram (log2 buckets):", {f"<{2**b}": int(s[8 + b] // nf) for b in range(16) if s[8 + b]})
