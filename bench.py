@@ -210,6 +210,31 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------------ B200
+def cupti_kernel_ms(pipe, raw_dev, poses, flush, warmup, n, name):
+    """Mean device duration (ms) of kernel `name` over frames warmup..warmup+n-1
+    replayed through the pipeline's frame graph (torch.profiler / CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    stream = torch.cuda.ExternalStream(pipe.stream)
+    torch.cuda.synchronize()
+    pipe.map.clear()
+    pipe.reset()
+    for f in range(warmup):
+        pipe.process(raw_dev[f], poses[0] if f == 0 else None)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for f in range(warmup, min(N_FRAMES, warmup + n)):
+            flush.fill_(f & 0xFF)
+            stream.wait_stream(torch.cuda.current_stream())
+            pipe.process(raw_dev[f])
+            torch.cuda.current_stream().wait_stream(stream)
+        torch.cuda.synchronize()
+    d = [e.time_range.end - e.time_range.start for e in prof.events()
+         if e.device_type == torch.autograd.DeviceType.CUDA and name in e.name]
+    return float(np.mean(d)) / 1e3 if d else None
+
+
 def make_frames():
     from paper_1708_00783_b200 import fusion as F
     intr = F.Intrinsics(**INTR)
@@ -366,6 +391,18 @@ def run_b200(args):
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_kind, "algorithmic_bytes_per_launch": int_bytes,
                 "mean_visible_blocks": mean_vis, "launch_ms": prof["integrate"]}
+        # cross-check: the kernel's own device duration (CUPTI activity records,
+        # as ncu's gpu__time_duration) in the plain frame graph, same frames;
+        # the event pair above also holds the event-record nodes' latency
+        try:
+            kms = cupti_kernel_ms(pipe, raw_dev, poses, flush, args.warmup, args.profile_frames, "k_integrate_depth")
+            if kms:
+                roof["kernel_ms_cupti"] = kms
+                roof["achieved_cupti"] = int_bytes / (kms * 1e-3) / 1e9
+                roof["frac_cupti"] = roof["achieved_cupti"] / peak
+        except Exception as e:  # informational only
+            roof["kernel_ms_cupti"] = None
+            roof["cupti_error"] = str(e)[:200]
         del ppipe
 
     if rank != 0:

@@ -218,6 +218,134 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
   return vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
 }
 
+// One visible block of the depth-only kernel (one warp, 16 voxels per lane).
+// kWindowKnown: the block-level test below has proven that every voxel's
+// projection quotients are inside div_fast's exactness window, so only the
+// eta quotient keeps a per-voxel window test.
+template <bool kWindowKnown>
+__device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int ox, int oy, int oz, const Pose& pose,
+                                                      const FrameArgs& fa, const float* __restrict__ depth, float wLim,
+                                                      float hLim, float mu, bool muOk, float rMu, bool capW, int maxW) {
+  const float vs = fa.voxelSize;
+#pragma unroll
+  for (int g = 0; g < 4; g += kQG) {
+    uint32_t wd[4 * kQG];
+#pragma unroll
+    for (int q = g; q < g + kQG; ++q) {
+      const uint4 r = blk[q * 32 + lane];
+      wd[(q - g) * 4 + 0] = r.x;
+      wd[(q - g) * 4 + 1] = r.y;
+      wd[(q - g) * 4 + 2] = r.z;
+      wd[(q - g) * 4 + 3] = r.w;
+    }
+    // ---- project
+    float zc[4 * kQG];
+    int pix[4 * kQG];
+    unsigned slow = 0u;
+#pragma unroll
+    for (int q = g; q < g + kQG; ++q) {
+      const int lin = (q * 32 + lane) * 4;
+      const float pz = (float)(oz + (lin >> 6)) * vs;
+      const float py = (float)(oy + ((lin >> 3) & 7)) * vs;
+      const float r0 = pose.R[1] * py + pose.R[2] * pz;
+      const float r1 = pose.R[4] * py + pose.R[5] * pz;
+      const float r2 = pose.R[7] * py + pose.R[8] * pz;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = (q - g) * 4 + i;
+        const float px = (float)(ox + (lin & 7) + i) * vs;
+        const float cxw = (pose.R[0] * px + r0) + pose.t[0];
+        const float cyw = (pose.R[3] * px + r1) + pose.t[1];
+        const float czw = (pose.R[6] * px + r2) + pose.t[2];
+        const float ax = fa.fx * cxw, ay = fa.fy * cyw;
+        const float rz = div_rcp(czw);
+        const float u = div_fast(ax, czw, rz) + fa.cx;
+        const float v = div_fast(ay, czw, rz) + fa.cy;
+        const bool in = czw > 0.f && !(u < 1 || u > wLim || v < 1 || v > hLim);
+        pix[k] = in ? (int)(v + 0.5f) * fa.w + (int)(u + 0.5f) : -1;
+        zc[k] = czw;
+        if (!kWindowKnown) {
+          const bool fast = czw >= 0x1p-40f && czw <= 0x1p40f && fabsf(ax) <= 0x1p40f && fabsf(ay) <= 0x1p40f;
+          slow |= (czw > 0.f && !fast) ? (1u << k) : 0u;
+        }
+      }
+    }
+    if (!kWindowKnown && __any_sync(0xffffffffu, slow != 0u)) {
+#pragma unroll
+      for (int k = 0; k < 4 * kQG; ++k) {
+        if (slow & (1u << k)) {
+          const int lin = ((g + (k >> 2)) * 32 + lane) * 4;
+          project_exact(pose, fa, wLim, hLim, (float)(ox + (lin & 7) + (k & 3)) * vs,
+                        (float)(oy + ((lin >> 3) & 7)) * vs, (float)(oz + (lin >> 6)) * vs, &pix[k]);
+        }
+      }
+    }
+    // ---- gather
+    float dm[4 * kQG];
+#pragma unroll
+    for (int k = 0; k < 4 * kQG; ++k) dm[k] = pix[k] >= 0 ? __ldg(depth + pix[k]) : -1.f;
+    // ---- update (update_voxel_depth, fusion.cpp:9-36)
+    unsigned redo = 0u;
+#pragma unroll
+    for (int k = 0; k < 4 * kQG; ++k) {
+      const uint32_t w0 = wd[k];
+      const int oldW = vox_w(w0);
+      const float eta = dm[k] - zc[k];
+      const bool upd = pix[k] >= 0 && !(dm[k] <= 0.f) && !(eta < -mu) && !(capW && oldW >= maxW);
+      const float oldF = sdf_to_logical(vox_sdf(w0));
+      const float newF = smin(1.f, div_fast(eta, mu, rMu));
+      const float fw = (float)oldW;
+      const float num = fw * oldF + newF;
+      const float den = fw + 1.f;  // == (float)(oldW + 1): small integers are exact
+      const float merged = div_fast(num, den, div_rcp(den));
+      const uint32_t w1 = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
+      // out-of-window voxels keep w0 here and are redone exactly below
+      const bool slowK = kWindowKnown ? (upd && !(muOk && fabsf(eta) <= 0x1p40f))
+                                      : (upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << k))));
+      wd[k] = (upd && !slowK) ? w1 : w0;
+      redo |= slowK ? (1u << k) : 0u;
+    }
+    if (__any_sync(0xffffffffu, redo != 0u)) {
+#pragma unroll
+      for (int k = 0; k < 4 * kQG; ++k)
+        if (redo & (1u << k)) wd[k] = update_exact(wd[k], dm[k] - zc[k], mu, maxW);
+    }
+#pragma unroll
+    for (int q = g; q < g + kQG; ++q) {
+      const int k = (q - g) * 4;
+      blk[q * 32 + lane] = make_uint4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
+    }
+  }
+}
+
+// Block-level proof that every voxel of the block at (ox, oy, oz) projects
+// inside div_fast's window (camera z in [2^-40, 2^40], |fx X|, |fy Y| <=
+// 2^40).  The camera coordinates are affine in the voxel index, so their
+// extremes over the block are at its 8 corners (lanes 0-7, one corner each);
+// the computed values differ from the exact ones by a few ulp of the largest
+// term, which the 2^-20 relative margin covers with room to spare.
+__device__ __forceinline__ bool block_window_known(int lane, int ox, int oy, int oz, const Pose& pose,
+                                                   const FrameArgs& fa) {
+  bool ok = true;
+  if (lane < 8) {
+    const float vs = fa.voxelSize;
+    const float px = (float)(ox + ((lane & 1) ? 7 : 0)) * vs;
+    const float py = (float)(oy + ((lane & 2) ? 7 : 0)) * vs;
+    const float pz = (float)(oz + ((lane & 4) ? 7 : 0)) * vs;
+    const float cx = (pose.R[0] * px + (pose.R[1] * py + pose.R[2] * pz)) + pose.t[0];
+    const float cy = (pose.R[3] * px + (pose.R[4] * py + pose.R[5] * pz)) + pose.t[1];
+    const float cz = (pose.R[6] * px + (pose.R[7] * py + pose.R[8] * pz)) + pose.t[2];
+    const float mag = fabsf(px) + fabsf(py) + fabsf(pz) + fabsf(pose.t[0]) + fabsf(pose.t[1]) + fabsf(pose.t[2]);
+    const float f = fmaxf(1.f, fmaxf(fabsf(fa.fx), fabsf(fa.fy)));
+    // either the whole block is in front of the camera inside the window, or
+    // the whole block is behind it (z <= 0: every voxel is rejected before
+    // any quotient is used)
+    const bool front = cz > 0x1p-20f * mag + 0x1p-39f && cz < 0x1p38f;
+    ok = front && f * fabsf(cx) < 0x1p38f && f * fabsf(cy) < 0x1p38f && f * mag < 0x1p38f;
+  }
+  return __all_sync(0xffffffffu, ok);
+}
+
 __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m, const float* __restrict__ depth,
                                                                        FrameArgs fa) {
   const int lane = threadIdx.x & 31;
@@ -227,7 +355,7 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
   const int nVis = *((volatile int*)&m.state->nVisible);
   const Pose pose = frame_pose(fa);
   const float wLim = (float)(fa.w - 2), hLim = (float)(fa.h - 2);
-  const float mu = fa.mu, vs = fa.voxelSize;
+  const float mu = fa.mu;
   const bool muOk = mu >= 0x1p-20f && mu <= 0x1p20f;
   const float rMu = div_rcp(mu);
   const bool capW = fa.stopAtMaxW != 0;
@@ -238,90 +366,10 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
     if (e.w < 0) continue;
     const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
     uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
-#pragma unroll
-    for (int g = 0; g < 4; g += kQG) {
-      uint32_t wd[4 * kQG];
-#pragma unroll
-      for (int q = g; q < g + kQG; ++q) {
-        const uint4 r = blk[q * 32 + lane];
-        wd[(q - g) * 4 + 0] = r.x;
-        wd[(q - g) * 4 + 1] = r.y;
-        wd[(q - g) * 4 + 2] = r.z;
-        wd[(q - g) * 4 + 3] = r.w;
-      }
-      // ---- project
-      float zc[4 * kQG];
-      int pix[4 * kQG];
-      unsigned slow = 0u;
-#pragma unroll
-      for (int q = g; q < g + kQG; ++q) {
-        const int lin = (q * 32 + lane) * 4;
-        const float pz = (float)(oz + (lin >> 6)) * vs;
-        const float py = (float)(oy + ((lin >> 3) & 7)) * vs;
-        const float r0 = pose.R[1] * py + pose.R[2] * pz;
-        const float r1 = pose.R[4] * py + pose.R[5] * pz;
-        const float r2 = pose.R[7] * py + pose.R[8] * pz;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int k = (q - g) * 4 + i;
-          const float px = (float)(ox + (lin & 7) + i) * vs;
-          const float cxw = (pose.R[0] * px + r0) + pose.t[0];
-          const float cyw = (pose.R[3] * px + r1) + pose.t[1];
-          const float czw = (pose.R[6] * px + r2) + pose.t[2];
-          const float ax = fa.fx * cxw, ay = fa.fy * cyw;
-          const float rz = div_rcp(czw);
-          const float u = div_fast(ax, czw, rz) + fa.cx;
-          const float v = div_fast(ay, czw, rz) + fa.cy;
-          const bool in = czw > 0.f && !(u < 1 || u > wLim || v < 1 || v > hLim);
-          pix[k] = in ? (int)(v + 0.5f) * fa.w + (int)(u + 0.5f) : -1;
-          zc[k] = czw;
-          const bool fast = czw >= 0x1p-40f && czw <= 0x1p40f && fabsf(ax) <= 0x1p40f && fabsf(ay) <= 0x1p40f;
-          slow |= (czw > 0.f && !fast) ? (1u << k) : 0u;
-        }
-      }
-      if (__any_sync(0xffffffffu, slow != 0u)) {
-#pragma unroll
-        for (int k = 0; k < 4 * kQG; ++k) {
-          if (slow & (1u << k)) {
-            const int lin = ((g + (k >> 2)) * 32 + lane) * 4;
-            project_exact(pose, fa, wLim, hLim, (float)(ox + (lin & 7) + (k & 3)) * vs,
-                          (float)(oy + ((lin >> 3) & 7)) * vs, (float)(oz + (lin >> 6)) * vs, &pix[k]);
-          }
-        }
-      }
-      // ---- gather
-      float dm[4 * kQG];
-#pragma unroll
-      for (int k = 0; k < 4 * kQG; ++k) dm[k] = pix[k] >= 0 ? __ldg(depth + pix[k]) : -1.f;
-      // ---- update (update_voxel_depth, fusion.cpp:9-36)
-#pragma unroll
-      for (int k = 0; k < 4 * kQG; ++k) {
-        const uint32_t w0 = wd[k];
-        const int oldW = vox_w(w0);
-        const float eta = dm[k] - zc[k];
-        const bool upd = pix[k] >= 0 && !(dm[k] <= 0.f) && !(eta < -mu) && !(capW && oldW >= maxW);
-        const float oldF = sdf_to_logical(vox_sdf(w0));
-        const float newF = smin(1.f, div_fast(eta, mu, rMu));
-        const float num = (float)oldW * oldF + newF;
-        const float den = (float)(oldW + 1);
-        const float merged = div_fast(num, den, div_rcp(den));
-        const uint32_t w1 = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
-        // out-of-window voxels keep w0 here and are redone exactly below
-        const bool slowK = upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << k)));
-        wd[k] = (upd && !slowK) ? w1 : w0;
-        slow = slowK ? (slow | (1u << k)) : (slow & ~(1u << k));
-      }
-      if (__any_sync(0xffffffffu, slow != 0u)) {
-#pragma unroll
-        for (int k = 0; k < 4 * kQG; ++k)
-          if (slow & (1u << k)) wd[k] = update_exact(wd[k], dm[k] - zc[k], mu, maxW);
-      }
-#pragma unroll
-      for (int q = g; q < g + kQG; ++q) {
-        const int k = (q - g) * 4;
-        blk[q * 32 + lane] = make_uint4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
-      }
-    }
+    if (block_window_known(lane, ox, oy, oz, pose, fa))
+      integrate_block_depth<true>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW, maxW);
+    else
+      integrate_block_depth<false>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW, maxW);
   }
 }
 

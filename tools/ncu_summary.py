@@ -10,7 +10,7 @@ import sys
 
 
 def launches(path):
-    rows = list(csv.reader(open(path)))
+    rows = list(csv.reader(open(path, errors="replace")))
     hdr, data = None, []
     for r in rows:
         if r and r[0] == "ID":
