@@ -31,7 +31,7 @@ int icp_partial_slots();
 cudaError_t launch_icp_track(void* state, double* partials, const float* depthLevels, int levels, const Intr& in0,
                              const float4* points, const float4* normals, const int* iters, const float* dist,
                              int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
-                             cudaStream_t s);
+                             float* renderPoseOut, cudaStream_t s);
 cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* depth, int lw, int lh, const float* f4l,
                                    const Intr& in0, const float4* points, const float4* normals, const float* c2w,
                                    const float* renderPose, float dist, cudaStream_t s);
@@ -515,7 +515,7 @@ int rfg_icp_track(rfg_map* m, const float* depthLevels, int levels, const rfg_in
   const Intr in0{intr->width, intr->height, intr->fx, intr->fy, intr->cx, intr->cy};
   RFG_CK(launch_icp_track(m->icpOut, m->icpPartials, depthLevels, levels, in0, reinterpret_cast<const float4*>(points),
                           reinterpret_cast<const float4*>(normals), iters, dist, minCount, m->icpPose,
-                          m->icpPose + 12, m->icpPose + 24, m->stream));
+                          m->icpPose + 12, m->icpPose + 24, nullptr, m->stream));
   double st[8];
   float pose[12];
   RFG_CK(cudaMemcpyAsync(st, icp_stats_ptr(m->icpOut), sizeof(st), cudaMemcpyDeviceToHost, m->stream));
@@ -665,7 +665,7 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   if (track) {
     const Intr in0{c.intr.width, c.intr.height, c.intr.fx, c.intr.fy, c.intr.cx, c.intr.cy};
     e = launch_icp_track(m->icpOut, m->icpPartials, p->depthLevels, c.levels, in0, p->points, p->normals, c.iters,
-                         c.dist, c.min_count, p->poses, p->poses + 12, p->poses, s);
+                         c.dist, c.min_count, p->poses, p->poses + 12, p->poses, p->poses + 12, s);
     if (e != cudaSuccess) return e;
   }
   mark(2);
@@ -677,8 +677,10 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   if ((e = launch_ranges(m->d, fa, p->range, s)) != cudaSuccess) return e;
   mark(5);
   if ((e = launch_icp_maps(m->d, fa, p->range, p->raycast, p->points, p->normals, s)) != cudaSuccess) return e;
-  k_copy12<<<1, 32, 0, s>>>(p->poses + 12, p->poses);
-  count_launch();
+  if (!track) {  // a tracked frame's next render pose was written by the tracker
+    k_copy12<<<1, 32, 0, s>>>(p->poses + 12, p->poses);
+    count_launch();
+  }
   mark(6);
   return cudaGetLastError();
 }

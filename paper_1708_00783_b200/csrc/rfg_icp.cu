@@ -526,6 +526,7 @@ struct IcpTrackArgs {
   const float* w2cInit;
   const float* renderPose;
   float* w2cOut;
+  float* renderPoseOut;  // nullable: the next frame's render pose := the output pose
 };
 
 __global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrackArgs ta, double* partials) {
@@ -576,6 +577,10 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrac
     }
     if (ta.w2cOut)
       for (int i = 0; i < 12; ++i) ta.w2cOut[i] = st->w2cF[i];
+    // every CTA read renderPose before the first grid barrier, so it may be
+    // overwritten now (the frame's maps are rendered at the output pose)
+    if (ta.renderPoseOut)
+      for (int i = 0; i < 12; ++i) ta.renderPoseOut[i] = st->w2cF[i];
   }
 }
 
@@ -641,9 +646,10 @@ static IcpLevelArgs level_args(const float* depthLevels, int level, const Intr& 
 cudaError_t launch_icp_track(void* state, double* partials, const float* depthLevels, int levels, const Intr& in0,
                              const float4* points, const float4* normals, const int* iters, const float* dist,
                              int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
-                             cudaStream_t s) {
+                             float* renderPoseOut, cudaStream_t s) {
   IcpState* st = static_cast<IcpState*>(state);
   IcpTrackArgs ta{};
+  ta.renderPoseOut = renderPoseOut;
   ta.levels = levels;
   ta.w2cInit = w2cInit;
   ta.renderPose = renderPose;

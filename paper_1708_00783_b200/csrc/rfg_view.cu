@@ -52,6 +52,72 @@ __global__ void k_downsample(const float* __restrict__ in, int iw, float* __rest
   out[(size_t)y * ow + x] = n > 0 ? sum / (float)n : -1.f;
 }
 
+// The depth-only view (no bilateral filter, normals or intensity) in one
+// launch: a CTA converts a 32x16 tile of raw depth (toMetres, camera.hpp:54)
+// and reduces it to the 16x8 and 8x4 tiles of pyramid levels 1 and 2 in
+// shared memory (downsample_depth, view.cpp:69-88: 2x2 mean of the valid
+// samples in dy-major order).  Tile origins are multiples of 4 at level 0,
+// so every coarse pixel's 2x2 source lies inside the tile; per-pixel
+// arithmetic is k_depth_convert's and k_downsample's.
+__device__ __forceinline__ float raw_to_metres(uint16_t r, float scale, float offset, int bigEndian) {
+  if (bigEndian) r = (uint16_t)((r >> 8) | (r << 8));
+  const float m = (float)r * scale + offset;
+  return (r == 0) ? -1.f : (m > 0.f ? m : -1.f);
+}
+__device__ __forceinline__ float mean_valid4(float a, float b, float c, float d) {
+  const float v[4] = {a, b, c, d};
+  float sum = 0.f;
+  int n = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (v[k] > 0.f) {
+      sum += v[k];
+      ++n;
+    }
+  return n > 0 ? sum / (float)n : -1.f;
+}
+
+__global__ void __launch_bounds__(256) k_view_pyramid(const uint16_t* __restrict__ raw, int w, int h, float scale,
+                                                     float offset, int bigEndian, int levels, float* __restrict__ out) {
+  __shared__ float l0[16][32];
+  __shared__ float l1[8][16];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int X0 = blockIdx.x * 32, Y0 = blockIdx.y * 16;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int x = X0 + tx, y = Y0 + ty + 8 * r;
+    float m = -1.f;
+    if (x < w && y < h) {
+      m = raw_to_metres(__ldg(raw + (size_t)y * w + x), scale, offset, bigEndian);
+      out[(size_t)y * w + x] = m;
+    }
+    l0[ty + 8 * r][tx] = m;
+  }
+  if (levels < 2) return;
+  __syncthreads();
+  const int w1 = w / 2, h1 = h / 2;
+  float* out1 = out + (size_t)w * h;
+  if (threadIdx.x < 128) {
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int x = X0 / 2 + lx, y = Y0 / 2 + ly;
+    const float v = mean_valid4(l0[2 * ly][2 * lx], l0[2 * ly][2 * lx + 1], l0[2 * ly + 1][2 * lx],
+                                l0[2 * ly + 1][2 * lx + 1]);
+    l1[ly][lx] = v;
+    if (x < w1 && y < h1) out1[(size_t)y * w1 + x] = v;
+  }
+  if (levels < 3) return;
+  __syncthreads();
+  const int w2 = w1 / 2, h2 = h1 / 2;
+  float* out2 = out1 + (size_t)w1 * h1;
+  if (threadIdx.x < 32) {
+    const int lx = threadIdx.x & 7, ly = threadIdx.x >> 3;
+    const int x = X0 / 4 + lx, y = Y0 / 4 + ly;
+    if (x < w2 && y < h2)
+      out2[(size_t)y * w2 + x] = mean_valid4(l1[2 * ly][2 * lx], l1[2 * ly][2 * lx + 1], l1[2 * ly + 1][2 * lx],
+                                            l1[2 * ly + 1][2 * lx + 1]);
+  }
+}
+
 // bilateral_filter (view.cpp:18-44): 32x8 pixels per CTA, the 36x12 input
 // tile (2-pixel halo) staged in shared memory; the 25 neighbours in the
 // reference's dy-major order.  4 B in (+ halo) / 4 B out per pixel.
@@ -176,6 +242,12 @@ cudaError_t launch_build_view_full(const uint16_t* raw, const uint8_t* rgb, cons
                                    int bilateral, int levels, int bigEndian, float* depthLevels,
                                    float* intensityLevels, float4* normals, float* scratch, cudaStream_t s) {
   const int w = in.w, h = in.h, n = w * h;
+  if (!bilateral && !normals && !(rgb && intensityLevels) && levels <= 3) {
+    k_view_pyramid<<<dim3((w + 31) / 32, (h + 15) / 16), 256, 0, s>>>(raw, w, h, scale, offset, bigEndian, levels,
+                                                                     depthLevels);
+    count_launch();
+    return cudaGetLastError();
+  }
   float* conv = bilateral ? scratch : depthLevels;
   k_depth_convert<<<(n / 2 + 255) / 256 + 1, 256, 0, s>>>(raw, conv, n, scale, offset, bigEndian);
   count_launch();
