@@ -284,7 +284,7 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
 // time so their loads are in flight together; pixels are accumulated in
 // the same order as a plain loop, so the sums do not depend on kIcpGroup.
 constexpr int kIcpPxCache = 4;
-constexpr int kIcpGroup = 2;
+constexpr int kIcpGroup = 2;  // 1 and 4 measured no faster
 
 // J J^T, J r, r^2, count of one associated pixel (the oracle's per-pixel
 // body, rfo_icp_track).
@@ -467,7 +467,11 @@ __device__ __forceinline__ void icp_run_level(const IcpLevelArgs& a, double* par
         gn_step(g, a.level, a.minCount);
     }
     __syncthreads();
+#ifdef RFG_ICP_LEVEL_ONLY
+    if (timed && a.level == RFG_ICP_LEVEL_ONLY) {  // debug: phases of one level only
+#else
     if (timed) {  // in registers; flushed once at the end of the kernel
+#endif
       const unsigned long long t4 = gtimer();
       tacc[0] += t1 - t0;
       tacc[1] += t2 - t1;
