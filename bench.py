@@ -205,7 +205,7 @@ def run_reference_arm(args):
                          "stage_ms": per},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -235,6 +235,27 @@ def cupti_kernel_ms(pipe, raw_dev, poses, flush, warmup, n, name):
     return float(np.mean(d)) / 1e3 if d else None
 
 
+_JSON_OUT = None
+
+
+def guard_stdout():
+    """The contract is ONE JSON line on stdout.  Native libraries print to
+    fd 1 on their own (NCCL's version banner at communicator init on rank
+    0), so fd 1 is pointed at stderr for the whole run and the JSON line is
+    written to a saved copy of the original stdout."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def make_frames():
     from paper_1708_00783_b200 import fusion as F
     intr = F.Intrinsics(**INTR)
@@ -254,7 +275,13 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
+        if world == 1:  # --sharded on one GPU: the N > 1 code path with a world of one
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     intr = F.Intrinsics(**INTR)
     params = F.SceneParams(**PARAMS)
@@ -262,7 +289,7 @@ def run_b200(args):
     raw_dev = torch.from_numpy(raws.view(np.int16)).cuda()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    if world > 1:
+    if sharded:
         from paper_1708_00783_b200.shard import ShardedPipeline
         make_pipe = lambda m, graph, profile=False: ShardedPipeline(  # noqa: E731
             m, intr, params, rank, world, levels=3, iters=ICP_ITERS, dist=ICP_DIST)
@@ -272,7 +299,7 @@ def run_b200(args):
             use_graph=graph, profile=profile)
 
     m = F.VoxelBlockMap(F.VoxelBlockMapConfig(*MAPCFG), device=local)
-    if world > 1:
+    if sharded:
         m.set_shard(rank, world, 3)
     pipe = make_pipe(m, True)
     stream = torch.cuda.ExternalStream(pipe.stream)
@@ -425,14 +452,14 @@ def run_b200(args):
         "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "l2": "flushed (256 MiB write) before every timed frame",
-                   "parallelism": f"spatial hash shards x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"spatial hash shards x{world}" if sharded else "single GPU",
                    "graph": True, "last_frame_stats": stats.as_array().tolist(),
                    "icp_last": {"iterations": int(icp[0]), "count": int(icp[1]), "per_level": icp[4:7].tolist()}},
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roof, "stage_ms": prof,
         "cpu_baseline": cpu, "step_ms_p50": float(np.median(step_ms)), "step_ms_max": float(np.max(step_ms)),
     }
-    print(json.dumps(line), flush=True)
-    if world > 1:
+    emit(line)
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
@@ -446,11 +473,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--profile-frames", type=int, default=95)
     ap.add_argument("--cpu-frames", type=int, default=5)
+    ap.add_argument("--sharded", action="store_true", help="run the sharded (N > 1) pipeline even at N = 1")
     ap.add_argument("--clock-ms", type=int, default=5, help="nvidia-smi clock sampling period (0 = off)")
     ap.add_argument("--ref-budget", type=float, default=150.0, help="reference arm time budget (s)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    guard_stdout()
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_b200(args)

@@ -307,6 +307,12 @@ int rfg_pipeline_reset(rfg_pipeline* p);
 int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]);
 /* The pipeline's stream (cudaStream_t) for event timing by the caller. */
 void* rfg_pipeline_stream(rfg_pipeline* p);
+/* Device pointer to the pipeline's current world->camera pose (12 floats,
+ * row-major 3x4; written by the tracker or rfg_pipeline_process*'s pose34),
+ * valid for work ordered after the frame on the pipeline's stream.  The
+ * three maps of rfg_pipeline_buffers are one allocation, in the order
+ * raycast | points | normals (3 x width x height float4). */
+int rfg_pipeline_pose_buffer(rfg_pipeline* p, float** pose_dev);
 
 /* --------------------------------------------- multi-GPU composition */
 /* Per-pixel nearest-hit composition of spatially sharded renders
@@ -317,6 +323,9 @@ void* rfg_pipeline_stream(rfg_pipeline* p);
  * the three maps yields the composed render exactly. */
 int rfg_compose_keys(const float* points_dev, const float pose34[12], int rank, int n, int64_t* keys_dev,
                      void* cuda_stream);
+/* Same, with the pose read on the device (e.g. rfg_pipeline_pose_buffer). */
+int rfg_compose_keys_dev(const float* points_dev, const float* pose34_dev, int rank, int n, int64_t* keys_dev,
+                         void* cuda_stream);
 int rfg_compose_select(const int64_t* keymin_dev, int rank, int n, float* raycast_dev, float* points_dev,
                        float* normals_dev, void* cuda_stream);
 

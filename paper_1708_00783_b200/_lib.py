@@ -125,7 +125,9 @@ SIGNATURES = {
     "rfg_pipeline_reset": ([_vp], C.c_int),
     "rfg_pipeline_stage_times": ([_vp, _f], C.c_int),
     "rfg_pipeline_stream": ([_vp], _vp),
+    "rfg_pipeline_pose_buffer": ([_vp, C.POINTER(_vp)], C.c_int),
     "rfg_compose_keys": ([_vp, _f, C.c_int, C.c_int, _vp, _vp], C.c_int),
+    "rfg_compose_keys_dev": ([_vp, _vp, C.c_int, C.c_int, _vp, _vp], C.c_int),
     "rfg_compose_select": ([_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp], C.c_int),
     "rfg_icp_timers": ([_vp, C.POINTER(C.c_uint64), C.c_int], C.c_int),
     "rfg_total_entries": ([_vp], C.c_uint32),

@@ -739,9 +739,9 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
             cudaMalloc(&p->rawDev, n * 2 + 16) == cudaSuccess &&
             cudaMalloc(&p->depthLevels, lv * 4 + 16) == cudaSuccess &&
             cudaMalloc(&p->range, n * sizeof(float2)) == cudaSuccess &&
-            cudaMalloc(&p->raycast, n * sizeof(float4)) == cudaSuccess &&
-            cudaMalloc(&p->points, n * sizeof(float4)) == cudaSuccess &&
-            cudaMalloc(&p->normals, n * sizeof(float4)) == cudaSuccess &&
+            // raycast | points | normals in one allocation, so a sharded
+            // rank composes all three with one in-place collective
+            cudaMalloc(&p->raycast, 3 * n * sizeof(float4)) == cudaSuccess &&
             cudaMalloc(&p->poses, 32 * sizeof(float)) == cudaSuccess &&
             cudaMallocHost(&p->hostIcp, 8 * sizeof(double)) == cudaSuccess &&
             cudaMallocHost(&p->hostPose, 12 * sizeof(float)) == cudaSuccess &&
@@ -753,6 +753,8 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
     set_error("pipeline allocation failed");
     return RFG_ENOMEM;
   }
+  p->points = p->raycast + n;
+  p->normals = p->raycast + 2 * n;
   for (int k = 0; k < 7; ++k)
     if (cudaEventCreate(&p->ev[k]) != cudaSuccess) ok = false;
   if (cudaEventCreateWithFlags(&p->stageFree, cudaEventDisableTiming) != cudaSuccess) ok = false;
@@ -783,7 +785,7 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (int i = 0; i < 2; ++i)
     if (p->exec[i]) cudaGraphExecDestroy(p->exec[i]);
-  void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->points, p->normals, p->poses, p->viewScratch};
+  void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->poses, p->viewScratch};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int k = 0; k < 7; ++k)
@@ -885,6 +887,12 @@ int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]) {
 }
 
 void* rfg_pipeline_stream(rfg_pipeline* p) { return p ? (void*)p->stream : nullptr; }
+
+int rfg_pipeline_pose_buffer(rfg_pipeline* p, float** poseDev) {
+  RFG_REQUIRE(p && poseDev, "null argument");
+  *poseDev = p->poses;
+  return RFG_OK;
+}
 
 int rfg_pipeline_buffers(rfg_pipeline* p, float** depthLevels, float** range, float** raycast, float** points,
                          float** normals) {

@@ -713,14 +713,14 @@ cudaError_t launch_forward_project(int hasRaycast, float4* raycast, float4* poin
 // ------------------------------------------------ multi-GPU composition
 namespace rfg {
 
-__global__ void k_compose_keys(const float4* __restrict__ points, Pose12 pose, int rank, int n,
-                               long long* __restrict__ keys) {
+__global__ void k_compose_keys(const float4* __restrict__ points, Pose12 pose, const float* __restrict__ poseDev,
+                               int rank, int n, long long* __restrict__ keys) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float4 p = points[i];
   long long k = 0x7fffffffffffffffLL;
   if (p.w > 0.f) {
-    const Pose P = pose_from12(pose.v);
+    const Pose P = poseDev ? pose_from12(poseDev) : pose_from12(pose.v);
     const float z = pose_apply(P, f3{p.x, p.y, p.z}).z;  // camera depth of the hit (> 0)
     k = ((long long)(uint32_t)__float_as_int(fmaxf(z, 0.f)) << 32) | (long long)(uint32_t)rank;
   }
@@ -752,7 +752,21 @@ extern "C" int rfg_compose_keys(const float* points, const float pose34[12], int
   rfg::Pose12 p;
   for (int i = 0; i < 12; ++i) p.v[i] = pose34[i];
   rfg::k_compose_keys<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const float4*>(points), p, rank, n, reinterpret_cast<long long*>(keys));
+      reinterpret_cast<const float4*>(points), p, nullptr, rank, n, reinterpret_cast<long long*>(keys));
+  rfg::count_launch();
+  RFG_CK(cudaGetLastError());
+  return RFG_OK;
+}
+
+extern "C" int rfg_compose_keys_dev(const float* points, const float* poseDev, int rank, int n, int64_t* keys,
+                                    void* stream) {
+  if (!points || !poseDev || !keys || n < 0 || rank < 0) {
+    rfg::set_error("rfg_compose_keys_dev: invalid argument");
+    return RFG_EINVAL;
+  }
+  rfg::Pose12 p{};
+  rfg::k_compose_keys<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(points), p, poseDev, rank, n, reinterpret_cast<long long*>(keys));
   rfg::count_launch();
   RFG_CK(cudaGetLastError());
   return RFG_OK;

@@ -804,6 +804,12 @@ class Pipeline:
         check(lib().rfg_pipeline_result(self._h, C.byref(st), _fp(pose), icp.ctypes.data_as(_d)))
         return AllocationStats(st.requested, st.allocated, st.allocFailures, st.visibleCount), pose, icp
 
+    def pose_buffer(self) -> int:
+        """Device pointer of the current world->camera pose (12 floats)."""
+        ptr = C.c_void_p()
+        check(lib().rfg_pipeline_pose_buffer(self._h, C.byref(ptr)))
+        return ptr.value
+
     def buffers(self):
         ptrs = [C.c_void_p() for _ in range(5)]
         check(lib().rfg_pipeline_buffers(self._h, *[C.byref(p) for p in ptrs]))

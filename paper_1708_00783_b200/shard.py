@@ -7,14 +7,18 @@ world; the filter runs inside k_alloc_stage1, rfg_map_set_shard).  Every rank
 renders its shard; the ICP maps are then composed by a per-pixel nearest-hit
 reduction — the only data-path exchange:
 
-  keys = (float bits of hit camera-z) << 32 | rank   (rfg_compose_keys)
+  keys = (float bits of hit camera-z) << 32 | rank   (rfg_compose_keys[_dev])
   all_reduce(keys, MIN)                              (NCCL, 2.46 MB @ 640x480)
   zero every pixel this rank did not win             (rfg_compose_select)
-  all_reduce(raycast | points | normals, SUM)        (NCCL, 14.7 MB; exact —
-                                                      one nonzero term per pixel)
+  all_reduce(raycast | points | normals, SUM)        (NCCL, 14.7 MB in place;
+                                                      exact — one nonzero term
+                                                      per pixel)
 
 The ICP tracker then runs replicated on the composed maps, so tracking needs
 no per-iteration collective and every rank ends the frame with the same pose.
+`Composer` is the collective sequence on caller-owned tensors (the gloo
+world-size-2 test drives it with CPU stand-ins for the two kernels);
+`ShardedPipeline` runs it on the device-resident frame graph.
 """
 from __future__ import annotations
 
@@ -64,58 +68,74 @@ class Composer:
         return keys
 
 
+class _DeviceBuffer:
+    """A raw device allocation seen by torch without a copy
+    (__cuda_array_interface__); the owner keeps it alive."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
 class ShardedPipeline:
-    """Per-frame driver for one rank of a spatially sharded map:
-    build_view -> [replicated ICP on the composed maps] -> allocate ->
-    integrate -> expected ranges -> raycast -> nearest-hit composition."""
+    """Per-frame driver for one rank of a spatially sharded map: the rank's
+    device-resident frame graph (rfg_pipeline: build_view -> ICP on the last
+    COMPOSED maps -> allocate (owned blocks + halo) -> integrate -> expected
+    ranges -> raycast) followed, on the same stream, by the nearest-hit
+    composition written back into the graph's map buffers, so the next
+    frame tracks against the composed render.  No host round trip per frame:
+    the pose stays on the device (every rank tracks on identical maps and
+    frames, so every rank computes the identical pose)."""
 
     def __init__(self, map: F.VoxelBlockMap, intr: F.Intrinsics, params: F.SceneParams, rank: int, world: int,
                  levels: int = 3, iters=(6, 10, 20), dist=(0.01, 0.02, 0.04),
-                 affine: F.DepthAffine = F.DepthAffine(1.0 / 5000.0, 0.0), min_count: int = 10):
+                 affine: F.DepthAffine = F.DepthAffine(1.0 / 5000.0, 0.0), min_count: int = 10,
+                 use_graph: bool = True):
         self.map, self.intr, self.params = map, intr, params
         self.rank, self.world = rank, world
-        self.levels, self.iters, self.dist, self.min_count = levels, iters, dist, min_count
-        self.calib = F.RgbdCalib(intrinsics_rgb=intr, intrinsics_d=intr, depth_affine=affine)
-        self.engine = F.FusionEngine()
-        self.state = F.RenderState()
-        self.composer = Composer(rank, world)
-        self._stream = torch.cuda.Stream()
-        self.reset()
+        self.pipe = F.Pipeline(map, intr, params, affine, levels=levels, track=True, iters=iters, dist=dist,
+                               min_count=min_count, use_graph=use_graph)
+        self.n = intr.width * intr.height
+        _, _, raycast, points, normals = self.pipe.buffers()
+        assert points == raycast + 16 * self.n and normals == raycast + 32 * self.n  # one allocation
+        self._ptrs = (raycast, points, normals)
+        self._pose_dev = self.pipe.pose_buffer()
+        self._maps = torch.as_tensor(_DeviceBuffer(raycast, 3 * 4 * self.n), device="cuda")
+        self._keys = torch.empty(self.n, dtype=torch.int64, device="cuda")
+        self._stream = torch.cuda.ExternalStream(self.pipe.stream)
+        self.frames = 0
 
     @property
     def stream(self) -> int:
-        return self._stream.cuda_stream
+        return self.pipe.stream
 
     def reset(self):
-        self.pose = np.eye(3, 4, dtype=np.float32)
+        self.pipe.reset()
         self.frames = 0
-        self.last_stats = F.AllocationStats()
-        self.last_icp = np.zeros(8)
-        self.state = F.RenderState()
+
+    def maps(self):
+        """(raycastResult, points, normals) of the last composed render, each
+        a (H, W, 4) view of the pipeline's buffers."""
+        h, w = self.intr.height, self.intr.width
+        m = self._maps.view(3, h, w, 4)
+        return m[0], m[1], m[2]
+
+    def compose(self):
+        """Nearest-hit composition of this rank's last render with the other
+        ranks', in place, on the pipeline's stream."""
+        raycast, points, normals = self._ptrs
+        with torch.cuda.stream(self._stream):
+            check(lib().rfg_compose_keys_dev(C.c_void_p(points), C.c_void_p(self._pose_dev), self.rank, self.n,
+                                             C.c_void_p(self._keys.data_ptr()), C.c_void_p(self.pipe.stream)))
+            dist.all_reduce(self._keys, op=dist.ReduceOp.MIN)
+            check(lib().rfg_compose_select(C.c_void_p(self._keys.data_ptr()), self.rank, self.n, C.c_void_p(raycast),
+                                           C.c_void_p(points), C.c_void_p(normals), C.c_void_p(self.pipe.stream)))
+            dist.all_reduce(self._maps, op=dist.ReduceOp.SUM)  # raycast | points | normals, one collective
 
     def process(self, raw, pose=None):
-        # a device frame is read on this pipeline's stream: order it after its
-        # producer and keep it alive until read (torch pool streams are never
-        # destroyed, so record_stream is safe here)
-        self._stream.wait_stream(torch.cuda.current_stream())
-        if torch.is_tensor(raw) and raw.is_cuda:
-            raw.record_stream(self._stream)
-        with torch.cuda.stream(self._stream):
-            if pose is not None:
-                self.pose = np.asarray(pose, np.float32).reshape(3, 4).copy()
-            view = F.build_view(raw if torch.is_tensor(raw) else np.asarray(raw), None, self.calib, self.levels)
-            if self.frames > 0 and self.state.hasRaycast:
-                self.pose, summ = F.track_depth(self.map, view, self.state, self.pose, self.iters, self.dist,
-                                                self.min_count)
-                self.last_icp = np.array([summ.iterations, summ.count, summ.residual_sum, summ.converged,
-                                          *summ.per_level, summ.ok], np.float64)
-            self.last_stats = self.engine.allocate_from_depth(self.map, view, self.pose, self.params)
-            self.engine.integrate_frame(self.map, view, self.pose, self.params)
-            F.render_expected_ranges(self.map, self.pose, self.intr, self.params, self.state)
-            F.render_maps(self.map, self.pose, self.intr, self.params, F.RenderMode.kIcpMaps, self.state)
-            self.composer.compose(self.pose, self.state.raycastResult, self.state.points, self.state.normals)
+        self.pipe.process(raw, pose)
+        self.compose()
         self.frames += 1
 
     def result(self):
-        torch.cuda.synchronize()
-        return self.last_stats, self.pose.copy(), self.last_icp
+        return self.pipe.result()

@@ -76,8 +76,8 @@ def test_sharded_pipeline_world1_equals_single_gpu_pipeline():
         rs = F.RenderState()
         F.render_expected_ranges(m2, p1, intr, params, rs)
         F.render_maps(m2, p1, intr, params, F.RenderMode.kIcpMaps, rs)
-        for a, b in ((sp.state.points, rs.points), (sp.state.normals, rs.normals),
-                     (sp.state.raycastResult, rs.raycastResult)):
+        sr, sp_pts, sn = sp.maps()
+        for a, b in ((sp_pts, rs.points), (sn, rs.normals), (sr, rs.raycastResult)):
             assert torch.equal(a, b)
         assert (rs.points[..., 3] > 0).float().mean().item() > 0.8
     finally:
