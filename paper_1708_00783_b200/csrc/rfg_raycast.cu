@@ -263,15 +263,18 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
   enum { COARSE, FINE, SURFACE };
   int state = field.resident(at_t(oV, dV, t)) ? FINE : COARSE;
 #ifdef RFG_RC_STATS
-  int nSteps = 0, nCoarse = 0, nInv = 0, nNear = 0;
+  int nSteps = 0, nCoarse = 0, nInv = 0, nNear = 0, nVs = 0;
   struct Fin {
-    int& a; int& b; int& c; int& d;
+    int& a; int& b; int& c; int& d; int& e;
     __device__ ~Fin() {
       RC_STAT(0, 1); RC_STAT(1, a); RC_STAT(2, b); RC_STAT(3, c); RC_STAT(4, d);
       RC_STAT(8 + min(15, 32 - __clz(a)), 1);
       atomicMax(&g_rc_stats[31], (unsigned long long)a);
+      if (a >= 64) {  // the long rays: what their steps are
+        RC_STAT(24, 1); RC_STAT(25, a); RC_STAT(26, b); RC_STAT(27, c); RC_STAT(28, e); RC_STAT(29, d - e);
+      }
     }
-  } fin{nSteps, nCoarse, nInv, nNear};
+  } fin{nSteps, nCoarse, nInv, nNear, nVs};
 #endif
   while (t <= tMaxM) {
 #ifdef RFG_RC_STATS
@@ -321,6 +324,9 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
       *hit = at_t(oV, dV, tHit);
       return true;
     }
+#ifdef RFG_RC_STATS
+    if (!(vs < sdf * stepScale)) ++nVs;
+#endif
     t += smax(sdf * stepScale, vs);
   }
   return false;
@@ -412,13 +418,13 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_icp(DevMap m, Fram
                                                      float4* raycast, float4* points) {
   const int x = blockIdx.x * 16 + (threadIdx.x & 15);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
-#if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
+#if defined(RFG_RC_TIMING)
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   if (threadIdx.x == 0) atomicMin(&g_rc_stats[24], t0);
 #endif
   if (x < fa.w && y < fa.h) raycast_pixel(m, fa, range, x, y, raycast, points);
-#if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
+#if defined(RFG_RC_TIMING)
   unsigned long long t1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   unsigned long long dur = t1 - t0, end = t1, sum = t1 - t0;

@@ -33,8 +33,13 @@ for f in range(40):
 s = acc
 nf = 10
 tm = np.array(timing)
-print(f"k_raycast_icp per frame: span {tm[:, 1].mean():.1f} us, longest ray {tm[:, 0].mean():.1f} us "
-      f"(max {tm[:, 0].max():.1f}), mean ray {tm[:, 2].mean():.2f} us")
+if s[0] == 0:  # RFG_RC_TIMING build (slots 7, 24-27: kernel span and ray durations)
+    print(f"k_raycast_icp per frame: span {tm[:, 1].mean():.1f} us, longest ray {tm[:, 0].mean():.1f} us "
+          f"(max {tm[:, 0].max():.1f}), mean ray {tm[:, 2].mean():.2f} us")
+    sys.exit(0)
 print(f"per frame: rays {s[0]/nf:.0f} steps {s[1]/nf:.0f} coarse {s[2]/nf:.0f} invalid-fine {s[3]/nf:.0f} "
       f"nearest {s[4]/nf:.0f} trilinear {s[5]/nf:.0f} lookups {s[6]/nf:.0f}  max steps (last frame) {buf[31]}")
+if s[24]:
+    print(f"rays >= 64 steps: {s[24]/nf:.0f}/frame, their steps: {s[25]/s[24]:.1f}/ray = coarse {s[26]/s[24]:.1f} + "
+          f"invalid-fine {s[27]/s[24]:.1f} + one-voxel {s[28]/s[24]:.1f} + longer {s[29]/s[24]:.1f} (+ the hit/miss step)")
 print("steps/ray histogram (log2 buckets):", {f"<{2**b}": int(s[8 + b] // nf) for b in range(16) if s[8 + b]})
