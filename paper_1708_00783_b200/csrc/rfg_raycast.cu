@@ -113,15 +113,27 @@ __global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m,
   for (int base = 0; base < n; base += kRangeTile * kRangeTile) {
     const int i = base + threadIdx.x;
     __syncthreads();
-    if (i < n) sb[threadIdx.x] = m.rangeBounds[overflow ? i : m.bins[(size_t)t * m.binCap + i]];
+    if (i < n) {
+      // the block's rectangle clipped to this tile as a column mask (bits
+      // 0-15) and a row mask (bits 16-31): pixel (lx, ly) of the tile is
+      // covered iff both of its bits are set (0 for an empty clip)
+      const int4 bb = m.rangeBounds[overflow ? i : m.bins[(size_t)t * m.binCap + i]];
+      const int tx = blockIdx.x * kRangeTile, ty = blockIdx.y * kRangeTile;
+      const int lx0 = max((bb.x & 0xFFFF) - tx, 0), lx1 = min((bb.y & 0xFFFF) - tx, kRangeTile - 1);
+      const int ly0 = max((bb.x >> 16) - ty, 0), ly1 = min((bb.y >> 16) - ty, kRangeTile - 1);
+      uint32_t mask = 0u;
+      if (lx0 <= lx1 && ly0 <= ly1)
+        mask = (((2u << lx1) - 1u) & ~((1u << lx0) - 1u)) | ((((2u << ly1) - 1u) & ~((1u << ly0) - 1u)) << 16);
+      sb[threadIdx.x] = make_int4((int)mask, bb.z, bb.w, 0);
+    }
     __syncthreads();
     const int cnt = min(n - base, kRangeTile * kRangeTile);
+    const uint32_t me = (1u << (threadIdx.x & (kRangeTile - 1))) | (1u << (16 + threadIdx.x / kRangeTile));
     for (int j = 0; j < cnt; ++j) {
       const int4 bb = sb[j];
-      const int bx0 = bb.x & 0xFFFF, by0 = bb.x >> 16, bx1 = bb.y & 0xFFFF, by1 = bb.y >> 16;
-      if (x >= bx0 && x <= bx1 && y >= by0 && y <= by1) {
-        lo = min(lo, bb.z);  // positive floats order like their bit patterns
-        hi = max(hi, bb.w);  // -1.f (negative int) loses against any z > 0
+      if (((uint32_t)bb.x & me) == me) {
+        lo = min(lo, bb.y);  // positive floats order like their bit patterns
+        hi = max(hi, bb.z);  // -1.f (negative int) loses against any z > 0
       }
     }
   }
