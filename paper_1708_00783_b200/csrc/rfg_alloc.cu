@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kTileThreads) k_req_count(DevMap m) {
     st->snapFreeExcess = st->nFreeExcess;
     st->succ = 0;
     st->succType2 = 0;
+    st->nVisible = 0;  // stage 3 appends to the visible list
   }
   const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
   int n = 0, n2 = 0;
@@ -407,7 +408,8 @@ __device__ __forceinline__ bool block_in_frustum(int bx, int by, int bz, const P
 // spread over the CTA whatever the hash distribution.
 __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs fa) {
   __shared__ int queue[kTile];
-  __shared__ int nq, nvis;
+  __shared__ int vis[kTile];
+  __shared__ int nq, nvis, listBase;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // finalise stage 2 (all k_req_assign CTAs have completed)
     MapState* st = m.state;
@@ -436,7 +438,6 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
   if (mk) *mp = 0u;
   __syncthreads();
   const Pose pose = frame_pose(fa);
-  int n = 0;
   for (int i = threadIdx.x; i < nq; i += kTileThreads) {
     const int idx = queue[i];
     const int4 e = ld_entry(m.entries, idx);
@@ -450,12 +451,30 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
       type = 3;
     if (type) {
       m.visibility[idx] = type;
-      ++n;
+      vis[atomicAdd(&nvis, 1)] = idx;
     }
   }
-  if (n) atomicAdd(&nvis, n);
   __syncthreads();
-  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = make_int2(nvis, 0);
+  // append this tile's visible entries to the list (one global atomic per
+  // CTA); the in-frame consumers (integration, expected ranges) do not
+  // depend on the order, and rfg_export_visible regenerates the reference's
+  // ascending order (fusion.cpp:231) from the visibility bytes
+  if (threadIdx.x == 0) listBase = nvis ? atomicAdd(&m.state->nVisible, nvis) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nvis; i += kTileThreads) m.visibleList[listBase + i] = vis[i];
+}
+
+// Per-tile count of visible entries (visibility bytes), for regenerating the
+// ascending visible list (k_scan_tiles mode 1 + k_vis_emit).
+__global__ void __launch_bounds__(kTileThreads) k_vis_tilecount(DevMap m) {
+  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
+  const uint32_t w = *reinterpret_cast<const uint32_t*>(m.visibility + base);
+  int n = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) n += ((w >> (8 * j)) & 0xFFu) ? 1 : 0;
+  int2 total;
+  block_exclusive_scan2<kTileThreads>(make_int2(n, 0), &total);
+  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
@@ -480,9 +499,17 @@ cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs
   k_scan_tiles<<<1, 1024, 0, s>>>(m.tileCounts, m.tilePrefix, m.nTiles, m.state, 0);
   k_req_assign<<<m.nTiles, kTileThreads, 0, s>>>(m, depth, fa);
   k_vis_count<<<m.nTiles, kTileThreads, 0, s>>>(m, fa);
+  count_launch(5);
+  return cudaGetLastError();
+}
+
+// The visible list in the reference's ascending entry order (fusion.cpp:231),
+// rebuilt from the visibility bytes (the frame's kernels append it unordered).
+cudaError_t launch_sort_visible(const DevMap& m, cudaStream_t s) {
+  k_vis_tilecount<<<m.nTiles, kTileThreads, 0, s>>>(m);
   k_scan_tiles<<<1, 1024, 0, s>>>(m.tileCounts, m.tilePrefix, m.nTiles, m.state, 1);
   k_vis_emit<<<m.nTiles, kTileThreads, 0, s>>>(m);
-  count_launch(7);
+  count_launch(3);
   return cudaGetLastError();
 }
 

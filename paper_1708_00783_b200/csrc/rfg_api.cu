@@ -315,6 +315,7 @@ int rfg_allocate_from_depth_ex(rfg_map* m, const float* depth, const rfg_intrins
     const int rc = check_device_error(m);  // synchronises, refreshes hostState
     if (rc != RFG_OK) return rc;
     memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
+    stats->visibleCount = m->hostState->nVisible;  // stage 3 appends the list; its length is the count
   }
   return RFG_OK;
 }
@@ -600,7 +601,10 @@ int rfg_export_visible(rfg_map* m, int32_t* list, uint8_t* types, int32_t* count
   if (rc != RFG_OK) return rc;
   const int n = m->hostState->nVisible;
   *count = n;
-  if (list && n) RFG_CK(cudaMemcpyAsync(list, m->d.visibleList, n * sizeof(int), cudaMemcpyDeviceToHost, m->stream));
+  if (list && n) {
+    RFG_CK(launch_sort_visible(m->d, m->stream));
+    RFG_CK(cudaMemcpyAsync(list, m->d.visibleList, n * sizeof(int), cudaMemcpyDeviceToHost, m->stream));
+  }
   if (types) RFG_CK(cudaMemcpyAsync(types, m->d.visibility, m->d.total, cudaMemcpyDeviceToHost, m->stream));
   RFG_CK(cudaStreamSynchronize(m->stream));
   return RFG_OK;
@@ -870,7 +874,10 @@ int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34
     RFG_CK(cudaMemcpyAsync(p->hostIcp, icp_stats_ptr(m->icpOut), 64, cudaMemcpyDeviceToHost, p->stream));
   RFG_CK(cudaStreamSynchronize(p->stream));
   if (m->hostState->error) return check_device_error(m);
-  if (stats) memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
+  if (stats) {
+    memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
+    stats->visibleCount = m->hostState->nVisible;  // stage 3 appends the list; its length is the count
+  }
   if (poseOut34) memcpy(poseOut34, p->hostPose, 48);
   if (icpStats8) memcpy(icpStats8, p->hostIcp, 64);
   return RFG_OK;

@@ -21,7 +21,7 @@ struct MapState {
   // per-frame allocation bookkeeping
   int snapFreeBlocks, snapFreeExcess;  // stack sizes at the start of stage 2
   int succ, succType2;                 // stage-2 successes (all / excess-linked)
-  int stats[4];                        // requested, allocated, allocFailures, visibleCount
+  int stats[4];                        // requested, allocated, allocFailures, (visibleCount = nVisible)
   int nRequests;                       // stage-2 request count
   int pad[5];
 };
@@ -81,6 +81,7 @@ FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p,
 
 // kernel launchers (return cudaError_t of the launch)
 cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s);
+cudaError_t launch_sort_visible(const DevMap& m, cudaStream_t s);
 cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint8_t* rgb, const FrameArgs& fa,
                              const rfg_intrinsics* intrRgb, const float* extr34, cudaStream_t s);
 cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s);
