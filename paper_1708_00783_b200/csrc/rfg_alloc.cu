@@ -285,7 +285,6 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int2* counts, int2* prefix,
   }
   if (threadIdx.x == 0) {
     prefix[n] = total;
-    if (mode == 0) st->nRequests = total.x;
     if (mode == 1) {
       st->nVisible = total.x;
       st->stats[3] = total.x;
@@ -341,8 +340,20 @@ __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const flo
     }
   int2 total;
   const int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
+  const bool last = blockIdx.x == gridDim.x - 1;
+  if (total.x == 0 && !last) return;  // (CTA-uniform) most tiles hold no request
+  // this tile's prefix: the counts of the tiles before it, summed by the CTA
+  // itself (no separate scan launch; integer sums, so order-free)
+  int2 pre = make_int2(0, 0);
+  for (int i = threadIdx.x; i < (int)blockIdx.x; i += kTileThreads) {
+    const int2 c = m.tileCounts[i];
+    pre.x += c.x;
+    pre.y += c.y;
+  }
+  int2 tp;
+  block_exclusive_scan2<kTileThreads>(pre, &tp);
+  if (last && threadIdx.x == 0) m.state->nRequests = tp.x + total.x;
   if (n == 0) return;
-  const int2 tp = m.tilePrefix[blockIdx.x];
   int before = tp.x + ex.x, before2 = tp.y + ex.y;
   const int nB = m.state->snapFreeBlocks, nE = m.state->snapFreeExcess;
   const Pose camToWorld = pose_inverse(frame_pose(fa));
@@ -496,10 +507,9 @@ cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs
   dim3 g1((fa.w + 31) / 32, (fa.h + kStage1Rows - 1) / kStage1Rows);
   k_alloc_stage1<<<g1, 256, 0, s>>>(m, depth, fa);
   k_req_count<<<m.nTiles, kTileThreads, 0, s>>>(m);
-  k_scan_tiles<<<1, 1024, 0, s>>>(m.tileCounts, m.tilePrefix, m.nTiles, m.state, 0);
   k_req_assign<<<m.nTiles, kTileThreads, 0, s>>>(m, depth, fa);
   k_vis_count<<<m.nTiles, kTileThreads, 0, s>>>(m, fa);
-  count_launch(5);
+  count_launch(4);
   return cudaGetLastError();
 }
 
