@@ -133,7 +133,13 @@ __device__ __forceinline__ void mark_or_request(const DevMap& m, i3 cell, uint32
       e = ld_entry(m.entries, idx);
     }
   }
-  if (m.reqKey[idx] < key) atomicMax(&m.reqKey[idx], key);
+  if (m.reqKey[idx] < key && atomicMax(&m.reqKey[idx], key) == 0u) {
+    // the slot's first request this frame: count it for stage 2 (per
+    // kTile-entry tile: requests, and those that extend a chain)
+    int2* tc = m.tileCounts + idx / kTile;
+    atomicAdd(&tc->x, 1);
+    if (entry_allocated(e)) atomicAdd(&tc->y, 1);
+  }
 }
 
 // The pixels of a CTA (a 32x8 tile) stab a handful of distinct blocks many
@@ -152,6 +158,15 @@ constexpr int kStage1Rows = 16;
 __global__ void __launch_bounds__(256, 5) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
   __shared__ unsigned long long sCell[kCellSlots];  // (x | y << 16 | z << 32 | 1 << 48), 0 = empty
   __shared__ uint32_t sKey[kCellSlots];
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    // stage-2 / stage-3 bookkeeping of this frame (no stage-1 CTA reads it)
+    MapState* st = m.state;
+    st->snapFreeBlocks = st->nFreeBlocks;
+    st->snapFreeExcess = st->nFreeExcess;
+    st->succ = 0;
+    st->succType2 = 0;
+    st->nVisible = 0;  // stage 3 appends to the visible list
+  }
   for (int i = threadIdx.x; i < kCellSlots; i += blockDim.x) {
     sCell[i] = 0ull;
     sKey[i] = 0u;
@@ -297,30 +312,8 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int2* counts, int2* prefix,
 // 16-byte load of keys, one 4-byte load of flag bytes), so a tile's threads
 // cover it in ascending entry order and a CTA scan gives the serial ranks.
 
-// Count requests (and excess-linked requests) per tile.
-__global__ void __launch_bounds__(kTileThreads) k_req_count(DevMap m) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    MapState* st = m.state;
-    st->snapFreeBlocks = st->nFreeBlocks;
-    st->snapFreeExcess = st->nFreeExcess;
-    st->succ = 0;
-    st->succType2 = 0;
-    st->nVisible = 0;  // stage 3 appends to the visible list
-  }
-  const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
-  int n = 0, n2 = 0;
-  const uint4 k4 = *reinterpret_cast<const uint4*>(m.reqKey + base);  // padded: always in bounds
-  const uint32_t ks[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (ks[j]) {
-      ++n;
-      if (entry_allocated(ld_entry(m.entries, base + j))) ++n2;
-    }
-  int2 total;
-  block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
-  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = total;
-}
+// (The per-tile request counts come from stage 1: mark_or_request counts a
+// slot's first request.)
 
 // Serve requests in ascending index order with serial-equivalent ranks.
 __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
@@ -470,7 +463,10 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
   // CTA); the in-frame consumers (integration, expected ranges) do not
   // depend on the order, and rfg_export_visible regenerates the reference's
   // ascending order (fusion.cpp:231) from the visibility bytes
-  if (threadIdx.x == 0) listBase = nvis ? atomicAdd(&m.state->nVisible, nvis) : 0;
+  if (threadIdx.x == 0) {
+    listBase = nvis ? atomicAdd(&m.state->nVisible, nvis) : 0;
+    m.tileCounts[blockIdx.x] = make_int2(0, 0);  // stage 2 is done with it: ready for the next stage 1
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < nvis; i += kTileThreads) m.visibleList[listBase + i] = vis[i];
 }
@@ -496,6 +492,7 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
   for (int j = 0; j < 4; ++j) n += ((w >> (8 * j)) & 0xFFu) ? 1 : 0;
   int2 total;
   const int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, 0), &total);
+  if (threadIdx.x == 0) m.tileCounts[blockIdx.x] = make_int2(0, 0);  // zero again for the next stage 1
   if (n == 0) return;
   int o = m.tilePrefix[blockIdx.x].x + ex.x;
 #pragma unroll
@@ -506,10 +503,9 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
 cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s) {
   dim3 g1((fa.w + 31) / 32, (fa.h + kStage1Rows - 1) / kStage1Rows);
   k_alloc_stage1<<<g1, 256, 0, s>>>(m, depth, fa);
-  k_req_count<<<m.nTiles, kTileThreads, 0, s>>>(m);
   k_req_assign<<<m.nTiles, kTileThreads, 0, s>>>(m, depth, fa);
   k_vis_count<<<m.nTiles, kTileThreads, 0, s>>>(m, fa);
-  count_launch(4);
+  count_launch(3);
   return cudaGetLastError();
 }
 

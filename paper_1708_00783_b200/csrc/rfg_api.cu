@@ -267,6 +267,7 @@ int rfg_map_clear(rfg_map* m) {
   RFG_CK(cudaMemsetAsync(d.visibility, 0, padded, s));
   RFG_CK(cudaMemsetAsync(d.marked, 0, padded, s));
   RFG_CK(cudaMemsetAsync(d.reqKey, 0, padded * 4, s));
+  RFG_CK(cudaMemsetAsync(d.tileCounts, 0, (size_t)d.nTiles * sizeof(int2), s));  // stage-1 request counts
   k_state_init<<<1, 32, 0, s>>>(d.state, (int)d.capacity, (int)d.excess);
   count_launch(5);
   RFG_CK(cudaGetLastError());
