@@ -83,6 +83,22 @@ __global__ void k_set12(float* dst, Pose12 p) {
 __global__ void k_copy12(float* dst, const float* src) {
   if (threadIdx.x < 12) dst[threadIdx.x] = src[threadIdx.x];
 }
+// A frame's results {MapState, pose (12 floats), ICP stats (8 doubles)}
+// written straight into mapped pinned host memory: one launch instead of
+// three device-to-host copies on the end-to-end path.
+struct FrameResult {
+  MapState state;
+  float pose[12];
+  double icp[8];
+};
+__global__ void k_frame_result(FrameResult* out, const MapState* st, const float* pose, const double* icp) {
+  const int t = threadIdx.x;
+  const int* s = reinterpret_cast<const int*>(st);
+  int* d = reinterpret_cast<int*>(&out->state);
+  for (int i = t; i < (int)(sizeof(MapState) / sizeof(int)); i += blockDim.x) d[i] = s[i];
+  if (t < 12) out->pose[t] = pose[t];
+  if (t < 8) out->icp[t] = icp[t];
+}
 // Gather VBA blocks (depth + colour planes) into VoxelSRgb byte layout.
 __global__ void k_export_blocks(const uint32_t* vbaD, const uint32_t* vbaC, const int* ptrs, int n, uint8_t* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * kBlock3; i += gridDim.x * blockDim.x) {
@@ -634,8 +650,7 @@ struct rfg_pipeline {
   float4* points;
   float4* normals;
   float* poses;  // [0..11] current w2c, [12..23] render pose of the last raycast
-  double* hostIcp;
-  float* hostPose;
+  FrameResult* hostResult;  // mapped pinned: k_frame_result's target
   float* viewScratch;  // unfiltered depth when cfg.bilateral
   void* pgmStage;      // pinned staging for rfg_pipeline_process_pgm
   cudaEvent_t stageFree;  // the last upload out of pgmStage has been read
@@ -748,8 +763,7 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
             // rank composes all three with one in-place collective
             cudaMalloc(&p->raycast, 3 * n * sizeof(float4)) == cudaSuccess &&
             cudaMalloc(&p->poses, 32 * sizeof(float)) == cudaSuccess &&
-            cudaMallocHost(&p->hostIcp, 8 * sizeof(double)) == cudaSuccess &&
-            cudaMallocHost(&p->hostPose, 12 * sizeof(float)) == cudaSuccess &&
+            cudaHostAlloc(&p->hostResult, sizeof(FrameResult), cudaHostAllocMapped) == cudaSuccess &&
             cudaMallocHost(&p->pgmStage, n * 2 + 16) == cudaSuccess &&
             (!cfg->bilateral || cudaMalloc(&p->viewScratch, n * 4 + 16) == cudaSuccess);
   if (!ok) {
@@ -798,8 +812,7 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   if (p->stageFree) cudaEventDestroy(p->stageFree);
   if (p->rawReady) cudaEventDestroy(p->rawReady);
   if (p->rawRead) cudaEventDestroy(p->rawRead);
-  if (p->hostIcp) cudaFreeHost(p->hostIcp);
-  if (p->hostPose) cudaFreeHost(p->hostPose);
+  if (p->hostResult) cudaFreeHost(p->hostResult);
   if (p->pgmStage) cudaFreeHost(p->pgmStage);
   if (p->map && p->map->stream == p->stream) p->map->stream = nullptr;
   if (p->stream) cudaStreamDestroy(p->stream);
@@ -869,18 +882,20 @@ int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pos
 int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34[12], double icpStats8[8]) {
   RFG_REQUIRE(p, "null pipeline");
   rfg_map* m = p->map;
-  RFG_CK(cudaMemcpyAsync(m->hostState, m->d.state, sizeof(MapState), cudaMemcpyDeviceToHost, p->stream));
-  if (poseOut34) RFG_CK(cudaMemcpyAsync(p->hostPose, p->poses, 48, cudaMemcpyDeviceToHost, p->stream));
-  if (icpStats8)
-    RFG_CK(cudaMemcpyAsync(p->hostIcp, icp_stats_ptr(m->icpOut), 64, cudaMemcpyDeviceToHost, p->stream));
+  FrameResult* dev = nullptr;
+  RFG_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), p->hostResult, 0));
+  k_frame_result<<<1, 32, 0, p->stream>>>(dev, m->d.state, p->poses, icp_stats_ptr(m->icpOut));
+  count_launch();
+  RFG_CK(cudaGetLastError());
   RFG_CK(cudaStreamSynchronize(p->stream));
+  *m->hostState = p->hostResult->state;
   if (m->hostState->error) return check_device_error(m);
   if (stats) {
     memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
     stats->visibleCount = m->hostState->nVisible;  // stage 3 appends the list; its length is the count
   }
-  if (poseOut34) memcpy(poseOut34, p->hostPose, 48);
-  if (icpStats8) memcpy(icpStats8, p->hostIcp, 64);
+  if (poseOut34) memcpy(poseOut34, p->hostResult->pose, 48);
+  if (icpStats8) memcpy(icpStats8, p->hostResult->icp, 64);
   return RFG_OK;
 }
 
