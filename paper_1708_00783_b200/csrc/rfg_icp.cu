@@ -562,6 +562,10 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrac
     __syncthreads();
     icp_run_level(ta.lv[l], partials, ta.nCta[l], g, sh, pcs, gi, tacc);
   }
+  // every CTA read renderPose before its first grid barrier; with no
+  // iteration at all (every level capped at 0) there was none, so one is
+  // needed before CTA 0 may overwrite it below (gi is the same in every CTA)
+  if (gi == 0 && ta.renderPoseOut) cg::this_grid().sync();
 #ifdef RFG_ICP_PHASES
   // kernel entry -> exit of CTA 0 (replaces the per-level slots)
   tacc[5] = gtimer() - tEntry;
