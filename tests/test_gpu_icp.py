@@ -87,3 +87,20 @@ def test_icp_degenerate_empty_depth_keeps_pose():
     pose_g, summ = F.track_depth(g.map, view, g.state, poses[0], iters=ITERS, dist=DIST)
     assert not summ.ok and summ.iterations == 0
     assert np.abs(pose_g - poses[0]).max() < 1e-6
+
+
+def test_pipeline_with_zero_tracker_iterations_keeps_pose():
+    """iters = (0, 0, 0): the tracker launch runs no iteration (and so no
+    grid barrier of its own); the frame still renders at, and hands on, the
+    seed pose."""
+    from paper_1708_00783_b200 import fusion as F
+    intr = F.Intrinsics(320, 240, 262.5, 262.5, 159.5, 119.5)
+    poses = F.orbit_trajectory(frames=100)
+    m = F.VoxelBlockMap(F.VoxelBlockMapConfig(1 << 16, 1 << 14, 1 << 16))
+    p = F.Pipeline(m, intr, F.SceneParams(), iters=(0, 0, 0))
+    for f in range(4):
+        p.process(F.synth_render(0, poses[f], intr)[0], poses[0] if f == 0 else None)
+        st, pose, icp = p.result()
+        assert icp[0] == 0  # no iteration
+        assert np.abs(pose - poses[0]).max() < 1e-6
+        assert st.visibleCount > 0
