@@ -337,7 +337,9 @@ int rfg_export_entries(rfg_map* map, int32_t* out5_host);
 /* VoxelSRgb bytes {sdf lo, sdf hi, w_depth, r, g, b, w_color, 0} of the given
  * VBA blocks (512 voxels each) */
 int rfg_export_blocks(rfg_map* map, const int32_t* ptrs_host, int n, uint8_t* out_host);
-/* visibleList (sorted entry indices) and per-entry visibility bytes
+/* visibleList in the reference's ascending entry order (fusion.cpp:231;
+ * the frame's kernels append it unordered, and this call rebuilds the order
+ * on the device from the visibility bytes) and per-entry visibility bytes
  * (nullable); returns the count in *count */
 int rfg_export_visible(rfg_map* map, int32_t* list_host, uint8_t* types_host, int32_t* count);
 int rfg_free_counts(rfg_map* map, int32_t* free_blocks, int32_t* free_excess);
