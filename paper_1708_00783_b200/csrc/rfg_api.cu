@@ -19,6 +19,8 @@ void set_error(const std::string& msg) { t_lastError = msg; }
 cudaError_t launch_build_view_full(const uint16_t* raw, const uint8_t* rgb, const Intr& in, float scale, float offset,
                                    int bilateral, int levels, int bigEndian, float* depthLevels,
                                    float* intensityLevels, float4* normals, float* scratch, cudaStream_t s);
+const void* view_pyramid_kernel();
+bool view_is_fused(int bilateral, bool normals, bool intensity, int levels);
 cudaError_t launch_bilateral(const float* in, int w, int h, float spatialSigma, float rangeSigma, float* out,
                              cudaStream_t s);
 cudaError_t launch_view_normals(const float* depth, const Intr& in, float4* out, cudaStream_t s);
@@ -658,6 +660,10 @@ struct rfg_pipeline {
   cudaEvent_t rawRead;    // pipeline stream has copied the caller's frame
   int frames;
   cudaGraphExec_t exec[2];  // [0] no tracking, [1] tracking
+  cudaGraph_t graph[2];     // kept for the view node's handle
+  cudaGraphNode_t viewNode[2];            // the k_view_pyramid node (fused view only)
+  cudaKernelNodeParams viewParams[2];     // its launch shape
+  const uint16_t* viewRaw[2];             // the raw frame it reads now
   uint64_t graphKernels[2];
   cudaEvent_t ev[7];        // stage boundaries (profile mode)
   bool tracked;             // last frame ran the tracker
@@ -705,7 +711,24 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   return cudaGetLastError();
 }
 
-int run_frame(rfg_pipeline* p, const float* pose34) {
+// Point the frame graph's view kernel at a device raw frame (no copy).
+cudaError_t set_view_raw(rfg_pipeline* p, int gi, const uint16_t* raw) {
+  if (p->viewRaw[gi] == raw) return cudaSuccess;
+  const rfg_pipeline_config& c = p->cfg;
+  const uint16_t* r = raw;
+  int w = c.intr.width, h = c.intr.height, be = c.raw_big_endian, lv = c.levels;
+  float sc = c.aff_scale, of = c.aff_offset;
+  float* out = p->depthLevels;
+  void* args[] = {&r, &w, &h, &sc, &of, &be, &lv, &out};  // k_view_pyramid's parameters
+  cudaKernelNodeParams kp = p->viewParams[gi];
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  const cudaError_t e = cudaGraphExecKernelNodeSetParams(p->exec[gi], p->viewNode[gi], &kp);
+  if (e == cudaSuccess) p->viewRaw[gi] = raw;
+  return e;
+}
+
+int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc) {
   const bool track = p->cfg.track && p->frames > 0;
   p->tracked = track;
   if (pose34) {
@@ -729,8 +752,27 @@ int run_frame(rfg_pipeline* p, const float* pose34) {
       p->graphKernels[gi] = g_launches.load() - before;
       g_launches.fetch_sub(p->graphKernels[gi]);  // capture does not launch
       RFG_CK(cudaGraphInstantiate(&p->exec[gi], g, 0));
-      cudaGraphDestroy(g);
+      p->graph[gi] = g;
+      p->viewRaw[gi] = p->rawDev;
+      if (view_is_fused(p->cfg.bilateral, false, false, p->cfg.levels)) {
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(g, nodes.data(), &nn);
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType ty;
+          cudaKernelNodeParams kp{};
+          if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel &&
+              cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == view_pyramid_kernel()) {
+            p->viewNode[gi] = nd;
+            p->viewParams[gi] = kp;
+            break;
+          }
+        }
+        cudaGetLastError();
+      }
     }
+    if (p->viewNode[gi]) RFG_CK(set_view_raw(p, gi, rawSrc));
     RFG_CK(cudaGraphLaunch(p->exec[gi], p->stream));
     count_launch(p->graphKernels[gi]);
   }
@@ -804,6 +846,8 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (int i = 0; i < 2; ++i)
     if (p->exec[i]) cudaGraphExecDestroy(p->exec[i]);
+  for (int i = 0; i < 2; ++i)
+    if (p->graph[i]) cudaGraphDestroy(p->graph[i]);
   void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->poses, p->viewScratch};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -837,7 +881,7 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw, const float* 
   RFG_REQUIRE(p && raw, "null argument");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
   if (raw != p->rawDev) RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
-  return run_frame(p, pose34);
+  return run_frame(p, pose34, p->rawDev);
 }
 
 int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const float* pose34, void* producer) {
@@ -847,18 +891,25 @@ int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const 
   // the frame is read after the producer's pending work (its upload) ...
   RFG_CK(cudaEventRecord(p->rawReady, ps));
   RFG_CK(cudaStreamWaitEvent(p->stream, p->rawReady, 0));
-  if (raw != p->rawDev) RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
-  // ... and the producer's later work (e.g. reusing the buffer) waits for the copy
+  // a captured frame graph with the fused view reads the caller's frame in
+  // place (its view node is re-pointed); otherwise the frame is copied in
+  const int gi = (p->cfg.track && p->frames > 0) ? 1 : 0;
+  const bool direct = p->cfg.use_graph && p->exec[gi] && p->viewNode[gi];
+  if (!direct && raw != p->rawDev)
+    RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
+  const int rc = run_frame(p, pose34, direct ? raw : p->rawDev);
+  // ... and the producer's later work (e.g. reusing the buffer) waits until
+  // the frame has been read
   RFG_CK(cudaEventRecord(p->rawRead, p->stream));
   RFG_CK(cudaStreamWaitEvent(ps, p->rawRead, 0));
-  return run_frame(p, pose34);
+  return rc;
 }
 
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const float* pose34) {
   RFG_REQUIRE(p && rawHost, "null argument");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
   RFG_CK(cudaMemcpyAsync(p->rawDev, rawHost, n * 2, cudaMemcpyHostToDevice, p->stream));
-  return run_frame(p, pose34);
+  return run_frame(p, pose34, p->rawDev);
 }
 
 int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pose34) {
@@ -876,7 +927,7 @@ int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pos
               "build_view: depth image size does not match calibration");
   RFG_CK(cudaMemcpyAsync(p->rawDev, p->pgmStage, (size_t)n * 2, cudaMemcpyHostToDevice, p->stream));
   RFG_CK(cudaEventRecord(p->stageFree, p->stream));
-  return run_frame(p, pose34);
+  return run_frame(p, pose34, p->rawDev);
 }
 
 int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34[12], double icpStats8[8]) {

@@ -289,6 +289,13 @@ cudaError_t launch_build_view_full(const uint16_t* raw, const uint8_t* rgb, cons
   return cudaGetLastError();
 }
 
+// The fused depth-view kernel and whether a view configuration uses it (the
+// frame graph re-points its raw-frame argument instead of copying frames).
+const void* view_pyramid_kernel() { return reinterpret_cast<const void*>(&k_view_pyramid); }
+bool view_is_fused(int bilateral, bool normals, bool intensity, int levels) {
+  return !bilateral && !normals && !intensity && levels <= 3;
+}
+
 cudaError_t launch_build_view(const uint16_t* raw, int w, int h, float scale, float offset, int levels, float* out,
                               cudaStream_t s) {
   const Intr in{w, h, 1.f, 1.f, 0.f, 0.f};
