@@ -455,6 +455,48 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_icp(DevMap m, Fram
 #endif
 }
 
+// The march and the normal of each pixel in one kernel.  A lane computes
+// its normal after its march returns, i.e. after the warp's lanes have
+// reconverged behind the longest march of the warp, so the six trilinear
+// reads of the normals run warp-uniform; and a tile's normals are done while
+// other SMs still march their long rays (the separate normals kernel could
+// only start after the longest ray of the whole image).
+__global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_maps(DevMap m, FrameArgs fa,
+                                                                   const float2* __restrict__ range,
+                                                                   float4* raycast, float4* points, float4* normals) {
+  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (x >= fa.w || y >= fa.h) return;
+  const size_t i = (size_t)y * fa.w + x;
+  const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
+  float4 rc = invalid, pt = invalid, nm = invalid;
+  const float2 r = range[i];
+  FieldReader field{m.entries, m.vbaDepth, m.buckets};
+  field.cache.reset();
+  bool isHit = false;
+  f3 hit{0.f, 0.f, 0.f};
+  if (r.y >= r.x) {
+    const Pose c2w = pose_inverse(frame_pose(fa));
+    const f3 origin{c2w.t[0], c2w.t[1], c2w.t[2]};
+    const f3 dirCam{((float)x - fa.cx) / fa.fx, ((float)y - fa.cy) / fa.fy, 1.f};
+    const float norm = sqrtf(sqnorm3(dirCam));
+    const f3 dw = rot_apply(c2w.R, dirCam);
+    const f3 dirW{dw.x / norm, dw.y / norm, dw.z / norm};
+    isHit = cast_ray(field, origin, dirW, r.x * norm, r.y * norm, fa.mu, fa.voxelSize, &hit);
+    if (isHit) {
+      rc = make_float4(hit.x, hit.y, hit.z, 1.f);
+      pt = make_float4(hit.x * fa.voxelSize, hit.y * fa.voxelSize, hit.z * fa.voxelSize, 1.f);
+    }
+  }
+  raycast[i] = rc;
+  points[i] = pt;
+  if (isHit) {
+    f3 n;
+    if (field_normal(field, hit, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
+  }
+  normals[i] = nm;
+}
+
 // Normals at every hit, in their own kernel: the six trilinear reads are
 // uniform work across the warp instead of running behind the divergent march.
 __global__ void __launch_bounds__(128, RFG_NRM_MINB) k_raycast_normals(DevMap m, FrameArgs fa, const float4* __restrict__ raycast,
@@ -687,9 +729,14 @@ cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* 
                             float4* points, float4* normals, cudaStream_t s) {
   if (!raycast) return cudaErrorInvalidValue;  // the normals pass reads the hits
   dim3 g((fa.w + 15) / 16, (fa.h + 7) / 8);
+#ifdef RFG_RC_SPLIT
   k_raycast_icp<<<g, 128, 0, s>>>(m, fa, range, raycast, points);
   k_raycast_normals<<<g, 128, 0, s>>>(m, fa, raycast, normals);
   count_launch(2);
+#else
+  k_raycast_maps<<<g, 128, 0, s>>>(m, fa, range, raycast, points, normals);
+  count_launch(1);
+#endif
   return cudaGetLastError();
 }
 

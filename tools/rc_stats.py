@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Ray-march statistics of the C2 frames (needs a RFG_RC_STATS or RFG_RC_TIMING build:
+"""Ray-march statistics of the C2 frames (needs a RFG_RC_STATS or RFG_RC_TIMING build,
+with RFG_RC_SPLIT for the timing slots of k_raycast_icp:
 RFG_LIB_PATH=.variants/stats/librfg.so)."""
 import ctypes as C
 import os
