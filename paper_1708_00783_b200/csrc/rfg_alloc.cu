@@ -218,9 +218,18 @@ __global__ void __launch_bounds__(256, 5) k_alloc_stage1(DevMap m, const float* 
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kCellSlots; i += blockDim.x) {
+  // compact the occupied slots first, so the chain probes are spread one per
+  // thread instead of trailing on the threads whose slots happen to be full
+  __shared__ int sList[kCellSlots];
+  __shared__ int nList;
+  if (threadIdx.x == 0) nList = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCellSlots; i += blockDim.x)
+    if (sCell[i]) sList[atomicAdd(&nList, 1)] = i;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nList; k += blockDim.x) {
+    const int i = sList[k];
     const unsigned long long c = sCell[i];
-    if (!c) continue;
     const i3 cell{(int)(int16_t)(c & 0xFFFFu), (int)(int16_t)((c >> 16) & 0xFFFFu), (int)(int16_t)((c >> 32) & 0xFFFFu)};
     mark_or_request(m, cell, sKey[i]);
   }
