@@ -287,7 +287,9 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const flo
 /* Enqueue one frame from HOST raw depth (copied H2D inside the call). */
 /* As rfg_pipeline_process_raw for a frame produced on another CUDA stream:
  * the pipeline reads it after the producer stream's pending work, and the
- * producer stream's later work waits until the frame has been copied. */
+ * producer stream's later work waits until the frame has been read.  Once
+ * the frame graph is captured, the frame is read in place (its view kernel
+ * is re-pointed at raw_dev) instead of being copied. */
 int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw_dev, const float pose34[12],
                                     void* producer_cuda_stream);
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* raw_host, const float* pose34);
