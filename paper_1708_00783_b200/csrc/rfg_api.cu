@@ -700,9 +700,11 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   mark(3);
   if ((e = launch_integrate(m->d, p->depthLevels, nullptr, fa, nullptr, nullptr, s)) != cudaSuccess) return e;
   mark(4);
-  if ((e = launch_ranges(m->d, fa, p->range, s)) != cudaSuccess) return e;
+  // expected ranges + ICP maps: the range tiles are reduced inside the
+  // raycast's CTAs (profile mode: "ranges" = the binning, "raycast" = the rest)
+  if ((e = launch_range_bin(m->d, fa, s)) != cudaSuccess) return e;
   mark(5);
-  if ((e = launch_icp_maps(m->d, fa, p->range, p->raycast, p->points, p->normals, s)) != cudaSuccess) return e;
+  if ((e = launch_raycast_tiles(m->d, fa, p->range, p->raycast, p->points, p->normals, s)) != cudaSuccess) return e;
   if (!track) {  // a tracked frame's next render pose was written by the tracker
     k_copy12<<<1, 32, 0, s>>>(p->poses + 12, p->poses);
     count_launch();

@@ -88,6 +88,9 @@ cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, c
 // (Re)allocate the expected-range bins for a width x height image (host call,
 // not capturable; done at pipeline creation or on first use of a size).
 int ensure_range_scratch(struct ::rfg_map* m, int width, int height);
+cudaError_t launch_range_bin(const DevMap& m, const FrameArgs& fa, cudaStream_t s);
+cudaError_t launch_raycast_tiles(const DevMap& m, const FrameArgs& fa, float2* range, float4* raycast, float4* points,
+                                 float4* normals, cudaStream_t s);
 cudaError_t launch_icp_maps(const DevMap& m, const FrameArgs& fa, const float2* range, float4* raycast,
                             float4* points, float4* normals, cudaStream_t s);
 cudaError_t launch_icp_maps_list(const DevMap& m, const FrameArgs& fa, const float2* range, const int* list,

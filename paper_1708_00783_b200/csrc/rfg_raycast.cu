@@ -101,11 +101,10 @@ __global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa) {
   }
 }
 
-__global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m, FrameArgs fa, float2* range) {
-  __shared__ int4 sb[kRangeTile * kRangeTile];
-  const int t = blockIdx.y * m.binTilesX + blockIdx.x;
-  const int x = blockIdx.x * kRangeTile + (threadIdx.x & (kRangeTile - 1));
-  const int y = blockIdx.y * kRangeTile + threadIdx.x / kRangeTile;
+// The expected range (min, max bits) of this thread's pixel of screen tile t
+// (blockIdx), from the tile's bin; every thread of the CTA must call it (it
+// synchronises the CTA), and it re-zeroes the bin count for the next frame.
+__device__ __forceinline__ int2 tile_ranges(const DevMap& m, int t, int4* sb) {
   const int count = m.binCount[t];
   const bool overflow = count > m.binCap;
   const int n = overflow ? *((volatile int*)&m.state->nVisible) : count;
@@ -137,9 +136,18 @@ __global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m,
       }
     }
   }
-  if (x < fa.w && y < fa.h) range[(size_t)y * fa.w + x] = make_float2(__int_as_float(lo), __int_as_float(hi));
   __syncthreads();
   if (threadIdx.x == 0) m.binCount[t] = 0;  // ready for the next frame
+  return make_int2(lo, hi);
+}
+
+__global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m, FrameArgs fa, float2* range) {
+  __shared__ int4 sb[kRangeTile * kRangeTile];
+  const int t = blockIdx.y * m.binTilesX + blockIdx.x;
+  const int x = blockIdx.x * kRangeTile + (threadIdx.x & (kRangeTile - 1));
+  const int y = blockIdx.y * kRangeTile + threadIdx.x / kRangeTile;
+  const int2 lh = tile_ranges(m, t, sb);
+  if (x < fa.w && y < fa.h) range[(size_t)y * fa.w + x] = make_float2(__int_as_float(lh.x), __int_as_float(lh.y));
 }
 
 #if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
@@ -461,16 +469,11 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_icp(DevMap m, Fram
 // reads of the normals run warp-uniform; and a tile's normals are done while
 // other SMs still march their long rays (the separate normals kernel could
 // only start after the longest ray of the whole image).
-__global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_maps(DevMap m, FrameArgs fa,
-                                                                   const float2* __restrict__ range,
-                                                                   float4* raycast, float4* points, float4* normals) {
-  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
-  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
-  if (x >= fa.w || y >= fa.h) return;
+__device__ __forceinline__ void raycast_and_normal(const DevMap& m, const FrameArgs& fa, int x, int y, float2 r,
+                                                   float4* raycast, float4* points, float4* normals) {
   const size_t i = (size_t)y * fa.w + x;
   const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
   float4 rc = invalid, pt = invalid, nm = invalid;
-  const float2 r = range[i];
   FieldReader field{m.entries, m.vbaDepth, m.buckets};
   field.cache.reset();
   bool isHit = false;
@@ -495,6 +498,34 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_maps(DevMap m, Fra
     if (field_normal(field, hit, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
   }
   normals[i] = nm;
+}
+
+__global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_maps(DevMap m, FrameArgs fa,
+                                                                   const float2* __restrict__ range,
+                                                                   float4* raycast, float4* points, float4* normals) {
+  const int x = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (x >= fa.w || y >= fa.h) return;
+  raycast_and_normal(m, fa, x, y, range[(size_t)y * fa.w + x], raycast, points, normals);
+}
+
+// The frame pipeline's form: one CTA per 16x16 screen tile first reduces the
+// tile's expected ranges from its bin (k_range_tile's work, the range stays
+// in a register; it is also stored for the caller), then marches its pixels
+// (warps of 16x2 pixels, as k_raycast_maps).  One launch and one pass over
+// the range image fewer.
+__global__ void __launch_bounds__(kRangeTile* kRangeTile) k_raycast_tiles(DevMap m, FrameArgs fa, float2* range,
+                                                                          float4* raycast, float4* points,
+                                                                          float4* normals) {
+  __shared__ int4 sb[kRangeTile * kRangeTile];
+  const int t = blockIdx.y * m.binTilesX + blockIdx.x;
+  const int x = blockIdx.x * kRangeTile + (threadIdx.x & (kRangeTile - 1));
+  const int y = blockIdx.y * kRangeTile + threadIdx.x / kRangeTile;
+  const int2 lh = tile_ranges(m, t, sb);
+  if (x >= fa.w || y >= fa.h) return;
+  const float2 r = make_float2(__int_as_float(lh.x), __int_as_float(lh.y));
+  range[(size_t)y * fa.w + x] = r;
+  raycast_and_normal(m, fa, x, y, r, raycast, points, normals);
 }
 
 // Normals at every hit, in their own kernel: the six trilinear reads are
@@ -722,6 +753,24 @@ cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, c
   k_range_bin<<<range_grid(), 256, 0, s>>>(m, fa);
   k_range_tile<<<dim3(tx, ty), kRangeTile * kRangeTile, 0, s>>>(m, fa, range);
   count_launch(2);
+  return cudaGetLastError();
+}
+
+// Expected ranges + ICP maps for the frame pipeline: launch_range_bin, then
+// launch_raycast_tiles (the range tiles are reduced inside the raycast's CTAs).
+cudaError_t launch_range_bin(const DevMap& m, const FrameArgs& fa, cudaStream_t s) {
+  const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
+  if (tx != m.binTilesX || ty > m.binTilesY) return cudaErrorInvalidValue;  // scratch sized by ensure_range_scratch
+  k_range_bin<<<range_grid(), 256, 0, s>>>(m, fa);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_raycast_tiles(const DevMap& m, const FrameArgs& fa, float2* range, float4* raycast, float4* points,
+                                 float4* normals, cudaStream_t s) {
+  const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
+  if (tx != m.binTilesX || ty > m.binTilesY || !raycast) return cudaErrorInvalidValue;
+  k_raycast_tiles<<<dim3(tx, ty), kRangeTile * kRangeTile, 0, s>>>(m, fa, range, raycast, points, normals);
+  count_launch();
   return cudaGetLastError();
 }
 
