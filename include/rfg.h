@@ -161,13 +161,17 @@ int rfg_allocate_from_depth_ex(rfg_map* map, const float* depth_dev, const rfg_i
  * resident, 0 VBA exhausted) and releaseBlock (voxel_block_map.cpp:107-123). */
 int rfg_map_reserve_block(rfg_map* map, int entry_index);
 int rfg_map_release_block(rfg_map* map, int entry_index);
-/* The swapping engine (rfg_swap.cu): host voxel store per
- * entry + transfer buffers of `capacity` blocks per frame and direction.
+/* The swapping engine (rfg_swap.cu): a pinned, device-mapped
+ * host slot per stored entry (the whole host tier is pinned at create when it
+ * fits 4 GiB), at most `capacity` blocks per frame and direction, copied by
+ * the GPU straight between VBA and host slots.
  * Per frame: rfg_allocate_from_depth_ex(swapping_enabled = 1) ->
  * rfg_swap_in (blocks visible but swapped out come back, ascending entry
  * index, merged into fresh VBA blocks) -> integrate / render ->
  * rfg_swap_out (blocks invisible for 2 frames go to the host, ascending
- * index).  Both synchronise the map's stream. */
+ * index).  Both wait for the device-side selection (one small readback);
+ * the block copies stay queued on the map's stream (rfg_swap_host_block
+ * synchronises before reading a slot). */
 typedef struct rfg_swap rfg_swap;
 int rfg_swap_create(rfg_map* map, int capacity_blocks, rfg_swap** out);
 int rfg_swap_destroy(rfg_swap* swap);

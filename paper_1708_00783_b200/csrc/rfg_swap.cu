@@ -3,28 +3,31 @@
 // reserveBlockForEntry / releaseBlock (voxel_block_map.cpp:107-123) and the
 // kVisibleSwapped / kBoundary visibility types (fusion.cpp:219-229).
 //
-// B200 layout: the host tier is a voxel store indexed by hash entry (depth
-// plane, + colour plane for colour maps) in host memory; transfers go through
-// one pinned host buffer and one device buffer of `capacity` blocks per
-// direction per frame (the SPEC's fixed-size transfer buffers).  Everything
+// B200 layout: the host tier is a pool of pinned, device-mapped host slots
+// (one 2 KiB slot per plane for every entry ever swapped out; the pool grows
+// in 4096-slot chunks, so only stored entries cost host memory, and pinned
+// pages never fault).  The GPU reads and writes the slots itself over PCIe:
+// there is no staging buffer and no host pass over voxel data.  Everything
 // that decides *which* blocks move runs on the device:
 //   swap-in  (after allocation, before integration): flags = visibility 2 and
 //            stored on the host; an exclusive scan gives ascending-index ranks;
-//            the first `capacity` indices go to the host, which gathers their
-//            blocks into the pinned buffer (the only host pass over voxel
-//            data), one H2D, then one warp per block pops a VBA block in the
-//            serial reserveBlockForEntry order and merges the host voxels
-//            into it (a fresh block takes the host voxel; SPEC apply_swapped_in);
+//            the first `capacity` indices come back to the host, which looks up
+//            their slots (one pointer pair per block, one small H2D), then one
+//            warp per block pops a VBA block in the serial reserveBlockForEntry
+//            order and reads the host voxels straight into it (a fresh block
+//            takes the host voxel; SPEC apply_swapped_in);
 //   swap-out (after integration): per resident entry the invisible-frame age
 //            is updated on the device; entries with age >= 2 are ranked by
-//            index, the first `capacity` are copied into the device transfer
-//            buffer and released (free-stack pushes in releaseBlock order),
-//            one D2H, and the host scatters them into the store.
+//            index, the host assigns a slot to each of the first `capacity`
+//            that has none, and one warp per block writes it straight into its
+//            host slot and releases it (free-stack pushes in releaseBlock
+//            order).
 // The result — entries, free stack, VBA, host store — is bit-identical to the
 // serial restatement (oracle/rfo.c:rfo_swap_in / rfo_swap_out).
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "rfg_common.cuh"
 
@@ -62,23 +65,25 @@ __global__ void k_swap_select(const int* __restrict__ flags, const int* __restri
 }
 
 // one warp per staged block; nFree0 = free-stack size before the swap-in
-__global__ void k_swapin_apply(DevMap m, const int* __restrict__ idx, const uint32_t* __restrict__ depthIn,
-                               const uint32_t* __restrict__ colourIn, int n, int maxW) {
+__global__ void k_swapin_apply(DevMap m, const int* __restrict__ idx, const uint64_t* __restrict__ src, int n,
+                               int maxW) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nFree0 = m.state->nFreeBlocks;
   if (k >= n || k >= nFree0) return;  // VBA exhausted: the rest stay queued
   const int ptr = m.freeBlocks[nFree0 - 1 - k];
-  uint32_t* dst = m.vbaDepth + (size_t)ptr * kBlock3;
-  const uint32_t* src = depthIn + (size_t)k * kBlock3;
-  for (int v = lane; v < kBlock3; v += 32) {
-    // reserveBlockForEntry resets the block to Voxel{} (w = 0), so the merge
-    // (SPEC apply_swapped_in) takes the host voxel
-    dst[v] = src[v];
-  }
+  // reserveBlockForEntry resets the block to Voxel{} (w = 0), so the merge
+  // (SPEC apply_swapped_in) takes the host voxel: a 16-B copy per lane from
+  // the mapped host slot (512 B per warp request over PCIe)
+  uint4* dst = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)ptr * kBlock3);
+  const uint4* hs = reinterpret_cast<const uint4*>(src[2 * k]);
+#pragma unroll
+  for (int v = lane; v < kBlock3 / 4; v += 32) dst[v] = hs[v];
   if (m.vbaColour) {
-    uint32_t* cd = m.vbaColour + (size_t)ptr * kBlock3;
-    for (int v = lane; v < kBlock3; v += 32) cd[v] = colourIn ? colourIn[(size_t)k * kBlock3 + v] : 0u;
+    uint4* cd = reinterpret_cast<uint4*>(m.vbaColour + (size_t)ptr * kBlock3);
+    const uint4* hc = reinterpret_cast<const uint4*>(src[2 * k + 1]);
+#pragma unroll
+    for (int v = lane; v < kBlock3 / 4; v += 32) cd[v] = hc ? hc[v] : make_uint4(0u, 0u, 0u, 0u);
   }
   if (lane == 0) reinterpret_cast<int*>(m.entries + idx[k])[3] = ptr;  // entry.ptr
   (void)maxW;
@@ -89,9 +94,10 @@ __global__ void k_swapin_commit(DevMap m, int n) {
   st->nFreeBlocks -= min(n, st->nFreeBlocks);
 }
 
-// one warp per selected entry: copy out, release (push in index order)
+// one warp per selected entry: copy out into its mapped host slot, release
+// (push in index order)
 __global__ void k_swapout_gather(DevMap m, const int* __restrict__ idx, const int* __restrict__ total, int cap,
-                                 uint32_t* depthOut, uint32_t* colourOut, uint8_t* has) {
+                                 const uint64_t* __restrict__ dstPtr, uint8_t* has) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int n = min(*total, cap);
@@ -102,16 +108,21 @@ __global__ void k_swapout_gather(DevMap m, const int* __restrict__ idx, const in
   // stack: allocateBlock does not clear reused blocks (voxel_block_map.cpp:
   // 74-105), and the SPEC's equivalence invariant needs a
   // swapped-out block's memory to come back clean
-  uint32_t* src = m.vbaDepth + (size_t)ptr * kBlock3;
-  for (int v = lane; v < kBlock3; v += 32) {
-    depthOut[(size_t)k * kBlock3 + v] = src[v];
-    src[v] = kDefaultDepthVoxel;
+  const uint4 dflt = make_uint4(kDefaultDepthVoxel, kDefaultDepthVoxel, kDefaultDepthVoxel, kDefaultDepthVoxel);
+  uint4* src = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)ptr * kBlock3);
+  uint4* hd = reinterpret_cast<uint4*>(dstPtr[2 * k]);
+#pragma unroll
+  for (int v = lane; v < kBlock3 / 4; v += 32) {
+    hd[v] = src[v];
+    src[v] = dflt;
   }
   if (m.vbaColour) {
-    uint32_t* cs = m.vbaColour + (size_t)ptr * kBlock3;
-    for (int v = lane; v < kBlock3; v += 32) {
-      if (colourOut) colourOut[(size_t)k * kBlock3 + v] = cs[v];
-      cs[v] = 0u;
+    uint4* cs = reinterpret_cast<uint4*>(m.vbaColour + (size_t)ptr * kBlock3);
+    uint4* hc = reinterpret_cast<uint4*>(dstPtr[2 * k + 1]);
+#pragma unroll
+    for (int v = lane; v < kBlock3 / 4; v += 32) {
+      if (hc) hc[v] = cs[v];
+      cs[v] = make_uint4(0u, 0u, 0u, 0u);
     }
   }
   if (lane == 0) {
@@ -163,8 +174,14 @@ struct rfg_swap {
   int cap = 0;
   uint32_t total = 0;
   bool colour = false;
-  // host tier (indexed by entry; pages are touched only for stored entries)
-  std::unique_ptr<uint32_t[]> hostDepth, hostColour;
+  // host tier: per entry its slot (host pointer, device alias) per plane, or
+  // null; slots come from pinned mapped chunks of kSlotChunk blocks
+  std::vector<uint32_t*> slotDepth, slotColour;
+  std::vector<uint64_t> devDepth, devColour;
+  std::vector<void*> chunks;
+  uint32_t* chunkHost[2] = {nullptr, nullptr};
+  uint64_t chunkDev[2] = {0, 0};
+  size_t chunkUsed = 0, chunkCap = 0;
   std::unique_ptr<uint8_t[]> hostHas;
   // device state
   uint8_t* hasDev = nullptr;
@@ -174,13 +191,11 @@ struct rfg_swap {
   int* tiles = nullptr;
   int* dTotal = nullptr;
   int* dIdx = nullptr;
-  uint32_t* dDepth = nullptr;
-  uint32_t* dColour = nullptr;
-  // pinned transfer buffers
+  uint64_t* dPtr = nullptr;  // per selected block: {depth slot, colour slot} device addresses
+  // pinned
   int* hIdx = nullptr;
   int* hTotal = nullptr;
-  uint32_t* hDepth = nullptr;
-  uint32_t* hColour = nullptr;
+  uint64_t* hPtr = nullptr;
 };
 
 namespace {
@@ -193,14 +208,60 @@ namespace {
     }                         \
   } while (0)
 
+// The whole host tier is pinned up front when it fits kSlotUpFront bytes (the
+// InfiniTAM global cache is one host array of every entry's block); larger
+// maps grow it in chunks of kSlotChunk slots (128 MiB per plane).  Pinning
+// costs ~ms per 10 MiB, so it is kept out of the per-frame swap-out.
+constexpr size_t kSlotUpFront = size_t(4) << 30;
+constexpr size_t kSlotChunk = 65536;
+
+int slot_chunk(rfg_swap* w, size_t slots) {
+  const size_t bytes = slots * (size_t)rfg::kBlock3 * 4;
+  for (int p = 0; p < (w->colour ? 2 : 1); ++p) {
+    void* h = nullptr;
+    void* dv = nullptr;
+    if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped) != cudaSuccess) {
+      cudaGetLastError();
+      rfg::set_error("swap host slot allocation failed");
+      return RFG_ENOMEM;
+    }
+    w->chunks.push_back(h);
+    RFG_CK(cudaHostGetDevicePointer(&dv, h, 0));
+    w->chunkHost[p] = static_cast<uint32_t*>(h);
+    w->chunkDev[p] = reinterpret_cast<uint64_t>(dv);
+  }
+  w->chunkUsed = 0;
+  w->chunkCap = slots;
+  return RFG_OK;
+}
+
 void swap_free(rfg_swap* w) {
-  void* d[] = {w->hasDev, w->age, w->flags, w->rank, w->tiles, w->dTotal, w->dIdx, w->dDepth, w->dColour};
+  void* d[] = {w->hasDev, w->age, w->flags, w->rank, w->tiles, w->dTotal, w->dIdx, w->dPtr};
   for (void* p : d)
     if (p) cudaFree(p);
-  void* h[] = {w->hIdx, w->hTotal, w->hDepth, w->hColour};
+  void* h[] = {w->hIdx, w->hTotal, w->hPtr};
   for (void* p : h)
     if (p) cudaFreeHost(p);
+  for (void* p : w->chunks) cudaFreeHost(p);
   delete w;
+}
+
+// the host slot of entry i (assigned on its first swap-out; kept for life)
+int slot_for(rfg_swap* w, size_t i) {
+  if (w->slotDepth[i]) return RFG_OK;
+  const size_t blk = (size_t)rfg::kBlock3;
+  if (w->chunkUsed == w->chunkCap) {
+    const int rc = slot_chunk(w, kSlotChunk);
+    if (rc != RFG_OK) return rc;
+  }
+  const size_t off = (size_t)w->chunkUsed++ * blk;
+  w->slotDepth[i] = w->chunkHost[0] + off;
+  w->devDepth[i] = w->chunkDev[0] + off * 4;
+  if (w->colour) {
+    w->slotColour[i] = w->chunkHost[1] + off;
+    w->devColour[i] = w->chunkDev[1] + off * 4;
+  }
+  return RFG_OK;
 }
 
 // rank the flagged entries; returns the selected count (synchronises)
@@ -229,25 +290,30 @@ int rfg_swap_create(rfg_map* m, int capacity, rfg_swap** out) {
   w->cap = capacity;
   w->total = m->d.total;
   w->colour = m->d.vbaColour != nullptr;
-  const size_t nE = w->total, blk = (size_t)rfg::kBlock3;
-  w->hostDepth.reset(new (std::nothrow) uint32_t[nE * blk]);
-  if (w->colour) w->hostColour.reset(new (std::nothrow) uint32_t[nE * blk]);
+  const size_t nE = w->total;
+  w->slotDepth.assign(nE, nullptr);
+  w->devDepth.assign(nE, 0);
+  if (w->colour) {
+    w->slotColour.assign(nE, nullptr);
+    w->devColour.assign(nE, 0);
+  }
   w->hostHas.reset(new (std::nothrow) uint8_t[nE]());
-  bool ok = w->hostDepth && w->hostHas && (!w->colour || w->hostColour);
+  bool ok = w->hostHas != nullptr;
   const long long tilesN = rfg::scan_tile_scratch_ints(nE);
   ok = ok && cudaMalloc(&w->hasDev, nE) == cudaSuccess && cudaMalloc(&w->age, nE) == cudaSuccess &&
        cudaMalloc(&w->flags, nE * 4) == cudaSuccess && cudaMalloc(&w->rank, nE * 4) == cudaSuccess &&
        cudaMalloc(&w->tiles, tilesN * 4) == cudaSuccess && cudaMalloc(&w->dTotal, 4) == cudaSuccess &&
-       cudaMalloc(&w->dIdx, capacity * 4) == cudaSuccess &&
-       cudaMalloc(&w->dDepth, (size_t)capacity * blk * 4) == cudaSuccess &&
-       (!w->colour || cudaMalloc(&w->dColour, (size_t)capacity * blk * 4) == cudaSuccess) &&
+       cudaMalloc(&w->dIdx, capacity * 4) == cudaSuccess && cudaMalloc(&w->dPtr, capacity * 16) == cudaSuccess &&
        cudaMallocHost(&w->hIdx, capacity * 4) == cudaSuccess && cudaMallocHost(&w->hTotal, 4) == cudaSuccess &&
-       cudaMallocHost(&w->hDepth, (size_t)capacity * blk * 4) == cudaSuccess &&
-       (!w->colour || cudaMallocHost(&w->hColour, (size_t)capacity * blk * 4) == cudaSuccess);
+       cudaMallocHost(&w->hPtr, capacity * 16) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     swap_free(w);
     rfg::set_error("swap allocation failed");
+    return RFG_ENOMEM;
+  }
+  if (nE * (size_t)rfg::kBlock3 * 4 * (w->colour ? 2 : 1) <= kSlotUpFront && slot_chunk(w, nE) != RFG_OK) {
+    swap_free(w);
     return RFG_ENOMEM;
   }
   cudaStream_t s = m->stream;
@@ -282,17 +348,14 @@ int rfg_swap_in(rfg_swap* w, int maxW, int* nIn) {
   const int nFree0 = m->hostState->nFreeBlocks;
   if (sel > nFree0) sel = nFree0;
   if (sel == 0) return RFG_OK;
-  // host gather: the only host pass over voxel data
-  const size_t blk = (size_t)rfg::kBlock3;
+  // the selected blocks' host slots (no host pass over voxel data)
   for (int k = 0; k < sel; ++k) {
     const size_t i = (size_t)w->hIdx[k];
-    std::memcpy(w->hDepth + k * blk, w->hostDepth.get() + i * blk, blk * 4);
-    if (w->colour) std::memcpy(w->hColour + k * blk, w->hostColour.get() + i * blk, blk * 4);
+    w->hPtr[2 * k] = w->devDepth[i];
+    w->hPtr[2 * k + 1] = w->colour ? w->devColour[i] : 0;
   }
-  RFG_CK(cudaMemcpyAsync(w->dDepth, w->hDepth, sel * blk * 4, cudaMemcpyHostToDevice, s));
-  if (w->colour) RFG_CK(cudaMemcpyAsync(w->dColour, w->hColour, sel * blk * 4, cudaMemcpyHostToDevice, s));
-  rfg::k_swapin_apply<<<(sel + 7) / 8, 256, 0, s>>>(m->d, w->dIdx, w->dDepth, w->colour ? w->dColour : nullptr,
-                                                   sel, maxW);
+  RFG_CK(cudaMemcpyAsync(w->dPtr, w->hPtr, (size_t)sel * 16, cudaMemcpyHostToDevice, s));
+  rfg::k_swapin_apply<<<(sel + 7) / 8, 256, 0, s>>>(m->d, w->dIdx, w->dPtr, sel, maxW);
   rfg::k_swapin_commit<<<1, 1, 0, s>>>(m->d, sel);
   rfg::count_launch(2);
   RFG_CK(cudaGetLastError());
@@ -312,20 +375,20 @@ int rfg_swap_out(rfg_swap* w, int* nOut) {
   if (rc != RFG_OK) return rc;
   *nOut = sel;
   if (sel == 0) return RFG_OK;
-  rfg::k_swapout_gather<<<(sel + 7) / 8, 256, 0, s>>>(m->d, w->dIdx, w->dTotal, w->cap, w->dDepth,
-                                                     w->colour ? w->dColour : nullptr, w->hasDev);
-  rfg::k_swapout_commit<<<1, 1, 0, s>>>(m->d, w->dTotal, w->cap);
-  rfg::count_launch(2);
-  const size_t blk = (size_t)rfg::kBlock3;
-  RFG_CK(cudaMemcpyAsync(w->hDepth, w->dDepth, sel * blk * 4, cudaMemcpyDeviceToHost, s));
-  if (w->colour) RFG_CK(cudaMemcpyAsync(w->hColour, w->dColour, sel * blk * 4, cudaMemcpyDeviceToHost, s));
-  RFG_CK(cudaStreamSynchronize(s));
-  for (int k = 0; k < sel; ++k) {  // host scatter into the store
+  // slots for the selected entries; the gather writes straight into them
+  for (int k = 0; k < sel; ++k) {
     const size_t i = (size_t)w->hIdx[k];
-    std::memcpy(w->hostDepth.get() + i * blk, w->hDepth + k * blk, blk * 4);
-    if (w->colour) std::memcpy(w->hostColour.get() + i * blk, w->hColour + k * blk, blk * 4);
+    rc = slot_for(w, i);
+    if (rc != RFG_OK) return rc;
+    w->hPtr[2 * k] = w->devDepth[i];
+    w->hPtr[2 * k + 1] = w->colour ? w->devColour[i] : 0;
     w->hostHas[i] = 1;
   }
+  RFG_CK(cudaMemcpyAsync(w->dPtr, w->hPtr, (size_t)sel * 16, cudaMemcpyHostToDevice, s));
+  rfg::k_swapout_gather<<<(sel + 7) / 8, 256, 0, s>>>(m->d, w->dIdx, w->dTotal, w->cap, w->dPtr, w->hasDev);
+  rfg::k_swapout_commit<<<1, 1, 0, s>>>(m->d, w->dTotal, w->cap);
+  rfg::count_launch(2);
+  RFG_CK(cudaGetLastError());
   return RFG_OK;
 }
 
@@ -365,8 +428,9 @@ int rfg_swap_export(rfg_swap* w, uint8_t* hasOut, uint8_t* ageOut) {
 int rfg_swap_host_block(rfg_swap* w, int idx, uint8_t* out4096) {
   SW_REQUIRE(w && out4096 && idx >= 0 && (uint32_t)idx < w->total, "invalid swap_host_block arguments");
   SW_REQUIRE(w->hostHas[idx], "entry has no host data");
-  const uint32_t* d = w->hostDepth.get() + (size_t)idx * rfg::kBlock3;
-  const uint32_t* c = w->colour ? w->hostColour.get() + (size_t)idx * rfg::kBlock3 : nullptr;
+  RFG_CK(cudaStreamSynchronize(w->map->stream));  // the slot is written by the swap-out kernel
+  const uint32_t* d = w->slotDepth[idx];
+  const uint32_t* c = w->colour ? w->slotColour[idx] : nullptr;
   for (int v = 0; v < rfg::kBlock3; ++v) {
     uint8_t* o = out4096 + 8 * v;
     const uint32_t dw = d[v], cw = c ? c[v] : 0u;
