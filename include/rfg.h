@@ -164,7 +164,10 @@ int rfg_map_release_block(rfg_map* map, int entry_index);
 /* The swapping engine (rfg_swap.cu): a pinned, device-mapped
  * host slot per stored entry (the whole host tier is pinned at create when it
  * fits 4 GiB), at most `capacity` blocks per frame and direction, copied by
- * the GPU straight between VBA and host slots.
+ * the GPU straight between VBA and host slots.  Larger host tiers grow in
+ * pinned chunks of 65,536 slots; the environment variables
+ * RFG_SWAP_PIN_UPFRONT (bytes) and RFG_SWAP_CHUNK_SLOTS, read at create,
+ * lower both limits.
  * Per frame: rfg_allocate_from_depth_ex(swapping_enabled = 1) ->
  * rfg_swap_in (blocks visible but swapped out come back, ascending entry
  * index, merged into fresh VBA blocks) -> integrate / render ->

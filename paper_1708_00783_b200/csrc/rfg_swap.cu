@@ -24,6 +24,7 @@
 //            order).
 // The result — entries, free stack, VBA, host store — is bit-identical to the
 // serial restatement (oracle/rfo.c:rfo_swap_in / rfo_swap_out).
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -181,7 +182,7 @@ struct rfg_swap {
   std::vector<void*> chunks;
   uint32_t* chunkHost[2] = {nullptr, nullptr};
   uint64_t chunkDev[2] = {0, 0};
-  size_t chunkUsed = 0, chunkCap = 0;
+  size_t chunkUsed = 0, chunkCap = 0, chunkSlots = 0;
   std::unique_ptr<uint8_t[]> hostHas;
   // device state
   uint8_t* hasDev = nullptr;
@@ -212,8 +213,18 @@ namespace {
 // InfiniTAM global cache is one host array of every entry's block); larger
 // maps grow it in chunks of kSlotChunk slots (128 MiB per plane).  Pinning
 // costs ~ms per 10 MiB, so it is kept out of the per-frame swap-out.
+// Both limits can be lowered through the environment (RFG_SWAP_PIN_UPFRONT
+// bytes, RFG_SWAP_CHUNK_SLOTS) so the tests can drive the chunked growth.
 constexpr size_t kSlotUpFront = size_t(4) << 30;
 constexpr size_t kSlotChunk = 65536;
+
+size_t env_size(const char* name, size_t dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  char* end = nullptr;
+  const unsigned long long x = std::strtoull(v, &end, 10);
+  return (end && *end == 0) ? (size_t)x : dflt;
+}
 
 int slot_chunk(rfg_swap* w, size_t slots) {
   const size_t bytes = slots * (size_t)rfg::kBlock3 * 4;
@@ -251,7 +262,7 @@ int slot_for(rfg_swap* w, size_t i) {
   if (w->slotDepth[i]) return RFG_OK;
   const size_t blk = (size_t)rfg::kBlock3;
   if (w->chunkUsed == w->chunkCap) {
-    const int rc = slot_chunk(w, kSlotChunk);
+    const int rc = slot_chunk(w, w->chunkSlots);
     if (rc != RFG_OK) return rc;
   }
   const size_t off = (size_t)w->chunkUsed++ * blk;
@@ -312,7 +323,10 @@ int rfg_swap_create(rfg_map* m, int capacity, rfg_swap** out) {
     rfg::set_error("swap allocation failed");
     return RFG_ENOMEM;
   }
-  if (nE * (size_t)rfg::kBlock3 * 4 * (w->colour ? 2 : 1) <= kSlotUpFront && slot_chunk(w, nE) != RFG_OK) {
+  w->chunkSlots = env_size("RFG_SWAP_CHUNK_SLOTS", kSlotChunk);
+  if (w->chunkSlots == 0) w->chunkSlots = kSlotChunk;
+  const size_t upFront = env_size("RFG_SWAP_PIN_UPFRONT", kSlotUpFront);
+  if (nE * (size_t)rfg::kBlock3 * 4 * (w->colour ? 2 : 1) <= upFront && slot_chunk(w, nE) != RFG_OK) {
     swap_free(w);
     return RFG_ENOMEM;
   }

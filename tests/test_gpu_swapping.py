@@ -15,8 +15,11 @@ from test_oracle_swapping import CFG, ORDER, _frames, _params, _same_state
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cap", [37, 100000])
-def test_swapping_engine_bit_exact_vs_oracle(cap):
+@pytest.mark.parametrize("cap,chunked", [(37, False), (100000, False), (37, True)])
+def test_swapping_engine_bit_exact_vs_oracle(cap, chunked, monkeypatch):
+    if chunked:  # host tier grown in 64-slot pinned chunks instead of pinned up front
+        monkeypatch.setenv("RFG_SWAP_PIN_UPFRONT", "0")
+        monkeypatch.setenv("RFG_SWAP_CHUNK_SLOTS", "64")
     intr, pd = small_intr(), _params()
     g, o = GpuEngine(*CFG), rfo.OracleEngine(*CFG)
     for e in (g, o):
