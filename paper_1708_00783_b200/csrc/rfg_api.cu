@@ -910,6 +910,16 @@ int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const 
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const float* pose34) {
   RFG_REQUIRE(p && rawHost, "null argument");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
+  // a pinned (device-mapped) host frame is read over PCIe by the captured
+  // graph's view kernel itself — no separate DMA and no copy->graph gap;
+  // pageable frames, and frames before the graph exists, are copied in
+  const int gi = (p->cfg.track && p->frames > 0) ? 1 : 0;
+  if (p->cfg.use_graph && p->exec[gi] && p->viewNode[gi]) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, rawHost) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer)
+      return run_frame(p, pose34, static_cast<const uint16_t*>(a.devicePointer));
+    cudaGetLastError();
+  }
   RFG_CK(cudaMemcpyAsync(p->rawDev, rawHost, n * 2, cudaMemcpyHostToDevice, p->stream));
   return run_frame(p, pose34, p->rawDev);
 }

@@ -112,3 +112,33 @@ def test_pipeline_ragged_graph_equals_step_calls():
     assert np.array_equal(e1, g.entries())
     ptrs = e1[e1[:, 4] >= 0, 4]
     assert np.array_equal(m1.blocks(ptrs), g.blocks(ptrs))
+
+
+def test_pipeline_pinned_host_frames_equal_device_frames():
+    """rfg_pipeline_process_host reads a pinned host frame in place (the
+    graph's view node is pointed at its device alias), a pageable frame is
+    copied in: both, with tracking on, give the device-frame pipeline's map,
+    pose and tracker summary bit for bit."""
+    import torch
+    from paper_1708_00783_b200 import fusion as F
+    fi = F.Intrinsics(**_intr(160, 120))
+    params = F.SceneParams(voxelSize=0.01)
+    cfg = F.VoxelBlockMapConfig(1 << 13, 1 << 12, 1 << 13)
+    poses = F.orbit_trajectory(frames=100)
+    raws = [F.synth_render(0, poses[2 * f], fi)[0] for f in range(8)]
+    outs = []
+    for mode in ("device", "pinned", "pageable"):
+        m = F.VoxelBlockMap(cfg)
+        p = F.Pipeline(m, fi, params, levels=2, track=True, use_graph=True)
+        res = []
+        for f, r in enumerate(raws):
+            t = torch.from_numpy(r.view(np.int16))
+            src = t.cuda() if mode == "device" else (t.pin_memory().numpy().view(np.uint16) if mode == "pinned" else r)
+            p.process(src, poses[0] if f == 0 else None)
+            st, pose, icp = p.result()
+            res.append((np.asarray(pose).copy(), np.asarray(icp).copy(), str(st)))
+        outs.append((res, m.entries()))
+    for res, ent in outs[1:]:
+        assert np.array_equal(ent, outs[0][1])
+        for (pa, ia, sa), (pb, ib, sb) in zip(res, outs[0][0]):
+            assert np.array_equal(pa, pb) and np.array_equal(ia, ib) and sa == sb
