@@ -390,10 +390,12 @@ int rfg_swap_out(rfg_swap* w, int* nOut) {
   *nOut = sel;
   if (sel == 0) return RFG_OK;
   // slots for the selected entries; the gather writes straight into them
+  for (int k = 0; k < sel; ++k) {  // may fail (ENOMEM) before anything moved
+    rc = slot_for(w, (size_t)w->hIdx[k]);
+    if (rc != RFG_OK) return rc;
+  }
   for (int k = 0; k < sel; ++k) {
     const size_t i = (size_t)w->hIdx[k];
-    rc = slot_for(w, i);
-    if (rc != RFG_OK) return rc;
     w->hPtr[2 * k] = w->devDepth[i];
     w->hPtr[2 * k + 1] = w->colour ? w->devColour[i] : 0;
     w->hostHas[i] = 1;
