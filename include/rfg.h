@@ -291,7 +291,6 @@ int rfg_pipeline_destroy(rfg_pipeline* p);
  * used when tracking is off or for the first frame; NULL keeps the device
  * pose.  Asynchronous. */
 int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const float* pose34);
-/* Enqueue one frame from HOST raw depth (copied H2D inside the call). */
 /* As rfg_pipeline_process_raw for a frame produced on another CUDA stream:
  * the pipeline reads it after the producer stream's pending work, and the
  * producer stream's later work waits until the frame has been read.  Once
@@ -299,12 +298,18 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const flo
  * is re-pointed at raw_dev) instead of being copied. */
 int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw_dev, const float pose34[12],
                                     void* producer_cuda_stream);
+/* Enqueue one frame from HOST raw depth.  A pageable frame is copied H2D
+ * (asynchronously from the caller's view only once the copy has been
+ * staged by the driver); a pinned (cudaHostAlloc / cudaHostRegister) frame is
+ * read in place over PCIe by the captured frame graph's view kernel, so —
+ * as with any asynchronous copy from pinned memory — the caller keeps the
+ * buffer unchanged until rfg_pipeline_result returns. */
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* raw_host, const float* pose34);
-/* Read back the last frame's stats and pose (synchronises). */
 /* One frame straight from a PGM16 file (image_io.cpp:96-113): the payload is
  * read into pinned staging and uploaded as stored; with raw_big_endian = 1
  * the GPU view stage decodes it (no host pass over the pixels). */
 int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float pose34[12]);
+/* Read back the last frame's stats, pose and tracker summary (synchronises). */
 int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float pose_out34[12], double icp_stats8[8]);
 /* Device pointers of the pipeline's buffers (for parity checks). */
 int rfg_pipeline_buffers(rfg_pipeline* p, float** depth_levels, float** range, float** raycast, float** points,
