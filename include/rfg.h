@@ -299,8 +299,7 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const flo
 int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw_dev, const float pose34[12],
                                     void* producer_cuda_stream);
 /* Enqueue one frame from HOST raw depth.  A pageable frame is copied H2D
- * (asynchronously from the caller's view only once the copy has been
- * staged by the driver); a pinned (cudaHostAlloc / cudaHostRegister) frame is
+ * (its buffer may be reused once the call returns); a pinned (cudaHostAlloc / cudaHostRegister) frame is
  * read in place over PCIe by the captured frame graph's view kernel, so —
  * as with any asynchronous copy from pinned memory — the caller keeps the
  * buffer unchanged until rfg_pipeline_result returns. */
