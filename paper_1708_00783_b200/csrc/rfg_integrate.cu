@@ -373,13 +373,16 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
   }
 }
 
+#ifndef RFG_INT_GRID_PER_SM
+#define RFG_INT_GRID_PER_SM 8
+#endif
 int integrate_grid() {
   static int grid = 0;
   if (!grid) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = sms * 8;  // 8 CTAs x 8 warps per SM
+    grid = sms * RFG_INT_GRID_PER_SM;  // two waves of 4 resident CTAs x 8 warps per SM
   }
   return grid;
 }
