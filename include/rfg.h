@@ -244,23 +244,40 @@ int rfg_write_ppm(const char* path, const uint8_t* rgb, int width, int height);
 
 /* ----------------------------------------------------------------- ICP */
 /* Point-to-plane ICP tracker (ITMDepthTracker; absent in the reference, see
- * DESIGN.md "ICP oracle" and SPEC.md:348-356).  depth_levels_dev as produced
+ * DESIGN.md "ICP oracle" and SPEC.md:333-356).  depth_levels_dev as produced
  * by rfg_build_view_depth; points/normals_dev and render_pose34 describe the
  * previous ICP-map render at level-0 resolution.  iters[3] per level (level 0
- * = finest), dist[3] outlier gates (m).  pose_out34 = tracked world->camera.
- * stats8 = {iterations, count, sum r^2, converged, it_l0, it_l1, it_l2, ok}. */
+ * = finest), dist[3] outlier gates (m, in (0, 2]).  pose_out34 = tracked
+ * world->camera; a degenerate Hessian (det(H/n) < 1e-12) returns
+ * init_pose34 with ok = 0.  stats12 = TrackerIterationSummary
+ * of the last evaluation, indexed by RFG_ICP_*: iterations, inliers,
+ * sum r^2, converged, iterations per level x3, ok, inlier_fraction,
+ * hessian_det (det(H/n)), residual_mean (sum |r| / inliers), valid pixels.
+ * The sums are fixed-point integers (bit-identical to the CPU oracle); a
+ * world point with a coordinate beyond +-128 m returns RFG_ERANGE. */
+#define RFG_ICP_STATS 12
+#define RFG_ICP_SUMS 31
+enum {
+  RFG_ICP_ITERATIONS = 0, RFG_ICP_COUNT = 1, RFG_ICP_RESIDUAL_SUM = 2, RFG_ICP_CONVERGED = 3, RFG_ICP_IT_L0 = 4,
+  RFG_ICP_IT_L1 = 5, RFG_ICP_IT_L2 = 6, RFG_ICP_OK = 7, RFG_ICP_INLIER_FRACTION = 8, RFG_ICP_HESSIAN_DET = 9,
+  RFG_ICP_RESIDUAL_MEAN = 10, RFG_ICP_VALID = 11
+};
 int rfg_icp_track(rfg_map* map, const float* depth_levels_dev, int levels, const rfg_intrinsics* intr,
                   const float* points_dev, const float* normals_dev, const float render_pose34[12],
                   const float init_pose34[12], const int iters[3], const float dist[3], int min_count,
-                  float pose_out34[12], double stats8[8]);
-/* One evaluation of the 29 normal-equation sums (H upper 21, g 6, sum r^2,
- * count) at pyramid level `level` for camera->world pose cam_to_world34. */
+                  float pose_out34[12], double stats12[RFG_ICP_STATS]);
+/* One evaluation of the 31 normal-equation sums (H upper 21, g 6, sum r^2,
+ * inliers, sum |r|, valid pixels) at pyramid level `level` for camera->world
+ * pose cam_to_world34: fixed31 = the fixed-point integers (H 2^-32, g 2^-38,
+ * r^2 and |r| 2^-44 units, counts), out31 = decoded doubles; either may be
+ * NULL. */
 int rfg_icp_reduce(rfg_map* map, const float* depth_level_dev, int level, const rfg_intrinsics* intr,
                    const float* points_dev, const float* normals_dev, const float render_pose34[12],
-                   const float cam_to_world34[12], float dist, double out29[29]);
+                   const float cam_to_world34[12], float dist, int64_t fixed31[RFG_ICP_SUMS],
+                   double out31[RFG_ICP_SUMS]);
 
 /* Tracker phase timers of CTA 0 (ns, accumulated since the last reset):
- * {associate + block reduce, grid barrier wait, final sum, solve,
+ * {associate + block reduce + atomics, grid barrier wait, read totals, solve,
  *  iterations, 0, 0, 0}.  Synchronises the map's stream. */
 int rfg_icp_timers(rfg_map* map, uint64_t out8[8], int reset);
 
@@ -283,6 +300,11 @@ typedef struct {
   int32_t profile;         /* record CUDA events between stages (graph mode: event-record nodes) */
   int32_t bilateral;       /* ViewBuildOptions::bilateral (view.hpp:13) */
   int32_t raw_big_endian;  /* raw frames are PGM16 payloads (decoded in the view stage) */
+  /* ITMVoxel_s_rgb colour fusion (BASELINE configs[2]): the map must have a
+   * colour plane and frames come with an RGB8 image (rfg_pipeline_process_rgbd_*) */
+  int32_t colour;
+  rfg_intrinsics intr_rgb;        /* RgbdCalib::intrinsics_rgb */
+  float extr_d_to_rgb[12];        /* RgbdCalib::extrinsics_d_to_rgb (row-major 3x4) */
 } rfg_pipeline_config;
 
 int rfg_pipeline_create(rfg_map* map, const rfg_pipeline_config* cfg, rfg_pipeline** out);
@@ -304,12 +326,22 @@ int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw_dev, co
  * as with any asynchronous copy from pinned memory — the caller keeps the
  * buffer unchanged until rfg_pipeline_result returns. */
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* raw_host, const float* pose34);
+/* RGB-D frames of a colour pipeline (cfg.colour = 1): depth as in
+ * rfg_pipeline_process_raw_stream / _host plus the RGB8 image (width x height
+ * x 3 bytes, intr_rgb's size), read in place by the captured graph's colour
+ * packing kernel (device, or pinned host memory over PCIe). */
+int rfg_pipeline_process_rgbd_stream(rfg_pipeline* p, const uint16_t* raw_dev, const uint8_t* rgb_dev,
+                                     const float pose34[12], void* producer_cuda_stream);
+int rfg_pipeline_process_rgbd_host(rfg_pipeline* p, const uint16_t* raw_host, const uint8_t* rgb_host,
+                                   const float pose34[12]);
 /* One frame straight from a PGM16 file (image_io.cpp:96-113): the payload is
  * read into pinned staging and uploaded as stored; with raw_big_endian = 1
  * the GPU view stage decodes it (no host pass over the pixels). */
 int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float pose34[12]);
-/* Read back the last frame's stats, pose and tracker summary (synchronises). */
-int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float pose_out34[12], double icp_stats8[8]);
+/* Read back the last frame's stats, pose and tracker summary (RFG_ICP_STATS
+ * doubles, see rfg_icp_track; synchronises). */
+int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float pose_out34[12],
+                        double icp_stats[RFG_ICP_STATS]);
 /* Device pointers of the pipeline's buffers (for parity checks). */
 int rfg_pipeline_buffers(rfg_pipeline* p, float** depth_levels, float** range, float** raycast, float** points,
                          float** normals);

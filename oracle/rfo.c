@@ -10,6 +10,14 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <pthread.h>
+
+/* Threads for the per-pixel raycast loops (rfo_set_threads).  Default 1: the
+ * oracle is a single-threaded restatement; tests may raise it to shorten long
+ * parity runs.  Every pixel is independent and reads the map only, so the
+ * output does not depend on the thread count. */
+static int g_threads = 1;
+void rfo_set_threads(int n) { g_threads = n > 0 ? n : 1; }
 
 typedef struct {
   float x, y, z;
@@ -740,51 +748,113 @@ static int field_normal(const rfo_map* m, v3 h, v3* n) {
   return 1;
 }
 
+/* One pixel of render_maps_field (proj/include/rf/raycast.hpp:157-207, mode
+ * kIcpMaps): the doPixel lambda. */
+typedef struct {
+  const rfo_map* m;
+  intr_t in;
+  params_t s;
+  pose_t c2w;
+  v3 origin;
+  const int* list; /* NULL: every pixel, row-major; else (x, y) pairs */
+  float *raycast, *points, *normals;
+} icp_job_t;
+
+static void icp_pixel(const icp_job_t* j, int x, int y) {
+  const rfo_map* m = j->m;
+  const intr_t in = j->in;
+  size_t i = (size_t)y * in.w + x;
+  float* rc = j->raycast + 4 * i;
+  float* pt = j->points + 4 * i;
+  float* nm = j->normals + 4 * i;
+  rc[0] = rc[1] = rc[2] = 0.f;
+  rc[3] = -1.f;
+  pt[0] = pt[1] = pt[2] = 0.f;
+  pt[3] = -1.f;
+  nm[0] = nm[1] = nm[2] = 0.f;
+  nm[3] = -1.f;
+  float r0 = m->range[2 * i], r1 = m->range[2 * i + 1];
+  if (!(r1 >= r0)) return;
+  v3 dirCam = {((float)x - in.cx) / in.fx, ((float)y - in.cy) / in.fy, 1.f};
+  float norm = sqrtf(sqnorm3(dirCam));
+  v3 dw = rot_apply(j->c2w.R, dirCam);
+  v3 dirW = {dw.x / norm, dw.y / norm, dw.z / norm};
+  v3 hit;
+  if (!cast_ray(m, j->origin, dirW, r0 * norm, r1 * norm, j->s.mu, j->s.voxelSize, &hit)) return;
+  rc[0] = hit.x;
+  rc[1] = hit.y;
+  rc[2] = hit.z;
+  rc[3] = 1.f;
+  pt[0] = hit.x * j->s.voxelSize;
+  pt[1] = hit.y * j->s.voxelSize;
+  pt[2] = hit.z * j->s.voxelSize;
+  pt[3] = 1.f;
+  v3 n;
+  if (field_normal(m, hit, &n)) {
+    nm[0] = n.x;
+    nm[1] = n.y;
+    nm[2] = n.z;
+    nm[3] = 1.f;
+  }
+}
+
+/* The pixels are split into chunks handed out by an atomic counter to
+ * g_threads workers (each pixel is independent and reads the map only). */
+typedef struct {
+  const icp_job_t* job;
+  int n, chunk;
+  int next; /* atomic */
+} icp_pool_t;
+
+static void icp_run_item(const icp_job_t* j, int k) {
+  if (j->list)
+    icp_pixel(j, j->list[2 * k], j->list[2 * k + 1]);
+  else
+    icp_pixel(j, k % j->in.w, k / j->in.w);
+}
+
+static void* icp_worker(void* arg) {
+  icp_pool_t* p = (icp_pool_t*)arg;
+  for (;;) {
+    const int k0 = __atomic_fetch_add(&p->next, p->chunk, __ATOMIC_RELAXED);
+    if (k0 >= p->n) break;
+    const int k1 = k0 + p->chunk < p->n ? k0 + p->chunk : p->n;
+    for (int k = k0; k < k1; ++k) icp_run_item(p->job, k);
+  }
+  return NULL;
+}
+
+static void icp_run(const icp_job_t* j, int n) {
+  if (g_threads <= 1) {
+    for (int k = 0; k < n; ++k) icp_run_item(j, k);
+    return;
+  }
+  icp_pool_t pool = {j, n, 256, 0};
+  pthread_t th[256];
+  const int nt = g_threads < 256 ? g_threads : 256;
+  int started = 0;
+  for (int t = 1; t < nt; ++t)
+    if (pthread_create(&th[started], NULL, icp_worker, &pool) == 0) ++started;
+  icp_worker(&pool);
+  for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+}
+
 /* render_maps_field proj/include/rf/raycast.hpp:157-207, mode kIcpMaps */
 int rfo_render_icp(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
                    float* raycastOut, float* pointsOut, float* normalsOut) {
-  intr_t in = intr_from(wh, f4);
-  params_t s = params_from(params6);
+  icp_job_t j;
+  j.m = m;
+  j.in = intr_from(wh, f4);
+  j.s = params_from(params6);
   pose_t pose = pose_from12(pose12);
-  pose_t c2w = pose_inverse(&pose);
-  v3 origin = {c2w.t[0], c2w.t[1], c2w.t[2]};
-  if (m->rangeW != in.w || m->rangeH != in.h) return -1;
-  for (int y = 0; y < in.h; ++y)
-    for (int x = 0; x < in.w; ++x) {
-      size_t i = (size_t)y * in.w + x;
-      float* rc = raycastOut + 4 * i;
-      float* pt = pointsOut + 4 * i;
-      float* nm = normalsOut + 4 * i;
-      rc[0] = rc[1] = rc[2] = 0.f;
-      rc[3] = -1.f;
-      pt[0] = pt[1] = pt[2] = 0.f;
-      pt[3] = -1.f;
-      nm[0] = nm[1] = nm[2] = 0.f;
-      nm[3] = -1.f;
-      float r0 = m->range[2 * i], r1 = m->range[2 * i + 1];
-      if (!(r1 >= r0)) continue;
-      v3 dirCam = {((float)x - in.cx) / in.fx, ((float)y - in.cy) / in.fy, 1.f};
-      float norm = sqrtf(sqnorm3(dirCam));
-      v3 dw = rot_apply(c2w.R, dirCam);
-      v3 dirW = {dw.x / norm, dw.y / norm, dw.z / norm};
-      v3 hit;
-      if (!cast_ray(m, origin, dirW, r0 * norm, r1 * norm, s.mu, s.voxelSize, &hit)) continue;
-      rc[0] = hit.x;
-      rc[1] = hit.y;
-      rc[2] = hit.z;
-      rc[3] = 1.f;
-      pt[0] = hit.x * s.voxelSize;
-      pt[1] = hit.y * s.voxelSize;
-      pt[2] = hit.z * s.voxelSize;
-      pt[3] = 1.f;
-      v3 n;
-      if (field_normal(m, hit, &n)) {
-        nm[0] = n.x;
-        nm[1] = n.y;
-        nm[2] = n.z;
-        nm[3] = 1.f;
-      }
-    }
+  j.c2w = pose_inverse(&pose);
+  j.origin = (v3){j.c2w.t[0], j.c2w.t[1], j.c2w.t[2]};
+  j.list = NULL;
+  j.raycast = raycastOut;
+  j.points = pointsOut;
+  j.normals = normalsOut;
+  if (m->rangeW != j.in.w || m->rangeH != j.in.h) return -1;
+  icp_run(&j, j.in.w * j.in.h);
   return 0;
 }
 
@@ -793,48 +863,19 @@ int rfo_render_icp(rfo_map* m, const float* pose12, const int* wh, const float* 
  * values. */
 int rfo_render_icp_list(rfo_map* m, const float* pose12, const int* wh, const float* f4, const float* params6,
                         const int* missingXY, int n, float* raycastOut, float* pointsOut, float* normalsOut) {
-  intr_t in = intr_from(wh, f4);
-  params_t s = params_from(params6);
+  icp_job_t j;
+  j.m = m;
+  j.in = intr_from(wh, f4);
+  j.s = params_from(params6);
   pose_t pose = pose_from12(pose12);
-  pose_t c2w = pose_inverse(&pose);
-  v3 origin = {c2w.t[0], c2w.t[1], c2w.t[2]};
-  if (m->rangeW != in.w || m->rangeH != in.h) return -1;
-  for (int k = 0; k < n; ++k) {
-    const int x = missingXY[2 * k], y = missingXY[2 * k + 1];
-    size_t i = (size_t)y * in.w + x;
-    float* rc = raycastOut + 4 * i;
-    float* pt = pointsOut + 4 * i;
-    float* nm = normalsOut + 4 * i;
-    rc[0] = rc[1] = rc[2] = 0.f;
-    rc[3] = -1.f;
-    pt[0] = pt[1] = pt[2] = 0.f;
-    pt[3] = -1.f;
-    nm[0] = nm[1] = nm[2] = 0.f;
-    nm[3] = -1.f;
-    float r0 = m->range[2 * i], r1 = m->range[2 * i + 1];
-    if (!(r1 >= r0)) continue;
-    v3 dirCam = {((float)x - in.cx) / in.fx, ((float)y - in.cy) / in.fy, 1.f};
-    float norm = sqrtf(sqnorm3(dirCam));
-    v3 dw = rot_apply(c2w.R, dirCam);
-    v3 dirW = {dw.x / norm, dw.y / norm, dw.z / norm};
-    v3 hit;
-    if (!cast_ray(m, origin, dirW, r0 * norm, r1 * norm, s.mu, s.voxelSize, &hit)) continue;
-    rc[0] = hit.x;
-    rc[1] = hit.y;
-    rc[2] = hit.z;
-    rc[3] = 1.f;
-    pt[0] = hit.x * s.voxelSize;
-    pt[1] = hit.y * s.voxelSize;
-    pt[2] = hit.z * s.voxelSize;
-    pt[3] = 1.f;
-    v3 nrm;
-    if (field_normal(m, hit, &nrm)) {
-      nm[0] = nrm.x;
-      nm[1] = nrm.y;
-      nm[2] = nrm.z;
-      nm[3] = 1.f;
-    }
-  }
+  j.c2w = pose_inverse(&pose);
+  j.origin = (v3){j.c2w.t[0], j.c2w.t[1], j.c2w.t[2]};
+  j.list = missingXY;
+  j.raycast = raycastOut;
+  j.points = pointsOut;
+  j.normals = normalsOut;
+  if (m->rangeW != j.in.w || m->rangeH != j.in.h) return -1;
+  icp_run(&j, n);
   return 0;
 }
 
@@ -1521,21 +1562,47 @@ int rfo_build_view_full(const uint16_t* raw, const uint8_t* rgb, const int* wh, 
 }
 
 /* ---------------------------------------------------------------- ICP */
-/* One evaluation of the point-to-plane normal equations:
- * per valid pixel p of the level, p_w = T_cw p_cam; project p_w into the last
- * render (nearest pixel); V, N = render point/normal; reject invalid maps and
+/* Point-to-plane ICP depth tracker (absent in the reference; restated from
+ * DESIGN.md §5 "ICP oracle").
+ *
+ * One evaluation of the normal equations: per valid pixel p
+ * of the level, p_w = T_cw p_cam; project p_w into the last render (nearest
+ * pixel); V, N = render point/normal; reject invalid maps and
  * |p_w - V| > dist; r = (p_w - V).N; J = [p_w x N; N] (left-multiplied
- * world-frame twist [omega; nu]).  Sums accumulate in double, row-major
- * pixel order. */
-static void icp_accumulate(const float* depth, int lw, int lh, const intr_t* inl, const float* points,
-                           const float* normals, const intr_t* inr, const pose_t* renderPose, const pose_t* c2w,
-                           float dist, double* acc29) {
-  memset(acc29, 0, sizeof(double) * 29);
+ * world-frame twist [omega; nu]).
+ *
+ * The sums are FIXED-POINT integers: every per-pixel term (a product of two
+ * floats, exact in double) is scaled by a power of two and floored to an
+ * int64, and the int64 terms are summed.  Integer addition is associative, so
+ * the sums do not depend on the summation order: the GPU's tree/atomic
+ * reduction yields exactly these sums, and the whole tracker (solve, SE(3)
+ * update, convergence test) is bit-identical between this oracle and the B200.
+ *   S[0..20]  H upper, row-major   floor(J_a J_b 2^32)
+ *   S[21..26] g                    floor(J_a r   2^38)
+ *   S[27]     sum r^2              floor(r^2     2^44)
+ *   S[28]     inliers (count)
+ *   S[29]     sum |r|              floor(|r|     2^44)
+ *   S[30]     valid depth pixels of the level
+ * Range: |p_w| components < 128 m (so |J_a J_b| < 2^16) and gates <= 2 m;
+ * a term outside the range fails the evaluation (RFO_ICP_ERANGE). */
+#define ICP_SUMS 31
+#define RFO_ICP_ERANGE (-2)
+static const int kIcpShift[ICP_SUMS] = {32, 32, 32, 32, 32, 32, 32, 32, 32, 32, 32, 32, 32, 32, 32, 32,
+                                        32, 32, 32, 32, 32, 38, 38, 38, 38, 38, 38, 44, 0,  44, 0};
+
+static int64_t icp_fixed(double x, int shift) { return (int64_t)floor(ldexp(x, shift)); }
+
+static int icp_accumulate(const float* depth, int lw, int lh, const intr_t* inl, const float* points,
+                          const float* normals, const intr_t* inr, const pose_t* renderPose, const pose_t* c2w,
+                          float dist, int64_t* S) {
+  memset(S, 0, sizeof(int64_t) * ICP_SUMS);
   const float dist2 = dist * dist;
+  int err = 0;
   for (int y = 0; y < lh; ++y)
     for (int x = 0; x < lw; ++x) {
       float d = depth[(size_t)y * lw + x];
       if (!(d > 0.f)) continue;
+      S[30] += 1;
       v3 pc = backproject(inl, (float)x, (float)y, d);
       v3 pw = pose_apply(c2w, pc);
       v3 q = pose_apply(renderPose, pw);
@@ -1549,6 +1616,7 @@ static void icp_accumulate(const float* depth, int lw, int lh, const intr_t* inl
       if (!(V[3] > 0.f) || !(N[3] > 0.f)) continue;
       v3 diff = {pw.x - V[0], pw.y - V[1], pw.z - V[2]};
       if (sqnorm3(diff) > dist2) continue;
+      if (!(fabsf(pw.x) < 128.f && fabsf(pw.y) < 128.f && fabsf(pw.z) < 128.f)) err = 1;
       v3 n = {N[0], N[1], N[2]};
       float r = dot3(diff, n);
       v3 pxn = cross3(pw, n);
@@ -1556,23 +1624,33 @@ static void icp_accumulate(const float* depth, int lw, int lh, const intr_t* inl
       double rd = r;
       int k = 0;
       for (int a = 0; a < 6; ++a)
-        for (int b = a; b < 6; ++b) acc29[k++] += J[a] * J[b];
-      for (int a = 0; a < 6; ++a) acc29[21 + a] += J[a] * rd;
-      acc29[27] += rd * rd;
-      acc29[28] += 1.0;
+        for (int b = a; b < 6; ++b, ++k) S[k] += icp_fixed(J[a] * J[b], 32);
+      for (int a = 0; a < 6; ++a) S[21 + a] += icp_fixed(J[a] * rd, 38);
+      S[27] += icp_fixed(rd * rd, 44);
+      S[28] += 1;
+      S[29] += icp_fixed(fabs(rd), 44);
     }
+  return err ? RFO_ICP_ERANGE : 0;
+}
+
+/* The fixed-point sums as doubles (round to nearest, exact power-of-two scaling). */
+static void icp_decode(const int64_t* S, double* out) {
+  for (int k = 0; k < ICP_SUMS; ++k) out[k] = ldexp((double)S[k], -kIcpShift[k]);
 }
 
 int rfo_icp_reduce(const float* depth, int lw, int lh, const float* f4l, const float* points, const float* normals,
                    const int* wh, const float* renderPose12, const float* renderF4, const float* camToWorld12,
-                   float dist, double* out29) {
+                   float dist, int64_t* sums31, double* out31) {
   int lwh[2] = {lw, lh};
   intr_t inl = intr_from(lwh, f4l);
   intr_t inr = intr_from(wh, renderF4);
   pose_t rp = pose_from12(renderPose12);
   pose_t c2w = pose_from12(camToWorld12);
-  icp_accumulate(depth, lw, lh, &inl, points, normals, &inr, &rp, &c2w, dist, out29);
-  return 0;
+  int64_t S[ICP_SUMS];
+  const int rc = icp_accumulate(depth, lw, lh, &inl, points, normals, &inr, &rp, &c2w, dist, S);
+  if (sums31) memcpy(sums31, S, sizeof(S));
+  if (out31) icp_decode(S, out31);
+  return rc;
 }
 
 /* double-precision SE(3) helpers (proj/include/rf/pose.hpp:38-60, S = double) */
@@ -1584,24 +1662,56 @@ static void matmul3d(const double* A, const double* B, double* C) {
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) C[r * 3 + c] = A[r * 3 + 0] * B[c] + (A[r * 3 + 1] * B[3 + c] + A[r * 3 + 2] * B[6 + c]);
 }
+/* sin(x)/x, (1 - cos x)/x^2, (x - sin x)/x^3 for t = x^2 < 1 by their Taylor
+ * series (nested; the truncation is below 1e-19): basic IEEE operations only,
+ * so the B200 (rfg_icp.cu:se3_coeffs) evaluates them bit-identically. */
+static void se3_series(double t, double* a, double* b, double* c) {
+  *a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+       (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+       (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+  *b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
+       (1.0 - t * (1.0 / 132.0) * (1.0 - t * (1.0 / 182.0) * (1.0 - t * (1.0 / 240.0) * (1.0 - t * (1.0 / 306.0) *
+       (1.0 - t * (1.0 / 380.0))))))))));
+  *c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+       (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+       (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+}
+/* Rodrigues coefficients of exp([omega]x) for th2 = |omega|^2: the series
+ * below 1 rad; above, sin/cos of theta / 2^k by the series and k exact
+ * double-angle steps (no libm: bit-identical on the B200). */
+static void se3_coeffs(double th2, double* a, double* b, double* c) {
+  if (th2 < 1.0) {
+    se3_series(th2, a, b, c);
+    return;
+  }
+  const double theta = sqrt(th2);
+  double h = theta;
+  int k = 0;
+  while (h >= 1.0) {
+    h *= 0.5;
+    ++k;
+  }
+  double sa, sb, sc;
+  se3_series(h * h, &sa, &sb, &sc);
+  double s = h * sa, co = 1.0 - (h * h) * sb;
+  for (int i = 0; i < k; ++i) {
+    const double s2 = 2.0 * s * co;
+    co = 1.0 - 2.0 * s * s;
+    s = s2;
+  }
+  *a = s / theta;
+  *b = (1.0 - co) / th2;
+  *c = (theta - s) / (theta * th2);
+}
 static posed_t se3_exp(const double* tau) {
   const double* w = tau;
   const double* v = tau + 3;
-  double theta = sqrt(w[0] * w[0] + (w[1] * w[1] + w[2] * w[2]));
+  const double th2 = w[0] * w[0] + (w[1] * w[1] + w[2] * w[2]);
   double W[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
   double WW[9];
   matmul3d(W, W, WW);
   double a, b, c;
-  if (theta < 1e-8) {
-    a = 1.0;
-    b = 0.5;
-    c = 1.0 / 6.0;
-  } else {
-    double s = sin(theta), co = cos(theta);
-    a = s / theta;
-    b = (1.0 - co) / (theta * theta);
-    c = (theta - s) / (theta * theta * theta);
-  }
+  se3_coeffs(th2, &a, &b, &c);
   posed_t p;
   double V[9];
   for (int i = 0; i < 9; ++i) {
@@ -1633,58 +1743,72 @@ static pose_t posed_to_f(const posed_t* p) {
   return q;
 }
 
-/* Solve H x = -g for symmetric positive-definite H (Cholesky, fixed order).
- * Returns 0 on success, -1 if H is not positive definite / det < 1e-12. */
-int rfo_solve6(const double* acc29, double* x) {
-  double A[36];
-  int k = 0;
-  for (int a = 0; a < 6; ++a)
-    for (int b = a; b < 6; ++b) {
-      A[a * 6 + b] = acc29[k];
-      A[b * 6 + a] = acc29[k];
-      ++k;
-    }
-  /* Cholesky with the reciprocal of each pivot taken once (6 divisions instead
-   * of 33 — the GPU solver, rfg_icp.cu:solve6, runs the identical sequence) */
+/* Solve H x = -g from the decoded sums by an LDL^T factorisation (no square
+ * roots; one IEEE reciprocal per pivot), in a fixed operation order that the
+ * B200 solver (rfg_icp.cu:solve6) repeats:
+ *   D_j  = H_jj - sum_{p<j} (L_jp L_jp) D_p,   inv_j = 1 / D_j
+ *   L_ij = (H_ij - sum_{p<j} (L_ip L_jp) D_p) inv_j          (i > j)
+ *   y_i  = -g_i - sum_{p<i} L_ip y_p;  z_i = y_i inv_i;  x_i = z_i - sum_{p>i} L_pi x_p
+ * *detOut = det(H / n) = prod_j (D_j / n), the Hessian determinant "after
+ * scaling" by the inlier count n; 0 when H is not positive
+ * definite.  Returns 0, or -1 when H is not positive definite or
+ * det(H / n) < 1e-12 (degenerate). */
+static int sym6(int a, int b) { /* index of H_ab in the row-major upper triangle */
+  if (a > b) {
+    int t = a;
+    a = b;
+    b = t;
+  }
+  return a * 6 - a * (a - 1) / 2 + (b - a);
+}
+int rfo_solve6(const double* sums, double* x, double* detOut) {
+  const double n = sums[28];
   double L[36] = {0};
-  double inv[6];
-  double det = 1.0;
+  double D[6], inv[6];
+  *detOut = 0.0;
   for (int j = 0; j < 6; ++j) {
-    double s = A[j * 6 + j];
-    for (int p = 0; p < j; ++p) s -= L[j * 6 + p] * L[j * 6 + p];
-    if (!(s > 0.0)) return -1;
-    det *= s;
-    double ljj = sqrt(s);
-    L[j * 6 + j] = ljj;
-    inv[j] = 1.0 / ljj;
+    double d = sums[sym6(j, j)];
+    for (int p = 0; p < j; ++p) d -= (L[j * 6 + p] * L[j * 6 + p]) * D[p];
+    if (!(d > 0.0)) return -1;
+    D[j] = d;
+    inv[j] = 1.0 / d;
     for (int i = j + 1; i < 6; ++i) {
-      double t = A[i * 6 + j];
-      for (int p = 0; p < j; ++p) t -= L[i * 6 + p] * L[j * 6 + p];
+      double t = sums[sym6(i, j)];
+      for (int p = 0; p < j; ++p) t -= (L[i * 6 + p] * L[j * 6 + p]) * D[p];
       L[i * 6 + j] = t * inv[j];
     }
   }
-  if (det < 1e-12) return -1; /* SPEC.md:352 degenerate Hessian */
-  double yv[6];
+  double det = 1.0;
+  for (int j = 0; j < 6; ++j) det *= D[j] / n;
+  *detOut = det;
+  if (!(det >= 1e-12)) return -1; /* SPEC.md:352 degenerate Hessian */
+  double y[6];
   for (int i = 0; i < 6; ++i) {
-    double t = -acc29[21 + i];
-    for (int p = 0; p < i; ++p) t -= L[i * 6 + p] * yv[p];
-    yv[i] = t * inv[i];
+    double t = -sums[21 + i];
+    for (int p = 0; p < i; ++p) t -= L[i * 6 + p] * y[p];
+    y[i] = t;
   }
   for (int i = 5; i >= 0; --i) {
-    double t = yv[i];
+    double t = y[i] * inv[i];
     for (int p = i + 1; p < 6; ++p) t -= L[p * 6 + i] * x[p];
-    x[i] = t * inv[i];
+    x[i] = t;
   }
   return 0;
 }
 
 /* Coarse-to-fine tracking loop: levels
  * coarse -> fine, at most iters[l] iterations per level, stop a level when
- * ||delta|| < 1e-4, give up on a level when fewer than minCount pixels
- * associate or the Hessian is degenerate.  T_cw <- exp(delta) T_cw. */
+ * ||delta|| < 1e-4; a level with fewer than minCount inliers is skipped
+ * (ok = 0, the pose so far is kept); a degenerate Hessian ends the track and
+ * returns the INIT pose, as does a track that never updated
+ * the pose.  T_cw <- exp(delta) T_cw.
+ * statsOut12 (TrackerIterationSummary, of the last
+ * evaluation): {iterations run, inliers, sum r^2, converged, iterations per
+ * level x3, ok, inlier_fraction, hessian_det (det(H/n)), residual_mean
+ * (sum |r| / n), valid pixels}.  Returns 0, or RFO_ICP_ERANGE. */
 int rfo_icp_track(const float* depthLevels, const int* wh, const float* f4, const float* points,
                   const float* normals, const float* renderPose12, const float* renderF4, const float* initPose12,
-                  const int* icp6, const float* dist3, float* poseOut12, double* statsOut8) {
+                  const int* icp6, const float* dist3, float* poseOut12, double* statsOut12) {
   const int levels = icp6[0];
   const int minCount = icp6[4];
   intr_t in0 = intr_from(wh, f4);
@@ -1692,9 +1816,10 @@ int rfo_icp_track(const float* depthLevels, const int* wh, const float* f4, cons
   pose_t rp = pose_from12(renderPose12);
   pose_t init = pose_from12(initPose12);
   pose_t c2wf = pose_inverse(&init);
-  posed_t c2w;
+  posed_t c2w, c2wInit;
   for (int i = 0; i < 9; ++i) c2w.R[i] = c2wf.R[i];
   for (int i = 0; i < 3; ++i) c2w.t[i] = c2wf.t[i];
+  c2wInit = c2w;
   /* level offsets inside depthLevels */
   size_t off[8];
   size_t o = 0;
@@ -1702,11 +1827,13 @@ int rfo_icp_track(const float* depthLevels, const int* wh, const float* f4, cons
     off[l] = o;
     o += (size_t)(in0.w >> l) * (in0.h >> l);
   }
-  double acc[29];
-  int totalIt = 0, converged = 0;
-  memset(statsOut8, 0, sizeof(double) * 8);
-  statsOut8[7] = 1;
-  for (int l = levels - 1; l >= 0; --l) {
+  int64_t S[ICP_SUMS];
+  double acc[ICP_SUMS];
+  int totalIt = 0, converged = 0, rc = 0, failed = 0;
+  double* st = statsOut12;
+  memset(st, 0, sizeof(double) * 12);
+  st[7] = 1;
+  for (int l = levels - 1; l >= 0 && !failed; --l) {
     intr_t inl = in0;
     float sc = ldexpf(1.f, -l);
     inl.w = in0.w >> l;
@@ -1718,40 +1845,54 @@ int rfo_icp_track(const float* depthLevels, const int* wh, const float* f4, cons
     int it;
     for (it = 0; it < icp6[1 + l]; ++it) {
       pose_t c2wF = posed_to_f(&c2w);
-      icp_accumulate(depthLevels + off[l], inl.w, inl.h, &inl, points, normals, &inr, &rp, &c2wF, dist3[l], acc);
-      statsOut8[1] = acc[28];
-      statsOut8[2] = acc[27];
+      if (icp_accumulate(depthLevels + off[l], inl.w, inl.h, &inl, points, normals, &inr, &rp, &c2wF, dist3[l], S))
+        rc = RFO_ICP_ERANGE;
+      icp_decode(S, acc);
+      st[1] = acc[28];
+      st[2] = acc[27];
+      st[8] = acc[30] > 0.0 ? acc[28] / acc[30] : 0.0;
+      st[9] = 0.0;
+      st[10] = acc[28] > 0.0 ? acc[29] / acc[28] : 0.0;
+      st[11] = acc[30];
       if (acc[28] < (double)minCount) {
-        statsOut8[7] = 0;
+        st[7] = 0;
         break;
       }
       double delta[6];
-      if (rfo_solve6(acc, delta) != 0) {
-        statsOut8[7] = 0;
+      if (rfo_solve6(acc, delta, &st[9]) != 0) {
+        st[7] = 0;
+        failed = 1;
+        c2w = c2wInit;
         break;
       }
       posed_t inc = se3_exp(delta);
       c2w = posed_compose(&inc, &c2w);
       ++totalIt;
-      double nrm = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2] + delta[3] * delta[3] +
-                        delta[4] * delta[4] + delta[5] * delta[5]);
-      if (nrm < 1e-4) {
+      /* ||delta|| < 1e-4, compared squared */
+      double nrm2 = delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2] + delta[3] * delta[3] +
+                    delta[4] * delta[4] + delta[5] * delta[5];
+      if (nrm2 < 1e-8) {
         converged = 1;
         ++it;
         break;
       }
     }
-    statsOut8[4 + l] = it;
+    st[4 + l] = it;
   }
-  statsOut8[0] = totalIt;
-  statsOut8[3] = converged;
+  st[0] = totalIt;
+  st[3] = converged && !failed;
+  if (failed || totalIt == 0) {
+    /* never updated (or degenerate): the init pose itself */
+    memcpy(poseOut12, initPose12, 12 * sizeof(float));
+    return rc;
+  }
   posed_t w2c = posed_inverse(&c2w);
   pose_t outp = posed_to_f(&w2c);
   for (int r = 0; r < 3; ++r) {
     for (int c = 0; c < 3; ++c) poseOut12[r * 4 + c] = outp.R[r * 3 + c];
     poseOut12[r * 4 + 3] = outp.t[r];
   }
-  return 0;
+  return rc;
 }
 
 /* ------------------------------------------------------------- export */

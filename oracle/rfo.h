@@ -27,6 +27,9 @@ extern "C" {
 
 typedef struct rfo_map rfo_map;
 
+/* threads for the per-pixel raycast loops (default 1; output is independent of it) */
+void rfo_set_threads(int n);
+
 uint32_t rfo_hash_index(const int* pos3, uint32_t mask);
 int rfo_traverse_blocks(const float* a3, const float* b3, int* cellsOut, int maxCells);
 int rfo_block_in_frustum(const int* pos3, const float* pose12, const int* wh, const float* f4, const float* params6);
@@ -86,25 +89,29 @@ int rfo_build_view_full(const uint16_t* raw, const uint8_t* rgb, const int* wh, 
                         float* normals4);
 
 /* ICP point-to-plane depth tracker (absent in the reference; restated from
- * SPEC.md:348-356,390-395 — see DESIGN.md "ICP oracle").
+ * SPEC.md:333-356,390-395 — see DESIGN.md "ICP oracle").
  *   depthLevels: pyramid as produced by rfo_build_view, level 0 is wh
  *   points/normals: last render (float4 per pixel, w > 0 valid), renderPose12
  *   and renderF4 describe that render (resolution wh).
  *   icp6 = {levels, iters_l0, iters_l1, iters_l2, minCount, reserved}
- *   dist3 = outlier distance gate per level (metres)
- *   poseOut12 = tracked world->camera pose; statsOut8 = {iterations run,
- *   final count, final sum r^2, converged flag, per-level iterations x3, ok} */
+ *   dist3 = outlier distance gate per level (metres, <= 2)
+ *   poseOut12 = tracked world->camera pose; statsOut12 = TrackerIterationSummary
+ *   {iterations run, inliers, sum r^2, converged, per-level iterations x3, ok,
+ *    inlier_fraction, hessian_det = det(H/n), residual_mean = sum|r|/n, valid px}
+ * Returns 0, or -2 when a world point is outside the fixed-point range. */
 int rfo_icp_track(const float* depthLevels, const int* wh, const float* f4, const float* points,
                   const float* normals, const float* renderPose12, const float* renderF4, const float* initPose12,
-                  const int* icp6, const float* dist3, float* poseOut12, double* statsOut8);
-/* One ICP evaluation (29 sums) at a given level and float pose; used by the
- * GPU reduction parity test. out29 = H upper (21, row-major), g (6), E, n. */
+                  const int* icp6, const float* dist3, float* poseOut12, double* statsOut12);
+/* One ICP evaluation at a given level and float pose: the 31 fixed-point sums
+ * (sums31, int64) and their decoded doubles (out31): H upper (21, row-major),
+ * g (6), sum r^2, n, sum |r|, valid pixels.  Either output may be NULL. */
 int rfo_icp_reduce(const float* depth, int lw, int lh, const float* f4l, const float* points, const float* normals,
                    const int* wh, const float* renderPose12, const float* renderF4, const float* camToWorld12,
-                   float dist, double* out29);
+                   float dist, int64_t* sums31, double* out31);
 
-/* Cholesky solve of H delta = -g from the 29 sums; -1 when degenerate. */
-int rfo_solve6(const double* acc29, double* x);
+/* Cholesky solve of H delta = -g from the decoded sums; det(H/n) to *det;
+ * -1 when degenerate. */
+int rfo_solve6(const double* sums31, double* x, double* det);
 
 uint32_t rfo_total_entries(const rfo_map* m);
 int rfo_export_entries(const rfo_map* m, int* out5);

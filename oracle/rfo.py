@@ -71,10 +71,12 @@ def lib():
         L.rfo_rgb_to_intensity.argtypes = [_u8, C.c_int, C.c_int, _f]
         L.rfo_downsample_intensity.argtypes = [_f, C.c_int, C.c_int, _f]
         L.rfo_icp_track.argtypes = [_f, _i, _f, _f, _f, _f, _f, _f, _i, _f, _f, _d]
-        L.rfo_icp_reduce.argtypes = [_f, C.c_int, C.c_int, _f, _f, _f, _i, _f, _f, _f, C.c_float, _d]
-        L.rfo_solve6.argtypes = [_d, _d]
+        L.rfo_icp_reduce.argtypes = [_f, C.c_int, C.c_int, _f, _f, _f, _i, _f, _f, _f, C.c_float,
+                                     C.POINTER(C.c_int64), _d]
+        L.rfo_solve6.argtypes = [_d, _d, _d]
         L.rfo_forward_project.argtypes = [C.c_int, _f, _f, _f, _f, _i, _f, C.c_float, _i]
         L.rfo_render_icp_list.argtypes = [vp, _f, _i, _f, _f, _i, C.c_int, _f, _f, _f]
+        L.rfo_set_threads.argtypes = [C.c_int]
         L.rfo_total_entries.argtypes = [vp]
         L.rfo_total_entries.restype = C.c_uint32
         L.rfo_export_entries.argtypes = [vp, _i]
@@ -83,6 +85,12 @@ def lib():
         L.rfo_free_counts.argtypes = [vp, _i, _i]
         _lib = L
     return _lib
+
+
+def set_threads(n: int | None = None):
+    """Threads for the oracle's per-pixel raycast (default 1; results do not
+    depend on it).  None = every core of this host."""
+    lib().rfo_set_threads(int(n if n else (os.cpu_count() or 1)))
 
 
 def hash_index(pos, mask):
@@ -164,33 +172,53 @@ def downsample_intensity(img):
     return out
 
 
+ICP_STATS = ("iterations", "count", "residual_sum", "converged", "it_l0", "it_l1", "it_l2", "ok",
+             "inlier_fraction", "hessian_det", "residual_mean", "valid")
+
+
 def icp_track(levels_depth, intr, points, normals, render_pose34, render_intr, init_pose34,
               iters=(6, 10, 20), min_count=10, dist=(0.01, 0.02, 0.04)):
+    """rfo_icp_track: (pose (3, 4) f32, stats (12,) f64 in ICP_STATS order)."""
     flat = np.ascontiguousarray(np.concatenate([d.reshape(-1) for d in levels_depth]), np.float32)
     wh, f4 = _wh(intr), _f4(intr)
     rf4 = _f4(render_intr)
     icp6 = np.array([len(levels_depth), iters[0], iters[1], iters[2], min_count, 0], np.int32)
     d3 = _f32(dist)
     out = np.zeros((3, 4), np.float32)
-    stats = np.zeros(8, np.float64)
+    stats = np.zeros(12, np.float64)
     pts, nrm = _f32(points), _f32(normals)
     rp, ip = _f32(render_pose34), _f32(init_pose34)
-    lib().rfo_icp_track(P(flat, _f), P(wh, _i), P(f4, _f), P(pts, _f), P(nrm, _f), P(rp, _f), P(rf4, _f),
-                        P(ip, _f), P(icp6, _i), P(d3, _f), P(out, _f), P(stats, _d))
+    rc = lib().rfo_icp_track(P(flat, _f), P(wh, _i), P(f4, _f), P(pts, _f), P(nrm, _f), P(rp, _f), P(rf4, _f),
+                             P(ip, _f), P(icp6, _i), P(d3, _f), P(out, _f), P(stats, _d))
+    if rc != 0:
+        raise ValueError("icp_track: world point outside the fixed-point range (|p| >= 128 m)")
     return out, stats
 
 
-def icp_reduce(depth_l, f4l, points, normals, intr, render_pose34, render_intr, cam_to_world34, dist):
+def icp_reduce(depth_l, f4l, points, normals, intr, render_pose34, render_intr, cam_to_world34, dist,
+               fixed=False):
+    """One evaluation: the 31 sums decoded to float64 (fixed=False) or the raw
+    int64 fixed-point sums (fixed=True)."""
     d = _f32(depth_l)
     lh, lw = d.shape
     f4l = _f32(f4l)
-    out = np.zeros(29, np.float64)
+    out = np.zeros(31, np.float64)
+    raw = np.zeros(31, np.int64)
     pts, nrm = _f32(points), _f32(normals)
     rp, c2w = _f32(render_pose34), _f32(cam_to_world34)
     wh, rf4 = _wh(intr), _f4(render_intr)
     lib().rfo_icp_reduce(P(d, _f), lw, lh, P(f4l, _f), P(pts, _f), P(nrm, _f), P(wh, _i), P(rp, _f), P(rf4, _f),
-                         P(c2w, _f), dist, P(out, _d))
-    return out
+                         P(c2w, _f), dist, raw.ctypes.data_as(C.POINTER(C.c_int64)), P(out, _d))
+    return raw if fixed else out
+
+
+def solve6(sums31):
+    """rfo_solve6: (ok, delta (6,), det(H/n))."""
+    s = np.ascontiguousarray(sums31, np.float64)
+    x = np.zeros(6, np.float64)
+    det = np.zeros(1, np.float64)
+    rc = lib().rfo_solve6(P(s, _d), P(x, _d), P(det, _d))
+    return rc == 0, x, float(det[0])
 
 
 def forward_project(has_raycast, raycast, points, normals, pose34, intr, voxel_size):

@@ -52,7 +52,8 @@ class PipelineConfig_(C.Structure):
                 ("aff_offset", C.c_float), ("levels", C.c_int32), ("track", C.c_int32),
                 ("iters", C.c_int32 * 3), ("dist", C.c_float * 3), ("min_count", C.c_int32),
                 ("use_graph", C.c_int32), ("profile", C.c_int32), ("bilateral", C.c_int32),
-                ("raw_big_endian", C.c_int32)]
+                ("raw_big_endian", C.c_int32), ("colour", C.c_int32), ("intr_rgb", Intrinsics_),
+                ("extr_d_to_rgb", C.c_float * 12)]
 
 
 # every symbol include/rfg.h declares, with its ctypes signature
@@ -112,13 +113,16 @@ SIGNATURES = {
     "rfg_write_ppm": ([C.c_char_p, _vp, C.c_int, C.c_int], C.c_int),
     "rfg_icp_track": ([_vp, _vp, C.c_int, C.POINTER(Intrinsics_), _vp, _vp, _f, _f, _i, _f, C.c_int, _f, _d],
                       C.c_int),
-    "rfg_icp_reduce": ([_vp, _vp, C.c_int, C.POINTER(Intrinsics_), _vp, _vp, _f, _f, C.c_float, _d], C.c_int),
+    "rfg_icp_reduce": ([_vp, _vp, C.c_int, C.POINTER(Intrinsics_), _vp, _vp, _f, _f, C.c_float,
+                        C.POINTER(C.c_int64), _d], C.c_int),
     "rfg_pipeline_create": ([_vp, C.POINTER(PipelineConfig_), C.POINTER(_vp)], C.c_int),
     "rfg_pipeline_destroy": ([_vp], C.c_int),
     "rfg_pipeline_process_raw": ([_vp, _vp, _f], C.c_int),
     "rfg_pipeline_process_host": ([_vp, _vp, _f], C.c_int),
     "rfg_pipeline_process_raw_stream": ([_vp, _vp, _f, _vp], C.c_int),
     "rfg_pipeline_process_pgm": ([_vp, C.c_char_p, _f], C.c_int),
+    "rfg_pipeline_process_rgbd_stream": ([_vp, _vp, _vp, _f, _vp], C.c_int),
+    "rfg_pipeline_process_rgbd_host": ([_vp, _vp, _vp, _f], C.c_int),
     "rfg_pipeline_result": ([_vp, C.POINTER(AllocStats_), _f, _d], C.c_int),
     "rfg_pipeline_buffers": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                               C.POINTER(_vp)], C.c_int),

@@ -29,17 +29,18 @@ cudaError_t launch_downsample_intensity(const float* in, int w, int h, float* ou
 
 // rfg_icp.cu
 size_t icp_state_bytes();
-int icp_partial_slots();
-cudaError_t launch_icp_track(void* state, double* partials, const float* depthLevels, int levels, const Intr& in0,
+cudaError_t launch_icp_track(void* state, const float* depthLevels, int levels, const Intr& in0,
                              const float4* points, const float4* normals, const int* iters, const float* dist,
                              int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
                              float* renderPoseOut, cudaStream_t s);
-cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* depth, int lw, int lh, const float* f4l,
-                                   const Intr& in0, const float4* points, const float4* normals, const float* c2w,
+cudaError_t launch_icp_reduce_once(void* state, const float* depth, int lw, int lh, const float* f4l, const Intr& in0,
+                                   const float4* points, const float4* normals, const float* c2w,
                                    const float* renderPose, float dist, cudaStream_t s);
 const double* icp_sums_ptr(void* state);
+const long long* icp_fixed_ptr(void* state);
 unsigned long long* icp_timers_ptr(void* state);
 const double* icp_stats_ptr(void* state);
+const int* icp_error_ptr(void* state);
 const float* icp_w2c_ptr(void* state);
 
 FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p, const float* pose34,
@@ -91,15 +92,18 @@ __global__ void k_copy12(float* dst, const float* src) {
 struct FrameResult {
   MapState state;
   float pose[12];
-  double icp[8];
+  double icp[RFG_ICP_STATS];
+  int icpError;
 };
-__global__ void k_frame_result(FrameResult* out, const MapState* st, const float* pose, const double* icp) {
+__global__ void k_frame_result(FrameResult* out, const MapState* st, const float* pose, const double* icp,
+                               const int* icpError) {
   const int t = threadIdx.x;
   const int* s = reinterpret_cast<const int*>(st);
   int* d = reinterpret_cast<int*>(&out->state);
   for (int i = t; i < (int)(sizeof(MapState) / sizeof(int)); i += blockDim.x) d[i] = s[i];
   if (t < 12) out->pose[t] = pose[t];
-  if (t < 8) out->icp[t] = icp[t];
+  if (t < RFG_ICP_STATS) out->icp[t] = icp[t];
+  if (t == 0) out->icpError = *icpError;
 }
 // Gather VBA blocks (depth + colour planes) into VoxelSRgb byte layout.
 __global__ void k_export_blocks(const uint32_t* vbaD, const uint32_t* vbaC, const int* ptrs, int n, uint8_t* out) {
@@ -159,6 +163,8 @@ int ensure_range_scratch(rfg_map* m, int width, int height) {
 using namespace rfg;
 
 namespace {
+
+constexpr float kIcpMaxDist = 2.f;  // fixed-point range of the tracker sums (rfg_icp.cu)
 
 bool valid_intr(const rfg_intrinsics* i) { return i && i->width > 0 && i->height > 0; }
 bool valid_params(const rfg_scene_params* p) { return p && p->voxelSize > 0.f && p->mu > 0.f; }
@@ -234,8 +240,9 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
             alloc((void**)&d.state, sizeof(MapState)) && alloc((void**)&d.tileCounts, d.nTiles * sizeof(int2)) &&
             alloc((void**)&d.tilePrefix, (d.nTiles + 1) * sizeof(int2)) &&
             alloc((void**)&d.rangeBounds, padded * sizeof(int4)) &&
-            alloc((void**)&m->icpPartials, (size_t)icp_partial_slots() * 29 * sizeof(double)) &&
             alloc((void**)&m->icpOut, icp_state_bytes()) && alloc((void**)&m->icpPose, 64 * sizeof(float));
+  // the tracker's rotating accumulators must start at zero (rfg_icp.cu:IcpState)
+  if (ok && cudaMemset(m->icpOut, 0, icp_state_bytes()) != cudaSuccess) ok = false;
   if (ok && cudaMallocHost((void**)&m->hostState, sizeof(MapState)) != cudaSuccess) {
     cudaGetLastError();
     ok = false;
@@ -245,7 +252,6 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
     set_error("device allocation failed");
     return RFG_ENOMEM;
   }
-  m->icpPartialSlots = icp_partial_slots();
   const int rc = rfg_map_clear(m);
   if (rc != RFG_OK) {
     rfg_map_destroy(m);
@@ -260,8 +266,8 @@ int rfg_map_destroy(rfg_map* m) {
   DevMap& d = m->d;
   void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
                   d.visibility, d.reqKey, d.marked,     d.state,          d.tileCounts, d.tilePrefix,
-                  m->icpPartials, m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount,
-                  m->fwdPrev, m->fwdKeys, m->fwdTileCounts, m->fwdTilePrefix};
+                  m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount,
+                  m->fwdPrev, m->fwdKeys, m->fwdTileCounts, m->fwdTilePrefix, m->rgbaScratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->hostState) cudaFreeHost(m->hostState);
@@ -346,7 +352,25 @@ int rfg_integrate(rfg_map* m, const float* depth, const uint8_t* rgb, const rfg_
   RFG_REQUIRE(valid_intr(intrD) && valid_params(params), "invalid intrinsics / scene params");
   RFG_REQUIRE(!rgb || (m->d.vbaColour && valid_intr(intrRgb)), "colour integration needs a colour map + rgb intrinsics");
   const FrameArgs fa = make_frame_args(intrD, params, pose34, nullptr);
-  RFG_CK(launch_integrate(m->d, depth, rgb, fa, intrRgb, extr34, m->stream));
+  const uint32_t* rgba = nullptr;
+  if (rgb) {
+    const int n = intrRgb->width * intrRgb->height;
+    if (m->rgbaN < n) {
+      RFG_CK(cudaStreamSynchronize(m->stream));
+      cudaFree(m->rgbaScratch);
+      m->rgbaScratch = nullptr;
+      m->rgbaN = 0;
+      if (cudaMalloc(&m->rgbaScratch, (size_t)n * 4) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("colour scratch allocation failed");
+        return RFG_ENOMEM;
+      }
+      m->rgbaN = n;
+    }
+    RFG_CK(launch_rgb_to_rgba(rgb, m->rgbaScratch, n, m->stream));
+    rgba = m->rgbaScratch;
+  }
+  RFG_CK(launch_integrate(m->d, depth, rgba, fa, intrRgb, extr34, m->stream));
   return RFG_OK;
 }
 
@@ -524,33 +548,42 @@ int rfg_downsample_intensity(const float* in, int w, int h, float* out, void* st
 
 int rfg_icp_track(rfg_map* m, const float* depthLevels, int levels, const rfg_intrinsics* intr, const float* points,
                   const float* normals, const float renderPose34[12], const float initPose34[12], const int iters[3],
-                  const float dist[3], int minCount, float poseOut34[12], double stats8[8]) {
+                  const float dist[3], int minCount, float poseOut34[12], double stats12[RFG_ICP_STATS]) {
   RFG_REQUIRE(m && depthLevels && points && normals && renderPose34 && initPose34 && iters && dist,
               "null argument");
   RFG_REQUIRE(valid_intr(intr) && levels >= 1 && levels <= 3, "invalid intrinsics / levels");
+  for (int l = 0; l < levels; ++l)
+    RFG_REQUIRE(dist[l] > 0.f && dist[l] <= kIcpMaxDist, "ICP outlier gates must be in (0, 2] m");
   float host[24];
   memcpy(host, initPose34, 48);
   memcpy(host + 12, renderPose34, 48);
   RFG_CK(cudaMemcpyAsync(m->icpPose, host, sizeof(host), cudaMemcpyHostToDevice, m->stream));
   const Intr in0{intr->width, intr->height, intr->fx, intr->fy, intr->cx, intr->cy};
-  RFG_CK(launch_icp_track(m->icpOut, m->icpPartials, depthLevels, levels, in0, reinterpret_cast<const float4*>(points),
+  RFG_CK(launch_icp_track(m->icpOut, depthLevels, levels, in0, reinterpret_cast<const float4*>(points),
                           reinterpret_cast<const float4*>(normals), iters, dist, minCount, m->icpPose,
                           m->icpPose + 12, m->icpPose + 24, nullptr, m->stream));
-  double st[8];
+  double st[RFG_ICP_STATS];
   float pose[12];
+  int err = 0;
   RFG_CK(cudaMemcpyAsync(st, icp_stats_ptr(m->icpOut), sizeof(st), cudaMemcpyDeviceToHost, m->stream));
   RFG_CK(cudaMemcpyAsync(pose, m->icpPose + 24, sizeof(pose), cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaMemcpyAsync(&err, icp_error_ptr(m->icpOut), sizeof(int), cudaMemcpyDeviceToHost, m->stream));
   RFG_CK(cudaStreamSynchronize(m->stream));
+  if (err) {
+    set_error("ICP: a world point outside the fixed-point range (|p| components >= 128 m)");
+    return RFG_ERANGE;
+  }
   if (poseOut34) memcpy(poseOut34, pose, sizeof(pose));
-  if (stats8) memcpy(stats8, st, sizeof(st));
+  if (stats12) memcpy(stats12, st, sizeof(st));
   return RFG_OK;
 }
 
 int rfg_icp_reduce(rfg_map* m, const float* depthLevel, int level, const rfg_intrinsics* intr, const float* points,
                    const float* normals, const float renderPose34[12], const float camToWorld34[12], float dist,
-                   double out29[29]) {
-  RFG_REQUIRE(m && depthLevel && points && normals && renderPose34 && camToWorld34 && out29, "null argument");
+                   int64_t fixed31[RFG_ICP_SUMS], double out31[RFG_ICP_SUMS]) {
+  RFG_REQUIRE(m && depthLevel && points && normals && renderPose34 && camToWorld34, "null argument");
   RFG_REQUIRE(valid_intr(intr) && level >= 0 && level < 4, "invalid intrinsics / level");
+  RFG_REQUIRE(dist > 0.f && dist <= kIcpMaxDist, "ICP outlier gate must be in (0, 2] m");
   float host[24];
   memcpy(host, camToWorld34, 48);
   memcpy(host + 12, renderPose34, 48);
@@ -558,12 +591,22 @@ int rfg_icp_reduce(rfg_map* m, const float* depthLevel, int level, const rfg_int
   const Intr in0{intr->width, intr->height, intr->fx, intr->fy, intr->cx, intr->cy};
   const float sc = ldexpf(1.f, -level);
   const float f4l[4] = {intr->fx * sc, intr->fy * sc, intr->cx * sc, intr->cy * sc};
-  RFG_CK(launch_icp_reduce_once(m->icpOut, m->icpPartials, depthLevel, intr->width >> level, intr->height >> level,
-                                f4l, in0, reinterpret_cast<const float4*>(points),
-                                reinterpret_cast<const float4*>(normals), m->icpPose, m->icpPose + 12, dist,
-                                m->stream));
-  RFG_CK(cudaMemcpyAsync(out29, icp_sums_ptr(m->icpOut), 29 * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(launch_icp_reduce_once(m->icpOut, depthLevel, intr->width >> level, intr->height >> level, f4l, in0,
+                                reinterpret_cast<const float4*>(points), reinterpret_cast<const float4*>(normals),
+                                m->icpPose, m->icpPose + 12, dist, m->stream));
+  int err = 0;
+  if (out31)
+    RFG_CK(cudaMemcpyAsync(out31, icp_sums_ptr(m->icpOut), RFG_ICP_SUMS * sizeof(double), cudaMemcpyDeviceToHost,
+                           m->stream));
+  if (fixed31)
+    RFG_CK(cudaMemcpyAsync(fixed31, icp_fixed_ptr(m->icpOut), RFG_ICP_SUMS * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, m->stream));
+  RFG_CK(cudaMemcpyAsync(&err, icp_error_ptr(m->icpOut), sizeof(int), cudaMemcpyDeviceToHost, m->stream));
   RFG_CK(cudaStreamSynchronize(m->stream));
+  if (err) {
+    set_error("ICP: a world point outside the fixed-point range (|p| components >= 128 m)");
+    return RFG_ERANGE;
+  }
   return RFG_OK;
 }
 
@@ -667,6 +710,14 @@ struct rfg_pipeline {
   uint64_t graphKernels[2];
   cudaEvent_t ev[7];        // stage boundaries (profile mode)
   bool tracked;             // last frame ran the tracker
+  // colour pipelines: the RGB8 frame is packed to RGBA8 words by the graph's
+  // k_rgb_to_rgba node, which reads the caller's image in place (re-pointed
+  // like the view node); rgbDev holds copied-in frames
+  uint8_t* rgbDev;
+  uint32_t* rgba;
+  cudaGraphNode_t rgbNode[2];
+  cudaKernelNodeParams rgbParams[2];
+  const uint8_t* rgbSrc[2];
 };
 
 namespace {
@@ -690,7 +741,7 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   mark(1);
   if (track) {
     const Intr in0{c.intr.width, c.intr.height, c.intr.fx, c.intr.fy, c.intr.cx, c.intr.cy};
-    e = launch_icp_track(m->icpOut, m->icpPartials, p->depthLevels, c.levels, in0, p->points, p->normals, c.iters,
+    e = launch_icp_track(m->icpOut, p->depthLevels, c.levels, in0, p->points, p->normals, c.iters,
                          c.dist, c.min_count, p->poses, p->poses + 12, p->poses, p->poses + 12, s);
     if (e != cudaSuccess) return e;
   }
@@ -698,7 +749,14 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   const FrameArgs fa = make_frame_args(&c.intr, &c.params, nullptr, p->poses);
   if ((e = launch_allocate(m->d, p->depthLevels, fa, s)) != cudaSuccess) return e;
   mark(3);
-  if ((e = launch_integrate(m->d, p->depthLevels, nullptr, fa, nullptr, nullptr, s)) != cudaSuccess) return e;
+  if (c.colour) {
+    const int nRgb = c.intr_rgb.width * c.intr_rgb.height;
+    if ((e = launch_rgb_to_rgba(p->rgbDev, p->rgba, nRgb, s)) != cudaSuccess) return e;
+    if ((e = launch_integrate(m->d, p->depthLevels, p->rgba, fa, &c.intr_rgb, c.extr_d_to_rgb, s)) != cudaSuccess)
+      return e;
+  } else if ((e = launch_integrate(m->d, p->depthLevels, nullptr, fa, nullptr, nullptr, s)) != cudaSuccess) {
+    return e;
+  }
   mark(4);
   // expected ranges + ICP maps: the range tiles are reduced inside the
   // raycast's CTAs (profile mode: "ranges" = the binning, "raycast" = the rest)
@@ -730,7 +788,22 @@ cudaError_t set_view_raw(rfg_pipeline* p, int gi, const uint16_t* raw) {
   return e;
 }
 
-int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc) {
+// Point the frame graph's colour packing kernel at an RGB8 frame (no copy).
+cudaError_t set_rgb_src(rfg_pipeline* p, int gi, const uint8_t* rgb) {
+  if (p->rgbSrc[gi] == rgb) return cudaSuccess;
+  const uint8_t* r = rgb;
+  uint32_t* out = p->rgba;
+  int n = p->cfg.intr_rgb.width * p->cfg.intr_rgb.height;
+  void* args[] = {&r, &out, &n};  // k_rgb_to_rgba's parameters
+  cudaKernelNodeParams kp = p->rgbParams[gi];
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  const cudaError_t e = cudaGraphExecKernelNodeSetParams(p->exec[gi], p->rgbNode[gi], &kp);
+  if (e == cudaSuccess) p->rgbSrc[gi] = rgb;
+  return e;
+}
+
+int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc, const uint8_t* rgbSrc = nullptr) {
   const bool track = p->cfg.track && p->frames > 0;
   p->tracked = track;
   if (pose34) {
@@ -740,6 +813,9 @@ int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc) {
     count_launch();
   }
   if (!p->cfg.use_graph) {
+    if (p->cfg.colour && rgbSrc && rgbSrc != p->rgbDev)
+      RFG_CK(cudaMemcpyAsync(p->rgbDev, rgbSrc, (size_t)p->cfg.intr_rgb.width * p->cfg.intr_rgb.height * 3,
+                             cudaMemcpyDefault, p->stream));
     RFG_CK(enqueue_frame(p, track));
   } else {
     const int gi = track ? 1 : 0;
@@ -756,25 +832,30 @@ int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc) {
       RFG_CK(cudaGraphInstantiate(&p->exec[gi], g, 0));
       p->graph[gi] = g;
       p->viewRaw[gi] = p->rawDev;
-      if (view_is_fused(p->cfg.bilateral, false, false, p->cfg.levels)) {
-        size_t nn = 0;
-        cudaGraphGetNodes(g, nullptr, &nn);
-        std::vector<cudaGraphNode_t> nodes(nn);
-        cudaGraphGetNodes(g, nodes.data(), &nn);
-        for (cudaGraphNode_t nd : nodes) {
-          cudaGraphNodeType ty;
-          cudaKernelNodeParams kp{};
-          if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel &&
-              cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == view_pyramid_kernel()) {
-            p->viewNode[gi] = nd;
-            p->viewParams[gi] = kp;
-            break;
-          }
+      p->rgbSrc[gi] = p->rgbDev;
+      const bool fusedView = view_is_fused(p->cfg.bilateral, false, false, p->cfg.levels);
+      size_t nn = 0;
+      cudaGraphGetNodes(g, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      cudaGraphGetNodes(g, nodes.data(), &nn);
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaKernelNodeParams kp{};
+        if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel ||
+            cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess)
+          continue;
+        if (fusedView && kp.func == view_pyramid_kernel()) {
+          p->viewNode[gi] = nd;
+          p->viewParams[gi] = kp;
+        } else if (p->cfg.colour && kp.func == rgb_to_rgba_kernel()) {
+          p->rgbNode[gi] = nd;
+          p->rgbParams[gi] = kp;
         }
-        cudaGetLastError();
       }
+      cudaGetLastError();
     }
     if (p->viewNode[gi]) RFG_CK(set_view_raw(p, gi, rawSrc));
+    if (p->rgbNode[gi]) RFG_CK(set_rgb_src(p, gi, rgbSrc ? rgbSrc : p->rgbDev));
     RFG_CK(cudaGraphLaunch(p->exec[gi], p->stream));
     count_launch(p->graphKernels[gi]);
   }
@@ -791,6 +872,12 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
   RFG_REQUIRE(valid_intr(&cfg->intr) && valid_params(&cfg->params), "invalid intrinsics / scene params");
   RFG_REQUIRE(cfg->levels >= 1 && cfg->levels <= 3, "levels must be 1..3");
   RFG_REQUIRE(!cfg->track || cfg->levels >= 1, "tracking needs a pyramid");
+  for (int l = 0; l < cfg->levels; ++l)
+    RFG_REQUIRE(!cfg->track || (cfg->dist[l] > 0.f && cfg->dist[l] <= kIcpMaxDist),
+                "ICP outlier gates must be in (0, 2] m");
+  RFG_REQUIRE((size_t)cfg->intr.width * cfg->intr.height < (1u << 25), "image too large for the 25-bit pixel key");
+  RFG_REQUIRE(!cfg->colour || (m->d.vbaColour && valid_intr(&cfg->intr_rgb)),
+              "a colour pipeline needs a colour map and valid rgb intrinsics");
   *out = nullptr;
   rfg_pipeline* p = new rfg_pipeline();
   memset(p, 0, sizeof(*p));
@@ -809,7 +896,10 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
             cudaMalloc(&p->poses, 32 * sizeof(float)) == cudaSuccess &&
             cudaHostAlloc(&p->hostResult, sizeof(FrameResult), cudaHostAllocMapped) == cudaSuccess &&
             cudaMallocHost(&p->pgmStage, n * 2 + 16) == cudaSuccess &&
-            (!cfg->bilateral || cudaMalloc(&p->viewScratch, n * 4 + 16) == cudaSuccess);
+            (!cfg->bilateral || cudaMalloc(&p->viewScratch, n * 4 + 16) == cudaSuccess) &&
+            (!cfg->colour ||
+             (cudaMalloc(&p->rgbDev, (size_t)cfg->intr_rgb.width * cfg->intr_rgb.height * 3 + 16) == cudaSuccess &&
+              cudaMalloc(&p->rgba, (size_t)cfg->intr_rgb.width * cfg->intr_rgb.height * 4 + 16) == cudaSuccess));
   if (!ok) {
     cudaGetLastError();
     rfg_pipeline_destroy(p);
@@ -850,7 +940,7 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
     if (p->exec[i]) cudaGraphExecDestroy(p->exec[i]);
   for (int i = 0; i < 2; ++i)
     if (p->graph[i]) cudaGraphDestroy(p->graph[i]);
-  void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->poses, p->viewScratch};
+  void* ptrs[] = {p->rawDev, p->depthLevels, p->range, p->raycast, p->poses, p->viewScratch, p->rgbDev, p->rgba};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int k = 0; k < 7; ++k)
@@ -881,6 +971,7 @@ int rfg_pipeline_reset(rfg_pipeline* p) {
 
 int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw, const float* pose34) {
   RFG_REQUIRE(p && raw, "null argument");
+  RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
   if (raw != p->rawDev) RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
   return run_frame(p, pose34, p->rawDev);
@@ -888,6 +979,7 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw, const float* 
 
 int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const float* pose34, void* producer) {
   RFG_REQUIRE(p && raw, "null argument");
+  RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   cudaStream_t ps = static_cast<cudaStream_t>(producer);
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
   // the frame is read after the producer's pending work (its upload) ...
@@ -909,6 +1001,7 @@ int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const 
 
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const float* pose34) {
   RFG_REQUIRE(p && rawHost, "null argument");
+  RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
   // a pinned (device-mapped) host frame is read over PCIe by the captured
   // graph's view kernel itself — no separate DMA and no copy->graph gap;
@@ -924,8 +1017,53 @@ int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const fl
   return run_frame(p, pose34, p->rawDev);
 }
 
+int rfg_pipeline_process_rgbd_stream(rfg_pipeline* p, const uint16_t* raw, const uint8_t* rgb, const float* pose34,
+                                     void* producer) {
+  RFG_REQUIRE(p && raw && rgb, "null argument");
+  RFG_REQUIRE(p->cfg.colour, "rgbd frames need a colour pipeline (cfg.colour = 1)");
+  cudaStream_t ps = static_cast<cudaStream_t>(producer);
+  const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
+  RFG_CK(cudaEventRecord(p->rawReady, ps));
+  RFG_CK(cudaStreamWaitEvent(p->stream, p->rawReady, 0));
+  const int gi = (p->cfg.track && p->frames > 0) ? 1 : 0;
+  const bool direct = p->cfg.use_graph && p->exec[gi] && p->viewNode[gi] && p->rgbNode[gi];
+  if (!direct) {
+    if (raw != p->rawDev) RFG_CK(cudaMemcpyAsync(p->rawDev, raw, n * 2, cudaMemcpyDeviceToDevice, p->stream));
+    if (rgb != p->rgbDev)
+      RFG_CK(cudaMemcpyAsync(p->rgbDev, rgb, (size_t)p->cfg.intr_rgb.width * p->cfg.intr_rgb.height * 3,
+                             cudaMemcpyDeviceToDevice, p->stream));
+  }
+  const int rc = direct ? run_frame(p, pose34, raw, rgb) : run_frame(p, pose34, p->rawDev, p->rgbDev);
+  RFG_CK(cudaEventRecord(p->rawRead, p->stream));
+  RFG_CK(cudaStreamWaitEvent(ps, p->rawRead, 0));
+  return rc;
+}
+
+int rfg_pipeline_process_rgbd_host(rfg_pipeline* p, const uint16_t* rawHost, const uint8_t* rgbHost,
+                                   const float* pose34) {
+  RFG_REQUIRE(p && rawHost && rgbHost, "null argument");
+  RFG_REQUIRE(p->cfg.colour, "rgbd frames need a colour pipeline (cfg.colour = 1)");
+  const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
+  const size_t nRgb = (size_t)p->cfg.intr_rgb.width * p->cfg.intr_rgb.height * 3;
+  // pinned (device-mapped) host frames are read in place by the graph's view
+  // and colour packing kernels; anything else is copied in
+  const int gi = (p->cfg.track && p->frames > 0) ? 1 : 0;
+  if (p->cfg.use_graph && p->exec[gi] && p->viewNode[gi] && p->rgbNode[gi]) {
+    cudaPointerAttributes a{}, b{};
+    if (cudaPointerGetAttributes(&a, rawHost) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer &&
+        cudaPointerGetAttributes(&b, rgbHost) == cudaSuccess && b.type == cudaMemoryTypeHost && b.devicePointer)
+      return run_frame(p, pose34, static_cast<const uint16_t*>(a.devicePointer),
+                       static_cast<const uint8_t*>(b.devicePointer));
+    cudaGetLastError();
+  }
+  RFG_CK(cudaMemcpyAsync(p->rawDev, rawHost, n * 2, cudaMemcpyHostToDevice, p->stream));
+  RFG_CK(cudaMemcpyAsync(p->rgbDev, rgbHost, nRgb, cudaMemcpyHostToDevice, p->stream));
+  return run_frame(p, pose34, p->rawDev, p->rgbDev);
+}
+
 int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pose34) {
   RFG_REQUIRE(p && path, "null argument");
+  RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   const int64_t n = (int64_t)p->cfg.intr.width * p->cfg.intr.height;
   int w = 0, h = 0;
   // the previous frame's upload may still be reading the staging buffer
@@ -942,12 +1080,14 @@ int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pos
   return run_frame(p, pose34, p->rawDev);
 }
 
-int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34[12], double icpStats8[8]) {
+int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34[12],
+                        double icpStats[RFG_ICP_STATS]) {
   RFG_REQUIRE(p, "null pipeline");
   rfg_map* m = p->map;
   FrameResult* dev = nullptr;
   RFG_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), p->hostResult, 0));
-  k_frame_result<<<1, 32, 0, p->stream>>>(dev, m->d.state, p->poses, icp_stats_ptr(m->icpOut));
+  k_frame_result<<<1, 32, 0, p->stream>>>(dev, m->d.state, p->poses, icp_stats_ptr(m->icpOut),
+                                          icp_error_ptr(m->icpOut));
   count_launch();
   RFG_CK(cudaGetLastError());
   RFG_CK(cudaStreamSynchronize(p->stream));
@@ -957,8 +1097,12 @@ int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34
     memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
     stats->visibleCount = m->hostState->nVisible;  // stage 3 appends the list; its length is the count
   }
+  if (p->hostResult->icpError) {
+    set_error("ICP: a world point outside the fixed-point range (|p| components >= 128 m)");
+    return RFG_ERANGE;
+  }
   if (poseOut34) memcpy(poseOut34, p->hostResult->pose, 48);
-  if (icpStats8) memcpy(icpStats8, p->hostResult->icp, 64);
+  if (icpStats) memcpy(icpStats, p->hostResult->icp, sizeof(p->hostResult->icp));
   return RFG_OK;
 }
 

@@ -1,28 +1,32 @@
 // rfg_icp.cu — point-to-plane ICP depth tracker (ITMDepthTracker).
 //
 // The reference has no tracker; the algorithm is restated
-// from SPEC.md:348-356,390-395 and fixed by the CPU oracle
-// oracle/rfo.c:rfo_icp_track.
+// from SPEC.md:333-356,390-395 and fixed by the CPU oracle
+// oracle/rfo.c:rfo_icp_track (DESIGN.md §5 "ICP oracle").
 //
-// One cooperative kernel per pyramid level runs that level's whole
-// Gauss-Newton loop on the device.  Per iteration:
-//   reduce  — every valid pyramid pixel is backprojected, moved to the world
-//             by the current estimate, projected into the last ICP-map render
-//             (nearest pixel) and, if associated and within the level's
-//             distance gate, adds J J^T (21), J r (6), r^2 and 1 to double
-//             accumulators; warp-shuffle tree + shared-memory reduction to one
-//             partial per CTA (partials double-buffered by iteration parity);
-//   grid.sync();
-//   solve   — EVERY CTA sums all partials in the same fixed order and runs
-//             the same Cholesky solve and SE(3) update, so all CTAs hold the
-//             identical new estimate without a second grid barrier; CTA 0
-//             publishes it (pose, stats, done flag) to global memory.
-// A frame's whole tracker is ONE cooperative launch (k_icp_track: seed,
-// levels coarse to fine, output pose) with one grid barrier per iteration;
-// nothing is enqueued for iterations that are not needed, and the launch is
-// capturable in the frame's CUDA graph.  The
-// grid size is fixed per level, so the reduction order — and the result — is
-// run-to-run deterministic.
+// Bit-exact with the oracle.  The per-pixel terms of the normal equations
+// (products of floats, exact in double) are accumulated as FIXED-POINT
+// integers (each term scaled by 2^32 / 2^38 / 2^44 and floored, oracle
+// rfo.c:icp_accumulate), and integer sums do not depend on the order of
+// summation: the per-thread, warp-shuffle, CTA and cross-CTA (64-bit atomic)
+// reductions below yield exactly the oracle's serial sums.  The solve, the
+// SE(3) update and the convergence test then run the oracle's IEEE double
+// operation sequence (no FMA contraction, IEEE sqrt/division, no libm), so
+// the tracked pose is bit-identical.
+//
+// Per thread the floor-to-grid accumulation costs one add per term: an
+// accumulator offset by M = 1.5 * 2^(52-s) lies in [2^(52-s), 2^(53-s)),
+// whose doubles are exactly the multiples of 2^-s, so adding a term with
+// round-toward-zero (__dadd_rz; the sum is positive) adds floor(term * 2^s)
+// * 2^-s exactly, independent of the order; the accumulator's bits minus
+// M's bits are the integer sum.
+//
+// A frame's whole tracker is ONE cooperative launch (k_icp_track: seed from
+// the device pose, levels coarse to fine, output pose) with one grid barrier
+// per iteration: each CTA adds its 31 partial sums to a global accumulator
+// with 64-bit atomics, and after the barrier every CTA reads the totals and
+// runs the same solve, so all CTAs hold the identical new estimate without a
+// second barrier.  The launch is capturable in the frame's CUDA graph.
 #include <cooperative_groups.h>
 
 #include "rfg_common.cuh"
@@ -32,22 +36,31 @@ namespace cg = cooperative_groups;
 namespace rfg {
 
 constexpr int kIcpThreads = 512;
-constexpr int kIcpMaxCtas = 512;
+constexpr int kIcpSums = 31;   // H upper 21, g 6, sum r^2, inliers, sum |r|, valid pixels
+constexpr int kIcpStats = 12;  // TrackerIterationSummary (include/rfg.h)
+// fixed-point scale (log2) per sum; 0 = plain integer count (rfo.c:kIcpShift)
+__host__ __device__ constexpr int icp_shift(int k) { return k < 21 ? 32 : (k < 27 ? 38 : (k == 28 || k == 30 ? 0 : 44)); }
 
 // Device tracking state (rfg_map::icpOut).
 struct IcpState {
-  double c2w[12];       // current camera->world estimate (row-major 3x4)
-  double sums[29];      // last evaluation
-  double stats[8];      // {iterations, count, E, converged, it_l0, it_l1, it_l2, ok}
-  float c2wF[12];       // float cast of c2w
-  float w2cF[12];       // tracked world->camera (output pose)
-  float renderPose[12]; // world->camera of the render being tracked against
-  int done[4];          // per-level stop flags
-  int pad[4];
+  double c2w[12];                 // current camera->world estimate (row-major 3x4)
+  double sums[kIcpSums];          // last evaluation, decoded
+  long long fixed[kIcpSums];      // last evaluation, fixed-point
+  double stats[kIcpStats];        // TrackerIterationSummary
+  float c2wF[12];                 // float cast of c2w
+  float w2cF[12];                 // tracked world->camera (output pose)
+  float renderPose[12];           // world->camera of the render being tracked against
+  int done[4];                    // per-level stop flags (single evaluations)
+  unsigned gen;                   // iterations so far: rotates the accumulators
+  int error;                      // sticky: a world point outside the fixed-point range
   // phase timers of CTA 0 (ns, %globaltimer), accumulated over iterations:
-  // {associate+reduce, grid barrier, final sum, solve, iterations,
+  // {associate+reduce, grid barrier, read totals, solve, iterations,
   //  level-0 total, level-1 total, level-2 total}
   unsigned long long timers[8];
+  // three rotating cross-CTA accumulators: iteration i adds into [i % 3]
+  // and zeroes [(i + 1) % 3], which iteration i - 2 used and every CTA has
+  // read before the barrier of iteration i - 1 (all zero between launches)
+  unsigned long long acc[3][32];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -74,16 +87,19 @@ struct IcpLevelArgs {
 // Per-CTA copy of the Gauss-Newton state (identical in every CTA).
 struct GnShared {
   double c2w[12];
-  double sums[29];
-  double stats[8];
+  double c2wInit[12];
+  double sums[kIcpSums];
+  long long fixed[kIcpSums];
+  double stats[kIcpStats];
   float c2wF[12];
   float rp[12];
   int done;
+  int failed;  // degenerate Hessian: the track returns the init pose
 };
 
-// double-precision SE(3) (proj/include/rf/pose.hpp:45-60 with S = double)
-// (all small-matrix loops are fully unrolled so the solver state stays in
-// registers instead of local memory)
+// ------------------------------------------------------------- the solve
+// double-precision SE(3) (proj/include/rf/pose.hpp:45-60 with S = double);
+// every function is the oracle's operation sequence (rfo.c), IEEE ops only
 __device__ __forceinline__ void matmul3d(const double* A, const double* B, double* C) {
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -95,123 +111,129 @@ __device__ void c2w_to_float(const double* c, float* f) {
   for (int i = 0; i < 12; ++i) f[i] = (float)c[i];
 }
 
-// Load an explicit float camera->world pose (single evaluations).
-__global__ void k_icp_set_c2w(IcpState* st, const float* c2w, const float* renderPose) {
-  if (threadIdx.x != 0) return;
-  for (int i = 0; i < 12; ++i) {
-    st->c2wF[i] = c2w[i];
-    st->c2w[i] = c2w[i];
-    st->renderPose[i] = renderPose[i];
+// rfo.c:se3_series — sin(x)/x, (1 - cos x)/x^2, (x - sin x)/x^3 for t = x^2 < 1
+__device__ __forceinline__ void se3_series(double t, double& a, double& b, double& c) {
+  a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+      (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+      (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+  b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
+      (1.0 - t * (1.0 / 132.0) * (1.0 - t * (1.0 / 182.0) * (1.0 - t * (1.0 / 240.0) * (1.0 - t * (1.0 / 306.0) *
+      (1.0 - t * (1.0 / 380.0))))))))));
+  c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+      (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+      (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+}
+
+// rfo.c:se3_coeffs — the series below 1 rad, else halving + double angles
+__device__ __noinline__ void se3_coeffs(double th2, double& a, double& b, double& c) {
+  if (th2 < 1.0) {
+    se3_series(th2, a, b, c);
+    return;
   }
-  for (int i = 0; i < 4; ++i) st->done[i] = 0;
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// 1/sqrt(s) for s > 0: MUFU seed + two Newton steps (within ~1 ulp of the
-// correctly rounded value).  Inline, unlike the IEEE sqrt/rcp, whose
-// out-of-line slow paths made ptxas spill the whole factorisation.
-__device__ __forceinline__ double rsqrt_nr(double s) {
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const double e = __fma_rn(-__dmul_rn(s, r), r, 1.0);  // 1 - s r^2
-    r = __fma_rn(__dmul_rn(r, 0.5), e, r);
-  }
-  return r;
-}
-
-// Cholesky solve (same operation order as oracle/rfo.c:rfo_solve6; the
-// pivot's 1/sqrt comes from rsqrt_nr, so the solution agrees with the oracle
-// to rounding — the tracker's pose tolerance is 1e-5).
-__device__ __forceinline__ int solve6(const double* acc, double* x) {
-  // every loop has constant bounds (guards instead of j-dependent limits) so
-  // the whole factorisation unrolls into registers
-  double A[36];
+  const double theta = sqrt(th2);
+  double h = theta;
   int k = 0;
-#pragma unroll
-  for (int a = 0; a < 6; ++a)
-#pragma unroll
-    for (int b = a; b < 6; ++b) {
-      A[a * 6 + b] = acc[k];
-      A[b * 6 + a] = acc[k];
-      ++k;
-    }
+  while (h >= 1.0) {
+    h *= 0.5;
+    ++k;
+  }
+  double sa, sb, sc;
+  se3_series(h * h, sa, sb, sc);
+  double s = h * sa, co = 1.0 - (h * h) * sb;
+  for (int i = 0; i < k; ++i) {
+    const double s2 = 2.0 * s * co;
+    co = 1.0 - 2.0 * s * s;
+    s = s2;
+  }
+  a = s / theta;
+  b = (1.0 - co) / th2;
+  c = (theta - s) / (theta * th2);
+}
+
+// rfo.c:rfo_solve6 — LDL^T of H (no square roots), det(H / n), substitution.
+// Every loop has constant bounds and is fully unrolled, so the factorisation
+// lives in registers; a non-positive pivot raises `bad` (and is replaced by 1
+// so the rest stays finite) instead of leaving the unrolled code early.
+// 1/D_j is the correctly rounded reciprocal (__drcp_rn == the oracle's 1.0/d).
+__host__ __device__ constexpr int sym6(int a, int b) {
+  return a <= b ? a * 6 - a * (a - 1) / 2 + (b - a) : b * 6 - b * (b - 1) / 2 + (a - b);
+}
+__device__ __forceinline__ int solve6(const double* sums, double* x, double* detOut) {
+  const double n = sums[28];
   double L[36];
-#pragma unroll
-  for (int i = 0; i < 36; ++i) L[i] = 0.0;
-  // no early exits either: a non-positive pivot raises `bad`, is replaced by
-  // 1 so the rest stays finite, and the solve reports failure at the end
-  double inv[6];
-  double det = 1.0;
+  double D[6], inv[6];
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < 6; ++j) {
-    double s = A[j * 6 + j];
+    double d = sums[sym6(j, j)];
 #pragma unroll
     for (int p = 0; p < 6; ++p)
-      if (p < j) s -= L[j * 6 + p] * L[j * 6 + p];
-    if (!(s > 0.0)) {
+      if (p < j) d -= __dmul_rn(__dmul_rn(L[j * 6 + p], L[j * 6 + p]), D[p]);
+    if (!(d > 0.0)) {
       bad = true;
-      s = 1.0;
+      d = 1.0;
     }
-    det *= s;
-    inv[j] = rsqrt_nr(s);
-    L[j * 6 + j] = s * inv[j];
+    D[j] = d;
+    inv[j] = __drcp_rn(d);
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
       if (i > j) {
-        double t = A[i * 6 + j];
+        double t = sums[sym6(i, j)];
 #pragma unroll
         for (int p = 0; p < 6; ++p)
-          if (p < j) t -= L[i * 6 + p] * L[j * 6 + p];
-        L[i * 6 + j] = t * inv[j];
+          if (p < j) t -= __dmul_rn(__dmul_rn(L[i * 6 + p], L[j * 6 + p]), D[p]);
+        L[i * 6 + j] = __dmul_rn(t, inv[j]);
       }
     }
   }
-  bad = bad || det < 1e-12;
-  double yv[6];
+  double det = 1.0;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) det = __dmul_rn(det, __ddiv_rn(D[j], n));
+  *detOut = bad ? 0.0 : det;
+  if (bad || !(det >= 1e-12)) return -1;  // SPEC.md:352 degenerate Hessian
+  double y[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    double t = -acc[21 + i];
+    double t = -sums[21 + i];
 #pragma unroll
     for (int p = 0; p < 6; ++p)
-      if (p < i) t -= L[i * 6 + p] * yv[p];
-    yv[i] = t * inv[i];
+      if (p < i) t -= __dmul_rn(L[i * 6 + p], y[p]);
+    y[i] = t;
   }
-  double xv[6];
 #pragma unroll
   for (int i = 5; i >= 0; --i) {
-    double t = yv[i];
+    double t = __dmul_rn(y[i], inv[i]);
 #pragma unroll
     for (int p = 0; p < 6; ++p)
-      if (p > i) t -= L[p * 6 + i] * xv[p];
-    xv[i] = t * inv[i];
+      if (p > i) t -= __dmul_rn(L[p * 6 + i], x[p]);
+    x[i] = t;
   }
-#pragma unroll
-  for (int i = 0; i < 6; ++i) x[i] = xv[i];
-  return bad ? -1 : 0;
+  return 0;
 }
 
 // One Gauss-Newton step on the CTA-local state (oracle: rfo_icp_track loop
-// body): count gate, Cholesky solve, T_cw <- exp(delta) T_cw, convergence.
+// body): summary, count gate, solve, T_cw <- exp(delta) T_cw, convergence.
 __device__ void gn_step(GnShared& g, int level, int minCount) {
-  g.stats[1] = g.sums[28];
-  g.stats[2] = g.sums[27];
-  if (g.sums[28] < (double)minCount) {
-    g.stats[7] = 0.0;
+  const double* acc = g.sums;
+  double* st = g.stats;
+  st[1] = acc[28];
+  st[2] = acc[27];
+  st[8] = acc[30] > 0.0 ? acc[28] / acc[30] : 0.0;
+  st[9] = 0.0;
+  st[10] = acc[28] > 0.0 ? acc[29] / acc[28] : 0.0;
+  st[11] = acc[30];
+  if (acc[28] < (double)minCount) {
+    st[7] = 0.0;
     g.done = 1;
     return;
   }
   double delta[6];
-  if (solve6(g.sums, delta) != 0) {
-    g.stats[7] = 0.0;
+  if (solve6(acc, delta, &st[9]) != 0) {
+    st[7] = 0.0;
     g.done = 1;
+    g.failed = 1;
+    for (int i = 0; i < 12; ++i) g.c2w[i] = g.c2wInit[i];
+    c2w_to_float(g.c2w, g.c2wF);
     return;
   }
   const double* w = delta;
@@ -221,23 +243,7 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
   double WW[9];
   matmul3d(W, W, WW);
   double ca, cb, cc;
-  if (th2 < 0.0625 * 0.0625) {
-    // sin(t)/t, (1 - cos t)/t^2, (t - sin t)/t^3 by their Taylor series
-    // (nested to t^10; the truncation error is below 1e-19 for t < 1/16):
-    // no sincos, no divisions on the solver's serial path, and no
-    // cancellation in 1 - cos t and t - sin t at small angles
-    const double t2 = th2;
-    ca = 1.0 - t2 * (1.0 / 6.0) * (1.0 - t2 * (1.0 / 20.0) * (1.0 - t2 * (1.0 / 42.0) * (1.0 - t2 * (1.0 / 72.0) * (1.0 - t2 * (1.0 / 110.0)))));
-    cb = 0.5 * (1.0 - t2 * (1.0 / 12.0) * (1.0 - t2 * (1.0 / 30.0) * (1.0 - t2 * (1.0 / 56.0) * (1.0 - t2 * (1.0 / 90.0) * (1.0 - t2 * (1.0 / 132.0))))));
-    cc = (1.0 / 6.0) * (1.0 - t2 * (1.0 / 20.0) * (1.0 - t2 * (1.0 / 42.0) * (1.0 - t2 * (1.0 / 72.0) * (1.0 - t2 * (1.0 / 110.0) * (1.0 - t2 * (1.0 / 156.0))))));
-  } else {
-    const double theta = sqrt(th2);
-    double s, co;
-    sincos(theta, &s, &co);
-    ca = s / theta;
-    cb = (1.0 - co) / (theta * theta);
-    cc = (theta - s) / (theta * theta * theta);
-  }
+  se3_coeffs(th2, ca, cb, cc);
   double ER[9], V[9], Et[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
@@ -262,36 +268,55 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
     g.c2w[r * 4 + 3] = (ER[r * 3] * Ct[0] + (ER[r * 3 + 1] * Ct[1] + ER[r * 3 + 2] * Ct[2])) + Et[r];
   }
   c2w_to_float(g.c2w, g.c2wF);
-  g.stats[0] += 1.0;
-  g.stats[4 + level] += 1.0;
-  const double nrm = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2] + delta[3] * delta[3] +
-                          delta[4] * delta[4] + delta[5] * delta[5]);
-  if (nrm < 1e-4) {
-    g.stats[3] = 1.0;
+  st[0] += 1.0;
+  st[4 + level] += 1.0;
+  // ||delta|| < 1e-4, compared squared (rfo.c)
+  const double nrm2 = delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2] + delta[3] * delta[3] +
+                      delta[4] * delta[4] + delta[5] * delta[5];
+  if (nrm2 < 1e-8) {
+    st[3] = 1.0;
     g.done = 1;
   }
 }
 
-// One evaluation's per-CTA partial: every valid level pixel p (grid stride)
-// is associated and accumulated in double (J J^T, J r, r^2, count), reduced
-// per warp by recursive halving and over the CTA's warps; on return thread k
-// < 29 of the CTA holds sum k of its pixels (returned), the others 0.
-// Pixels per thread whose camera-space point is kept in shared memory for
-// the whole level (computed at the level's first iteration; the depth and the
-// backprojection do not depend on the pose).  Level 0 at 640x480 on 148 CTAs
-// is 4.05 pixels per thread; pixels beyond the cached slots take the
-// uncached path.  Projection + gathers are issued kIcpGroup pixels at a
-// time so their loads are in flight together; pixels are accumulated in
-// the same order as a plain loop, so the sums do not depend on kIcpGroup.
-constexpr int kIcpPxCache = 4;
-constexpr int kIcpGroup = 2;  // 1 and 4 measured no faster
+// ------------------------------------------------------ the reduction
+// Pixels per thread and round; a level's first round keeps each thread's
+// camera-space points (pose-independent) in shared memory for the level's
+// later iterations.  Level 0 at 640x480 on 148 CTAs is 4.05 pixels per
+// thread: one cached round plus a few uncached pixels.
+constexpr int kIcpPx = 4;
+constexpr int kIcpGroup = 2;  // projections + gathers issued 2 pixels at a time
+// pixels per thread between flushes of the per-thread fixed-point
+// accumulators (|term| < 2^16 H units, so 8 terms stay inside the 2^19 range)
+constexpr int kIcpFlush = 8;
 
-// J J^T, J r, r^2, count of one associated pixel (the oracle's per-pixel
-// body, rfo_icp_track).
-__device__ __forceinline__ void icp_accumulate(double* acc, f3 pw, float4 V, float4 N, float dist2) {
-  if (!(V.w > 0.f) || !(N.w > 0.f)) return;
+// fixed-point offsets M = 1.5 * 2^(52 - s)
+__device__ __forceinline__ double icp_offset(int k) {
+  return icp_shift(k) == 32 ? 1572864.0 : (icp_shift(k) == 38 ? 24576.0 : 384.0);
+}
+
+// Per-thread accumulators: offset doubles for the 29 fixed-point sums (slots
+// 28 and 30 unused) and the two counts.
+struct IcpAcc {
+  double a[kIcpSums];
+  int count, valid;
+};
+
+__device__ __forceinline__ void acc_reset(IcpAcc& s) {
+#pragma unroll
+  for (int k = 0; k < kIcpSums; ++k) s.a[k] = icp_offset(k);
+  s.count = 0;
+  s.valid = 0;
+}
+
+// J J^T, J r, r^2, |r| and the count of one associated pixel (the oracle's
+// per-pixel body, rfo.c:icp_accumulate); false when the world point is
+// outside the fixed-point range (|p_w| components < 128 m).
+__device__ __forceinline__ bool icp_add(IcpAcc& s, f3 pw, float4 V, float4 N, float dist2) {
+  if (!(V.w > 0.f) || !(N.w > 0.f)) return true;
   const f3 diff{pw.x - V.x, pw.y - V.y, pw.z - V.z};
-  if (sqnorm3(diff) > dist2) return;
+  if (sqnorm3(diff) > dist2) return true;
+  const bool inRange = fabsf(pw.x) < 128.f && fabsf(pw.y) < 128.f && fabsf(pw.z) < 128.f;
   const f3 nn{N.x, N.y, N.z};
   const float r = dot3(diff, nn);
   const f3 pxn = cross3(pw, nn);
@@ -301,11 +326,13 @@ __device__ __forceinline__ void icp_accumulate(double* acc, f3 pw, float4 V, flo
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
-    for (int j = i; j < 6; ++j) acc[k++] += J[i] * J[j];
+    for (int j = i; j < 6; ++j, ++k) s.a[k] = __dadd_rz(s.a[k], __dmul_rn(J[i], J[j]));
 #pragma unroll
-  for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * rd;
-  acc[27] += rd * rd;
-  acc[28] += 1.0;
+  for (int i = 0; i < 6; ++i) s.a[21 + i] = __dadd_rz(s.a[21 + i], __dmul_rn(J[i], rd));
+  s.a[27] = __dadd_rz(s.a[27], __dmul_rn(rd, rd));
+  s.a[29] = __dadd_rz(s.a[29], fabs(rd));
+  s.count += 1;
+  return inRange;
 }
 
 // nearest-pixel association in the last render: pixel index or -1
@@ -319,22 +346,58 @@ __device__ __forceinline__ int icp_associate(const IcpLevelArgs& a, const Pose& 
   return iv * a.rw + iu;
 }
 
-// One evaluation's per-CTA partial: every valid level pixel p (grid stride)
-// is associated and accumulated in double (J J^T, J r, r^2, count), reduced
-// per warp by recursive halving and over the CTA's warps; on return thread k
-// < 29 of the CTA holds sum k of its pixels (returned), the others 0.
-__device__ __forceinline__ double icp_cta_partial(const IcpLevelArgs& a, const GnShared& g, const Pose& rp,
-                                                  const Intr& inl, float dist2, int n, int p0, int pstride,
-                                                  double (*sh)[29], float4* pcs, bool fill) {
+// The CTA's fixed-point sums of the thread accumulators, added to the global
+// accumulator `dst` (64-bit atomics; integer sums, so the order is
+// irrelevant).  Warp: recursive halving (lane l ends with sum l: 31
+// shuffles of 64 bits instead of 31 x 5); CTA: shared memory.
+__device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[32], unsigned long long* dst) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double out = 0.0;
-  const Pose c2w = pose_from12(g.c2wF);
-  double acc[29];
+  long long v[32];
 #pragma unroll
-  for (int k = 0; k < 29; ++k) acc[k] = 0.0;
+  for (int k = 0; k < 32; ++k) {
+    if (k == 28)
+      v[k] = s.count;
+    else if (k == 30)
+      v[k] = s.valid;
+    else if (k < kIcpSums)
+      v[k] = __double_as_longlong(s.a[k]) - __double_as_longlong(icp_offset(k));
+    else
+      v[k] = 0;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const long long send = hi ? v[i] : v[i + o];
+      const long long keep = hi ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  sh[wid][lane] = v[0];
+  __syncthreads();
+  if (threadIdx.x < kIcpSums) {
+    long long t = 0;
+#pragma unroll
+    for (int w = 0; w < kIcpThreads / 32; ++w) t += sh[w][threadIdx.x];
+    if (t) atomicAdd(dst + threadIdx.x, (unsigned long long)t);
+  }
+  __syncthreads();  // sh is reused by the next round
+}
+
+// One evaluation's contribution of this CTA: its pixels p0 + k * pstride
+// (k < kIcpPx: camera points cached when `fill`; the rest uncached), added
+// to dst.  Returns false when a world point was outside the fixed-point range.
+__device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShared& g, const Pose& rp,
+                                             const Intr& inl, float dist2, int n, int p0, int pstride,
+                                             long long (*sh)[32], float4* pcs, bool fill, unsigned long long* dst) {
+  const Pose c2w = pose_from12(g.c2wF);
+  bool ok = true;
+  IcpAcc s;
+  acc_reset(s);
   if (fill) {
 #pragma unroll
-    for (int k = 0; k < kIcpPxCache; ++k) {
+    for (int k = 0; k < kIcpPx; ++k) {
       const int p = p0 + k * pstride;
       float4 c = make_float4(0.f, 0.f, 0.f, -1.f);
       if (p < n) {
@@ -349,7 +412,7 @@ __device__ __forceinline__ double icp_cta_partial(const IcpLevelArgs& a, const G
     }
   }
 #pragma unroll
-  for (int kb = 0; kb < kIcpPxCache; kb += kIcpGroup) {
+  for (int kb = 0; kb < kIcpPx; kb += kIcpGroup) {
     f3 pw[kIcpGroup];
     int pix[kIcpGroup];
 #pragma unroll
@@ -358,6 +421,7 @@ __device__ __forceinline__ double icp_cta_partial(const IcpLevelArgs& a, const G
       pix[j] = -1;
       pw[j] = f3{0.f, 0.f, 0.f};
       if (c.w > 0.f) {
+        s.valid += 1;
         pw[j] = pose_apply(c2w, f3{c.x, c.y, c.z});
         pix[j] = icp_associate(a, rp, pw[j]);
       }
@@ -372,57 +436,42 @@ __device__ __forceinline__ double icp_cta_partial(const IcpLevelArgs& a, const G
     }
 #pragma unroll
     for (int j = 0; j < kIcpGroup; ++j)
-      if (pix[j] >= 0) icp_accumulate(acc, pw[j], V[j], N[j], dist2);
+      if (pix[j] >= 0) ok &= icp_add(s, pw[j], V[j], N[j], dist2);
   }
-  // pixels beyond the cached slots
-  for (int p = p0 + kIcpPxCache * pstride; p < n; p += pstride) {
+  // the pixels beyond the cached slots, uncached: k = kIcpPx.. of this
+  // thread's sequence p0 + k * pstride, flushed every kIcpFlush pixels (the
+  // fixed-point accumulators' range); every CTA runs the same number of
+  // flushes (they depend on n and pstride only)
+  for (int k = kIcpPx;; ++k) {
+    const int base = k * pstride;
+    if (base >= n) break;  // uniform: pixels p0 + base exist in some CTA iff base < n
+    if (k % kIcpFlush == 0) {
+      icp_cta_flush(s, sh, dst);
+      acc_reset(s);
+    }
+    const int p = p0 + base;
+    if (p >= n) continue;
     const float d = __ldg(a.depth + p);
     if (!(d > 0.f)) continue;
+    s.valid += 1;
     const int x = p % a.lw, y = p / a.lw;
     const f3 pc = backproject(inl, (float)x, (float)y, d);
     const f3 pw = pose_apply(c2w, pc);
     const int pix = icp_associate(a, rp, pw);
     if (pix < 0) continue;
-    icp_accumulate(acc, pw, __ldg(a.points + pix), __ldg(a.normals + pix), dist2);
+    ok &= icp_add(s, pw, __ldg(a.points + pix), __ldg(a.normals + pix), dist2);
   }
-  {
-    // multi-value warp reduction by recursive halving: at offset o every
-    // lane keeps one half of its live values and sends the other half to
-    // lane^o, so 32 (29 + 3 zero) sums take 16+8+4+2+1 = 31 shuffles
-    // instead of 29 x 5.  Lane l ends with sum number l.
-    double v[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = k < 29 ? acc[k] : 0.0;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const bool hi = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < o; ++i) {
-        const double send = hi ? v[i] : v[i + o];
-        const double keep = hi ? v[i + o] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
-    if (lane < 29) sh[wid][lane] = v[0];
-  }
-  __syncthreads();
-  if (threadIdx.x < 29) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kIcpThreads / 32; ++w) s += sh[w][threadIdx.x];
-    out = s;
-  }
-  return out;
+  icp_cta_flush(s, sh, dst);
+  return ok;
 }
 
 // One level's Gauss-Newton loop on the CTA-local state g.  CTAs with
 // blockIdx.x < nCta own the level's pixels (grid stride nCta x kIcpThreads);
-// the others only join the barriers, sum the same partials and run the same
-// solve.  `gi` counts iterations across levels so the partial buffers
-// alternate without a second barrier.
-__device__ __forceinline__ void icp_run_level(const IcpLevelArgs& a, double* partials, int nCta, GnShared& g,
-                                              double (*sh)[29], float4* pcs, int& gi, unsigned long long* tacc) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+// the others only join the barriers and run the same solve.  `gi` counts
+// iterations across levels (accumulator rotation, with the launch's `gen`).
+__device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& a, int nCta, GnShared& g,
+                                              long long (*sh)[32], float4* pcs, unsigned gen, int& gi,
+                                              unsigned long long* tacc) {
   const Intr inl{a.lw, a.lh, a.fx, a.fy, a.cx, a.cy};
   const float dist2 = a.dist * a.dist;
   const int n = a.lw * a.lh;
@@ -433,30 +482,20 @@ __device__ __forceinline__ void icp_run_level(const IcpLevelArgs& a, double* par
   for (int it = 0; it < a.iters && !g.done; ++it, ++gi) {
     unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (timed) t0 = gtimer();
-    double* part = partials + (size_t)(gi & 1) * kIcpMaxCtas * 29;
+    unsigned long long* buf = st->acc[(gen + gi) % 3];
     if (owner) {
-      const double ps = icp_cta_partial(a, g, rp, inl, dist2, n, blockIdx.x * blockDim.x + threadIdx.x,
-                                        nCta * blockDim.x, sh, pcs, it == 0);
-      if (threadIdx.x < 29) part[threadIdx.x * kIcpMaxCtas + blockIdx.x] = ps;  // [sum][cta]: coalesced final sum
+      const bool ok = icp_cta_eval(a, g, rp, inl, dist2, n, blockIdx.x * blockDim.x + threadIdx.x,
+                                   nCta * blockDim.x, sh, pcs, it == 0, buf);
+      if (!ok) st->error = 1;
     }
+    if (blockIdx.x == 0 && threadIdx.x < 32) st->acc[(gen + gi + 1) % 3][threadIdx.x] = 0ull;
     if (timed) t1 = gtimer();
     grid.sync();
     if (timed) t2 = gtimer();
-    // every CTA: fixed-order final sum over the owners (warp w owns sums w,
-    // w+16; lanes stride the CTAs; shuffle tree) and the identical solve
-    for (int k = wid; k < 29; k += kIcpThreads / 32) {
-      // issue all of this lane's loads before the dependent adds
-      double v[kIcpMaxCtas / 32];
-#pragma unroll
-      for (int j = 0; j < kIcpMaxCtas / 32; ++j) {
-        const int c = lane + 32 * j;
-        v[j] = c < nCta ? __ldcg(part + k * kIcpMaxCtas + c) : 0.0;
-      }
-      double sum = 0.0;
-#pragma unroll
-      for (int j = 0; j < kIcpMaxCtas / 32; ++j) sum += v[j];
-      sum = warp_sum(sum);
-      if (lane == 0) g.sums[k] = sum;
+    if (threadIdx.x < kIcpSums) {
+      const long long v = (long long)__ldcg(buf + threadIdx.x);
+      g.fixed[threadIdx.x] = v;
+      g.sums[threadIdx.x] = ldexp((double)v, -icp_shift(threadIdx.x));
     }
     __syncthreads();
     if (timed) t3 = gtimer();
@@ -483,46 +522,53 @@ __device__ __forceinline__ void icp_run_level(const IcpLevelArgs& a, double* par
   }
 }
 
-__device__ __forceinline__ void icp_publish(IcpState* st, const GnShared& g, const unsigned long long* tacc) {
+__device__ __forceinline__ void icp_publish(IcpState* st, const GnShared& g, const unsigned long long* tacc,
+                                            unsigned gen, int gi) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) st->timers[i] += tacc[i];
   for (int i = 0; i < 12; ++i) {
     st->c2w[i] = g.c2w[i];
     st->c2wF[i] = g.c2wF[i];
   }
-  for (int k = 0; k < 29; ++k) st->sums[k] = g.sums[k];
-  for (int i = 0; i < 8; ++i) st->stats[i] = g.stats[i];
+  for (int k = 0; k < kIcpSums; ++k) {
+    st->sums[k] = g.sums[k];
+    st->fixed[k] = g.fixed[k];
+  }
+  for (int i = 0; i < kIcpStats; ++i) st->stats[i] = g.stats[i];
+  st->gen = (gen + (unsigned)gi) % 3u;
 }
 
 // Single evaluation / single level on the state in `st` (rfg_icp_reduce).
-__global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a, double* partials) {
-  __shared__ double sh[kIcpThreads / 32][29];
+__global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a) {
+  __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
-  __shared__ float4 pcs[kIcpPxCache * kIcpThreads];
+  __shared__ float4 pcs[kIcpPx * kIcpThreads];
+  const unsigned gen = __ldcg(&st->gen);
   if (threadIdx.x == 0) {
     for (int i = 0; i < 12; ++i) {
       g.c2w[i] = __ldcg(&st->c2w[i]);
+      g.c2wInit[i] = g.c2w[i];
       g.c2wF[i] = __ldcg(&st->c2wF[i]);
       g.rp[i] = __ldcg(&st->renderPose[i]);
     }
-    for (int i = 0; i < 8; ++i) g.stats[i] = __ldcg(&st->stats[i]);
+    for (int i = 0; i < kIcpStats; ++i) g.stats[i] = __ldcg(&st->stats[i]);
     g.done = __ldcg(&st->done[a.level]);
+    g.failed = 0;
   }
   __syncthreads();
   int gi = 0;
   unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  icp_run_level(a, partials, gridDim.x, g, sh, pcs, gi, tacc);
+  icp_run_level(st, a, gridDim.x, g, sh, pcs, gen, gi, tacc);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    icp_publish(st, g, tacc);
+    icp_publish(st, g, tacc, gen, gi);
     st->done[a.level] = g.done;
   }
 }
 
-// The whole coarse-to-fine track of a frame in ONE cooperative launch
-// (k_icp_init + a launch per level + k_icp_final before): every CTA seeds
-// its state from the device-resident pose, runs the levels coarse to fine
-// with the same per-level pixel partition as a per-level launch (so the sums
-// and the pose are identical), and CTA 0 publishes the result.
+// The whole coarse-to-fine track of a frame in ONE cooperative launch:
+// every CTA seeds its state from the device-resident pose, runs the levels
+// coarse to fine with the same per-level pixel partition as a per-level
+// launch, and CTA 0 publishes the result.
 struct IcpTrackArgs {
   IcpLevelArgs lv[3];
   int nCta[3];
@@ -533,34 +579,41 @@ struct IcpTrackArgs {
   float* renderPoseOut;  // nullable: the next frame's render pose := the output pose
 };
 
-__global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrackArgs ta, double* partials) {
-  __shared__ double sh[kIcpThreads / 32][29];
+__global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrackArgs ta) {
+  __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
-  __shared__ float4 pcs[kIcpPxCache * kIcpThreads];
+  __shared__ float4 pcs[kIcpPx * kIcpThreads];
 #ifdef RFG_ICP_PHASES
   const unsigned long long tEntry = gtimer();
 #endif
+  const unsigned gen = __ldcg(&st->gen);
   if (threadIdx.x == 0) {
-    // k_icp_init: inverse of the float pose, widened to double (as the oracle)
+    // inverse of the float pose, widened to double (as the oracle)
     const Pose q = pose_inverse(pose_from12(ta.w2cInit));
     for (int r = 0; r < 3; ++r) {
       for (int c = 0; c < 3; ++c) g.c2w[r * 4 + c] = (double)q.R[r * 3 + c];
       g.c2w[r * 4 + 3] = (double)q.t[r];
     }
+    for (int i = 0; i < 12; ++i) g.c2wInit[i] = g.c2w[i];
     c2w_to_float(g.c2w, g.c2wF);
     for (int i = 0; i < 12; ++i) g.rp[i] = ta.renderPose[i];
-    for (int i = 0; i < 8; ++i) g.stats[i] = 0.0;
+    for (int i = 0; i < kIcpStats; ++i) g.stats[i] = 0.0;
     g.stats[7] = 1.0;
-    for (int k = 0; k < 29; ++k) g.sums[k] = 0.0;
+    for (int k = 0; k < kIcpSums; ++k) {
+      g.sums[k] = 0.0;
+      g.fixed[k] = 0;
+    }
+    g.failed = 0;
   }
   __syncthreads();
   int gi = 0;
   unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int l = ta.levels - 1; l >= 0; --l) {
+    if (g.failed) break;  // identical in every CTA
     if (ta.lv[l].iters <= 0) continue;
     if (threadIdx.x == 0) g.done = 0;
     __syncthreads();
-    icp_run_level(ta.lv[l], partials, ta.nCta[l], g, sh, pcs, gi, tacc);
+    icp_run_level(st, ta.lv[l], ta.nCta[l], g, sh, pcs, gen, gi, tacc);
   }
   // every CTA read renderPose before its first grid barrier; with no
   // iteration at all (every level capped at 0) there was none, so one is
@@ -572,16 +625,22 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrac
   tacc[6] = tacc[7] = 0;
 #endif
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    icp_publish(st, g, tacc);
+    if (g.failed) g.stats[3] = 0.0;
+    icp_publish(st, g, tacc, gen, gi);
     for (int i = 0; i < 12; ++i) st->renderPose[i] = g.rp[i];
-    // k_icp_final: world->camera output = inverse(c2w) cast to float
-    double R[9], t[3];
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) R[r * 3 + c] = g.c2w[c * 4 + r];
-    for (int r = 0; r < 3; ++r) t[r] = -(R[r * 3] * g.c2w[3] + (R[r * 3 + 1] * g.c2w[7] + R[r * 3 + 2] * g.c2w[11]));
-    for (int r = 0; r < 3; ++r) {
-      for (int c = 0; c < 3; ++c) st->w2cF[r * 4 + c] = (float)R[r * 3 + c];
-      st->w2cF[r * 4 + 3] = (float)t[r];
+    if (g.failed || g.stats[0] == 0.0) {
+      // never updated (or degenerate): the init pose itself
+      for (int i = 0; i < 12; ++i) st->w2cF[i] = ta.w2cInit[i];
+    } else {
+      // world->camera output = inverse(c2w) (double) cast to float
+      double R[9], t[3];
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) R[r * 3 + c] = g.c2w[c * 4 + r];
+      for (int r = 0; r < 3; ++r) t[r] = -(R[r * 3] * g.c2w[3] + (R[r * 3 + 1] * g.c2w[7] + R[r * 3 + 2] * g.c2w[11]));
+      for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) st->w2cF[r * 4 + c] = (float)R[r * 3 + c];
+        st->w2cF[r * 4 + 3] = (float)t[r];
+      }
     }
     if (ta.w2cOut)
       for (int i = 0; i < 12; ++i) ta.w2cOut[i] = st->w2cF[i];
@@ -611,18 +670,6 @@ static int icp_grid(int n) {
 }
 
 size_t icp_state_bytes() { return sizeof(IcpState); }
-int icp_partial_slots() { return 2 * kIcpMaxCtas; }
-
-static cudaError_t launch_level(IcpState* st, const IcpLevelArgs& a, double* partials, cudaStream_t s) {
-  const int grid = icp_grid(a.lw * a.lh);
-  if (grid <= 0) return cudaErrorCooperativeLaunchTooLarge;
-  IcpState* stp = st;
-  IcpLevelArgs ap = a;
-  double* pp = partials;
-  void* args[] = {&stp, &ap, &pp};
-  count_launch();
-  return cudaLaunchCooperativeKernel((const void*)k_icp_level, dim3(grid), dim3(kIcpThreads), args, 0, s);
-}
 
 static IcpLevelArgs level_args(const float* depthLevels, int level, const Intr& in0, const float4* points,
                                const float4* normals) {
@@ -650,8 +697,8 @@ static IcpLevelArgs level_args(const float* depthLevels, int level, const Intr& 
 }
 
 // Enqueue a complete coarse-to-fine track: init from (w2c, renderPose) device
-// pointers, one cooperative launch per level, final pose to w2cOut (device).
-cudaError_t launch_icp_track(void* state, double* partials, const float* depthLevels, int levels, const Intr& in0,
+// pointers, ONE cooperative launch, final pose to w2cOut (device).
+cudaError_t launch_icp_track(void* state, const float* depthLevels, int levels, const Intr& in0,
                              const float4* points, const float4* normals, const int* iters, const float* dist,
                              int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
                              float* renderPoseOut, cudaStream_t s) {
@@ -674,14 +721,23 @@ cudaError_t launch_icp_track(void* state, double* partials, const float* depthLe
     if (iters[l] > 0 && ta.nCta[l] > grid) grid = ta.nCta[l];
   }
   IcpState* stp = st;
-  double* pp = partials;
-  void* args[] = {&stp, &ta, &pp};
+  void* args[] = {&stp, &ta};
   count_launch();
   return cudaLaunchCooperativeKernel((const void*)k_icp_track, dim3(grid), dim3(kIcpThreads), args, 0, s);
 }
 
-cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* depth, int lw, int lh, const float* f4l,
-                                   const Intr& in0, const float4* points, const float4* normals, const float* c2w,
+__global__ void k_icp_set_c2w(IcpState* st, const float* c2w, const float* renderPose) {
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < 12; ++i) {
+    st->c2wF[i] = c2w[i];
+    st->c2w[i] = c2w[i];
+    st->renderPose[i] = renderPose[i];
+  }
+  for (int i = 0; i < 4; ++i) st->done[i] = 0;
+}
+
+cudaError_t launch_icp_reduce_once(void* state, const float* depth, int lw, int lh, const float* f4l, const Intr& in0,
+                                   const float4* points, const float4* normals, const float* c2w,
                                    const float* renderPose, float dist, cudaStream_t s) {
   IcpState* st = static_cast<IcpState*>(state);
   k_icp_set_c2w<<<1, 32, 0, s>>>(st, c2w, renderPose);
@@ -699,12 +755,19 @@ cudaError_t launch_icp_reduce_once(void* state, double* partials, const float* d
   a.iters = 1;
   a.minCount = 0;
   a.evalOnly = 1;
-  return launch_level(st, a, partials, s);
+  const int grid = icp_grid(a.lw * a.lh);
+  if (grid <= 0) return cudaErrorCooperativeLaunchTooLarge;
+  IcpState* stp = st;
+  void* args[] = {&stp, &a};
+  count_launch();
+  return cudaLaunchCooperativeKernel((const void*)k_icp_level, dim3(grid), dim3(kIcpThreads), args, 0, s);
 }
 
 unsigned long long* icp_timers_ptr(void* state) { return static_cast<IcpState*>(state)->timers; }
 const double* icp_sums_ptr(void* state) { return static_cast<IcpState*>(state)->sums; }
+const long long* icp_fixed_ptr(void* state) { return static_cast<IcpState*>(state)->fixed; }
 const double* icp_stats_ptr(void* state) { return static_cast<IcpState*>(state)->stats; }
+const int* icp_error_ptr(void* state) { return &static_cast<IcpState*>(state)->error; }
 const float* icp_w2c_ptr(void* state) { return static_cast<IcpState*>(state)->w2cF; }
 
 }  // namespace rfg

@@ -12,52 +12,6 @@
 
 namespace rfg {
 
-struct ColourArgs {
-  const uint8_t* rgb;  // packed RGB8, nullptr = depth-only
-  int rw, rh;
-  float fx, fy, cx, cy;
-  float extr[12];      // extrinsics_d_to_rgb
-};
-
-// update_voxel_colour (fusion.cpp:38-70)
-__device__ __forceinline__ void update_colour(uint32_t& word, f3 pt, const Pose& M, const ColourArgs& ca, int maxW) {
-  const f3 pc = pose_apply(M, pt);
-  if (pc.z <= 0.f) return;
-  const float px = ca.fx * pc.x / pc.z + ca.cx;
-  const float py = ca.fy * pc.y / pc.z + ca.cy;
-  if (px < 1 || px > (float)(ca.rw - 2) || py < 1 || py > (float)(ca.rh - 2)) return;
-  const int x0 = (int)floorf(px), y0 = (int)floorf(py);
-  const float fx = px - (float)x0, fy = py - (float)y0;
-  const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
-  const uint8_t* c00 = ca.rgb + 3 * ((size_t)y0 * ca.rw + x0);
-  const uint8_t* c01 = c00 + 3 * (size_t)ca.rw;
-  const int oldW = (int)(word >> 24);
-  uint32_t out = 0;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const float sample = w00 * (float)__ldg(c00 + k) + w10 * (float)__ldg(c00 + 3 + k) +
-                         w01 * (float)__ldg(c01 + k) + w11 * (float)__ldg(c01 + 3 + k);
-    const float old = (float)((word >> (8 * k)) & 0xFFu);
-    const float merged = ((float)oldW * old + sample) / (float)(oldW + 1);
-    int r = lround_haz(merged);
-    r = r < 0 ? 0 : (r > 255 ? 255 : r);
-    out |= (uint32_t)r << (8 * k);
-  }
-  out |= (uint32_t)min(oldW + 1, maxW) << 24;
-  word = out;
-}
-
-// The depth update of one voxel (update_voxel_depth, fusion.cpp:9-36) is
-// split into three phases over a lane's 16 voxels so the depth gathers are
-// all in flight together:
-//   1. project: pc = M p, pixel = round(project(pc)) or -1 (z <= 0, outside
-//      [1, W-2] x [1, H-2]);
-//   2. gather:  16 predicated depth loads;
-//   3. update:  eta = d - pc.z; unless invalid / eta < -mu / weight-capped,
-//      F = (w F + min(1, eta/mu)) / (w + 1), w = min(w + 1, maxW), quantise.
-// Every division is the IEEE quotient (div_fast inside div_ok's window, `/`
-// outside it), every rounding is the reference's, so the result is
-// bit-identical to the per-voxel function.
 #ifndef RFG_INT_MINB
 #define RFG_INT_MINB 4
 #endif
@@ -65,123 +19,6 @@ __device__ __forceinline__ void update_colour(uint32_t& word, f3 pt, const Pose&
 #define RFG_INT_QG 2
 #endif
 constexpr int kQG = RFG_INT_QG;  // rows (of 4 voxels) per project/gather/update group
-template <bool kColour>
-__global__ void __launch_bounds__(256, 2) k_integrate(DevMap m, const float* __restrict__ depth, FrameArgs fa,
-                                                   ColourArgs ca) {
-  const int lane = threadIdx.x & 31;
-  const int warpsPerCta = blockDim.x >> 5;
-  const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
-  const int nw = gridDim.x * warpsPerCta;
-  const int nVis = *((volatile int*)&m.state->nVisible);
-  const Pose pose = frame_pose(fa);
-  Pose Mrgb;
-  if (kColour) Mrgb = pose_compose(pose_from12(ca.extr), pose);
-  const float wLim = (float)(fa.w - 2), hLim = (float)(fa.h - 2);
-  const float mu = fa.mu;
-  const bool muOk = div_ok(mu);
-  const float rMu = div_rcp(mu);
-  const bool capW = fa.stopAtMaxW != 0;
-  for (int b = gw; b < nVis; b += nw) {
-    const int idx = m.visibleList[b];
-    const int4 e = ld_entry(m.entries, idx);
-    if (e.w < 0) continue;
-    const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
-    uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
-    uint4* cblk = kColour ? reinterpret_cast<uint4*>(m.vbaColour + (size_t)e.w * kBlock3) : nullptr;
-    uint4 v[4], c[4];
-#pragma unroll
-    for (int g = 0; g < 4; g += kQG) {
-    // the group's rows: one coalesced 128-bit load per lane and row (a
-    // warp-wide row access is 512 contiguous bytes of the block)
-#pragma unroll
-    for (int q = g; q < g + kQG; ++q) {
-      v[q] = blk[q * 32 + lane];
-      if (kColour) c[q] = cblk[q * 32 + lane];
-    }
-    // ---- phase 1: project the group's voxels (kQG rows of 4 along x)
-    float zc[4 * kQG];
-    int pix[4 * kQG];
-#pragma unroll
-    for (int q = g; q < g + kQG; ++q) {
-      const int lin = (q * 32 + lane) * 4;
-      const int z = lin >> 6, y = (lin >> 3) & 7, x0 = lin & 7;
-      const float pz = (float)(oz + z) * fa.voxelSize;
-      const float py = (float)(oy + y) * fa.voxelSize;
-      // pose_apply's (R1 y + R2 z) terms are shared by the row
-      const float r0 = pose.R[1] * py + pose.R[2] * pz;
-      const float r1 = pose.R[4] * py + pose.R[5] * pz;
-      const float r2 = pose.R[7] * py + pose.R[8] * pz;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = (q - g) * 4 + i;
-        const float px = (float)(ox + x0 + i) * fa.voxelSize;
-        const float cxw = (pose.R[0] * px + r0) + pose.t[0];
-        const float cyw = (pose.R[3] * px + r1) + pose.t[1];
-        const float czw = (pose.R[6] * px + r2) + pose.t[2];
-        int p = -1;
-        if (czw > 0.f) {
-          const float ax = fa.fx * cxw, ay = fa.fy * cyw;
-          float qx, qy;
-          if (div_ok(czw) && div_ok(ax) && div_ok(ay)) {
-            const float rz = div_rcp(czw);
-            qx = div_fast(ax, czw, rz);
-            qy = div_fast(ay, czw, rz);
-          } else {
-            qx = div_ieee(ax, czw);
-            qy = div_ieee(ay, czw);
-          }
-          const float u = qx + fa.cx, vv = qy + fa.cy;
-          if (!(u < 1 || u > wLim || vv < 1 || vv > hLim)) p = (int)(vv + 0.5f) * fa.w + (int)(u + 0.5f);
-        }
-        pix[k] = p;
-        zc[k] = czw;
-      }
-    }
-    // ---- phase 2: gather (all loads issued before any is consumed)
-    float dm[4 * kQG];
-#pragma unroll
-    for (int k = 0; k < 4 * kQG; ++k) dm[k] = pix[k] >= 0 ? __ldg(depth + pix[k]) : -1.f;
-    // ---- phase 3: update
-#pragma unroll
-    for (int q = g; q < g + kQG; ++q) {
-      uint32_t w[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-      uint32_t cw[4];
-      if (kColour) {
-        cw[0] = c[q].x;
-        cw[1] = c[q].y;
-        cw[2] = c[q].z;
-        cw[3] = c[q].w;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = (q - g) * 4 + i;
-        float eta = -1.f;  // update_voxel_depth's "invalid" return
-        if (pix[k] >= 0 && !(dm[k] <= 0.f)) {
-          eta = dm[k] - zc[k];
-          const int oldW = vox_w(w[i]);
-          if (!(eta < -mu) && !(capW && oldW >= fa.maxW)) {
-            const float oldF = sdf_to_logical(vox_sdf(w[i]));
-            float newF = (muOk && div_ok(eta)) ? div_fast(eta, mu, rMu) : div_ieee(eta, mu);
-            newF = smin(1.f, newF);
-            const float num = (float)oldW * oldF + newF;
-            const float den = (float)(oldW + 1);
-            const float merged = div_ok(num) ? div_fast(num, den, div_rcp(den)) : div_ieee(num, den);
-            w[i] = vox_pack(sdf_from_logical(merged), min(oldW + 1, fa.maxW));
-          }
-        }
-        if (kColour && eta >= -mu) {
-          const int lin = (q * 32 + lane) * 4;
-          const f3 pt{(float)(ox + (lin & 7) + i) * fa.voxelSize, (float)(oy + ((lin >> 3) & 7)) * fa.voxelSize,
-                      (float)(oz + (lin >> 6)) * fa.voxelSize};
-          update_colour(cw[i], pt, Mrgb, ca, fa.maxW);
-        }
-      }
-      blk[q * 32 + lane] = make_uint4(w[0], w[1], w[2], w[3]);
-      if (kColour) cblk[q * 32 + lane] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-    }
-    }
-  }
-}
 
 // ------------------------------------------------- depth-only, branch-free
 // The depth-only kernel (the C1/C2 hot path) computes every voxel's
@@ -373,6 +210,228 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
   }
 }
 
+// --------------------------------------------------- RGB-D, branch-free
+// ITMVoxel_s_rgb: the depth update above plus update_voxel_colour
+// (fusion.cpp:38-70) for every voxel whose depth update returned
+// eta >= -mu (fusion.cpp:257; update_voxel_depth returns -1 when the voxel
+// does not project onto valid depth).  The colour image is read as packed
+// RGBA8 words (k_rgb_to_rgba), one 32-bit load per bilinear tap.
+struct ColourArgs {
+  const uint32_t* rgba;  // RGBA8 words, rw x rh
+  int rw, rh;
+  float fx, fy, cx, cy;
+  float extr[12];        // extrinsics_d_to_rgb
+  int sameCamera;        // identity extrinsics + equal intrinsics: M_rgb == pose bitwise
+};
+
+// bilinear colour merge of one voxel (fusion.cpp:52-68); px, py inside
+// [1, rw-2] x [1, rh-2]
+__device__ __forceinline__ uint32_t colour_merge(uint32_t cw, float px, float py, const ColourArgs& ca, int maxW,
+                                                 uint32_t c00, uint32_t c10, uint32_t c01, uint32_t c11) {
+  const float fx = px - floorf(px), fy = py - floorf(py);
+  const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
+  const int oldW = (int)(cw >> 24);
+  const float fw = (float)oldW;
+  const float den = (float)(oldW + 1);
+  const float rden = div_rcp(den);
+  uint32_t out = (uint32_t)min(oldW + 1, maxW) << 24;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int sh = 8 * k;
+    const float sample = w00 * (float)((c00 >> sh) & 0xFFu) + w10 * (float)((c10 >> sh) & 0xFFu) +
+                         w01 * (float)((c01 >> sh) & 0xFFu) + w11 * (float)((c11 >> sh) & 0xFFu);
+    const float old = (float)((cw >> sh) & 0xFFu);
+    // num in [0, 65535] and den in [1, 256]: inside div_fast's window (or 0)
+    const float merged = div_fast(fw * old + sample, den, rden);
+    const int r = lround_haz(merged);  // in [0, 255]: merged is a convex combination of bytes
+    out |= (uint32_t)(r < 0 ? 0 : (r > 255 ? 255 : r)) << sh;
+  }
+  return out;
+}
+
+// the colour camera's pixel of a voxel (update_voxel_colour's projection,
+// fusion.cpp:48-52): false when behind the camera or outside the margin
+__device__ __forceinline__ bool colour_pixel(const Pose& M, const ColourArgs& ca, f3 pt, float* px, float* py) {
+  const f3 pc = pose_apply(M, pt);
+  if (!(pc.z > 0.f)) return false;
+  const float ax = ca.fx * pc.x, ay = ca.fy * pc.y;
+  float qx, qy;
+  if (div_ok(pc.z) && div_ok(ax) && div_ok(ay)) {
+    const float rz = div_rcp(pc.z);
+    qx = div_fast(ax, pc.z, rz);
+    qy = div_fast(ay, pc.z, rz);
+  } else {
+    qx = div_ieee(ax, pc.z);
+    qy = div_ieee(ay, pc.z);
+  }
+  *px = qx + ca.cx;
+  *py = qy + ca.cy;
+  return !(*px < 1 || *px > (float)(ca.rw - 2) || *py < 1 || *py > (float)(ca.rh - 2));
+}
+
+template <bool kSameCamera>
+__device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, int lane, int ox, int oy, int oz,
+                                                     const Pose& pose, const Pose& Mrgb, const FrameArgs& fa,
+                                                     const ColourArgs& ca, const float* __restrict__ depth,
+                                                     float wLim, float hLim, float mu, bool muOk, float rMu, bool capW,
+                                                     int maxW) {
+  const float vs = fa.voxelSize;
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const uint4 r = blk[q * 32 + lane];
+    const uint4 rc = cblk[q * 32 + lane];
+    uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+    uint32_t cw[4] = {rc.x, rc.y, rc.z, rc.w};
+    const int lin = (q * 32 + lane) * 4;
+    const float pz = (float)(oz + (lin >> 6)) * vs;
+    const float py = (float)(oy + ((lin >> 3) & 7)) * vs;
+    const float r0 = pose.R[1] * py + pose.R[2] * pz;
+    const float r1 = pose.R[4] * py + pose.R[5] * pz;
+    const float r2 = pose.R[7] * py + pose.R[8] * pz;
+    float zc[4], uu[4], vv[4];
+    int pix[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float px = (float)(ox + (lin & 7) + i) * vs;
+      const float cxw = (pose.R[0] * px + r0) + pose.t[0];
+      const float cyw = (pose.R[3] * px + r1) + pose.t[1];
+      const float czw = (pose.R[6] * px + r2) + pose.t[2];
+      const float ax = fa.fx * cxw, ay = fa.fy * cyw;
+      float u, v;
+      if (czw > 0.f && !(div_ok(czw) && div_ok(ax) && div_ok(ay))) {
+        u = div_ieee(ax, czw) + fa.cx;
+        v = div_ieee(ay, czw) + fa.cy;
+      } else {
+        const float rz = div_rcp(czw);
+        u = div_fast(ax, czw, rz) + fa.cx;
+        v = div_fast(ay, czw, rz) + fa.cy;
+      }
+      const bool in = czw > 0.f && !(u < 1 || u > wLim || v < 1 || v > hLim);
+      pix[i] = in ? (int)(v + 0.5f) * fa.w + (int)(u + 0.5f) : -1;
+      zc[i] = czw;
+      uu[i] = u;
+      vv[i] = v;
+    }
+    float dm[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dm[i] = pix[i] >= 0 ? __ldg(depth + pix[i]) : -1.f;
+    bool gate[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t w0 = wd[i];
+      const int oldW = vox_w(w0);
+      const bool valid = pix[i] >= 0 && !(dm[i] <= 0.f);
+      const float eta = dm[i] - zc[i];
+      const bool upd = valid && !(eta < -mu) && !(capW && oldW >= maxW);
+      if (upd) {
+        const float oldF = sdf_to_logical(vox_sdf(w0));
+        const float newF = smin(1.f, (muOk && div_ok(eta)) ? div_fast(eta, mu, rMu) : div_ieee(eta, mu));
+        const float fw = (float)oldW;
+        const float num = fw * oldF + newF;
+        const float den = fw + 1.f;
+        const float merged = div_ok(num) ? div_fast(num, den, div_rcp(den)) : div_ieee(num, den);
+        wd[i] = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
+      }
+      gate[i] = (valid ? eta : -1.f) >= -mu;  // fusion.cpp:257 on update_voxel_depth's return value
+    }
+    // colour: the camera pixel, then the four bilinear taps of every gated voxel
+    float cx4[4], cy4[4];
+    bool cin[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (kSameCamera) {
+        cx4[i] = uu[i];
+        cy4[i] = vv[i];
+        cin[i] = gate[i] && pix[i] >= 0;
+      } else {
+        cin[i] = false;
+        if (gate[i]) {
+          const f3 pt{(float)(ox + (lin & 7) + i) * vs, py, pz};
+          cin[i] = colour_pixel(Mrgb, ca, pt, &cx4[i], &cy4[i]);
+        }
+      }
+    }
+    uint32_t tap[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (cin[i]) {
+        const int x0 = (int)floorf(cx4[i]), y0 = (int)floorf(cy4[i]);
+        const uint32_t* p0 = ca.rgba + (size_t)y0 * ca.rw + x0;
+        tap[i][0] = __ldg(p0);
+        tap[i][1] = __ldg(p0 + 1);
+        tap[i][2] = __ldg(p0 + ca.rw);
+        tap[i][3] = __ldg(p0 + ca.rw + 1);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (cin[i]) cw[i] = colour_merge(cw[i], cx4[i], cy4[i], ca, maxW, tap[i][0], tap[i][1], tap[i][2], tap[i][3]);
+    blk[q * 32 + lane] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    cblk[q * 32 + lane] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+  }
+}
+
+template <bool kSameCamera>
+__global__ void __launch_bounds__(256, 2) k_integrate_rgbd(DevMap m, const float* __restrict__ depth, FrameArgs fa,
+                                                           ColourArgs ca) {
+  const int lane = threadIdx.x & 31;
+  const int warpsPerCta = blockDim.x >> 5;
+  const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
+  const int nw = gridDim.x * warpsPerCta;
+  const int nVis = *((volatile int*)&m.state->nVisible);
+  const Pose pose = frame_pose(fa);
+  Pose Mrgb = pose;
+  if (!kSameCamera) Mrgb = pose_compose(pose_from12(ca.extr), pose);  // extrinsics_d_to_rgb * pose
+  const float wLim = (float)(fa.w - 2), hLim = (float)(fa.h - 2);
+  const float mu = fa.mu;
+  const bool muOk = mu >= 0x1p-20f && mu <= 0x1p20f;
+  const float rMu = div_rcp(mu);
+  const bool capW = fa.stopAtMaxW != 0;
+  const int maxW = fa.maxW;
+  for (int b = gw; b < nVis; b += nw) {
+    const int idx = m.visibleList[b];
+    const int4 e = ld_entry(m.entries, idx);
+    if (e.w < 0) continue;
+    const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
+    uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
+    uint4* cblk = reinterpret_cast<uint4*>(m.vbaColour + (size_t)e.w * kBlock3);
+    integrate_block_rgbd<kSameCamera>(blk, cblk, lane, ox, oy, oz, pose, Mrgb, fa, ca, depth, wLim, hLim, mu, muOk,
+                                      rMu, capW, maxW);
+  }
+}
+
+// RGB8 (3 bytes per pixel) -> RGBA8 words, 4 pixels per thread (three
+// aligned 32-bit loads when the image is 4-byte aligned)
+__global__ void k_rgb_to_rgba(const uint8_t* __restrict__ rgb, uint32_t* __restrict__ out, int n) {
+  const int i4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i4 >= n) return;
+  if (i4 + 4 <= n && (reinterpret_cast<uintptr_t>(rgb) & 3u) == 0) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(rgb + (size_t)i4 * 3);
+    const uint32_t a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + 2);
+    // bytes: a = r0 g0 b0 r1, b = g1 b1 r2 g2, c = b2 r3 g3 b3
+    uint4 o;
+    o.x = a & 0xFFFFFFu;
+    o.y = (a >> 24) | ((b & 0xFFFFu) << 8);
+    o.z = (b >> 16) | ((c & 0xFFu) << 16);
+    o.w = c >> 8;
+    *reinterpret_cast<uint4*>(out + i4) = o;
+    return;
+  }
+  for (int i = i4; i < n && i < i4 + 4; ++i) {
+    const uint8_t* s = rgb + (size_t)i * 3;
+    out[i] = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16);
+  }
+}
+
+const void* rgb_to_rgba_kernel() { return (const void*)k_rgb_to_rgba; }
+
+cudaError_t launch_rgb_to_rgba(const uint8_t* rgb, uint32_t* out, int n, cudaStream_t s) {
+  const int threads = 256, per = threads * 4;
+  k_rgb_to_rgba<<<(n + per - 1) / per, threads, 0, s>>>(rgb, out, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
 #ifndef RFG_INT_GRID_PER_SM
 #define RFG_INT_GRID_PER_SM 8
 #endif
@@ -387,19 +446,32 @@ int integrate_grid() {
   return grid;
 }
 
-cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint8_t* rgb, const FrameArgs& fa,
+// Depth-only (rgba == nullptr) or RGB-D integration of the visible blocks.
+// extr34 nullptr = identity extrinsics.
+cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint32_t* rgba, const FrameArgs& fa,
                              const rfg_intrinsics* intrRgb, const float* extr34, cudaStream_t s) {
-  ColourArgs ca{};
-  ca.rgb = rgb;
-  if (rgb) {
+  if (rgba) {
+    ColourArgs ca{};
+    ca.rgba = rgba;
     ca.rw = intrRgb->width;
     ca.rh = intrRgb->height;
     ca.fx = intrRgb->fx;
     ca.fy = intrRgb->fy;
     ca.cx = intrRgb->cx;
     ca.cy = intrRgb->cy;
-    for (int i = 0; i < 12; ++i) ca.extr[i] = extr34 ? extr34[i] : ((i % 5 == 0) ? 1.f : 0.f);
-    k_integrate<true><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
+    bool ident = true;
+    for (int i = 0; i < 12; ++i) {
+      ca.extr[i] = extr34 ? extr34[i] : ((i % 5 == 0) ? 1.f : 0.f);
+      // identity: M_rgb = extr * pose equals pose up to the sign of zero
+      // entries, which cannot change a projection or a test downstream
+      ident = ident && ca.extr[i] == ((i % 5 == 0) ? 1.f : 0.f);
+    }
+    ca.sameCamera = ident && ca.rw == fa.w && ca.rh == fa.h && ca.fx == fa.fx && ca.fy == fa.fy && ca.cx == fa.cx &&
+                    ca.cy == fa.cy;
+    if (ca.sameCamera)
+      k_integrate_rgbd<true><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
+    else
+      k_integrate_rgbd<false><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
   } else {
     k_integrate_depth<<<integrate_grid(), 256, 0, s>>>(m, depth, fa);
   }

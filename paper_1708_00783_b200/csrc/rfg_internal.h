@@ -82,8 +82,12 @@ FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p,
 // kernel launchers (return cudaError_t of the launch)
 cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s);
 cudaError_t launch_sort_visible(const DevMap& m, cudaStream_t s);
-cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint8_t* rgb, const FrameArgs& fa,
+// depth-only (rgba nullptr) or RGB-D integration; rgba = packed RGBA8 colour
+// image (launch_rgb_to_rgba), extr34 nullptr = identity extrinsics
+cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint32_t* rgba, const FrameArgs& fa,
                              const rfg_intrinsics* intrRgb, const float* extr34, cudaStream_t s);
+cudaError_t launch_rgb_to_rgba(const uint8_t* rgb, uint32_t* out, int n, cudaStream_t s);
+const void* rgb_to_rgba_kernel();
 cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s);
 // (Re)allocate the expected-range bins for a width x height image (host call,
 // not capturable; done at pipeline creation or on first use of a size).
@@ -123,9 +127,7 @@ struct rfg_map {
   cudaStream_t stream;
   rfg::MapState* hostState;  // pinned mirror for readback
   // ICP scratch
-  double* icpPartials;
-  int icpPartialSlots;
-  double* icpOut;            // device: 29 sums + solver state
+  void* icpOut;              // device: rfg_icp.cu IcpState (sums, solver state, accumulators)
   float* icpPose;            // device: current cam->world (12) + world->cam (12) + render pose (12)
   // forward-projection scratch (approximate raycast), sized for fwdN pixels
   float4* fwdPrev;
@@ -134,6 +136,8 @@ struct rfg_map {
   int2* fwdTilePrefix;
   int fwdN;
   void* mesh;  // rfg_mesh.cu MeshBuffers (extract_mesh scratch + result)
+  uint32_t* rgbaScratch;  // packed colour image for rfg_integrate (rgbaN pixels)
+  int rgbaN;
 };
 
 #define RFG_CK(call)                                                                      \

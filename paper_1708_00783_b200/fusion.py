@@ -688,21 +688,40 @@ def forward_project(state: RenderState, newPose, intr: Intrinsics, voxelSize: fl
 
 
 # ------------------------------------------------------------------ ICP
+ICP_STATS = 12  # RFG_ICP_STATS
+ICP_SUMS = 31   # RFG_ICP_SUMS
+
+
 @dataclass
 class TrackerIterationSummary:
-    iterations: int
-    count: int
-    residual_sum: float
-    converged: bool
-    per_level: tuple
-    ok: bool
+    """SPEC.md:342-346 (TrackerIterationSummary) of the tracker's last
+    evaluation, plus the run's iteration counts and outcome."""
+    iterations: int          # Gauss-Newton updates, all levels
+    count: int               # inliers (associated, within the gate)
+    residual_sum: float      # sum r^2 over the inliers
+    converged: bool          # a level stopped on ||delta|| < 1e-4
+    per_level: tuple         # updates per level (finest first)
+    ok: bool                 # False: too few inliers, or degenerate (init pose returned)
+    inlier_fraction: float = 0.0   # inliers / valid depth pixels of the level
+    hessian_det: float = 0.0       # det(H / inliers) ("after scaling", SPEC.md:352)
+    residual_mean: float = 0.0     # sum |r| / inliers
+    valid: int = 0                 # valid depth pixels of the level
+
+    @staticmethod
+    def from_stats(st) -> "TrackerIterationSummary":
+        st = np.asarray(st, np.float64)
+        return TrackerIterationSummary(int(st[0]), int(st[1]), float(st[2]), bool(st[3]),
+                                       (int(st[4]), int(st[5]), int(st[6])), bool(st[7]), float(st[8]),
+                                       float(st[9]), float(st[10]), int(st[11]))
 
 
 def track_depth(map: VoxelBlockMap, view: View, state: RenderState, init_pose, iters=(6, 10, 20),
                 dist=(0.01, 0.02, 0.04), min_count: int = 10):
     """Point-to-plane ICP of the view's depth pyramid against
     the last ICP-map render in `state`.  iters/dist are indexed by pyramid
-    level (0 = finest; SPEC.md:391 caps 20/10/6 coarse -> fine)."""
+    level (0 = finest; SPEC.md:391 caps 20/10/6 coarse -> fine).  Returns
+    (world->camera pose (3, 4), TrackerIterationSummary); a degenerate Hessian
+    returns init_pose with summary.ok False."""
     if not state.hasRaycast:
         raise RuntimeError("track_depth needs an ICP-map render (render_maps) first")
     levels = len(view.pyramid)
@@ -719,30 +738,40 @@ def track_depth(map: VoxelBlockMap, view: View, state: RenderState, init_pose, i
     it = (C.c_int32 * 3)(*[int(x) for x in iters])
     ds = (C.c_float * 3)(*[float(x) for x in dist])
     out = np.zeros((3, 4), np.float32)
-    st = np.zeros(8, np.float64)
+    st = np.zeros(ICP_STATS, np.float64)
     map.bind_stream()
     check(lib().rfg_icp_track(map.handle, C.c_void_p(p0), levels, C.byref(view.calib.intrinsics_d.c()),
                               _ptr(state.points), _ptr(state.normals), _fp(rp), _fp(init), it, ds, min_count,
                               _fp(out), st.ctypes.data_as(_d)))
-    summ = TrackerIterationSummary(int(st[0]), int(st[1]), float(st[2]), bool(st[3]),
-                                   (int(st[4]), int(st[5]), int(st[6])), bool(st[7]))
-    return out, summ
+    return out, TrackerIterationSummary.from_stats(st)
 
 
 def icp_reduce(map: VoxelBlockMap, depth_level: torch.Tensor, level: int, intr0: Intrinsics, state: RenderState,
-               cam_to_world, dist: float) -> np.ndarray:
-    """One evaluation of the 29 point-to-plane sums (H upper 21, g 6, sum r^2, n)."""
-    out = np.zeros(29, np.float64)
+               cam_to_world, dist: float, fixed: bool = False) -> np.ndarray:
+    """One evaluation of the 31 point-to-plane sums (H upper 21, g 6, sum r^2,
+    inliers, sum |r|, valid pixels): decoded float64, or with fixed=True the
+    int64 fixed-point sums themselves."""
+    out = np.zeros(ICP_SUMS, np.float64)
+    raw = np.zeros(ICP_SUMS, np.int64)
     c2w = _pose(cam_to_world)
     rp = _pose(state.pose)
     map.bind_stream()
     check(lib().rfg_icp_reduce(map.handle, _ptr(depth_level.contiguous()), level, C.byref(intr0.c()),
                                _ptr(state.points), _ptr(state.normals), _fp(rp), _fp(c2w), dist,
-                               out.ctypes.data_as(_d)))
-    return out
+                               raw.ctypes.data_as(C.POINTER(C.c_int64)), out.ctypes.data_as(_d)))
+    return raw if fixed else out
 
 
 # ------------------------------------------------------------- pipeline
+class DeviceBuffer:
+    """A raw device allocation seen by torch without a copy
+    (__cuda_array_interface__); the owner keeps it alive."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
 class Pipeline:
     """Device-resident per-frame driver (ITMMainEngine::ProcessFrame order,
     SPEC.md:764): [ICP track] -> allocate -> integrate -> expected ranges ->
@@ -751,9 +780,15 @@ class Pipeline:
     def __init__(self, map: VoxelBlockMap, intr: Intrinsics, params: SceneParams,
                  affine: DepthAffine = DepthAffine(1.0 / 5000.0, 0.0), levels: int = 3, track: bool = True,
                  iters=(6, 10, 20), dist=(0.01, 0.02, 0.04), min_count: int = 10, use_graph: bool = True,
-                 profile: bool = False, bilateral: bool = False, raw_big_endian: bool = False):
+                 profile: bool = False, bilateral: bool = False, raw_big_endian: bool = False,
+                 colour: bool = False, intr_rgb: Intrinsics | None = None, extr_d_to_rgb=None):
+        """colour: ITMVoxel_s_rgb fusion (the map needs a colour plane); frames
+        then come with an RGB8 image, process(raw, pose, rgb=...), taken with
+        intrinsics intr_rgb (default: the depth camera's) and
+        extrinsics_d_to_rgb (default: identity)."""
         self.map = map
         self.intr = intr
+        self.colour = colour
         cfg = _lib.PipelineConfig_()
         cfg.intr = intr.c()
         cfg.params = params.c()
@@ -768,6 +803,11 @@ class Pipeline:
         cfg.profile = 1 if profile else 0
         cfg.bilateral = 1 if bilateral else 0
         cfg.raw_big_endian = 1 if raw_big_endian else 0
+        cfg.colour = 1 if colour else 0
+        if colour:
+            cfg.intr_rgb = (intr_rgb or intr).c()
+            ex = np.eye(3, 4, dtype=np.float32) if extr_d_to_rgb is None else _pose(extr_d_to_rgb)
+            cfg.extr_d_to_rgb = (C.c_float * 12)(*ex.reshape(-1).tolist())
         self._h = C.c_void_p()
         check(lib().rfg_pipeline_create(map.handle, C.byref(cfg), C.byref(self._h)))
         self._levels = levels
@@ -780,12 +820,26 @@ class Pipeline:
         except Exception:  # interpreter shutdown: module globals may be gone
             pass
 
-    def process(self, raw, pose=None):
+    def process(self, raw, pose=None, rgb=None):
         """raw: CUDA uint16/int16 tensor (device path) or numpy uint16 (host path).
         A device frame is ordered after the work queued on torch's current
         stream (e.g. the upload that produced it) and kept alive until the
-        pipeline's stream has read it."""
+        pipeline's stream has read it.  rgb: the (H, W, 3) uint8 colour image
+        of a colour pipeline, on the same side as raw."""
         p = _fp(_pose(pose)) if pose is not None else None
+        if self.colour:
+            if rgb is None:
+                raise ValueError("a colour pipeline needs the rgb image")
+            if torch.is_tensor(raw) and raw.is_cuda:
+                c = rgb if torch.is_tensor(rgb) else torch.as_tensor(np.ascontiguousarray(rgb, np.uint8))
+                c = c.cuda().contiguous()
+                check(lib().rfg_pipeline_process_rgbd_stream(self._h, _ptr(raw), _ptr(c), p, _stream_handle()))
+            else:
+                a = np.ascontiguousarray(raw, np.uint16) if not torch.is_tensor(raw) else raw.numpy()
+                c = np.ascontiguousarray(rgb, np.uint8) if not torch.is_tensor(rgb) else rgb.numpy()
+                check(lib().rfg_pipeline_process_rgbd_host(self._h, a.ctypes.data_as(C.c_void_p),
+                                                           c.ctypes.data_as(C.c_void_p), p))
+            return
         if torch.is_tensor(raw) and raw.is_cuda:
             check(lib().rfg_pipeline_process_raw_stream(self._h, _ptr(raw), p, _stream_handle()))
         else:
@@ -800,7 +854,7 @@ class Pipeline:
     def result(self):
         st = _lib.AllocStats_()
         pose = np.zeros((3, 4), np.float32)
-        icp = np.zeros(8, np.float64)
+        icp = np.zeros(ICP_STATS, np.float64)
         check(lib().rfg_pipeline_result(self._h, C.byref(st), _fp(pose), icp.ctypes.data_as(_d)))
         return AllocationStats(st.requested, st.allocated, st.allocFailures, st.visibleCount), pose, icp
 
@@ -814,6 +868,29 @@ class Pipeline:
         ptrs = [C.c_void_p() for _ in range(5)]
         check(lib().rfg_pipeline_buffers(self._h, *[C.byref(p) for p in ptrs]))
         return [p.value for p in ptrs]
+
+    def maps(self):
+        """The last frame's render, as zero-copy torch views of the pipeline's
+        device buffers: (expectedRange (H, W, 2), raycastResult, points,
+        normals (H, W, 4)) — the outputs of render_expected_ranges +
+        render_maps(kIcpMaps) at the frame's output pose (RenderState,
+        proj/include/rf/raycast.hpp:15-26).  Valid after result(); the next
+        process() overwrites them."""
+        h, w = self.intr.height, self.intr.width
+        _, rng, raycast, points, normals = self.buffers()
+        view = lambda ptr, c: torch.as_tensor(DeviceBuffer(ptr, h * w * c), device="cuda").view(h, w, c)  # noqa: E731
+        return view(rng, 2), view(raycast, 4), view(points, 4), view(normals, 4)
+
+    def depth_levels(self):
+        """The last frame's depth pyramid (View::depth_m + levels), zero-copy
+        views of the pipeline's buffer, finest first."""
+        dl = self.buffers()[0]
+        out, off = [], 0
+        for lv in range(self._levels):
+            h, w = self.intr.height >> lv, self.intr.width >> lv
+            out.append(torch.as_tensor(DeviceBuffer(dl + 4 * off, h * w), device="cuda").view(h, w))
+            off += h * w
+        return out
 
     def reset(self):
         check(lib().rfg_pipeline_reset(self._h))

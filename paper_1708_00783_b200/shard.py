@@ -68,13 +68,7 @@ class Composer:
         return keys
 
 
-class _DeviceBuffer:
-    """A raw device allocation seen by torch without a copy
-    (__cuda_array_interface__); the owner keeps it alive."""
-
-    def __init__(self, ptr: int, n: int, typestr: str = "<f4"):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
-                                         "strides": None, "stream": None}
+_DeviceBuffer = F.DeviceBuffer
 
 
 class ShardedPipeline:
