@@ -1748,10 +1748,11 @@ static pose_t posed_to_f(const posed_t* p) {
  * B200 solver (rfg_icp.cu:solve6) repeats:
  *   D_j  = H_jj - sum_{p<j} (L_jp L_jp) D_p,   inv_j = 1 / D_j
  *   L_ij = (H_ij - sum_{p<j} (L_ip L_jp) D_p) inv_j          (i > j)
- *   y_i  = -g_i - sum_{p<i} L_ip y_p;  z_i = y_i inv_i;  x_i = z_i - sum_{p>i} L_pi x_p
- * *detOut = det(H / n) = prod_j (D_j / n), the Hessian determinant "after
- * scaling" by the inlier count n; 0 when H is not positive
- * definite.  Returns 0, or -1 when H is not positive definite or
+ *   y_i  = -g_i - sum_{p<i} L_ip y_p  (p ascending)
+ *   x_i  = y_i inv_i - sum_{p>i} L_pi x_p  (p descending, i.e. as the x_p appear)
+ * *detOut = det(H / n) = prod_j (D_j * (1/n)), the Hessian determinant
+ * "after scaling" by the inlier count n; 0 when H is not
+ * positive definite.  Returns 0, or -1 when H is not positive definite or
  * det(H / n) < 1e-12 (degenerate). */
 static int sym6(int a, int b) { /* index of H_ab in the row-major upper triangle */
   if (a > b) {
@@ -1778,8 +1779,9 @@ int rfo_solve6(const double* sums, double* x, double* detOut) {
       L[i * 6 + j] = t * inv[j];
     }
   }
+  const double ninv = 1.0 / n;
   double det = 1.0;
-  for (int j = 0; j < 6; ++j) det *= D[j] / n;
+  for (int j = 0; j < 6; ++j) det *= D[j] * ninv;
   *detOut = det;
   if (!(det >= 1e-12)) return -1; /* SPEC.md:352 degenerate Hessian */
   double y[6];
@@ -1790,7 +1792,7 @@ int rfo_solve6(const double* sums, double* x, double* detOut) {
   }
   for (int i = 5; i >= 0; --i) {
     double t = y[i] * inv[i];
-    for (int p = i + 1; p < 6; ++p) t -= L[p * 6 + i] * x[p];
+    for (int p = 5; p > i; --p) t -= L[p * 6 + i] * x[p];
     x[i] = t;
   }
   return 0;

@@ -125,11 +125,7 @@ __device__ __forceinline__ void se3_series(double t, double& a, double& b, doubl
 }
 
 // rfo.c:se3_coeffs — the series below 1 rad, else halving + double angles
-__device__ __noinline__ void se3_coeffs(double th2, double& a, double& b, double& c) {
-  if (th2 < 1.0) {
-    se3_series(th2, a, b, c);
-    return;
-  }
+__device__ __noinline__ void se3_coeffs_large(double th2, double& a, double& b, double& c) {
   const double theta = sqrt(th2);
   double h = theta;
   int k = 0;
@@ -149,8 +145,15 @@ __device__ __noinline__ void se3_coeffs(double th2, double& a, double& b, double
   b = (1.0 - co) / th2;
   c = (theta - s) / (theta * th2);
 }
+__device__ __forceinline__ void se3_coeffs(double th2, double& a, double& b, double& c) {
+  if (th2 < 1.0)
+    se3_series(th2, a, b, c);
+  else
+    se3_coeffs_large(th2, a, b, c);
+}
 
-// rfo.c:rfo_solve6 — LDL^T of H (no square roots), det(H / n), substitution.
+// rfo.c:rfo_solve6 — LDL^T of H (no square roots), det(H / n) = prod D_j (1/n),
+// forward substitution (p ascending), back substitution (p descending).
 // Every loop has constant bounds and is fully unrolled, so the factorisation
 // lives in registers; a non-positive pivot raises `bad` (and is replaced by 1
 // so the rest stays finite) instead of leaving the unrolled code early.
@@ -186,11 +189,12 @@ __device__ __forceinline__ int solve6(const double* sums, double* x, double* det
       }
     }
   }
+  // (x is computed unconditionally: the degeneracy test is not on the
+  // substitution's dependency chain)
+  const double ninv = __drcp_rn(n);
   double det = 1.0;
 #pragma unroll
-  for (int j = 0; j < 6; ++j) det = __dmul_rn(det, __ddiv_rn(D[j], n));
-  *detOut = bad ? 0.0 : det;
-  if (bad || !(det >= 1e-12)) return -1;  // SPEC.md:352 degenerate Hessian
+  for (int j = 0; j < 6; ++j) det = __dmul_rn(det, __dmul_rn(D[j], ninv));
   double y[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
@@ -204,11 +208,21 @@ __device__ __forceinline__ int solve6(const double* sums, double* x, double* det
   for (int i = 5; i >= 0; --i) {
     double t = __dmul_rn(y[i], inv[i]);
 #pragma unroll
-    for (int p = 0; p < 6; ++p)
+    for (int p = 5; p >= 0; --p)
       if (p > i) t -= __dmul_rn(L[p * 6 + i], x[p]);
     x[i] = t;
   }
-  return 0;
+  *detOut = bad ? 0.0 : det;
+  return (bad || !(det >= 1e-12)) ? -1 : 0;  // SPEC.md:352 degenerate Hessian
+}
+
+// The evaluation's summary ratios (rfo_icp_track: inlier_fraction,
+// residual_mean, valid pixels); off the solve's path.
+__device__ __forceinline__ void icp_summary(GnShared& g) {
+  const double* acc = g.sums;
+  g.stats[8] = acc[30] > 0.0 ? acc[28] / acc[30] : 0.0;
+  g.stats[10] = acc[28] > 0.0 ? acc[29] / acc[28] : 0.0;
+  g.stats[11] = acc[30];
 }
 
 // One Gauss-Newton step on the CTA-local state (oracle: rfo_icp_track loop
@@ -216,12 +230,10 @@ __device__ __forceinline__ int solve6(const double* sums, double* x, double* det
 __device__ void gn_step(GnShared& g, int level, int minCount) {
   const double* acc = g.sums;
   double* st = g.stats;
+  // (st[8], st[10], st[11]: icp_summary, on another warp)
   st[1] = acc[28];
   st[2] = acc[27];
-  st[8] = acc[30] > 0.0 ? acc[28] / acc[30] : 0.0;
   st[9] = 0.0;
-  st[10] = acc[28] > 0.0 ? acc[29] / acc[28] : 0.0;
-  st[11] = acc[30];
   if (acc[28] < (double)minCount) {
     st[7] = 0.0;
     g.done = 1;
@@ -284,7 +296,7 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
 // camera-space points (pose-independent) in shared memory for the level's
 // later iterations.  Level 0 at 640x480 on 148 CTAs is 4.05 pixels per
 // thread: one cached round plus a few uncached pixels.
-constexpr int kIcpPx = 4;
+constexpr int kIcpPx = 5;     // 148 x 512 x 5 >= 640 x 480: one cached round at C1/C2
 constexpr int kIcpGroup = 2;  // projections + gathers issued 2 pixels at a time
 // pixels per thread between flushes of the per-thread fixed-point
 // accumulators (|term| < 2^16 H units, so 8 terms stay inside the 2^19 range)
@@ -417,8 +429,9 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
     int pix[kIcpGroup];
 #pragma unroll
     for (int j = 0; j < kIcpGroup; ++j) {
-      const float4 c = pcs[(kb + j) * kIcpThreads + threadIdx.x];
       pix[j] = -1;
+      if (kb + j >= kIcpPx) continue;
+      const float4 c = pcs[(kb + j) * kIcpThreads + threadIdx.x];
       pw[j] = f3{0.f, 0.f, 0.f};
       if (c.w > 0.f) {
         s.valid += 1;
@@ -504,6 +517,8 @@ __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& 
         g.done = 1;
       else
         gn_step(g, a.level, a.minCount);
+    } else if (threadIdx.x == 32) {
+      icp_summary(g);
     }
     __syncthreads();
 #ifdef RFG_ICP_LEVEL_ONLY
