@@ -13,6 +13,11 @@ pre-staged in HBM; L2 is flushed (256 MiB write) before every timed frame and
 timing uses CUDA events on the pipeline's stream around each frame.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload c2|c3|c4|c5]
+
+The headline line is C2 (the metric's config) unless --workload says
+otherwise; at N = 1 the line also carries the C3 (colour) and C4 (2 mm
+multi-room) frame rates and integration rooflines under "configs".
 
 Under torchrun (N > 1) the voxel-hash space is sharded spatially over the
 ranks (each allocates/integrates its own blocks + a 1-block halo) and the
@@ -197,8 +202,9 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
         "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 / fps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "frames_timed": n, "steps_requested": args.steps,
-                   "sample": f"frames {args.warmup}..{args.warmup + n - 1} of the orbit sequence"},
+        "config": {"workload": WORKLOAD},
+        "run": {"frames_timed": n, "steps_requested": args.steps,
+                "sample": f"frames {args.warmup}..{args.warmup + n - 1} of the orbit sequence"},
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": 1, "kind": kind,
                          "sample": f"{n} frames after {args.warmup} warm-up frames; single-threaded reference "
                                    "(oracle/_ref = /root/reference/proj sources) + C-port ICP",
@@ -210,29 +216,30 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------------ B200
-def cupti_kernel_ms(pipe, raw_dev, poses, flush, warmup, n, name):
-    """Mean device duration (ms) of kernel `name` over frames warmup..warmup+n-1
-    replayed through the pipeline's frame graph (torch.profiler / CUPTI)."""
+def cupti_kernel_us(step, stream, flush, frames):
+    """Mean device duration (us) of each of our kernels per launch and per
+    frame over `frames` (torch.profiler / CUPTI activity records: the same
+    quantity as ncu's gpu__time_duration), L2 flushed before each frame."""
     import torch
     from torch.profiler import ProfilerActivity, profile
 
-    stream = torch.cuda.ExternalStream(pipe.stream)
-    torch.cuda.synchronize()
-    pipe.map.clear()
-    pipe.reset()
-    for f in range(warmup):
-        pipe.process(raw_dev[f], poses[0] if f == 0 else None)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        for f in range(warmup, min(N_FRAMES, warmup + n)):
+        for f in frames:
             flush.fill_(f & 0xFF)
             stream.wait_stream(torch.cuda.current_stream())
-            pipe.process(raw_dev[f])
+            with torch.cuda.stream(stream):
+                step(f)
             torch.cuda.current_stream().wait_stream(stream)
         torch.cuda.synchronize()
-    d = [e.time_range.end - e.time_range.start for e in prof.events()
-         if e.device_type == torch.autograd.DeviceType.CUDA and name in e.name]
-    return float(np.mean(d)) / 1e3 if d else None
+    acc = {}
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA and "rfg::" in e.name:
+            name = e.name.split("(")[0].replace("void ", "").split("<")[0]
+            acc.setdefault(name, []).append(e.time_range.end - e.time_range.start)
+    n = max(len(frames), 1)
+    return {k: {"us_per_launch": float(np.mean(v)), "us_per_frame": float(np.sum(v)) / n, "launches": len(v)}
+            for k, v in acc.items()}
 
 
 _JSON_OUT = None
@@ -256,93 +263,211 @@ def emit(line: dict):
     out.flush()
 
 
-def make_frames():
+# The BASELINE.json configs as workloads.  c2 is the headline (configs[1]).
+WORKLOADS = {
+    "c2": dict(desc=WORKLOAD, scene=0, n=N_FRAMES, voxel=0.005, mapcfg=MAPCFG, colour=False, track=True),
+    "c3": dict(desc="C3: ITMVoxel_s_rgb colour fusion, sphere-in-room orbit 300 frames 640x480 depth + RGB, known "
+                    "poses, 4 mm voxels, mu 2 cm, 0x40000-bucket hash; step = 1 frame: view + RGB pack + alloc + "
+                    "visible + integrate (depth + colour) + ranges + raycast",
+               scene=0, n=300, voxel=0.004, mapcfg=MAPCFG, colour=True, track=False),
+    "c4": dict(desc="C4: builder-defined multi-room scene, 100 frames 640x480, known poses, 2 mm voxels, mu 2 cm, "
+                    "2^21-bucket hash (+2^19 excess, 2^22 blocks), swapping off; step = 1 frame: view + alloc + "
+                    "visible + integrate + ranges + raycast",
+               scene=1, n=100, voxel=0.002, mapcfg=(1 << 21, 1 << 19, 1 << 22), colour=False, track=False),
+}
+WORKLOADS["c5"] = dict(WORKLOADS["c4"], desc="C5: the C4 scene with the voxel-hash space sharded over the ranks "
+                                             "(owner = hash of 8^3-block super-tiles, 1-block halo), raycast "
+                                             "composed by a per-pixel nearest-hit NCCL reduction", sharded=True)
+
+
+def make_frames(wl=None):
     from paper_1708_00783_b200 import fusion as F
+    wl = wl or WORKLOADS["c2"]
     intr = F.Intrinsics(**INTR)
-    poses = F.orbit_trajectory(frames=N_FRAMES)
-    raws = np.stack([F.synth_render(F.SCENE_SPHERE_IN_ROOM, poses[f], intr)[0] for f in range(N_FRAMES)])
-    return poses, raws
+    poses = F.orbit_trajectory(frames=wl["n"]) if wl["scene"] == 0 else F.multiroom_trajectory(wl["n"])
+    raws, rgbs = [], []
+    for f in range(wl["n"]):
+        raw, _, rgb = F.synth_render(wl["scene"], poses[f], intr, rgb=wl["colour"])
+        raws.append(raw)
+        rgbs.append(rgb)
+    return poses, np.stack(raws), (np.stack(rgbs) if wl["colour"] else None)
+
+
+class Workload:
+    """One BASELINE config on this rank: frames staged in HBM, a map and a
+    (sharded when world > 1) frame pipeline."""
+
+    def __init__(self, name, rank, world, local, sharded, profile=False):
+        import torch
+        from paper_1708_00783_b200 import fusion as F
+        self.name, self.wl = name, WORKLOADS[name]
+        wl = self.wl
+        self.intr = F.Intrinsics(**INTR)
+        self.params = F.SceneParams(**dict(PARAMS, voxelSize=wl["voxel"]))
+        self.poses, raws, rgbs = make_frames(wl)
+        self.raws_host = raws
+        self.rgbs_host = rgbs
+        self.raw_dev = torch.from_numpy(raws.view(np.int16)).cuda()
+        self.rgb_dev = torch.from_numpy(rgbs).cuda() if rgbs is not None else None
+        self.n = wl["n"]
+        self.track = wl["track"]
+        self.map = F.VoxelBlockMap(F.VoxelBlockMapConfig(*wl["mapcfg"]), device=local, colour=wl["colour"])
+        self.sharded = sharded
+        if sharded:
+            from paper_1708_00783_b200.shard import ShardedPipeline
+            self.map.set_shard(rank, world, 3)
+            self.pipe = ShardedPipeline(self.map, self.intr, self.params, rank, world, levels=3, iters=ICP_ITERS,
+                                        dist=ICP_DIST, track=self.track)
+        else:
+            self.pipe = F.Pipeline(self.map, self.intr, self.params, F.DepthAffine(*AFF), levels=3, track=self.track,
+                                   iters=ICP_ITERS, dist=ICP_DIST, use_graph=True, profile=profile,
+                                   colour=wl["colour"])
+        self.stream = torch.cuda.ExternalStream(self.pipe.stream)
+
+    def reset(self):
+        import torch
+        torch.cuda.synchronize()
+        self.map.clear()
+        self.pipe.reset()
+        torch.cuda.synchronize()
+
+    def pose_arg(self, f):
+        return self.poses[f] if (f == 0 or not self.track) else None
+
+    def step(self, f):
+        """One frame from HBM (frame index f of the sequence)."""
+        rgb = self.rgb_dev[f] if self.rgb_dev is not None else None
+        if rgb is not None:
+            self.pipe.process(self.raw_dev[f], self.pose_arg(f), rgb=rgb)
+        else:
+            self.pipe.process(self.raw_dev[f], self.pose_arg(f))
+
+    def bytes_in(self):
+        n = INTR["width"] * INTR["height"]
+        return n * 2 + (n * 3 if self.rgb_dev is not None else 0)
+
+
+def timed_frames(w, flush, order, warmup):
+    """Device ms per frame (CUDA events on the pipeline's stream around each
+    frame, L2 flushed before each, outside the pair) for frames order[warmup:]."""
+    import torch
+    evs = []
+    for i, f in enumerate(order):
+        if f == 0:
+            w.reset()
+        flush.fill_(i & 0xFF)  # evict L2 (untimed; outside the event pair)
+        w.stream.wait_stream(torch.cuda.current_stream())  # the frame starts after the flush
+        with torch.cuda.stream(w.stream):
+            if i >= warmup:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(w.stream)
+            w.step(f)
+            if i >= warmup:
+                b.record(w.stream)
+                evs.append((a, b))
+        torch.cuda.current_stream().wait_stream(w.stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def integrate_bytes(nvis, colour):
+    """Algorithmic bytes of one integration launch (SURVEY §8(d) B_int with the
+    4-B depth plane): read + write 2 KiB of depth voxels per visible block
+    (+ the same for the colour plane) + the depth image (+ the RGBA image)."""
+    n = INTR["width"] * INTR["height"]
+    return nvis * 2 * 512 * 4 * (2 if colour else 1) + n * 4 + (n * 4 if colour else 0)
+
+
+def measure_config(name, flush, peak, n_frames, warmup=5):
+    """A side config (c3 / c4) on one GPU: frames/s over frames warmup..,
+    and the integration kernel's roofline from CUPTI durations."""
+    import torch
+    w = Workload(name, 0, 1, torch.cuda.current_device(), sharded=False)
+    total = min(w.n, warmup + n_frames)
+    ms = timed_frames(w, flush, list(range(total)), warmup)
+    w.reset()
+    nvis = []
+    for f in range(warmup):
+        w.step(f)
+    kt = cupti_kernel_us(w.step, w.stream, flush, range(warmup, total))
+    w.reset()
+    for f in range(total):
+        w.step(f)
+        nvis.append(w.pipe.result()[0].visibleCount)
+    mean_vis = float(np.mean(nvis[warmup:]))
+    kname = "rfg::k_integrate_rgbd" if w.wl["colour"] else "rfg::k_integrate_depth"
+    out = {"workload": w.wl["desc"], "frames_timed": len(ms), "value": len(ms) / (sum(ms) / 1e3),
+           "unit": UNIT, "ms_per_step": float(np.mean(ms)), "mean_visible_blocks": mean_vis}
+    if kname in kt:
+        b = integrate_bytes(mean_vis, w.wl["colour"])
+        us = kt[kname]["us_per_launch"]
+        out["integrate"] = {"kernel": kname, "us": us, "algorithmic_bytes_per_launch": b,
+                            "achieved_GBps": b / (us * 1e-6) / 1e9, "frac": b / (us * 1e-6) / 1e9 / peak}
+    out["kernel_us_per_frame"] = {k: round(v["us_per_frame"], 2) for k, v in
+                                  sorted(kt.items(), key=lambda x: -x[1]["us_per_frame"])}
+    del w
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_b200(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1708_00783_b200 import fusion as F
     from paper_1708_00783_b200._lib import launch_count
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    sharded = world > 1 or args.sharded
+    wl_name = args.workload
+    sharded = world > 1 or args.sharded or WORKLOADS[wl_name].get("sharded", False)
     if sharded:
-        if world == 1:  # --sharded on one GPU: the N > 1 code path with a world of one
+        if world == 1:  # the N > 1 code path with a world of one
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    intr = F.Intrinsics(**INTR)
-    params = F.SceneParams(**PARAMS)
-    poses, raws = make_frames()
-    raw_dev = torch.from_numpy(raws.view(np.int16)).cuda()
+    peak, peak_kind = load_peaks()
+    w = Workload(wl_name, rank, world, local, sharded)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    if sharded:
-        from paper_1708_00783_b200.shard import ShardedPipeline
-        make_pipe = lambda m, graph, profile=False: ShardedPipeline(  # noqa: E731
-            m, intr, params, rank, world, levels=3, iters=ICP_ITERS, dist=ICP_DIST)
-    else:
-        make_pipe = lambda m, graph, profile=False: F.Pipeline(  # noqa: E731
-            m, intr, params, F.DepthAffine(*AFF), levels=3, track=True, iters=ICP_ITERS, dist=ICP_DIST,
-            use_graph=graph, profile=profile)
-
-    m = F.VoxelBlockMap(F.VoxelBlockMapConfig(*MAPCFG), device=local)
-    if sharded:
-        m.set_shard(rank, world, 3)
-    pipe = make_pipe(m, True)
-    stream = torch.cuda.ExternalStream(pipe.stream)
-
-    def reset():
-        torch.cuda.synchronize()
-        m.clear()
-        pipe.reset()
-        torch.cuda.synchronize()
-
-    # ---- timed region: warmup W frames, then K frames (sequence restarts with
-    # a fresh map, untimed, every 100 frames) ----
+    # ---- timed region: warmup W frames, then K frames (the sequence restarts
+    # with a fresh map, untimed, every n frames) ----
     total = args.warmup + args.steps
-    order = [i % N_FRAMES for i in range(total)]
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    order = [i % w.n for i in range(total)]
     sampler = ClockSampler(local, period_ms=max(args.clock_ms, 1))
     if args.clock_ms > 0:
         sampler.start()
-    launches0 = None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    launches0 = [None]
+
+    evs = []
     for i, f in enumerate(order):
         if f == 0:
-            reset()
+            w.reset()
         if i == args.warmup:
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             sampler.mark()
-            launches0 = launch_count()
+            launches0[0] = launch_count()
         flush.fill_(i & 0xFF)  # evict L2 (untimed; outside the event pair)
-        # the frame starts after the flush has finished (ordered on the device)
-        stream.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(stream):
+        w.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(w.stream):
             if i >= args.warmup:
-                evs[i - args.warmup][0].record(stream)
-            pipe.process(raw_dev[f], poses[0] if f == 0 else None)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(w.stream)
+            w.step(f)
             if i >= args.warmup:
-                evs[i - args.warmup][1].record(stream)
-        torch.cuda.current_stream().wait_stream(stream)
+                b.record(w.stream)
+                evs.append((a, b))
+        torch.cuda.current_stream().wait_stream(w.stream)
     torch.cuda.synchronize()
-    launches = launch_count() - launches0
+    launches = launch_count() - launches0[0]
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms_total = float(sum(step_ms))
@@ -352,22 +477,27 @@ def run_b200(args):
         ms_total = float(t.item())
         dist.barrier()
     fps = args.steps / (ms_total / 1e3)  # one frame stream (strong scaling over ranks)
-    stats, pose_out, icp = pipe.result()
+    stats, pose_out, icp = w.pipe.result()
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if args.e2e_steps > 0:
-        raw_pinned = torch.from_numpy(raws.view(np.int16)).pin_memory()
-        reset()
+        raw_pinned = torch.from_numpy(w.raws_host.view(np.int16)).pin_memory()
+        rgb_pinned = torch.from_numpy(w.rgbs_host).pin_memory() if w.rgbs_host is not None else None
+        w.reset()
         e2e_total = 0.0
-        n_e2e = min(args.e2e_steps, N_FRAMES)
+        n_e2e = min(args.e2e_steps, w.n)
         warm = min(args.warmup, n_e2e - 1)
         for f in range(n_e2e):
             flush.fill_(f & 0xFF)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            pipe.process(raw_pinned[f].numpy().view(np.uint16), poses[0] if f == 0 else None)
-            st, _, _ = pipe.result()  # D2H of stats + pose + ICP summary
+            raw_h = raw_pinned[f].numpy().view(np.uint16)
+            if rgb_pinned is not None:
+                w.pipe.process(raw_h, w.pose_arg(f), rgb=rgb_pinned[f].numpy())
+            else:
+                w.pipe.process(raw_h, w.pose_arg(f))
+            st, _, _ = w.pipe.result()  # D2H of stats + pose + ICP summary
             t1 = time.perf_counter()
             if f >= warm:
                 e2e_total += t1 - t0
@@ -375,62 +505,103 @@ def run_b200(args):
             t = torch.tensor([e2e_total], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_total = float(t.item())
-        e2e = {"value": (n_e2e - warm) / e2e_total, "unit": UNIT, "h2d_bytes_per_step": INTR["width"] * INTR["height"] * 2,
-               "d2h_bytes_per_step": 64 + 48 + 64, "frames": n_e2e - warm,
-               "path": "Pipeline.process(host raw u16) + Pipeline.result() per frame (rfg_pipeline_process_host/result)"}
+        e2e = {"value": (n_e2e - warm) / e2e_total, "unit": UNIT, "h2d_bytes_per_step": w.bytes_in(),
+               "d2h_bytes_per_step": 64 + 48 + 8 * 12 + 4, "frames": n_e2e - warm,
+               "path": "Pipeline.process(host raw u16 [+ rgb]) + Pipeline.result() per frame "
+                       "(rfg_pipeline_process_host / _rgbd_host, rfg_pipeline_result)"}
 
-    # ---- per-stage device times: the same frames replayed through the same
-    # frame graph with event-record nodes between the stages ----
-    prof = None
-    roof = None
-    if world == 1 and args.profile_frames > 0:
-        ppipe = F.Pipeline(m, intr, params, F.DepthAffine(*AFF), levels=3, track=True, iters=ICP_ITERS,
-                           dist=ICP_DIST, use_graph=True, profile=True)
+    # ---- per-stage device times (event-record nodes inside the frame graph)
+    # and per-kernel device durations (CUPTI) over the same frames ----
+    prof = roof = secondary = kt = None
+    if args.profile_frames > 0 and not sharded:
+        from paper_1708_00783_b200 import fusion as F
+        nprof = min(w.n, args.warmup + args.profile_frames)
+        ppipe = F.Pipeline(w.map, w.intr, w.params, F.DepthAffine(*AFF), levels=3, track=w.track, iters=ICP_ITERS,
+                           dist=ICP_DIST, use_graph=True, profile=True, colour=w.wl["colour"])
         torch.cuda.synchronize()
-        m.clear()
+        w.map.clear()
         ppipe.reset()
-        acc, nvis = {}, []
+        acc, nvis, icp_bytes = {}, [], []
         n_prof = 0
-        for f in range(min(N_FRAMES, args.warmup + args.profile_frames)):
+        for f in range(nprof):
             flush.fill_(f & 0xFF)
             torch.cuda.synchronize()
-            ppipe.process(raw_dev[f], poses[0] if f == 0 else None)
+            rgb = w.rgb_dev[f] if w.rgb_dev is not None else None
+            if rgb is not None:
+                ppipe.process(w.raw_dev[f], w.pose_arg(f), rgb=rgb)
+            else:
+                ppipe.process(w.raw_dev[f], w.pose_arg(f))
             st_ms = ppipe.stage_times()
-            st, _, _ = ppipe.result()
+            st, _, icp_f = ppipe.result()
             if f >= args.warmup:
                 n_prof += 1
                 nvis.append(st.visibleCount)
+                # tracker: per iteration and level pixel, a 4-B depth read and a
+                # 32-B point + normal gather (SURVEY §8(d) B_icp)
+                npx = [INTR["width"] * INTR["height"] >> (2 * lv) for lv in range(3)]
+                icp_bytes.append(sum(icp_f[4 + lv] * npx[lv] * 36 for lv in range(3)))
                 for k, v in st_ms.items():
                     acc[k] = acc.get(k, 0.0) + v
         prof = {k: v / n_prof for k, v in acc.items()}
-        peak, peak_kind = load_peaks()
+        del ppipe
         mean_vis = float(np.mean(nvis))
-        # integration: 2 x 2 KiB depth plane per visible block + the depth image
-        int_bytes = mean_vis * 2 * 512 * 4 + INTR["width"] * INTR["height"] * 4
-        achieved = int_bytes / (prof["integrate"] * 1e-3) / 1e9
+        # the same frames through the plain frame graph, kernel by kernel (CUPTI)
+        w.reset()
+        for f in range(args.warmup):
+            w.step(f)
+        kt = cupti_kernel_us(w.step, w.stream, flush, range(args.warmup, nprof))
+        kname = "rfg::k_integrate_rgbd" if w.wl["colour"] else "rfg::k_integrate_depth"
+        int_bytes = integrate_bytes(mean_vis, w.wl["colour"])
         traffic = None
         try:
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                traffic = json.load(f).get("integrate_dram_bytes_per_launch")
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                traffic = json.load(fh).get("integrate_dram_bytes_per_launch")
         except Exception:
             pass
-        roof = {"kernel": "k_integrate (TSDF integration, rfg_integrate.cu)", "bound": "hbm", "achieved": achieved,
-                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+        k_us = kt.get(kname, {}).get("us_per_launch")
+        ev_ms = prof["integrate"]
+        roof = {"kernel": f"{kname} (TSDF integration, rfg_integrate.cu)", "bound": "hbm",
+                "achieved": int_bytes / (k_us * 1e-6) / 1e9 if k_us else None, "peak": peak, "unit": "GB/s",
+                "frac": int_bytes / (k_us * 1e-6) / 1e9 / peak if k_us else None, "traffic": traffic,
                 "peak_source": peak_kind, "algorithmic_bytes_per_launch": int_bytes,
-                "mean_visible_blocks": mean_vis, "launch_ms": prof["integrate"]}
-        # cross-check: the kernel's own device duration (CUPTI activity records,
-        # as ncu's gpu__time_duration) in the plain frame graph, same frames;
-        # the event pair above also holds the event-record nodes' latency
-        try:
-            kms = cupti_kernel_ms(pipe, raw_dev, poses, flush, args.warmup, args.profile_frames, "k_integrate_depth")
-            if kms:
-                roof["kernel_ms_cupti"] = kms
-                roof["achieved_cupti"] = int_bytes / (kms * 1e-3) / 1e9
-                roof["frac_cupti"] = roof["achieved_cupti"] / peak
-        except Exception as e:  # informational only
-            roof["kernel_ms_cupti"] = None
-            roof["cupti_error"] = str(e)[:200]
-        del ppipe
+                "mean_visible_blocks": mean_vis, "launch_us": k_us,
+                "timing": "kernel device duration from CUPTI activity records (= ncu gpu__time_duration), "
+                          "measured live in this run over the profiled frames",
+                "launch_us_events": ev_ms * 1e3,
+                "achieved_events": int_bytes / (ev_ms * 1e-3) / 1e9,
+                "frac_events": int_bytes / (ev_ms * 1e-3) / 1e9 / peak,
+                "events_note": "CUDA-event pair around the kernel inside the frame graph (event-record nodes); "
+                               "includes the nodes' own latency"}
+        secondary = []
+        rc = kt.get("rfg::k_raycast_tiles")
+        if rc:
+            b = INTR["width"] * INTR["height"] * (8 + 3 * 16)
+            secondary.append({"kernel": "rfg::k_raycast_tiles (ranges + march + normals)",
+                              "bound": "latency: the longest ray's chain of dependent voxel gathers",
+                              "launch_us": rc["us_per_launch"], "algorithmic_bytes_per_launch": b,
+                              "achieved": b / (rc["us_per_launch"] * 1e-6) / 1e9, "peak": peak, "unit": "GB/s",
+                              "frac": b / (rc["us_per_launch"] * 1e-6) / 1e9 / peak,
+                              "bytes_note": "range read + raycast/points/normals written per pixel; the voxel "
+                                            "gathers (L1/L2 hits) are not counted"})
+        it = kt.get("rfg::k_icp_track")
+        if it and icp_bytes:
+            b = float(np.mean(icp_bytes))
+            secondary.append({"kernel": "rfg::k_icp_track (whole coarse-to-fine track, one cooperative launch)",
+                              "bound": "latency: one grid barrier + a serial 6x6 LDL^T solve per Gauss-Newton "
+                                       "iteration", "launch_us": it["us_per_launch"],
+                              "algorithmic_bytes_per_launch": b,
+                              "achieved": b / (it["us_per_launch"] * 1e-6) / 1e9, "peak": peak, "unit": "GB/s",
+                              "frac": b / (it["us_per_launch"] * 1e-6) / 1e9 / peak})
+        w.reset()
+
+    configs = None
+    if rank == 0 and world == 1 and args.configs and wl_name == "c2":
+        configs = {}
+        for cname, nf in (("c3", args.config_frames), ("c4", args.config_frames)):
+            try:
+                configs[cname] = measure_config(cname, flush, peak, nf)
+            except Exception as e:  # side measurements must not take the bench down
+                configs[cname] = {"error": str(e)[:300]}
 
     if rank != 0:
         if world > 1:
@@ -438,7 +609,7 @@ def run_b200(args):
         return 0
 
     cpu = None
-    if args.cpu_frames > 0 and world == 1:
+    if args.cpu_frames > 0 and world == 1 and wl_name == "c2":
         try:
             v, kind, n, per = cpu_reference_run(2, args.cpu_frames)
             cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
@@ -451,11 +622,21 @@ def run_b200(args):
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "l2": "flushed (256 MiB write) before every timed frame",
-                   "parallelism": f"spatial hash shards x{world}" if sharded else "single GPU",
-                   "graph": True, "last_frame_stats": stats.as_array().tolist(),
-                   "icp_last": {"iterations": int(icp[0]), "count": int(icp[1]), "per_level": icp[4:7].tolist()}},
-        "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roof, "stage_ms": prof,
+        "config": {"workload": w.wl["desc"]},
+        "run": {"l2": "flushed (256 MiB write) before every timed frame", "graph": True,
+                "parallelism": f"spatial hash shards x{world}" if sharded else "single GPU",
+                "gpus_active": world, "last_frame_stats": stats.as_array().tolist(),
+                "icp_last": {"iterations": int(icp[0]), "count": int(icp[1]), "per_level": icp[4:7].tolist(),
+                             "inlier_fraction": float(icp[8]), "hessian_det": float(icp[9])},
+                "scaling_note": "one frame stream at every N (strong): allocation and integration split over the "
+                                "ranks' spatial shards, while view, tracker and the per-pixel march run on every "
+                                "rank and the composition adds two all-reduces per frame, so N GPUs buy map "
+                                "capacity, not frame rate (DESIGN.md §7)" if sharded else None},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roof,
+        "roofline_secondary": secondary, "stage_ms": prof,
+        "kernel_us_per_frame": {k: round(v["us_per_frame"], 2) for k, v in
+                                sorted(kt.items(), key=lambda x: -x[1]["us_per_frame"])} if kt else None,
+        "configs": configs,
         "cpu_baseline": cpu, "step_ms_p50": float(np.median(step_ms)), "step_ms_max": float(np.max(step_ms)),
     }
     emit(line)
@@ -470,9 +651,13 @@ def main():
     ap.add_argument("--steps", type=int, default=95)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS),
+                    help="BASELINE config of the headline line (c2 = configs[1], the metric's config)")
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--profile-frames", type=int, default=95)
     ap.add_argument("--cpu-frames", type=int, default=5)
+    ap.add_argument("--configs", type=int, default=1, help="also measure C3 and C4 on one GPU (side lines)")
+    ap.add_argument("--config-frames", type=int, default=95)
     ap.add_argument("--sharded", action="store_true", help="run the sharded (N > 1) pipeline even at N = 1")
     ap.add_argument("--clock-ms", type=int, default=5, help="nvidia-smi clock sampling period (0 = off)")
     ap.add_argument("--ref-budget", type=float, default=150.0, help="reference arm time budget (s)")

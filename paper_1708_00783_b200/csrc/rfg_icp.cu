@@ -35,7 +35,7 @@ namespace cg = cooperative_groups;
 
 namespace rfg {
 
-constexpr int kIcpThreads = 512;
+constexpr int kIcpThreads = 512;  // 16 warps: more would cap the registers at 96 (5 warps per SM sub-partition)
 constexpr int kIcpSums = 31;   // H upper 21, g 6, sum r^2, inliers, sum |r|, valid pixels
 constexpr int kIcpStats = 12;  // TrackerIterationSummary (include/rfg.h)
 // fixed-point scale (log2) per sum; 0 = plain integer count (rfo.c:kIcpShift)
@@ -296,7 +296,7 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
 // camera-space points (pose-independent) in shared memory for the level's
 // later iterations.  Level 0 at 640x480 on 148 CTAs is 4.05 pixels per
 // thread: one cached round plus a few uncached pixels.
-constexpr int kIcpPx = 5;     // 148 x 512 x 5 >= 640 x 480: one cached round at C1/C2
+constexpr int kIcpPx = 5;  // 148 x 512 x 5 >= 640 x 480: one cached round at C1/C2
 constexpr int kIcpGroup = 2;  // projections + gathers issued 2 pixels at a time
 // pixels per thread between flushes of the per-thread fixed-point
 // accumulators (|term| < 2^16 H units, so 8 terms stay inside the 2^19 range)
@@ -362,8 +362,10 @@ __device__ __forceinline__ int icp_associate(const IcpLevelArgs& a, const Pose& 
 // accumulator `dst` (64-bit atomics; integer sums, so the order is
 // irrelevant).  Warp: recursive halving (lane l ends with sum l: 31
 // shuffles of 64 bits instead of 31 x 5); CTA: shared memory.
-__device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[32], unsigned long long* dst) {
+__device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[32], unsigned long long* dst,
+                                              int activeWarps) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid < activeWarps) {  // warps without pixels hold zeros: skip their reduction
   long long v[32];
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
@@ -387,32 +389,41 @@ __device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[3
     }
   }
   sh[wid][lane] = v[0];
+  }
   __syncthreads();
   if (threadIdx.x < kIcpSums) {
     long long t = 0;
 #pragma unroll
-    for (int w = 0; w < kIcpThreads / 32; ++w) t += sh[w][threadIdx.x];
+    for (int w = 0; w < kIcpThreads / 32; ++w)
+      if (w < activeWarps) t += sh[w][threadIdx.x];
     if (t) atomicAdd(dst + threadIdx.x, (unsigned long long)t);
   }
   __syncthreads();  // sh is reused by the next round
 }
 
-// One evaluation's contribution of this CTA: its pixels p0 + k * pstride
+// One evaluation's contribution of this CTA: its contiguous pixel range
+// [p0, p0 + span), thread t taking pixels p0 + t + k * kIcpThreads
 // (k < kIcpPx: camera points cached when `fill`; the rest uncached), added
-// to dst.  Returns false when a world point was outside the fixed-point range.
+// to dst.  Every CTA has the same span, so they all run the same number of
+// flushes.  Returns false when a world point was outside the fixed-point
+// range.  (The sums are order-independent integers, so the pixel-to-thread
+// mapping does not change them.)
 __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShared& g, const Pose& rp,
-                                             const Intr& inl, float dist2, int n, int p0, int pstride,
+                                             const Intr& inl, float dist2, int n, int p0, int span,
                                              long long (*sh)[32], float4* pcs, bool fill, unsigned long long* dst) {
   const Pose c2w = pose_from12(g.c2wF);
+  const int t = threadIdx.x;
+  const int activeWarps = min(kIcpThreads, span) / 32;  // span is a multiple of 32
   bool ok = true;
   IcpAcc s;
   acc_reset(s);
   if (fill) {
 #pragma unroll
     for (int k = 0; k < kIcpPx; ++k) {
-      const int p = p0 + k * pstride;
+      const int o = t + k * kIcpThreads;
+      const int p = p0 + o;
       float4 c = make_float4(0.f, 0.f, 0.f, -1.f);
-      if (p < n) {
+      if (o < span && p < n) {
         const float d = __ldg(a.depth + p);
         if (d > 0.f) {
           const int x = p % a.lw, y = p / a.lw;
@@ -420,18 +431,19 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
           c = make_float4(pc.x, pc.y, pc.z, 1.f);
         }
       }
-      pcs[k * kIcpThreads + threadIdx.x] = c;  // each thread reads back only its own slots
+      pcs[k * kIcpThreads + t] = c;  // each thread reads back only its own slots
     }
   }
 #pragma unroll
   for (int kb = 0; kb < kIcpPx; kb += kIcpGroup) {
+    if (kb * kIcpThreads >= span) break;  // uniform
     f3 pw[kIcpGroup];
     int pix[kIcpGroup];
 #pragma unroll
     for (int j = 0; j < kIcpGroup; ++j) {
       pix[j] = -1;
       if (kb + j >= kIcpPx) continue;
-      const float4 c = pcs[(kb + j) * kIcpThreads + threadIdx.x];
+      const float4 c = pcs[(kb + j) * kIcpThreads + t];
       pw[j] = f3{0.f, 0.f, 0.f};
       if (c.w > 0.f) {
         s.valid += 1;
@@ -451,19 +463,16 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
     for (int j = 0; j < kIcpGroup; ++j)
       if (pix[j] >= 0) ok &= icp_add(s, pw[j], V[j], N[j], dist2);
   }
-  // the pixels beyond the cached slots, uncached: k = kIcpPx.. of this
-  // thread's sequence p0 + k * pstride, flushed every kIcpFlush pixels (the
-  // fixed-point accumulators' range); every CTA runs the same number of
-  // flushes (they depend on n and pstride only)
-  for (int k = kIcpPx;; ++k) {
-    const int base = k * pstride;
-    if (base >= n) break;  // uniform: pixels p0 + base exist in some CTA iff base < n
+  // pixels beyond the cached slots (large images), uncached, flushed every
+  // kIcpFlush pixels (the fixed-point accumulators' range)
+  for (int k = kIcpPx; k * kIcpThreads < span; ++k) {
     if (k % kIcpFlush == 0) {
-      icp_cta_flush(s, sh, dst);
+      icp_cta_flush(s, sh, dst, activeWarps);
       acc_reset(s);
     }
-    const int p = p0 + base;
-    if (p >= n) continue;
+    const int o = t + k * kIcpThreads;
+    const int p = p0 + o;
+    if (o >= span || p >= n) continue;
     const float d = __ldg(a.depth + p);
     if (!(d > 0.f)) continue;
     s.valid += 1;
@@ -474,13 +483,17 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
     if (pix < 0) continue;
     ok &= icp_add(s, pw, __ldg(a.points + pix), __ldg(a.normals + pix), dist2);
   }
-  icp_cta_flush(s, sh, dst);
+  icp_cta_flush(s, sh, dst, activeWarps);
   return ok;
 }
 
+// Pixels per CTA when n pixels are spread over nCta CTAs (a multiple of 32).
+__host__ __device__ __forceinline__ int icp_span(int n, int nCta) { return ((n + nCta - 1) / nCta + 31) & ~31; }
+
 // One level's Gauss-Newton loop on the CTA-local state g.  CTAs with
-// blockIdx.x < nCta own the level's pixels (grid stride nCta x kIcpThreads);
-// the others only join the barriers and run the same solve.  `gi` counts
+// blockIdx.x < nCta own the level's pixels (contiguous ranges of
+// icp_span(n, nCta)); the others only join the barriers and run the same
+// solve.  `gi` counts
 // iterations across levels (accumulator rotation, with the launch's `gen`).
 __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& a, int nCta, GnShared& g,
                                               long long (*sh)[32], float4* pcs, unsigned gen, int& gi,
@@ -497,8 +510,8 @@ __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& 
     if (timed) t0 = gtimer();
     unsigned long long* buf = st->acc[(gen + gi) % 3];
     if (owner) {
-      const bool ok = icp_cta_eval(a, g, rp, inl, dist2, n, blockIdx.x * blockDim.x + threadIdx.x,
-                                   nCta * blockDim.x, sh, pcs, it == 0, buf);
+      const int span = icp_span(n, nCta);
+      const bool ok = icp_cta_eval(a, g, rp, inl, dist2, n, blockIdx.x * span, span, sh, pcs, it == 0, buf);
       if (!ok) st->error = 1;
     }
     if (blockIdx.x == 0 && threadIdx.x < 32) st->acc[(gen + gi + 1) % 3][threadIdx.x] = 0ull;
@@ -554,7 +567,7 @@ __device__ __forceinline__ void icp_publish(IcpState* st, const GnShared& g, con
 }
 
 // Single evaluation / single level on the state in `st` (rfg_icp_reduce).
-__global__ void __launch_bounds__(kIcpThreads) k_icp_level(IcpState* st, IcpLevelArgs a) {
+__global__ void __launch_bounds__(kIcpThreads, 1) k_icp_level(IcpState* st, IcpLevelArgs a) {
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
@@ -594,7 +607,7 @@ struct IcpTrackArgs {
   float* renderPoseOut;  // nullable: the next frame's render pose := the output pose
 };
 
-__global__ void __launch_bounds__(kIcpThreads) k_icp_track(IcpState* st, IcpTrackArgs ta) {
+__global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpTrackArgs ta) {
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
@@ -680,7 +693,10 @@ static int icp_grid(int n) {
     if (perSm < 1 || perSmTrack < 1) sms = -1;
   }
   if (sms <= 0) return 0;
-  const int want = (n + kIcpThreads - 1) / kIcpThreads;
+  // every SM takes a part of every level (at least a warp of pixels per CTA):
+  // spreading a coarse level over all SMs leaves fewer busy warps per SM for
+  // the accumulation and the CTA reduction
+  const int want = (n + 31) / 32;
   return want < 1 ? 1 : (want < sms ? want : sms);
 }
 

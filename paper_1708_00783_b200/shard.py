@@ -84,10 +84,10 @@ class ShardedPipeline:
     def __init__(self, map: F.VoxelBlockMap, intr: F.Intrinsics, params: F.SceneParams, rank: int, world: int,
                  levels: int = 3, iters=(6, 10, 20), dist=(0.01, 0.02, 0.04),
                  affine: F.DepthAffine = F.DepthAffine(1.0 / 5000.0, 0.0), min_count: int = 10,
-                 use_graph: bool = True):
+                 use_graph: bool = True, track: bool = True):
         self.map, self.intr, self.params = map, intr, params
         self.rank, self.world = rank, world
-        self.pipe = F.Pipeline(map, intr, params, affine, levels=levels, track=True, iters=iters, dist=dist,
+        self.pipe = F.Pipeline(map, intr, params, affine, levels=levels, track=track, iters=iters, dist=dist,
                                min_count=min_count, use_graph=use_graph)
         self.n = intr.width * intr.height
         _, _, raycast, points, normals = self.pipe.buffers()
