@@ -12,6 +12,21 @@
 namespace rfg {
 
 std::atomic<uint64_t> g_launches{0};
+
+int current_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int n = dev < 64 ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (!n) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    if (dev < 64) cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 static thread_local std::string t_lastError;
 void set_error(const std::string& msg) { t_lastError = msg; }
 
@@ -140,7 +155,11 @@ int ensure_range_scratch(rfg_map* m, int width, int height) {
   DevMap& d = m->d;
   const int tx = (width + kRangeTilePx - 1) / kRangeTilePx, ty = (height + kRangeTilePx - 1) / kRangeTilePx;
   if (d.bins && d.binTilesX == tx && d.binTilesY >= ty) return RFG_OK;
-  RFG_CK(cudaStreamSynchronize(m->stream));
+  // a pipeline's captured frame graph may hold the old bins (and binTilesX):
+  // wait for all work on the device, and bump the generation so such graphs
+  // are re-captured before their next replay (run_frame)
+  RFG_CK(cudaDeviceSynchronize());
+  ++d.binGen;
   if (d.bins) cudaFree(d.bins);
   if (d.binCount) cudaFree(d.binCount);
   d.bins = nullptr;
@@ -167,7 +186,13 @@ namespace {
 constexpr float kIcpMaxDist = 2.f;  // fixed-point range of the tracker sums (rfg_icp.cu)
 
 bool valid_intr(const rfg_intrinsics* i) { return i && i->width > 0 && i->height > 0; }
-bool valid_params(const rfg_scene_params* p) { return p && p->voxelSize > 0.f && p->mu > 0.f; }
+// mu / voxelSize < 80 keeps every pixel's near-far DDA walk (fusion.cpp:72-114)
+// under the 64 cells a 6-bit request-key ordinal can name (rfg_alloc.cu:
+// k_alloc_stage1); the reference walks any length, so larger ratios are
+// rejected here instead of being truncated on the device.
+bool valid_params(const rfg_scene_params* p) {
+  return p && p->voxelSize > 0.f && p->mu > 0.f && p->mu < 80.f * p->voxelSize;
+}
 
 #define RFG_REQUIRE(cond, msg)      \
   do {                              \
@@ -209,7 +234,8 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
     set_error("no CUDA device available (librfg has no CPU fallback)");
     return RFG_ECUDA;
   }
-  RFG_CK(cudaSetDevice(device));
+  RFG_REQUIRE(device >= 0 && device < ndev, "no such CUDA device");
+  DeviceGuard guard(device);  // the caller's current device is restored on return
   rfg_map* m = new rfg_map();
   memset(&m->d, 0, sizeof(DevMap));
   m->cfg = *cfg;
@@ -232,6 +258,7 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
   };
   bool ok = alloc((void**)&d.entries, padded * sizeof(int4)) &&
             alloc((void**)&d.vbaDepth, (size_t)d.capacity * kBlock3 * sizeof(uint32_t)) &&
+            (!RFG_SDF_MIRROR || alloc((void**)&d.vbaSdf, (size_t)d.capacity * kBlock3 * sizeof(int16_t))) &&
             (!cfg->hasColour || alloc((void**)&d.vbaColour, (size_t)d.capacity * kBlock3 * sizeof(uint32_t))) &&
             alloc((void**)&d.freeBlocks, (size_t)d.capacity * sizeof(int)) &&
             alloc((void**)&d.freeExcess, (size_t)(d.excess ? d.excess : 1) * sizeof(int)) &&
@@ -262,9 +289,10 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
 }
 
 int rfg_map_destroy(rfg_map* m) {
+  DeviceGuard dg_(m ? m->device : -1);
   if (!m) return RFG_OK;
   DevMap& d = m->d;
-  void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
+  void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaSdf, d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
                   d.visibility, d.reqKey, d.marked,     d.state,          d.tileCounts, d.tilePrefix,
                   m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount,
                   m->fwdPrev, m->fwdKeys, m->fwdTileCounts, m->fwdTilePrefix, m->rgbaScratch};
@@ -278,6 +306,7 @@ int rfg_map_destroy(rfg_map* m) {
 
 // VoxelBlockMap::clear (voxel_block_map.cpp:15-24)
 int rfg_map_clear(rfg_map* m) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m, "null map");
   DevMap& d = m->d;
   cudaStream_t s = m->stream;
@@ -285,6 +314,8 @@ int rfg_map_clear(rfg_map* m) {
   const int4 e0 = make_entry(0, 0, 0, 0, -2);
   k_fill_u4<<<1024, 256, 0, s>>>(reinterpret_cast<uint4*>(d.entries), make_uint4(e0.x, e0.y, e0.z, e0.w), padded);
   k_fill_u32<<<4096, 256, 0, s>>>(d.vbaDepth, kDefaultDepthVoxel, (size_t)d.capacity * kBlock3);
+  if (d.vbaSdf) k_fill_u32<<<4096, 256, 0, s>>>(reinterpret_cast<uint32_t*>(d.vbaSdf), 0x7FFF7FFFu,
+                                                (size_t)d.capacity * kBlock3 / 2);
   if (d.vbaColour) RFG_CK(cudaMemsetAsync(d.vbaColour, 0, (size_t)d.capacity * kBlock3 * 4, s));
   k_iota<<<512, 256, 0, s>>>(d.freeBlocks, (int)d.capacity);
   if (d.excess) k_iota<<<512, 256, 0, s>>>(d.freeExcess, (int)d.excess);
@@ -300,18 +331,21 @@ int rfg_map_clear(rfg_map* m) {
 }
 
 int rfg_map_set_stream(rfg_map* m, void* stream) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m, "null map");
   m->stream = static_cast<cudaStream_t>(stream);
   return RFG_OK;
 }
 
 int rfg_map_sync(rfg_map* m) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m, "null map");
   RFG_CK(cudaStreamSynchronize(m->stream));
   return check_device_error(m);
 }
 
 int rfg_map_set_shard(rfg_map* m, int rank, int world, int tileShift) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && world >= 1 && rank >= 0 && rank < world && tileShift >= 0 && tileShift < 16, "bad shard");
   m->d.rank = rank;
   m->d.world = world;
@@ -321,12 +355,14 @@ int rfg_map_set_shard(rfg_map* m, int rank, int world, int tileShift) {
 
 int rfg_allocate_from_depth(rfg_map* m, const float* depth, const rfg_intrinsics* intr, const float pose34[12],
                             const rfg_scene_params* params, rfg_alloc_stats* stats) {
+  DeviceGuard dg_(m ? m->device : -1);
   return rfg_allocate_from_depth_ex(m, depth, intr, pose34, params, nullptr, stats);
 }
 
 int rfg_allocate_from_depth_ex(rfg_map* m, const float* depth, const rfg_intrinsics* intr, const float pose34[12],
                                const rfg_scene_params* params, const rfg_fusion_options* opts,
                                rfg_alloc_stats* stats) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && depth && pose34, "null argument");
   RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
   RFG_REQUIRE((size_t)intr->width * intr->height < (1u << 25), "image too large for the 25-bit pixel key");
@@ -348,6 +384,7 @@ int rfg_allocate_from_depth_ex(rfg_map* m, const float* depth, const rfg_intrins
 int rfg_integrate(rfg_map* m, const float* depth, const uint8_t* rgb, const rfg_intrinsics* intrD,
                   const rfg_intrinsics* intrRgb, const float extr34[12], const float pose34[12],
                   const rfg_scene_params* params) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && depth && pose34, "null argument");
   RFG_REQUIRE(valid_intr(intrD) && valid_params(params), "invalid intrinsics / scene params");
   RFG_REQUIRE(!rgb || (m->d.vbaColour && valid_intr(intrRgb)), "colour integration needs a colour map + rgb intrinsics");
@@ -376,6 +413,7 @@ int rfg_integrate(rfg_map* m, const float* depth, const uint8_t* rgb, const rfg_
 
 int rfg_render_expected_ranges(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
                                const rfg_scene_params* params, float* range) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && pose34 && range, "null argument");
   RFG_REQUIRE(valid_intr(intr) && valid_params(params), "invalid intrinsics / scene params");
   const FrameArgs fa = make_frame_args(intr, params, pose34, nullptr);
@@ -388,6 +426,7 @@ int rfg_render_expected_ranges(rfg_map* m, const float pose34[12], const rfg_int
 int rfg_render_icp_maps(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
                         const rfg_scene_params* params, const float* range, float* raycast, float* points,
                         float* normals) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && pose34 && points && normals, "null argument");
   if (!range) {
     set_error("render_icp_maps needs the expected-range image (render_expected_ranges first)");
@@ -403,6 +442,7 @@ int rfg_render_icp_maps(rfg_map* m, const float pose34[12], const rfg_intrinsics
 int rfg_forward_project(rfg_map* m, int hasRaycast, float* raycast, float* points, float* normals,
                         const float newPose34[12], const rfg_intrinsics* intr, float voxelSize, int32_t* missing,
                         int32_t* nMissing) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && raycast && points && normals && newPose34 && missing && nMissing, "null argument");
   RFG_REQUIRE(valid_intr(intr) && voxelSize > 0.f, "invalid intrinsics / voxel size");
   const int n = intr->width * intr->height;
@@ -412,6 +452,11 @@ int rfg_forward_project(rfg_map* m, int hasRaycast, float* raycast, float* point
     cudaFree(m->fwdKeys);
     cudaFree(m->fwdTileCounts);
     cudaFree(m->fwdTilePrefix);
+    m->fwdPrev = nullptr;  // a failed allocation below must not leave freed pointers for rfg_map_destroy
+    m->fwdKeys = nullptr;
+    m->fwdTileCounts = nullptr;
+    m->fwdTilePrefix = nullptr;
+    m->fwdN = 0;
     const int tiles = (n + kTile - 1) / kTile;
     if (cudaMalloc(&m->fwdPrev, (size_t)n * sizeof(float4)) != cudaSuccess ||
         cudaMalloc(&m->fwdKeys, (size_t)n * 8) != cudaSuccess ||
@@ -434,6 +479,7 @@ int rfg_forward_project(rfg_map* m, int hasRaycast, float* raycast, float* point
 int rfg_render_icp_maps_list(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
                              const rfg_scene_params* params, const float* range, const int32_t* missing,
                              const int32_t* nMissing, float* raycast, float* points, float* normals) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && pose34 && missing && nMissing && raycast && points && normals, "null argument");
   if (!range) {
     set_error("render_icp_maps_list needs the expected-range image (render_expected_ranges first)");
@@ -449,6 +495,7 @@ int rfg_render_icp_maps_list(rfg_map* m, const float pose34[12], const rfg_intri
 
 int rfg_render_maps(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr, const rfg_scene_params* params,
                     int mode, const float* range, float* raycast, float* points, float* normals, uint8_t* colour) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (kIcpMaps), 1 (kColour) or 2 (kGrey)");
   RFG_REQUIRE(mode == 0 || colour, "colour / grey modes need a colour image");
   RFG_REQUIRE(raycast, "render_maps needs the raycast image (the colour pass reads the hits)");
@@ -463,6 +510,7 @@ int rfg_render_maps(rfg_map* m, const float pose34[12], const rfg_intrinsics* in
 int rfg_render_maps_list(rfg_map* m, const float pose34[12], const rfg_intrinsics* intr,
                          const rfg_scene_params* params, int mode, const float* range, const int32_t* missing,
                          const int32_t* nMissing, float* raycast, float* points, float* normals, uint8_t* colour) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (kIcpMaps), 1 (kColour) or 2 (kGrey)");
   RFG_REQUIRE(mode == 0 || colour, "colour / grey modes need a colour image");
   const int rc = rfg_render_icp_maps_list(m, pose34, intr, params, range, missing, nMissing, raycast, points, normals);
@@ -475,6 +523,7 @@ int rfg_render_maps_list(rfg_map* m, const float pose34[12], const rfg_intrinsic
 }
 
 int rfg_extract_mesh(rfg_map* m, float voxelSize, int64_t* nVertices, int64_t* nTriangles) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && nVertices && nTriangles && voxelSize > 0.f, "invalid extract_mesh arguments");
   long long nv = 0, nt = 0;
   RFG_CK(mesh_extract(m->d, voxelSize, &m->mesh, &nv, &nt, m->stream));
@@ -484,6 +533,7 @@ int rfg_extract_mesh(rfg_map* m, float voxelSize, int64_t* nVertices, int64_t* n
 }
 
 int rfg_mesh_copy(rfg_map* m, float* vertices3, uint32_t* triangles3) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m, "null map");
   if (!m->mesh) {
     set_error("mesh_copy before extract_mesh");
@@ -549,6 +599,7 @@ int rfg_downsample_intensity(const float* in, int w, int h, float* out, void* st
 int rfg_icp_track(rfg_map* m, const float* depthLevels, int levels, const rfg_intrinsics* intr, const float* points,
                   const float* normals, const float renderPose34[12], const float initPose34[12], const int iters[3],
                   const float dist[3], int minCount, float poseOut34[12], double stats12[RFG_ICP_STATS]) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && depthLevels && points && normals && renderPose34 && initPose34 && iters && dist,
               "null argument");
   RFG_REQUIRE(valid_intr(intr) && levels >= 1 && levels <= 3, "invalid intrinsics / levels");
@@ -581,6 +632,7 @@ int rfg_icp_track(rfg_map* m, const float* depthLevels, int levels, const rfg_in
 int rfg_icp_reduce(rfg_map* m, const float* depthLevel, int level, const rfg_intrinsics* intr, const float* points,
                    const float* normals, const float renderPose34[12], const float camToWorld34[12], float dist,
                    int64_t fixed31[RFG_ICP_SUMS], double out31[RFG_ICP_SUMS]) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && depthLevel && points && normals && renderPose34 && camToWorld34, "null argument");
   RFG_REQUIRE(valid_intr(intr) && level >= 0 && level < 4, "invalid intrinsics / level");
   RFG_REQUIRE(dist > 0.f && dist <= kIcpMaxDist, "ICP outlier gate must be in (0, 2] m");
@@ -611,6 +663,7 @@ int rfg_icp_reduce(rfg_map* m, const float* depthLevel, int level, const rfg_int
 }
 
 int rfg_icp_timers(rfg_map* m, uint64_t out8[8], int reset) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && out8, "null argument");
   unsigned long long* t = icp_timers_ptr(m->icpOut);
   RFG_CK(cudaMemcpyAsync(out8, t, 64, cudaMemcpyDeviceToHost, m->stream));
@@ -622,6 +675,7 @@ int rfg_icp_timers(rfg_map* m, uint64_t out8[8], int reset) {
 uint32_t rfg_total_entries(const rfg_map* m) { return m ? m->d.total : 0; }
 
 int rfg_export_entries(rfg_map* m, int32_t* out5) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && out5, "null argument");
   int* dbuf = nullptr;
   RFG_CK(cudaMalloc(&dbuf, (size_t)m->d.total * 5 * sizeof(int)));
@@ -635,6 +689,7 @@ int rfg_export_entries(rfg_map* m, int32_t* out5) {
 }
 
 int rfg_export_blocks(rfg_map* m, const int32_t* ptrs, int n, uint8_t* out) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && (n == 0 || (ptrs && out)) && n >= 0, "null argument");
   if (n == 0) return RFG_OK;
   for (int i = 0; i < n; ++i) RFG_REQUIRE(ptrs[i] >= 0 && (uint32_t)ptrs[i] < m->d.capacity, "block ptr out of range");
@@ -658,6 +713,7 @@ int rfg_export_blocks(rfg_map* m, const int32_t* ptrs, int n, uint8_t* out) {
 }
 
 int rfg_export_visible(rfg_map* m, int32_t* list, uint8_t* types, int32_t* count) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && count, "null argument");
   const int rc = check_device_error(m);
   if (rc != RFG_OK) return rc;
@@ -673,6 +729,7 @@ int rfg_export_visible(rfg_map* m, int32_t* list, uint8_t* types, int32_t* count
 }
 
 int rfg_free_counts(rfg_map* m, int32_t* nb, int32_t* ne) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && nb && ne, "null argument");
   const int rc = check_device_error(m);
   if (rc != RFG_OK) return rc;
@@ -868,6 +925,7 @@ int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc, cons
 extern "C" {
 
 int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline** out) {
+  DeviceGuard dg_(m ? m->device : -1);
   RFG_REQUIRE(m && cfg && out, "null argument");
   RFG_REQUIRE(valid_intr(&cfg->intr) && valid_params(&cfg->params), "invalid intrinsics / scene params");
   RFG_REQUIRE(cfg->levels >= 1 && cfg->levels <= 3, "levels must be 1..3");
@@ -934,6 +992,7 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
 }
 
 int rfg_pipeline_destroy(rfg_pipeline* p) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   if (!p) return RFG_OK;
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (int i = 0; i < 2; ++i)
@@ -957,6 +1016,7 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
 }
 
 int rfg_pipeline_reset(rfg_pipeline* p) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p, "null pipeline");
   Pose12 id{};
   id.v[0] = id.v[5] = id.v[10] = 1.f;
@@ -970,6 +1030,7 @@ int rfg_pipeline_reset(rfg_pipeline* p) {
 }
 
 int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw, const float* pose34) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && raw, "null argument");
   RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
@@ -978,6 +1039,7 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw, const float* 
 }
 
 int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const float* pose34, void* producer) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && raw, "null argument");
   RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   cudaStream_t ps = static_cast<cudaStream_t>(producer);
@@ -1000,6 +1062,7 @@ int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const 
 }
 
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const float* pose34) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && rawHost, "null argument");
   RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
@@ -1019,6 +1082,7 @@ int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const fl
 
 int rfg_pipeline_process_rgbd_stream(rfg_pipeline* p, const uint16_t* raw, const uint8_t* rgb, const float* pose34,
                                      void* producer) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && raw && rgb, "null argument");
   RFG_REQUIRE(p->cfg.colour, "rgbd frames need a colour pipeline (cfg.colour = 1)");
   cudaStream_t ps = static_cast<cudaStream_t>(producer);
@@ -1041,6 +1105,7 @@ int rfg_pipeline_process_rgbd_stream(rfg_pipeline* p, const uint16_t* raw, const
 
 int rfg_pipeline_process_rgbd_host(rfg_pipeline* p, const uint16_t* rawHost, const uint8_t* rgbHost,
                                    const float* pose34) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && rawHost && rgbHost, "null argument");
   RFG_REQUIRE(p->cfg.colour, "rgbd frames need a colour pipeline (cfg.colour = 1)");
   const size_t n = (size_t)p->cfg.intr.width * p->cfg.intr.height;
@@ -1062,6 +1127,7 @@ int rfg_pipeline_process_rgbd_host(rfg_pipeline* p, const uint16_t* rawHost, con
 }
 
 int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pose34) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && path, "null argument");
   RFG_REQUIRE(!p->cfg.colour, "a colour pipeline takes RGB-D frames (rfg_pipeline_process_rgbd_*)");
   const int64_t n = (int64_t)p->cfg.intr.width * p->cfg.intr.height;
@@ -1082,6 +1148,7 @@ int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float* pos
 
 int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34[12],
                         double icpStats[RFG_ICP_STATS]) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p, "null pipeline");
   rfg_map* m = p->map;
   FrameResult* dev = nullptr;
@@ -1107,6 +1174,7 @@ int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34
 }
 
 int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && ms7, "null argument");
   RFG_REQUIRE(p->cfg.profile, "stage times need profile = 1");
   RFG_CK(cudaEventSynchronize(p->ev[6]));
@@ -1119,6 +1187,7 @@ int rfg_pipeline_stage_times(rfg_pipeline* p, float ms7[7]) {
 void* rfg_pipeline_stream(rfg_pipeline* p) { return p ? (void*)p->stream : nullptr; }
 
 int rfg_pipeline_pose_buffer(rfg_pipeline* p, float** poseDev) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && poseDev, "null argument");
   *poseDev = p->poses;
   return RFG_OK;
@@ -1126,6 +1195,7 @@ int rfg_pipeline_pose_buffer(rfg_pipeline* p, float** poseDev) {
 
 int rfg_pipeline_buffers(rfg_pipeline* p, float** depthLevels, float** range, float** raycast, float** points,
                          float** normals) {
+  DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p, "null pipeline");
   if (depthLevels) *depthLevels = p->depthLevels;
   if (range) *range = reinterpret_cast<float*>(p->range);

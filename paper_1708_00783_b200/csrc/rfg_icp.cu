@@ -682,17 +682,19 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpT
 // CTAs for a level of n pixels: about one pixel per thread, at most one CTA
 // per SM (co-residency for grid.sync).  Fixed per (device, level size).
 static int icp_grid(int n) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0, perSm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int fits[64] = {};  // per device: 1 fits one CTA per SM, -1 does not
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int f = dev < 64 ? fits[dev] : 0;
+  if (!f) {
+    int perSm = 0, perSmTrack = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, k_icp_level, kIcpThreads, 0);
-    int perSmTrack = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSmTrack, k_icp_track, kIcpThreads, 0);
-    if (perSm < 1 || perSmTrack < 1) sms = -1;
+    f = (perSm < 1 || perSmTrack < 1) ? -1 : 1;
+    if (dev < 64) fits[dev] = f;
   }
-  if (sms <= 0) return 0;
+  if (f < 0) return 0;
+  const int sms = current_sm_count();
   // every SM takes a part of every level (at least a warp of pixels per CTA):
   // spreading a coarse level over all SMs leaves fewer busy warps per SM for
   // the accumulation and the CTA reduction

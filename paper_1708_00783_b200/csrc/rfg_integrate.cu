@@ -59,11 +59,44 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 // kWindowKnown: the block-level test below has proven that every voxel's
 // projection quotients are inside div_fast's exactness window, so only the
 // eta quotient keeps a per-voxel window test.
+#ifndef RFG_INT_DIET
+#define RFG_INT_DIET 1
+#endif
+// RFG_INT_DIET: the per-voxel int<->float conversions and roundings on the
+// FMA/ALU pipes (rfg_common.cuh magic conversions), the lane's x-column
+// products R_0x px, R_3x px, R_6x px hoisted out of the rows (a lane's four
+// voxels per row have the same x in every row), and 1/(w+1) from a per-CTA
+// table (the exact div_rcp values) instead of a reciprocal per voxel.
+__device__ __forceinline__ float sdf_to_logical_alu(int16_t s) {
+  const float x = s16_to_float(s);
+  const float r = 1.f / 32767.f;
+  const float q = x * r;
+  const float e = __fmaf_rn(-q, (float)kSdfOne, x);
+  return __fmaf_rn(e, r, q);
+}
+__device__ __forceinline__ int16_t sdf_from_logical_alu(float f) {
+  float c = f < -1.f ? -1.f : (1.f < f ? 1.f : f);
+  return (int16_t)lround_haz_alu(c * (float)kSdfOne);
+}
+
 template <bool kWindowKnown>
-__device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int ox, int oy, int oz, const Pose& pose,
+__device__ __forceinline__ void integrate_block_depth(uint4* blk, uint2* sblk, int lane, int ox, int oy, int oz,
+                                                      const Pose& pose,
                                                       const FrameArgs& fa, const float* __restrict__ depth, float wLim,
-                                                      float hLim, float mu, bool muOk, float rMu, bool capW, int maxW) {
+                                                      float hLim, float mu, bool muOk, float rMu, bool capW, int maxW,
+                                                      const float* rcpTab) {
   const float vs = fa.voxelSize;
+#if RFG_INT_DIET
+  // this lane's four x columns: the same in all of its rows
+  float rx0[4], rx3[4], rx6[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float px = (float)(ox + ((lane * 4) & 7) + i) * vs;
+    rx0[i] = pose.R[0] * px;
+    rx3[i] = pose.R[3] * px;
+    rx6[i] = pose.R[6] * px;
+  }
+#endif
 #pragma unroll
   for (int g = 0; g < 4; g += kQG) {
     uint32_t wd[4 * kQG];
@@ -90,16 +123,27 @@ __device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int 
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = (q - g) * 4 + i;
+#if RFG_INT_DIET
+        const float cxw = (rx0[i] + r0) + pose.t[0];
+        const float cyw = (rx3[i] + r1) + pose.t[1];
+        const float czw = (rx6[i] + r2) + pose.t[2];
+#else
         const float px = (float)(ox + (lin & 7) + i) * vs;
         const float cxw = (pose.R[0] * px + r0) + pose.t[0];
         const float cyw = (pose.R[3] * px + r1) + pose.t[1];
         const float czw = (pose.R[6] * px + r2) + pose.t[2];
+#endif
         const float ax = fa.fx * cxw, ay = fa.fy * cyw;
         const float rz = div_rcp(czw);
         const float u = div_fast(ax, czw, rz) + fa.cx;
         const float v = div_fast(ay, czw, rz) + fa.cy;
         const bool in = czw > 0.f && !(u < 1 || u > wLim || v < 1 || v > hLim);
+#if RFG_INT_DIET
+        // u, v in [1, W-2] when `in`: the truncations of u + 0.5, v + 0.5 (static_cast<int>, fusion.cpp:18)
+        pix[k] = in ? trunc_pos_to_int(v + 0.5f) * fa.w + trunc_pos_to_int(u + 0.5f) : -1;
+#else
         pix[k] = in ? (int)(v + 0.5f) * fa.w + (int)(u + 0.5f) : -1;
+#endif
         zc[k] = czw;
         if (!kWindowKnown) {
           const bool fast = czw >= 0x1p-40f && czw <= 0x1p40f && fabsf(ax) <= 0x1p40f && fabsf(ay) <= 0x1p40f;
@@ -129,6 +173,15 @@ __device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int 
       const int oldW = vox_w(w0);
       const float eta = dm[k] - zc[k];
       const bool upd = pix[k] >= 0 && !(dm[k] <= 0.f) && !(eta < -mu) && !(capW && oldW >= maxW);
+#if RFG_INT_DIET
+      const float oldF = sdf_to_logical_alu(vox_sdf(w0));
+      const float newF = smin(1.f, div_fast(eta, mu, rMu));
+      const float fw = u23_to_float((uint32_t)oldW);
+      const float num = fw * oldF + newF;
+      const float den = fw + 1.f;  // == (float)(oldW + 1): small integers are exact
+      const float merged = div_fast(num, den, rcpTab[oldW]);  // rcpTab[w] == div_rcp(w + 1)
+      const uint32_t w1 = vox_pack(sdf_from_logical_alu(merged), min(oldW + 1, maxW));
+#else
       const float oldF = sdf_to_logical(vox_sdf(w0));
       const float newF = smin(1.f, div_fast(eta, mu, rMu));
       const float fw = (float)oldW;
@@ -136,6 +189,7 @@ __device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int 
       const float den = fw + 1.f;  // == (float)(oldW + 1): small integers are exact
       const float merged = div_fast(num, den, div_rcp(den));
       const uint32_t w1 = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
+#endif
       // out-of-window voxels keep w0 here and are redone exactly below
       const bool slowK = kWindowKnown ? (upd && !(muOk && fabsf(eta) <= 0x1p40f))
                                       : (upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << k))));
@@ -151,6 +205,9 @@ __device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int 
     for (int q = g; q < g + kQG; ++q) {
       const int k = (q - g) * 4;
       blk[q * 32 + lane] = make_uint4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
+#if RFG_SDF_MIRROR
+      sblk[q * 32 + lane] = sdf_pack4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
+#endif
     }
   }
 }
@@ -197,16 +254,22 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
   const float rMu = div_rcp(mu);
   const bool capW = fa.stopAtMaxW != 0;
   const int maxW = fa.maxW;
+  __shared__ float rcpTab[256];  // 1 / (w + 1) as div_rcp computes it, w = 0..255
+  rcpTab[threadIdx.x] = div_rcp((float)(threadIdx.x + 1));  // blockDim.x == 256
+  __syncthreads();
   for (int b = gw; b < nVis; b += nw) {
     const int idx = m.visibleList[b];
     const int4 e = ld_entry(m.entries, idx);
     if (e.w < 0) continue;
     const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
     uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
+    uint2* sblk = RFG_SDF_MIRROR ? reinterpret_cast<uint2*>(m.vbaSdf + (size_t)e.w * kBlock3) : nullptr;
     if (block_window_known(lane, ox, oy, oz, pose, fa))
-      integrate_block_depth<true>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW, maxW);
+      integrate_block_depth<true>(blk, sblk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
+                                  maxW, rcpTab);
     else
-      integrate_block_depth<false>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW, maxW);
+      integrate_block_depth<false>(blk, sblk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
+                                   maxW, rcpTab);
   }
 }
 
@@ -270,7 +333,8 @@ __device__ __forceinline__ bool colour_pixel(const Pose& M, const ColourArgs& ca
 }
 
 template <bool kSameCamera>
-__device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, int lane, int ox, int oy, int oz,
+__device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, uint2* sblk, int lane, int ox, int oy,
+                                                     int oz,
                                                      const Pose& pose, const Pose& Mrgb, const FrameArgs& fa,
                                                      const ColourArgs& ca, const float* __restrict__ depth,
                                                      float wLim, float hLim, float mu, bool muOk, float rMu, bool capW,
@@ -368,11 +432,135 @@ __device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, in
       if (cin[i]) cw[i] = colour_merge(cw[i], cx4[i], cy4[i], ca, maxW, tap[i][0], tap[i][1], tap[i][2], tap[i][3]);
     blk[q * 32 + lane] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     cblk[q * 32 + lane] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+#if RFG_SDF_MIRROR
+    sblk[q * 32 + lane] = sdf_pack4(wd[0], wd[1], wd[2], wd[3]);
+#endif
   }
 }
 
+// The same-camera form (identity extrinsics, equal intrinsics — the
+// synthetic C3 stream): one projection serves both updates, and like the
+// depth-only kernel every voxel of a row is computed unconditionally and the
+// results selected (kWindowKnown: block_window_known proved the projection
+// quotients inside div_fast's window).  The colour taps of the gated voxels
+// are loaded (predicated) before any is used.
+template <bool kWindowKnown>
+__device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cblk, uint2* sblk, int lane, int ox,
+                                                          int oy, int oz,
+                                                          const Pose& pose, const FrameArgs& fa, const ColourArgs& ca,
+                                                          const float* __restrict__ depth, float wLim, float hLim,
+                                                          float mu, bool muOk, float rMu, bool capW, int maxW) {
+  const float vs = fa.voxelSize;
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const uint4 r = blk[q * 32 + lane];
+    const uint4 rc = cblk[q * 32 + lane];
+    uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+    uint32_t cw[4] = {rc.x, rc.y, rc.z, rc.w};
+    const int lin = (q * 32 + lane) * 4;
+    const float pz = (float)(oz + (lin >> 6)) * vs;
+    const float py = (float)(oy + ((lin >> 3) & 7)) * vs;
+    const float r0 = pose.R[1] * py + pose.R[2] * pz;
+    const float r1 = pose.R[4] * py + pose.R[5] * pz;
+    const float r2 = pose.R[7] * py + pose.R[8] * pz;
+    float zc[4], uu[4], vv[4];
+    int pix[4];
+    unsigned slow = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float px = (float)(ox + (lin & 7) + i) * vs;
+      const float cxw = (pose.R[0] * px + r0) + pose.t[0];
+      const float cyw = (pose.R[3] * px + r1) + pose.t[1];
+      const float czw = (pose.R[6] * px + r2) + pose.t[2];
+      const float ax = fa.fx * cxw, ay = fa.fy * cyw;
+      const float rz = div_rcp(czw);
+      float u = div_fast(ax, czw, rz) + fa.cx;
+      float v = div_fast(ay, czw, rz) + fa.cy;
+      if (!kWindowKnown) {
+        const bool fast = czw >= 0x1p-40f && czw <= 0x1p40f && fabsf(ax) <= 0x1p40f && fabsf(ay) <= 0x1p40f;
+        slow |= (czw > 0.f && !fast) ? (1u << i) : 0u;
+      }
+      zc[i] = czw;
+      uu[i] = u;
+      vv[i] = v;
+    }
+    if (!kWindowKnown && __any_sync(0xffffffffu, slow != 0u)) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (slow & (1u << i)) {
+          const float px = (float)(ox + (lin & 7) + i) * vs;
+          const f3 pc = pose_apply(pose, f3{px, py, pz});
+          uu[i] = div_ieee(fa.fx * pc.x, pc.z) + fa.cx;
+          vv[i] = div_ieee(fa.fy * pc.y, pc.z) + fa.cy;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool in = zc[i] > 0.f && !(uu[i] < 1 || uu[i] > wLim || vv[i] < 1 || vv[i] > hLim);
+      pix[i] = in ? (int)(vv[i] + 0.5f) * fa.w + (int)(uu[i] + 0.5f) : -1;
+    }
+    float dm[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dm[i] = pix[i] >= 0 ? __ldg(depth + pix[i]) : -1.f;
+    bool cin[4];
+    unsigned redo = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t w0 = wd[i];
+      const int oldW = vox_w(w0);
+      const bool valid = pix[i] >= 0 && !(dm[i] <= 0.f);
+      const float eta = dm[i] - zc[i];
+      const bool upd = valid && !(eta < -mu) && !(capW && oldW >= maxW);
+      const float oldF = sdf_to_logical(vox_sdf(w0));
+      const float newF = smin(1.f, div_fast(eta, mu, rMu));
+      const float fw = (float)oldW;
+      const float num = fw * oldF + newF;
+      const float den = fw + 1.f;
+      const float merged = div_fast(num, den, div_rcp(den));
+      const uint32_t w1 = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
+      // (a voxel whose projection left the window may also have a tiny eta:
+      // its update is redone exactly too, as in integrate_block_depth)
+      const bool slowK = upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << i)));
+      wd[i] = (upd && !slowK) ? w1 : w0;
+      redo |= slowK ? (1u << i) : 0u;
+      // fusion.cpp:257 on update_voxel_depth's return value (-1 when invalid);
+      // same camera: the colour pixel is the depth pixel, in the same margin
+      cin[i] = ((valid ? eta : -1.f) >= -mu) && pix[i] >= 0;
+    }
+    if (__any_sync(0xffffffffu, redo != 0u)) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (redo & (1u << i)) wd[i] = update_exact(wd[i], dm[i] - zc[i], mu, maxW);
+    }
+    uint32_t tap[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x0 = (int)floorf(uu[i]), y0 = (int)floorf(vv[i]);
+      const uint32_t* p0 = ca.rgba + (cin[i] ? (size_t)y0 * ca.rw + x0 : 0);
+      tap[i][0] = cin[i] ? __ldg(p0) : 0u;
+      tap[i][1] = cin[i] ? __ldg(p0 + 1) : 0u;
+      tap[i][2] = cin[i] ? __ldg(p0 + ca.rw) : 0u;
+      tap[i][3] = cin[i] ? __ldg(p0 + ca.rw + 1) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t c1 = colour_merge(cw[i], uu[i], vv[i], ca, maxW, tap[i][0], tap[i][1], tap[i][2], tap[i][3]);
+      cw[i] = cin[i] ? c1 : cw[i];
+    }
+    blk[q * 32 + lane] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    cblk[q * 32 + lane] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+#if RFG_SDF_MIRROR
+    sblk[q * 32 + lane] = sdf_pack4(wd[0], wd[1], wd[2], wd[3]);
+#endif
+  }
+}
+
+#ifndef RFG_RGBD_MINB
+#define RFG_RGBD_MINB 3
+#endif
 template <bool kSameCamera>
-__global__ void __launch_bounds__(256, 2) k_integrate_rgbd(DevMap m, const float* __restrict__ depth, FrameArgs fa,
+__global__ void __launch_bounds__(256, RFG_RGBD_MINB) k_integrate_rgbd(DevMap m, const float* __restrict__ depth, FrameArgs fa,
                                                            ColourArgs ca) {
   const int lane = threadIdx.x & 31;
   const int warpsPerCta = blockDim.x >> 5;
@@ -395,8 +583,22 @@ __global__ void __launch_bounds__(256, 2) k_integrate_rgbd(DevMap m, const float
     const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
     uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
     uint4* cblk = reinterpret_cast<uint4*>(m.vbaColour + (size_t)e.w * kBlock3);
-    integrate_block_rgbd<kSameCamera>(blk, cblk, lane, ox, oy, oz, pose, Mrgb, fa, ca, depth, wLim, hLim, mu, muOk,
-                                      rMu, capW, maxW);
+    uint2* sblk = RFG_SDF_MIRROR ? reinterpret_cast<uint2*>(m.vbaSdf + (size_t)e.w * kBlock3) : nullptr;
+#ifdef RFG_RGBD_OLD
+    if (false) {
+#else
+    if (kSameCamera) {
+#endif
+      if (block_window_known(lane, ox, oy, oz, pose, fa))
+        integrate_block_rgbd_same<true>(blk, cblk, sblk, lane, ox, oy, oz, pose, fa, ca, depth, wLim, hLim, mu, muOk, rMu,
+                                        capW, maxW);
+      else
+        integrate_block_rgbd_same<false>(blk, cblk, sblk, lane, ox, oy, oz, pose, fa, ca, depth, wLim, hLim, mu, muOk, rMu,
+                                         capW, maxW);
+    } else {
+      integrate_block_rgbd<kSameCamera>(blk, cblk, sblk, lane, ox, oy, oz, pose, Mrgb, fa, ca, depth, wLim, hLim, mu, muOk,
+                                        rMu, capW, maxW);
+    }
   }
 }
 
@@ -436,14 +638,7 @@ cudaError_t launch_rgb_to_rgba(const uint8_t* rgb, uint32_t* out, int n, cudaStr
 #define RFG_INT_GRID_PER_SM 8
 #endif
 int integrate_grid() {
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = sms * RFG_INT_GRID_PER_SM;  // two waves of 4 resident CTAs x 8 warps per SM
-  }
-  return grid;
+  return current_sm_count() * RFG_INT_GRID_PER_SM;  // two waves of 4 resident CTAs x 8 warps per SM
 }
 
 // Depth-only (rgba == nullptr) or RGB-D integration of the visible blocks.

@@ -10,6 +10,10 @@
 
 #include "../../include/rfg.h"
 
+#ifndef RFG_SDF_MIRROR
+#define RFG_SDF_MIRROR 0
+#endif
+
 namespace rfg {
 
 // Device-resident mutable scalars of a map.
@@ -31,6 +35,7 @@ struct DevMap {
   uint32_t buckets, excess, capacity, total;
   int4* entries;           // total x 16 B
   uint32_t* vbaDepth;      // capacity x 512 depth voxels (4 B)
+  int16_t* vbaSdf;         // RFG_SDF_MIRROR: capacity x 512 sdf values (2 B), the raycast's copy
   uint32_t* vbaColour;     // capacity x 512 colour voxels (4 B) or nullptr
   int* freeBlocks;         // capacity
   int* freeExcess;         // excess
@@ -48,6 +53,7 @@ struct DevMap {
   int* binCount;           // per 32x32 screen tile
   int* bins;               // binTilesX * binTilesY * binCap block indices
   int binTilesX, binTilesY, binCap;
+  unsigned binGen;         // bumped whenever the range scratch is reallocated (captured graphs re-capture)
 };
 
 // Per-call frame arguments (camera, scene params, pose).
@@ -75,6 +81,28 @@ constexpr int kTileThreads = 256;    // 4 consecutive entries per thread
 void set_error(const std::string& msg);
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// SM count of the current device, cached per device (grid sizes).
+int current_sm_count();
+
+// Makes `device` current for the scope of an entry point and restores the
+// caller's device afterwards (a map lives on the device it was created on).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (device < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+      return;
+    }
+    if (prev != device) cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p, const float* pose34,
                           const float* poseDev);

@@ -481,7 +481,8 @@ void mesh_free(void* mb) {
 
 static int grid_for(long long n, int threads) {
   const long long g = (n + threads - 1) / threads;
-  return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+  const long long cap = (long long)current_sm_count() * 16;
+  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
 }
 
 // Extracts the mesh into *mbp (allocated / grown as needed); synchronises.

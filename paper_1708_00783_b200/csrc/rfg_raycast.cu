@@ -165,9 +165,22 @@ __device__ unsigned long long g_rc_stats[32];
 // TSDF field reader (MapField, raycast.hpp:32-45) with the reference's
 // last-block cache.  Voxel offsets inside a block use bit operations
 // (v & 7 == v - (v >> 3) * 8 for negative v too).
+// The voxels the raycast reads: the 2-B sdf mirror plane (RFG_SDF_MIRROR:
+// twice the voxels per L1 / L2 line of the 4-B depth plane), or the depth
+// plane's sdf halves.
+#if RFG_SDF_MIRROR
+typedef int16_t FieldVoxel;
+#define RFG_FIELD_PLANE(m) ((m).vbaSdf)
+__device__ __forceinline__ int16_t field_sdf(int16_t v) { return v; }
+#else
+typedef uint32_t FieldVoxel;
+#define RFG_FIELD_PLANE(m) ((m).vbaDepth)
+__device__ __forceinline__ int16_t field_sdf(uint32_t v) { return vox_sdf(v); }
+#endif
+
 struct FieldReader {
   const int4* entries;
-  const uint32_t* vba;
+  const FieldVoxel* vba;
   uint32_t buckets;
   BlockCache cache;
 
@@ -210,8 +223,8 @@ struct FieldReader {
     const int ptr = ptr_of(vx >> 3, vy >> 3, vz >> 3);
     ok = ptr >= 0;
     if (!ok) return 1.f;
-    const uint32_t w = __ldg(vba + (size_t)ptr * kBlock3 + ((vx & 7) | ((vy & 7) << 3) | ((vz & 7) << 6)));
-    return sdf_to_logical(vox_sdf(w));
+    const FieldVoxel w = __ldg(vba + (size_t)ptr * kBlock3 + ((vx & 7) | ((vy & 7) << 3) | ((vz & 7) << 6)));
+    return sdf_to_logical(field_sdf(w));
   }
   // readSdfWeightTrilinear (voxel_block_map.cpp:130-156).  Any missing
   // corner invalidates the read, so the corner order only matters for the
@@ -243,7 +256,7 @@ struct FieldReader {
     }
     const int ox0 = lx, ox1 = (lx + 1) & 7, oy0 = ly << 3, oy1 = ((ly + 1) & 7) << 3, oz0 = lz << 6,
               oz1 = ((lz + 1) & 7) << 6;
-    uint32_t w[8];
+    FieldVoxel w[8];
     w[0] = __ldg(vba + (size_t)q0 * kBlock3 + (ox0 | oy0 | oz0));
     w[1] = __ldg(vba + (size_t)qx * kBlock3 + (ox1 | oy0 | oz0));
     w[2] = __ldg(vba + (size_t)qy * kBlock3 + (ox0 | oy1 | oz0));
@@ -257,7 +270,7 @@ struct FieldReader {
     for (int k = 0; k < 8; ++k) {
       const float bw =
           ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
-      sdf += bw * sdf_to_logical(vox_sdf(w[k]));
+      sdf += bw * sdf_to_logical(field_sdf(w[k]));
     }
     ok = true;
     return sdf;
@@ -401,7 +414,7 @@ __device__ __forceinline__ void raycast_pixel(const DevMap& m, const FrameArgs& 
     const float norm = sqrtf(sqnorm3(dirCam));
     const f3 dw = rot_apply(c2w.R, dirCam);
     const f3 dirW{dw.x / norm, dw.y / norm, dw.z / norm};
-    FieldReader field{m.entries, m.vbaDepth, m.buckets};
+    FieldReader field{m.entries, RFG_FIELD_PLANE(m), m.buckets};
     field.cache.reset();
     f3 hit;
     if (cast_ray(field, origin, dirW, r.x * norm, r.y * norm, fa.mu, fa.voxelSize, &hit)) {
@@ -419,7 +432,7 @@ __device__ __forceinline__ void normal_pixel(const DevMap& m, const float4* __re
   const float4 r = raycast[i];
   float4 nm = make_float4(0.f, 0.f, 0.f, -1.f);
   if (r.w > 0.f) {
-    FieldReader field{m.entries, m.vbaDepth, m.buckets};
+    FieldReader field{m.entries, RFG_FIELD_PLANE(m), m.buckets};
     field.cache.reset();
     f3 n;
     if (field_normal(field, f3{r.x, r.y, r.z}, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
@@ -474,7 +487,7 @@ __device__ __forceinline__ void raycast_and_normal(const DevMap& m, const FrameA
   const size_t i = (size_t)y * fa.w + x;
   const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
   float4 rc = invalid, pt = invalid, nm = invalid;
-  FieldReader field{m.entries, m.vbaDepth, m.buckets};
+  FieldReader field{m.entries, RFG_FIELD_PLANE(m), m.buckets};
   field.cache.reset();
   bool isHit = false;
   f3 hit{0.f, 0.f, 0.f};
@@ -581,7 +594,7 @@ __global__ void __launch_bounds__(128) k_render_colour(DevMap m, FrameArgs fa, i
   const float4 r = raycast[i];
   if (r.w > 0.f) {
     if (mode == 1 && m.vbaColour) {
-      FieldReader field{m.entries, m.vbaDepth, m.buckets};
+      FieldReader field{m.entries, RFG_FIELD_PLANE(m), m.buckets};
       field.cache.reset();
       const int bx = (int)floorf(r.x), by = (int)floorf(r.y), bz = (int)floorf(r.z);
       const float fx = r.x - (float)bx, fy = r.y - (float)by, fz = r.z - (float)bz;
@@ -736,16 +749,7 @@ __global__ void k_iota_count(int* list, int n, int* count) {
   if (i == 0) *count = n;
 }
 
-int range_grid() {
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = sms * 8;
-  }
-  return grid;
-}
+int range_grid() { return current_sm_count() * 8; }
 
 cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s) {
   const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;

@@ -79,7 +79,11 @@ __global__ void k_swapin_apply(DevMap m, const int* __restrict__ idx, const uint
   uint4* dst = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)ptr * kBlock3);
   const uint4* hs = reinterpret_cast<const uint4*>(src[2 * k]);
 #pragma unroll
-  for (int v = lane; v < kBlock3 / 4; v += 32) dst[v] = hs[v];
+  for (int v = lane; v < kBlock3 / 4; v += 32) {
+    const uint4 h = hs[v];
+    dst[v] = h;
+    if (RFG_SDF_MIRROR) reinterpret_cast<uint2*>(m.vbaSdf + (size_t)ptr * kBlock3)[v] = sdf_pack4(h.x, h.y, h.z, h.w);
+  }
   if (m.vbaColour) {
     uint4* cd = reinterpret_cast<uint4*>(m.vbaColour + (size_t)ptr * kBlock3);
     const uint4* hc = reinterpret_cast<const uint4*>(src[2 * k + 1]);
@@ -116,6 +120,7 @@ __global__ void k_swapout_gather(DevMap m, const int* __restrict__ idx, const in
   for (int v = lane; v < kBlock3 / 4; v += 32) {
     hd[v] = src[v];
     src[v] = dflt;
+    if (RFG_SDF_MIRROR) reinterpret_cast<uint2*>(m.vbaSdf + (size_t)ptr * kBlock3)[v] = make_uint2(0x7FFF7FFFu, 0x7FFF7FFFu);
   }
   if (m.vbaColour) {
     uint4* cs = reinterpret_cast<uint4*>(m.vbaColour + (size_t)ptr * kBlock3);
@@ -157,6 +162,7 @@ __global__ void k_reserve_one(DevMap m, int idx, int* result) {
   if (ptr < 0) return;
   for (int v = threadIdx.x; v < kBlock3; v += blockDim.x) {  // Voxel{}: sdf 32767, w 0, colour 0
     m.vbaDepth[(size_t)ptr * kBlock3 + v] = kDefaultDepthVoxel;
+    if (RFG_SDF_MIRROR) m.vbaSdf[(size_t)ptr * kBlock3 + v] = (int16_t)kSdfOne;
     if (m.vbaColour) m.vbaColour[(size_t)ptr * kBlock3 + v] = 0u;
   }
 }
@@ -294,6 +300,7 @@ int swap_rank(rfg_swap* w, cudaStream_t s, int* nSel) {
 extern "C" {
 
 int rfg_swap_create(rfg_map* m, int capacity, rfg_swap** out) {
+  rfg::DeviceGuard dg_(m ? m->device : -1);
   SW_REQUIRE(m && out && capacity > 0, "invalid swap_create arguments");
   *out = nullptr;
   auto* w = new rfg_swap();
@@ -341,6 +348,7 @@ int rfg_swap_create(rfg_map* m, int capacity, rfg_swap** out) {
 }
 
 int rfg_swap_destroy(rfg_swap* w) {
+  rfg::DeviceGuard dg_(w && w->map ? w->map->device : -1);
   if (!w) return RFG_OK;
   if (w->map && w->map->stream) cudaStreamSynchronize(w->map->stream);
   swap_free(w);
@@ -348,6 +356,7 @@ int rfg_swap_destroy(rfg_swap* w) {
 }
 
 int rfg_swap_in(rfg_swap* w, int maxW, int* nIn) {
+  rfg::DeviceGuard dg_(w && w->map ? w->map->device : -1);
   SW_REQUIRE(w && nIn, "null argument");
   rfg_map* m = w->map;
   cudaStream_t s = m->stream;
@@ -378,6 +387,7 @@ int rfg_swap_in(rfg_swap* w, int maxW, int* nIn) {
 }
 
 int rfg_swap_out(rfg_swap* w, int* nOut) {
+  rfg::DeviceGuard dg_(w && w->map ? w->map->device : -1);
   SW_REQUIRE(w && nOut, "null argument");
   rfg_map* m = w->map;
   cudaStream_t s = m->stream;
@@ -409,6 +419,7 @@ int rfg_swap_out(rfg_swap* w, int* nOut) {
 }
 
 int rfg_map_reserve_block(rfg_map* m, int idx) {
+  rfg::DeviceGuard dg_(m ? m->device : -1);
   SW_REQUIRE(m && idx >= 0 && (uint32_t)idx < m->d.total, "invalid entry index");
   int* d = nullptr;
   int h = 0;
@@ -423,6 +434,7 @@ int rfg_map_reserve_block(rfg_map* m, int idx) {
 }
 
 int rfg_map_release_block(rfg_map* m, int idx) {
+  rfg::DeviceGuard dg_(m ? m->device : -1);
   SW_REQUIRE(m && idx >= 0 && (uint32_t)idx < m->d.total, "invalid entry index");
   rfg::k_release_one<<<1, 1, 0, m->stream>>>(m->d, idx);
   rfg::count_launch();
@@ -431,6 +443,7 @@ int rfg_map_release_block(rfg_map* m, int idx) {
 }
 
 int rfg_swap_export(rfg_swap* w, uint8_t* hasOut, uint8_t* ageOut) {
+  rfg::DeviceGuard dg_(w && w->map ? w->map->device : -1);
   SW_REQUIRE(w, "null swap");
   if (hasOut) std::memcpy(hasOut, w->hostHas.get(), w->total);
   if (ageOut) {
@@ -442,6 +455,7 @@ int rfg_swap_export(rfg_swap* w, uint8_t* hasOut, uint8_t* ageOut) {
 
 // the host-tier copy of entry idx as VoxelSRgb bytes (8 per voxel)
 int rfg_swap_host_block(rfg_swap* w, int idx, uint8_t* out4096) {
+  rfg::DeviceGuard dg_(w && w->map ? w->map->device : -1);
   SW_REQUIRE(w && out4096 && idx >= 0 && (uint32_t)idx < w->total, "invalid swap_host_block arguments");
   SW_REQUIRE(w->hostHas[idx], "entry has no host data");
   RFG_CK(cudaStreamSynchronize(w->map->stream));  // the slot is written by the swap-out kernel
