@@ -258,7 +258,6 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
   };
   bool ok = alloc((void**)&d.entries, padded * sizeof(int4)) &&
             alloc((void**)&d.vbaDepth, (size_t)d.capacity * kBlock3 * sizeof(uint32_t)) &&
-            (!RFG_SDF_MIRROR || alloc((void**)&d.vbaSdf, (size_t)d.capacity * kBlock3 * sizeof(int16_t))) &&
             (!cfg->hasColour || alloc((void**)&d.vbaColour, (size_t)d.capacity * kBlock3 * sizeof(uint32_t))) &&
             alloc((void**)&d.freeBlocks, (size_t)d.capacity * sizeof(int)) &&
             alloc((void**)&d.freeExcess, (size_t)(d.excess ? d.excess : 1) * sizeof(int)) &&
@@ -292,7 +291,7 @@ int rfg_map_destroy(rfg_map* m) {
   DeviceGuard dg_(m ? m->device : -1);
   if (!m) return RFG_OK;
   DevMap& d = m->d;
-  void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaSdf, d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
+  void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
                   d.visibility, d.reqKey, d.marked,     d.state,          d.tileCounts, d.tilePrefix,
                   m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount,
                   m->fwdPrev, m->fwdKeys, m->fwdTileCounts, m->fwdTilePrefix, m->rgbaScratch};
@@ -314,8 +313,6 @@ int rfg_map_clear(rfg_map* m) {
   const int4 e0 = make_entry(0, 0, 0, 0, -2);
   k_fill_u4<<<1024, 256, 0, s>>>(reinterpret_cast<uint4*>(d.entries), make_uint4(e0.x, e0.y, e0.z, e0.w), padded);
   k_fill_u32<<<4096, 256, 0, s>>>(d.vbaDepth, kDefaultDepthVoxel, (size_t)d.capacity * kBlock3);
-  if (d.vbaSdf) k_fill_u32<<<4096, 256, 0, s>>>(reinterpret_cast<uint32_t*>(d.vbaSdf), 0x7FFF7FFFu,
-                                                (size_t)d.capacity * kBlock3 / 2);
   if (d.vbaColour) RFG_CK(cudaMemsetAsync(d.vbaColour, 0, (size_t)d.capacity * kBlock3 * 4, s));
   k_iota<<<512, 256, 0, s>>>(d.freeBlocks, (int)d.capacity);
   if (d.excess) k_iota<<<512, 256, 0, s>>>(d.freeExcess, (int)d.excess);

@@ -401,53 +401,64 @@ __device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[3
   __syncthreads();  // sh is reused by the next round
 }
 
-// One evaluation's contribution of this CTA: its contiguous pixel range
-// [p0, p0 + span), thread t taking pixels p0 + t + k * kIcpThreads
-// (k < kIcpPx: camera points cached when `fill`; the rest uncached), added
-// to dst.  Every CTA has the same span, so they all run the same number of
-// flushes.  Returns false when a world point was outside the fixed-point
-// range.  (The sums are order-independent integers, so the pixel-to-thread
-// mapping does not change them.)
+// One evaluation's contribution of this CTA, added to dst.  The level's
+// pixels are dealt in 32-pixel chunks round-robin over the CTAs and their
+// warps: warp w of CTA c takes chunks c + nCta (w + 16 k), k = 0, 1, ...
+// (k < kIcpPx: camera points cached when `fill`; the rest uncached), so
+// every CTA samples the whole image (balanced work before the grid barrier)
+// and a coarse level still reaches every SM.  Returns false when a world
+// point was outside the fixed-point range.  (The sums are order-independent
+// integers, so the pixel-to-thread mapping does not change them.)
 __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShared& g, const Pose& rp,
-                                             const Intr& inl, float dist2, int n, int p0, int span,
-                                             long long (*sh)[32], float4* pcs, bool fill, unsigned long long* dst) {
+                                             const Intr& inl, float dist2, int n, int nCta, long long (*sh)[32],
+                                             float4* pcs, bool fill, unsigned long long* dst) {
   const Pose c2w = pose_from12(g.c2wF);
-  const int t = threadIdx.x;
-  const int activeWarps = min(kIcpThreads, span) / 32;  // span is a multiple of 32
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  constexpr int kWarps = kIcpThreads / 32;
+  const int nChunks = (n + 31) >> 5;
+  const int c = blockIdx.x;
+  // warps with at least one chunk (CTA-uniform), and the CTA's rounds
+  const int myChunks = nChunks > c ? (nChunks - c + nCta - 1) / nCta : 0;
+  const int activeWarps = min(kWarps, myChunks);
+  const int rounds = (myChunks + kWarps - 1) / kWarps;
+  auto pixel = [&](int k) -> int {
+    const int chunk = c + nCta * (wid + kWarps * k);
+    const int p = chunk * 32 + lane;
+    return (chunk < nChunks && p < n) ? p : -1;
+  };
   bool ok = true;
   IcpAcc s;
   acc_reset(s);
   if (fill) {
 #pragma unroll
     for (int k = 0; k < kIcpPx; ++k) {
-      const int o = t + k * kIcpThreads;
-      const int p = p0 + o;
-      float4 c = make_float4(0.f, 0.f, 0.f, -1.f);
-      if (o < span && p < n) {
+      const int p = pixel(k);
+      float4 cp = make_float4(0.f, 0.f, 0.f, -1.f);
+      if (p >= 0) {
         const float d = __ldg(a.depth + p);
         if (d > 0.f) {
           const int x = p % a.lw, y = p / a.lw;
           const f3 pc = backproject(inl, (float)x, (float)y, d);
-          c = make_float4(pc.x, pc.y, pc.z, 1.f);
+          cp = make_float4(pc.x, pc.y, pc.z, 1.f);
         }
       }
-      pcs[k * kIcpThreads + t] = c;  // each thread reads back only its own slots
+      pcs[k * kIcpThreads + t] = cp;  // each thread reads back only its own slots
     }
   }
 #pragma unroll
   for (int kb = 0; kb < kIcpPx; kb += kIcpGroup) {
-    if (kb * kIcpThreads >= span) break;  // uniform
+    if (kb >= rounds) break;  // CTA-uniform
     f3 pw[kIcpGroup];
     int pix[kIcpGroup];
 #pragma unroll
     for (int j = 0; j < kIcpGroup; ++j) {
       pix[j] = -1;
       if (kb + j >= kIcpPx) continue;
-      const float4 c = pcs[(kb + j) * kIcpThreads + t];
+      const float4 cp = pcs[(kb + j) * kIcpThreads + t];
       pw[j] = f3{0.f, 0.f, 0.f};
-      if (c.w > 0.f) {
+      if (cp.w > 0.f) {
         s.valid += 1;
-        pw[j] = pose_apply(c2w, f3{c.x, c.y, c.z});
+        pw[j] = pose_apply(c2w, f3{cp.x, cp.y, cp.z});
         pix[j] = icp_associate(a, rp, pw[j]);
       }
     }
@@ -463,16 +474,15 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
     for (int j = 0; j < kIcpGroup; ++j)
       if (pix[j] >= 0) ok &= icp_add(s, pw[j], V[j], N[j], dist2);
   }
-  // pixels beyond the cached slots (large images), uncached, flushed every
+  // rounds beyond the cached slots (large images), uncached, flushed every
   // kIcpFlush pixels (the fixed-point accumulators' range)
-  for (int k = kIcpPx; k * kIcpThreads < span; ++k) {
+  for (int k = kIcpPx; k < rounds; ++k) {
     if (k % kIcpFlush == 0) {
       icp_cta_flush(s, sh, dst, activeWarps);
       acc_reset(s);
     }
-    const int o = t + k * kIcpThreads;
-    const int p = p0 + o;
-    if (o >= span || p >= n) continue;
+    const int p = pixel(k);
+    if (p < 0) continue;
     const float d = __ldg(a.depth + p);
     if (!(d > 0.f)) continue;
     s.valid += 1;
@@ -487,13 +497,9 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
   return ok;
 }
 
-// Pixels per CTA when n pixels are spread over nCta CTAs (a multiple of 32).
-__host__ __device__ __forceinline__ int icp_span(int n, int nCta) { return ((n + nCta - 1) / nCta + 31) & ~31; }
-
 // One level's Gauss-Newton loop on the CTA-local state g.  CTAs with
-// blockIdx.x < nCta own the level's pixels (contiguous ranges of
-// icp_span(n, nCta)); the others only join the barriers and run the same
-// solve.  `gi` counts
+// blockIdx.x < nCta own the level's pixels (icp_cta_eval's chunks); the
+// others only join the barriers and run the same solve.  `gi` counts
 // iterations across levels (accumulator rotation, with the launch's `gen`).
 __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& a, int nCta, GnShared& g,
                                               long long (*sh)[32], float4* pcs, unsigned gen, int& gi,
@@ -510,8 +516,7 @@ __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& 
     if (timed) t0 = gtimer();
     unsigned long long* buf = st->acc[(gen + gi) % 3];
     if (owner) {
-      const int span = icp_span(n, nCta);
-      const bool ok = icp_cta_eval(a, g, rp, inl, dist2, n, blockIdx.x * span, span, sh, pcs, it == 0, buf);
+      const bool ok = icp_cta_eval(a, g, rp, inl, dist2, n, nCta, sh, pcs, it == 0, buf);
       if (!ok) st->error = 1;
     }
     if (blockIdx.x == 0 && threadIdx.x < 32) st->acc[(gen + gi + 1) % 3][threadIdx.x] = 0ull;

@@ -80,8 +80,7 @@ __device__ __forceinline__ int16_t sdf_from_logical_alu(float f) {
 }
 
 template <bool kWindowKnown>
-__device__ __forceinline__ void integrate_block_depth(uint4* blk, uint2* sblk, int lane, int ox, int oy, int oz,
-                                                      const Pose& pose,
+__device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int ox, int oy, int oz, const Pose& pose,
                                                       const FrameArgs& fa, const float* __restrict__ depth, float wLim,
                                                       float hLim, float mu, bool muOk, float rMu, bool capW, int maxW,
                                                       const float* rcpTab) {
@@ -205,9 +204,6 @@ __device__ __forceinline__ void integrate_block_depth(uint4* blk, uint2* sblk, i
     for (int q = g; q < g + kQG; ++q) {
       const int k = (q - g) * 4;
       blk[q * 32 + lane] = make_uint4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
-#if RFG_SDF_MIRROR
-      sblk[q * 32 + lane] = sdf_pack4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
-#endif
     }
   }
 }
@@ -263,12 +259,11 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
     if (e.w < 0) continue;
     const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
     uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
-    uint2* sblk = RFG_SDF_MIRROR ? reinterpret_cast<uint2*>(m.vbaSdf + (size_t)e.w * kBlock3) : nullptr;
     if (block_window_known(lane, ox, oy, oz, pose, fa))
-      integrate_block_depth<true>(blk, sblk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
+      integrate_block_depth<true>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
                                   maxW, rcpTab);
     else
-      integrate_block_depth<false>(blk, sblk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
+      integrate_block_depth<false>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
                                    maxW, rcpTab);
   }
 }
@@ -333,8 +328,7 @@ __device__ __forceinline__ bool colour_pixel(const Pose& M, const ColourArgs& ca
 }
 
 template <bool kSameCamera>
-__device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, uint2* sblk, int lane, int ox, int oy,
-                                                     int oz,
+__device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, int lane, int ox, int oy, int oz,
                                                      const Pose& pose, const Pose& Mrgb, const FrameArgs& fa,
                                                      const ColourArgs& ca, const float* __restrict__ depth,
                                                      float wLim, float hLim, float mu, bool muOk, float rMu, bool capW,
@@ -432,9 +426,6 @@ __device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, ui
       if (cin[i]) cw[i] = colour_merge(cw[i], cx4[i], cy4[i], ca, maxW, tap[i][0], tap[i][1], tap[i][2], tap[i][3]);
     blk[q * 32 + lane] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     cblk[q * 32 + lane] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-#if RFG_SDF_MIRROR
-    sblk[q * 32 + lane] = sdf_pack4(wd[0], wd[1], wd[2], wd[3]);
-#endif
   }
 }
 
@@ -445,8 +436,7 @@ __device__ __forceinline__ void integrate_block_rgbd(uint4* blk, uint4* cblk, ui
 // quotients inside div_fast's window).  The colour taps of the gated voxels
 // are loaded (predicated) before any is used.
 template <bool kWindowKnown>
-__device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cblk, uint2* sblk, int lane, int ox,
-                                                          int oy, int oz,
+__device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cblk, int lane, int ox, int oy, int oz,
                                                           const Pose& pose, const FrameArgs& fa, const ColourArgs& ca,
                                                           const float* __restrict__ depth, float wLim, float hLim,
                                                           float mu, bool muOk, float rMu, bool capW, int maxW) {
@@ -550,9 +540,6 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
     }
     blk[q * 32 + lane] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     cblk[q * 32 + lane] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-#if RFG_SDF_MIRROR
-    sblk[q * 32 + lane] = sdf_pack4(wd[0], wd[1], wd[2], wd[3]);
-#endif
   }
 }
 
@@ -583,20 +570,19 @@ __global__ void __launch_bounds__(256, RFG_RGBD_MINB) k_integrate_rgbd(DevMap m,
     const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
     uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
     uint4* cblk = reinterpret_cast<uint4*>(m.vbaColour + (size_t)e.w * kBlock3);
-    uint2* sblk = RFG_SDF_MIRROR ? reinterpret_cast<uint2*>(m.vbaSdf + (size_t)e.w * kBlock3) : nullptr;
 #ifdef RFG_RGBD_OLD
     if (false) {
 #else
     if (kSameCamera) {
 #endif
       if (block_window_known(lane, ox, oy, oz, pose, fa))
-        integrate_block_rgbd_same<true>(blk, cblk, sblk, lane, ox, oy, oz, pose, fa, ca, depth, wLim, hLim, mu, muOk, rMu,
+        integrate_block_rgbd_same<true>(blk, cblk, lane, ox, oy, oz, pose, fa, ca, depth, wLim, hLim, mu, muOk, rMu,
                                         capW, maxW);
       else
-        integrate_block_rgbd_same<false>(blk, cblk, sblk, lane, ox, oy, oz, pose, fa, ca, depth, wLim, hLim, mu, muOk, rMu,
+        integrate_block_rgbd_same<false>(blk, cblk, lane, ox, oy, oz, pose, fa, ca, depth, wLim, hLim, mu, muOk, rMu,
                                          capW, maxW);
     } else {
-      integrate_block_rgbd<kSameCamera>(blk, cblk, sblk, lane, ox, oy, oz, pose, Mrgb, fa, ca, depth, wLim, hLim, mu, muOk,
+      integrate_block_rgbd<kSameCamera>(blk, cblk, lane, ox, oy, oz, pose, Mrgb, fa, ca, depth, wLim, hLim, mu, muOk,
                                         rMu, capW, maxW);
     }
   }

@@ -10,10 +10,6 @@
 
 #include "../../include/rfg.h"
 
-#ifndef RFG_SDF_MIRROR
-#define RFG_SDF_MIRROR 0
-#endif
-
 namespace rfg {
 
 // Device-resident mutable scalars of a map.
@@ -35,7 +31,6 @@ struct DevMap {
   uint32_t buckets, excess, capacity, total;
   int4* entries;           // total x 16 B
   uint32_t* vbaDepth;      // capacity x 512 depth voxels (4 B)
-  int16_t* vbaSdf;         // RFG_SDF_MIRROR: capacity x 512 sdf values (2 B), the raycast's copy
   uint32_t* vbaColour;     // capacity x 512 colour voxels (4 B) or nullptr
   int* freeBlocks;         // capacity
   int* freeExcess;         // excess

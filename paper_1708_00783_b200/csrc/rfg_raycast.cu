@@ -165,18 +165,13 @@ __device__ unsigned long long g_rc_stats[32];
 // TSDF field reader (MapField, raycast.hpp:32-45) with the reference's
 // last-block cache.  Voxel offsets inside a block use bit operations
 // (v & 7 == v - (v >> 3) * 8 for negative v too).
-// The voxels the raycast reads: the 2-B sdf mirror plane (RFG_SDF_MIRROR:
-// twice the voxels per L1 / L2 line of the 4-B depth plane), or the depth
-// plane's sdf halves.
-#if RFG_SDF_MIRROR
-typedef int16_t FieldVoxel;
-#define RFG_FIELD_PLANE(m) ((m).vbaSdf)
-__device__ __forceinline__ int16_t field_sdf(int16_t v) { return v; }
-#else
+// The voxels the raycast reads (the depth plane's sdf halves).  (A 2-B sdf
+// mirror plane written by the integration — twice the voxels per L1 / L2
+// line — was measured: raycast -2 % at C2 / -4 % at C4, integration +2 %,
+// frame +1 %; not kept.)
 typedef uint32_t FieldVoxel;
 #define RFG_FIELD_PLANE(m) ((m).vbaDepth)
 __device__ __forceinline__ int16_t field_sdf(uint32_t v) { return vox_sdf(v); }
-#endif
 
 struct FieldReader {
   const int4* entries;

@@ -82,7 +82,6 @@ __global__ void k_swapin_apply(DevMap m, const int* __restrict__ idx, const uint
   for (int v = lane; v < kBlock3 / 4; v += 32) {
     const uint4 h = hs[v];
     dst[v] = h;
-    if (RFG_SDF_MIRROR) reinterpret_cast<uint2*>(m.vbaSdf + (size_t)ptr * kBlock3)[v] = sdf_pack4(h.x, h.y, h.z, h.w);
   }
   if (m.vbaColour) {
     uint4* cd = reinterpret_cast<uint4*>(m.vbaColour + (size_t)ptr * kBlock3);
@@ -120,7 +119,6 @@ __global__ void k_swapout_gather(DevMap m, const int* __restrict__ idx, const in
   for (int v = lane; v < kBlock3 / 4; v += 32) {
     hd[v] = src[v];
     src[v] = dflt;
-    if (RFG_SDF_MIRROR) reinterpret_cast<uint2*>(m.vbaSdf + (size_t)ptr * kBlock3)[v] = make_uint2(0x7FFF7FFFu, 0x7FFF7FFFu);
   }
   if (m.vbaColour) {
     uint4* cs = reinterpret_cast<uint4*>(m.vbaColour + (size_t)ptr * kBlock3);
@@ -162,7 +160,6 @@ __global__ void k_reserve_one(DevMap m, int idx, int* result) {
   if (ptr < 0) return;
   for (int v = threadIdx.x; v < kBlock3; v += blockDim.x) {  // Voxel{}: sdf 32767, w 0, colour 0
     m.vbaDepth[(size_t)ptr * kBlock3 + v] = kDefaultDepthVoxel;
-    if (RFG_SDF_MIRROR) m.vbaSdf[(size_t)ptr * kBlock3 + v] = (int16_t)kSdfOne;
     if (m.vbaColour) m.vbaColour[(size_t)ptr * kBlock3 + v] = 0u;
   }
 }
