@@ -1663,18 +1663,37 @@ static void matmul3d(const double* A, const double* B, double* C) {
     for (int c = 0; c < 3; ++c) C[r * 3 + c] = A[r * 3 + 0] * B[c] + (A[r * 3 + 1] * B[3 + c] + A[r * 3 + 2] * B[6 + c]);
 }
 /* sin(x)/x, (1 - cos x)/x^2, (x - sin x)/x^3 for t = x^2 < 1 by their Taylor
- * series (nested; the truncation is below 1e-19): basic IEEE operations only,
- * so the B200 (rfg_icp.cu:se3_coeffs) evaluates them bit-identically. */
+ * series, nested, with as many terms as t needs: the first dropped term is
+ * below 2^-64 of the value (t < 2^-40: 2 terms; < 2^-20: 3; < 2^-8: 6;
+ * else 10).  Basic IEEE operations only, so the B200
+ * (rfg_icp.cu:se3_series) evaluates them bit-identically. */
 static void se3_series(double t, double* a, double* b, double* c) {
-  *a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
-       (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
-       (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
-  *b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
-       (1.0 - t * (1.0 / 132.0) * (1.0 - t * (1.0 / 182.0) * (1.0 - t * (1.0 / 240.0) * (1.0 - t * (1.0 / 306.0) *
-       (1.0 - t * (1.0 / 380.0))))))))));
-  *c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
-       (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
-       (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+  if (t < 0x1p-40) {
+    *a = 1.0 - t * (1.0 / 6.0);
+    *b = 0.5 * (1.0 - t * (1.0 / 12.0));
+    *c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0));
+  } else if (t < 0x1p-20) {
+    *a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0));
+    *b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0)));
+    *c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0)));
+  } else if (t < 0x1p-8) {
+    *a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0)))));
+    *b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
+         (1.0 - t * (1.0 / 132.0))))));
+    *c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0))))));
+  } else {
+    *a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+         (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+    *b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
+         (1.0 - t * (1.0 / 132.0) * (1.0 - t * (1.0 / 182.0) * (1.0 - t * (1.0 / 240.0) * (1.0 - t * (1.0 / 306.0) *
+         (1.0 - t * (1.0 / 380.0))))))))));
+    *c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+         (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+  }
 }
 /* Rodrigues coefficients of exp([omega]x) for th2 = |omega|^2: the series
  * below 1 rad; above, sin/cos of theta / 2^k by the series and k exact
@@ -1703,6 +1722,9 @@ static void se3_coeffs(double th2, double* a, double* b, double* c) {
   *b = (1.0 - co) / th2;
   *c = (theta - s) / (theta * th2);
 }
+/* test hook: the three Rodrigues coefficients for th2 */
+void rfo_se3_coeffs(double th2, double* abc) { se3_coeffs(th2, &abc[0], &abc[1], &abc[2]); }
+
 static posed_t se3_exp(const double* tau) {
   const double* w = tau;
   const double* v = tau + 3;

@@ -109,7 +109,9 @@ int rfo_icp_reduce(const float* depth, int lw, int lh, const float* f4l, const f
                    const int* wh, const float* renderPose12, const float* renderF4, const float* camToWorld12,
                    float dist, int64_t* sums31, double* out31);
 
-/* Cholesky solve of H delta = -g from the decoded sums; det(H/n) to *det;
+/* the Rodrigues coefficients sin t/t, (1-cos t)/t^2, (t-sin t)/t^3 at th2 = t^2 */
+void rfo_se3_coeffs(double th2, double* abc3);
+/* LDL^T solve of H delta = -g from the decoded sums; det(H/n) to *det;
  * -1 when degenerate. */
 int rfo_solve6(const double* sums31, double* x, double* det);
 

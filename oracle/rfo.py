@@ -74,6 +74,7 @@ def lib():
         L.rfo_icp_reduce.argtypes = [_f, C.c_int, C.c_int, _f, _f, _f, _i, _f, _f, _f, C.c_float,
                                      C.POINTER(C.c_int64), _d]
         L.rfo_solve6.argtypes = [_d, _d, _d]
+        L.rfo_se3_coeffs.argtypes = [C.c_double, _d]
         L.rfo_forward_project.argtypes = [C.c_int, _f, _f, _f, _f, _i, _f, C.c_float, _i]
         L.rfo_render_icp_list.argtypes = [vp, _f, _i, _f, _f, _i, C.c_int, _f, _f, _f]
         L.rfo_set_threads.argtypes = [C.c_int]
@@ -210,6 +211,12 @@ def icp_reduce(depth_l, f4l, points, normals, intr, render_pose34, render_intr, 
     lib().rfo_icp_reduce(P(d, _f), lw, lh, P(f4l, _f), P(pts, _f), P(nrm, _f), P(wh, _i), P(rp, _f), P(rf4, _f),
                          P(c2w, _f), dist, raw.ctypes.data_as(C.POINTER(C.c_int64)), P(out, _d))
     return raw if fixed else out
+
+
+def se3_coeffs(th2):
+    out = np.zeros(3, np.float64)
+    lib().rfo_se3_coeffs(float(th2), P(out, _d))
+    return out
 
 
 def solve6(sums31):

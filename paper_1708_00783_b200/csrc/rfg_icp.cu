@@ -111,17 +111,35 @@ __device__ void c2w_to_float(const double* c, float* f) {
   for (int i = 0; i < 12; ++i) f[i] = (float)c[i];
 }
 
-// rfo.c:se3_series — sin(x)/x, (1 - cos x)/x^2, (x - sin x)/x^3 for t = x^2 < 1
+// rfo.c:se3_series — sin(x)/x, (1 - cos x)/x^2, (x - sin x)/x^3 for t = x^2 < 1,
+// as many Taylor terms as t needs (the same tiers as the oracle)
 __device__ __forceinline__ void se3_series(double t, double& a, double& b, double& c) {
-  a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
-      (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
-      (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
-  b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
-      (1.0 - t * (1.0 / 132.0) * (1.0 - t * (1.0 / 182.0) * (1.0 - t * (1.0 / 240.0) * (1.0 - t * (1.0 / 306.0) *
-      (1.0 - t * (1.0 / 380.0))))))))));
-  c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
-      (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
-      (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+  if (t < 0x1p-40) {
+    a = 1.0 - t * (1.0 / 6.0);
+    b = 0.5 * (1.0 - t * (1.0 / 12.0));
+    c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0));
+  } else if (t < 0x1p-20) {
+    a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0));
+    b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0)));
+    c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0)));
+  } else if (t < 0x1p-8) {
+    a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0)))));
+    b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
+         (1.0 - t * (1.0 / 132.0))))));
+    c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0))))));
+  } else {
+    a = 1.0 - t * (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+         (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+    b = 0.5 * (1.0 - t * (1.0 / 12.0) * (1.0 - t * (1.0 / 30.0) * (1.0 - t * (1.0 / 56.0) * (1.0 - t * (1.0 / 90.0) *
+         (1.0 - t * (1.0 / 132.0) * (1.0 - t * (1.0 / 182.0) * (1.0 - t * (1.0 / 240.0) * (1.0 - t * (1.0 / 306.0) *
+         (1.0 - t * (1.0 / 380.0))))))))));
+    c = (1.0 / 6.0) * (1.0 - t * (1.0 / 20.0) * (1.0 - t * (1.0 / 42.0) * (1.0 - t * (1.0 / 72.0) *
+         (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
+         (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
+  }
 }
 
 // rfo.c:se3_coeffs — the series below 1 rad, else halving + double angles
@@ -259,9 +277,15 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
   double ER[9], V[9], Et[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
-    const double I = (i % 4 == 0) ? 1.0 : 0.0;
-    ER[i] = I + ca * W[i] + cb * WW[i];
-    V[i] = I + cb * W[i] + cc * WW[i];
+    if (i % 4 == 0) {
+      // diagonal: W[i] = 0, and 1 + (a * 0) == 1 exactly for any finite a,
+      // so the oracle's (I + a W) + b WW is 1 + b WW here
+      ER[i] = 1.0 + cb * WW[i];
+      V[i] = 1.0 + cc * WW[i];
+    } else {
+      ER[i] = 0.0 + ca * W[i] + cb * WW[i];
+      V[i] = 0.0 + cb * W[i] + cc * WW[i];
+    }
   }
 #pragma unroll
   for (int r = 0; r < 3; ++r) Et[r] = V[r * 3] * v[0] + (V[r * 3 + 1] * v[1] + V[r * 3 + 2] * v[2]);
