@@ -67,13 +67,6 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 // products R_0x px, R_3x px, R_6x px hoisted out of the rows (a lane's four
 // voxels per row have the same x in every row), and 1/(w+1) from a per-CTA
 // table (the exact div_rcp values) instead of a reciprocal per voxel.
-__device__ __forceinline__ float sdf_to_logical_alu(int16_t s) {
-  const float x = s16_to_float(s);
-  const float r = 1.f / 32767.f;
-  const float q = x * r;
-  const float e = __fmaf_rn(-q, (float)kSdfOne, x);
-  return __fmaf_rn(e, r, q);
-}
 __device__ __forceinline__ int16_t sdf_from_logical_alu(float f) {
   float c = f < -1.f ? -1.f : (1.f < f ? 1.f : f);
   return (int16_t)lround_haz_alu(c * (float)kSdfOne);

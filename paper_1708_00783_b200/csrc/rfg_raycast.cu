@@ -4,6 +4,10 @@
 //  cast_ray_field :54-112 and field_normal :137-153).
 #include "rfg_common.cuh"
 
+#ifndef RFG_RC_ALU
+#define RFG_RC_ALU 1  // the march's conversions on the FMA/ALU pipes (0: XU conversions)
+#endif
+
 namespace rfg {
 
 // ------------------------------------------------------ expected ranges
@@ -214,12 +218,20 @@ struct FieldReader {
   }
   // readSdfNearest (voxel_block_map.cpp:178-185)
   __device__ __forceinline__ float nearest(f3 p, bool& ok) {
+#if RFG_RC_ALU
+    const int vx = lround_haz_alu(p.x), vy = lround_haz_alu(p.y), vz = lround_haz_alu(p.z);
+#else
     const int vx = lround_haz(p.x), vy = lround_haz(p.y), vz = lround_haz(p.z);
+#endif
     const int ptr = ptr_of(vx >> 3, vy >> 3, vz >> 3);
     ok = ptr >= 0;
     if (!ok) return 1.f;
     const FieldVoxel w = __ldg(vba + (size_t)ptr * kBlock3 + ((vx & 7) | ((vy & 7) << 3) | ((vz & 7) << 6)));
+#if RFG_RC_ALU
+    return sdf_to_logical_alu(field_sdf(w));
+#else
     return sdf_to_logical(field_sdf(w));
+#endif
   }
   // readSdfWeightTrilinear (voxel_block_map.cpp:130-156).  Any missing
   // corner invalidates the read, so the corner order only matters for the
@@ -265,7 +277,11 @@ struct FieldReader {
     for (int k = 0; k < 8; ++k) {
       const float bw =
           ((k & 1) ? fx : 1.f - fx) * (((k >> 1) & 1) ? fy : 1.f - fy) * (((k >> 2) & 1) ? fz : 1.f - fz);
+#if RFG_RC_ALU
+      sdf += bw * sdf_to_logical_alu(field_sdf(w[k]));
+#else
       sdf += bw * sdf_to_logical(field_sdf(w[k]));
+#endif
     }
     ok = true;
     return sdf;
@@ -522,7 +538,10 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_maps(DevMap m, Fra
 // in a register; it is also stored for the caller), then marches its pixels
 // (warps of 16x2 pixels, as k_raycast_maps).  One launch and one pass over
 // the range image fewer.
-__global__ void __launch_bounds__(kRangeTile* kRangeTile) k_raycast_tiles(DevMap m, FrameArgs fa, float2* range,
+#ifndef RFG_RC_TILES_MINB
+#define RFG_RC_TILES_MINB 1
+#endif
+__global__ void __launch_bounds__(kRangeTile* kRangeTile, RFG_RC_TILES_MINB) k_raycast_tiles(DevMap m, FrameArgs fa, float2* range,
                                                                           float4* raycast, float4* points,
                                                                           float4* normals) {
   __shared__ int4 sb[kRangeTile * kRangeTile];
