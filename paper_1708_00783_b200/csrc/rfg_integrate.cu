@@ -62,6 +62,9 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 #ifndef RFG_INT_DIET
 #define RFG_INT_DIET 1
 #endif
+#ifndef RFG_INT_TMA
+#define RFG_INT_TMA 0  // depth integration with TMA-prefetched voxel rows (k_integrate_depth_tma)
+#endif
 // RFG_INT_DIET: the per-voxel int<->float conversions and roundings on the
 // FMA/ALU pipes (rfg_common.cuh magic conversions), the lane's x-column
 // products R_0x px, R_3x px, R_6x px hoisted out of the rows (a lane's four
@@ -73,7 +76,8 @@ __device__ __forceinline__ int16_t sdf_from_logical_alu(float f) {
 }
 
 template <bool kWindowKnown>
-__device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int ox, int oy, int oz, const Pose& pose,
+__device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* blk, int lane, int ox, int oy, int oz,
+                                                      const Pose& pose,
                                                       const FrameArgs& fa, const float* __restrict__ depth, float wLim,
                                                       float hLim, float mu, bool muOk, float rMu, bool capW, int maxW,
                                                       const float* rcpTab) {
@@ -94,7 +98,7 @@ __device__ __forceinline__ void integrate_block_depth(uint4* blk, int lane, int 
     uint32_t wd[4 * kQG];
 #pragma unroll
     for (int q = g; q < g + kQG; ++q) {
-      const uint4 r = blk[q * 32 + lane];
+      const uint4 r = src[q * 32 + lane];  // the voxel rows: global memory, or the TMA-staged copy
       wd[(q - g) * 4 + 0] = r.x;
       wd[(q - g) * 4 + 1] = r.y;
       wd[(q - g) * 4 + 2] = r.z;
@@ -253,11 +257,114 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
     const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
     uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
     if (block_window_known(lane, ox, oy, oz, pose, fa))
-      integrate_block_depth<true>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
+      integrate_block_depth<true>(blk, blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
                                   maxW, rcpTab);
     else
-      integrate_block_depth<false>(blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
+      integrate_block_depth<false>(blk, blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
                                    maxW, rcpTab);
+  }
+}
+
+// ---------------------------------------- depth-only, TMA-prefetched rows
+// The same per-block update with the block's 2 KiB of depth voxels brought
+// into shared memory by the bulk-copy engine (cp.async.bulk, completion on
+// an mbarrier) one block ahead of the warp that integrates it: a persistent
+// grid (every CTA resident), each warp owning every nw-th visible block; a
+// warp's lanes fetch the entries of its next 32 blocks in one batch, lane 0
+// issues the bulk copy of block k+1 before integrating block k from its
+// staged copy (2 stages per warp), and the results are stored to global
+// memory directly.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load_2k(void* dst, const void* src, unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage's generic reads before the async write
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(2048u) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(2048u), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kTmaWarps = 8;
+__global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth_tma(DevMap m, const float* __restrict__ depth,
+                                                                           FrameArgs fa) {
+  __shared__ __align__(128) uint4 stage[kTmaWarps][2][kBlock3 / 4];
+  __shared__ __align__(8) unsigned long long bar[kTmaWarps][2];
+  __shared__ float rcpTab[256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kTmaWarps + w;
+  const int nw = gridDim.x * kTmaWarps;
+  const int nVis = *((volatile int*)&m.state->nVisible);
+  const Pose pose = frame_pose(fa);
+  const float wLim = (float)(fa.w - 2), hLim = (float)(fa.h - 2);
+  const float mu = fa.mu;
+  const bool muOk = mu >= 0x1p-20f && mu <= 0x1p20f;
+  const float rMu = div_rcp(mu);
+  const bool capW = fa.stopAtMaxW != 0;
+  const int maxW = fa.maxW;
+  rcpTab[threadIdx.x] = div_rcp((float)(threadIdx.x + 1));
+  if (lane == 0) {
+    mbar_init(&bar[w][0], 1);
+    mbar_init(&bar[w][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nMine = nVis > gw ? (nVis - gw + nw - 1) / nw : 0;  // this warp's blocks
+  unsigned phase = 0u;  // bit s: the parity stage s waits for next
+  int4 eb = make_int4(0, 0, 0, -1);  // lane k: the entry of batch block k
+  for (int base = 0; base < nMine; base += 32) {
+    // one batched round of entry loads for the next 32 blocks
+    const int kk = base + lane;
+    eb = kk < nMine ? ld_entry(m.entries, m.visibleList[gw + kk * nw]) : make_int4(0, 0, 0, -1);
+    const int nb = min(32, nMine - base);
+    // prologue: the batch's first block
+    {
+      const int ptr0 = __shfl_sync(0xffffffffu, eb.w, 0);
+      if (lane == 0 && ptr0 >= 0)
+        bulk_load_2k(stage[w][base & 1], m.vbaDepth + (size_t)ptr0 * kBlock3, &bar[w][base & 1]);
+    }
+    for (int k = 0; k < nb; ++k) {
+      const int i = base + k, s = i & 1;
+      int4 e;
+      e.x = __shfl_sync(0xffffffffu, eb.x, k);
+      e.y = __shfl_sync(0xffffffffu, eb.y, k);
+      e.w = __shfl_sync(0xffffffffu, eb.w, k);
+      // the next block of the batch into the other stage (its last reader,
+      // block i - 1, finished before the __syncwarp below)
+      if (k + 1 < nb) {
+        const int pn = __shfl_sync(0xffffffffu, eb.w, k + 1);
+        if (lane == 0 && pn >= 0)
+          bulk_load_2k(stage[w][s ^ 1], m.vbaDepth + (size_t)pn * kBlock3, &bar[w][s ^ 1]);
+      }
+      if (e.w >= 0) {
+        mbar_wait(&bar[w][s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+        const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
+        uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
+        if (block_window_known(lane, ox, oy, oz, pose, fa))
+          integrate_block_depth<true>(stage[w][s], blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk,
+                                      rMu, capW, maxW, rcpTab);
+        else
+          integrate_block_depth<false>(stage[w][s], blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk,
+                                       rMu, capW, maxW, rcpTab);
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -647,7 +754,11 @@ cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint32_t
     else
       k_integrate_rgbd<false><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
   } else {
+#if RFG_INT_TMA
+    k_integrate_depth_tma<<<current_sm_count() * RFG_INT_MINB, 256, 0, s>>>(m, depth, fa);
+#else
     k_integrate_depth<<<integrate_grid(), 256, 0, s>>>(m, depth, fa);
+#endif
   }
   count_launch();
   return cudaGetLastError();
