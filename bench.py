@@ -428,6 +428,10 @@ def run_b200(args):
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
+        # NCCL's communicator-init lines (nranks, NVLS / P2P transport) on
+        # stderr, so a multi-GPU run shows the world it ran on
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind = load_peaks()
     w = Workload(wl_name, rank, world, local, sharded)
@@ -594,6 +598,31 @@ def run_b200(args):
                               "frac": b / (it["us_per_launch"] * 1e-6) / 1e9 / peak})
         w.reset()
 
+    per_rank = None
+    if args.profile_frames > 0 and sharded:
+        # every rank: its integration kernel's CUPTI duration and its shard's
+        # visible blocks over the same frames -> its integration GB/s
+        nprof = min(w.n, args.warmup + args.profile_frames)
+        w.reset()
+        for f in range(args.warmup):
+            w.step(f)
+        kt_r = cupti_kernel_us(w.step, w.stream, flush, range(args.warmup, nprof))
+        w.reset()
+        nv = []
+        for f in range(nprof):
+            w.step(f)
+            if f >= args.warmup:
+                nv.append(w.pipe.result()[0].visibleCount)
+        mine = {"rank": rank, "mean_visible_blocks": float(np.mean(nv))}
+        ki = kt_r.get("rfg::k_integrate_depth")
+        if ki:
+            b = integrate_bytes(mine["mean_visible_blocks"], False)
+            mine.update({"integrate_us": ki["us_per_launch"], "integrate_GBps": b / (ki["us_per_launch"] * 1e-6) / 1e9,
+                         "integrate_frac": b / (ki["us_per_launch"] * 1e-6) / 1e9 / peak})
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+        w.reset()
+
     configs = None
     if rank == 0 and world == 1 and args.configs and wl_name == "c2":
         configs = {}
@@ -636,7 +665,7 @@ def run_b200(args):
         "roofline_secondary": secondary, "stage_ms": prof,
         "kernel_us_per_frame": {k: round(v["us_per_frame"], 2) for k, v in
                                 sorted(kt.items(), key=lambda x: -x[1]["us_per_frame"])} if kt else None,
-        "configs": configs,
+        "configs": configs, "per_rank": per_rank,
         "cpu_baseline": cpu, "step_ms_p50": float(np.median(step_ms)), "step_ms_max": float(np.max(step_ms)),
     }
     emit(line)

@@ -772,6 +772,7 @@ struct rfg_pipeline {
   cudaGraphNode_t rgbNode[2];
   cudaKernelNodeParams rgbParams[2];
   const uint8_t* rgbSrc[2];
+  unsigned binGen[2];  // the map's range-scratch generation each graph captured
 };
 
 namespace {
@@ -866,6 +867,20 @@ int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc, cons
     k_set12<<<1, 32, 0, p->stream>>>(p->poses, pv);
     count_launch();
   }
+  // the map's range scratch may have been reallocated for another image size
+  // (a map-level render): size it for this pipeline again, and re-capture a
+  // graph that holds the old scratch (no replay of freed bins)
+  if (ensure_range_scratch(p->map, p->cfg.intr.width, p->cfg.intr.height) != RFG_OK) return RFG_ENOMEM;
+  for (int k = 0; k < 2; ++k) {
+    if (p->exec[k] && p->binGen[k] != p->map->d.binGen) {
+      cudaGraphExecDestroy(p->exec[k]);
+      cudaGraphDestroy(p->graph[k]);
+      p->exec[k] = nullptr;
+      p->graph[k] = nullptr;
+      p->viewNode[k] = nullptr;
+      p->rgbNode[k] = nullptr;
+    }
+  }
   if (!p->cfg.use_graph) {
     if (p->cfg.colour && rgbSrc && rgbSrc != p->rgbDev)
       RFG_CK(cudaMemcpyAsync(p->rgbDev, rgbSrc, (size_t)p->cfg.intr_rgb.width * p->cfg.intr_rgb.height * 3,
@@ -885,6 +900,7 @@ int run_frame(rfg_pipeline* p, const float* pose34, const uint16_t* rawSrc, cons
       g_launches.fetch_sub(p->graphKernels[gi]);  // capture does not launch
       RFG_CK(cudaGraphInstantiate(&p->exec[gi], g, 0));
       p->graph[gi] = g;
+      p->binGen[gi] = p->map->d.binGen;
       p->viewRaw[gi] = p->rawDev;
       p->rgbSrc[gi] = p->rgbDev;
       const bool fusedView = view_is_fused(p->cfg.bilateral, false, false, p->cfg.levels);

@@ -142,3 +142,69 @@ def test_pipeline_pinned_host_frames_equal_device_frames():
         assert np.array_equal(ent, outs[0][1])
         for (pa, ia, sa), (pb, ib, sb) in zip(res, outs[0][0]):
             assert np.array_equal(pa, pb) and np.array_equal(ia, ib) and sa == sb
+
+
+def test_pipeline_recaptures_after_range_scratch_reallocation():
+    """a map-level render at another image size
+    reallocates the map's expected-range scratch, which a pipeline's captured
+    frame graph holds; the pipeline must re-capture instead of replaying the
+    freed scratch.  The interrupted pipeline matches an uninterrupted one
+    bit for bit."""
+    import torch
+    from paper_1708_00783_b200 import fusion as F
+    intr = F.Intrinsics(320, 240, 262.5, 262.5, 159.5, 119.5)
+    small = F.Intrinsics(160, 120, 131.25, 131.25, 79.5, 59.5)
+    params = F.SceneParams()
+    poses = F.orbit_trajectory(frames=100)
+    cfg = F.VoxelBlockMapConfig(1 << 16, 1 << 14, 1 << 16)
+    m1, m2 = F.VoxelBlockMap(cfg), F.VoxelBlockMap(cfg)
+    p1, p2 = F.Pipeline(m1, intr, params), F.Pipeline(m2, intr, params)
+    for f in range(8):
+        raw = torch.from_numpy(F.synth_render(0, poses[f], intr)[0].view(np.int16)).cuda()
+        if f in (3, 5):  # another size on the pipeline's map, between frames
+            rs = F.RenderState()
+            F.render_expected_ranges(m1, poses[f], small, params, rs)
+            torch.cuda.synchronize()
+        p1.process(raw, poses[0] if f == 0 else None)
+        p2.process(raw, poses[0] if f == 0 else None)
+        s1, q1, i1 = p1.result()
+        s2, q2, i2 = p2.result()
+        assert np.array_equal(q1, q2) and np.array_equal(i1, i2) and s1 == s2, f"frame {f}"
+        for a, b in zip(p1.maps(), p2.maps()):
+            assert torch.equal(a.view(torch.int32), b.view(torch.int32)), f"frame {f}: maps differ"
+
+
+def test_limits_are_rejected_not_truncated():
+    """Configurations outside the B200 path's limits fail loudly (the
+    reference would run them): mu / voxelSize >= 80 (the 64-cell request-key
+    ordinal) and images of >= 2^25 pixels (the 25-bit pixel key)."""
+    from paper_1708_00783_b200 import fusion as F
+    m = F.VoxelBlockMap(F.VoxelBlockMapConfig(1 << 12, 1 << 10, 1 << 12))
+    intr = F.Intrinsics(160, 120, 131.25, 131.25, 79.5, 59.5)
+    with pytest.raises(Exception):
+        F.Pipeline(m, intr, F.SceneParams(voxelSize=0.001, mu=0.1))
+    with pytest.raises(Exception, match="25-bit"):
+        F.Pipeline(m, F.Intrinsics(8192, 4096, 4000.0, 4000.0, 4095.5, 2047.5), F.SceneParams())
+
+
+def test_icp_world_point_out_of_fixed_point_range_fails_loudly():
+    """The tracker's fixed-point sums hold world points within +-128 m; a
+    frame 200 m from the origin returns RFG_ERANGE instead of wrong sums."""
+    import icp_cases as K
+    from test_gpu_icp import _track_both  # noqa: F401  (same setup helpers)
+    from paper_1708_00783_b200 import fusion as F
+    from test_gpu_icp import _state_from_maps, _view
+    from helpers import INTR_C1
+    intr = F.Intrinsics(**INTR_C1)
+    gt = K.plane_pose()
+    raw = K.frames(F, 2, [gt], [0])[0]
+    lv = rfo.build_view(raw, INTR_C1, AFF, 3)
+    far = gt.copy()
+    far[0, 3] -= 200.0  # camera (and the wall it sees) 200 m along x
+    pts, nrm = K.zero_residual_maps(lv[0], INTR_C1, far, rfo.compute_normals(lv[0], INTR_C1))
+    rs = _state_from_maps(F, intr, pts, nrm, far)
+    m = F.VoxelBlockMap(F.VoxelBlockMapConfig(1 << 10, 1 << 8, 1 << 8))
+    with pytest.raises(Exception, match="fixed-point range"):
+        F.track_depth(m, _view(F, intr, raw), rs, far, iters=(6, 0, 0))
+    with pytest.raises(ValueError):
+        rfo.icp_track(lv, INTR_C1, pts, nrm, far, INTR_C1, far, (6, 0, 0), 10, K.DIST)
