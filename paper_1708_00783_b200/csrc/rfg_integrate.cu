@@ -62,6 +62,9 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 #ifndef RFG_INT_DIET
 #define RFG_INT_DIET 1
 #endif
+#ifndef RFG_INT_SKIP
+#define RFG_INT_SKIP 0  // warp-uniform skip of the update math of voxel slots no lane updates
+#endif
 #ifndef RFG_INT_TMA
 #define RFG_INT_TMA 0  // depth integration with TMA-prefetched voxel rows (k_integrate_depth_tma)
 #endif
@@ -169,6 +172,10 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
       const int oldW = vox_w(w0);
       const float eta = dm[k] - zc[k];
       const bool upd = pix[k] >= 0 && !(dm[k] <= 0.f) && !(eta < -mu) && !(capW && oldW >= maxW);
+#if RFG_INT_SKIP
+      // a voxel slot no lane of the warp updates skips the update math
+      if (!__any_sync(0xffffffffu, upd)) continue;
+#endif
 #if RFG_INT_DIET
       const float oldF = sdf_to_logical_alu(vox_sdf(w0));
       const float newF = smin(1.f, div_fast(eta, mu, rMu));
