@@ -63,7 +63,7 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 #define RFG_INT_DIET 1
 #endif
 #ifndef RFG_INT_SKIP
-#define RFG_INT_SKIP 0  // warp-uniform skip of the update math of voxel slots no lane updates
+#define RFG_INT_SKIP 1  // warp-uniform skip of the update math of voxel slots no lane updates
 #endif
 #ifndef RFG_INT_TMA
 #define RFG_INT_TMA 0  // depth integration with TMA-prefetched voxel rows (k_integrate_depth_tma)
@@ -609,6 +609,12 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
       const bool valid = pix[i] >= 0 && !(dm[i] <= 0.f);
       const float eta = dm[i] - zc[i];
       const bool upd = valid && !(eta < -mu) && !(capW && oldW >= maxW);
+      // fusion.cpp:257 on update_voxel_depth's return value (-1 when invalid);
+      // same camera: the colour pixel is the depth pixel, in the same margin
+      cin[i] = ((valid ? eta : -1.f) >= -mu) && pix[i] >= 0;
+#if RFG_INT_SKIP
+      if (!__any_sync(0xffffffffu, upd)) continue;  // no lane updates this voxel slot
+#endif
       const float oldF = sdf_to_logical(vox_sdf(w0));
       const float newF = smin(1.f, div_fast(eta, mu, rMu));
       const float fw = (float)oldW;
@@ -621,9 +627,6 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
       const bool slowK = upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << i)));
       wd[i] = (upd && !slowK) ? w1 : w0;
       redo |= slowK ? (1u << i) : 0u;
-      // fusion.cpp:257 on update_voxel_depth's return value (-1 when invalid);
-      // same camera: the colour pixel is the depth pixel, in the same margin
-      cin[i] = ((valid ? eta : -1.f) >= -mu) && pix[i] >= 0;
     }
     if (__any_sync(0xffffffffu, redo != 0u)) {
 #pragma unroll
@@ -642,6 +645,9 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
+#if RFG_INT_SKIP
+      if (!__any_sync(0xffffffffu, cin[i])) continue;  // no lane colours this voxel slot
+#endif
       const uint32_t c1 = colour_merge(cw[i], uu[i], vv[i], ca, maxW, tap[i][0], tap[i][1], tap[i][2], tap[i][3]);
       cw[i] = cin[i] ? c1 : cw[i];
     }
