@@ -488,6 +488,10 @@ def run_b200(args):
     if args.e2e_steps > 0:
         raw_pinned = torch.from_numpy(w.raws_host.view(np.int16)).pin_memory()
         rgb_pinned = torch.from_numpy(w.rgbs_host).pin_memory() if w.rgbs_host is not None else None
+        # the user's host frames: numpy views of the pinned buffers, made
+        # before the timed region (a caller holds its frames as arrays)
+        raw_views = [raw_pinned[f].numpy().view(np.uint16) for f in range(w.n)]
+        rgb_views = [rgb_pinned[f].numpy() for f in range(w.n)] if rgb_pinned is not None else None
         w.reset()
         e2e_total = 0.0
         n_e2e = min(args.e2e_steps, w.n)
@@ -496,11 +500,10 @@ def run_b200(args):
             flush.fill_(f & 0xFF)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            raw_h = raw_pinned[f].numpy().view(np.uint16)
-            if rgb_pinned is not None:
-                w.pipe.process(raw_h, w.pose_arg(f), rgb=rgb_pinned[f].numpy())
+            if rgb_views is not None:
+                w.pipe.process(raw_views[f], w.pose_arg(f), rgb=rgb_views[f])
             else:
-                w.pipe.process(raw_h, w.pose_arg(f))
+                w.pipe.process(raw_views[f], w.pose_arg(f))
             st, _, _ = w.pipe.result()  # D2H of stats + pose + ICP summary
             t1 = time.perf_counter()
             if f >= warm:

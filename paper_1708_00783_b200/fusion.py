@@ -811,6 +811,14 @@ class Pipeline:
         self._h = C.c_void_p()
         check(lib().rfg_pipeline_create(map.handle, C.byref(cfg), C.byref(self._h)))
         self._levels = levels
+        # per-frame call state, prepared once (the end-to-end path calls
+        # process / result every frame)
+        L = lib()
+        self._fn_host = L.rfg_pipeline_process_host
+        self._fn_rgbd_host = L.rfg_pipeline_process_rgbd_host
+        self._fn_result = L.rfg_pipeline_result
+        self._res = (_lib.AllocStats_(), np.zeros((3, 4), np.float32), np.zeros(ICP_STATS, np.float64))
+        self._res_args = (C.byref(self._res[0]), _fp(self._res[1]), self._res[2].ctypes.data_as(_d))
 
     def __del__(self):
         try:
@@ -837,14 +845,13 @@ class Pipeline:
             else:
                 a = np.ascontiguousarray(raw, np.uint16) if not torch.is_tensor(raw) else raw.numpy()
                 c = np.ascontiguousarray(rgb, np.uint8) if not torch.is_tensor(rgb) else rgb.numpy()
-                check(lib().rfg_pipeline_process_rgbd_host(self._h, a.ctypes.data_as(C.c_void_p),
-                                                           c.ctypes.data_as(C.c_void_p), p))
+                check(self._fn_rgbd_host(self._h, a.ctypes.data, c.ctypes.data, p))
             return
         if torch.is_tensor(raw) and raw.is_cuda:
             check(lib().rfg_pipeline_process_raw_stream(self._h, _ptr(raw), p, _stream_handle()))
         else:
             a = np.ascontiguousarray(raw, np.uint16) if not torch.is_tensor(raw) else raw.numpy()
-            check(lib().rfg_pipeline_process_host(self._h, a.ctypes.data_as(C.c_void_p), p))
+            check(self._fn_host(self._h, a.ctypes.data, p))
 
     def process_pgm(self, path: str, pose=None):
         """One frame straight from a PGM16 file (rfg_pipeline_process_pgm)."""
@@ -852,11 +859,12 @@ class Pipeline:
         check(lib().rfg_pipeline_process_pgm(self._h, path.encode(), p))
 
     def result(self):
-        st = _lib.AllocStats_()
-        pose = np.zeros((3, 4), np.float32)
-        icp = np.zeros(ICP_STATS, np.float64)
-        check(lib().rfg_pipeline_result(self._h, C.byref(st), _fp(pose), icp.ctypes.data_as(_d)))
-        return AllocationStats(st.requested, st.allocated, st.allocFailures, st.visibleCount), pose, icp
+        """(AllocationStats, world->camera pose (3, 4), tracker summary
+        (ICP_STATS,)) of the last frame; synchronises the pipeline."""
+        st, pose, icp = self._res
+        check(self._fn_result(self._h, self._res_args[0], self._res_args[1], self._res_args[2]))
+        return (AllocationStats(st.requested, st.allocated, st.allocFailures, st.visibleCount), pose.copy(),
+                icp.copy())
 
     def pose_buffer(self) -> int:
         """Device pointer of the current world->camera pose (12 floats)."""
