@@ -85,3 +85,38 @@ def test_swapping_colour_map():
             e.integrate(d, intr, poses[f], pd, rgb=col, intr_rgb=intr)
         assert g.swap_out() == o.swap_out()
         _same_state(g, o)
+
+
+def test_swapping_equivalence_on_the_gpu():
+    """SPEC.md:444-446 (the swapping engine's external anchor) on the B200
+    path itself: a GPU map fused with swapping enabled ends with the same
+    hash structure and, for every block, the same sdf / w_depth as a GPU map
+    fused without swapping (host-tier copy for blocks still swapped out);
+    allocated + free = capacity after every frame.  (Margin 0, as the oracle
+    test: kBoundary blocks are integrated only with swapping.)"""
+    intr, pd = small_intr(), _params()
+    frames = _frames(intr)
+    a, b = GpuEngine(*CFG), GpuEngine(*CFG)
+    for pose, d in frames:
+        a.allocate(d, intr, pose, pd)
+        a.integrate(d, intr, pose, pd)
+    b.set_fusion_options(True, 0.0)
+    b.swap_create(100000)
+    swapped = 0
+    for pose, d in frames:
+        b.allocate(d, intr, pose, pd)
+        swapped += b.swap_in()
+        b.integrate(d, intr, pose, pd)
+        swapped += b.swap_out()
+        ent = b.entries()
+        assert (ent[:, 4] >= 0).sum() + b.free_counts()[0] == CFG[2]
+    assert swapped > 100
+    ea, eb = a.entries(), b.entries()
+    assert np.array_equal(ea[:, :4], eb[:, :4])  # same hash structure
+    has, _ = b.swap_stored()
+    resident_a = np.nonzero(ea[:, 4] >= 0)[0]
+    assert has[resident_a].sum() > 0  # some blocks end the run on the host tier
+    want = a.blocks(ea[resident_a, 4])
+    for k, i in enumerate(resident_a):
+        got = b.blocks(np.array([eb[i, 4]]))[0] if eb[i, 4] >= 0 else b.swap_host_block(int(i))
+        assert np.array_equal(want[k][:, :3], got[:, :3]), i  # sdf + w_depth
