@@ -44,6 +44,7 @@ cudaError_t launch_downsample_intensity(const float* in, int w, int h, float* ou
 
 // rfg_icp.cu
 size_t icp_state_bytes();
+void icp_warmup();
 cudaError_t launch_icp_track(void* state, const float* depthLevels, int levels, const Intr& in0,
                              const float4* points, const float4* normals, const int* iters, const float* dist,
                              int minCount, const float* w2cInit, const float* renderPose, float* w2cOut,
@@ -991,6 +992,7 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
     return RFG_ECUDA;
   }
   m->stream = p->stream;
+  icp_warmup();
   if (ensure_range_scratch(m, cfg->intr.width, cfg->intr.height) != RFG_OK) {
     rfg_pipeline_destroy(p);
     return RFG_ENOMEM;

@@ -53,6 +53,9 @@ struct IcpState {
   int done[4];                    // per-level stop flags (single evaluations)
   unsigned gen;                   // iterations so far: rotates the accumulators
   int error;                      // sticky: a world point outside the fixed-point range
+  // hand-off of the coarse level (k_icp_coarse) to k_icp_track
+  double c2wInit[12];
+  int failed;
   // phase timers of CTA 0 (ns, %globaltimer), accumulated over iterations:
   // {associate+reduce, grid barrier, read totals, solve, iterations,
   //  level-0 total, level-1 total, level-2 total}
@@ -634,7 +637,113 @@ struct IcpTrackArgs {
   const float* renderPose;
   float* w2cOut;
   float* renderPoseOut;  // nullable: the next frame's render pose := the output pose
+  int fromState;         // 1: continue the track k_icp_coarse left in the state (its level skipped here)
 };
+
+// The track's seed: inverse of the float init pose, widened to double (as
+// the oracle).
+__device__ __forceinline__ void icp_seed(const IcpTrackArgs& ta, GnShared& g) {
+  const Pose q = pose_inverse(pose_from12(ta.w2cInit));
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) g.c2w[r * 4 + c] = (double)q.R[r * 3 + c];
+    g.c2w[r * 4 + 3] = (double)q.t[r];
+  }
+  for (int i = 0; i < 12; ++i) g.c2wInit[i] = g.c2w[i];
+  c2w_to_float(g.c2w, g.c2wF);
+  for (int i = 0; i < kIcpStats; ++i) g.stats[i] = 0.0;
+  g.stats[7] = 1.0;
+  for (int k = 0; k < kIcpSums; ++k) {
+    g.sums[k] = 0.0;
+    g.fixed[k] = 0;
+  }
+  g.failed = 0;
+}
+// The track as k_icp_coarse left it.
+__device__ __forceinline__ void icp_seed_from_state(IcpState* st, GnShared& g) {
+  for (int i = 0; i < 12; ++i) {
+    g.c2w[i] = __ldcg(&st->c2w[i]);
+    g.c2wInit[i] = __ldcg(&st->c2wInit[i]);
+    g.c2wF[i] = __ldcg(&st->c2wF[i]);
+  }
+  for (int i = 0; i < kIcpStats; ++i) g.stats[i] = __ldcg(&st->stats[i]);
+  for (int k = 0; k < kIcpSums; ++k) {
+    g.sums[k] = __ldcg(&st->sums[k]);
+    g.fixed[k] = __ldcg(&st->fixed[k]);
+  }
+  g.failed = __ldcg(&st->failed);
+}
+
+// The coarsest level on ONE thread-block cluster (kIcpCluster CTAs, one per
+// SM of a GPC): the CTAs add their partial sums into CTA rank 0's shared
+// memory over DSMEM (64-bit atomics: integer sums, order-free), a cluster
+// barrier (~0.25 us) replaces the grid barrier (~1.2 us), and every CTA reads
+// the totals from rank 0's shared memory.  The coarse level has few pixels
+// (19,200 at 640x480), so 16 SMs hold it; its iterations are the most
+// numerous of the track.  k_icp_track then continues from the state.
+constexpr int kIcpCluster = 16;
+__global__ void __launch_bounds__(kIcpThreads, 1) k_icp_coarse(IcpState* st, IcpTrackArgs ta) {
+  __shared__ long long sh[kIcpThreads / 32][32];
+  __shared__ GnShared g;
+  __shared__ float4 pcs[kIcpPx * kIcpThreads];
+  __shared__ unsigned long long cacc[3][32];  // rank 0's are the cluster's accumulators
+  cg::cluster_group cl = cg::this_cluster();
+  const int l = ta.levels - 1;
+  const IcpLevelArgs& a = ta.lv[l];
+  if (threadIdx.x < 96) (&cacc[0][0])[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) {
+    icp_seed(ta, g);
+    for (int i = 0; i < 12; ++i) g.rp[i] = ta.renderPose[i];
+    g.done = 0;
+  }
+  cl.sync();  // zeroed accumulators before any CTA adds into rank 0's
+  const Intr inl{a.lw, a.lh, a.fx, a.fy, a.cx, a.cy};
+  const float dist2 = a.dist * a.dist;
+  const int n = a.lw * a.lh;
+  const Pose rp = pose_from12(g.rp);
+  const int nCta = (int)gridDim.x;
+  const bool rank0 = cl.block_rank() == 0;
+  const bool timed = rank0 && threadIdx.x == 0;
+  unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool ok = true;
+  for (int it = 0; it < a.iters && !g.done; ++it) {
+    unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    if (timed) t0 = gtimer();
+    unsigned long long* dst = cl.map_shared_rank(&cacc[it % 3][0], 0);
+    ok &= icp_cta_eval(a, g, rp, inl, dist2, n, nCta, sh, pcs, it == 0, dst);
+    if (rank0 && threadIdx.x < 32) cacc[(it + 1) % 3][threadIdx.x] = 0ull;  // read by no CTA since it - 2
+    if (timed) t1 = gtimer();
+    cl.sync();
+    if (timed) t2 = gtimer();
+    if (threadIdx.x < kIcpSums) {
+      const long long v = (long long)dst[threadIdx.x];
+      g.fixed[threadIdx.x] = v;
+      g.sums[threadIdx.x] = ldexp((double)v, -icp_shift(threadIdx.x));
+    }
+    __syncthreads();
+    if (timed) t3 = gtimer();
+    if (threadIdx.x == 0)
+      gn_step(g, a.level, a.minCount);
+    else if (threadIdx.x == 32)
+      icp_summary(g);
+    __syncthreads();
+    if (timed) {
+      const unsigned long long t4 = gtimer();
+      tacc[0] += t1 - t0;
+      tacc[1] += t2 - t1;
+      tacc[2] += t3 - t2;
+      tacc[3] += t4 - t3;
+      tacc[4] += 1;
+      tacc[5 + (a.level < 3 ? a.level : 0)] += t4 - t0;
+    }
+  }
+  if (!ok) st->error = 1;
+  if (timed) {
+    icp_publish(st, g, tacc, __ldcg(&st->gen), 0);  // the global accumulators were not used
+    for (int i = 0; i < 12; ++i) st->c2wInit[i] = g.c2wInit[i];
+    st->failed = g.failed;
+  }
+  cl.sync();  // rank 0's shared memory stays alive until every CTA has read it
+}
 
 __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpTrackArgs ta) {
   __shared__ long long sh[kIcpThreads / 32][32];
@@ -645,22 +754,12 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpT
 #endif
   const unsigned gen = __ldcg(&st->gen);
   if (threadIdx.x == 0) {
-    // inverse of the float pose, widened to double (as the oracle)
-    const Pose q = pose_inverse(pose_from12(ta.w2cInit));
-    for (int r = 0; r < 3; ++r) {
-      for (int c = 0; c < 3; ++c) g.c2w[r * 4 + c] = (double)q.R[r * 3 + c];
-      g.c2w[r * 4 + 3] = (double)q.t[r];
+    if (ta.fromState) {
+      icp_seed_from_state(st, g);
+    } else {
+      icp_seed(ta, g);
     }
-    for (int i = 0; i < 12; ++i) g.c2wInit[i] = g.c2w[i];
-    c2w_to_float(g.c2w, g.c2wF);
     for (int i = 0; i < 12; ++i) g.rp[i] = ta.renderPose[i];
-    for (int i = 0; i < kIcpStats; ++i) g.stats[i] = 0.0;
-    g.stats[7] = 1.0;
-    for (int k = 0; k < kIcpSums; ++k) {
-      g.sums[k] = 0.0;
-      g.fixed[k] = 0;
-    }
-    g.failed = 0;
   }
   __syncthreads();
   int gi = 0;
@@ -733,6 +832,38 @@ static int icp_grid(int n) {
 
 size_t icp_state_bytes() { return sizeof(IcpState); }
 
+#ifndef RFG_ICP_COARSE_CLUSTER
+#define RFG_ICP_COARSE_CLUSTER 0  // 1: the coarsest level on one 16-CTA cluster (k_icp_coarse; measured slower)
+#endif
+// Whether a 16-CTA cluster of k_icp_coarse fits this device (one GPC with 16
+// free SMs); cached per device.
+static bool coarse_cluster_ok() {
+  static int ok[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = dev < 64 ? ok[dev] : 0;
+  if (!v) {
+    v = -1;
+    if (cudaFuncSetAttribute(k_icp_coarse, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kIcpCluster);
+      cfg.blockDim = dim3(kIcpThreads);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kIcpCluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, k_icp_coarse, &cfg) == cudaSuccess && n >= 1) v = 1;
+    }
+    cudaGetLastError();
+    if (dev < 64) ok[dev] = v;
+  }
+  return v > 0;
+}
+
 static IcpLevelArgs level_args(const float* depthLevels, int level, const Intr& in0, const float4* points,
                                const float4* normals) {
   IcpLevelArgs a{};
@@ -783,6 +914,29 @@ cudaError_t launch_icp_track(void* state, const float* depthLevels, int levels, 
     if (iters[l] > 0 && ta.nCta[l] > grid) grid = ta.nCta[l];
   }
   IcpState* stp = st;
+  const int lc = levels - 1;
+  if (RFG_ICP_COARSE_CLUSTER && levels >= 2 && iters[lc] > 0 && coarse_cluster_ok()) {
+    // the coarsest level on one cluster, then the rest of the track
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kIcpCluster);
+    cfg.blockDim = dim3(kIcpThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kIcpCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    count_launch();
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_icp_coarse, stp, ta);
+    if (e != cudaSuccess) return e;
+    ta.fromState = 1;
+    ta.lv[lc].iters = 0;
+    grid = 1;
+    for (int l = 0; l < lc; ++l)
+      if (iters[l] > 0 && ta.nCta[l] > grid) grid = ta.nCta[l];
+  }
   void* args[] = {&stp, &ta};
   count_launch();
   return cudaLaunchCooperativeKernel((const void*)k_icp_track, dim3(grid), dim3(kIcpThreads), args, 0, s);
@@ -823,6 +977,12 @@ cudaError_t launch_icp_reduce_once(void* state, const float* depth, int lw, int 
   void* args[] = {&stp, &a};
   count_launch();
   return cudaLaunchCooperativeKernel((const void*)k_icp_level, dim3(grid), dim3(kIcpThreads), args, 0, s);
+}
+
+// Device queries the launches need, made outside any stream capture.
+void icp_warmup() {
+  coarse_cluster_ok();
+  icp_grid(1);
 }
 
 unsigned long long* icp_timers_ptr(void* state) { return static_cast<IcpState*>(state)->timers; }
