@@ -8,8 +8,8 @@ the work's stream around each frame; frames W..N-1 timed.
       the frame graph with the ground-truth pose per frame
   C2  C1 + the ICP tracker (3-level pyramid)                 (= bench.py)
   C3  ITMVoxel_s_rgb colour fusion, 640x480 depth + RGB, 4 mm voxels,
-      known poses: build_view + allocate + integrate (depth + colour) +
-      expected ranges + ICP-map raycast through the map-level calls
+      known poses: the colour frame pipeline (view, RGB pack, allocate,
+      RGB-D integrate, expected ranges, ICP-map raycast)
   C4  builder-defined multi-room scene, 2 mm voxels, 2^21 buckets, 2^22
       blocks (8 GiB depth plane), known poses: the frame graph
 
@@ -102,28 +102,26 @@ out["C1"] = {"ms": ms, "fps": 1e3 / ms, "visible_last": st.visibleCount}
 ms, st, _ = pipeline_config(0, poses, (0x40000, 0x20000, 0x40000), p5, track=True)
 out["C2"] = {"ms": ms, "fps": 1e3 / ms, "visible_last": st.visibleCount}
 
-# C3: colour fusion through the map-level calls
+# C3: colour fusion through the colour frame pipeline (graph: view, RGB
+# pack, allocate, RGB-D integrate, ranges, raycast), 300-frame orbit at 4 mm
 p4 = F.SceneParams(voxelSize=0.004, mu=0.02)
-frames = [F.synth_render(0, poses[f % 100], INTR, rgb=True) for f in range(args.frames)]
-raws = [torch.from_numpy(r.view(np.int16)).cuda() for r, _, _ in frames]
-rgbs = [torch.from_numpy(c).cuda() for _, _, c in frames]
-calib = F.RgbdCalib(intrinsics_rgb=INTR, intrinsics_d=INTR, depth_affine=F.DepthAffine(1.0 / 5000.0, 0.0))
+poses3 = F.orbit_trajectory(frames=300)
+n3 = min(300, args.frames)
+frames = [F.synth_render(0, poses3[f], INTR, rgb=True) for f in range(n3)]
+raws = torch.from_numpy(np.stack([r for r, _, _ in frames]).view(np.int16)).cuda()
+rgbs = torch.from_numpy(np.stack([c for _, _, c in frames])).cuda()
 mc = F.VoxelBlockMap(F.VoxelBlockMapConfig(0x40000, 0x20000, 0x40000), colour=True)
-eng = F.FusionEngine()
-rs = F.RenderState()
-sc = torch.cuda.current_stream()  # the map-level calls run on torch's current stream (bind_stream)
+pc = F.Pipeline(mc, INTR, p4, track=False, colour=True)
+sc = torch.cuda.ExternalStream(pc.stream)
 
 
 def c3(f):
-    view = F.build_view(raws[f], rgbs[f], calib, levels=1)
-    eng.allocate_from_depth(mc, view, poses[f % 100], p4, sync=False)
-    eng.integrate_frame(mc, view, poses[f % 100], p4)
-    F.render_expected_ranges(mc, poses[f % 100], INTR, p4, rs)
-    F.render_maps(mc, poses[f % 100], INTR, p4, F.RenderMode.kIcpMaps, rs)
+    pc.process(raws[f], poses3[f], rgb=rgbs[f])
 
 
-ms = timed(c3, sc, args.frames)
-out["C3"] = {"ms": ms, "fps": 1e3 / ms, "path": "map-level calls (no frame graph)"}
+ms = timed(c3, sc, n3)
+out["C3"] = {"ms": ms, "fps": 1e3 / ms, "path": "colour frame pipeline (CUDA graph)",
+             "visible_last": pc.result()[0].visibleCount}
 
 # C4: multi-room, 2 mm, full capacity
 mr = F.multiroom_trajectory(100)
