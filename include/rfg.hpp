@@ -288,11 +288,40 @@ class SwappingEngine {
   rfg_swap* s_ = nullptr;
 };
 
-// ITMMainEngine::ProcessFrame-style driver (absent in the reference).
+// TrackerIterationSummary of a track's last evaluation,
+// plus the run's outcome (rfg_icp_track's RFG_ICP_* values).
+struct TrackerIterationSummary {
+  int iterations = 0, inliers = 0;
+  double residualSum = 0.0;
+  bool converged = false, ok = false;
+  int perLevel[3] = {0, 0, 0};
+  double inlierFraction = 0.0, hessianDet = 0.0, residualMean = 0.0;
+  int validPixels = 0;
+  static TrackerIterationSummary from(const double* st) {
+    TrackerIterationSummary t;
+    t.iterations = (int)st[RFG_ICP_ITERATIONS];
+    t.inliers = (int)st[RFG_ICP_COUNT];
+    t.residualSum = st[RFG_ICP_RESIDUAL_SUM];
+    t.converged = st[RFG_ICP_CONVERGED] != 0.0;
+    for (int l = 0; l < 3; ++l) t.perLevel[l] = (int)st[RFG_ICP_IT_L0 + l];
+    t.ok = st[RFG_ICP_OK] != 0.0;
+    t.inlierFraction = st[RFG_ICP_INLIER_FRACTION];
+    t.hessianDet = st[RFG_ICP_HESSIAN_DET];
+    t.residualMean = st[RFG_ICP_RESIDUAL_MEAN];
+    t.validPixels = (int)st[RFG_ICP_VALID];
+    return t;
+  }
+};
+
+// ITMMainEngine::ProcessFrame-style driver (absent in the reference).  With
+// colour = true the map needs a colour plane and frames come with RGB8
+// images (processRgbdHost); intrRgb / extrinsics default to the depth
+// camera / identity.
 class Pipeline {
  public:
   Pipeline(VoxelBlockMap& map, const Intrinsics& intr, const SceneParams& params, float affScale, float affOffset,
-           int levels = 3, bool track = true) {
+           int levels = 3, bool track = true, bool colour = false, const Intrinsics* intrRgb = nullptr,
+           const Pose34* extrDToRgb = nullptr) {
     rfg_pipeline_config c{};
     c.intr = intr.c();
     c.params = params.c();
@@ -308,6 +337,11 @@ class Pipeline {
     c.dist[2] = 0.04f;
     c.min_count = 10;
     c.use_graph = 1;
+    c.colour = colour ? 1 : 0;
+    if (colour) {
+      c.intr_rgb = (intrRgb ? *intrRgb : intr).c();
+      for (int i = 0; i < 12; ++i) c.extr_d_to_rgb[i] = extrDToRgb ? (*extrDToRgb)[i] : ((i % 5 == 0) ? 1.f : 0.f);
+    }
     check(rfg_pipeline_create(map.handle(), &c, &p_));
   }
   ~Pipeline() { rfg_pipeline_destroy(p_); }
@@ -321,10 +355,16 @@ class Pipeline {
   void processPgm(const std::string& path, const Pose34* pose = nullptr) {
     check(rfg_pipeline_process_pgm(p_, path.c_str(), pose ? pose->data() : nullptr));
   }
-  AllocationStats result(Pose34* poseOut = nullptr) {
+  // one RGB-D frame of a colour pipeline (RGB8, intrRgb's size)
+  void processRgbdHost(const std::uint16_t* rawHost, const std::uint8_t* rgbHost, const Pose34* pose = nullptr) {
+    check(rfg_pipeline_process_rgbd_host(p_, rawHost, rgbHost, pose ? pose->data() : nullptr));
+  }
+  AllocationStats result(Pose34* poseOut = nullptr, TrackerIterationSummary* tracker = nullptr) {
     rfg_alloc_stats s{};
     Pose34 tmp;
-    check(rfg_pipeline_result(p_, &s, poseOut ? poseOut->data() : tmp.data(), nullptr));
+    double st[RFG_ICP_STATS] = {};
+    check(rfg_pipeline_result(p_, &s, poseOut ? poseOut->data() : tmp.data(), st));
+    if (tracker) *tracker = TrackerIterationSummary::from(st);
     return {s.requested, s.allocated, s.allocFailures, s.visibleCount};
   }
 

@@ -2,6 +2,8 @@
 // reference's own doctest cases.  Without a GPU it checks the error contract
 // and exits 0; with one it fuses a short synthetic sequence through the
 // public pipeline and checks the reference's frame-0 statistics.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -73,6 +75,38 @@ int main() {
     map.releaseBlock(idx);
     CHECK(map.entries()[idx].ptr == -1 && map.allocatedBlockCount() == 8348);
     CHECK(map.reserveBlockForEntry(idx) && map.entries()[idx].inMemory());
+    // the tracked pipeline (C2): frame 0 at its pose, then tracking; the
+    // summary of the last evaluation
+    {
+      rfg::VoxelBlockMap tmap({0x40000, 0x20000, 0x40000});
+      rfg::Pipeline tp(tmap, intr, params, 1.f / 5000.f, 0.f, 3, /*track=*/true);
+      rfg::TrackerIterationSummary ts;
+      for (int f = 0; f < 4; ++f) {
+        rfg_synth_render(0, poses[f].data(), &ci, 1.f / 5000.f, 0.f, 0, raw.data(), depth.data(), nullptr);
+        tp.processHost(raw.data(), f == 0 ? &poses[0] : nullptr);
+        rfg::Pose34 pose;
+        tp.result(&pose, &ts);
+        if (f > 0) {
+          CHECK(ts.ok && ts.iterations > 0 && ts.inlierFraction > 0.5 && ts.inlierFraction <= 1.0);
+          CHECK(ts.hessianDet > 1e-12);
+          float err = 0.f;
+          for (int r = 0; r < 3; ++r) err = std::max(err, std::abs(pose[r * 4 + 3] - poses[f][r * 4 + 3]));
+          CHECK(err < 2e-3f);  // tracks the synthetic orbit
+        }
+      }
+    }
+    // colour fusion (C3): a colour map, RGB-D frames
+    {
+      rfg::VoxelBlockMap cmap({0x40000, 0x20000, 0x40000}, /*colour=*/true);
+      rfg::SceneParams p4;
+      p4.voxelSize = 0.004f;
+      rfg::Pipeline cp(cmap, intr, p4, 1.f / 5000.f, 0.f, 1, /*track=*/false, /*colour=*/true);
+      std::vector<std::uint8_t> rgb(640 * 480 * 3);
+      rfg_synth_render(0, poses[0].data(), &ci, 1.f / 5000.f, 0.f, 1, raw.data(), depth.data(), rgb.data());
+      cp.processRgbdHost(raw.data(), rgb.data(), &poses[0]);
+      const rfg::AllocationStats cs = cp.result();
+      CHECK(cs.allocated > 10000 && cs.allocFailures == 0);
+    }
     std::printf("adapter_test: GPU sequence ok\n");
   } catch (const rfg::Error& e) {
     CHECK(e.code() == RFG_ECUDA);  // no device: fail loudly, no CPU fallback
