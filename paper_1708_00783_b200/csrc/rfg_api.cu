@@ -165,13 +165,18 @@ int ensure_range_scratch(rfg_map* m, int width, int height) {
   if (d.binCount) cudaFree(d.binCount);
   d.bins = nullptr;
   d.binCount = nullptr;
+  d.tileCost = nullptr;
+  d.tileOrder = nullptr;
   if (cudaMalloc(&d.bins, (size_t)tx * ty * kBinCap * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&d.binCount, (size_t)tx * ty * sizeof(int)) != cudaSuccess) {
+      cudaMalloc(&d.binCount, (size_t)tx * ty * 3 * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     set_error("range scratch allocation failed");
     return RFG_ENOMEM;
   }
-  RFG_CK(cudaMemset(d.binCount, 0, (size_t)tx * ty * sizeof(int)));
+  // [binCount | tileCost | tileOrder], tx * ty each
+  RFG_CK(cudaMemset(d.binCount, 0, (size_t)tx * ty * 3 * sizeof(int)));
+  d.tileCost = d.binCount + (size_t)tx * ty;
+  d.tileOrder = d.binCount + (size_t)tx * ty * 2;
   d.binTilesX = tx;
   d.binTilesY = ty;
   d.binCap = kBinCap;

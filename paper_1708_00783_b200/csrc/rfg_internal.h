@@ -47,6 +47,8 @@ struct DevMap {
   int4* rangeBounds;       // per visible block: packed pixel rectangle + z span
   int* binCount;           // per 32x32 screen tile
   int* bins;               // binTilesX * binTilesY * binCap block indices
+  int* tileCost;           // per tile: the last raycast's longest march (steps), for the next frame's order
+  int* tileOrder;          // per tile: the raycast's CTA -> tile order (heaviest tiles first)
   int binTilesX, binTilesY, binCap;
   unsigned binGen;         // bumped whenever the range scratch is reallocated (captured graphs re-capture)
 };

@@ -7,6 +7,12 @@
 #ifndef RFG_RC_ALU
 #define RFG_RC_ALU 1  // the march's conversions on the FMA/ALU pipes (0: XU conversions)
 #endif
+#ifndef RFG_RC_ORDER
+#define RFG_RC_ORDER 1  // the frame pipeline's raycast CTAs take the previous frame's heaviest tiles first
+#endif
+#ifndef RFG_RC_ORDER_K
+#define RFG_RC_ORDER_K 2  // ... that many tiles per SM
+#endif
 
 namespace rfg {
 
@@ -31,11 +37,89 @@ __device__ __forceinline__ int4 pack_bounds(int x0, int y0, int x1, int y1, floa
   return make_int4(x0 | (y0 << 16), x1 | (y1 << 16), __float_as_int(lo), __float_as_int(hi));
 }
 
-__global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa) {
+// The raycast's tile order for this frame (one extra CTA of the pipeline's
+// k_range_bin launch, 256 threads): the tiles whose longest march in the
+// previous frame (tileCost, steps) is among the K longest come first, the
+// rest follow, each group in raster order; the costs are re-zeroed for this
+// frame's raycast.  Only the schedule changes — every pixel's march is the
+// same whichever CTA runs it.
+__device__ void order_tiles(const DevMap& m, int n, int K) {
+  __shared__ int hist[256];
+  __shared__ int warpHeavy[8], warpLight[8];
+  __shared__ int sT, sH;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  hist[tid] = 0;
+  if (tid == 0) {
+    sT = 1;
+    sH = 0;
+  }
+  __syncthreads();
+  for (int t = tid; t < n; t += 256) atomicAdd(&hist[min(m.tileCost[t], 255)], 1);
+  __syncthreads();
+  // acc = number of tiles with cost >= b for b = 255 - tid (b >= 1): an
+  // inclusive scan over the bins in descending order; T = the largest b with
+  // acc >= K (1 when fewer than K tiles have a cost)
+  int acc = tid < 255 ? hist[255 - tid] : 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, acc, o);
+    if (lane >= o) acc += v;
+  }
+  if (lane == 31) warpHeavy[wid] = acc;
+  __syncthreads();
+  for (int w = 0; w < wid; ++w) acc += warpHeavy[w];
+  const bool reach = tid < 255 && acc >= K;
+  const bool first = reach && (tid == 0 || !(acc - (tid < 255 ? hist[255 - tid] : 0) >= K));
+  if (first) {
+    sT = 255 - tid;
+    sH = acc;
+  }
+  if (tid == 254 && acc < K) sH = acc;  // fewer than K tiles with a cost: all of them first (T = 1)
+  __syncthreads();
+  const int T = sT, H = sH;
+  int hBase = 0, lBase = H;
+  for (int base = 0; base < n; base += 256) {
+    const int t = base + tid;
+    const bool in = t < n;
+    const int c = in ? m.tileCost[t] : 0;
+    const bool heavy = in && min(c, 255) >= T && c > 0;
+    const bool light = in && !heavy;
+    const unsigned bh = __ballot_sync(0xffffffffu, heavy), bl = __ballot_sync(0xffffffffu, light);
+    if (lane == 0) {
+      warpHeavy[wid] = __popc(bh);
+      warpLight[wid] = __popc(bl);
+    }
+    __syncthreads();
+    int ph = 0, pl = 0, th = 0, tl = 0;
+    for (int w = 0; w < 8; ++w) {
+      if (w < wid) {
+        ph += warpHeavy[w];
+        pl += warpLight[w];
+      }
+      th += warpHeavy[w];
+      tl += warpLight[w];
+    }
+    const unsigned below = (1u << lane) - 1u;
+    if (heavy) m.tileOrder[hBase + ph + __popc(bh & below)] = t;
+    if (light) m.tileOrder[lBase + pl + __popc(bl & below)] = t;
+    if (in) m.tileCost[t] = 0;
+    hBase += th;
+    lBase += tl;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa, int orderK) {
+  // orderK > 0: CTA 0 (dispatched first) writes the raycast's tile order
+  if (orderK > 0 && blockIdx.x == 0) {
+    order_tiles(m, m.binTilesX * ((fa.h + kRangeTile - 1) / kRangeTile), orderK);
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int warpsPerCta = blockDim.x >> 5;
-  const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
-  const int nw = gridDim.x * warpsPerCta;
+  const int cta = blockIdx.x - (orderK > 0 ? 1 : 0);
+  const int gw = cta * warpsPerCta + (threadIdx.x >> 5);
+  const int nw = (gridDim.x - (orderK > 0 ? 1 : 0)) * warpsPerCta;
   const int nVis = *((volatile int*)&m.state->nVisible);
   const Pose pose = frame_pose(fa);
   const float bs = fa.voxelSize * (float)kBlock;
@@ -108,7 +192,7 @@ __global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa) {
 // The expected range (min, max bits) of this thread's pixel of screen tile t
 // (blockIdx), from the tile's bin; every thread of the CTA must call it (it
 // synchronises the CTA), and it re-zeroes the bin count for the next frame.
-__device__ __forceinline__ int2 tile_ranges(const DevMap& m, int t, int4* sb) {
+__device__ __forceinline__ int2 tile_ranges(const DevMap& m, int t, int tileX, int tileY, int4* sb) {
   const int count = m.binCount[t];
   const bool overflow = count > m.binCap;
   const int n = overflow ? *((volatile int*)&m.state->nVisible) : count;
@@ -121,7 +205,7 @@ __device__ __forceinline__ int2 tile_ranges(const DevMap& m, int t, int4* sb) {
       // 0-15) and a row mask (bits 16-31): pixel (lx, ly) of the tile is
       // covered iff both of its bits are set (0 for an empty clip)
       const int4 bb = m.rangeBounds[overflow ? i : m.bins[(size_t)t * m.binCap + i]];
-      const int tx = blockIdx.x * kRangeTile, ty = blockIdx.y * kRangeTile;
+      const int tx = tileX * kRangeTile, ty = tileY * kRangeTile;
       const int lx0 = max((bb.x & 0xFFFF) - tx, 0), lx1 = min((bb.y & 0xFFFF) - tx, kRangeTile - 1);
       const int ly0 = max((bb.x >> 16) - ty, 0), ly1 = min((bb.y >> 16) - ty, kRangeTile - 1);
       uint32_t mask = 0u;
@@ -150,12 +234,16 @@ __global__ void __launch_bounds__(kRangeTile* kRangeTile) k_range_tile(DevMap m,
   const int t = blockIdx.y * m.binTilesX + blockIdx.x;
   const int x = blockIdx.x * kRangeTile + (threadIdx.x & (kRangeTile - 1));
   const int y = blockIdx.y * kRangeTile + threadIdx.x / kRangeTile;
-  const int2 lh = tile_ranges(m, t, sb);
+  const int2 lh = tile_ranges(m, t, blockIdx.x, blockIdx.y, sb);
   if (x < fa.w && y < fa.h) range[(size_t)y * fa.w + x] = make_float2(__int_as_float(lh.x), __int_as_float(lh.y));
 }
 
 #if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
 __device__ unsigned long long g_rc_stats[32];
+#endif
+#if defined(RFG_RC_TIMING)
+constexpr int kRcWarps = 1 << 14;
+__device__ unsigned long long g_rc_warp[kRcWarps][16];
 #endif
 #ifdef RFG_RC_STATS
 // debug build only: march statistics {rays, steps, coarse, invalid-fine,
@@ -182,15 +270,27 @@ struct FieldReader {
   const FieldVoxel* vba;
   uint32_t buckets;
   BlockCache cache;
+  int nSteps = 0;  // march steps of this ray (the pipeline's tile costs)
+#ifdef RFG_RC_TIMING
+  // debug build: what one ray did (hash lookups, entry loads of the chain
+  // walks, nearest voxel loads, trilinear reads)
+  int nLook = 0, nChain = 0, nNear = 0, nTri = 0;
+  unsigned long long tseg[5] = {0, 0, 0, 0, 0};  // %globaltimer at steps 0, 16, 32, 48, 64
+#define RC_CNT(f) (++(f))
+#else
+#define RC_CNT(f)
+#endif
 
   // findEntry + ptr (voxel_block_map.cpp:26-34,63-72), uncached
   __device__ __forceinline__ int lookup(int bx, int by, int bz) const {
     RC_STAT(6, 1);
+    RC_CNT(const_cast<FieldReader*>(this)->nLook);
     int ptr = -1;
     if (bx >= -32768 && bx <= 32767 && by >= -32768 && by <= 32767 && bz >= -32768 && bz <= 32767) {
       int idx = (int)hash_index(bx, by, bz, buckets - 1);
       const int xy = (int)((uint32_t)(uint16_t)bx | ((uint32_t)(uint16_t)by << 16));
       for (;;) {
+        RC_CNT(const_cast<FieldReader*>(this)->nChain);
         const int4 e = __ldg(entries + idx);
         if (e.w >= -1 && e.x == xy && e.y == bz) {
           ptr = e.w;
@@ -226,6 +326,7 @@ struct FieldReader {
     const int ptr = ptr_of(vx >> 3, vy >> 3, vz >> 3);
     ok = ptr >= 0;
     if (!ok) return 1.f;
+    RC_CNT(nNear);
     const FieldVoxel w = __ldg(vba + (size_t)ptr * kBlock3 + ((vx & 7) | ((vy & 7) << 3) | ((vz & 7) << 6)));
 #if RFG_RC_ALU
     return sdf_to_logical_alu(field_sdf(w));
@@ -242,6 +343,7 @@ struct FieldReader {
   // independently.
   __device__ __forceinline__ float trilinear(f3 p, bool& ok) {
     RC_STAT(5, 1);
+    RC_CNT(nTri);
     const int bx = (int)floorf(p.x), by = (int)floorf(p.y), bz = (int)floorf(p.z);
     const float fx = p.x - (float)bx, fy = p.y - (float)by, fz = p.z - (float)bz;
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
@@ -321,6 +423,11 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
   } fin{nSteps, nCoarse, nInv, nNear, nVs};
 #endif
   while (t <= tMaxM) {
+#ifdef RFG_RC_TIMING
+    if ((field.nSteps & 15) == 0 && field.nSteps < 80)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(field.tseg[field.nSteps >> 4]));
+#endif
+    ++field.nSteps;
 #ifdef RFG_RC_STATS
     ++nSteps;
 #endif
@@ -494,7 +601,8 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_icp(DevMap m, Fram
 // other SMs still march their long rays (the separate normals kernel could
 // only start after the longest ray of the whole image).
 __device__ __forceinline__ void raycast_and_normal(const DevMap& m, const FrameArgs& fa, int x, int y, float2 r,
-                                                   float4* raycast, float4* points, float4* normals) {
+                                                   float4* raycast, float4* points, float4* normals,
+                                                   unsigned long long* ctr = nullptr, int* stepsOut = nullptr) {
   const size_t i = (size_t)y * fa.w + x;
   const float4 invalid = make_float4(0.f, 0.f, 0.f, -1.f);
   float4 rc = invalid, pt = invalid, nm = invalid;
@@ -522,6 +630,19 @@ __device__ __forceinline__ void raycast_and_normal(const DevMap& m, const FrameA
     if (field_normal(field, hit, &n)) nm = make_float4(n.x, n.y, n.z, 1.f);
   }
   normals[i] = nm;
+  if (stepsOut) *stepsOut = field.nSteps;
+#ifdef RFG_RC_TIMING
+  if (ctr) {
+    ctr[0] = field.nSteps;
+    ctr[1] = field.nLook;
+    ctr[2] = field.nChain;
+    ctr[3] = field.nNear;
+    ctr[4] = field.nTri;
+    for (int k = 0; k < 5; ++k) ctr[5 + k] = field.tseg[k];
+  }
+#else
+  (void)ctr;
+#endif
 }
 
 __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_maps(DevMap m, FrameArgs fa,
@@ -543,16 +664,61 @@ __global__ void __launch_bounds__(128, RFG_RC_MINB) k_raycast_maps(DevMap m, Fra
 #endif
 __global__ void __launch_bounds__(kRangeTile* kRangeTile, RFG_RC_TILES_MINB) k_raycast_tiles(DevMap m, FrameArgs fa, float2* range,
                                                                           float4* raycast, float4* points,
-                                                                          float4* normals) {
+                                                                          float4* normals, int ordered) {
   __shared__ int4 sb[kRangeTile * kRangeTile];
-  const int t = blockIdx.y * m.binTilesX + blockIdx.x;
-  const int x = blockIdx.x * kRangeTile + (threadIdx.x & (kRangeTile - 1));
-  const int y = blockIdx.y * kRangeTile + threadIdx.x / kRangeTile;
-  const int2 lh = tile_ranges(m, t, sb);
+  // ordered: a 1-D grid over the tiles in this frame's order (order_tiles)
+  const int t = ordered ? m.tileOrder[blockIdx.x] : blockIdx.y * m.binTilesX + blockIdx.x;
+  const int tileX = ordered ? t % m.binTilesX : blockIdx.x, tileY = ordered ? t / m.binTilesX : blockIdx.y;
+  const int x = tileX * kRangeTile + (threadIdx.x & (kRangeTile - 1));
+  const int y = tileY * kRangeTile + threadIdx.x / kRangeTile;
+#if defined(RFG_RC_TIMING)
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
+  const int2 lh = tile_ranges(m, t, tileX, tileY, sb);
   if (x >= fa.w || y >= fa.h) return;
   const float2 r = make_float2(__int_as_float(lh.x), __int_as_float(lh.y));
   range[(size_t)y * fa.w + x] = r;
-  raycast_and_normal(m, fa, x, y, r, raycast, points, normals);
+#if defined(RFG_RC_TIMING)
+  // debug build: per warp, the longest march (+ normal) and what it did:
+  // g_rc_warp[warp] = {dur, start, end, steps, lookups, chain loads, nearest
+  // loads, trilinear reads, max steps of the warp, sum of ray ns, CTA start}
+  unsigned long long tr;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr));
+  unsigned long long ctr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int steps = 0;
+  raycast_and_normal(m, fa, x, y, r, raycast, points, normals, ctr, &steps);
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  const unsigned act = __activemask();
+  const unsigned long long dur = t1 - tr;
+  unsigned long long key = (dur << 5) | (threadIdx.x & 31), sum = dur;
+  int ms = (int)ctr[0];
+  for (int o = 16; o >= 1; o >>= 1) {
+    key = max(key, __shfl_xor_sync(act, key, o));
+    sum += __shfl_xor_sync(act, sum, o);
+    ms = max(ms, __shfl_xor_sync(act, ms, o));
+  }
+  if ((threadIdx.x & 31) == (unsigned)(key & 31)) {
+    unsigned long long* rec = g_rc_warp[(t * (kRangeTile * kRangeTile / 32) + (threadIdx.x >> 5)) & (kRcWarps - 1)];
+    rec[0] = dur;
+    rec[1] = tr;
+    rec[2] = t1;
+    for (int k = 0; k < 5; ++k) rec[3 + k] = (unsigned long long)ctr[k];
+    rec[8] = (unsigned long long)ms;
+    rec[9] = sum;
+    rec[10] = t0;
+    for (int k = 0; k < 3; ++k) rec[11 + k] = ctr[5 + k];  // steps 0, 16, 32
+  }
+#else
+  int steps = 0;
+  raycast_and_normal(m, fa, x, y, r, raycast, points, normals, nullptr, &steps);
+#endif
+  // the tile's cost for the next frame's order: its longest march
+  if (ordered) {
+    const int ws = __reduce_max_sync(__activemask(), steps);
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(__activemask()) - 1)) atomicMax(&m.tileCost[t], ws);
+  }
 }
 
 // Normals at every hit, in their own kernel: the six trilinear reads are
@@ -768,7 +934,7 @@ int range_grid() { return current_sm_count() * 8; }
 cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, cudaStream_t s) {
   const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
   if (tx != m.binTilesX || ty > m.binTilesY) return cudaErrorInvalidValue;  // scratch sized by ensure_range_scratch
-  k_range_bin<<<range_grid(), 256, 0, s>>>(m, fa);
+  k_range_bin<<<range_grid(), 256, 0, s>>>(m, fa, 0);
   k_range_tile<<<dim3(tx, ty), kRangeTile * kRangeTile, 0, s>>>(m, fa, range);
   count_launch(2);
   return cudaGetLastError();
@@ -779,7 +945,8 @@ cudaError_t launch_ranges(const DevMap& m, const FrameArgs& fa, float2* range, c
 cudaError_t launch_range_bin(const DevMap& m, const FrameArgs& fa, cudaStream_t s) {
   const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
   if (tx != m.binTilesX || ty > m.binTilesY) return cudaErrorInvalidValue;  // scratch sized by ensure_range_scratch
-  k_range_bin<<<range_grid(), 256, 0, s>>>(m, fa);
+  const int orderK = RFG_RC_ORDER ? current_sm_count() * RFG_RC_ORDER_K : 0;
+  k_range_bin<<<range_grid() + (orderK > 0 ? 1 : 0), 256, 0, s>>>(m, fa, orderK);
   count_launch();
   return cudaGetLastError();
 }
@@ -787,7 +954,10 @@ cudaError_t launch_raycast_tiles(const DevMap& m, const FrameArgs& fa, float2* r
                                  float4* normals, cudaStream_t s) {
   const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
   if (tx != m.binTilesX || ty > m.binTilesY || !raycast) return cudaErrorInvalidValue;
-  k_raycast_tiles<<<dim3(tx, ty), kRangeTile * kRangeTile, 0, s>>>(m, fa, range, raycast, points, normals);
+  if (RFG_RC_ORDER)  // the CTAs take the tiles in the order k_range_bin's extra CTA wrote
+    k_raycast_tiles<<<tx * ty, kRangeTile * kRangeTile, 0, s>>>(m, fa, range, raycast, points, normals, 1);
+  else
+    k_raycast_tiles<<<dim3(tx, ty), kRangeTile * kRangeTile, 0, s>>>(m, fa, range, raycast, points, normals, 0);
   count_launch();
   return cudaGetLastError();
 }
@@ -919,6 +1089,19 @@ extern "C" int rfg_compose_select(const int64_t* keymin, int rank, int n, float*
 }
 
 #if defined(RFG_RC_STATS) || defined(RFG_RC_TIMING)
+#if defined(RFG_RC_TIMING)
+// debug build: the per-warp records of k_raycast_tiles (kRcWarps x 16)
+extern "C" int rfg_debug_rc_warps(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpyFromSymbol(out, rfg::g_rc_warp, sizeof(rfg::g_rc_warp));
+  if (reset) {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, rfg::g_rc_warp);
+    cudaMemset(p, 0, sizeof(rfg::g_rc_warp));
+  }
+  return 0;
+}
+#endif
 extern "C" int rfg_debug_rc_stats(unsigned long long* out32, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out32, rfg::g_rc_stats, sizeof(rfg::g_rc_stats));
