@@ -154,8 +154,11 @@ constexpr int kCellSlots = 1024;  // power of two; ~30-90 distinct blocks per CT
 // 600 CTAs, one wave at 5 CTAs per SM (740 slots), instead of 1.35 waves
 // of 32x8 tiles.
 constexpr int kStage1Rows = 16;
+#ifndef RFG_ALLOC_MINB
+#define RFG_ALLOC_MINB 5  // stage-1 CTAs per SM (640x480: 600 CTAs in one wave)
+#endif
 
-__global__ void __launch_bounds__(256, 5) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
+__global__ void __launch_bounds__(256, RFG_ALLOC_MINB) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
   __shared__ unsigned long long sCell[kCellSlots];  // (x | y << 16 | z << 32 | 1 << 48), 0 = empty
   __shared__ uint32_t sKey[kCellSlots];
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {

@@ -756,11 +756,14 @@ struct rfg_pipeline {
   float4* normals;
   float* poses;  // [0..11] current w2c, [12..23] render pose of the last raycast
   FrameResult* hostResult;  // mapped pinned: k_frame_result's target
+  FrameResult* resultDev;   // its device address (the frame graph's last node writes it)
   float* viewScratch;  // unfiltered depth when cfg.bilateral
   void* pgmStage;      // pinned staging for rfg_pipeline_process_pgm
   cudaEvent_t stageFree;  // the last upload out of pgmStage has been read
   cudaEvent_t rawReady;   // producer stream -> pipeline stream (process_raw_stream)
   cudaEvent_t rawRead;    // pipeline stream has copied the caller's frame
+  cudaStream_t side;      // the frame's second branch (range binning + results, beside the integration)
+  cudaEvent_t fork, join;
   int frames;
   cudaGraphExec_t exec[2];  // [0] no tracking, [1] tracking
   cudaGraph_t graph[2];     // kept for the view node's handle
@@ -782,6 +785,16 @@ struct rfg_pipeline {
 };
 
 namespace {
+
+#ifndef RFG_FRAME_FORK
+#define RFG_FRAME_FORK 1  // the frame's results on a second graph branch (range binning there too measured slower)
+#endif
+#define RFG_TRY(x)                          \
+  do {                                      \
+    const cudaError_t e_ = (x);             \
+    if (e_ != cudaSuccess) return e_;       \
+  } while (0)
+cudaError_t launch_frame_result(rfg_pipeline* p, cudaStream_t s);
 
 cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   rfg_map* m = p->map;
@@ -810,6 +823,16 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
   const FrameArgs fa = make_frame_args(&c.intr, &c.params, nullptr, p->poses);
   if ((e = launch_allocate(m->d, p->depthLevels, fa, s)) != cudaSuccess) return e;
   mark(3);
+#if RFG_FRAME_FORK
+  // the frame's results (the map state is final after the allocation) on a
+  // second graph branch, off the critical path; the raycast joins it
+  if (!prof) {
+    RFG_TRY(cudaEventRecord(p->fork, s));
+    RFG_TRY(cudaStreamWaitEvent(p->side, p->fork, 0));
+    if ((e = launch_frame_result(p, p->side)) != cudaSuccess) return e;
+    RFG_TRY(cudaEventRecord(p->join, p->side));
+  }
+#endif
   if (c.colour) {
     const int nRgb = c.intr_rgb.width * c.intr_rgb.height;
     if ((e = launch_rgb_to_rgba(p->rgbDev, p->rgba, nRgb, s)) != cudaSuccess) return e;
@@ -829,6 +852,22 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
     count_launch();
   }
   mark(6);
+#if RFG_FRAME_FORK
+  if (!prof) {
+    RFG_TRY(cudaStreamWaitEvent(s, p->join, 0));
+    return cudaGetLastError();
+  }
+#endif
+  return launch_frame_result(p, s);
+}
+
+// The frame's results (map state after the allocation, pose, tracker
+// summary) into the mapped host buffer: rfg_pipeline_result only waits.
+cudaError_t launch_frame_result(rfg_pipeline* p, cudaStream_t s) {
+  rfg_map* m = p->map;
+  k_frame_result<<<1, 32, 0, s>>>(p->resultDev, m->d.state, p->poses, icp_stats_ptr(m->icpOut),
+                                  icp_error_ptr(m->icpOut));
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -985,11 +1024,16 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
   }
   p->points = p->raycast + n;
   p->normals = p->raycast + 2 * n;
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->resultDev), p->hostResult, 0) != cudaSuccess) ok = false;
+  memset(p->hostResult, 0, sizeof(FrameResult));  // result() before any frame: zeros
   for (int k = 0; k < 7; ++k)
     if (cudaEventCreate(&p->ev[k]) != cudaSuccess) ok = false;
   if (cudaEventCreateWithFlags(&p->stageFree, cudaEventDisableTiming) != cudaSuccess) ok = false;
   if (cudaEventCreateWithFlags(&p->rawReady, cudaEventDisableTiming) != cudaSuccess) ok = false;
   if (cudaEventCreateWithFlags(&p->rawRead, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  if (cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  if (cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess) ok = false;
   if (!ok) {
     cudaGetLastError();
     rfg_pipeline_destroy(p);
@@ -1027,6 +1071,12 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   if (p->stageFree) cudaEventDestroy(p->stageFree);
   if (p->rawReady) cudaEventDestroy(p->rawReady);
   if (p->rawRead) cudaEventDestroy(p->rawRead);
+  if (p->fork) cudaEventDestroy(p->fork);
+  if (p->join) cudaEventDestroy(p->join);
+  if (p->side) {
+    cudaStreamSynchronize(p->side);
+    cudaStreamDestroy(p->side);
+  }
   if (p->hostResult) cudaFreeHost(p->hostResult);
   if (p->pgmStage) cudaFreeHost(p->pgmStage);
   if (p->map && p->map->stream == p->stream) p->map->stream = nullptr;
@@ -1081,6 +1131,9 @@ int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw, const 
   return rc;
 }
 
+#ifndef RFG_HOST_ZEROCOPY
+#define RFG_HOST_ZEROCOPY 0  // 1: pinned host frames read in place by the graph's view kernel (measured no faster than the copy)
+#endif
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const float* pose34) {
   DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p && rawHost, "null argument");
@@ -1090,7 +1143,7 @@ int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* rawHost, const fl
   // graph's view kernel itself — no separate DMA and no copy->graph gap;
   // pageable frames, and frames before the graph exists, are copied in
   const int gi = (p->cfg.track && p->frames > 0) ? 1 : 0;
-  if (p->cfg.use_graph && p->exec[gi] && p->viewNode[gi]) {
+  if (RFG_HOST_ZEROCOPY && p->cfg.use_graph && p->exec[gi] && p->viewNode[gi]) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, rawHost) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer)
       return run_frame(p, pose34, static_cast<const uint16_t*>(a.devicePointer));
@@ -1133,7 +1186,7 @@ int rfg_pipeline_process_rgbd_host(rfg_pipeline* p, const uint16_t* rawHost, con
   // pinned (device-mapped) host frames are read in place by the graph's view
   // and colour packing kernels; anything else is copied in
   const int gi = (p->cfg.track && p->frames > 0) ? 1 : 0;
-  if (p->cfg.use_graph && p->exec[gi] && p->viewNode[gi] && p->rgbNode[gi]) {
+  if (RFG_HOST_ZEROCOPY && p->cfg.use_graph && p->exec[gi] && p->viewNode[gi] && p->rgbNode[gi]) {
     cudaPointerAttributes a{}, b{};
     if (cudaPointerGetAttributes(&a, rawHost) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer &&
         cudaPointerGetAttributes(&b, rgbHost) == cudaSuccess && b.type == cudaMemoryTypeHost && b.devicePointer)
@@ -1171,18 +1224,13 @@ int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float poseOut34
   DeviceGuard dg_(p && p->map ? p->map->device : -1);
   RFG_REQUIRE(p, "null pipeline");
   rfg_map* m = p->map;
-  FrameResult* dev = nullptr;
-  RFG_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), p->hostResult, 0));
-  k_frame_result<<<1, 32, 0, p->stream>>>(dev, m->d.state, p->poses, icp_stats_ptr(m->icpOut),
-                                          icp_error_ptr(m->icpOut));
-  count_launch();
-  RFG_CK(cudaGetLastError());
+  // the frame graph's last node wrote the results (enqueue_frame)
   RFG_CK(cudaStreamSynchronize(p->stream));
-  *m->hostState = p->hostResult->state;
-  if (m->hostState->error) return check_device_error(m);
+  const MapState& ms = p->hostResult->state;
+  if (ms.error) return check_device_error(m);
   if (stats) {
-    memcpy(stats, m->hostState->stats, sizeof(rfg_alloc_stats));
-    stats->visibleCount = m->hostState->nVisible;  // stage 3 appends the list; its length is the count
+    memcpy(stats, ms.stats, sizeof(rfg_alloc_stats));
+    stats->visibleCount = ms.nVisible;  // stage 3 appends the list; its length is the count
   }
   if (p->hostResult->icpError) {
     set_error("ICP: a world point outside the fixed-point range (|p| components >= 128 m)");

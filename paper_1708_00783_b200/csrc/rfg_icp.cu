@@ -356,13 +356,6 @@ constexpr int kIcpGroup = RFG_ICP_GROUP;  // projections + gathers issued this m
 // accumulators (|term| < 2^16 H units, so 8 terms stay inside the 2^19 range)
 constexpr int kIcpFlush = 8;
 
-// a fixed-point sum as a double: ldexp((double)v, -s) (rfo.c icp_decode), as
-// one multiplication by 2^-s (exact: no underflow at these scales)
-__device__ __forceinline__ double icp_decode(long long v, int k) {
-  const int sh = icp_shift(k);
-  return (double)v * (sh == 32 ? 0x1p-32 : (sh == 38 ? 0x1p-38 : (sh == 44 ? 0x1p-44 : 1.0)));
-}
-
 // fixed-point offsets M = 1.5 * 2^(52 - s)
 __device__ __forceinline__ double icp_offset(int k) {
   return icp_shift(k) == 32 ? 1572864.0 : (icp_shift(k) == 38 ? 24576.0 : 384.0);
@@ -690,7 +683,7 @@ __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& 
       // sum = (sum of the high halves) * 2^32 + (sum of the low halves), mod 2^64
       const long long v = (long long)((x.part[kIcpSums + threadIdx.x] << 32) + x.part[threadIdx.x]);
       g.fixed[threadIdx.x] = v;
-      g.sums[threadIdx.x] = icp_decode(v, threadIdx.x);
+      g.sums[threadIdx.x] = ldexp((double)v, -icp_shift(threadIdx.x));
     }
 #else
     unsigned long long* buf = st->acc[(gen + gi) % 3];
@@ -709,7 +702,7 @@ __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& 
     if (threadIdx.x < kIcpSums) {
       const long long v = (long long)__ldcg(buf + threadIdx.x * RFG_ICP_PAD);
       g.fixed[threadIdx.x] = v;
-      g.sums[threadIdx.x] = icp_decode(v, threadIdx.x);
+      g.sums[threadIdx.x] = ldexp((double)v, -icp_shift(threadIdx.x));
     }
 #endif
     __syncthreads();
@@ -879,7 +872,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_coarse(IcpState* st, Icp
     if (threadIdx.x < kIcpSums) {
       const long long v = (long long)dst[threadIdx.x];
       g.fixed[threadIdx.x] = v;
-      g.sums[threadIdx.x] = icp_decode(v, threadIdx.x);
+      g.sums[threadIdx.x] = ldexp((double)v, -icp_shift(threadIdx.x));
     }
     __syncthreads();
     if (timed) t3 = gtimer();
