@@ -41,13 +41,6 @@ constexpr int kIcpStats = 12;  // TrackerIterationSummary (include/rfg.h)
 // fixed-point scale (log2) per sum; 0 = plain integer count (rfo.c:kIcpShift)
 __host__ __device__ constexpr int icp_shift(int k) { return k < 21 ? 32 : (k < 27 ? 38 : (k == 28 || k == 30 ? 0 : 44)); }
 
-#ifndef RFG_ICP_SLOTS
-#define RFG_ICP_SLOTS 0  // 1: cross-CTA sums in counted slots instead of atomics + grid barrier (measured no faster)
-#endif
-#ifndef RFG_ICP_PAD
-#define RFG_ICP_PAD 1    // u64 stride of the cross-CTA sums (16: one 128-B line each; measured no faster)
-#endif
-
 // Device tracking state (rfg_map::icpOut).
 struct IcpState {
   double c2w[12];                 // current camera->world estimate (row-major 3x4)
@@ -70,12 +63,7 @@ struct IcpState {
   // three rotating cross-CTA accumulators: iteration i adds into [i % 3]
   // and zeroes [(i + 1) % 3], which iteration i - 2 used and every CTA has
   // read before the barrier of iteration i - 1 (all zero between launches)
-  // (RFG_ICP_SLOTS = 0 only)
-  unsigned long long acc[3][32 * RFG_ICP_PAD];
-  // RFG_ICP_SLOTS = 1: two alternating sets of 62 counted slots (below) and
-  // their values at the end of the last launch
-  unsigned long long slotBase[2][64];
-  alignas(128) unsigned long long slots[2][64 * RFG_ICP_PAD];
+  unsigned long long acc[3][32];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -348,10 +336,7 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
 // later iterations.  Level 0 at 640x480 on 148 CTAs is 4.05 pixels per
 // thread: one cached round plus a few uncached pixels.
 constexpr int kIcpPx = 5;  // 148 x 512 x 5 >= 640 x 480: one cached round at C1/C2
-#ifndef RFG_ICP_GROUP
-#define RFG_ICP_GROUP 2
-#endif
-constexpr int kIcpGroup = RFG_ICP_GROUP;  // projections + gathers issued this many pixels at a time
+constexpr int kIcpGroup = 2;  // projections + gathers issued 2 pixels at a time
 // pixels per thread between flushes of the per-thread fixed-point
 // accumulators (|term| < 2^16 H units, so 8 terms stay inside the 2^19 range)
 constexpr int kIcpFlush = 8;
@@ -415,11 +400,11 @@ __device__ __forceinline__ int icp_associate(const IcpLevelArgs& a, const Pose& 
   return iv * a.rw + iu;
 }
 
-// The CTA's fixed-point sums of the thread accumulators, added to the CTA's
-// partial sums ctaSum (shared memory; integer sums, so the order is
+// The CTA's fixed-point sums of the thread accumulators, added to the global
+// accumulator `dst` (64-bit atomics; integer sums, so the order is
 // irrelevant).  Warp: recursive halving (lane l ends with sum l: 31
 // shuffles of 64 bits instead of 31 x 5); CTA: shared memory.
-__device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[32], long long* ctaSum,
+__device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[32], unsigned long long* dst,
                                               int activeWarps, unsigned long long* subT = nullptr) {
   (void)subT;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -460,7 +445,7 @@ __device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[3
 #pragma unroll
     for (int w = 0; w < kIcpThreads / 32; ++w)
       if (w < activeWarps) t += sh[w][threadIdx.x];
-    ctaSum[threadIdx.x] += t;  // this thread's own slot
+    if (t) atomicAdd(dst + threadIdx.x, (unsigned long long)t);
   }
   __syncthreads();  // sh is reused by the next round
 #ifdef RFG_ICP_SUB
@@ -468,7 +453,7 @@ __device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[3
 #endif
 }
 
-// One evaluation's contribution of this CTA, left in ctaSum.  The level's
+// One evaluation's contribution of this CTA, added to dst.  The level's
 // pixels are dealt in 32-pixel chunks round-robin over the CTAs and their
 // warps: warp w of CTA c takes chunks c + nCta (w + 16 k), k = 0, 1, ...
 // (k < kIcpPx: camera points cached when `fill`; the rest uncached), so
@@ -476,11 +461,10 @@ __device__ __forceinline__ void icp_cta_flush(const IcpAcc& s, long long (*sh)[3
 // and a coarse level still reaches every SM.  Returns false when a world
 // point was outside the fixed-point range.  (The sums are order-independent
 // integers, so the pixel-to-thread mapping does not change them.)
-__device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShared& g, const Pose& rp, const Intr& inl,
-                                             float dist2, int n, int nCta, long long (*sh)[32], float4* pcs,
-                                             bool fill, long long* ctaSum) {
+__device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShared& g, const Pose& rp,
+                                             const Intr& inl, float dist2, int n, int nCta, long long (*sh)[32],
+                                             float4* pcs, bool fill, unsigned long long* dst) {
   const Pose c2w = pose_from12(g.c2wF);
-
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   constexpr int kWarps = kIcpThreads / 32;
   const int nChunks = (n + 31) >> 5;
@@ -497,7 +481,6 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
   bool ok = true;
   IcpAcc s;
   acc_reset(s);
-  if (t < kIcpSums) ctaSum[t] = 0;  // added to by the same thread in the flushes
 #ifdef RFG_ICP_SUB
   unsigned long long subT[6] = {0, 0, 0, 0, 0, 0};
   ICP_SUB(0);
@@ -554,7 +537,7 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
   // kIcpFlush pixels (the fixed-point accumulators' range)
   for (int k = kIcpPx; k < rounds; ++k) {
     if (k % kIcpFlush == 0) {
-      icp_cta_flush(s, sh, ctaSum, activeWarps);
+      icp_cta_flush(s, sh, dst, activeWarps);
       acc_reset(s);
     }
     const int p = pixel(k);
@@ -570,7 +553,7 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
     ok &= icp_add(s, pw, __ldg(a.points + pix), __ldg(a.normals + pix), dist2);
   }
   ICP_SUB(2);
-  icp_cta_flush(s, sh, ctaSum, activeWarps, subT);
+  icp_cta_flush(s, sh, dst, activeWarps, subT);
 #ifdef RFG_ICP_SUB
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int k = 0; k < 5; ++k) g_icp_sub[a.level][k] += subT[k + 1] - subT[k];
@@ -580,53 +563,12 @@ __device__ __forceinline__ bool icp_cta_eval(const IcpLevelArgs& a, const GnShar
   return ok;
 }
 
-// The cross-CTA exchange of one evaluation's sums, per CTA (shared memory).
-// RFG_ICP_SLOTS = 1: every sum k is added as two 64-bit "counted slots" —
-// its low 32 bits (unsigned) and its high 32 bits (signed), each plus 2^56 —
-// so a slot's value since its last completed iteration is
-//   (CTAs arrived) * 2^56 + (their partial sums),   |partial sums| < 2^55,
-// and a reader knows the slot is complete, without a barrier, when the count
-// reaches the number of CTAs (<= 255; every CTA adds to every slot, zeros
-// when it owns no pixels of the level): one RED per slot and CTA, then each
-// of 62 threads polls its own slot (one 128-B line each).
-// Two slot sets alternate between iterations: a CTA adds to iteration i + 2
-// only after every CTA has added to i + 1, i.e. finished reading i.  The
-// slots are never cleared: each thread keeps the value its slot had when it
-// last completed (prev), and CTA 0 stores them for the next launch (slotBase).
-struct IcpXchg {
-  long long cta[32];               // this CTA's partial sums of the evaluation
-  unsigned long long prev[2][64];  // each slot's value after its last completed iteration
-  unsigned long long part[64];     // the completed iteration's slot sums
-};
-constexpr unsigned long long kSlotOne = 1ull << 56, kSlotHalf = 1ull << 55;
-
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void icp_xchg_init(IcpState* st, IcpXchg& x) {
-  if (threadIdx.x < 64) {
-    x.prev[0][threadIdx.x] = __ldcg(&st->slotBase[0][threadIdx.x]);
-    x.prev[1][threadIdx.x] = __ldcg(&st->slotBase[1][threadIdx.x]);
-  }
-}
-// CTA 0 at the end of a launch: every slot's value, for the next launch
-__device__ __forceinline__ void icp_xchg_save(IcpState* st, const IcpXchg& x) {
-  if (blockIdx.x == 0 && threadIdx.x < 64) {
-    st->slotBase[0][threadIdx.x] = x.prev[0][threadIdx.x];
-    st->slotBase[1][threadIdx.x] = x.prev[1][threadIdx.x];
-  }
-}
-
 // One level's Gauss-Newton loop on the CTA-local state g.  CTAs with
 // blockIdx.x < nCta own the level's pixels (icp_cta_eval's chunks); the
-// others only wait for the sums and run the same solve.  `gi` counts
-// iterations across levels (slot-set / accumulator rotation, with the
-// launch's `gen`).
+// others only join the barriers and run the same solve.  `gi` counts
+// iterations across levels (accumulator rotation, with the launch's `gen`).
 __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& a, int nCta, GnShared& g,
-                                              long long (*sh)[32], float4* pcs, IcpXchg& x, unsigned gen, int& gi,
+                                              long long (*sh)[32], float4* pcs, unsigned gen, int& gi,
                                               unsigned long long* tacc) {
   const Intr inl{a.lw, a.lh, a.fx, a.fy, a.cx, a.cy};
   const float dist2 = a.dist * a.dist;
@@ -634,44 +576,24 @@ __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& 
   const Pose rp = pose_from12(g.rp);
   const bool timed = blockIdx.x == 0 && threadIdx.x == 0;
   const bool owner = (int)blockIdx.x < nCta;
+  cg::grid_group grid = cg::this_grid();
   for (int it = 0; it < a.iters && !g.done; ++it, ++gi) {
     unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (timed) t0 = gtimer();
+    unsigned long long* buf = st->acc[(gen + gi) % 3];
 #ifdef RFG_ICP_SUB
     const unsigned long long tEv = gtimer();
 #endif
     if (owner) {
-      const bool ok = icp_cta_eval(a, g, rp, inl, dist2, n, nCta, sh, pcs, it == 0, x.cta);
+      const bool ok = icp_cta_eval(a, g, rp, inl, dist2, n, nCta, sh, pcs, it == 0, buf);
       if (!ok) st->error = 1;
     }
 #ifdef RFG_ICP_SUB
     if (threadIdx.x == 0) atomicMax(&g_icp_maxev, gtimer() - tEv);
 #endif
-#if RFG_ICP_SLOTS
-    const int par = (int)((gen + (unsigned)gi) & 1u);
-    unsigned long long* slots = st->slots[par];
-    // every CTA adds to every slot (zeros when it owns no pixels of the
-    // level), so no CTA can run more than one iteration ahead of another
-    if (threadIdx.x < kIcpSums) {
-      const long long t = owner ? x.cta[threadIdx.x] : 0ll;
-      atomicAdd(slots + threadIdx.x * RFG_ICP_PAD, (unsigned long long)(uint32_t)t + kSlotOne);
-      atomicAdd(slots + (kIcpSums + threadIdx.x) * RFG_ICP_PAD,
-                (unsigned long long)(long long)(int)(t >> 32) + kSlotOne);
-    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) st->acc[(gen + gi + 1) % 3][threadIdx.x] = 0ull;
     if (timed) t1 = gtimer();
-    if (threadIdx.x < 2 * kIcpSums) {
-      const unsigned long long* sp = slots + threadIdx.x * RFG_ICP_PAD;
-      const unsigned long long pv = x.prev[par][threadIdx.x];
-      const unsigned long long want = gridDim.x & 255u;  // gridDim.x <= 255 (launch_icp_*)
-      unsigned long long v, d;
-      do {
-        v = ld_relaxed_u64(sp);
-        d = v - pv;
-      } while ((((d + kSlotHalf) >> 56) & 255u) != want);
-      x.prev[par][threadIdx.x] = v;
-      x.part[threadIdx.x] = d - ((unsigned long long)gridDim.x << 56);
-    }
-    __syncthreads();
+    grid.sync();
     if (timed) t2 = gtimer();
 #ifdef RFG_ICP_SUB
     if (timed && a.level < 3) {
@@ -680,31 +602,10 @@ __device__ __forceinline__ void icp_run_level(IcpState* st, const IcpLevelArgs& 
     }
 #endif
     if (threadIdx.x < kIcpSums) {
-      // sum = (sum of the high halves) * 2^32 + (sum of the low halves), mod 2^64
-      const long long v = (long long)((x.part[kIcpSums + threadIdx.x] << 32) + x.part[threadIdx.x]);
+      const long long v = (long long)__ldcg(buf + threadIdx.x);
       g.fixed[threadIdx.x] = v;
       g.sums[threadIdx.x] = ldexp((double)v, -icp_shift(threadIdx.x));
     }
-#else
-    unsigned long long* buf = st->acc[(gen + gi) % 3];
-    if (owner && threadIdx.x < kIcpSums && x.cta[threadIdx.x])
-      atomicAdd(buf + threadIdx.x * RFG_ICP_PAD, (unsigned long long)x.cta[threadIdx.x]);
-    if (blockIdx.x == 0 && threadIdx.x < 32) st->acc[(gen + gi + 1) % 3][threadIdx.x * RFG_ICP_PAD] = 0ull;
-    if (timed) t1 = gtimer();
-    cg::this_grid().sync();
-    if (timed) t2 = gtimer();
-#ifdef RFG_ICP_SUB
-    if (timed && a.level < 3) {
-      g_icp_sub[a.level][5] += *((volatile unsigned long long*)&g_icp_maxev);
-      g_icp_maxev = 0;
-    }
-#endif
-    if (threadIdx.x < kIcpSums) {
-      const long long v = (long long)__ldcg(buf + threadIdx.x * RFG_ICP_PAD);
-      g.fixed[threadIdx.x] = v;
-      g.sums[threadIdx.x] = ldexp((double)v, -icp_shift(threadIdx.x));
-    }
-#endif
     __syncthreads();
     if (timed) t3 = gtimer();
     if (threadIdx.x == 0) {
@@ -753,9 +654,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_level(IcpState* st, IcpL
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
-  __shared__ IcpXchg x;
   const unsigned gen = __ldcg(&st->gen);
-  icp_xchg_init(st, x);
   if (threadIdx.x == 0) {
     for (int i = 0; i < 12; ++i) {
       g.c2w[i] = __ldcg(&st->c2w[i]);
@@ -770,8 +669,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_level(IcpState* st, IcpL
   __syncthreads();
   int gi = 0;
   unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  icp_run_level(st, a, gridDim.x, g, sh, pcs, x, gen, gi, tacc);
-  icp_xchg_save(st, x);
+  icp_run_level(st, a, gridDim.x, g, sh, pcs, gen, gi, tacc);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     icp_publish(st, g, tacc, gen, gi);
     st->done[a.level] = g.done;
@@ -839,7 +737,6 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_coarse(IcpState* st, Icp
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
   __shared__ unsigned long long cacc[3][32];  // rank 0's are the cluster's accumulators
-  __shared__ long long ctaSum[32];
   cg::cluster_group cl = cg::this_cluster();
   const int l = ta.levels - 1;
   const IcpLevelArgs& a = ta.lv[l];
@@ -863,8 +760,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_coarse(IcpState* st, Icp
     unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (timed) t0 = gtimer();
     unsigned long long* dst = cl.map_shared_rank(&cacc[it % 3][0], 0);
-    ok &= icp_cta_eval(a, g, rp, inl, dist2, n, nCta, sh, pcs, it == 0, ctaSum);
-    if (threadIdx.x < kIcpSums && ctaSum[threadIdx.x]) atomicAdd(dst + threadIdx.x, (unsigned long long)ctaSum[threadIdx.x]);
+    ok &= icp_cta_eval(a, g, rp, inl, dist2, n, nCta, sh, pcs, it == 0, dst);
     if (rank0 && threadIdx.x < 32) cacc[(it + 1) % 3][threadIdx.x] = 0ull;  // read by no CTA since it - 2
     if (timed) t1 = gtimer();
     cl.sync();
@@ -904,12 +800,10 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpT
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
-  __shared__ IcpXchg x;
 #ifdef RFG_ICP_PHASES
   const unsigned long long tEntry = gtimer();
 #endif
   const unsigned gen = __ldcg(&st->gen);
-  icp_xchg_init(st, x);
   if (threadIdx.x == 0) {
     if (ta.fromState) {
       icp_seed_from_state(st, g);
@@ -926,9 +820,8 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpT
     if (ta.lv[l].iters <= 0) continue;
     if (threadIdx.x == 0) g.done = 0;
     __syncthreads();
-    icp_run_level(st, ta.lv[l], ta.nCta[l], g, sh, pcs, x, gen, gi, tacc);
+    icp_run_level(st, ta.lv[l], ta.nCta[l], g, sh, pcs, gen, gi, tacc);
   }
-  icp_xchg_save(st, x);
   // every CTA read renderPose before its first grid barrier; with no
   // iteration at all (every level capped at 0) there was none, so one is
   // needed before CTA 0 may overwrite it below (gi is the same in every CTA)
@@ -967,9 +860,6 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpT
 
 // CTAs for a level of n pixels: about one pixel per thread, at most one CTA
 // per SM (co-residency for grid.sync).  Fixed per (device, level size).
-#ifndef RFG_ICP_MIN_WARPS
-#define RFG_ICP_MIN_WARPS 1  // a level's owner CTAs: at least this many warps of pixels each
-#endif
 static int icp_grid(int n) {
   static int fits[64] = {};  // per device: 1 fits one CTA per SM, -1 does not
   int dev = 0;
@@ -987,10 +877,8 @@ static int icp_grid(int n) {
   // every SM takes a part of every level (at least a warp of pixels per CTA):
   // spreading a coarse level over all SMs leaves fewer busy warps per SM for
   // the accumulation and the CTA reduction
-  const int want = (n + 32 * RFG_ICP_MIN_WARPS - 1) / (32 * RFG_ICP_MIN_WARPS);
-  // (<= 255 CTAs: the counted slots' 8-bit arrival count, icp_run_level)
-  const int cap = sms < 255 ? sms : 255;
-  return want < 1 ? 1 : (want < cap ? want : cap);
+  const int want = (n + 31) / 32;
+  return want < 1 ? 1 : (want < sms ? want : sms);
 }
 
 size_t icp_state_bytes() { return sizeof(IcpState); }
