@@ -78,6 +78,7 @@ FrameArgs make_frame_args(const rfg_intrinsics* intr, const rfg_scene_params* p,
   fa.poseDev = poseDev;
   fa.swapping = 0;
   fa.swapMargin = 8.f;
+  fa.depthBounded = 0;
   return fa;
 }
 
@@ -820,7 +821,9 @@ cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
     if (e != cudaSuccess) return e;
   }
   mark(2);
-  const FrameArgs fa = make_frame_args(&c.intr, &c.params, nullptr, p->poses);
+  FrameArgs fa = make_frame_args(&c.intr, &c.params, nullptr, p->poses);
+  // the frame's depths are raw u16 * scale + offset (view kernels): bounded
+  fa.depthBounded = 65535.0 * fabs((double)c.aff_scale) + fabs((double)c.aff_offset) < 0x1p36 ? 1 : 0;
   if ((e = launch_allocate(m->d, p->depthLevels, fa, s)) != cudaSuccess) return e;
   mark(3);
 #if RFG_FRAME_FORK

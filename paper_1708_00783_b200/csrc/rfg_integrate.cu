@@ -57,13 +57,20 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 
 // One visible block of the depth-only kernel (one warp, 16 voxels per lane).
 // kWindowKnown: the block-level test below has proven that every voxel's
-// projection quotients are inside div_fast's exactness window, so only the
-// eta quotient keeps a per-voxel window test.
+// projection quotients are inside div_fast's exactness window, and the frame
+// that every eta quotient is (depths below 2^36 m, mu in [2^-20, 2^20]), so
+// no voxel needs a per-voxel window test.
 #ifndef RFG_INT_DIET
 #define RFG_INT_DIET 1
 #endif
 #ifndef RFG_INT_SKIP
 #define RFG_INT_SKIP 1  // warp-uniform skip of the update math of voxel slots no lane updates
+#endif
+#ifndef RFG_INT_V2
+#define RFG_INT_V2 1  // fewer ALU-pipe instructions per voxel (folded pixel index, F2I lround, sentinel depth)
+#endif
+#ifndef RFG_INT_V2_RANGE
+#define RFG_INT_V2_RANGE 0  // the u / v window tests as (u - 1) bit compares
 #endif
 #ifndef RFG_INT_TMA
 #define RFG_INT_TMA 0  // depth integration with TMA-prefetched voxel rows (k_integrate_depth_tma)
@@ -85,6 +92,13 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
                                                       float hLim, float mu, bool muOk, float rMu, bool capW, int maxW,
                                                       const float* rcpTab) {
   const float vs = fa.voxelSize;
+#if RFG_INT_V2
+  const uint32_t pixMagic = 0x4B000000u * ((uint32_t)fa.w + 1u);
+  const int capMax = capW ? maxW : 256;  // oldW < capMax <=> !(capW && oldW >= maxW) (oldW <= 255)
+#endif
+#if RFG_INT_V2_RANGE
+  const uint32_t uBound = __float_as_uint(wLim - 1.f), vBound = __float_as_uint(hLim - 1.f);
+#endif
 #if RFG_INT_DIET
   // this lane's four x columns: the same in all of its rows
   float rx0[4], rx3[4], rx6[4];
@@ -136,8 +150,27 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
         const float rz = div_rcp(czw);
         const float u = div_fast(ax, czw, rz) + fa.cx;
         const float v = div_fast(ay, czw, rz) + fa.cy;
+#if RFG_INT_V2_RANGE
+        // 1 <= u <= wLim as one unsigned compare of the bits of u - 1 (exact
+        // for u >= 0.5, negative below; negative floats compare above every
+        // positive bound)
+        const bool in = czw > 0.f && __float_as_uint(u - 1.f) <= uBound && __float_as_uint(v - 1.f) <= vBound;
+#elif RFG_INT_V2
+        // the reference's tests (fusion.cpp:15-17) as non-short-circuit ANDs,
+        // so the projection stays branch-free
+        const bool in = (czw > 0.f) & !(u < 1.f) & !(u > wLim) & !(v < 1.f) & !(v > hLim);
+#else
         const bool in = czw > 0.f && !(u < 1 || u > wLim || v < 1 || v > hLim);
-#if RFG_INT_DIET
+#endif
+#if RFG_INT_V2
+        // u, v in [1, W-2] when `in`: the truncations of u + 0.5, v + 0.5
+        // (static_cast<int>, fusion.cpp:18) by the 2^23 magic number, with
+        // both magic offsets folded into one constant (mod 2^32); computed
+        // for every voxel, selected by `in`
+        const int pv = (int)(__float_as_uint(__fadd_rz(v + 0.5f, 8388608.0f)) * (uint32_t)fa.w +
+                             __float_as_uint(__fadd_rz(u + 0.5f, 8388608.0f)) - pixMagic);
+        pix[k] = in ? pv : -1;
+#elif RFG_INT_DIET
         // u, v in [1, W-2] when `in`: the truncations of u + 0.5, v + 0.5 (static_cast<int>, fusion.cpp:18)
         pix[k] = in ? trunc_pos_to_int(v + 0.5f) * fa.w + trunc_pos_to_int(u + 0.5f) : -1;
 #else
@@ -171,7 +204,12 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
       const uint32_t w0 = wd[k];
       const int oldW = vox_w(w0);
       const float eta = dm[k] - zc[k];
+#if RFG_INT_V2
+      // dm = -1 for a voxel outside the image, so the depth test covers it
+      const bool upd = !(dm[k] <= 0.f) && !(eta < -mu) && oldW < capMax;
+#else
       const bool upd = pix[k] >= 0 && !(dm[k] <= 0.f) && !(eta < -mu) && !(capW && oldW >= maxW);
+#endif
 #if RFG_INT_SKIP
       // a voxel slot no lane of the warp updates skips the update math
       if (!__any_sync(0xffffffffu, upd)) continue;
@@ -183,7 +221,15 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
       const float num = fw * oldF + newF;
       const float den = fw + 1.f;  // == (float)(oldW + 1): small integers are exact
       const float merged = div_fast(num, den, rcpTab[oldW]);  // rcpTab[w] == div_rcp(w + 1)
+#if RFG_INT_V2
+      // lround (half away from zero) of the clamped value * 32767: the sum
+      // with +-0.5 rounded toward zero, then truncated (F2I.TRUNC)
+      const float cl = fminf(fmaxf(merged, -1.f), 1.f) * (float)kSdfOne;
+      const int sdfI = __float2int_rz(__fadd_rz(cl, __uint_as_float((__float_as_uint(cl) & 0x80000000u) | 0x3F000000u)));
+      const uint32_t w1 = ((uint32_t)sdfI & 0xFFFFu) | ((uint32_t)min(oldW + 1, maxW) << 16);
+#else
       const uint32_t w1 = vox_pack(sdf_from_logical_alu(merged), min(oldW + 1, maxW));
+#endif
 #else
       const float oldF = sdf_to_logical(vox_sdf(w0));
       const float newF = smin(1.f, div_fast(eta, mu, rMu));
@@ -193,13 +239,18 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
       const float merged = div_fast(num, den, div_rcp(den));
       const uint32_t w1 = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
 #endif
+      if (kWindowKnown) {
+        // the block's quotients and the frame's depths, mu are proven inside
+        // div_fast's window (integrate_block_depth's caller)
+        wd[k] = upd ? w1 : w0;
+        continue;
+      }
       // out-of-window voxels keep w0 here and are redone exactly below
-      const bool slowK = kWindowKnown ? (upd && !(muOk && fabsf(eta) <= 0x1p40f))
-                                      : (upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << k))));
+      const bool slowK = upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << k)));
       wd[k] = (upd && !slowK) ? w1 : w0;
       redo |= slowK ? (1u << k) : 0u;
     }
-    if (__any_sync(0xffffffffu, redo != 0u)) {
+    if (!kWindowKnown && __any_sync(0xffffffffu, redo != 0u)) {
 #pragma unroll
       for (int k = 0; k < 4 * kQG; ++k)
         if (redo & (1u << k)) wd[k] = update_exact(wd[k], dm[k] - zc[k], mu, maxW);
@@ -254,6 +305,9 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
   const float rMu = div_rcp(mu);
   const bool capW = fa.stopAtMaxW != 0;
   const int maxW = fa.maxW;
+  // |eta| = |depth - z| <= 2^36 + 2^38 < 2^40 for every voxel of a block
+  // whose projection window is proven, when the frame's depths are bounded
+  const bool frameKnown = muOk && fa.depthBounded;
   __shared__ float rcpTab[256];  // 1 / (w + 1) as div_rcp computes it, w = 0..255
   rcpTab[threadIdx.x] = div_rcp((float)(threadIdx.x + 1));  // blockDim.x == 256
   __syncthreads();
@@ -263,7 +317,7 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
     if (e.w < 0) continue;
     const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
     uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
-    if (block_window_known(lane, ox, oy, oz, pose, fa))
+    if (frameKnown && block_window_known(lane, ox, oy, oz, pose, fa))
       integrate_block_depth<true>(blk, blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
                                   maxW, rcpTab);
     else
@@ -363,7 +417,7 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth_tma(DevMa
         phase ^= 1u << s;
         const int ox = entry_x(e) * kBlock, oy = entry_y(e) * kBlock, oz = entry_z(e) * kBlock;
         uint4* blk = reinterpret_cast<uint4*>(m.vbaDepth + (size_t)e.w * kBlock3);
-        if (block_window_known(lane, ox, oy, oz, pose, fa))
+        if (muOk && fa.depthBounded && block_window_known(lane, ox, oy, oz, pose, fa))
           integrate_block_depth<true>(stage[w][s], blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk,
                                       rMu, capW, maxW, rcpTab);
         else

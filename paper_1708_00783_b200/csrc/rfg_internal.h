@@ -65,6 +65,7 @@ struct FrameArgs {
   const float* poseDev;    // device-resident pose (tracking pipeline)
   int swapping;            // FusionEngine::Options::swappingEnabled (fusion.hpp:55)
   float swapMargin;        // Options::swapMarginPx (fusion.hpp:56)
+  int depthBounded;        // every depth value is below 2^36 m in magnitude (the pipeline's u16 frames)
 };
 
 struct Pose12 {
