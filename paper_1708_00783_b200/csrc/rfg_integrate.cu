@@ -69,6 +69,9 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 #ifndef RFG_INT_V2
 #define RFG_INT_V2 1  // fewer ALU-pipe instructions per voxel (folded pixel index, F2I lround, sentinel depth)
 #endif
+#ifndef RFG_INT_RCP_INLINE
+#define RFG_INT_RCP_INLINE 0  // 1/(w+1) by MUFU + 2 FFMA per voxel instead of the shared table
+#endif
 #ifndef RFG_INT_V2_RANGE
 #define RFG_INT_V2_RANGE 0  // the u / v window tests as (u - 1) bit compares
 #endif
@@ -84,6 +87,12 @@ __device__ __forceinline__ int16_t sdf_from_logical_alu(float f) {
   float c = f < -1.f ? -1.f : (1.f < f ? 1.f : f);
   return (int16_t)lround_haz_alu(c * (float)kSdfOne);
 }
+
+// 1 / (w + 1) as div_rcp computes it, w = 0..255, per CTA (filled by the
+// depth kernels' prologue).  A file-scope __shared__ array, so a load is one
+// LDS at the symbol's offset (through a pointer parameter the compiler
+// re-derives the CTA's shared window base at every use).
+__shared__ float s_rcpTab[256];
 
 template <bool kWindowKnown>
 __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* blk, int lane, int ox, int oy, int oz,
@@ -156,9 +165,13 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
         // positive bound)
         const bool in = czw > 0.f && __float_as_uint(u - 1.f) <= uBound && __float_as_uint(v - 1.f) <= vBound;
 #elif RFG_INT_V2
-        // the reference's tests (fusion.cpp:15-17) as non-short-circuit ANDs,
-        // so the projection stays branch-free
-        const bool in = (czw > 0.f) & !(u < 1.f) & !(u > wLim) & !(v < 1.f) & !(v > hLim);
+        // the reference's window tests (fusion.cpp:15-17) as the sign of one
+        // max: 1 - u <= 0 <=> u >= 1 and u - wLim <= 0 <=> u <= wLim exactly
+        // (a rounded difference keeps the sign of the exact one, and is zero
+        // only when it is), so the projection stays branch-free with one
+        // predicate
+        const float outside = fmaxf(fmaxf(1.f - u, u - wLim), fmaxf(1.f - v, v - hLim));
+        const bool in = (czw > 0.f) & (outside <= 0.f);
 #else
         const bool in = czw > 0.f && !(u < 1 || u > wLim || v < 1 || v > hLim);
 #endif
@@ -220,7 +233,15 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
       const float fw = u23_to_float((uint32_t)oldW);
       const float num = fw * oldF + newF;
       const float den = fw + 1.f;  // == (float)(oldW + 1): small integers are exact
+#if RFG_INT_V2 && RFG_INT_RCP_INLINE
+      const float merged = div_fast(num, den, div_rcp(den));
+      (void)rcpTab;
+#elif RFG_INT_V2
+      const float merged = div_fast(num, den, s_rcpTab[oldW]);  // == div_rcp(oldW + 1)
+      (void)rcpTab;
+#else
       const float merged = div_fast(num, den, rcpTab[oldW]);  // rcpTab[w] == div_rcp(w + 1)
+#endif
 #if RFG_INT_V2
       // lround (half away from zero) of the clamped value * 32767: the sum
       // with +-0.5 rounded toward zero, then truncated (F2I.TRUNC)
@@ -308,7 +329,7 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
   // |eta| = |depth - z| <= 2^36 + 2^38 < 2^40 for every voxel of a block
   // whose projection window is proven, when the frame's depths are bounded
   const bool frameKnown = muOk && fa.depthBounded;
-  __shared__ float rcpTab[256];  // 1 / (w + 1) as div_rcp computes it, w = 0..255
+  float* rcpTab = s_rcpTab;  // 1 / (w + 1) as div_rcp computes it, w = 0..255
   rcpTab[threadIdx.x] = div_rcp((float)(threadIdx.x + 1));  // blockDim.x == 256
   __syncthreads();
   for (int b = gw; b < nVis; b += nw) {
@@ -366,7 +387,7 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth_tma(DevMa
                                                                            FrameArgs fa) {
   __shared__ __align__(128) uint4 stage[kTmaWarps][2][kBlock3 / 4];
   __shared__ __align__(8) unsigned long long bar[kTmaWarps][2];
-  __shared__ float rcpTab[256];
+  float* rcpTab = s_rcpTab;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * kTmaWarps + w;
   const int nw = gridDim.x * kTmaWarps;
