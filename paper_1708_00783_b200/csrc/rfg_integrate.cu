@@ -669,8 +669,17 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
+#if RFG_INT_V2
+      // as integrate_block_depth: one predicate, the folded magic pixel index
+      const float outside = fmaxf(fmaxf(1.f - uu[i], uu[i] - wLim), fmaxf(1.f - vv[i], vv[i] - hLim));
+      const bool in = (zc[i] > 0.f) & (outside <= 0.f);
+      const int pv = (int)(__float_as_uint(__fadd_rz(vv[i] + 0.5f, 8388608.0f)) * (uint32_t)fa.w +
+                           __float_as_uint(__fadd_rz(uu[i] + 0.5f, 8388608.0f)) - 0x4B000000u * ((uint32_t)fa.w + 1u));
+      pix[i] = in ? pv : -1;
+#else
       const bool in = zc[i] > 0.f && !(uu[i] < 1 || uu[i] > wLim || vv[i] < 1 || vv[i] > hLim);
       pix[i] = in ? (int)(vv[i] + 0.5f) * fa.w + (int)(uu[i] + 0.5f) : -1;
+#endif
     }
     float dm[4];
 #pragma unroll
@@ -690,6 +699,21 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
 #if RFG_INT_SKIP
       if (!__any_sync(0xffffffffu, upd)) continue;  // no lane updates this voxel slot
 #endif
+#if RFG_INT_V2
+      const float oldF = sdf_to_logical_alu(vox_sdf(w0));
+      const float newF = smin(1.f, div_fast(eta, mu, rMu));
+      const float fw = u23_to_float((uint32_t)oldW);
+      const float num = fw * oldF + newF;
+      const float den = fw + 1.f;
+      const float merged = div_fast(num, den, s_rcpTab[oldW]);  // == div_rcp(oldW + 1)
+      const float cl = fminf(fmaxf(merged, -1.f), 1.f) * (float)kSdfOne;
+      const int sdfI = __float2int_rz(__fadd_rz(cl, __uint_as_float((__float_as_uint(cl) & 0x80000000u) | 0x3F000000u)));
+      const uint32_t w1 = ((uint32_t)sdfI & 0xFFFFu) | ((uint32_t)min(oldW + 1, maxW) << 16);
+      if (kWindowKnown) {  // window, depths and mu proven (k_integrate_rgbd)
+        wd[i] = upd ? w1 : w0;
+        continue;
+      }
+#else
       const float oldF = sdf_to_logical(vox_sdf(w0));
       const float newF = smin(1.f, div_fast(eta, mu, rMu));
       const float fw = (float)oldW;
@@ -697,13 +721,18 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
       const float den = fw + 1.f;
       const float merged = div_fast(num, den, div_rcp(den));
       const uint32_t w1 = vox_pack(sdf_from_logical(merged), min(oldW + 1, maxW));
+#endif
       // (a voxel whose projection left the window may also have a tiny eta:
       // its update is redone exactly too, as in integrate_block_depth)
       const bool slowK = upd && !(muOk && fabsf(eta) <= 0x1p40f && !(slow & (1u << i)));
       wd[i] = (upd && !slowK) ? w1 : w0;
       redo |= slowK ? (1u << i) : 0u;
     }
+#if RFG_INT_V2
+    if (!kWindowKnown && __any_sync(0xffffffffu, redo != 0u)) {
+#else
     if (__any_sync(0xffffffffu, redo != 0u)) {
+#endif
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (redo & (1u << i)) wd[i] = update_exact(wd[i], dm[i] - zc[i], mu, maxW);
@@ -751,6 +780,13 @@ __global__ void __launch_bounds__(256, RFG_RGBD_MINB) k_integrate_rgbd(DevMap m,
   const float rMu = div_rcp(mu);
   const bool capW = fa.stopAtMaxW != 0;
   const int maxW = fa.maxW;
+#if RFG_INT_V2
+  const bool frameKnown = muOk && fa.depthBounded;  // see k_integrate_depth
+  s_rcpTab[threadIdx.x] = div_rcp((float)(threadIdx.x + 1));  // blockDim.x == 256
+  __syncthreads();
+#else
+  const bool frameKnown = true;
+#endif
   for (int b = gw; b < nVis; b += nw) {
     const int idx = m.visibleList[b];
     const int4 e = ld_entry(m.entries, idx);
@@ -763,7 +799,7 @@ __global__ void __launch_bounds__(256, RFG_RGBD_MINB) k_integrate_rgbd(DevMap m,
 #else
     if (kSameCamera) {
 #endif
-      if (block_window_known(lane, ox, oy, oz, pose, fa))
+      if (frameKnown && block_window_known(lane, ox, oy, oz, pose, fa))
         integrate_block_rgbd_same<true>(blk, cblk, lane, ox, oy, oz, pose, fa, ca, depth, wLim, hLim, mu, muOk, rMu,
                                         capW, maxW);
       else
