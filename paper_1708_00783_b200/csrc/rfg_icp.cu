@@ -41,6 +41,10 @@ constexpr int kIcpStats = 12;  // TrackerIterationSummary (include/rfg.h)
 // fixed-point scale (log2) per sum; 0 = plain integer count (rfo.c:kIcpShift)
 __host__ __device__ constexpr int icp_shift(int k) { return k < 21 ? 32 : (k < 27 ? 38 : (k == 28 || k == 30 ? 0 : 44)); }
 
+#ifndef RFG_ICP_SOLVE_PRELOAD
+#define RFG_ICP_SOLVE_PRELOAD 1  // the solve's 28 inputs loaded into registers before the factorisation
+#endif
+
 // Device tracking state (rfg_map::icpOut).
 struct IcpState {
   double c2w[12];                 // current camera->world estimate (row-major 3x4)
@@ -128,7 +132,13 @@ __device__ void c2w_to_float(const double* c, float* f) {
 
 // rfo.c:se3_series — sin(x)/x, (1 - cos x)/x^2, (x - sin x)/x^3 for t = x^2 < 1,
 // as many Taylor terms as t needs (the same tiers as the oracle)
-__device__ __forceinline__ void se3_series(double t, double& a, double& b, double& c) {
+// (returned by value: the coefficients stay in registers — through reference
+// parameters across the noinline call they went through local memory)
+struct Se3C {
+  double a, b, c;
+};
+__device__ __forceinline__ Se3C se3_series(double t) {
+  double a, b, c;
   if (t < 0x1p-40) {
     a = 1.0 - t * (1.0 / 6.0);
     b = 0.5 * (1.0 - t * (1.0 / 12.0));
@@ -155,10 +165,11 @@ __device__ __forceinline__ void se3_series(double t, double& a, double& b, doubl
          (1.0 - t * (1.0 / 110.0) * (1.0 - t * (1.0 / 156.0) * (1.0 - t * (1.0 / 210.0) * (1.0 - t * (1.0 / 272.0) *
          (1.0 - t * (1.0 / 342.0) * (1.0 - t * (1.0 / 420.0))))))))));
   }
+  return Se3C{a, b, c};
 }
 
 // rfo.c:se3_coeffs — the series below 1 rad, else halving + double angles
-__device__ __noinline__ void se3_coeffs_large(double th2, double& a, double& b, double& c) {
+__device__ __noinline__ Se3C se3_coeffs_large(double th2) {
   const double theta = sqrt(th2);
   double h = theta;
   int k = 0;
@@ -166,23 +177,17 @@ __device__ __noinline__ void se3_coeffs_large(double th2, double& a, double& b, 
     h *= 0.5;
     ++k;
   }
-  double sa, sb, sc;
-  se3_series(h * h, sa, sb, sc);
-  double s = h * sa, co = 1.0 - (h * h) * sb;
+  const Se3C ser = se3_series(h * h);
+  double s = h * ser.a, co = 1.0 - (h * h) * ser.b;
   for (int i = 0; i < k; ++i) {
     const double s2 = 2.0 * s * co;
     co = 1.0 - 2.0 * s * s;
     s = s2;
   }
-  a = s / theta;
-  b = (1.0 - co) / th2;
-  c = (theta - s) / (theta * th2);
+  return Se3C{s / theta, (1.0 - co) / th2, (theta - s) / (theta * th2)};
 }
-__device__ __forceinline__ void se3_coeffs(double th2, double& a, double& b, double& c) {
-  if (th2 < 1.0)
-    se3_series(th2, a, b, c);
-  else
-    se3_coeffs_large(th2, a, b, c);
+__device__ __forceinline__ Se3C se3_coeffs(double th2) {
+  return th2 < 1.0 ? se3_series(th2) : se3_coeffs_large(th2);
 }
 
 // rfo.c:rfo_solve6 — LDL^T of H (no square roots), det(H / n) = prod D_j (1/n),
@@ -194,7 +199,19 @@ __device__ __forceinline__ void se3_coeffs(double th2, double& a, double& b, dou
 __host__ __device__ constexpr int sym6(int a, int b) {
   return a <= b ? a * 6 - a * (a - 1) / 2 + (b - a) : b * 6 - b * (b - 1) / 2 + (a - b);
 }
-__device__ __forceinline__ int solve6(const double* sums, double* x, double* detOut) {
+__device__ __forceinline__ int solve6(const double* sumsIn, double* x, double* detOut) {
+#if RFG_ICP_SOLVE_PRELOAD
+  // the 28 inputs into registers up front: the reciprocals' slow-path
+  // branches would otherwise keep each column's shared-memory loads behind
+  // the previous column's reciprocal
+  double sums[29];
+#pragma unroll
+  for (int k = 0; k < 29; ++k) sums[k] = sumsIn[k];
+#pragma unroll
+  for (int k = 0; k < 29; ++k) asm volatile("" ::"d"(sums[k]));
+#else
+  const double* sums = sumsIn;
+#endif
   const double n = sums[28];
   double L[36];
   double D[6], inv[6];
@@ -287,8 +304,8 @@ __device__ void gn_step(GnShared& g, int level, int minCount) {
   const double W[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
   double WW[9];
   matmul3d(W, W, WW);
-  double ca, cb, cc;
-  se3_coeffs(th2, ca, cb, cc);
+  const Se3C co = se3_coeffs(th2);
+  const double ca = co.a, cb = co.b, cc = co.c;
   double ER[9], V[9], Et[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
