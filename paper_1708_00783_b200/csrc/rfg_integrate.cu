@@ -246,7 +246,7 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
       // lround (half away from zero) of the clamped value * 32767: the sum
       // with +-0.5 rounded toward zero, then truncated (F2I.TRUNC)
       const float cl = fminf(fmaxf(merged, -1.f), 1.f) * (float)kSdfOne;
-      const int sdfI = __float2int_rz(__fadd_rz(cl, __uint_as_float((__float_as_uint(cl) & 0x80000000u) | 0x3F000000u)));
+      const int sdfI = lround_haz_f2i(cl);
       const uint32_t w1 = ((uint32_t)sdfI & 0xFFFFu) | ((uint32_t)min(oldW + 1, maxW) << 16);
 #else
       const uint32_t w1 = vox_pack(sdf_from_logical_alu(merged), min(oldW + 1, maxW));
@@ -707,7 +707,7 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
       const float den = fw + 1.f;
       const float merged = div_fast(num, den, s_rcpTab[oldW]);  // == div_rcp(oldW + 1)
       const float cl = fminf(fmaxf(merged, -1.f), 1.f) * (float)kSdfOne;
-      const int sdfI = __float2int_rz(__fadd_rz(cl, __uint_as_float((__float_as_uint(cl) & 0x80000000u) | 0x3F000000u)));
+      const int sdfI = lround_haz_f2i(cl);
       const uint32_t w1 = ((uint32_t)sdfI & 0xFFFFu) | ((uint32_t)min(oldW + 1, maxW) << 16);
       if (kWindowKnown) {  // window, depths and mu proven (k_integrate_rgbd)
         wd[i] = upd ? w1 : w0;

@@ -7,6 +7,9 @@
 #ifndef RFG_RC_ALU
 #define RFG_RC_ALU 1  // the march's conversions on the FMA/ALU pipes (0: XU conversions)
 #endif
+#ifndef RFG_RC_F2I
+#define RFG_RC_F2I 0  // 1: the nearest read's roundings as RZ add + F2I.TRUNC (measured slower)
+#endif
 #ifndef RFG_RC_ORDER
 #define RFG_RC_ORDER 1  // the frame pipeline's raycast CTAs take the previous frame's heaviest tiles first
 #endif
@@ -318,7 +321,9 @@ struct FieldReader {
   }
   // readSdfNearest (voxel_block_map.cpp:178-185)
   __device__ __forceinline__ float nearest(f3 p, bool& ok) {
-#if RFG_RC_ALU
+#if RFG_RC_F2I
+    const int vx = lround_haz_f2i(p.x), vy = lround_haz_f2i(p.y), vz = lround_haz_f2i(p.z);
+#elif RFG_RC_ALU
     const int vx = lround_haz_alu(p.x), vy = lround_haz_alu(p.y), vz = lround_haz_alu(p.z);
 #else
     const int vx = lround_haz(p.x), vy = lround_haz(p.y), vz = lround_haz(p.z);
@@ -618,6 +623,21 @@ __device__ __forceinline__ void raycast_and_normal(const DevMap& m, const FrameA
     const f3 dw = rot_apply(c2w.R, dirCam);
     const f3 dirW{dw.x / norm, dw.y / norm, dw.z / norm};
     isHit = cast_ray(field, origin, dirW, r.x * norm, r.y * norm, fa.mu, fa.voxelSize, &hit);
+#ifdef RFG_RC_REMARCH
+    // debug experiment: a long ray marches again with its blocks now warm in
+    // L1 / L2; ctr[10] = that second march's ns, ctr[11] = its steps
+    if (ctr && field.nSteps >= 48) {
+      unsigned long long ta, tb;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
+      FieldReader f2{m.entries, RFG_FIELD_PLANE(m), m.buckets};
+      f2.cache.reset();
+      f3 h2;
+      const bool again = cast_ray(f2, origin, dirW, r.x * norm, r.y * norm, fa.mu, fa.voxelSize, &h2);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb));
+      ctr[10] = (tb - ta) + (again ? 0ull : 0ull);
+      ctr[11] = (unsigned long long)f2.nSteps;
+    }
+#endif
     if (isHit) {
       rc = make_float4(hit.x, hit.y, hit.z, 1.f);
       pt = make_float4(hit.x * fa.voxelSize, hit.y * fa.voxelSize, hit.z * fa.voxelSize, 1.f);
@@ -709,6 +729,8 @@ __global__ void __launch_bounds__(kRangeTile* kRangeTile, RFG_RC_TILES_MINB) k_r
     rec[9] = sum;
     rec[10] = t0;
     for (int k = 0; k < 3; ++k) rec[11 + k] = ctr[5 + k];  // steps 0, 16, 32
+    rec[14] = ctr[10];
+    rec[15] = ctr[11];
   }
 #else
   int steps = 0;

@@ -1,7 +1,7 @@
 // Exhaustive check of the ALU-pipe conversions of rfg_common.cuh against the
 // hardware conversions: u23_to_float (every v < 2^23), s16_to_float (every
-// int16), trunc_pos_to_int (every float in [0, 2^23)) and lround_haz_alu
-// (every float with |v| < 2^22, against lround_haz / lroundf).
+// int16), trunc_pos_to_int (every float in [0, 2^23)) and lround_haz_alu /
+// lround_haz_f2i (every float with |v| < 2^22, against lround_haz / lroundf).
 #include <cstdio>
 #include "../../paper_1708_00783_b200/csrc/rfg_common.cuh"
 
@@ -25,7 +25,8 @@ __global__ void k_float(unsigned long long* bad) {
       for (int sgn = 0; sgn < 2; ++sgn) {
         const float v = sgn ? -t : t;
         const int ref = (int)lroundf(v);
-        if (rfg::lround_haz_alu(v) != ref || rfg::lround_haz(v) != ref) atomicAdd(&bad[3], 1ull);
+        if (rfg::lround_haz_alu(v) != ref || rfg::lround_haz(v) != ref || rfg::lround_haz_f2i(v) != ref)
+          atomicAdd(&bad[3], 1ull);
       }
     }
   }

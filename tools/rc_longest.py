@@ -46,7 +46,7 @@ for f in range(100):
     rows.append((f, span, lw[0] / 1e3, (lw[1] - k0) / 1e3, *[int(v) for v in lw[3:8]], int(r[:, 8].max()),
                  r[:, 9].sum() / (len(r) * 32) / 1e3, int(tail.sum()), (lw[1] - lw[10]) / 1e3))
     seg = [(lw[12 + k] - lw[11 + k]) / 16.0 if lw[12 + k] else 0.0 for k in range(2)]
-    segs.append([(lw[11] - k0) / 1e3] + seg)
+    segs.append([(lw[11] - k0) / 1e3] + seg + [lw[14] / max(lw[15], 1) if lw[15] else 0.0])
 print("frame span_us longest_us start_us steps lookups chain_loads nearest trilinear | max_steps mean_ray_us "
       "tail_warps its_range_us ns/step")
 for r in rows[5:]:
@@ -61,3 +61,5 @@ print(f"mean over frames 5..99: span {a[:, 0].mean():.1f} us, longest ray {a[:, 
 sg = np.array(segs[5:], np.float64)
 print("longest ray: march starts at %.1f us; ns per step over steps 0-15 / 16-31: %s" %
       (sg[:, 0].mean(), " / ".join(f"{v:.0f}" for v in sg[:, 1:3].mean(axis=0))))
+if sg[:, 3].any():  # RFG_RC_REMARCH build: the same ray marched again right after, its blocks warm
+    print("  marched again with its blocks warm: %.0f ns per step" % sg[:, 3][sg[:, 3] > 0].mean())
