@@ -320,16 +320,17 @@ int rfg_pipeline_process_raw(rfg_pipeline* p, const uint16_t* raw_dev, const flo
  * is re-pointed at raw_dev) instead of being copied. */
 int rfg_pipeline_process_raw_stream(rfg_pipeline* p, const uint16_t* raw_dev, const float pose34[12],
                                     void* producer_cuda_stream);
-/* Enqueue one frame from HOST raw depth.  A pageable frame is copied H2D
- * (its buffer may be reused once the call returns); a pinned (cudaHostAlloc / cudaHostRegister) frame is
- * read in place over PCIe by the captured frame graph's view kernel, so —
- * as with any asynchronous copy from pinned memory — the caller keeps the
- * buffer unchanged until rfg_pipeline_result returns. */
+/* Enqueue one frame from HOST raw depth, copied H2D on the pipeline's
+ * stream.  A pageable frame's buffer may be reused once the call returns; a
+ * pinned (cudaHostAlloc / cudaHostRegister) frame is copied asynchronously,
+ * so — as with any asynchronous copy from pinned memory — the caller keeps
+ * the buffer unchanged until rfg_pipeline_result returns. */
 int rfg_pipeline_process_host(rfg_pipeline* p, const uint16_t* raw_host, const float* pose34);
 /* RGB-D frames of a colour pipeline (cfg.colour = 1): depth as in
  * rfg_pipeline_process_raw_stream / _host plus the RGB8 image (width x height
- * x 3 bytes, intr_rgb's size), read in place by the captured graph's colour
- * packing kernel (device, or pinned host memory over PCIe). */
+ * x 3 bytes, intr_rgb's size): a device image is read in place by the
+ * captured graph's colour packing kernel, a host image is copied H2D with
+ * the depth (pinned: asynchronously, kept unchanged until the result). */
 int rfg_pipeline_process_rgbd_stream(rfg_pipeline* p, const uint16_t* raw_dev, const uint8_t* rgb_dev,
                                      const float pose34[12], void* producer_cuda_stream);
 int rfg_pipeline_process_rgbd_host(rfg_pipeline* p, const uint16_t* raw_host, const uint8_t* rgb_host,
@@ -339,7 +340,9 @@ int rfg_pipeline_process_rgbd_host(rfg_pipeline* p, const uint16_t* raw_host, co
  * the GPU view stage decodes it (no host pass over the pixels). */
 int rfg_pipeline_process_pgm(rfg_pipeline* p, const char* path, const float pose34[12]);
 /* Read back the last frame's stats, pose and tracker summary (RFG_ICP_STATS
- * doubles, see rfg_icp_track; synchronises). */
+ * doubles, see rfg_icp_track): the frame graph itself writes them into mapped
+ * pinned host memory (the map state as the frame's allocation left it), so
+ * this only synchronises the pipeline's stream. */
 int rfg_pipeline_result(rfg_pipeline* p, rfg_alloc_stats* stats, float pose_out34[12],
                         double icp_stats[RFG_ICP_STATS]);
 /* Device pointers of the pipeline's buffers (for parity checks). */
