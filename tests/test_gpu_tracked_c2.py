@@ -93,8 +93,11 @@ def test_tracked_c2_sequence_matches_oracle():
             eg, eo = m.entries(), o.entries()
             assert np.array_equal(eg, eo), f"frame {f}: hash entries differ"
             ptrs = eo[eo[:, 4] >= 0, 4]
-            assert np.array_equal(m.blocks(ptrs), o.blocks(ptrs)), f"frame {f}: voxel blocks differ"
+            bg = m.blocks(ptrs)
+            assert np.array_equal(bg, o.blocks(ptrs)), f"frame {f}: voxel blocks differ"
             assert tuple(m.free_counts()) == tuple(o.free_counts()), f"frame {f}: free stacks differ"
+            if f == N_FRAMES - 1:  # voxels seen in every frame have reached maxW (fusion.cpp:26-31)
+                assert int(bg[..., 2].max()) == PARAMS_C1["maxW"]
         prev = (pts_o, nrm_o, pose_o.copy())
 
     # and the run tracks the ground truth (frame-to-model, no loop closure)
