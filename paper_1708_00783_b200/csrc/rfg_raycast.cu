@@ -7,6 +7,9 @@
 #ifndef RFG_RC_ALU
 #define RFG_RC_ALU 1  // the march's conversions on the FMA/ALU pipes (0: XU conversions)
 #endif
+#ifndef RFG_RC_MERGE
+#define RFG_RC_MERGE 1  // coarse residency tests and fine reads share one block resolution per step
+#endif
 #ifndef RFG_RC_F2I
 #define RFG_RC_F2I 0  // 1: the nearest read's roundings as RZ add + F2I.TRUNC (measured slower)
 #endif
@@ -339,6 +342,12 @@ struct FieldReader {
     return sdf_to_logical(field_sdf(w));
 #endif
   }
+  // the sdf of voxel (vx, vy, vz) of block ptr (nearest's load and conversion)
+  __device__ __forceinline__ float read_voxel(int ptr, int vx, int vy, int vz) {
+    RC_CNT(nNear);
+    const FieldVoxel w = __ldg(vba + (size_t)ptr * kBlock3 + ((vx & 7) | ((vy & 7) << 3) | ((vz & 7) << 6)));
+    return sdf_to_logical_alu(field_sdf(w));
+  }
   // readSdfWeightTrilinear (voxel_block_map.cpp:130-156).  Any missing
   // corner invalidates the read, so the corner order only matters for the
   // weighted sum, which is accumulated in the reference's k order.  Each
@@ -436,6 +445,37 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
 #ifdef RFG_RC_STATS
     ++nSteps;
 #endif
+#if RFG_RC_MERGE
+    // the coarse step's residency test and the fine step's nearest read share
+    // one block resolution (one lookup pass for a warp whose lanes are in
+    // both states): floor-based block for COARSE (MapField::resident),
+    // round-based for the reads
+    bool ok = false;
+    float sdf = 1.f;
+    {
+      const f3 p = at_t(oV, dV, t);
+      const bool coarse = state == COARSE;
+      const int vx = lround_haz_alu(p.x), vy = lround_haz_alu(p.y), vz = lround_haz_alu(p.z);
+      const int bx = coarse ? (((int)floorf(p.x)) >> 3) : (vx >> 3);
+      const int by = coarse ? (((int)floorf(p.y)) >> 3) : (vy >> 3);
+      const int bz = coarse ? (((int)floorf(p.z)) >> 3) : (vz >> 3);
+      const int ptr = field.ptr_of(bx, by, bz);
+      if (coarse) {
+#ifdef RFG_RC_STATS
+        ++nCoarse;
+#endif
+        if (ptr >= 0) {
+          state = FINE;
+          t = smax(tMinM, t - coarseStep);
+        } else {
+          t += coarseStep;
+        }
+        continue;
+      }
+      ok = ptr >= 0;
+      if (ok) sdf = field.read_voxel(ptr, vx, vy, vz);
+    }
+#else
     if (state == COARSE) {
 #ifdef RFG_RC_STATS
       ++nCoarse;
@@ -451,6 +491,7 @@ __device__ bool cast_ray(FieldReader& field, f3 originM, f3 dirUnit, float tMinM
     // reads
     bool ok = false;
     float sdf = field.nearest(at_t(oV, dV, t), ok);
+#endif
     if (ok && sdf <= 0.1f) {
       bool okTri = false;
       const float tri = field.trilinear(at_t(oV, dV, t), okTri);
