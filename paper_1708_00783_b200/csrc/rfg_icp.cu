@@ -35,7 +35,13 @@ namespace cg = cooperative_groups;
 
 namespace rfg {
 
-constexpr int kIcpThreads = 512;  // 16 warps: more would cap the registers at 96 (5 warps per SM sub-partition)
+#ifndef RFG_ICP_THREADS
+#define RFG_ICP_THREADS 512
+#endif
+#ifndef RFG_ICP_CPS
+#define RFG_ICP_CPS 1  // resident tracker CTAs per SM
+#endif
+constexpr int kIcpThreads = RFG_ICP_THREADS;  // 16 warps: more would cap the registers at 96 (5 warps per SM sub-partition)
 constexpr int kIcpSums = 31;   // H upper 21, g 6, sum r^2, inliers, sum |r|, valid pixels
 constexpr int kIcpStats = 12;  // TrackerIterationSummary (include/rfg.h)
 // fixed-point scale (log2) per sum; 0 = plain integer count (rfo.c:kIcpShift)
@@ -667,7 +673,7 @@ __device__ __forceinline__ void icp_publish(IcpState* st, const GnShared& g, con
 }
 
 // Single evaluation / single level on the state in `st` (rfg_icp_reduce).
-__global__ void __launch_bounds__(kIcpThreads, 1) k_icp_level(IcpState* st, IcpLevelArgs a) {
+__global__ void __launch_bounds__(kIcpThreads, RFG_ICP_CPS) k_icp_level(IcpState* st, IcpLevelArgs a) {
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
@@ -749,7 +755,7 @@ __device__ __forceinline__ void icp_seed_from_state(IcpState* st, GnShared& g) {
 // (19,200 at 640x480), so 16 SMs hold it; its iterations are the most
 // numerous of the track.  k_icp_track then continues from the state.
 constexpr int kIcpCluster = 16;
-__global__ void __launch_bounds__(kIcpThreads, 1) k_icp_coarse(IcpState* st, IcpTrackArgs ta) {
+__global__ void __launch_bounds__(kIcpThreads, RFG_ICP_CPS) k_icp_coarse(IcpState* st, IcpTrackArgs ta) {
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
@@ -813,7 +819,7 @@ __global__ void __launch_bounds__(kIcpThreads, 1) k_icp_coarse(IcpState* st, Icp
   cl.sync();  // rank 0's shared memory stays alive until every CTA has read it
 }
 
-__global__ void __launch_bounds__(kIcpThreads, 1) k_icp_track(IcpState* st, IcpTrackArgs ta) {
+__global__ void __launch_bounds__(kIcpThreads, RFG_ICP_CPS) k_icp_track(IcpState* st, IcpTrackArgs ta) {
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
@@ -890,7 +896,7 @@ static int icp_grid(int n) {
     if (dev < 64) fits[dev] = f;
   }
   if (f < 0) return 0;
-  const int sms = current_sm_count();
+  const int sms = current_sm_count() * RFG_ICP_CPS;
   // every SM takes a part of every level (at least a warp of pixels per CTA):
   // spreading a coarse level over all SMs leaves fewer busy warps per SM for
   // the accumulation and the CTA reduction
