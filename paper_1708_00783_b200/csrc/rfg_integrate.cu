@@ -69,6 +69,9 @@ __device__ __forceinline__ uint32_t update_exact(uint32_t wd, float eta, float m
 #ifndef RFG_INT_V2
 #define RFG_INT_V2 1  // fewer ALU-pipe instructions per voxel (folded pixel index, F2I lround, sentinel depth)
 #endif
+#ifndef RFG_INT_RCP_HOIST
+#define RFG_INT_RCP_HOIST 1  // a group's eight 1/(w+1) table reads before its per-slot skips
+#endif
 #ifndef RFG_INT_RCP_INLINE
 #define RFG_INT_RCP_INLINE 0  // 1/(w+1) by MUFU + 2 FFMA per voxel instead of the shared table
 #endif
@@ -212,6 +215,12 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
     for (int k = 0; k < 4 * kQG; ++k) dm[k] = pix[k] >= 0 ? __ldg(depth + pix[k]) : -1.f;
     // ---- update (update_voxel_depth, fusion.cpp:9-36)
     unsigned redo = 0u;
+#if RFG_INT_V2 && RFG_INT_RCP_HOIST
+    // the group's 1/(w+1) table reads in one block (one shared-window base)
+    float rwt[4 * kQG];
+#pragma unroll
+    for (int k = 0; k < 4 * kQG; ++k) rwt[k] = s_rcpTab[vox_w(wd[k])];
+#endif
 #pragma unroll
     for (int k = 0; k < 4 * kQG; ++k) {
       const uint32_t w0 = wd[k];
@@ -235,6 +244,9 @@ __device__ __forceinline__ void integrate_block_depth(const uint4* src, uint4* b
       const float den = fw + 1.f;  // == (float)(oldW + 1): small integers are exact
 #if RFG_INT_V2 && RFG_INT_RCP_INLINE
       const float merged = div_fast(num, den, div_rcp(den));
+      (void)rcpTab;
+#elif RFG_INT_V2 && RFG_INT_RCP_HOIST
+      const float merged = div_fast(num, den, rwt[k]);  // == div_rcp(oldW + 1)
       (void)rcpTab;
 #elif RFG_INT_V2
       const float merged = div_fast(num, den, s_rcpTab[oldW]);  // == div_rcp(oldW + 1)
