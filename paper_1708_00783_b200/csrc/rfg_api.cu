@@ -186,6 +186,10 @@ int ensure_range_scratch(rfg_map* m, int width, int height) {
 
 }  // namespace rfg
 
+#ifndef RFG_L2_PERSIST
+#define RFG_L2_PERSIST 1  // the map's hash entries as a persisting L2 access-policy window of the pipeline
+#endif
+
 using namespace rfg;
 
 namespace {
@@ -1045,6 +1049,31 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
   }
   m->stream = p->stream;
   icp_warmup();
+#if RFG_L2_PERSIST
+  // L2 residency control: the map's hash entries (every stage's lookups and
+  // probes) as a persisting access-policy window on the pipeline's stream
+  // (captured into the frame graph's kernel nodes), within the device's
+  // persisting set-aside
+  {
+    int maxPersist = 0, maxWindow = 0;
+    cudaDeviceGetAttribute(&maxPersist, cudaDevAttrMaxPersistingL2CacheSize, m->device);
+    cudaDeviceGetAttribute(&maxWindow, cudaDevAttrMaxAccessPolicyWindowSize, m->device);
+    const size_t bytes = (size_t)m->d.total * sizeof(int4);
+    if (maxPersist > 0 && maxWindow > 0) {
+      const size_t setAside = bytes < (size_t)maxPersist ? bytes : (size_t)maxPersist;
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setAside);
+      cudaStreamAttrValue av{};
+      av.accessPolicyWindow.base_ptr = m->d.entries;
+      av.accessPolicyWindow.num_bytes = bytes < (size_t)maxWindow ? bytes : (size_t)maxWindow;
+      av.accessPolicyWindow.hitRatio = (float)setAside / (float)av.accessPolicyWindow.num_bytes;
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &av);
+      cudaStreamSetAttribute(p->side, cudaStreamAttributeAccessPolicyWindow, &av);
+    }
+    cudaGetLastError();
+  }
+#endif
   if (ensure_range_scratch(m, cfg->intr.width, cfg->intr.height) != RFG_OK) {
     rfg_pipeline_destroy(p);
     return RFG_ENOMEM;
@@ -1062,6 +1091,9 @@ int rfg_pipeline_destroy(rfg_pipeline* p) {
   DeviceGuard dg_(p && p->map ? p->map->device : -1);
   if (!p) return RFG_OK;
   if (p->stream) cudaStreamSynchronize(p->stream);
+#if RFG_L2_PERSIST
+  cudaCtxResetPersistingL2Cache();  // the window's lines back to normal
+#endif
   for (int i = 0; i < 2; ++i)
     if (p->exec[i]) cudaGraphExecDestroy(p->exec[i]);
   for (int i = 0; i < 2; ++i)
