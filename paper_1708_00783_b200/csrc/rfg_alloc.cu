@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(256, RFG_ALLOC_MINB) k_alloc_stage1(DevMap m, 
     const i3 cell{(int)(int16_t)(c & 0xFFFFu), (int)(int16_t)((c >> 16) & 0xFFFFu), (int)(int16_t)((c >> 32) & 0xFFFFu)};
     mark_or_request(m, cell, sKey[i]);
   }
+  pdl_trigger();
 }
 
 // Recompute the block a request key refers to (pixel, DDA ordinal).
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int2* counts, int2* prefix,
 
 // Serve requests in ascending index order with serial-equivalent ranks.
 __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
+  pdl_wait();
   const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
   const uint4 k4 = *reinterpret_cast<const uint4*>(m.reqKey + base);
   const uint32_t keys[4] = {k4.x, k4.y, k4.z, k4.w};
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const flo
   }
   if (succ) atomicAdd(&m.state->succ, succ);
   if (succ2) atomicAdd(&m.state->succType2, succ2);
+  pdl_trigger();
 }
 
 // --------------------------------------------------------------- stage 3
@@ -426,6 +429,7 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
   __shared__ int queue[kTile];
   __shared__ int vis[kTile];
   __shared__ int nq, nvis, listBase;
+  pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // finalise stage 2 (all k_req_assign CTAs have completed)
     MapState* st = m.state;
@@ -481,6 +485,7 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nvis; i += kTileThreads) m.visibleList[listBase + i] = vis[i];
+  pdl_trigger();
 }
 
 // Per-tile count of visible entries (visibility bytes), for regenerating the
@@ -515,8 +520,9 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
 cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s) {
   dim3 g1((fa.w + 31) / 32, (fa.h + kStage1Rows - 1) / kStage1Rows);
   k_alloc_stage1<<<g1, 256, 0, s>>>(m, depth, fa);
-  k_req_assign<<<m.nTiles, kTileThreads, 0, s>>>(m, depth, fa);
-  k_vis_count<<<m.nTiles, kTileThreads, 0, s>>>(m, fa);
+  cudaError_t e = launch_pdl(k_req_assign, dim3(m.nTiles), dim3(kTileThreads), s, m, depth, fa);
+  if (e != cudaSuccess) return e;
+  if ((e = launch_pdl(k_vis_count, dim3(m.nTiles), dim3(kTileThreads), s, m, fa)) != cudaSuccess) return e;
   count_launch(3);
   return cudaGetLastError();
 }

@@ -190,6 +190,12 @@ int ensure_range_scratch(rfg_map* m, int width, int height) {
 #define RFG_L2_PERSIST 1  // the map's hash entries as a persisting L2 access-policy window of the pipeline
 #endif
 
+#ifndef RFG_PDL
+#define RFG_PDL 1  // programmatic dependent launches in the frame graph's chain
+#endif
+namespace rfg {
+thread_local bool g_pdl = false;
+}
 using namespace rfg;
 
 namespace {
@@ -802,6 +808,12 @@ namespace {
 cudaError_t launch_frame_result(rfg_pipeline* p, cudaStream_t s);
 
 cudaError_t enqueue_frame(rfg_pipeline* p, bool track) {
+  // the chain after the tracker with programmatic dependent launches
+  // (not in profile mode: its event nodes sit between the kernels)
+  struct PdlScope {
+    explicit PdlScope(bool on) { g_pdl = on; }
+    ~PdlScope() { g_pdl = false; }
+  } pdlScope_(RFG_PDL != 0 && p->cfg.profile == 0);
   rfg_map* m = p->map;
   const rfg_pipeline_config& c = p->cfg;
   cudaStream_t s = p->stream;

@@ -326,6 +326,7 @@ __device__ __forceinline__ bool block_window_known(int lane, int ox, int oy, int
 
 __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m, const float* __restrict__ depth,
                                                                        FrameArgs fa) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warpsPerCta = blockDim.x >> 5;
   const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(256, RFG_INT_MINB) k_integrate_depth(DevMap m,
       integrate_block_depth<false>(blk, blk, lane, ox, oy, oz, pose, fa, depth, wLim, hLim, mu, muOk, rMu, capW,
                                    maxW, rcpTab);
   }
+  pdl_trigger();
 }
 
 // ---------------------------------------- depth-only, TMA-prefetched rows
@@ -778,6 +780,7 @@ __device__ __forceinline__ void integrate_block_rgbd_same(uint4* blk, uint4* cbl
 template <bool kSameCamera>
 __global__ void __launch_bounds__(256, RFG_RGBD_MINB) k_integrate_rgbd(DevMap m, const float* __restrict__ depth, FrameArgs fa,
                                                            ColourArgs ca) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warpsPerCta = blockDim.x >> 5;
   const int gw = blockIdx.x * warpsPerCta + (threadIdx.x >> 5);
@@ -865,6 +868,11 @@ int integrate_grid() {
 
 // Depth-only (rgba == nullptr) or RGB-D integration of the visible blocks.
 // extr34 nullptr = identity extrinsics.
+#define RFG_LAUNCH_CK(call)                 \
+  do {                                      \
+    const cudaError_t e_ = (call);          \
+    if (e_ != cudaSuccess) return e_;       \
+  } while (0)
 cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint32_t* rgba, const FrameArgs& fa,
                              const rfg_intrinsics* intrRgb, const float* extr34, cudaStream_t s) {
   if (rgba) {
@@ -886,14 +894,14 @@ cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint32_t
     ca.sameCamera = ident && ca.rw == fa.w && ca.rh == fa.h && ca.fx == fa.fx && ca.fy == fa.fy && ca.cx == fa.cx &&
                     ca.cy == fa.cy;
     if (ca.sameCamera)
-      k_integrate_rgbd<true><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
+      RFG_LAUNCH_CK(launch_pdl(k_integrate_rgbd<true>, dim3(integrate_grid()), dim3(256), s, m, depth, fa, ca));
     else
-      k_integrate_rgbd<false><<<integrate_grid(), 256, 0, s>>>(m, depth, fa, ca);
+      RFG_LAUNCH_CK(launch_pdl(k_integrate_rgbd<false>, dim3(integrate_grid()), dim3(256), s, m, depth, fa, ca));
   } else {
 #if RFG_INT_TMA
     k_integrate_depth_tma<<<current_sm_count() * RFG_INT_MINB, 256, 0, s>>>(m, depth, fa);
 #else
-    k_integrate_depth<<<integrate_grid(), 256, 0, s>>>(m, depth, fa);
+    RFG_LAUNCH_CK(launch_pdl(k_integrate_depth, dim3(integrate_grid()), dim3(256), s, m, depth, fa));
 #endif
   }
   count_launch();

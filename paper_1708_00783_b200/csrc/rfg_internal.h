@@ -79,6 +79,26 @@ constexpr int kTileThreads = 256;    // 4 consecutive entries per thread
 void set_error(const std::string& msg);
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// Kernel launch with programmatic stream serialisation when the current
+// thread is enqueueing a frame graph (g_pdl, rfg_api.cu:enqueue_frame); a
+// plain launch otherwise.
+extern thread_local bool g_pdl;
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (g_pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // SM count of the current device, cached per device (grid sizes).
 int current_sm_count();

@@ -116,6 +116,7 @@ __device__ void order_tiles(const DevMap& m, int n, int K) {
 }
 
 __global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa, int orderK) {
+  pdl_wait();
   // orderK > 0: CTA 0 (dispatched first) writes the raycast's tile order
   if (orderK > 0 && blockIdx.x == 0) {
     order_tiles(m, m.binTilesX * ((fa.h + kRangeTile - 1) / kRangeTile), orderK);
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(256) k_range_bin(DevMap m, FrameArgs fa, int o
       if (slot < m.binCap) m.bins[(size_t)t * m.binCap + slot] = b;
     }
   }
+  pdl_trigger();
 }
 
 // The expected range (min, max bits) of this thread's pixel of screen tile t
@@ -727,6 +729,7 @@ __global__ void __launch_bounds__(kRangeTile* kRangeTile, RFG_RC_TILES_MINB) k_r
                                                                           float4* raycast, float4* points,
                                                                           float4* normals, int ordered) {
   __shared__ int4 sb[kRangeTile * kRangeTile];
+  pdl_wait();
   // ordered: a 1-D grid over the tiles in this frame's order (order_tiles)
   const int t = ordered ? m.tileOrder[blockIdx.x] : blockIdx.y * m.binTilesX + blockIdx.x;
   const int tileX = ordered ? t % m.binTilesX : blockIdx.x, tileY = ordered ? t / m.binTilesX : blockIdx.y;
@@ -1009,7 +1012,8 @@ cudaError_t launch_range_bin(const DevMap& m, const FrameArgs& fa, cudaStream_t 
   const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
   if (tx != m.binTilesX || ty > m.binTilesY) return cudaErrorInvalidValue;  // scratch sized by ensure_range_scratch
   const int orderK = RFG_RC_ORDER ? current_sm_count() * RFG_RC_ORDER_K : 0;
-  k_range_bin<<<range_grid() + (orderK > 0 ? 1 : 0), 256, 0, s>>>(m, fa, orderK);
+  const cudaError_t e = launch_pdl(k_range_bin, dim3(range_grid() + (orderK > 0 ? 1 : 0)), dim3(256), s, m, fa, orderK);
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }
@@ -1018,7 +1022,11 @@ cudaError_t launch_raycast_tiles(const DevMap& m, const FrameArgs& fa, float2* r
   const int tx = (fa.w + kRangeTile - 1) / kRangeTile, ty = (fa.h + kRangeTile - 1) / kRangeTile;
   if (tx != m.binTilesX || ty > m.binTilesY || !raycast) return cudaErrorInvalidValue;
   if (RFG_RC_ORDER)  // the CTAs take the tiles in the order k_range_bin's extra CTA wrote
-    k_raycast_tiles<<<tx * ty, kRangeTile * kRangeTile, 0, s>>>(m, fa, range, raycast, points, normals, 1);
+  {
+    const cudaError_t e = launch_pdl(k_raycast_tiles, dim3(tx * ty), dim3(kRangeTile * kRangeTile), s, m, fa, range,
+                                     raycast, points, normals, 1);
+    if (e != cudaSuccess) return e;
+  }
   else
     k_raycast_tiles<<<dim3(tx, ty), kRangeTile * kRangeTile, 0, s>>>(m, fa, range, raycast, points, normals, 0);
   count_launch();
