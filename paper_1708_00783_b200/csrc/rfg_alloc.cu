@@ -159,6 +159,7 @@ constexpr int kStage1Rows = 16;
 #endif
 
 __global__ void __launch_bounds__(256, RFG_ALLOC_MINB) k_alloc_stage1(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
+  pdl_wait();  // the pose (the tracker) and the depth
   __shared__ unsigned long long sCell[kCellSlots];  // (x | y << 16 | z << 32 | 1 << 48), 0 = empty
   __shared__ uint32_t sKey[kCellSlots];
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
@@ -519,8 +520,9 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_emit(DevMap m) {
 
 cudaError_t launch_allocate(const DevMap& m, const float* depth, const FrameArgs& fa, cudaStream_t s) {
   dim3 g1((fa.w + 31) / 32, (fa.h + kStage1Rows - 1) / kStage1Rows);
-  k_alloc_stage1<<<g1, 256, 0, s>>>(m, depth, fa);
-  cudaError_t e = launch_pdl(k_req_assign, dim3(m.nTiles), dim3(kTileThreads), s, m, depth, fa);
+  cudaError_t e = launch_pdl(k_alloc_stage1, g1, dim3(256), s, m, depth, fa);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(k_req_assign, dim3(m.nTiles), dim3(kTileThreads), s, m, depth, fa);
   if (e != cudaSuccess) return e;
   if ((e = launch_pdl(k_vis_count, dim3(m.nTiles), dim3(kTileThreads), s, m, fa)) != cudaSuccess) return e;
   count_launch(3);

@@ -823,6 +823,7 @@ __global__ void __launch_bounds__(kIcpThreads, RFG_ICP_CPS) k_icp_track(IcpState
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
+  pdl_wait();  // the depth pyramid (programmatic dependency on the view kernel)
 #ifdef RFG_ICP_PHASES
   const unsigned long long tEntry = gtimer();
 #endif
@@ -879,6 +880,7 @@ __global__ void __launch_bounds__(kIcpThreads, RFG_ICP_CPS) k_icp_track(IcpState
     if (ta.renderPoseOut)
       for (int i = 0; i < 12; ++i) ta.renderPoseOut[i] = st->w2cF[i];
   }
+  pdl_trigger();  // the allocation (programmatic dependent) may launch
 }
 
 // CTAs for a level of n pixels: about one pixel per thread, at most one CTA
@@ -1013,7 +1015,20 @@ cudaError_t launch_icp_track(void* state, const float* depthLevels, int levels, 
   }
   void* args[] = {&stp, &ta};
   count_launch();
-  return cudaLaunchCooperativeKernel((const void*)k_icp_track, dim3(grid), dim3(kIcpThreads), args, 0, s);
+  if (!g_pdl) return cudaLaunchCooperativeKernel((const void*)k_icp_track, dim3(grid), dim3(kIcpThreads), args, 0, s);
+  // a cooperative launch that is also a programmatic dependent of the view kernel
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kIcpThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_icp_track, stp, ta);
 }
 
 __global__ void k_icp_set_c2w(IcpState* st, const float* c2w, const float* renderPose) {

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(256) k_view_pyramid(const uint16_t* __restrict
       out2[(size_t)y * w2 + x] = mean_valid4(l1[2 * ly][2 * lx], l1[2 * ly][2 * lx + 1], l1[2 * ly + 1][2 * lx],
                                             l1[2 * ly + 1][2 * lx + 1]);
   }
+  pdl_trigger();  // the tracker (programmatic dependent) may launch
 }
 
 // bilateral_filter (view.cpp:18-44): 32x8 pixels per CTA, the 36x12 input
