@@ -868,11 +868,6 @@ int integrate_grid() {
 
 // Depth-only (rgba == nullptr) or RGB-D integration of the visible blocks.
 // extr34 nullptr = identity extrinsics.
-#define RFG_LAUNCH_CK(call)                 \
-  do {                                      \
-    const cudaError_t e_ = (call);          \
-    if (e_ != cudaSuccess) return e_;       \
-  } while (0)
 cudaError_t launch_integrate(const DevMap& m, const float* depth, const uint32_t* rgba, const FrameArgs& fa,
                              const rfg_intrinsics* intrRgb, const float* extr34, cudaStream_t s) {
   if (rgba) {
