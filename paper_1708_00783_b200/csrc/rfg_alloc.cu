@@ -329,42 +329,105 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int2* counts, int2* prefix,
 // (The per-tile request counts come from stage 1: mark_or_request counts a
 // slot's first request.)
 
+// Exclusive scan of v over the CTA, with the CTA totals of v and of r.
+template <int NT>
+__device__ __forceinline__ int2 block_scan2_with_sum2(int2 v, int2 r, int2* total, int2* rsum) {
+  __shared__ int4 warpSums[NT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int2 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, inc.x, o);
+    const int b = __shfl_up_sync(0xffffffffu, inc.y, o);
+    if (lane >= o) {
+      inc.x += a;
+      inc.y += b;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r.x += __shfl_xor_sync(0xffffffffu, r.x, o);
+    r.y += __shfl_xor_sync(0xffffffffu, r.y, o);
+  }
+  if (lane == 31) warpSums[wid] = make_int4(inc.x, inc.y, r.x, r.y);
+  __syncthreads();
+  int4 base = make_int4(0, 0, 0, 0), all = make_int4(0, 0, 0, 0);
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    const int4 s = warpSums[w];
+    if (w < wid) {
+      base.x += s.x;
+      base.y += s.y;
+    }
+    all.x += s.x;
+    all.y += s.y;
+    all.z += s.z;
+    all.w += s.w;
+  }
+  *total = make_int2(all.x, all.y);
+  *rsum = make_int2(all.z, all.w);
+  return make_int2(base.x + inc.x - v.x, base.y + inc.y - v.y);
+}
+
 // Serve requests in ascending index order with serial-equivalent ranks.
+// The kernel is a chain of dependent memory round trips, so the loads that
+// do not depend on each other are issued together up front: the tile's keys,
+// its own stage-1 request count (tiles without requests leave at once, with
+// no barrier), the counts of the tiles before it and the free-stack sizes.
+// One scan then gives the in-tile ranks and the prefix; the free-stack pops
+// are loaded before the request's block is re-derived by the DDA.
 __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const float* __restrict__ depth, FrameArgs fa) {
   pdl_wait();
   const uint32_t base = blockIdx.x * kTile + threadIdx.x * 4;
-  const uint4 k4 = *reinterpret_cast<const uint4*>(m.reqKey + base);
+  const bool last = blockIdx.x == gridDim.x - 1;
+  const uint4 k4 = __ldcg(reinterpret_cast<const uint4*>(m.reqKey + base));
+  const int2 own = __ldcg(m.tileCounts + blockIdx.x);  // this tile's requests (stage 1)
+  int nB, nE;
+  asm volatile("ld.global.cg.v2.s32 {%0, %1}, [%2];" : "=r"(nB), "=r"(nE) : "l"(&m.state->snapFreeBlocks));
+  // (volatile loads: issued here, not sunk below the early exit; four tiles
+  // per thread per batch, so a map of up to 1,024 tiles is one round trip)
+  int2 pre = make_int2(0, 0);
+  for (int i0 = threadIdx.x; i0 < (int)blockIdx.x; i0 += 4 * kTileThreads) {
+    int2 c[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * kTileThreads;
+      c[q] = make_int2(0, 0);
+      if (i < (int)blockIdx.x)
+        asm volatile("ld.global.cg.v2.s32 {%0, %1}, [%2];" : "=r"(c[q].x), "=r"(c[q].y) : "l"(m.tileCounts + i));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      pre.x += c[q].x;
+      pre.y += c[q].y;
+    }
+  }
+  // (nB in the exit test keeps its load ahead of the exit, beside the others;
+  // a free-stack size is never negative)
+  if (own.x == 0 && !last && nB >= 0) return;  // (CTA-uniform) most tiles hold no request
+  const Pose camToWorld = pose_inverse(frame_pose(fa));  // (loaded beside the entries, before the scan)
   const uint32_t keys[4] = {k4.x, k4.y, k4.z, k4.w};
   int n = 0, n2 = 0;
   uint32_t isT2 = 0;
+  int keep[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < 4; ++j) {
+    keep[j] = 0;
     if (keys[j]) {
       ++n;
-      if (entry_allocated(ld_entry(m.entries, base + j))) {
+      const int4 e = ld_entry(m.entries, base + j);
+      keep[j] = e.z;
+      if (entry_allocated(e)) {
         ++n2;
         isT2 |= 1u << j;
       }
     }
-  int2 total;
-  const int2 ex = block_exclusive_scan2<kTileThreads>(make_int2(n, n2), &total);
-  const bool last = blockIdx.x == gridDim.x - 1;
-  if (total.x == 0 && !last) return;  // (CTA-uniform) most tiles hold no request
-  // this tile's prefix: the counts of the tiles before it, summed by the CTA
-  // itself (no separate scan launch; integer sums, so order-free)
-  int2 pre = make_int2(0, 0);
-  for (int i = threadIdx.x; i < (int)blockIdx.x; i += kTileThreads) {
-    const int2 c = m.tileCounts[i];
-    pre.x += c.x;
-    pre.y += c.y;
   }
-  int2 tp;
-  block_exclusive_scan2<kTileThreads>(pre, &tp);
+  int2 total, tp;
+  const int2 ex = block_scan2_with_sum2<kTileThreads>(make_int2(n, n2), pre, &total, &tp);
   if (last && threadIdx.x == 0) m.state->nRequests = tp.x + total.x;
   if (n == 0) return;
   int before = tp.x + ex.x, before2 = tp.y + ex.y;
-  const int nB = m.state->snapFreeBlocks, nE = m.state->snapFreeExcess;
-  const Pose camToWorld = pose_inverse(frame_pose(fa));
   int succ = 0, succ2 = 0;
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
@@ -380,16 +443,16 @@ __global__ void __launch_bounds__(kTileThreads) k_req_assign(DevMap m, const flo
     ++before;
     if (t2) ++before2;
     if (!cand || rb >= nB) continue;
+    const int blockPtr = __ldcg(m.freeBlocks + (nB - 1 - rb));
+    const int excessIdx = t2 ? __ldcg(m.freeExcess + (nE - 1 - r2)) : 0;
     const i3 p = decode_request(key, depth, fa, camToWorld);
-    const int blockPtr = m.freeBlocks[nB - 1 - rb];
     if (!t2) {
       // free bucket slot (voxel_block_map.cpp:96-104)
-      const int keep = m.entries[idx].z;
-      m.entries[idx] = make_entry(p.x, p.y, p.z, keep, blockPtr);
+      const int kz = j == 0 ? keep[0] : (j == 1 ? keep[1] : (j == 2 ? keep[2] : keep[3]));
+      m.entries[idx] = make_entry(p.x, p.y, p.z, kz, blockPtr);
       m.marked[idx] = 1;
     } else {
       // chain tail: link a fresh excess slot (voxel_block_map.cpp:84-93)
-      const int excessIdx = m.freeExcess[nE - 1 - r2];
       const int newIdx = (int)m.buckets + excessIdx;
       m.entries[newIdx] = make_entry(p.x, p.y, p.z, 0, blockPtr);
       m.entries[idx].z = excessIdx + 1;
@@ -449,6 +512,7 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
   uint32_t* mp = reinterpret_cast<uint32_t*>(m.marked + base);
   uint32_t* vp = reinterpret_cast<uint32_t*>(m.visibility + base);
   const uint32_t mk = *mp, vk = *vp;
+  const Pose pose = frame_pose(fa);  // (loaded with the bytes, not after the barrier)
   const uint32_t cand = mk | vk;
   if (cand) {
 #pragma unroll
@@ -458,7 +522,6 @@ __global__ void __launch_bounds__(kTileThreads) k_vis_count(DevMap m, FrameArgs 
   }
   if (mk) *mp = 0u;
   __syncthreads();
-  const Pose pose = frame_pose(fa);
   for (int i = threadIdx.x; i < nq; i += kTileThreads) {
     const int idx = queue[i];
     const int4 e = ld_entry(m.entries, idx);
