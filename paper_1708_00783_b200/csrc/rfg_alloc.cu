@@ -125,7 +125,7 @@ __device__ __forceinline__ void mark_or_request(const DevMap& m, i3 cell, uint32
     for (;;) {
       if (e.x == xy && e.y == cell.z) {
         const uint8_t v = e.w >= 0 ? 1 : 2;
-        if (m.marked[idx] != v) m.marked[idx] = v;
+        m.marked[idx] = v;  // idempotent: stored without reading the byte first (the probe ends at the entry)
         return;
       }
       if (e.z < 1) break;
@@ -133,7 +133,8 @@ __device__ __forceinline__ void mark_or_request(const DevMap& m, i3 cell, uint32
       e = ld_entry(m.entries, idx);
     }
   }
-  if (m.reqKey[idx] < key && atomicMax(&m.reqKey[idx], key) == 0u) {
+  // (no read of the slot first: the atomic's return value is the only round trip)
+  if (atomicMax(&m.reqKey[idx], key) == 0u) {
     // the slot's first request this frame: count it for stage 2 (per
     // kTile-entry tile: requests, and those that extend a chain)
     int2* tc = m.tileCounts + idx / kTile;
