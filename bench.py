@@ -655,10 +655,11 @@ def run_b200(args):
         "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": w.wl["desc"]},
-        "run": {"l2": "flushed (256 MiB write) before every timed frame; the map's hash entries "
-                      f"({(w.wl['mapcfg'][0] + w.wl['mapcfg'][1]) * 16 / 2**20:.1f} MiB) are the pipeline's persisting "
+        "run": {"l2": "flushed (256 MiB write) before every timed frame; the map's hash metadata (entries, "
+                      "request keys, mark/visibility bytes: "
+                      f"{(w.wl['mapcfg'][0] + w.wl['mapcfg'][1]) * 22 / 2**20:.1f} MiB) is the pipeline's persisting "
                       "L2 access-policy window (cudaLimitPersistingL2CacheSize set-aside), which the flush does not "
-                      "evict", "graph": True,
+                      "evict; voxel blocks, maps and frames are flushed", "graph": True,
                 "parallelism": f"spatial hash shards x{world}" if sharded else "single GPU",
                 "gpus_active": world, "last_frame_stats": stats.as_array().tolist(),
                 "icp_last": {"iterations": int(icp[0]), "count": int(icp[1]), "per_level": icp[4:7].tolist(),

@@ -187,7 +187,7 @@ int ensure_range_scratch(rfg_map* m, int width, int height) {
 }  // namespace rfg
 
 #ifndef RFG_L2_PERSIST
-#define RFG_L2_PERSIST 1  // the map's hash entries as a persisting L2 access-policy window of the pipeline
+#define RFG_L2_PERSIST 1  // the map's hash metadata as a persisting L2 access-policy window of the pipeline
 #endif
 
 #ifndef RFG_PDL
@@ -273,14 +273,35 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
     }
     return true;
   };
-  bool ok = alloc((void**)&d.entries, padded * sizeof(int4)) &&
-            alloc((void**)&d.vbaDepth, (size_t)d.capacity * kBlock3 * sizeof(uint32_t)) &&
+  // The per-frame hash metadata — entries, request keys, mark and visibility
+  // bytes, tile counts, the map state — in ONE allocation, so that one L2
+  // access-policy window covers everything the allocation stages probe
+  // (RFG_L2_PERSIST); each part 256-B aligned.
+  size_t metaBytes = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = metaBytes;
+    metaBytes += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t oEntries = carve(padded * sizeof(int4)), oReq = carve(padded * sizeof(uint32_t)),
+               oMarked = carve(padded), oVis = carve(padded), oTiles = carve((size_t)d.nTiles * sizeof(int2)),
+               oState = carve(sizeof(MapState));
+  char* meta = nullptr;
+  bool ok = alloc((void**)&meta, metaBytes);
+  if (ok) {
+    d.entries = reinterpret_cast<int4*>(meta + oEntries);
+    d.reqKey = reinterpret_cast<uint32_t*>(meta + oReq);
+    d.marked = reinterpret_cast<uint8_t*>(meta + oMarked);
+    d.visibility = reinterpret_cast<uint8_t*>(meta + oVis);
+    d.tileCounts = reinterpret_cast<int2*>(meta + oTiles);
+    d.state = reinterpret_cast<MapState*>(meta + oState);
+    m->metaBytes = metaBytes;
+  }
+  ok = ok && alloc((void**)&d.vbaDepth, (size_t)d.capacity * kBlock3 * sizeof(uint32_t)) &&
             (!cfg->hasColour || alloc((void**)&d.vbaColour, (size_t)d.capacity * kBlock3 * sizeof(uint32_t))) &&
             alloc((void**)&d.freeBlocks, (size_t)d.capacity * sizeof(int)) &&
             alloc((void**)&d.freeExcess, (size_t)(d.excess ? d.excess : 1) * sizeof(int)) &&
-            alloc((void**)&d.visibleList, padded * sizeof(int)) && alloc((void**)&d.visibility, padded) &&
-            alloc((void**)&d.reqKey, padded * sizeof(uint32_t)) && alloc((void**)&d.marked, padded) &&
-            alloc((void**)&d.state, sizeof(MapState)) && alloc((void**)&d.tileCounts, d.nTiles * sizeof(int2)) &&
+            alloc((void**)&d.visibleList, padded * sizeof(int)) &&
             alloc((void**)&d.tilePrefix, (d.nTiles + 1) * sizeof(int2)) &&
             alloc((void**)&d.rangeBounds, padded * sizeof(int4)) &&
             alloc((void**)&m->icpOut, icp_state_bytes()) && alloc((void**)&m->icpPose, 64 * sizeof(float));
@@ -308,8 +329,10 @@ int rfg_map_destroy(rfg_map* m) {
   DeviceGuard dg_(m ? m->device : -1);
   if (!m) return RFG_OK;
   DevMap& d = m->d;
+  // (d.entries is the metadata allocation: reqKey, marked, visibility,
+  // tileCounts and state live inside it)
   void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
-                  d.visibility, d.reqKey, d.marked,     d.state,          d.tileCounts, d.tilePrefix,
+                  d.tilePrefix,
                   m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount,
                   m->fwdPrev, m->fwdKeys, m->fwdTileCounts, m->fwdTilePrefix, m->rgbaScratch};
   for (void* p : ptrs)
@@ -1062,15 +1085,17 @@ int rfg_pipeline_create(rfg_map* m, const rfg_pipeline_config* cfg, rfg_pipeline
   m->stream = p->stream;
   icp_warmup();
 #if RFG_L2_PERSIST
-  // L2 residency control: the map's hash entries (every stage's lookups and
-  // probes) as a persisting access-policy window on the pipeline's stream
+  // L2 residency control: the map's hash metadata (entries: every stage's
+  // lookups and probes; request keys, mark / visibility bytes, tile counts,
+  // state: the allocation stages) as a persisting access-policy window on the
+  // pipeline's stream
   // (captured into the frame graph's kernel nodes), within the device's
   // persisting set-aside
   {
     int maxPersist = 0, maxWindow = 0;
     cudaDeviceGetAttribute(&maxPersist, cudaDevAttrMaxPersistingL2CacheSize, m->device);
     cudaDeviceGetAttribute(&maxWindow, cudaDevAttrMaxAccessPolicyWindowSize, m->device);
-    const size_t bytes = (size_t)m->d.total * sizeof(int4);
+    const size_t bytes = m->metaBytes;  // entries first, then the other per-frame metadata
     if (maxPersist > 0 && maxWindow > 0) {
       const size_t setAside = bytes < (size_t)maxPersist ? bytes : (size_t)maxPersist;
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setAside);

@@ -172,6 +172,7 @@ struct rfg_map {
   int device;
   cudaStream_t stream;
   rfg::MapState* hostState;  // pinned mirror for readback
+  size_t metaBytes;          // the hash-metadata allocation (d.entries ... d.state)
   // ICP scratch
   void* icpOut;              // device: rfg_icp.cu IcpState (sums, solver state, accumulators)
   float* icpPose;            // device: current cam->world (12) + world->cam (12) + render pose (12)
