@@ -152,6 +152,7 @@ __global__ void k_export_entries(const int4* e, int* out5, int n) {
 }
 
 constexpr int kBinCap = 2048;  // blocks per 32x32 screen tile before the overflow path
+constexpr size_t kTileScratchBytes = 64 << 10;  // [binCount | tileCost | tileOrder] up to 5,461 screen tiles
 
 int ensure_range_scratch(rfg_map* m, int width, int height) {
   DevMap& d = m->d;
@@ -163,13 +164,17 @@ int ensure_range_scratch(rfg_map* m, int width, int height) {
   RFG_CK(cudaDeviceSynchronize());
   ++d.binGen;
   if (d.bins) cudaFree(d.bins);
-  if (d.binCount) cudaFree(d.binCount);
+  if (d.binCount && d.binCount != m->tileScratch) cudaFree(d.binCount);
   d.bins = nullptr;
   d.binCount = nullptr;
   d.tileCost = nullptr;
   d.tileOrder = nullptr;
+  // the per-tile counters carried from frame to frame sit in the map's
+  // metadata allocation (the persisting L2 window) when they fit
+  const size_t counterBytes = (size_t)tx * ty * 3 * sizeof(int);
+  if (counterBytes <= kTileScratchBytes) d.binCount = m->tileScratch;
   if (cudaMalloc(&d.bins, (size_t)tx * ty * kBinCap * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&d.binCount, (size_t)tx * ty * 3 * sizeof(int)) != cudaSuccess) {
+      (!d.binCount && cudaMalloc(&d.binCount, counterBytes) != cudaSuccess)) {
     cudaGetLastError();
     set_error("range scratch allocation failed");
     return RFG_ENOMEM;
@@ -285,7 +290,7 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
   };
   const size_t oEntries = carve(padded * sizeof(int4)), oReq = carve(padded * sizeof(uint32_t)),
                oMarked = carve(padded), oVis = carve(padded), oTiles = carve((size_t)d.nTiles * sizeof(int2)),
-               oState = carve(sizeof(MapState));
+               oState = carve(sizeof(MapState)), oTileScratch = carve(kTileScratchBytes);
   char* meta = nullptr;
   bool ok = alloc((void**)&meta, metaBytes);
   if (ok) {
@@ -295,6 +300,7 @@ int rfg_map_create(const rfg_map_config* cfg, int device, rfg_map** out) {
     d.visibility = reinterpret_cast<uint8_t*>(meta + oVis);
     d.tileCounts = reinterpret_cast<int2*>(meta + oTiles);
     d.state = reinterpret_cast<MapState*>(meta + oState);
+    m->tileScratch = reinterpret_cast<int*>(meta + oTileScratch);
     m->metaBytes = metaBytes;
   }
   ok = ok && alloc((void**)&d.vbaDepth, (size_t)d.capacity * kBlock3 * sizeof(uint32_t)) &&
@@ -330,7 +336,8 @@ int rfg_map_destroy(rfg_map* m) {
   if (!m) return RFG_OK;
   DevMap& d = m->d;
   // (d.entries is the metadata allocation: reqKey, marked, visibility,
-  // tileCounts and state live inside it)
+  // tileCounts, state and the tile scratch live inside it)
+  if (d.binCount == m->tileScratch) d.binCount = nullptr;  // inside the metadata allocation
   void* ptrs[] = {d.entries, d.vbaDepth,   d.vbaColour,  d.freeBlocks,     d.freeExcess, d.visibleList,
                   d.tilePrefix,
                   m->icpOut, m->icpPose, d.rangeBounds, d.bins, d.binCount,

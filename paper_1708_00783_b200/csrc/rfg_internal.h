@@ -172,7 +172,8 @@ struct rfg_map {
   int device;
   cudaStream_t stream;
   rfg::MapState* hostState;  // pinned mirror for readback
-  size_t metaBytes;          // the hash-metadata allocation (d.entries ... d.state)
+  size_t metaBytes;          // the hash-metadata allocation (d.entries ... d.state, tileScratch)
+  int* tileScratch;          // 64 KiB inside it: the range stage's per-tile counters when they fit
   // ICP scratch
   void* icpOut;              // device: rfg_icp.cu IcpState (sums, solver state, accumulators)
   float* icpPose;            // device: current cam->world (12) + world->cam (12) + render pose (12)
