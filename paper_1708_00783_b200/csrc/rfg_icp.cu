@@ -819,10 +819,28 @@ __global__ void __launch_bounds__(kIcpThreads, RFG_ICP_CPS) k_icp_coarse(IcpStat
   cl.sync();  // rank 0's shared memory stays alive until every CTA has read it
 }
 
+#ifndef RFG_ICP_PREFETCH
+#define RFG_ICP_PREFETCH 1  // render maps prefetched into L2 before the wait for the view kernel
+#endif
 __global__ void __launch_bounds__(kIcpThreads, RFG_ICP_CPS) k_icp_track(IcpState* st, IcpTrackArgs ta) {
   __shared__ long long sh[kIcpThreads / 32][32];
   __shared__ GnShared g;
   __shared__ float4 pcs[kIcpPx * kIcpThreads];
+#if RFG_ICP_PREFETCH
+  {
+    // the render maps the association gathers from (the previous frame's
+    // raycast, long complete) into L2 while the view kernel finishes: the
+    // first evaluation of each level would otherwise wait on DRAM for them
+    const IcpLevelArgs& l0 = ta.lv[0];
+    const size_t lines = ((size_t)l0.rw * l0.rh * sizeof(float4)) >> 7;
+    const char* pts = reinterpret_cast<const char*>(l0.points);
+    const char* nrm = reinterpret_cast<const char*>(l0.normals);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < lines; i += (size_t)gridDim.x * blockDim.x) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pts + (i << 7)));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(nrm + (i << 7)));
+    }
+  }
+#endif
   pdl_wait();  // the depth pyramid (programmatic dependency on the view kernel)
 #ifdef RFG_ICP_PHASES
   const unsigned long long tEntry = gtimer();
