@@ -144,16 +144,20 @@ def test_pipeline_pinned_host_frames_equal_device_frames():
             assert np.array_equal(pa, pb) and np.array_equal(ia, ib) and sa == sb
 
 
-def test_pipeline_recaptures_after_range_scratch_reallocation():
+@pytest.mark.parametrize("other", [(160, 120), (1408, 1024)])
+def test_pipeline_recaptures_after_range_scratch_reallocation(other):
     """a map-level render at another image size
     reallocates the map's expected-range scratch, which a pipeline's captured
     frame graph holds; the pipeline must re-capture instead of replaying the
     freed scratch.  The interrupted pipeline matches an uninterrupted one
-    bit for bit."""
+    bit for bit.  At 1408x1024 the per-tile counters (5,632 tiles) no longer
+    fit the map's in-allocation tile scratch and get an allocation of their
+    own; back at 320x240 they return to the scratch."""
     import torch
     from paper_1708_00783_b200 import fusion as F
     intr = F.Intrinsics(320, 240, 262.5, 262.5, 159.5, 119.5)
-    small = F.Intrinsics(160, 120, 131.25, 131.25, 79.5, 59.5)
+    s = other[0] / 640.0
+    small = F.Intrinsics(other[0], other[1], 525.0 * s, 525.0 * s, other[0] / 2 - 0.5, other[1] / 2 - 0.5)
     params = F.SceneParams()
     poses = F.orbit_trajectory(frames=100)
     cfg = F.VoxelBlockMapConfig(1 << 16, 1 << 14, 1 << 16)
