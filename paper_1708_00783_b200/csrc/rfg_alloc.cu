@@ -10,17 +10,19 @@
 //   (pixel << 6 | ordinal) + 1 and an atomicMax per slot keeps the serial
 //   winner; visits are first merged per distinct block inside the CTA, so
 //   each chain is probed once per block and CTA.
-// Stage 2 (k_req_count / k_scan_tiles / k_req_assign): requests are served in
+// Stage 2 (k_req_assign, one launch; stage 1 counts each tile's requests):
+//   requests are served in
 //   ascending entry-index order, exactly as the serial scan (fusion.cpp:190-201):
 //   a request succeeds iff it is a bucket request or among the first
 //   nFreeExcess excess requests, and its rank among such candidates is below
 //   nFreeBlocks.  Ranks come from a tile scan, so the VBA block and excess
 //   slot each request pops are the ones the serial free stacks would pop —
 //   the resulting hash table is bit-identical, not only set-identical.
-// Stage 3 (k_vis_count / k_scan_tiles / k_vis_emit): candidates = this
-//   frame's marks ∪ the previous visible list (its visibility bytes), frustum
-//   tested (fusion.cpp:116-130), compacted in ascending index order (= the
-//   reference's std::sort, fusion.cpp:231).
+// Stage 3 (k_vis_count): candidates = this frame's marks ∪ the previous
+//   visible list (its visibility bytes), frustum tested (fusion.cpp:116-130),
+//   appended to the list per tile; the reference's ascending order (its
+//   std::sort, fusion.cpp:231) is rebuilt on export (k_vis_tilecount /
+//   k_scan_tiles / k_vis_emit).
 #include "rfg_common.cuh"
 
 namespace rfg {
